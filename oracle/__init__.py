@@ -1,0 +1,197 @@
+"""CPU oracle for the adaptive-OpenMP model-building path.
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+package.  The product path (``paper_2303_08873_b200``) never imports it and has
+no CPU fallback.
+
+This is a ctypes wrapper (argument marshalling only) over ``oracle.c``, a plain
+single-threaded C implementation written from PAPER.md and the readings in
+DESIGN.md §3.  See ``oracle.h`` for the per-function citations.  Every function
+is pinned by ``tests/test_oracle_*.py`` (exact rational brute force, closed
+forms and the worked examples under ``tests/golden/``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.c")
+
+OK = 0
+E_INVALID_ARG = -1
+E_INSUFFICIENT_DATA = -4
+E_BAD_VALUE = -6
+E_TOO_MANY_DISTINCT = -7
+E_CAPACITY = -12
+
+NODE_DTYPE = np.dtype(
+    [
+        ("feature", np.int32),
+        ("left", np.int32),
+        ("right", np.int32),
+        ("label", np.int32),
+        ("depth", np.int32),
+        ("pad_", np.int32),
+        ("threshold", np.float64),
+        ("n", np.int64),
+        ("gini", np.float64),
+    ]
+)
+assert NODE_DTYPE.itemsize == 48
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (plain -O2, no FMA contraction)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
+        os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))
+    ):
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+             "-shared", "-o", _SO, _SRC, "-lm"]
+        )
+    return _SO
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        P = ctypes.c_void_p
+        i64, i32 = ctypes.c_int64, ctypes.c_int32
+        L.oracle_canon_features.argtypes = [P, i64, ctypes.c_int, P]
+        L.oracle_labels.argtypes = [P, i64, ctypes.c_int, P]
+        L.oracle_aggregate.argtypes = [P, P, P, i64, ctypes.c_int, ctypes.c_int, P, P, i64, P]
+        L.oracle_distinct_pairs.argtypes = [P, P, i64, ctypes.c_int]
+        L.oracle_distinct_pairs.restype = i64
+        L.oracle_value_table.argtypes = [P, i64, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P]
+        L.oracle_train.argtypes = [P, P, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, i32, P]
+        L.oracle_select.argtypes = [P, i32, P, i64, ctypes.c_int, P]
+        L.oracle_gini_counts.argtypes = [P, ctypes.c_int]
+        L.oracle_gini_counts.restype = ctypes.c_double
+        _lib = L
+    return _lib
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: oracle status {code}")
+        self.code = code
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f32(X, F=None):
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    if F is not None:
+        X = X.reshape(-1, F)
+    return X
+
+
+def canon_features(X: np.ndarray) -> np.ndarray:
+    X = _f32(X)
+    n, F = X.shape
+    out = np.empty_like(X)
+    rc = lib().oracle_canon_features(_p(X), n, F, _p(out))
+    if rc:
+        raise OracleError(rc, "canon_features")
+    return out
+
+
+def labels(times: np.ndarray) -> np.ndarray:
+    """Fastest-variant label per row."""
+    t = _f32(times)
+    n, V = t.shape
+    out = np.empty(n, np.uint8)
+    rc = lib().oracle_labels(_p(t), n, V, _p(out))
+    if rc:
+        raise OracleError(rc, "labels")
+    return out
+
+
+def aggregate(feat: np.ndarray, var: np.ndarray, ns: np.ndarray, V: int):
+    """Long-format records -> (wide features [n][F], wide times [n][V])."""
+    feat = _f32(feat)
+    R, F = feat.shape
+    var = np.ascontiguousarray(var, dtype=np.int32)
+    ns = np.ascontiguousarray(ns, dtype=np.uint64)
+    of = np.empty((max(R, 1), F), np.float32)
+    ot = np.empty((max(R, 1), V), np.float32)
+    n_out = np.zeros(1, np.int64)
+    rc = lib().oracle_aggregate(_p(feat), _p(var), _p(ns), R, F, V, _p(of), _p(ot), max(R, 1),
+                                _p(n_out))
+    if rc:
+        raise OracleError(rc, "aggregate")
+    n = int(n_out[0])
+    return of[:n].copy(), ot[:n].copy()
+
+
+def distinct_pairs(feat: np.ndarray, var: np.ndarray) -> int:
+    feat = _f32(feat)
+    R, F = feat.shape
+    var = np.ascontiguousarray(var, dtype=np.int32)
+    return int(lib().oracle_distinct_pairs(_p(feat), _p(var), R, F))
+
+
+def value_table(X: np.ndarray, f: int) -> np.ndarray:
+    """Sorted distinct values of feature f (a2)."""
+    X = _f32(X)
+    n, F = X.shape
+    vals = np.empty(max(n, 1), np.float32)
+    cnt = np.zeros(1, np.int32)
+    rc = lib().oracle_value_table(_p(X), n, F, f, _p(vals), vals.size, _p(cnt))
+    if rc:
+        raise OracleError(rc, "value_table")
+    return vals[: int(cnt[0])].copy()
+
+
+def bins(X: np.ndarray) -> np.ndarray:
+    """Rank of each value in its feature's value table (a3), u8 [n][F]."""
+    X = canon_features(X)
+    n, F = X.shape
+    out = np.empty((n, F), np.uint8)
+    for f in range(F):
+        out[:, f] = np.searchsorted(value_table(X, f), X[:, f]).astype(np.uint8)
+    return out
+
+
+def train(X: np.ndarray, y: np.ndarray, C: int, D: int, cap: int | None = None) -> np.ndarray:
+    """Exact greedy CART, canonical BFS node array (structured NODE_DTYPE)."""
+    X = _f32(X)
+    n, F = X.shape
+    y = np.ascontiguousarray(y, dtype=np.uint8)
+    if cap is None:
+        cap = int(min(2 * n + 1, (1 << (D + 1)) - 1 if D < 30 else 2 * n + 1))
+    out = np.zeros(max(cap, 1), NODE_DTYPE)
+    nn = np.zeros(1, np.int32)
+    rc = lib().oracle_train(_p(X), _p(y), n, F, C, D, _p(out), max(cap, 1), _p(nn))
+    if rc:
+        raise OracleError(rc, "train")
+    return out[: int(nn[0])].copy()
+
+
+def select(tree: np.ndarray, X: np.ndarray) -> np.ndarray:
+    X = _f32(X)
+    m, F = X.shape
+    tree = np.ascontiguousarray(tree, dtype=NODE_DTYPE)
+    out = np.empty(m, np.int32)
+    rc = lib().oracle_select(_p(tree), len(tree), _p(X), m, F, _p(out))
+    if rc:
+        raise OracleError(rc, "select")
+    return out
+
+
+def gini_counts(counts) -> float:
+    c = np.ascontiguousarray(counts, dtype=np.int64)
+    return float(lib().oracle_gini_counts(_p(c), c.size))
