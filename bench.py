@@ -1,0 +1,314 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: one step = a1..a9 over one
+profiling table — ingest (label + value tables + bins), level-wise CART to
+depth D, and batched selection of the same table's feature vectors.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+N > 1 runs under torchrun (one process per GPU); the table's rows are split
+into contiguous shards (strong scaling: the C4 table is 1e8 rows in total) and
+the per-level histograms are summed with NCCL inside libadapt.so.  Rank 0
+prints ONE JSON line.  See DESIGN.md §7 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import signal
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "CART train samples/s and variant selections/s at 1/2/4/8 B200; % HBM peak"
+WORKLOADS = {
+    "C4": "C4: 1e8-row profiling table, 16 features, 48 variants (offload x threads x block), "
+          "depth-12 CART + selection of the same 1e8 vectors",
+    "C3": "C3: 1e6-row table, 8 features, 6 variants (GPU block size), depth-12 CART + selection",
+    "C2": "C2 region 0: 3.3e4-row table, 4 features, 7 variants (num_threads), depth 8",
+    "C1": "C1: 512 profiled samples, 1 feature (trip count), host vs GPU offload, depth 4",
+}
+KERNEL_PHASES = ("ingest", "values", "merge", "zero", "hist", "subtract", "split", "winner", "select")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+                start_new_session=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.25)
+            os.killpg(self.proc.pid, signal.SIGTERM)
+            self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        if not getattr(self, "out", ""):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        load = [x for x in sm if x > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(cfg, rows: int, depth: int):
+    """The oracle as it stands (single-threaded C), on a bounded sample of the
+    same workload: the first `rows` rows of the table, labels + tree + select."""
+    import oracle
+
+    X, T = synth.generate(cfg, 0, rows)
+    t0 = time.perf_counter()
+    y = oracle.labels(T)
+    tree = oracle.train(X, y, cfg.V, depth)
+    oracle.select(tree, X)
+    dt = time.perf_counter() - t0
+    return rows / dt, dt
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    rows = args.ref_rows or {"C4": 300_000, "C3": 300_000}.get(args.config, cfg.N)
+    oracle_import = __import__("oracle")
+    oracle_import.build()
+    times = []
+    for i in range(args.warmup + args.steps):
+        v, dt = cpu_baseline(cfg, rows, cfg.D)
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * statistics.mean(times)
+    value = rows / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "sample_rows": rows},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": 1, "kind": "oracle",
+                         "sample": f"first {rows} rows of {args.config} (labels + depth-{cfg.D} "
+                                   f"exact CART + select), single-threaded C oracle"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", type=int, default=0, help="override table rows (testing only)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-rows", type=int, default=0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2303_08873_b200 as ad
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        uid = [ad.adapt_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ad.adapt_init(local, rank, world, uid[0])
+    else:
+        ad.adapt_init(local, 0, 1)
+
+    cfg = synth.CONFIGS[args.config]
+    N = args.rows or (cfg.N if cfg.regions == 1 else len(synth.region_rows(cfg, 0)))
+    lo, hi = rank * N // world, (rank + 1) * N // world
+    n = hi - lo
+    stream = torch.cuda.current_stream()
+    flat, off = cfg.grid_table
+    g, o = torch.from_numpy(flat).to(dev), torch.from_numpy(off).to(dev)
+    X = torch.empty((n, cfg.F), dtype=torch.float32, device=dev)
+    T = torch.empty((n, cfg.V), dtype=torch.float32, device=dev)
+    out = torch.empty(n, dtype=torch.int32, device=dev)
+    synth.generate_device(cfg, lo, n, X.data_ptr(), T.data_ptr(), g.data_ptr(), o.data_ptr(),
+                          stream.cuda_stream)
+    torch.cuda.synchronize()
+    h = ad.adapt_region_create(f"bench_{args.config}", cfg.F, cfg.V, f"dtree,depth={cfg.D}", 0)
+
+    def step():
+        ad.adapt_record_table(h, X, T, n, True, stream)
+        ad.adapt_train(h, stream)
+        ad.adapt_select_batch(h, X, n, out, stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    ad.adapt_profile_enable(True)
+    ad.adapt_profile_reset()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ad.adapt_profile_enable(False)
+    prof = ad.adapt_profile_get()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    tree = ad.adapt_get_tree(h)
+    levels = ad.adapt_train_stats(h)
+
+    # ---- end to end through the public API with HOST buffers ----
+    e2e = None
+    if not args.no_e2e:
+        hX = torch.empty((n, cfg.F), dtype=torch.float32, pin_memory=True)
+        hT = torch.empty((n, cfg.V), dtype=torch.float32, pin_memory=True)
+        hout = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        hX.copy_(X)
+        hT.copy_(T)
+        he = ad.adapt_region_create(f"bench_e2e_{args.config}", cfg.F, cfg.V, f"dtree,depth={cfg.D}", 0)
+
+        def step_host():
+            ad.adapt_record_table(he, hX, hT, n, False, stream)
+            ad.adapt_train(he, stream)
+            ad.adapt_select_batch_host(he, hX, n, hout, stream)
+
+        step_host()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            step_host()
+        barrier()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        et = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_ms = float(et.item())
+        assert np.array_equal(hout.numpy(), out.cpu().numpy()), "e2e selections differ from device path"
+        e2e = {"value": N / (e2e_ms / 1e3), "unit": "samples/s",
+               "h2d_bytes_per_step": int(N * (4 * cfg.F + 4 * cfg.V) + N * 4 * cfg.F),
+               "d2h_bytes_per_step": int(N * 4), "ms_per_step": e2e_ms, "steps": args.e2e_steps,
+               "timer": "host wall clock around synchronous C-ABI calls, max over ranks"}
+        del hX, hT, hout
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    kern = {k: v for k, v in prof.items() if k in KERNEL_PHASES}
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    d = kern[dom]
+    achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 and d["bytes"] > 0 else None
+    step_ms_phases = {k: round(v["ms"] / args.steps, 4) for k, v in kern.items()}
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "peak_source": peak_src,
+                "bytes_per_launch": d["bytes"] / max(d["launches"], 1),
+                "ms_per_launch": d["ms"] / max(d["launches"], 1)}
+    alg_bytes = sum(v["bytes"] for v in kern.values()) / args.steps
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        rows = {"C4": 300_000, "C3": 300_000}.get(args.config, N)
+        v, dt = cpu_baseline(cfg, min(rows, N), cfg.D)
+        cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {min(rows, N)} rows of {args.config}: labels + depth-{cfg.D} exact "
+                         f"CART + select, single-threaded C oracle ({dt:.1f} s)"}
+    line = {
+        "metric": METRIC, "value": N / (ms / 1e3), "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "rows": N, "features": cfg.F,
+                   "variants": cfg.V, "depth": cfg.D, "select_vectors": N,
+                   "parallelism": f"dp{world}",
+                   "l2": "inputs (%.1f GB) exceed the 126 MB L2; no flush needed" %
+                         (N * 4 * (cfg.F + cfg.V) / 1e9)},
+        "train_samples_per_s": N / ((ms - step_ms_phases.get("select", 0)) / 1e3),
+        "select_per_s": N / (step_ms_phases["select"] / 1e3) if step_ms_phases.get("select") else None,
+        "hbm_frac_step": alg_bytes / (ms / 1e3) / 1e9 / peak,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": int(sum(v["launches"] for v in kern.values())),
+        "gpu_launches_per_step": sum(v["launches"] for v in kern.values()) / args.steps,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "phase_ms_per_step": step_ms_phases,
+        "tree_nodes": int(len(tree)),
+        "levels": levels,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

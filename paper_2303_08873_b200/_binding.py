@@ -1,0 +1,323 @@
+"""Thin ctypes binding of libadapt.so (include/adapt.h).
+
+Argument marshalling only: every step of record -> label -> train -> select
+runs in the library's sm_100a kernels.  Same names as the C ABI.  Arrays may
+be numpy arrays (host) or torch tensors (host or CUDA); a CUDA stream may be a
+torch.cuda.Stream, an int handle or None (legacy default stream).
+
+There is no fallback: if libadapt.so is missing the import fails, and with no
+usable B200 every compute call raises AdaptError(ADAPT_E_CUDA).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libadapt.so")
+
+ADAPT_OK = 0
+ADAPT_E_INVALID_ARG = -1
+ADAPT_E_USAGE = -2
+ADAPT_E_ARITY = -3
+ADAPT_E_INSUFFICIENT_DATA = -4
+ADAPT_E_SPEC_MISMATCH = -5
+ADAPT_E_BAD_VALUE = -6
+ADAPT_E_TOO_MANY_DISTINCT = -7
+ADAPT_E_NOT_TRAINED = -8
+ADAPT_E_CUDA = -9
+ADAPT_E_NCCL = -10
+ADAPT_E_OOM = -11
+
+# the exported symbols of include/adapt.h (checked by tests/test_boundary.py)
+SYMBOLS = [
+    "adapt_init", "adapt_nccl_unique_id", "adapt_finalize", "adapt_last_error", "adapt_version",
+    "adapt_region_create", "adapt_region_destroy", "adapt_region_info", "adapt_record",
+    "adapt_record_table", "adapt_distinct_pairs", "adapt_train", "adapt_train_many",
+    "adapt_select", "adapt_select_batch", "adapt_select_batch_host", "adapt_get_tree",
+    "adapt_set_tree", "adapt_get_labels", "adapt_get_value_table", "adapt_get_bins",
+    "adapt_profile_enable", "adapt_profile_reset", "adapt_profile_get", "adapt_train_stats",
+    "__adapt_region_create", "__adapt_region_begin", "__adapt_region_end",
+    "__adapt_region_set_feature", "__adapt_region_get_policy", "__adapt_region_train",
+]
+
+NODE_DTYPE = np.dtype([
+    ("feature", np.int32), ("left", np.int32), ("right", np.int32), ("label", np.int32),
+    ("depth", np.int32), ("pad_", np.int32), ("threshold", np.float64), ("n", np.int64),
+    ("gini", np.float64),
+])
+assert NODE_DTYPE.itemsize == 48
+
+
+class adapt_phase_t(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_int64),
+                ("ms", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
+class AdaptError(RuntimeError):
+    def __init__(self, code: int, call: str, msg: str):
+        super().__init__(f"{call} -> {code}: {msg}")
+        self.code = code
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build()")
+_L = ctypes.CDLL(LIB_PATH)
+_P, _I, _I64, _U64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64
+_sigs = {
+    "adapt_init": [_I, _I, _I, _P],
+    "adapt_nccl_unique_id": [_P],
+    "adapt_finalize": [],
+    "adapt_region_create": [ctypes.c_char_p, _I, _I, ctypes.c_char_p, _I, _P],
+    "adapt_region_destroy": [_P],
+    "adapt_region_info": [_P, _P, _P, _P, _P, _P, _P],
+    "adapt_record": [_P, _P, _I, _U64],
+    "adapt_record_table": [_P, _P, _P, _I64, _I, _P],
+    "adapt_distinct_pairs": [_P, _P],
+    "adapt_train": [_P, _P],
+    "adapt_train_many": [_P, _I, _P],
+    "adapt_select": [_P, _P, _P],
+    "adapt_select_batch": [_P, _P, _I64, _P, _P],
+    "adapt_select_batch_host": [_P, _P, _I64, _P, _P],
+    "adapt_get_tree": [_P, _P, ctypes.c_int32, _P],
+    "adapt_set_tree": [_P, _P, ctypes.c_int32],
+    "adapt_get_labels": [_P, _P, _I64],
+    "adapt_get_value_table": [_P, _I, _P, _P],
+    "adapt_get_bins": [_P, _P, _I64],
+    "adapt_profile_enable": [_I],
+    "adapt_profile_reset": [],
+    "adapt_profile_get": [_P, _I, _P],
+    "adapt_train_stats": [_P, _P, _I, _P],
+}
+for _name, _args in _sigs.items():
+    getattr(_L, _name).argtypes = _args
+    getattr(_L, _name).restype = _I
+_L.adapt_last_error.restype = ctypes.c_char_p
+_L.adapt_version.restype = ctypes.c_char_p
+_L.__adapt_region_create.argtypes = [ctypes.c_char_p, _I, _I, ctypes.c_char_p, _I]
+_L.__adapt_region_create.restype = _P
+for _name in ("__adapt_region_begin", "__adapt_region_end", "__adapt_region_train"):
+    getattr(_L, _name).argtypes = [_P]
+    getattr(_L, _name).restype = None
+_L.__adapt_region_set_feature.argtypes = [_P, ctypes.c_float]
+_L.__adapt_region_set_feature.restype = None
+_L.__adapt_region_get_policy.argtypes = [_P]
+_L.__adapt_region_get_policy.restype = _I
+
+
+def lib() -> ctypes.CDLL:
+    return _L
+
+
+def _check(rc: int, call: str) -> None:
+    if rc != ADAPT_OK:
+        raise AdaptError(rc, call, adapt_last_error())
+
+
+def _ptr(a) -> int:
+    """Address of a numpy array or torch tensor (host or device)."""
+    if a is None:
+        return 0
+    if isinstance(a, int):
+        return a
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr()
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _stream(s) -> int:
+    if s is None:
+        return 0
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+# ------------------------------------------------------------------- C ABI --
+def adapt_last_error() -> str:
+    return (_L.adapt_last_error() or b"").decode()
+
+
+def adapt_version() -> str:
+    return _L.adapt_version().decode()
+
+
+def adapt_init(device: int = 0, rank: int = 0, world: int = 1, nccl_unique_id: bytes | None = None):
+    buf = None
+    if nccl_unique_id is not None:
+        buf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
+    _check(_L.adapt_init(device, rank, world, ctypes.cast(buf, _P) if buf else None), "adapt_init")
+
+
+def adapt_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_L.adapt_nccl_unique_id(ctypes.cast(buf, _P)), "adapt_nccl_unique_id")
+    return buf.raw
+
+
+def adapt_finalize():
+    _check(_L.adapt_finalize(), "adapt_finalize")
+
+
+def adapt_region_create(id: str, num_features: int, num_variants: int,
+                        model_params: str | None = None, min_train_data: int = 0) -> int:
+    out = ctypes.c_void_p()
+    _check(_L.adapt_region_create(id.encode(), num_features, num_variants,
+                                  model_params.encode() if model_params is not None else None,
+                                  min_train_data, ctypes.byref(out)), "adapt_region_create")
+    return out.value
+
+
+def adapt_region_destroy(h: int):
+    _check(_L.adapt_region_destroy(h), "adapt_region_destroy")
+
+
+def adapt_region_info(h: int) -> dict:
+    F, V, D, M, T = (ctypes.c_int() for _ in range(5))
+    rows = ctypes.c_int64()
+    _check(_L.adapt_region_info(h, ctypes.byref(F), ctypes.byref(V), ctypes.byref(D),
+                                ctypes.byref(M), ctypes.byref(rows), ctypes.byref(T)),
+           "adapt_region_info")
+    return dict(num_features=F.value, num_variants=V.value, max_depth=D.value,
+                min_train_data=M.value, num_rows=rows.value, trained=bool(T.value))
+
+
+def adapt_record(h: int, features, variant: int, elapsed_ns: int):
+    x = np.ascontiguousarray(features, dtype=np.float32)
+    _check(_L.adapt_record(h, x.ctypes.data, int(variant), int(elapsed_ns)), "adapt_record")
+
+
+def adapt_record_table(h: int, features, times, n: int | None = None, on_device: bool | None = None,
+                       stream=None):
+    if n is None:
+        n = int(features.shape[0])
+    if on_device is None:
+        on_device = bool(getattr(features, "is_cuda", False))
+    _check(_L.adapt_record_table(h, _ptr(features), _ptr(times), int(n), int(on_device),
+                                 _stream(stream)), "adapt_record_table")
+
+
+def adapt_distinct_pairs(h: int) -> int:
+    c = ctypes.c_int64()
+    _check(_L.adapt_distinct_pairs(h, ctypes.byref(c)), "adapt_distinct_pairs")
+    return c.value
+
+
+def adapt_train(h: int, stream=None):
+    _check(_L.adapt_train(h, _stream(stream)), "adapt_train")
+
+
+def adapt_train_many(hs, stream=None):
+    arr = (ctypes.c_void_p * len(hs))(*hs)
+    _check(_L.adapt_train_many(ctypes.cast(arr, _P), len(hs), _stream(stream)), "adapt_train_many")
+
+
+def adapt_select(h: int, features) -> int:
+    x = np.ascontiguousarray(features, dtype=np.float32)
+    v = ctypes.c_int32()
+    _check(_L.adapt_select(h, x.ctypes.data, ctypes.byref(v)), "adapt_select")
+    return v.value
+
+
+def adapt_select_batch(h: int, d_X, m: int, d_out, stream=None):
+    _check(_L.adapt_select_batch(h, _ptr(d_X), int(m), _ptr(d_out), _stream(stream)),
+           "adapt_select_batch")
+
+
+def adapt_select_batch_host(h: int, X, m: int, out, stream=None):
+    _check(_L.adapt_select_batch_host(h, _ptr(X), int(m), _ptr(out), _stream(stream)),
+           "adapt_select_batch_host")
+
+
+def adapt_get_tree(h: int) -> np.ndarray:
+    n = ctypes.c_int32()
+    rc = _L.adapt_get_tree(h, None, 0, ctypes.byref(n))
+    if rc not in (ADAPT_OK, ADAPT_E_INVALID_ARG) or n.value <= 0:
+        _check(rc, "adapt_get_tree")
+    out = np.zeros(n.value, NODE_DTYPE)
+    _check(_L.adapt_get_tree(h, out.ctypes.data, n.value, ctypes.byref(n)), "adapt_get_tree")
+    return out
+
+
+def adapt_set_tree(h: int, nodes: np.ndarray):
+    nodes = np.ascontiguousarray(nodes, dtype=NODE_DTYPE)
+    _check(_L.adapt_set_tree(h, nodes.ctypes.data, len(nodes)), "adapt_set_tree")
+
+
+def adapt_get_labels(h: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.uint8)
+    _check(_L.adapt_get_labels(h, out.ctypes.data, n), "adapt_get_labels")
+    return out
+
+
+def adapt_get_value_table(h: int, f: int) -> np.ndarray:
+    vals = np.zeros(256, np.float32)
+    c = ctypes.c_int()
+    _check(_L.adapt_get_value_table(h, f, vals.ctypes.data, ctypes.byref(c)), "adapt_get_value_table")
+    return vals[: c.value].copy()
+
+
+def adapt_get_bins(h: int, n: int, F: int) -> np.ndarray:
+    out = np.empty((n, F), np.uint8)
+    _check(_L.adapt_get_bins(h, out.ctypes.data, n), "adapt_get_bins")
+    return out
+
+
+def adapt_profile_enable(enable: bool = True):
+    _check(_L.adapt_profile_enable(int(enable)), "adapt_profile_enable")
+
+
+def adapt_profile_reset():
+    _check(_L.adapt_profile_reset(), "adapt_profile_reset")
+
+
+def adapt_profile_get() -> dict:
+    arr = (adapt_phase_t * 64)()
+    n = ctypes.c_int()
+    _check(_L.adapt_profile_get(ctypes.cast(arr, _P), 64, ctypes.byref(n)), "adapt_profile_get")
+    return {arr[i].name.decode(): dict(launches=arr[i].launches, ms=arr[i].ms, bytes=arr[i].bytes)
+            for i in range(min(n.value, 64))}
+
+
+def adapt_train_stats(h: int) -> list:
+    buf = np.zeros(3 * 64, np.int64)
+    lv = ctypes.c_int()
+    _check(_L.adapt_train_stats(h, buf.ctypes.data, buf.size, ctypes.byref(lv)), "adapt_train_stats")
+    return [dict(nodes=int(buf[3 * d]), rows_hist=int(buf[3 * d + 1]), rows_part=int(buf[3 * d + 2]))
+            for d in range(min(lv.value, 64))]
+
+
+# ------------------------------------------------------ Apollo Table-1 shim --
+def __adapt_region_create(id: str, num_features: int, num_policies: int,
+                          model_type_params: str | None = None, min_train_data: int = 0):
+    return _L.__adapt_region_create(id.encode(), num_features, num_policies,
+                                    model_type_params.encode() if model_type_params else None,
+                                    min_train_data)
+
+
+def __adapt_region_begin(r):
+    _L.__adapt_region_begin(r)
+
+
+def __adapt_region_end(r):
+    _L.__adapt_region_end(r)
+
+
+def __adapt_region_set_feature(r, v: float):
+    _L.__adapt_region_set_feature(r, ctypes.c_float(v))
+
+
+def __adapt_region_get_policy(r) -> int:
+    return _L.__adapt_region_get_policy(r)
+
+
+def __adapt_region_train(r):
+    _L.__adapt_region_train(r)

@@ -1,0 +1,119 @@
+// common.h — internal declarations shared by the engine's host code and its
+// sm_100a kernels.  Not part of the C ABI (see include/adapt.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace adapt {
+
+constexpr int kMaxF = 64;          // features per region (adapt.h)
+constexpr int kMaxC = 255;         // variants = classes (adapt.h)
+constexpr int kMaxBins = 256;      // lossless bins per feature (R14)
+constexpr int kGSlots = 1024;      // global value-discovery hash slots per feature
+constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;  // a NaN pattern: never a valid (finite) key
+constexpr uint32_t kPendingId = 0xFFFFFFFFu;
+
+// ingest error flags (atomicOr'ed by the kernels)
+constexpr uint32_t kFlagBadFeature = 1;   // NaN/Inf feature (R4)
+constexpr uint32_t kFlagNanTime = 2;      // NaN time (R3)
+constexpr uint32_t kFlagAllInf = 4;       // every variant unmeasured (R3)
+constexpr uint32_t kFlagTooMany = 8;      // > 256 distinct values of a feature (R14)
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char *what);
+#define CUDA_CHECK(x) ::adapt::cuda_check((x), #x)
+
+// ---- one segment of a level pass (host-built, read by hist_pass_kernel) ----
+// A segment is the span [off, off+len) of one parent node in the row-index
+// arrays.  The pass partitions it (feat >= 0) into the children's spans —
+// left rows from the front, right rows from the back — and accumulates the
+// class histogram of the "direct" child (or of all rows for the root pass).
+struct Seg {
+  uint32_t off;       // span start (position in idx arrays; row id if idx_prev == null)
+  uint32_t len;       // rows of this rank in the span
+  uint32_t row_base;  // prefix sum of len over previous segments (block work split)
+  int32_t feat;       // split feature, -1 = no partition (root pass)
+  int32_t thr;        // rank b_lo: rank <= thr goes left
+  int32_t direct;     // 0: histogram rows going left, 1: right, 2: all rows, -1: none
+  int32_t hslot;      // histogram slot of the direct child (-1: none)
+  int32_t write;      // bit0: write left rows to idx_next, bit1: right rows
+};
+
+// best cut of one (node, feature), exact key num/den (R13x)
+struct SplitCand {
+  uint64_t num_lo, num_hi;  // SL*nR + SR*nL  (< 2^97)
+  uint64_t den;             // nL*nR          (< 2^64)
+  uint64_t nL;              // rows at or left of the cut (global)
+  int32_t valid;            // a cut exists
+  int32_t b_lo, b_hi;       // ranks of the consecutive node-nonempty bins around the cut
+  int32_t pad;
+};
+
+// per-node outcome of the split search (device -> host once per level)
+struct NodeRes {
+  uint64_t n;               // rows in node (global)
+  uint64_t nL;              // rows left of the winning cut
+  int32_t valid, feat, b_lo, b_hi;
+  // followed in memory by uint32 P[C] (class totals) and uint32 cL[C]
+};
+
+// ---- kernel launchers (ingest.cu) ----
+void launch_ingest(const float *feat, const float *times, int64_t n, int F, int V, int RS,
+                   uint32_t *gkey, uint32_t *gid, uint32_t *gcount, uint32_t *flags,
+                   uint8_t *rec, cudaStream_t s);
+void launch_collect_values(const uint32_t *gkey, const uint32_t *gid, const uint32_t *gcount,
+                           int F, float *local_vals, int32_t *local_cnt, cudaStream_t s);
+void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int world, int rank,
+                         int F, float *val, int32_t *nval, uint8_t *lut, uint32_t *flags,
+                         cudaStream_t s);
+void launch_bins_out(const uint8_t *rec, int64_t n, int F, int RS, const uint8_t *lut,
+                     uint8_t *out, cudaStream_t s);
+void launch_labels_out(const uint8_t *rec, int64_t n, int F, int RS, uint8_t *out,
+                       cudaStream_t s);
+
+// ---- kernel launchers (train.cu) ----
+struct HistPassArgs {
+  const Seg *segs;
+  int nseg;
+  uint32_t total_rows;
+  const uint32_t *idx_prev;  // null: identity (root pass)
+  uint32_t *idx_next;
+  uint32_t *cursors;         // 2 per segment (left count, right count), zeroed
+  const uint8_t *rec;
+  int RS, F, C;
+  const uint8_t *lut;        // [F][256] prov -> rank
+  const int32_t *hoff;       // [F] counter offset of feature f in a node histogram
+  const int4 *groups;        // [ngroups] smem groups: features [x, y), classes [z, w)
+  int ngroups;
+  int smem_counters;         // max counters of a group
+  uint32_t *H;               // [slots][HS]
+  int64_t HS;
+  int blocks_per_group;
+};
+void launch_hist_pass(const HistPassArgs &a, cudaStream_t s);
+void launch_zero_slots(uint32_t *H, int64_t HS, const int32_t *slots, int n, cudaStream_t s);
+void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t HS, const int32_t *triples,
+                     int n, cudaStream_t s);
+void launch_split(const uint32_t *H, int64_t HS, const int32_t *node_slot, int nnodes, int F,
+                  int C, const int32_t *hoff, const int32_t *nval, SplitCand *out,
+                  cudaStream_t s);
+void launch_winner(const uint32_t *H, int64_t HS, const int32_t *node_slot, int nnodes, int F,
+                   int C, const int32_t *hoff, const int32_t *nval, const SplitCand *cand,
+                   uint8_t *res, int res_stride, cudaStream_t s);
+
+// ---- kernel launchers (select.cu) ----
+struct DNode {     // device inference node, 8 bytes
+  float thr;       // largest float32 <= threshold (x <= thr_f64  <=>  x <= thr_f32, V:A5)
+  int32_t meta;    // >= 0: (left << 6) | feature ; < 0: -1 - label
+};
+void launch_select(const DNode *tree, const float *X, int64_t m, int F, int32_t *out,
+                   cudaStream_t s);
+
+}  // namespace adapt

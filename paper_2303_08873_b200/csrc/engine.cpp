@@ -1,0 +1,1216 @@
+// engine.cpp — host side of libadapt.so: the C ABI of include/adapt.h, the
+// region registry, the level-by-level training loop that drives the kernels
+// of ingest.cu / train.cu / select.cu, NCCL plumbing for world > 1, per-phase
+// CUDA-event profiling, and the Apollo Table-1 shim.
+//
+// Host work here is bookkeeping only (a few hundred bytes per tree node per
+// level): every per-row step runs in the kernels.  The one row-level host
+// routine is the long -> wide aggregation of adapt_record() profiling records
+// (P:172-173), which is the small interactive path of the Table-1 shim; wide
+// tables (adapt_record_table) never touch the host.
+#include <dlfcn.h>
+#include <nccl.h>
+#include <time.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/adapt.h"
+#include "common.h"
+
+namespace adapt {
+
+void cuda_check(cudaError_t e, const char *what) {
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    throw Error(ADAPT_E_OOM, std::string("out of device memory: ") + what);
+  }
+  if (e != cudaSuccess) throw Error(ADAPT_E_CUDA, std::string(cudaGetErrorString(e)) + ": " + what);
+}
+
+namespace {
+
+// ------------------------------------------------------------ utilities --
+struct DevBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    release();
+    size_t want = std::max<size_t>(bytes, 256);
+    CUDA_CHECK(cudaMalloc(&p, want));
+    cap = want;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T *as() const { return static_cast<T *>(p); }
+  ~DevBuf() { release(); }
+};
+
+struct HostBuf {  // pinned staging for small D2H copies
+  void *p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    CUDA_CHECK(cudaMallocHost(&p, std::max<size_t>(bytes, 4096)));
+    cap = std::max<size_t>(bytes, 4096);
+  }
+  template <class T>
+  T *as() const { return static_cast<T *>(p); }
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+thread_local std::string g_last_error;
+std::recursive_mutex g_mu;
+
+// ------------------------------------------------------------ profiling --
+struct Prof {
+  bool on = false;
+  struct Rec {
+    int phase;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<std::string> names;
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  struct Acc {
+    int64_t launches = 0;
+    double ms = 0, bytes = 0;
+  };
+  std::vector<Acc> acc;
+  int id(const char *n) {
+    for (size_t i = 0; i < names.size(); i++)
+      if (names[i] == n) return (int)i;
+    names.push_back(n);
+    acc.emplace_back();
+    return (int)names.size() - 1;
+  }
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CUDA_CHECK(cudaEventCreate(&e));
+    return e;
+  }
+  void drain() {
+    for (auto &r : pending) {
+      float ms = 0;
+      CUDA_CHECK(cudaEventSynchronize(r.b));
+      CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+      acc[r.phase].launches += 1;
+      acc[r.phase].ms += ms;
+      acc[r.phase].bytes += r.bytes;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    pending.clear();
+  }
+};
+Prof g_prof;
+
+// RAII: events around the kernel(s) launched in its scope, on `s`
+struct Phase {
+  int ph = -1;
+  cudaEvent_t a{}, b{};
+  cudaStream_t s;
+  double bytes;
+  Phase(const char *name, cudaStream_t st, double by) : s(st), bytes(by) {
+    if (!g_prof.on) return;
+    ph = g_prof.id(name);
+    a = g_prof.ev();
+    b = g_prof.ev();
+    CUDA_CHECK(cudaEventRecord(a, s));
+  }
+  ~Phase() {
+    if (ph < 0) return;
+    cudaEventRecord(b, s);
+    g_prof.pending.push_back({ph, a, b, bytes});
+  }
+};
+
+// ------------------------------------------------------------ NCCL (dlopen) --
+struct Nccl {
+  void *h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
+                            ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  void load() {
+    if (h) return;
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *n : names)
+      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) throw Error(ADAPT_E_NCCL, "cannot dlopen libnccl.so.2");
+#define SYM(field, name)                                                     \
+  field = reinterpret_cast<decltype(field)>(dlsym(h, name));                 \
+  if (!field) throw Error(ADAPT_E_NCCL, std::string("missing NCCL symbol ") + name);
+    SYM(GetUniqueId, "ncclGetUniqueId");
+    SYM(CommInitRank, "ncclCommInitRank");
+    SYM(CommDestroy, "ncclCommDestroy");
+    SYM(AllReduce, "ncclAllReduce");
+    SYM(AllGather, "ncclAllGather");
+    SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+  }
+  void check(ncclResult_t r, const char *what) {
+    if (r != ncclSuccess)
+      throw Error(ADAPT_E_NCCL, std::string(what) + ": " + (GetErrorString ? GetErrorString(r) : "?"));
+  }
+};
+Nccl g_nccl;
+
+struct Ctx {
+  bool inited = false;
+  int device = 0, rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+};
+Ctx g_ctx;
+
+void ensure_init() {
+  if (g_ctx.inited) return;
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  int n = 0;
+  CUDA_CHECK(cudaGetDeviceCount(&n));
+  if (n == 0) throw Error(ADAPT_E_CUDA, "no CUDA device");
+  cudaDeviceProp prop;
+  CUDA_CHECK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10) throw Error(ADAPT_E_CUDA, "libadapt is built for sm_100a (B200) only");
+  g_ctx.device = dev;
+  g_ctx.rank = 0;
+  g_ctx.world = 1;
+  g_ctx.inited = true;
+}
+
+// ------------------------------------------------------------ regions --
+constexpr int kHistSmemBudget = 96 * 1024;  // counters + LUT per hist block (2 blocks/SM)
+
+struct FNode {  // a frontier node: histogrammed and split-searched at this level
+  int32_t tree_idx;
+  int32_t depth;
+  uint32_t off, len;  // local span in the idx arrays
+  int32_t slot;       // histogram slot at this level
+};
+
+}  // namespace
+}  // namespace adapt
+
+struct adapt_region {
+  std::string id;
+  int F = 0, V = 0, D = 2, min_train = 0;
+  // long-format records (adapt_record)
+  std::vector<float> rfeat;
+  std::vector<int32_t> rvar;
+  std::vector<uint64_t> rns;
+  // wide table
+  int64_t n = 0;
+  bool have_table = false;
+  const float *d_feat = nullptr, *d_times = nullptr;
+  adapt::DevBuf own_feat, own_times;
+  // products of the last train
+  int RS = 0;
+  int64_t trained_n = 0;
+  adapt::DevBuf rec;
+  std::vector<float> val;       // [F][256]
+  std::vector<int32_t> nval;    // [F]
+  std::vector<uint8_t> lut;     // [F][256]
+  adapt::DevBuf d_lut;
+  std::vector<adapt_node_t> tree;
+  adapt::DevBuf d_tree;
+  bool trained = false;
+  std::vector<int64_t> stats;
+  // scratch
+  adapt::DevBuf gkey, gid, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, idxA, idxB, H0,
+      H1, segs, cursors, slots, triples, nslot, cand, res, hoff, grp, xa, xb, oa, ob;
+  adapt::HostBuf hres, hsmall;
+  // Table-1 shim state
+  bool active = false;
+  std::vector<float> ctx_feat;
+  int ctx_policy = -1;
+  timespec t0{};
+  int cursor = 0;
+};
+
+namespace adapt {
+namespace {
+
+std::map<std::string, std::unique_ptr<adapt_region>> g_regions;
+
+int parse_params(const char *p, int *depth) {
+  *depth = 2;  // P:260 default: decision tree of depth 2
+  if (!p || !*p) return 0;
+  std::string s(p);
+  std::vector<std::string> tok;
+  size_t st = 0;
+  while (true) {
+    size_t c = s.find(',', st);
+    std::string t = s.substr(st, c == std::string::npos ? std::string::npos : c - st);
+    t.erase(0, t.find_first_not_of(" \t"));
+    t.erase(t.find_last_not_of(" \t") + 1);
+    tok.push_back(t);
+    if (c == std::string::npos) break;
+    st = c + 1;
+  }
+  if (tok[0] != "dtree" && tok[0] != "DecisionTree")
+    throw Error(ADAPT_E_INVALID_ARG, "model kind '" + tok[0] + "' not supported (dtree)");
+  for (size_t i = 1; i < tok.size(); i++) {
+    const std::string &t = tok[i];
+    if (t.empty()) continue;
+    std::string v = t;
+    if (t.rfind("depth=", 0) == 0) v = t.substr(6);
+    else if (t.rfind("max_depth=", 0) == 0) v = t.substr(10);
+    else if (t.rfind("explore=", 0) == 0) {
+      if (t != "explore=RoundRobin") throw Error(ADAPT_E_INVALID_ARG, "only explore=RoundRobin");
+      continue;
+    }
+    char *end = nullptr;
+    long d = strtol(v.c_str(), &end, 10);
+    if (v.empty() || *end) throw Error(ADAPT_E_INVALID_ARG, "bad model parameter '" + t + "'");
+    if (d < 0 || d > 24) throw Error(ADAPT_E_INVALID_ARG, "depth must be in [0,24]");
+    *depth = (int)d;
+  }
+  return 0;
+}
+
+adapt_region *checked(adapt_region *h) {
+  if (!h) throw Error(ADAPT_E_INVALID_ARG, "null region");
+  for (auto &kv : g_regions)
+    if (kv.second.get() == h) return h;
+  throw Error(ADAPT_E_INVALID_ARG, "unknown region handle");
+}
+
+float canon(float x) { return x == 0.0f ? 0.0f : x; }
+
+// long -> wide: one row per distinct feature vector (exact bits,
+// -0 == +0), in order of first appearance; mean time per variant (R1).
+void aggregate_records(adapt_region *h, std::vector<float> &wf, std::vector<float> &wt) {
+  const int F = h->F, V = h->V;
+  const size_t R = h->rvar.size();
+  std::unordered_map<std::string, int64_t> row_of;
+  std::vector<uint64_t> sum;
+  std::vector<int64_t> cnt;
+  std::string key(F * 4, '\0');
+  for (size_t r = 0; r < R; r++) {
+    for (int f = 0; f < F; f++) {
+      float x = canon(h->rfeat[r * F + f]);
+      memcpy(&key[f * 4], &x, 4);
+    }
+    auto it = row_of.find(key);
+    int64_t row;
+    if (it == row_of.end()) {
+      row = (int64_t)row_of.size();
+      row_of.emplace(key, row);
+      for (int f = 0; f < F; f++) wf.push_back(canon(h->rfeat[r * F + f]));
+      sum.resize(sum.size() + V, 0);
+      cnt.resize(cnt.size() + V, 0);
+    } else {
+      row = it->second;
+    }
+    sum[row * V + h->rvar[r]] += h->rns[r];
+    cnt[row * V + h->rvar[r]] += 1;
+  }
+  wt.resize(sum.size());
+  for (size_t i = 0; i < sum.size(); i++)
+    wt[i] = cnt[i] ? (float)((double)sum[i] / (double)cnt[i]) : INFINITY;
+}
+
+float round_down_f32(double t) {  // largest float32 <= t (V:A5)
+  float f = (float)t;
+  if ((double)f > t) f = std::nextafter(f, -INFINITY);
+  return f;
+}
+
+void upload_tree(adapt_region *h, cudaStream_t s) {
+  std::vector<DNode> d(h->tree.size());
+  for (size_t k = 0; k < h->tree.size(); k++) {
+    const adapt_node_t &nd = h->tree[k];
+    if (nd.feature >= 0) {
+      d[k].thr = round_down_f32(nd.threshold);
+      d[k].meta = (nd.left << 6) | nd.feature;
+    } else {
+      d[k].thr = 0;
+      d[k].meta = -1 - nd.label;
+    }
+  }
+  h->d_tree.ensure(d.size() * sizeof(DNode));
+  CUDA_CHECK(cudaMemcpyAsync(h->d_tree.p, d.data(), d.size() * sizeof(DNode),
+                             cudaMemcpyHostToDevice, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void fill_stats(adapt_node_t &nd, const uint64_t *P, int C) {
+  uint64_t n = 0;
+  unsigned __int128 S = 0;
+  int label = 0;
+  for (int k = 0; k < C; k++) {
+    n += P[k];
+    S += (unsigned __int128)P[k] * P[k];
+    if (P[k] > P[label]) label = k;  // ties -> lowest (R12)
+  }
+  nd.n = (int64_t)n;
+  nd.label = label;
+  nd.gini = n ? 1.0 - (double)(uint64_t)S / ((double)n * (double)n) : 0.0;
+}
+
+bool is_pure(const uint64_t *P, int C) {
+  int present = 0;
+  for (int k = 0; k < C; k++) present += P[k] > 0;
+  return present <= 1;
+}
+
+template <class T>
+void h2d(DevBuf &b, const std::vector<T> &v, cudaStream_t s) {
+  b.ensure(v.size() * sizeof(T) + 16);
+  if (!v.empty())
+    CUDA_CHECK(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+// ------------------------------------------------------------ training --
+void train_region(adapt_region *h, cudaStream_t s) {
+  const int F = h->F, V = h->V, C = V, D = h->D;
+  const int world = g_ctx.world, rank = g_ctx.rank;
+  // 0. source table (wide, or long records aggregated on the host)
+  const float *feat = h->d_feat, *times = h->d_times;
+  int64_t n = h->n;
+  if (!h->have_table) {
+    std::vector<float> wf, wt;
+    aggregate_records(h, wf, wt);
+    n = (int64_t)(wf.size() / F);
+    h->own_feat.ensure(wf.size() * 4 + 16);
+    h->own_times.ensure(wt.size() * 4 + 16);
+    if (n) {
+      CUDA_CHECK(cudaMemcpyAsync(h->own_feat.p, wf.data(), wf.size() * 4, cudaMemcpyHostToDevice, s));
+      CUDA_CHECK(cudaMemcpyAsync(h->own_times.p, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    feat = h->own_feat.as<float>();
+    times = h->own_times.as<float>();
+  }
+  uint64_t n_total = (uint64_t)n;
+  h->hsmall.ensure(1 << 16);
+  if (world > 1) {
+    DevBuf tmp;
+    tmp.ensure(8);
+    CUDA_CHECK(cudaMemcpyAsync(tmp.p, &n_total, 8, cudaMemcpyHostToDevice, s));
+    g_nccl.check(g_nccl.AllReduce(tmp.p, tmp.p, 1, ncclUint64, ncclSum, g_ctx.comm, s), "allreduce n");
+    CUDA_CHECK(cudaMemcpyAsync(&n_total, tmp.p, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  if (n_total == 0) throw Error(ADAPT_E_INSUFFICIENT_DATA, "no training rows");
+  if (n_total >= (1ull << 32)) throw Error(ADAPT_E_INVALID_ARG, "more than 2^32-1 rows");
+  int RS = 2;
+  while (RS < F + 1) RS <<= 1;
+  h->RS = RS;
+
+  // 1. a1 + a2 + a3: one pass over the table
+  h->gkey.ensure((size_t)F * kGSlots * 4);
+  h->gid.ensure((size_t)F * kGSlots * 4);
+  h->gcount.ensure((size_t)F * 4);
+  h->flags.ensure(16);
+  h->rec.ensure((size_t)std::max<int64_t>(n, 1) * RS);
+  CUDA_CHECK(cudaMemsetAsync(h->gkey.p, 0xFF, (size_t)F * kGSlots * 4, s));
+  CUDA_CHECK(cudaMemsetAsync(h->gid.p, 0xFF, (size_t)F * kGSlots * 4, s));
+  CUDA_CHECK(cudaMemsetAsync(h->gcount.p, 0, (size_t)F * 4, s));
+  CUDA_CHECK(cudaMemsetAsync(h->flags.p, 0, 16, s));
+  {
+    Phase ph("ingest", s, (double)n * (4.0 * F + 4.0 * V + F + 1));
+    launch_ingest(feat, times, n, F, V, RS, h->gkey.as<uint32_t>(), h->gid.as<uint32_t>(),
+                  h->gcount.as<uint32_t>(), h->flags.as<uint32_t>(), h->rec.as<uint8_t>(), s);
+  }
+  // a2: value tables, merged over ranks
+  h->lvals.ensure((size_t)F * kMaxBins * 4);
+  h->lcnt.ensure((size_t)F * 4);
+  h->avals.ensure((size_t)world * F * kMaxBins * 4);
+  h->acnt.ensure((size_t)world * F * 4);
+  h->dval.ensure((size_t)F * kMaxBins * 4);
+  h->dnval.ensure((size_t)F * 4);
+  h->d_lut.ensure((size_t)F * kMaxBins);
+  CUDA_CHECK(cudaMemsetAsync(h->lvals.p, 0, (size_t)F * kMaxBins * 4, s));
+  CUDA_CHECK(cudaMemsetAsync(h->d_lut.p, 0, (size_t)F * kMaxBins, s));
+  CUDA_CHECK(cudaMemsetAsync(h->dval.p, 0, (size_t)F * kMaxBins * 4, s));
+  {
+    Phase ph("values", s, 0);
+    launch_collect_values(h->gkey.as<uint32_t>(), h->gid.as<uint32_t>(), h->gcount.as<uint32_t>(),
+                          F, h->lvals.as<float>(), h->lcnt.as<int32_t>(), s);
+  }
+  {
+    if (world > 1) {
+      g_nccl.check(g_nccl.AllGather(h->lvals.p, h->avals.p, (size_t)F * kMaxBins, ncclFloat32,
+                                    g_ctx.comm, s), "allgather values");
+      g_nccl.check(g_nccl.AllGather(h->lcnt.p, h->acnt.p, (size_t)F, ncclInt32, g_ctx.comm, s),
+                   "allgather counts");
+    } else {
+      CUDA_CHECK(cudaMemcpyAsync(h->avals.p, h->lvals.p, (size_t)F * kMaxBins * 4,
+                                 cudaMemcpyDeviceToDevice, s));
+      CUDA_CHECK(cudaMemcpyAsync(h->acnt.p, h->lcnt.p, (size_t)F * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    Phase ph("merge", s, 0);
+    launch_merge_values(h->avals.as<float>(), h->acnt.as<int32_t>(), world, rank, F,
+                        h->dval.as<float>(), h->dnval.as<int32_t>(), h->d_lut.as<uint8_t>(),
+                        h->flags.as<uint32_t>(), s);
+  }
+  // error flags, OR-ed over ranks so that all ranks fail together
+  uint32_t *hs = h->hsmall.as<uint32_t>();
+  {
+    DevBuf fl;
+    fl.ensure(16);
+    // expand bits to counters (sum == OR for 0/1 values)
+    CUDA_CHECK(cudaMemcpyAsync(hs, h->flags.p, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    uint32_t bits[4] = {(hs[0] >> 0) & 1, (hs[0] >> 1) & 1, (hs[0] >> 2) & 1, (hs[0] >> 3) & 1};
+    if (world > 1) {
+      CUDA_CHECK(cudaMemcpyAsync(fl.p, bits, 16, cudaMemcpyHostToDevice, s));
+      g_nccl.check(g_nccl.AllReduce(fl.p, fl.p, 4, ncclUint32, ncclSum, g_ctx.comm, s), "allreduce flags");
+      CUDA_CHECK(cudaMemcpyAsync(bits, fl.p, 16, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    if (bits[0]) throw Error(ADAPT_E_BAD_VALUE, "NaN or Inf feature value");
+    if (bits[1]) throw Error(ADAPT_E_BAD_VALUE, "NaN time");
+    if (bits[2]) throw Error(ADAPT_E_BAD_VALUE, "row with every variant unmeasured (+inf)");
+    if (bits[3]) throw Error(ADAPT_E_TOO_MANY_DISTINCT, "a feature has more than 256 distinct values");
+  }
+  h->val.assign((size_t)F * kMaxBins, 0.f);
+  h->nval.assign(F, 0);
+  h->lut.assign((size_t)F * kMaxBins, 0);
+  CUDA_CHECK(cudaMemcpyAsync(h->val.data(), h->dval.p, (size_t)F * kMaxBins * 4, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaMemcpyAsync(h->nval.data(), h->dnval.p, (size_t)F * 4, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaMemcpyAsync(h->lut.data(), h->d_lut.p, (size_t)F * kMaxBins, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+
+  // histogram layout: node -> [f][rank][class], features packed by D_f
+  std::vector<int32_t> hoff(F);
+  int64_t HS = 0;
+  for (int f = 0; f < F; f++) {
+    hoff[f] = (int32_t)HS;
+    HS += (int64_t)h->nval[f] * C;
+  }
+  // shared-memory groups of the histogram pass: runs of whole features, or
+  // class slabs of one feature whose D_f x C counters alone exceed the budget
+  const int cap = (kHistSmemBudget - F * kMaxBins) / 4;
+  std::vector<int4> groups;
+  int max_group = 0;
+  {
+    int gf0 = 0;
+    int64_t used = 0;
+    auto close = [&](int fend) {
+      if (fend > gf0) {
+        groups.push_back(make_int4(gf0, fend, 0, C));
+        max_group = std::max<int>(max_group, (int)used);
+      }
+      gf0 = fend;
+      used = 0;
+    };
+    for (int f = 0; f < F; f++) {
+      const int64_t need = (int64_t)h->nval[f] * C;
+      if (need > cap) {
+        close(f);
+        const int kw = cap / std::max(1, h->nval[f]);
+        for (int k0 = 0; k0 < C; k0 += kw) groups.push_back(make_int4(f, f + 1, k0, std::min(C, k0 + kw)));
+        max_group = std::max<int>(max_group, h->nval[f] * kw);
+        gf0 = f + 1;
+        continue;
+      }
+      if (used + need > cap) close(f);
+      used += need;
+    }
+    close(F);
+  }
+  const int ngroups = (int)groups.size();
+  h2d(h->hoff, hoff, s);
+  h2d(h->grp, groups, s);
+
+  // 2. level loop (a4-a8)
+  h->tree.clear();
+  h->stats.clear();
+  adapt_node_t root{};
+  root.feature = -1;
+  root.left = root.right = -1;
+  h->tree.push_back(root);
+  std::vector<FNode> frontier{{0, 0, 0, (uint32_t)n, 0}};
+  std::vector<Seg> segs{{0, (uint32_t)n, 0, -1, 0, 2, 0, 0}};
+  std::vector<int32_t> direct_slots{0};
+  std::vector<int32_t> triples;
+  std::vector<int> seg_children;  // per seg: frontier index of left (or -1), right (or -1)
+  seg_children = {-1, -1};
+  h->idxA.ensure((size_t)std::max<int64_t>(n, 1) * 4);
+  h->idxB.ensure((size_t)std::max<int64_t>(n, 1) * 4);
+  uint32_t *idx_prev = nullptr, *idx_next = h->idxA.as<uint32_t>();
+  DevBuf *Hcur = &h->H0, *Hprev = &h->H1;
+  const int res_stride = (int)((sizeof(NodeRes) + 8 * (size_t)C + 7) / 8 * 8);
+  std::vector<uint64_t> P_of_tree;  // class totals per tree node (tree order), C each
+  P_of_tree.reserve(64 * C);
+
+  for (int level = 0; !frontier.empty(); level++) {
+    const int A = (int)frontier.size();
+    const int nseg = (int)segs.size();
+    uint32_t total = 0;
+    for (auto &sg : segs) {
+      sg.row_base = total;
+      total += sg.len;
+    }
+    Hcur->ensure((size_t)A * HS * 4);
+    h2d(h->segs, segs, s);
+    h->cursors.ensure((size_t)nseg * 8 + 8);
+    CUDA_CHECK(cudaMemsetAsync(h->cursors.p, 0, (size_t)nseg * 8, s));
+    h2d(h->slots, direct_slots, s);
+    {
+      Phase ph("zero", s, 0);
+      launch_zero_slots(Hcur->as<uint32_t>(), HS, h->slots.as<int32_t>(), (int)direct_slots.size(), s);
+    }
+    HistPassArgs a{};
+    a.segs = h->segs.as<Seg>();
+    a.nseg = nseg;
+    a.total_rows = total;
+    a.idx_prev = idx_prev;
+    a.idx_next = idx_next;
+    a.cursors = h->cursors.as<uint32_t>();
+    a.rec = h->rec.as<uint8_t>();
+    a.RS = RS;
+    a.F = F;
+    a.C = C;
+    a.lut = h->d_lut.as<uint8_t>();
+    a.hoff = h->hoff.as<int32_t>();
+    a.groups = h->grp.as<int4>();
+    a.ngroups = ngroups;
+    a.smem_counters = max_group;
+    a.H = Hcur->as<uint32_t>();
+    a.HS = HS;
+    a.blocks_per_group = (int)std::max<int64_t>(
+        1, std::min<int64_t>((total + 4095) / 4096, (2 * 148 + ngroups - 1) / ngroups * 2));
+    {
+      Phase ph("hist", s, (double)total * (F + 1));
+      launch_hist_pass(a, s);
+    }
+    if (world > 1 && !direct_slots.empty())
+      g_nccl.check(g_nccl.AllReduce(Hcur->p, Hcur->p, (size_t)direct_slots.size() * HS,
+                                    ncclUint32, ncclSum, g_ctx.comm, s), "allreduce histograms");
+    if (!triples.empty()) {
+      h2d(h->triples, triples, s);
+      Phase ph("subtract", s, 0);
+      launch_subtract(Hcur->as<uint32_t>(), Hprev->as<uint32_t>(), HS, h->triples.as<int32_t>(),
+                      (int)triples.size() / 3, s);
+    }
+    std::vector<int32_t> node_slot(A);
+    for (int j = 0; j < A; j++) node_slot[j] = frontier[j].slot;
+    h2d(h->nslot, node_slot, s);
+    h->cand.ensure((size_t)A * F * sizeof(SplitCand));
+    h->res.ensure((size_t)A * res_stride);
+    {
+      Phase ph("split", s, 0);
+      launch_split(Hcur->as<uint32_t>(), HS, h->nslot.as<int32_t>(), A, F, C, h->hoff.as<int32_t>(),
+                   h->dnval.as<int32_t>(), h->cand.as<SplitCand>(), s);
+    }
+    {
+      Phase ph("winner", s, 0);
+      launch_winner(Hcur->as<uint32_t>(), HS, h->nslot.as<int32_t>(), A, F, C,
+                    h->hoff.as<int32_t>(), h->dnval.as<int32_t>(), h->cand.as<SplitCand>(),
+                    h->res.as<uint8_t>(), res_stride, s);
+    }
+    h->hres.ensure((size_t)A * res_stride + (size_t)nseg * 8);
+    uint8_t *hr = h->hres.as<uint8_t>();
+    CUDA_CHECK(cudaMemcpyAsync(hr, h->res.p, (size_t)A * res_stride, cudaMemcpyDeviceToHost, s));
+    uint32_t *hcur = reinterpret_cast<uint32_t *>(hr + (size_t)A * res_stride);
+    CUDA_CHECK(cudaMemcpyAsync(hcur, h->cursors.p, (size_t)nseg * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+
+    // local spans of this level's frontier nodes from the partition cursors
+    int64_t rows_hist = 0;
+    for (int si = 0; si < nseg && level > 0; si++) {
+      const Seg &sg = segs[si];
+      const int jl = seg_children[2 * si], jr = seg_children[2 * si + 1];
+      if (jl >= 0) frontier[jl].off = sg.off, frontier[jl].len = hcur[2 * si];
+      if (jr >= 0) frontier[jr].off = sg.off + sg.len - hcur[2 * si + 1], frontier[jr].len = hcur[2 * si + 1];
+      if (sg.direct == 0) rows_hist += hcur[2 * si];
+      if (sg.direct == 1) rows_hist += hcur[2 * si + 1];
+    }
+    if (level == 0) rows_hist = total;
+    h->stats.push_back(A);
+    h->stats.push_back(rows_hist);
+    h->stats.push_back(level == 0 ? 0 : total);
+
+    // decide every frontier node; build the next level
+    std::vector<FNode> next;
+    std::vector<Seg> nsegs;
+    std::vector<int32_t> ndirect, nderived_par, nderived_sib;
+    std::vector<int> nderived_j, nchildren;
+    std::vector<uint64_t> P(C), PL(C), PR(C);
+    for (int j = 0; j < A; j++) {
+      const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + (size_t)j * res_stride);
+      const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);
+      const uint32_t *cLd = Pd + C;
+      FNode fn = frontier[j];
+      for (int k = 0; k < C; k++) P[k] = Pd[k];
+      fill_stats(h->tree[fn.tree_idx], P.data(), C);
+      h->tree[fn.tree_idx].depth = fn.depth;
+      if (is_pure(P.data(), C) || !nr->valid) continue;  // leaf (R10)
+      const int f = nr->feat;
+      adapt_node_t &nd = h->tree[fn.tree_idx];
+      nd.feature = f;
+      nd.threshold = ((double)h->val[f * kMaxBins + nr->b_lo] +
+                      (double)h->val[f * kMaxBins + nr->b_hi]) / 2;  // R7
+      const int32_t li = (int32_t)h->tree.size();
+      nd.left = li;
+      nd.right = li + 1;
+      for (int k = 0; k < C; k++) {
+        PL[k] = cLd[k];
+        PR[k] = P[k] - cLd[k];
+      }
+      adapt_node_t cl{}, cr{};
+      cl.feature = cr.feature = -1;
+      cl.left = cl.right = cr.left = cr.right = -1;
+      cl.depth = cr.depth = fn.depth + 1;
+      fill_stats(cl, PL.data(), C);
+      fill_stats(cr, PR.data(), C);
+      const bool inL = fn.depth + 1 < D && !is_pure(PL.data(), C);
+      const bool inR = fn.depth + 1 < D && !is_pure(PR.data(), C);
+      h->tree.push_back(cl);
+      h->tree.push_back(cr);
+      if (!inL && !inR) continue;
+      Seg sg{};
+      sg.off = fn.off;
+      sg.len = fn.len;
+      sg.feat = f;
+      sg.thr = nr->b_lo;
+      sg.write = (inL ? 1 : 0) | (inR ? 2 : 0);
+      const uint64_t nL = nr->nL, nR = nr->n - nr->nL;
+      int dir;
+      if (inL && inR) dir = nL <= nR ? 0 : 1;  // histogram the smaller child
+      else dir = inL ? 0 : 1;
+      sg.direct = dir;
+      sg.hslot = (int32_t)ndirect.size();
+      ndirect.push_back(sg.hslot);
+      int jl = -1, jr = -1;
+      if (inL) {
+        jl = (int)next.size();
+        next.push_back({li, fn.depth + 1, 0, 0, dir == 0 ? sg.hslot : -1});
+      }
+      if (inR) {
+        jr = (int)next.size();
+        next.push_back({li + 1, fn.depth + 1, 0, 0, dir == 1 ? sg.hslot : -1});
+      }
+      if (inL && inR) {  // the other child by subtraction from the parent
+        nderived_j.push_back(dir == 0 ? jr : jl);
+        nderived_par.push_back(fn.slot);
+        nderived_sib.push_back(sg.hslot);
+      }
+      nsegs.push_back(sg);
+      nchildren.push_back(jl);
+      nchildren.push_back(jr);
+    }
+    // derived slots follow the direct ones
+    triples.clear();
+    for (size_t i = 0; i < nderived_j.size(); i++) {
+      const int32_t slot = (int32_t)(ndirect.size() + i);
+      next[nderived_j[i]].slot = slot;
+      triples.push_back(slot);
+      triples.push_back(nderived_par[i]);
+      triples.push_back(nderived_sib[i]);
+    }
+    frontier.swap(next);
+    segs.swap(nsegs);
+    seg_children.swap(nchildren);
+    direct_slots.swap(ndirect);
+    std::swap(Hcur, Hprev);
+    // the spans just written become the input of the next pass
+    idx_prev = idx_next;
+    idx_next = (idx_next == h->idxA.as<uint32_t>()) ? h->idxB.as<uint32_t>() : h->idxA.as<uint32_t>();
+  }
+  // depth of every node (children got theirs when appended)
+  h->trained_n = n;
+  h->trained = true;
+  upload_tree(h, s);
+}
+
+int select_host_walk(adapt_region *h, const float *x) {
+  int k = 0;
+  while (h->tree[k].feature >= 0) {
+    const double v = (double)x[h->tree[k].feature];
+    k = v <= h->tree[k].threshold ? h->tree[k].left : h->tree[k].right;  // NaN -> right (R8)
+  }
+  return h->tree[k].label;
+}
+
+int64_t distinct_pairs(adapt_region *h) {
+  std::unordered_set<std::string> seen;
+  const int F = h->F;
+  std::string key(F * 4 + 4, '\0');
+  for (size_t r = 0; r < h->rvar.size(); r++) {
+    for (int f = 0; f < F; f++) {
+      float x = canon(h->rfeat[r * F + f]);
+      memcpy(&key[f * 4], &x, 4);
+    }
+    memcpy(&key[F * 4], &h->rvar[r], 4);
+    seen.insert(key);
+  }
+  return (int64_t)seen.size();
+}
+
+template <class Fn>
+int guarded(Fn &&fn) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  try {
+    fn();
+    return ADAPT_OK;
+  } catch (const Error &e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception &e) {
+    g_last_error = e.what();
+    return ADAPT_E_CUDA;
+  }
+}
+
+}  // namespace
+}  // namespace adapt
+
+using namespace adapt;
+
+extern "C" {
+
+const char *adapt_last_error(void) { return g_last_error.c_str(); }
+
+const char *adapt_version(void) {
+#ifndef ADAPT_GIT
+#define ADAPT_GIT "dev"
+#endif
+  return "adapt sm_100a " ADAPT_GIT;
+}
+
+int adapt_nccl_unique_id(void *out128) {
+  return guarded([&] {
+    if (!out128) throw Error(ADAPT_E_INVALID_ARG, "null out");
+    g_nccl.load();
+    ncclUniqueId id;
+    g_nccl.check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId");
+    memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int adapt_init(int device, int rank, int world, const void *nccl_unique_id) {
+  return guarded([&] {
+    if (world < 1 || rank < 0 || rank >= world || device < 0)
+      throw Error(ADAPT_E_INVALID_ARG, "bad device/rank/world");
+    if (g_ctx.inited) {
+      if (g_ctx.device == device && g_ctx.rank == rank && g_ctx.world == world) return;
+      if (g_ctx.world == 1 && world == 1 && g_regions.empty()) {
+        g_ctx.inited = false;
+      } else {
+        throw Error(ADAPT_E_USAGE, "already initialised with a different device/rank/world");
+      }
+    }
+    int n = 0;
+    CUDA_CHECK(cudaGetDeviceCount(&n));
+    if (device >= n) throw Error(ADAPT_E_INVALID_ARG, "no such device");
+    CUDA_CHECK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw Error(ADAPT_E_CUDA, "libadapt is built for sm_100a (B200) only");
+    if (world > 1) {
+      if (!nccl_unique_id) throw Error(ADAPT_E_INVALID_ARG, "world > 1 needs an ncclUniqueId");
+      g_nccl.load();
+      ncclUniqueId id;
+      memcpy(&id, nccl_unique_id, sizeof(id));
+      g_nccl.check(g_nccl.CommInitRank(&g_ctx.comm, world, id, rank), "ncclCommInitRank");
+    }
+    g_ctx.device = device;
+    g_ctx.rank = rank;
+    g_ctx.world = world;
+    g_ctx.inited = true;
+  });
+}
+
+int adapt_finalize(void) {
+  return guarded([&] {
+    g_regions.clear();
+    if (g_ctx.comm) g_nccl.CommDestroy(g_ctx.comm);
+    g_ctx = Ctx{};
+  });
+}
+
+int adapt_region_create(const char *id, int num_features, int num_variants,
+                        const char *model_params, int min_train_data, adapt_region_t **out) {
+  return guarded([&] {
+    if (!id || !*id || !out) throw Error(ADAPT_E_INVALID_ARG, "null id or out");
+    *out = nullptr;
+    if (num_features < 1 || num_features > kMaxF)
+      throw Error(ADAPT_E_INVALID_ARG, "num_features must be in [1,64]");
+    if (num_variants < 1 || num_variants > kMaxC)
+      throw Error(ADAPT_E_INVALID_ARG, "num_variants must be in [1,255]");
+    int depth = 2;
+    parse_params(model_params, &depth);
+    const int mtd = min_train_data > 0 ? min_train_data : num_variants;
+    auto it = g_regions.find(id);
+    if (it != g_regions.end()) {
+      adapt_region *h = it->second.get();
+      if (h->F != num_features || h->V != num_variants || h->D != depth || h->min_train != mtd)
+        throw Error(ADAPT_E_SPEC_MISMATCH, std::string("region '") + id + "' exists with another spec");
+      *out = h;
+      return;
+    }
+    auto h = std::make_unique<adapt_region>();
+    h->id = id;
+    h->F = num_features;
+    h->V = num_variants;
+    h->D = depth;
+    h->min_train = mtd;
+    *out = h.get();
+    g_regions.emplace(id, std::move(h));
+  });
+}
+
+int adapt_region_destroy(adapt_region_t *h) {
+  return guarded([&] {
+    checked(h);
+    g_regions.erase(h->id);
+  });
+}
+
+int adapt_region_info(adapt_region_t *h, int *F, int *V, int *D, int *mtd, int64_t *rows,
+                      int *trained) {
+  return guarded([&] {
+    checked(h);
+    if (F) *F = h->F;
+    if (V) *V = h->V;
+    if (D) *D = h->D;
+    if (mtd) *mtd = h->min_train;
+    if (rows) *rows = h->have_table ? h->n : (int64_t)h->rvar.size();
+    if (trained) *trained = h->trained;
+  });
+}
+
+int adapt_record(adapt_region_t *h, const float *features, int variant, uint64_t elapsed_ns) {
+  return guarded([&] {
+    checked(h);
+    if (!features) throw Error(ADAPT_E_INVALID_ARG, "null features");
+    if (variant < 0 || variant >= h->V) throw Error(ADAPT_E_BAD_VALUE, "variant out of range");
+    for (int f = 0; f < h->F; f++)
+      if (!std::isfinite(features[f])) throw Error(ADAPT_E_BAD_VALUE, "non-finite feature");
+    h->rfeat.insert(h->rfeat.end(), features, features + h->F);
+    h->rvar.push_back(variant);
+    h->rns.push_back(elapsed_ns);
+  });
+}
+
+int adapt_record_table(adapt_region_t *h, const float *features, const float *times, int64_t n,
+                       int on_device, void *stream) {
+  return guarded([&] {
+    checked(h);
+    ensure_init();
+    if (n < 0 || (n > 0 && (!features || !times))) throw Error(ADAPT_E_INVALID_ARG, "bad table");
+    cudaStream_t s = (cudaStream_t)stream;
+    h->n = n;
+    h->have_table = true;
+    if (on_device) {
+      h->d_feat = features;
+      h->d_times = times;
+    } else {
+      h->own_feat.ensure((size_t)n * h->F * 4 + 16);
+      h->own_times.ensure((size_t)n * h->V * 4 + 16);
+      Phase ph("h2d", s, (double)n * (h->F + h->V) * 4);
+      if (n) {
+        CUDA_CHECK(cudaMemcpyAsync(h->own_feat.p, features, (size_t)n * h->F * 4, cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(h->own_times.p, times, (size_t)n * h->V * 4, cudaMemcpyHostToDevice, s));
+      }
+      h->d_feat = h->own_feat.as<float>();
+      h->d_times = h->own_times.as<float>();
+    }
+    if (!on_device) CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int adapt_distinct_pairs(adapt_region_t *h, int64_t *count) {
+  return guarded([&] {
+    checked(h);
+    if (!count) throw Error(ADAPT_E_INVALID_ARG, "null count");
+    *count = distinct_pairs(h);
+  });
+}
+
+int adapt_train(adapt_region_t *h, void *stream) {
+  return guarded([&] {
+    checked(h);
+    ensure_init();
+    train_region(h, (cudaStream_t)stream);
+    if (h->have_table && h->d_feat != h->own_feat.as<float>()) {
+      h->d_feat = nullptr;  // borrowed pointers are released when train returns
+      h->d_times = nullptr;
+      h->have_table = false;
+    }
+  });
+}
+
+int adapt_train_many(adapt_region_t *const *hs, int k, void *stream) {
+  if (!hs || k < 0) return guarded([&] { throw Error(ADAPT_E_INVALID_ARG, "bad region list"); });
+  for (int i = 0; i < k; i++) {
+    int rc = adapt_train(hs[i], stream);
+    if (rc) return rc;
+  }
+  return ADAPT_OK;
+}
+
+int adapt_select(adapt_region_t *h, const float *features, int32_t *variant) {
+  return guarded([&] {
+    checked(h);
+    if (!features || !variant) throw Error(ADAPT_E_INVALID_ARG, "null argument");
+    if (!h->trained) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    *variant = select_host_walk(h, features);
+  });
+}
+
+int adapt_select_batch(adapt_region_t *h, const float *d_X, int64_t m, int32_t *d_out,
+                       void *stream) {
+  return guarded([&] {
+    checked(h);
+    ensure_init();
+    if (m < 0 || (m > 0 && (!d_X || !d_out))) throw Error(ADAPT_E_INVALID_ARG, "bad batch");
+    if (!h->trained) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    cudaStream_t s = (cudaStream_t)stream;
+    Phase ph("select", s, (double)m * (4.0 * h->F + 4));
+    launch_select(h->d_tree.as<DNode>(), d_X, m, h->F, d_out, s);
+  });
+}
+
+int adapt_select_batch_host(adapt_region_t *h, const float *X, int64_t m, int32_t *out,
+                            void *stream) {
+  return guarded([&] {
+    checked(h);
+    ensure_init();
+    if (m < 0 || (m > 0 && (!X || !out))) throw Error(ADAPT_E_INVALID_ARG, "bad batch");
+    if (!h->trained) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int F = h->F;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(m, (256ll << 20) / (4 * F)));
+    h->xa.ensure((size_t)chunk * F * 4);
+    h->xb.ensure((size_t)chunk * F * 4);
+    h->oa.ensure((size_t)chunk * 4);
+    h->ob.ensure((size_t)chunk * 4);
+    cudaStream_t st[2];
+    cudaEvent_t ready;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventRecord(ready, s));  // order after prior work on the caller's stream
+    CUDA_CHECK(cudaStreamWaitEvent(st[0], ready, 0));
+    CUDA_CHECK(cudaStreamWaitEvent(st[1], ready, 0));
+    for (int64_t c = 0, i = 0; c < m; c += chunk, i++) {
+      const int64_t k = std::min(chunk, m - c);
+      cudaStream_t q = st[i & 1];
+      float *dx = (i & 1) ? h->xb.as<float>() : h->xa.as<float>();
+      int32_t *dout = (i & 1) ? h->ob.as<int32_t>() : h->oa.as<int32_t>();
+      CUDA_CHECK(cudaMemcpyAsync(dx, X + c * F, (size_t)k * F * 4, cudaMemcpyHostToDevice, q));
+      {
+        Phase ph("select", q, (double)k * (4.0 * F + 4));
+        launch_select(h->d_tree.as<DNode>(), dx, k, F, dout, q);
+      }
+      CUDA_CHECK(cudaMemcpyAsync(out + c, dout, (size_t)k * 4, cudaMemcpyDeviceToHost, q));
+    }
+    CUDA_CHECK(cudaStreamSynchronize(st[0]));
+    CUDA_CHECK(cudaStreamSynchronize(st[1]));
+    cudaStreamDestroy(st[0]);
+    cudaStreamDestroy(st[1]);
+    cudaEventDestroy(ready);
+  });
+}
+
+int adapt_get_tree(adapt_region_t *h, adapt_node_t *out, int32_t cap, int32_t *n_nodes) {
+  return guarded([&] {
+    checked(h);
+    if (!n_nodes) throw Error(ADAPT_E_INVALID_ARG, "null n_nodes");
+    if (!h->trained) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    *n_nodes = (int32_t)h->tree.size();
+    if (!out || cap < (int32_t)h->tree.size()) throw Error(ADAPT_E_INVALID_ARG, "capacity too small");
+    memcpy(out, h->tree.data(), h->tree.size() * sizeof(adapt_node_t));
+  });
+}
+
+int adapt_set_tree(adapt_region_t *h, const adapt_node_t *nodes, int32_t n_nodes) {
+  return guarded([&] {
+    checked(h);
+    ensure_init();
+    if (!nodes || n_nodes < 1) throw Error(ADAPT_E_INVALID_ARG, "empty tree");
+    if (n_nodes >= (1 << 25)) throw Error(ADAPT_E_INVALID_ARG, "tree too large");
+    for (int32_t k = 0; k < n_nodes; k++) {
+      const adapt_node_t &nd = nodes[k];
+      if (nd.feature >= 0) {
+        if (nd.feature >= h->F || nd.left <= k || nd.right != nd.left + 1 || nd.right >= n_nodes ||
+            !std::isfinite(nd.threshold))
+          throw Error(ADAPT_E_INVALID_ARG, "bad internal node " + std::to_string(k));
+      } else if (nd.label < 0 || nd.label >= h->V) {
+        throw Error(ADAPT_E_INVALID_ARG, "bad leaf label at node " + std::to_string(k));
+      }
+    }
+    h->tree.assign(nodes, nodes + n_nodes);
+    h->trained = true;
+    upload_tree(h, 0);
+  });
+}
+
+int adapt_get_labels(adapt_region_t *h, uint8_t *out, int64_t n) {
+  return guarded([&] {
+    checked(h);
+    if (!h->trained || !h->RS) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    if (!out || n != h->trained_n) throw Error(ADAPT_E_INVALID_ARG, "n must equal the trained row count");
+    DevBuf tmp;
+    tmp.ensure((size_t)n + 16);
+    launch_labels_out(h->rec.as<uint8_t>(), n, h->F, h->RS, tmp.as<uint8_t>(), 0);
+    CUDA_CHECK(cudaMemcpy(out, tmp.p, (size_t)n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int adapt_get_value_table(adapt_region_t *h, int f, float *vals, int *count) {
+  return guarded([&] {
+    checked(h);
+    if (!h->trained || h->nval.empty()) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    if (f < 0 || f >= h->F || !vals || !count) throw Error(ADAPT_E_INVALID_ARG, "bad argument");
+    *count = h->nval[f];
+    memcpy(vals, &h->val[(size_t)f * kMaxBins], (size_t)h->nval[f] * 4);
+  });
+}
+
+int adapt_get_bins(adapt_region_t *h, uint8_t *out, int64_t n) {
+  return guarded([&] {
+    checked(h);
+    if (!h->trained || !h->RS) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    if (!out || n != h->trained_n) throw Error(ADAPT_E_INVALID_ARG, "n must equal the trained row count");
+    DevBuf tmp;
+    tmp.ensure((size_t)n * h->F + 16);
+    launch_bins_out(h->rec.as<uint8_t>(), n, h->F, h->RS, h->d_lut.as<uint8_t>(), tmp.as<uint8_t>(), 0);
+    CUDA_CHECK(cudaMemcpy(out, tmp.p, (size_t)n * h->F, cudaMemcpyDeviceToHost));
+  });
+}
+
+int adapt_profile_enable(int enable) {
+  return guarded([&] { g_prof.on = enable != 0; });
+}
+
+int adapt_profile_reset(void) {
+  return guarded([&] {
+    g_prof.drain();
+    for (auto &a : g_prof.acc) a = Prof::Acc{};
+  });
+}
+
+int adapt_profile_get(adapt_phase_t *out, int cap, int *n) {
+  return guarded([&] {
+    if (!n) throw Error(ADAPT_E_INVALID_ARG, "null n");
+    g_prof.drain();
+    *n = (int)g_prof.names.size();
+    for (int i = 0; i < *n && i < cap && out; i++) {
+      memset(&out[i], 0, sizeof(adapt_phase_t));
+      snprintf(out[i].name, sizeof(out[i].name), "%s", g_prof.names[i].c_str());
+      out[i].launches = g_prof.acc[i].launches;
+      out[i].ms = g_prof.acc[i].ms;
+      out[i].bytes = g_prof.acc[i].bytes;
+    }
+  });
+}
+
+int adapt_train_stats(adapt_region_t *h, int64_t *out, int cap, int *levels) {
+  return guarded([&] {
+    checked(h);
+    if (!levels) throw Error(ADAPT_E_INVALID_ARG, "null levels");
+    *levels = (int)(h->stats.size() / 3);
+    for (size_t i = 0; i < h->stats.size() && (int)i < cap && out; i++) out[i] = h->stats[i];
+  });
+}
+
+// ---------------------------------------------------- Apollo Table-1 shim --
+void *__adapt_region_create(const char *id, int num_features, int num_policies,
+                            const char *model_type_params, int min_train_data) {
+  adapt_region_t *h = nullptr;
+  if (adapt_region_create(id, num_features, num_policies, model_type_params, min_train_data, &h))
+    return nullptr;
+  return h;
+}
+
+void __adapt_region_begin(void *r) {
+  guarded([&] {
+    adapt_region *h = checked(static_cast<adapt_region *>(r));
+    if (h->active) throw Error(ADAPT_E_USAGE, "begin while active (S:141)");
+    h->active = true;
+    h->ctx_feat.clear();
+    h->ctx_policy = -1;
+    clock_gettime(CLOCK_MONOTONIC, &h->t0);
+  });
+}
+
+void __adapt_region_set_feature(void *r, float v) {
+  guarded([&] {
+    adapt_region *h = checked(static_cast<adapt_region *>(r));
+    if (!h->active) throw Error(ADAPT_E_USAGE, "set_feature without begin (S:151)");
+    if ((int)h->ctx_feat.size() >= h->F) throw Error(ADAPT_E_ARITY, "too many features (S:151)");
+    h->ctx_feat.push_back(v);
+  });
+}
+
+int __adapt_region_get_policy(void *r) {
+  int policy = 0;
+  int rc = guarded([&] {
+    adapt_region *h = checked(static_cast<adapt_region *>(r));
+    if (!h->active) throw Error(ADAPT_E_USAGE, "get_policy without begin");
+    if ((int)h->ctx_feat.size() != h->F) throw Error(ADAPT_E_ARITY, "features incomplete (S:161)");
+    if (h->trained) {
+      policy = select_host_walk(h, h->ctx_feat.data());
+    } else {  // round-robin exploration
+      policy = h->cursor;
+      h->cursor = (h->cursor + 1) % h->V;
+    }
+    h->ctx_policy = policy;
+  });
+  return rc ? 0 : policy;
+}
+
+void __adapt_region_end(void *r) {
+  guarded([&] {
+    adapt_region *h = checked(static_cast<adapt_region *>(r));
+    if (!h->active) throw Error(ADAPT_E_USAGE, "end without begin (S:171)");
+    timespec t1;
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    h->active = false;
+    if (h->ctx_policy < 0 || (int)h->ctx_feat.size() != h->F) return;  // nothing to record
+    int64_t ns = (int64_t)(t1.tv_sec - h->t0.tv_sec) * 1000000000ll + (t1.tv_nsec - h->t0.tv_nsec);
+    if (ns < 0) ns = 0;
+    int rc = adapt_record(h, h->ctx_feat.data(), h->ctx_policy, (uint64_t)ns);
+    if (rc) throw Error(rc, g_last_error);
+    if (!h->trained && !h->have_table && distinct_pairs(h) >= h->min_train) {  // P:569 auto-train
+      rc = adapt_train(h, nullptr);
+      if (rc) throw Error(rc, g_last_error);
+    }
+  });
+}
+
+void __adapt_region_train(void *r) {
+  guarded([&] {
+    adapt_region *h = checked(static_cast<adapt_region *>(r));
+    if (h->rvar.empty() && !h->have_table) throw Error(ADAPT_E_INSUFFICIENT_DATA, "no records (S:181)");
+    int rc = adapt_train(h, nullptr);
+    if (rc) throw Error(rc, g_last_error);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,482 @@
+// train.cu — the level-wise CART trainer's kernels.
+//
+// One tree level = one pass over the rows of the nodes being split:
+//   hist_pass_kernel  a7 partition of the previous level's splits (rows of a
+//                     parent span are scattered to the children's spans, left
+//                     from the front, right from the back) fused with a4, the
+//                     class histogram H[node][f][rank][class] of ONE child per
+//                     parent (the smaller, "direct" one), privatised in shared
+//                     memory and flushed with integer atomics;
+//   subtract_kernel   the other ("derived") child = parent - direct sibling
+//                     (exact integer histogram subtraction);
+//   split_kernel      a6 per (node, feature): class-chunked block prefix scan
+//                     over bins, exact rational Gini score of every cut
+//                     between consecutive node-nonempty bins, block argmax;
+//   winner_kernel     per node: best feature (ties -> lowest f), plus the class
+//                     totals of the node and of the winning left child.
+// Every quantity that decides the tree is an integer, so the result does not
+// depend on row order, on the number of ranks or on atomic ordering.
+#include "common.h"
+
+namespace adapt {
+namespace {
+
+constexpr int kHistThreads = 512;
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int RS>
+struct RecWords {
+  static constexpr int N = RS >= 4 ? RS / 4 : 1;
+  uint32_t w[N];
+};
+
+template <int RS>
+__device__ __forceinline__ void load_rec(const uint8_t *__restrict__ p, RecWords<RS> &r) {
+  if constexpr (RS >= 16) {
+#pragma unroll
+    for (int i = 0; i < RS / 16; i++) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p) + i);
+      r.w[4 * i + 0] = v.x;
+      r.w[4 * i + 1] = v.y;
+      r.w[4 * i + 2] = v.z;
+      r.w[4 * i + 3] = v.w;
+    }
+  } else if constexpr (RS == 8) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+    r.w[0] = v.x;
+    r.w[1] = v.y;
+  } else if constexpr (RS == 4) {
+    r.w[0] = __ldg(reinterpret_cast<const uint32_t *>(p));
+  } else {
+    r.w[0] = __ldg(reinterpret_cast<const uint16_t *>(p));
+  }
+}
+
+template <int RS>
+__device__ __forceinline__ int rec_byte(const RecWords<RS> &r, int f) {
+  // f is warp-uniform per segment; a small unrolled select keeps r in registers
+  int out = 0;
+#pragma unroll
+  for (int i = 0; i < RecWords<RS>::N; i++)
+    if ((f >> 2) == i) out = (int)((r.w[i] >> (8 * (f & 3))) & 0xFFu);
+  return out;
+}
+
+template <int RS>
+__global__ void __launch_bounds__(kHistThreads) hist_pass_kernel(HistPassArgs a) {
+  extern __shared__ uint32_t sh[];  // [smem_counters] counters | lut [F*256] bytes
+  uint8_t *slut = reinterpret_cast<uint8_t *>(sh + a.smem_counters);
+  __shared__ int32_t sloff[kMaxF];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int g = blockIdx.y;
+  // group g: features [f0, f1) x classes [k0, k1); its counters are laid out
+  // [f][rank][k - k0], i.e. the node layout restricted to the class slab
+  const int4 grp = a.groups[g];
+  const int f0 = grp.x, f1 = grp.y, k0 = grp.z, kw = grp.w - grp.z;
+  const int C = a.C;
+  const int gcount = ((f1 < a.F ? a.hoff[f1] : (int)a.HS) - a.hoff[f0]) / C * kw;
+  for (int i = tid; i < a.F * kMaxBins / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t *>(slut)[i] = reinterpret_cast<const uint32_t *>(a.lut)[i];
+  for (int f = tid; f < a.F; f += blockDim.x) sloff[f] = (a.hoff[f] - a.hoff[f0]) / C * kw;
+
+  const uint32_t R = (a.total_rows + a.blocks_per_group - 1) / a.blocks_per_group;
+  uint32_t p0 = blockIdx.x * R;
+  const uint32_t p1 = min(p0 + R, a.total_rows);
+  // first segment whose span contains position p0
+  int s = 0;
+  {
+    int lo = 0, hi = a.nseg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.segs[mid].row_base <= p0) lo = mid; else hi = mid - 1;
+    }
+    s = lo;
+  }
+  __syncthreads();
+  while (p0 < p1 && s < a.nseg) {
+    const Seg sg = a.segs[s];
+    const uint32_t q0 = p0 - sg.row_base;
+    const uint32_t q1 = min(sg.len, p1 - sg.row_base);
+    const bool hist_on = sg.direct >= 0 && sg.hslot >= 0;
+    const bool part_on = g == 0 && sg.feat >= 0 && sg.write != 0;
+    if (q0 < q1 && (hist_on || part_on)) {
+      if (hist_on) {
+        for (int i = tid; i < gcount; i += blockDim.x) sh[i] = 0;
+        __syncthreads();
+      }
+      for (uint32_t qb = q0; qb < q1; qb += blockDim.x) {
+        const uint32_t q = qb + tid;
+        const bool valid = q < q1;
+        uint32_t row = 0;
+        RecWords<RS> r;
+        int label = 0;
+        bool left = true;
+        if (valid) {
+          row = a.idx_prev ? __ldg(a.idx_prev + sg.off + q) : sg.off + q;
+          const uint8_t *rp = a.rec + (size_t)row * RS;
+          load_rec<RS>(rp, r);
+          label = rec_byte<RS>(r, a.F);
+          if (sg.feat >= 0) left = slut[sg.feat * kMaxBins + rec_byte<RS>(r, sg.feat)] <= sg.thr;
+        }
+        if (part_on) {  // a7: scatter the row id into the child's span
+#pragma unroll
+          for (int side = 0; side < 2; side++) {
+            const bool mine = valid && (side == 0 ? left : !left) && ((sg.write >> side) & 1);
+            const unsigned m = __ballot_sync(kFull, mine);
+            if (m) {
+              const int leader = __ffs(m) - 1;
+              uint32_t base = 0;
+              if (lane == leader) base = atomicAdd(a.cursors + 2 * s + side, __popc(m));
+              base = __shfl_sync(kFull, base, leader);
+              if (mine) {
+                const uint32_t k = base + __popc(m & ((1u << lane) - 1));
+                a.idx_next[side == 0 ? sg.off + k : sg.off + sg.len - 1 - k] = row;
+              }
+            }
+          }
+        }
+        if (hist_on && valid && (unsigned)(label - k0) < (unsigned)kw &&
+            (sg.direct == 2 || (sg.direct == 0 && left) || (sg.direct == 1 && !left))) {
+#pragma unroll
+          for (int wi = 0; wi < RecWords<RS>::N; wi++) {
+#pragma unroll
+            for (int bi = 0; bi < 4; bi++) {
+              const int f = wi * 4 + bi;
+              if (f >= f0 && f < f1) {
+                const int bin = (r.w[wi] >> (8 * bi)) & 0xFF;
+                atomicAdd(&sh[sloff[f] + (int)slut[f * kMaxBins + bin] * kw + (label - k0)], 1u);
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (hist_on) {  // flush the block's partial histogram
+        uint32_t *dst = a.H + (size_t)sg.hslot * a.HS + a.hoff[f0];
+        if (kw == C) {
+          for (int i = tid; i < gcount; i += blockDim.x) {
+            const uint32_t v = sh[i];
+            if (v) atomicAdd(dst + i, v);
+          }
+        } else {  // class slab of one feature: row r, class k0 + j
+          for (int i = tid; i < gcount; i += blockDim.x) {
+            const uint32_t v = sh[i];
+            const int r = i / kw, j = i - r * kw;
+            if (v) atomicAdd(dst + r * C + k0 + j, v);
+          }
+        }
+        __syncthreads();
+      }
+    }
+    p0 = sg.row_base + q1;
+    s++;
+  }
+}
+
+__global__ void zero_slots_kernel(uint32_t *H, int64_t HS, const int32_t *slots) {
+  uint32_t *h = H + (size_t)slots[blockIdx.y] * HS;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < HS;
+       i += (int64_t)gridDim.x * blockDim.x)
+    h[i] = 0;
+}
+
+// triples: (dst slot in H, parent slot in Hprev, direct sibling slot in H)
+__global__ void subtract_kernel(uint32_t *H, const uint32_t *Hprev, int64_t HS,
+                                const int32_t *triples) {
+  const int32_t *t = triples + 3 * blockIdx.y;
+  uint32_t *d = H + (size_t)t[0] * HS;
+  const uint32_t *p = Hprev + (size_t)t[1] * HS;
+  const uint32_t *q = H + (size_t)t[2] * HS;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < HS;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = p[i] - q[i];
+}
+
+// ---- exact comparison of scores num/den (num < 2^97, den < 2^64) ----
+struct Key {
+  uint64_t hi, lo, den;
+  int idx;     // bin rank (split) or feature (winner): lower wins ties
+  int valid;
+};
+
+__device__ __forceinline__ void mul128x64(uint64_t hi, uint64_t lo, uint64_t d, uint64_t &w2,
+                                          uint64_t &w1, uint64_t &w0) {
+  w0 = lo * d;
+  const uint64_t a = __umul64hi(lo, d);
+  const uint64_t b = hi * d;
+  const uint64_t c = __umul64hi(hi, d);
+  w1 = a + b;
+  w2 = c + (w1 < a ? 1 : 0);
+}
+
+// true if x is strictly better than y: valid first, larger score, then lower idx
+__device__ __forceinline__ bool better(const Key &x, const Key &y) {
+  if (x.valid != y.valid) return x.valid > y.valid;
+  if (!x.valid) return x.idx < y.idx;
+  uint64_t a2, a1, a0, b2, b1, b0;
+  mul128x64(x.hi, x.lo, y.den, a2, a1, a0);  // x.num * y.den
+  mul128x64(y.hi, y.lo, x.den, b2, b1, b0);  // y.num * x.den
+  if (a2 != b2) return a2 > b2;
+  if (a1 != b1) return a1 > b1;
+  if (a0 != b0) return a0 > b0;
+  return x.idx < y.idx;
+}
+
+__device__ __forceinline__ Key shfl_key(const Key &k, int src) {
+  Key o;
+  o.hi = __shfl_sync(kFull, k.hi, src);
+  o.lo = __shfl_sync(kFull, k.lo, src);
+  o.den = __shfl_sync(kFull, k.den, src);
+  o.idx = __shfl_sync(kFull, k.idx, src);
+  o.valid = __shfl_sync(kFull, k.valid, src);
+  return o;
+}
+
+constexpr int kSplitThreads = 256;  // = max bins per feature
+constexpr int kClassChunk = 32;
+
+__global__ void __launch_bounds__(kSplitThreads)
+    split_kernel(const uint32_t *__restrict__ H, int64_t HS, const int32_t *node_slot, int F,
+                 int C, const int32_t *hoff, const int32_t *nval, SplitCand *out) {
+  __shared__ uint32_t tile[kSplitThreads][kClassChunk + 1];
+  __shared__ uint32_t segtot[kSplitThreads / 32][kClassChunk];
+  __shared__ uint32_t Pk[kClassChunk];
+  __shared__ uint64_t nLs[kSplitThreads];
+  __shared__ uint32_t nonempty[kSplitThreads / 32];
+  __shared__ Key wbest[kSplitThreads / 32];
+
+  const int node = blockIdx.x, f = blockIdx.y;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int Df = nval[f];
+  const uint32_t *h = H + (size_t)node_slot[node] * HS + hoff[f];
+  uint64_t nl = 0, sl = 0, sr = 0, ntot = 0;
+  for (int c0 = 0; c0 < C; c0 += kClassChunk) {
+    const int kc = min(kClassChunk, C - c0);
+    for (int e = t; e < Df * kc; e += kSplitThreads) {
+      const int r = e / kc, k = e - r * kc;
+      tile[r][k] = __ldg(h + (size_t)r * C + c0 + k);
+    }
+    __syncthreads();
+    // prefix over bins: warp w scans rows [32w, 32w+32) of column `lane`
+    const int r0 = w * 32, r1 = min(r0 + 32, Df);
+    if (lane < kc) {
+      uint32_t acc = 0;
+      for (int r = r0; r < r1; r++) {
+        acc += tile[r][lane];
+        tile[r][lane] = acc;
+      }
+      segtot[w][lane] = acc;
+    }
+    __syncthreads();
+    if (lane < kc) {
+      uint32_t off = 0, tot = 0;
+      for (int v = 0; v < kSplitThreads / 32; v++) {
+        const uint32_t x = segtot[v][lane];
+        if (v < w) off += x;
+        tot += x;
+      }
+      for (int r = r0; r < r1; r++) tile[r][lane] += off;
+      if (w == 0) Pk[lane] = tot;
+    }
+    __syncthreads();
+    for (int k = 0; k < kc; k++) ntot += Pk[k];
+    if (t < Df) {
+      for (int k = 0; k < kc; k++) {
+        const uint64_t c = tile[t][k];
+        const uint64_t cr = (uint64_t)Pk[k] - c;
+        nl += c;
+        sl += c * c;
+        sr += cr * cr;
+      }
+    }
+    __syncthreads();
+  }
+  if (t < Df) nLs[t] = nl;
+  __syncthreads();
+  const uint64_t cnt = t < Df ? nl - (t > 0 ? nLs[t - 1] : 0) : 0;
+  const unsigned ne = __ballot_sync(kFull, cnt > 0);
+  if (lane == 0) nonempty[w] = ne;
+  __syncthreads();
+  Key k;
+  k.valid = 0;
+  k.idx = t;
+  k.hi = k.lo = 0;
+  k.den = 1;
+  int b_hi = -1;
+  if (t < Df && cnt > 0 && nl < ntot) {
+    // next node-nonempty bin after t
+    unsigned m = nonempty[w] & (lane == 31 ? 0u : (kFull << (lane + 1)));
+    int ww = w;
+    while (!m && ++ww < kSplitThreads / 32) m = nonempty[ww];
+    b_hi = ww * 32 + __ffs(m) - 1;
+    const uint64_t nR = ntot - nl;
+    // num = sl*nR + sr*nl  (128-bit)
+    const uint64_t x0 = sl * nR, x1 = __umul64hi(sl, nR);
+    const uint64_t y0 = sr * nl, y1 = __umul64hi(sr, nl);
+    k.lo = x0 + y0;
+    k.hi = x1 + y1 + (k.lo < x0 ? 1 : 0);
+    k.den = nl * nR;
+    k.valid = 1;
+  }
+  // block argmax (ties -> lowest bin rank = lowest threshold)
+  Key best = k;
+  int best_hi = b_hi;
+  uint64_t best_nl = nl;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const Key other = shfl_key(best, lane ^ o);
+    const int oh = __shfl_sync(kFull, best_hi, lane ^ o);
+    const uint64_t on = __shfl_sync(kFull, best_nl, lane ^ o);
+    if (better(other, best)) {
+      best = other;
+      best_hi = oh;
+      best_nl = on;
+    }
+  }
+  __shared__ int whi[kSplitThreads / 32];
+  __shared__ uint64_t wnl[kSplitThreads / 32];
+  if (lane == 0) {
+    wbest[w] = best;
+    whi[w] = best_hi;
+    wnl[w] = best_nl;
+  }
+  __syncthreads();
+  if (t == 0) {
+    Key b = wbest[0];
+    int bh = whi[0];
+    uint64_t bn = wnl[0];
+    for (int v = 1; v < kSplitThreads / 32; v++)
+      if (better(wbest[v], b)) {
+        b = wbest[v];
+        bh = whi[v];
+        bn = wnl[v];
+      }
+    SplitCand c;
+    c.num_lo = b.lo;
+    c.num_hi = b.hi;
+    c.den = b.den;
+    c.nL = bn;
+    c.valid = b.valid;
+    c.b_lo = b.idx;
+    c.b_hi = bh;
+    c.pad = 0;
+    out[(size_t)node * F + f] = c;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    winner_kernel(const uint32_t *__restrict__ H, int64_t HS, const int32_t *node_slot, int F,
+                  int C, const int32_t *hoff, const int32_t *nval, const SplitCand *cand,
+                  uint8_t *res, int res_stride) {
+  __shared__ int s_f;
+  __shared__ SplitCand s_c;
+  __shared__ unsigned long long s_n;
+  const int node = blockIdx.x, t = threadIdx.x;
+  if (t == 0) {
+    int bf = -1;
+    Key bk;
+    bk.valid = 0;
+    bk.idx = 0x7fffffff;
+    bk.hi = bk.lo = 0;
+    bk.den = 1;
+    for (int f = 0; f < F; f++) {
+      const SplitCand &c = cand[(size_t)node * F + f];
+      Key k;
+      k.valid = c.valid;
+      k.idx = f;
+      k.hi = c.num_hi;
+      k.lo = c.num_lo;
+      k.den = c.den;
+      if (k.valid && better(k, bk)) {
+        bk = k;
+        bf = f;
+      }
+    }
+    s_f = bf;
+    if (bf >= 0) s_c = cand[(size_t)node * F + bf];
+    s_n = 0;
+  }
+  __syncthreads();
+  const int fsel = s_f >= 0 ? s_f : 0;
+  const int blo = s_f >= 0 ? s_c.b_lo : -1;
+  const uint32_t *h = H + (size_t)node_slot[node] * HS + hoff[fsel];
+  const int Df = nval[fsel];
+  NodeRes *nr = reinterpret_cast<NodeRes *>(res + (size_t)node * res_stride);
+  uint32_t *P = reinterpret_cast<uint32_t *>(nr + 1);
+  uint32_t *cL = P + C;
+  for (int k = t; k < C; k += blockDim.x) {
+    uint32_t tot = 0, left = 0;
+    for (int r = 0; r < Df; r++) {
+      const uint32_t v = __ldg(h + (size_t)r * C + k);
+      tot += v;
+      if (r <= blo) left += v;
+    }
+    P[k] = tot;
+    cL[k] = left;
+    atomicAdd(&s_n, (unsigned long long)tot);
+  }
+  __syncthreads();
+  if (t == 0) {
+    nr->n = s_n;
+    nr->valid = s_f >= 0;
+    nr->feat = s_f;
+    nr->nL = s_f >= 0 ? s_c.nL : 0;
+    nr->b_lo = s_f >= 0 ? s_c.b_lo : -1;
+    nr->b_hi = s_f >= 0 ? s_c.b_hi : -1;
+  }
+}
+
+}  // namespace
+
+void launch_hist_pass(const HistPassArgs &a, cudaStream_t s) {
+  if (a.total_rows == 0 || a.nseg == 0) return;
+  const size_t smem = (size_t)a.smem_counters * 4 + (size_t)a.F * kMaxBins;
+  dim3 grid(a.blocks_per_group, a.ngroups);
+  switch (a.RS) {
+#define CASE(R)                                                                               \
+  case R:                                                                                     \
+    CUDA_CHECK(cudaFuncSetAttribute(hist_pass_kernel<R>,                                      \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
+    hist_pass_kernel<R><<<grid, kHistThreads, smem, s>>>(a);                                  \
+    break;
+    CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) CASE(128)
+#undef CASE
+    default:
+      throw Error(-1, "bad record stride");
+  }
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_zero_slots(uint32_t *H, int64_t HS, const int32_t *slots, int n, cudaStream_t s) {
+  if (n == 0) return;
+  const int bx = (int)std::min<int64_t>((HS + 1023) / 1024, 64);
+  zero_slots_kernel<<<dim3(bx, n), 1024, 0, s>>>(H, HS, slots);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t HS, const int32_t *triples,
+                     int n, cudaStream_t s) {
+  if (n == 0) return;
+  const int bx = (int)std::min<int64_t>((HS + 1023) / 1024, 64);
+  subtract_kernel<<<dim3(bx, n), 1024, 0, s>>>(H, Hprev, HS, triples);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_split(const uint32_t *H, int64_t HS, const int32_t *node_slot, int nnodes, int F,
+                  int C, const int32_t *hoff, const int32_t *nval, SplitCand *out,
+                  cudaStream_t s) {
+  if (nnodes == 0) return;
+  split_kernel<<<dim3(nnodes, F), kSplitThreads, 0, s>>>(H, HS, node_slot, F, C, hoff, nval, out);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_winner(const uint32_t *H, int64_t HS, const int32_t *node_slot, int nnodes, int F,
+                   int C, const int32_t *hoff, const int32_t *nval, const SplitCand *cand,
+                   uint8_t *res, int res_stride, cudaStream_t s) {
+  if (nnodes == 0) return;
+  winner_kernel<<<nnodes, 256, 0, s>>>(H, HS, node_slot, F, C, hoff, nval, cand, res,
+                                       res_stride);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace adapt

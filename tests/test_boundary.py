@@ -1,0 +1,125 @@
+"""The C-ABI boundary on a CPU box: libadapt.so loads, exports every symbol that
+include/adapt.h declares, validates arguments on the host, and fails loudly
+(ADAPT_E_CUDA) instead of falling back when no GPU is present."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "adapt.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(__adapt_\w+|adapt_\w+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported():
+    import paper_2303_08873_b200 as ad
+
+    lib = ctypes.CDLL(ad.LIB_PATH)
+    names = _declared()
+    assert len(names) >= 30
+    for n in names:
+        assert hasattr(lib, n), f"{n} declared in adapt.h but not exported"
+    assert sorted(ad.SYMBOLS) == names
+
+
+def test_host_side_validation():
+    import paper_2303_08873_b200 as ad
+
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_region_create("b0", 0, 2)
+    assert e.value.code == ad.ADAPT_E_INVALID_ARG
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_region_create("b0", 65, 2)
+    assert e.value.code == ad.ADAPT_E_INVALID_ARG
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_region_create("b0", 2, 256)
+    assert e.value.code == ad.ADAPT_E_INVALID_ARG
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_region_create("b0", 2, 2, "rfc,10,4")
+    assert e.value.code == ad.ADAPT_E_INVALID_ARG
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_region_create("b0", 2, 2, "dtree,depth=25")
+    assert e.value.code == ad.ADAPT_E_INVALID_ARG
+    h = ad.adapt_region_create("b1", 1, 2)  # P:249 / P:260 defaults
+    info = ad.adapt_region_info(h)
+    assert info["max_depth"] == 2 and info["min_train_data"] == 2 and not info["trained"]
+    assert ad.adapt_region_create("b1", 1, 2) == h  # S:134 same spec -> same handle
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_region_create("b1", 1, 3)
+    assert e.value.code == ad.ADAPT_E_SPEC_MISMATCH
+    for params, depth in [("dtree,4", 4), ("dtree,depth=7", 7), ("DecisionTree,explore=RoundRobin", 2)]:
+        h2 = ad.adapt_region_create(f"p_{depth}_{len(params)}", 1, 2, params)
+        assert ad.adapt_region_info(h2)["max_depth"] == depth
+    # long-format records are validated and counted on the host
+    ad.adapt_record(h, np.array([8.0], np.float32), 0, 5)
+    ad.adapt_record(h, np.array([8.0], np.float32), 0, 7)
+    ad.adapt_record(h, np.array([-0.0], np.float32), 1, 3)
+    ad.adapt_record(h, np.array([0.0], np.float32), 1, 3)
+    assert ad.adapt_distinct_pairs(h) == 2
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_record(h, np.array([np.nan], np.float32), 0, 1)
+    assert e.value.code == ad.ADAPT_E_BAD_VALUE
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_record(h, np.array([1.0], np.float32), 2, 1)
+    assert e.value.code == ad.ADAPT_E_BAD_VALUE
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_select(h, np.zeros(1, np.float32))
+    assert e.value.code == ad.ADAPT_E_NOT_TRAINED
+    ad.adapt_region_destroy(h)
+
+
+def test_shim_usage_errors_on_host():
+    import paper_2303_08873_b200 as ad
+
+    r = ad.__adapt_region_create("shim_cpu", 2, 3, None, 0)
+    assert r
+    ad.__adapt_region_end(r)
+    assert "end without begin" in ad.adapt_last_error()
+    ad.__adapt_region_begin(r)
+    ad.__adapt_region_begin(r)
+    assert "begin while active" in ad.adapt_last_error()
+    ad.__adapt_region_set_feature(r, 1.0)
+    assert ad.__adapt_region_get_policy(r) == 0 and "incomplete" in ad.adapt_last_error()
+    ad.__adapt_region_set_feature(r, 2.0)
+    ad.__adapt_region_set_feature(r, 3.0)
+    assert "too many features" in ad.adapt_last_error()
+    # untrained: round robin over the 3 variants, exploration cursor persists
+    assert ad.__adapt_region_get_policy(r) == 0
+    ad.__adapt_region_end(r)
+    pols = []
+    for _ in range(5):
+        ad.__adapt_region_begin(r)
+        ad.__adapt_region_set_feature(r, 1.0)
+        ad.__adapt_region_set_feature(r, 2.0)
+        pols.append(ad.__adapt_region_get_policy(r))
+        ad.__adapt_region_end(r)
+    assert pols == [1, 2, 0, 1, 2]
+    assert ad.__adapt_region_create("shim_cpu", 2, 4, None, 0) is None  # spec mismatch
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_gpu_fails_loudly():
+    import paper_2303_08873_b200 as ad
+
+    h = ad.adapt_region_create("nogpu", 1, 2)
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_record_table(h, np.ones((4, 1), np.float32), np.ones((4, 2), np.float32), 4, False)
+    assert e.value.code == ad.ADAPT_E_CUDA
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_train(h)
+    assert e.value.code == ad.ADAPT_E_CUDA
+
+
+def test_product_path_never_touches_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2303_08873_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "oracle.h" not in txt and "liboracle" not in txt, f

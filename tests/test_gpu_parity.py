@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by
+element, on seeded inputs.  Bit-exact for labels, value tables,
+bins, tree topology / features / thresholds / labels / counts and selections;
+Gini within 1e-12 relative (north_star), which the engine in fact meets exactly."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes too
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2303_08873_b200 as ad  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _init():
+    torch.cuda.set_device(DEV)
+    ad.adapt_init(0, 0, 1)
+    yield
+
+
+_uid = [0]
+
+
+def _region(F, V, D):
+    _uid[0] += 1
+    return ad.adapt_region_create(f"t{_uid[0]}", F, V, f"dtree,depth={D}", 0)
+
+
+def _train(X, T, D, on_device=True):
+    n, F = X.shape
+    V = T.shape[1]
+    h = _region(F, V, D)
+    s = torch.cuda.current_stream()
+    if on_device:
+        dX, dT = torch.from_numpy(X).to(DEV), torch.from_numpy(T).to(DEV)
+        ad.adapt_record_table(h, dX, dT, n, True, s)
+    else:
+        ad.adapt_record_table(h, X, T, n, False, s)
+    ad.adapt_train(h, s)
+    return h
+
+
+def assert_tree_equal(got, ref):
+    assert len(got) == len(ref), f"{len(got)} nodes vs oracle {len(ref)}"
+    for k in ("feature", "left", "right", "label", "depth", "n"):
+        bad = np.nonzero(got[k] != ref[k])[0]
+        assert bad.size == 0, f"{k} differs at nodes {bad[:10]}"
+    assert got["threshold"].tobytes() == ref["threshold"].tobytes(), "thresholds differ"
+    np.testing.assert_allclose(got["gini"], ref["gini"], rtol=1e-12, atol=0)
+
+
+def full_parity(X, T, D, select_X=None, on_device=True):
+    n, F = X.shape
+    V = T.shape[1]
+    h = _train(X, T, D, on_device)
+    y = oracle.labels(T)
+    assert np.array_equal(ad.adapt_get_labels(h, n), y), "labels differ"
+    for f in range(F):
+        assert np.array_equal(ad.adapt_get_value_table(h, f), oracle.value_table(X, f))
+    assert np.array_equal(ad.adapt_get_bins(h, n, F), oracle.bins(X)), "bins differ"
+    ref = oracle.train(X, y, V, D)
+    got = ad.adapt_get_tree(h)
+    assert_tree_equal(got, ref)
+    Xs = X if select_X is None else select_X
+    m = len(Xs)
+    out = torch.empty(m, dtype=torch.int32, device=DEV)
+    ad.adapt_select_batch(h, torch.from_numpy(np.ascontiguousarray(Xs)).to(DEV), m, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.select(ref, Xs)), "selections differ"
+    # host walk (Table-1 get_policy) agrees with the batch kernel
+    for i in range(0, m, max(1, m // 50)):
+        assert ad.adapt_select(h, Xs[i]) == int(out[i])
+    ad.adapt_region_destroy(h)
+    return got
+
+
+# ------------------------------------------------------------ generator --
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_synth_device_matches_host(name):
+    cfg = synth.CONFIGS[name]
+    n = min(cfg.N, 20000)
+    row0 = 12345 if cfg.N > 100000 else 0
+    X, T = synth.generate(cfg, row0, n)
+    flat, off = cfg.grid_table
+    g = torch.from_numpy(flat).to(DEV)
+    o = torch.from_numpy(off).to(DEV)
+    dX = torch.empty((n, cfg.F), dtype=torch.float32, device=DEV)
+    dT = torch.empty((n, cfg.V), dtype=torch.float32, device=DEV)
+    synth.generate_device(cfg, row0, n, dX.data_ptr(), dT.data_ptr(), g.data_ptr(), o.data_ptr())
+    torch.cuda.synchronize()
+    assert dX.cpu().numpy().tobytes() == X.tobytes()
+    assert dT.cpu().numpy().tobytes() == T.tobytes()
+
+
+# ------------------------------------------------------------ configs --
+def test_c1_full():
+    cfg = synth.CONFIGS["C1"]
+    X, T = synth.generate(cfg, 0, cfg.N)
+    full_parity(X, T, cfg.D)
+
+
+def test_c2_three_regions():
+    cfg = synth.CONFIGS["C2"]
+    X, T = synth.generate(cfg, 0, cfg.N)
+    hs, refs = [], []
+    s = torch.cuda.current_stream()
+    keep = []
+    for r in range(cfg.regions):
+        rows = synth.region_rows(cfg, r)
+        Xr, Tr = np.ascontiguousarray(X[rows]), np.ascontiguousarray(T[rows])
+        h = _region(cfg.F, cfg.V, cfg.D)
+        dX, dT = torch.from_numpy(Xr).to(DEV), torch.from_numpy(Tr).to(DEV)
+        keep.append((dX, dT))
+        ad.adapt_record_table(h, dX, dT, len(rows), True, s)
+        hs.append(h)
+        refs.append(oracle.train(Xr, oracle.labels(Tr), cfg.V, cfg.D))
+    ad.adapt_train_many(hs, s)
+    for h, ref in zip(hs, refs):
+        assert_tree_equal(ad.adapt_get_tree(h), ref)
+
+
+def test_c3_full():
+    cfg = synth.CONFIGS["C3"]
+    X, T = synth.generate(cfg, 0, cfg.N)
+    got = full_parity(X, T, cfg.D, select_X=X[:200000])
+    assert got["depth"].max() == cfg.D
+
+
+def test_c4_slice_depth12():
+    # C4's 16 features x 48 classes (feature groups, class chunks) on 2e5 rows
+    cfg = synth.CONFIGS["C4"]
+    X, T = synth.generate(cfg, 777, 200000)
+    full_parity(X, T, cfg.D)
+
+
+def test_host_table_path():
+    cfg = synth.CONFIGS["C3"]
+    X, T = synth.generate(cfg, 5, 30000)
+    full_parity(X, T, 6, on_device=False)
+
+
+# ------------------------------------------------------------ edge cases --
+@pytest.mark.parametrize("seed", range(8))
+def test_random_small_tables(seed):
+    rng = np.random.default_rng(seed)
+    for _ in range(6):
+        n = int(rng.integers(1, 3000))
+        F = int(rng.choice([1, 2, 3, 5, 8, 13, 16, 24]))
+        V = int(rng.integers(1, 12))
+        D = int(rng.integers(0, 9))
+        G = int(rng.integers(1, 40))
+        grid = np.unique(rng.normal(size=G).astype(np.float32) * 10)
+        X = rng.choice(grid, size=(n, F)).astype(np.float32)
+        T = rng.integers(1, 6, size=(n, V)).astype(np.float32)  # many label ties
+        if rng.random() < 0.3:
+            T[rng.random(size=T.shape) < 0.3] = np.inf
+            T[np.all(np.isinf(T), axis=1), 0] = 1.0
+        full_parity(X, T, D)
+
+
+def test_degenerate_cases():
+    # single row; all rows identical; one class; -0 vs +0; XOR (zero-gain splits)
+    full_parity(np.array([[1.5, 2.0]], np.float32), np.array([[3.0, 1.0]], np.float32), 4)
+    X = np.ones((100, 3), np.float32)
+    T = np.random.default_rng(0).random((100, 4)).astype(np.float32)
+    full_parity(X, T, 5)
+    X = np.random.default_rng(1).integers(0, 9, (500, 2)).astype(np.float32)
+    full_parity(X, np.tile(np.array([[1, 2, 3]], np.float32), (500, 1)), 3)
+    X = np.array([[-0.0], [0.0], [1.0], [2.0]] * 10, np.float32)
+    full_parity(X, np.array([[1, 2], [2, 1], [1, 2], [2, 1]] * 10, np.float32), 3)
+    X = np.array([[0, 0], [0, 1], [1, 0], [1, 1]] * 7, np.float32)
+    T = np.array([[1, 2], [2, 1], [2, 1], [1, 2]] * 7, np.float32)
+    got = full_parity(X, T, 8)
+    assert len(got) == 7
+
+
+def test_max_distinct_and_classes():
+    rng = np.random.default_rng(3)
+    n = 60000
+    X = np.stack([rng.permutation(np.arange(n) % 256), rng.integers(0, 256, n)], 1).astype(np.float32)
+    T = rng.random((n, 200)).astype(np.float32)
+    full_parity(X, T, 3)
+
+
+def test_errors():
+    s = torch.cuda.current_stream()
+    h = _region(1, 2, 2)
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_train(h, s)
+    assert e.value.code == ad.ADAPT_E_INSUFFICIENT_DATA
+    X = torch.tensor([[1.0], [float("nan")]], device=DEV)
+    T = torch.ones((2, 2), device=DEV)
+    ad.adapt_record_table(h, X, T, 2, True, s)
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_train(h, s)
+    assert e.value.code == ad.ADAPT_E_BAD_VALUE
+    X = torch.tensor([[1.0], [2.0]], device=DEV)
+    T = torch.tensor([[1.0, float("nan")], [1.0, 2.0]], device=DEV)
+    ad.adapt_record_table(h, X, T, 2, True, s)
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_train(h, s)
+    assert e.value.code == ad.ADAPT_E_BAD_VALUE
+    T = torch.tensor([[float("inf"), float("inf")], [1.0, 2.0]], device=DEV)
+    ad.adapt_record_table(h, X, T, 2, True, s)
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_train(h, s)
+    assert e.value.code == ad.ADAPT_E_BAD_VALUE
+    X = torch.arange(300, dtype=torch.float32, device=DEV).reshape(-1, 1)
+    T = torch.ones((300, 2), device=DEV)
+    ad.adapt_record_table(h, X, T, 300, True, s)
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_train(h, s)
+    assert e.value.code == ad.ADAPT_E_TOO_MANY_DISTINCT
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_select(h, np.zeros(1, np.float32))
+    assert e.value.code == ad.ADAPT_E_NOT_TRAINED
+
+
+def test_record_path_and_shim():
+    # long-format records -> aggregated wide rows -> tree; and the
+    # Table-1 shim: round-robin exploration then auto-train at end
+    rng = np.random.default_rng(7)
+    R = 4000
+    feat = rng.choice(np.arange(1, 40, dtype=np.float32), size=(R, 2))
+    var = rng.integers(0, 3, R).astype(np.int32)
+    ns = (feat[:, 0] * (var + 1) * 100 + rng.integers(0, 50, R)).astype(np.uint64)
+    h = _region(2, 3, 4)
+    for i in range(R):
+        ad.adapt_record(h, feat[i], int(var[i]), int(ns[i]))
+    assert ad.adapt_distinct_pairs(h) == oracle.distinct_pairs(feat, var)
+    ad.adapt_train(h)
+    wf, wt = oracle.aggregate(feat, var, ns, 3)
+    assert_tree_equal(ad.adapt_get_tree(h), oracle.train(wf, oracle.labels(wt), 3, 4))
+
+    r = ad.__adapt_region_create("shim_vecadd", 1, 2, "DecisionTree,explore=RoundRobin", 4)
+    assert r
+    pol = []
+    for N in [10.0, 20.0, 30.0, 40.0]:
+        ad.__adapt_region_begin(r)
+        ad.__adapt_region_set_feature(r, N)
+        pol.append(ad.__adapt_region_get_policy(r))
+        ad.__adapt_region_end(r)
+    assert pol == [0, 1, 0, 1]  # round robin before training
+    info = ad.adapt_region_info(r)
+    assert info["trained"]  # 4 distinct (feature, variant) pairs = min_train_data
