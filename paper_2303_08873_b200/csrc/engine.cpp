@@ -667,7 +667,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       for (int k = 0; k < C; k++) P[k] = Pd[k];
       fill_stats(h->tree[fn.tree_idx], P.data(), C);
       h->tree[fn.tree_idx].depth = fn.depth;
-      if (is_pure(P.data(), C) || !nr->valid) continue;  // leaf (R10)
+      if (fn.depth >= D || is_pure(P.data(), C) || !nr->valid) continue;  // leaf (R10, R11)
       const int f = nr->feat;
       adapt_node_t &nd = h->tree[fn.tree_idx];
       nd.feature = f;
@@ -736,9 +736,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
     seg_children.swap(nchildren);
     direct_slots.swap(ndirect);
     std::swap(Hcur, Hprev);
-    // the spans just written become the input of the next pass
-    idx_prev = idx_next;
-    idx_next = (idx_next == h->idxA.as<uint32_t>()) ? h->idxB.as<uint32_t>() : h->idxA.as<uint32_t>();
+    // the spans just written become the input of the next pass; the root pass
+    // partitions nothing, so level 1 still reads rows by identity
+    if (level > 0) {
+      idx_prev = idx_next;
+      idx_next = (idx_next == h->idxA.as<uint32_t>()) ? h->idxB.as<uint32_t>() : h->idxA.as<uint32_t>();
+    }
   }
   // depth of every node (children got theirs when appended)
   h->trained_n = n;
