@@ -31,19 +31,20 @@ void cuda_check(cudaError_t e, const char *what);
 #define CUDA_CHECK(x) ::adapt::cuda_check((x), #x)
 
 // ---- one segment of a level pass (host-built, read by hist_pass_kernel) ----
-// A segment is the span [off, off+len) of one parent node in the row-index
-// arrays.  The pass partitions it (feat >= 0) into the children's spans —
-// left rows from the front, right rows from the back — and accumulates the
-// class histogram of the "direct" child (or of all rows for the root pass).
+// A segment is the span [off, off+len) of one parent node in the level's row
+// planes.  The pass moves its rows (feat >= 0) into the children's spans of the
+// output planes — left rows from the front, right rows from the back — and
+// accumulates the class histogram of the "direct" child (or of all rows for
+// the root pass).
 struct Seg {
-  uint32_t off;       // span start (position in idx arrays; row id if idx_prev == null)
+  uint32_t off;       // span start (row position in the level's planes)
   uint32_t len;       // rows of this rank in the span
   uint32_t row_base;  // prefix sum of len over previous segments (block work split)
   int32_t feat;       // split feature, -1 = no partition (root pass)
   int32_t thr;        // rank b_lo: rank <= thr goes left
   int32_t direct;     // 0: histogram rows going left, 1: right, 2: all rows, -1: none
   int32_t hslot;      // histogram slot of the direct child (-1: none)
-  int32_t write;      // bit0: write left rows to idx_next, bit1: right rows
+  int32_t write;      // bit0: move left rows to the output planes, bit1: right rows
 };
 
 // best cut of one (node, feature), exact key num/den (R13x)
@@ -65,9 +66,9 @@ struct NodeRes {
 };
 
 // ---- kernel launchers (ingest.cu) ----
-void launch_ingest(const float *feat, const float *times, int64_t n, int F, int V, int RS,
+void launch_ingest(const float *feat, const float *times, int64_t n, int F, int V, int BS,
                    uint32_t *gkey, uint32_t *gid, uint32_t *gcount, uint32_t *flags,
-                   uint8_t *rec, cudaStream_t s);
+                   uint8_t *bins, uint8_t *labels, cudaStream_t s);
 void launch_collect_values(const uint32_t *gkey, const uint32_t *gid, const uint32_t *gcount,
                            int F, float *local_vals, int32_t *local_cnt, cudaStream_t s);
 void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int world, int rank,
@@ -75,27 +76,29 @@ void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int worl
                          cudaStream_t s);
 void launch_bins_out(const uint8_t *rec, int64_t n, int F, int RS, const uint8_t *lut,
                      uint8_t *out, cudaStream_t s);
-void launch_labels_out(const uint8_t *rec, int64_t n, int F, int RS, uint8_t *out,
-                       cudaStream_t s);
 
 // ---- kernel launchers (train.cu) ----
 struct HistPassArgs {
   const Seg *segs;
   int nseg;
   uint32_t total_rows;
-  const uint32_t *idx_prev;  // null: identity (root pass)
-  uint32_t *idx_next;
+  const uint8_t *bins_in;    // rows of this level, grouped by node span: [pos][BS]
+  const uint8_t *lab_in;     // [pos]
+  uint8_t *bins_out;         // partitioned rows for the next level (null: root pass)
+  uint8_t *lab_out;
   uint32_t *cursors;         // 2 per segment (left count, right count), zeroed
-  const uint8_t *rec;
-  int RS, F, C;
+  int BS, F, C;
   const uint8_t *lut;        // [F][256] prov -> rank
   const int32_t *hoff;       // [F] counter offset of feature f in a node histogram
-  const int4 *groups;        // [ngroups] smem groups: features [x, y), classes [z, w)
+  const int32_t *nval;       // [F] distinct values of f
+  const int4 *groups;        // [ngroups] x: first class, y: classes, z: padded stride, w: bins word
+  const int32_t *gsoff;      // [ngroups][F] smem offset of feature f in group g, -1 if absent
   int ngroups;
+  int clustered;             // launched as clusters of ngroups CTAs
   int smem_counters;         // max counters of a group
   uint32_t *H;               // [slots][HS]
   int64_t HS;
-  int blocks_per_group;
+  int nranges;               // row ranges; CTA x handles range x / ngroups, group x % ngroups
 };
 void launch_hist_pass(const HistPassArgs &a, cudaStream_t s);
 void launch_zero_slots(uint32_t *H, int64_t HS, const int32_t *slots, int n, cudaStream_t s);
@@ -113,7 +116,7 @@ struct DNode {     // device inference node, 8 bytes
   float thr;       // largest float32 <= threshold (x <= thr_f64  <=>  x <= thr_f32, V:A5)
   int32_t meta;    // >= 0: (left << 6) | feature ; < 0: -1 - label
 };
-void launch_select(const DNode *tree, const float *X, int64_t m, int F, int32_t *out,
-                   cudaStream_t s);
+void launch_select(const DNode *tree, int n_nodes, const float *X, int64_t m, int F,
+                   int32_t *out, cudaStream_t s);
 
 }  // namespace adapt

@@ -208,7 +208,7 @@ void ensure_init() {
 }
 
 // ------------------------------------------------------------ regions --
-constexpr int kHistSmemBudget = 96 * 1024;  // counters + LUT per hist block (2 blocks/SM)
+constexpr int kHistSmemBudget = 200 * 1024;  // counters + LUT per level-pass CTA (1 CTA/SM)
 
 struct FNode {  // a frontier node: histogrammed and split-searched at this level
   int32_t tree_idx;
@@ -233,9 +233,10 @@ struct adapt_region {
   const float *d_feat = nullptr, *d_times = nullptr;
   adapt::DevBuf own_feat, own_times;
   // products of the last train
-  int RS = 0;
+  int BS = 0;                   // bins row stride (F rounded up to a power of two)
   int64_t trained_n = 0;
-  adapt::DevBuf rec;
+  adapt::DevBuf bins, labels;   // ingest output in row order (kept for introspection)
+  adapt::DevBuf binsA, binsB, labA, labB;  // level planes, rows grouped by node span
   std::vector<float> val;       // [F][256]
   std::vector<int32_t> nval;    // [F]
   std::vector<uint8_t> lut;     // [F][256]
@@ -245,8 +246,8 @@ struct adapt_region {
   bool trained = false;
   std::vector<int64_t> stats;
   // scratch
-  adapt::DevBuf gkey, gid, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, idxA, idxB, H0,
-      H1, segs, cursors, slots, triples, nslot, cand, res, hoff, grp, xa, xb, oa, ob;
+  adapt::DevBuf gkey, gid, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, H0, H1, segs,
+      cursors, slots, triples, nslot, cand, res, hoff, grp, gsoff, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall;
   // Table-1 shim state
   bool active = false;
@@ -423,24 +424,26 @@ void train_region(adapt_region *h, cudaStream_t s) {
   }
   if (n_total == 0) throw Error(ADAPT_E_INSUFFICIENT_DATA, "no training rows");
   if (n_total >= (1ull << 32)) throw Error(ADAPT_E_INVALID_ARG, "more than 2^32-1 rows");
-  int RS = 2;
-  while (RS < F + 1) RS <<= 1;
-  h->RS = RS;
+  int BS = 1;
+  while (BS < F) BS <<= 1;
+  h->BS = BS;
 
   // 1. a1 + a2 + a3: one pass over the table
   h->gkey.ensure((size_t)F * kGSlots * 4);
   h->gid.ensure((size_t)F * kGSlots * 4);
   h->gcount.ensure((size_t)F * 4);
   h->flags.ensure(16);
-  h->rec.ensure((size_t)std::max<int64_t>(n, 1) * RS);
+  h->bins.ensure((size_t)std::max<int64_t>(n, 1) * BS);
+  h->labels.ensure((size_t)std::max<int64_t>(n, 1));
   CUDA_CHECK(cudaMemsetAsync(h->gkey.p, 0xFF, (size_t)F * kGSlots * 4, s));
   CUDA_CHECK(cudaMemsetAsync(h->gid.p, 0xFF, (size_t)F * kGSlots * 4, s));
   CUDA_CHECK(cudaMemsetAsync(h->gcount.p, 0, (size_t)F * 4, s));
   CUDA_CHECK(cudaMemsetAsync(h->flags.p, 0, 16, s));
   {
-    Phase ph("ingest", s, (double)n * (4.0 * F + 4.0 * V + F + 1));
-    launch_ingest(feat, times, n, F, V, RS, h->gkey.as<uint32_t>(), h->gid.as<uint32_t>(),
-                  h->gcount.as<uint32_t>(), h->flags.as<uint32_t>(), h->rec.as<uint8_t>(), s);
+    Phase ph("ingest", s, (double)n * (4.0 * F + 4.0 * V + F + 1));  // algorithmic
+    launch_ingest(feat, times, n, F, V, BS, h->gkey.as<uint32_t>(), h->gid.as<uint32_t>(),
+                  h->gcount.as<uint32_t>(), h->flags.as<uint32_t>(), h->bins.as<uint8_t>(),
+                  h->labels.as<uint8_t>(), s);
   }
   // a2: value tables, merged over ranks
   h->lvals.ensure((size_t)F * kMaxBins * 4);
@@ -509,40 +512,46 @@ void train_region(adapt_region *h, cudaStream_t s) {
     hoff[f] = (int32_t)HS;
     HS += (int64_t)h->nval[f] * C;
   }
-  // shared-memory groups of the histogram pass: runs of whole features, or
-  // class slabs of one feature whose D_f x C counters alone exceed the budget
+  // shared-memory groups of the level pass: group = one 32-bit word of the
+  // bins row (4 features) x a class slab [k0, k0+kw); feature f takes
+  // D_f x kwp counters, kwp = kw padded to an odd stride.  A word whose 4
+  // features x all classes exceed one CTA's budget is split into class slabs.
   const int cap = (kHistSmemBudget - F * kMaxBins) / 4;
-  std::vector<int4> groups;
-  int max_group = 0;
-  {
-    int gf0 = 0;
-    int64_t used = 0;
-    auto close = [&](int fend) {
-      if (fend > gf0) {
-        groups.push_back(make_int4(gf0, fend, 0, C));
-        max_group = std::max<int>(max_group, (int)used);
-      }
-      gf0 = fend;
-      used = 0;
-    };
-    for (int f = 0; f < F; f++) {
-      const int64_t need = (int64_t)h->nval[f] * C;
-      if (need > cap) {
-        close(f);
-        const int kw = cap / std::max(1, h->nval[f]);
-        for (int k0 = 0; k0 < C; k0 += kw) groups.push_back(make_int4(f, f + 1, k0, std::min(C, k0 + kw)));
-        max_group = std::max<int>(max_group, h->nval[f] * kw);
-        gf0 = f + 1;
-        continue;
-      }
-      if (used + need > cap) close(f);
-      used += need;
+  struct G {
+    int k0, kw, kwp, word, counters;
+    std::vector<int32_t> off;
+  };
+  std::vector<G> gl;
+  for (int w = 0; 4 * w < F; w++) {
+    int dsum = 0;
+    for (int f = 4 * w; f < std::min(F, 4 * w + 4); f++) dsum += h->nval[f];
+    int kwp = C | 1;
+    if ((int64_t)dsum * kwp > cap) {
+      kwp = cap / dsum;
+      if (!(kwp & 1)) kwp--;
     }
-    close(F);
+    for (int k0 = 0; k0 < C; k0 += kwp) {
+      G t{k0, std::min(kwp, C - k0), 0, w, 0, std::vector<int32_t>(F, -1)};
+      t.kwp = t.kw | 1;
+      for (int f = 4 * w; f < std::min(F, 4 * w + 4); f++) {
+        t.off[f] = t.counters;
+        t.counters += h->nval[f] * t.kwp;
+      }
+      gl.push_back(t);
+    }
   }
-  const int ngroups = (int)groups.size();
+  const int ngroups = (int)gl.size();
+  int max_group = 0;
+  std::vector<int4> groups;
+  std::vector<int32_t> gsoff;
+  for (auto &t : gl) {
+    groups.push_back(make_int4(t.k0, t.kw, t.kwp, t.word));
+    gsoff.insert(gsoff.end(), t.off.begin(), t.off.end());
+    max_group = std::max(max_group, t.counters);
+  }
   h2d(h->hoff, hoff, s);
   h2d(h->grp, groups, s);
+  h2d(h->gsoff, gsoff, s);
 
   // 2. level loop (a4-a8)
   h->tree.clear();
@@ -557,9 +566,16 @@ void train_region(adapt_region *h, cudaStream_t s) {
   std::vector<int32_t> triples;
   std::vector<int> seg_children;  // per seg: frontier index of left (or -1), right (or -1)
   seg_children = {-1, -1};
-  h->idxA.ensure((size_t)std::max<int64_t>(n, 1) * 4);
-  h->idxB.ensure((size_t)std::max<int64_t>(n, 1) * 4);
-  uint32_t *idx_prev = nullptr, *idx_next = h->idxA.as<uint32_t>();
+  // level planes: the root pass reads the ingest output; pass d >= 1 moves the
+  // rows of the split parents from one plane pair into the other
+  const uint8_t *bins_in = h->bins.as<uint8_t>(), *lab_in = h->labels.as<uint8_t>();
+  h->binsA.ensure((size_t)std::max<int64_t>(n, 1) * BS);
+  h->binsB.ensure((size_t)std::max<int64_t>(n, 1) * BS);
+  h->labA.ensure((size_t)std::max<int64_t>(n, 1));
+  h->labB.ensure((size_t)std::max<int64_t>(n, 1));
+  int out_plane = 0;  // 0: A, 1: B
+  int sms = 148;
+  CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g_ctx.device));
   DevBuf *Hcur = &h->H0, *Hprev = &h->H1;
   const int res_stride = (int)((sizeof(NodeRes) + 8 * (size_t)C + 7) / 8 * 8);
   std::vector<uint64_t> P_of_tree;  // class totals per tree node (tree order), C each
@@ -586,22 +602,27 @@ void train_region(adapt_region *h, cudaStream_t s) {
     a.segs = h->segs.as<Seg>();
     a.nseg = nseg;
     a.total_rows = total;
-    a.idx_prev = idx_prev;
-    a.idx_next = idx_next;
+    a.bins_in = bins_in;
+    a.lab_in = lab_in;
+    a.bins_out = level == 0 ? nullptr : (out_plane ? h->binsB : h->binsA).as<uint8_t>();
+    a.lab_out = level == 0 ? nullptr : (out_plane ? h->labB : h->labA).as<uint8_t>();
     a.cursors = h->cursors.as<uint32_t>();
-    a.rec = h->rec.as<uint8_t>();
-    a.RS = RS;
+    a.BS = BS;
     a.F = F;
     a.C = C;
     a.lut = h->d_lut.as<uint8_t>();
     a.hoff = h->hoff.as<int32_t>();
+    a.nval = h->dnval.as<int32_t>();
     a.groups = h->grp.as<int4>();
+    a.gsoff = h->gsoff.as<int32_t>();
+    a.clustered = ngroups > 1 && ngroups <= 8;
     a.ngroups = ngroups;
     a.smem_counters = max_group;
     a.H = Hcur->as<uint32_t>();
     a.HS = HS;
-    a.blocks_per_group = (int)std::max<int64_t>(
-        1, std::min<int64_t>((total + 4095) / 4096, (2 * 148 + ngroups - 1) / ngroups * 2));
+    // one wave: every cluster of ngroups CTAs (one CTA per SM) takes an equal row range
+    a.nranges = (int)std::max<int64_t>(
+        1, std::min<int64_t>((total + 2047) / 2048, std::max(1, sms / std::min(ngroups, 8))));
     {
       Phase ph("hist", s, (double)total * (F + 1));
       launch_hist_pass(a, s);
@@ -736,11 +757,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
     seg_children.swap(nchildren);
     direct_slots.swap(ndirect);
     std::swap(Hcur, Hprev);
-    // the spans just written become the input of the next pass; the root pass
-    // partitions nothing, so level 1 still reads rows by identity
+    // the planes just written are the input of the next pass; the root pass
+    // moves nothing, so level 1 still reads the ingest output
     if (level > 0) {
-      idx_prev = idx_next;
-      idx_next = (idx_next == h->idxA.as<uint32_t>()) ? h->idxB.as<uint32_t>() : h->idxA.as<uint32_t>();
+      bins_in = (out_plane ? h->binsB : h->binsA).as<uint8_t>();
+      lab_in = (out_plane ? h->labB : h->labA).as<uint8_t>();
+      out_plane ^= 1;
     }
   }
   // depth of every node (children got theirs when appended)
@@ -994,7 +1016,7 @@ int adapt_select_batch(adapt_region_t *h, const float *d_X, int64_t m, int32_t *
     if (!h->trained) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
     cudaStream_t s = (cudaStream_t)stream;
     Phase ph("select", s, (double)m * (4.0 * h->F + 4));
-    launch_select(h->d_tree.as<DNode>(), d_X, m, h->F, d_out, s);
+    launch_select(h->d_tree.as<DNode>(), (int)h->tree.size(), d_X, m, h->F, d_out, s);
   });
 }
 
@@ -1028,7 +1050,7 @@ int adapt_select_batch_host(adapt_region_t *h, const float *X, int64_t m, int32_
       CUDA_CHECK(cudaMemcpyAsync(dx, X + c * F, (size_t)k * F * 4, cudaMemcpyHostToDevice, q));
       {
         Phase ph("select", q, (double)k * (4.0 * F + 4));
-        launch_select(h->d_tree.as<DNode>(), dx, k, F, dout, q);
+        launch_select(h->d_tree.as<DNode>(), (int)h->tree.size(), dx, k, F, dout, q);
       }
       CUDA_CHECK(cudaMemcpyAsync(out + c, dout, (size_t)k * 4, cudaMemcpyDeviceToHost, q));
     }
@@ -1076,12 +1098,9 @@ int adapt_set_tree(adapt_region_t *h, const adapt_node_t *nodes, int32_t n_nodes
 int adapt_get_labels(adapt_region_t *h, uint8_t *out, int64_t n) {
   return guarded([&] {
     checked(h);
-    if (!h->trained || !h->RS) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    if (!h->trained || !h->BS) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
     if (!out || n != h->trained_n) throw Error(ADAPT_E_INVALID_ARG, "n must equal the trained row count");
-    DevBuf tmp;
-    tmp.ensure((size_t)n + 16);
-    launch_labels_out(h->rec.as<uint8_t>(), n, h->F, h->RS, tmp.as<uint8_t>(), 0);
-    CUDA_CHECK(cudaMemcpy(out, tmp.p, (size_t)n, cudaMemcpyDeviceToHost));
+    if (n) CUDA_CHECK(cudaMemcpy(out, h->labels.p, (size_t)n, cudaMemcpyDeviceToHost));
   });
 }
 
@@ -1098,11 +1117,11 @@ int adapt_get_value_table(adapt_region_t *h, int f, float *vals, int *count) {
 int adapt_get_bins(adapt_region_t *h, uint8_t *out, int64_t n) {
   return guarded([&] {
     checked(h);
-    if (!h->trained || !h->RS) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    if (!h->trained || !h->BS) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
     if (!out || n != h->trained_n) throw Error(ADAPT_E_INVALID_ARG, "n must equal the trained row count");
     DevBuf tmp;
     tmp.ensure((size_t)n * h->F + 16);
-    launch_bins_out(h->rec.as<uint8_t>(), n, h->F, h->RS, h->d_lut.as<uint8_t>(), tmp.as<uint8_t>(), 0);
+    launch_bins_out(h->bins.as<uint8_t>(), n, h->F, h->BS, h->d_lut.as<uint8_t>(), tmp.as<uint8_t>(), 0);
     CUDA_CHECK(cudaMemcpy(out, tmp.p, (size_t)n * h->F, cudaMemcpyDeviceToHost));
   });
 }

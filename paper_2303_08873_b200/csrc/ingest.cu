@@ -11,16 +11,19 @@
 //     ranks (R7, R14).
 // a3  the bin of x[i][f] is its provisional id; the rank LUT turns it into
 //     the rank in the sorted table wherever a rank is needed.  So features are
-//     read exactly once: 4F + 4V bytes in, RS bytes (bins + label) out per row.
+//     read exactly once: 4F + 4V bytes in, BS + 1 bytes out per row.
 //
-// Output record of row i (RS = F+1 rounded up to a power of two bytes):
-//     rec[i*RS + f] = provisional bin of feature f, rec[i*RS + F] = label.
+// Output planes (BS = F rounded up to a power of two bytes):
+//     bins[i*BS + f] = provisional bin of feature f, labels[i] = label.
+#include <algorithm>
+
 #include "common.h"
+#include "ptx.h"
 
 namespace adapt {
 namespace {
 
-constexpr int kIngestThreads = 256;  // threads per block; a tile holds TR <= 256 rows
+constexpr int kIngestThreads = 1024;
 
 __device__ __forceinline__ uint32_t hash_slot(uint32_t key, int log2slots) {
   return (key * 2654435761u) >> (32 - log2slots);
@@ -61,144 +64,227 @@ __device__ uint32_t global_lookup(uint32_t *gkey, uint32_t *gid, uint32_t *gcoun
   return kMaxBins - 1;
 }
 
-template <int RS>
-__global__ void __launch_bounds__(kIngestThreads)
-    ingest_kernel(const float *__restrict__ feat, const float *__restrict__ times, int64_t n,
-                  int F, int V, int TR, int log2sl, uint32_t *gkey, uint32_t *gid, uint32_t *gcount,
-                  uint32_t *flags, uint8_t *__restrict__ rec) {
-  extern __shared__ uint4 smem_u4[];
-  const int SL = 1 << log2sl;
-  uint32_t *skey = reinterpret_cast<uint32_t *>(smem_u4);
-  uint16_t *sid = reinterpret_cast<uint16_t *>(skey + F * SL);
-  float *tile_t = reinterpret_cast<float *>(
-      reinterpret_cast<uint4 *>(smem_u4) + ((F * SL * 6 + 15) / 16));
-  float *tile_f = tile_t + TR * V;
-  uint8_t *srec = reinterpret_cast<uint8_t *>(tile_f + TR * F);
+// One CTA per SM, persistent over row tiles of TR rows.  Thread 0 keeps
+// kStages tiles of (times, features) in flight with 1-D TMA bulk copies that
+// complete on "full" mbarriers.  Every warp owns TR/32 rows of a tile (P = 4
+// lanes per row for TR = 256): it labels them, bins them, writes its rows'
+// bins and labels straight to global memory (coalesced) and arrives on the
+// stage's "empty" mbarrier — no block-wide barrier in the loop.
+//
+// The per-block value cache is bucketised: a feature value hashes to a bucket
+// of 4 slots whose 4 keys (16 B) and 4 provisional ids (8 B) are fetched with
+// one 128-bit and one 64-bit shared load, so a hit costs one round trip.
+constexpr int kStages = 2;
+constexpr int kWarps = kIngestThreads / 32;
+constexpr uint16_t kNoId = 0xFFFF;
 
-  const int tid = threadIdx.x;
-  for (int i = tid; i < F * SL; i += blockDim.x) {
-    skey[i] = kEmptyKey;
-    sid[i] = 0xFFFF;
+struct IngestArgs {
+  const float *feat, *times;
+  int64_t n;
+  int F, V, BS, TR, P, log2nb, use_tma;
+  uint32_t *gkey, *gid, *gcount, *flags;
+  uint8_t *bins, *labels;
+};
+
+__device__ __forceinline__ int bucket_find(const uint4 K, const uint2 I, uint32_t key) {
+  // id of `key` in the bucket, -1 if absent or not yet published
+  int id = -1;
+  if (K.x == key) id = I.x & 0xFFFF;
+  if (K.y == key) id = I.x >> 16;
+  if (K.z == key) id = I.y & 0xFFFF;
+  if (K.w == key) id = I.y >> 16;
+  return id == kNoId ? -1 : id;
+}
+
+__device__ __noinline__ int cache_miss(uint32_t *keys, uint16_t *ids, int log2nb, uint32_t key,
+                                       const IngestArgs &a, int f) {
+  const int NB = 1 << log2nb;
+  const uint32_t b0 = hash_slot(key, log2nb);
+  for (int p = 1; p < NB; p++) {  // later buckets of the probe sequence
+    const uint32_t b = (b0 + p) & (NB - 1);
+    const int id = bucket_find(reinterpret_cast<const uint4 *>(keys)[b],
+                               reinterpret_cast<const uint2 *>(ids)[b], key);
+    if (id >= 0) return id;
+    if (keys[4 * b + 3] == kEmptyKey) break;  // a bucket with room ends the sequence
   }
-  uint32_t local_flags = 0;
-  const bool aligned_t = (reinterpret_cast<uintptr_t>(times) & 15) == 0;
-  const bool aligned_f = (reinterpret_cast<uintptr_t>(feat) & 15) == 0;
+  const uint32_t id = global_lookup(a.gkey, a.gid, a.gcount, a.flags, f, key);
+  for (int p = 0; p < NB; p++) {  // publish (best effort: a full cache just misses)
+    const uint32_t b = (b0 + p) & (NB - 1);
+    for (int e = 0; e < 4; e++) {
+      const uint32_t old = atomicCAS(keys + 4 * b + e, kEmptyKey, key);
+      if (old == kEmptyKey) {
+        ids[4 * b + e] = (uint16_t)id;
+        return (int)id;
+      }
+      if (old == key) return (int)id;
+    }
+  }
+  return (int)id;
+}
+
+__device__ __forceinline__ uint32_t canon_key(float x, uint32_t &flags) {
+  uint32_t key = __float_as_uint(x);
+  if ((key & 0x7f800000u) == 0x7f800000u) {
+    flags |= kFlagBadFeature;
+    key = 0;
+  }
+  return x == 0.0f ? 0u : key;  // -0 -> +0 (R4)
+}
+
+__device__ __forceinline__ int lookup(uint32_t *keys, uint16_t *ids, int log2nb, uint32_t key,
+                                      const IngestArgs &a, int f) {
+  const uint32_t b = hash_slot(key, log2nb);
+  const int id = bucket_find(reinterpret_cast<const uint4 *>(keys)[b],
+                             reinterpret_cast<const uint2 *>(ids)[b], key);
+  return id >= 0 ? id : cache_miss(keys, ids, log2nb, key, a, f);
+}
+
+__global__ void __launch_bounds__(kIngestThreads, 1) ingest_kernel(IngestArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int F = a.F, V = a.V, BS = a.BS, TR = a.TR, P = a.P;
+  const int NB = 1 << a.log2nb;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+  uint64_t *empty = full + kStages;
+  uint32_t *ckeys = reinterpret_cast<uint32_t *>(smem + 128);   // [F][NB][4]
+  uint16_t *cids = reinterpret_cast<uint16_t *>(ckeys + F * NB * 4);  // [F][NB][4]
+  const size_t o1 = 128 + (size_t)F * NB * 24;
+  float *stT = reinterpret_cast<float *>(smem + o1);
+  float *stF = stT + (size_t)kStages * TR * V;
+
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < F * NB * 4; i += blockDim.x) {
+    ckeys[i] = kEmptyKey;
+    cids[i] = kNoId;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    fence_mbar_init();
+  }
   __syncthreads();
 
-  const int64_t ntiles = (n + TR - 1) / TR;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t row0 = tile * TR;
-    const int rows = (n - row0 < TR) ? (int)(n - row0) : TR;
-    // ---- stage the tile: coalesced 16-byte streaming loads ----
-    {
-      const float *src = times + row0 * V;
-      const int cnt = rows * V;
-      int done = 0;
-      if (aligned_t) {
-        const float4 *s4 = reinterpret_cast<const float4 *>(src);
-        float4 *d4 = reinterpret_cast<float4 *>(tile_t);
-        const int n4 = cnt >> 2;
-        for (int i = tid; i < n4; i += kIngestThreads) d4[i] = __ldcs(s4 + i);
-        done = n4 << 2;
-      }
-      for (int i = done + tid; i < cnt; i += kIngestThreads) tile_t[i] = __ldcs(src + i);
-    }
-    {
-      const float *src = feat + row0 * F;
-      const int cnt = rows * F;
-      int done = 0;
-      if (aligned_f) {
-        const float4 *s4 = reinterpret_cast<const float4 *>(src);
-        float4 *d4 = reinterpret_cast<float4 *>(tile_f);
-        const int n4 = cnt >> 2;
-        for (int i = tid; i < n4; i += kIngestThreads) d4[i] = __ldcs(s4 + i);
-        done = n4 << 2;
-      }
-      for (int i = done + tid; i < cnt; i += kIngestThreads) tile_f[i] = __ldcs(src + i);
-    }
-    __syncthreads();
+  const int64_t ntiles = (a.n + TR - 1) / TR;
+  const int64_t nfull = a.n / TR;  // tiles that TMA can load whole
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t K = first < ntiles ? (ntiles - 1 - first) / stride + 1 : 0;
+  const uint32_t bytesT = (uint32_t)TR * V * 4, bytesF = (uint32_t)TR * F * 4;
+  auto issue = [&](int64_t k) {  // thread 0 only
+    const int64_t t = first + k * stride;
+    if (!a.use_tma || t >= nfull) return;
+    const int s = (int)(k % kStages);
+    if (k >= kStages) mbar_wait(&empty[s], (uint32_t)(((k / kStages) - 1) & 1));
+    mbar_arrive_expect_tx(&full[s], bytesT + bytesF);
+    tma_load_1d(stT + (size_t)s * TR * V, a.times + t * TR * V, bytesT, &full[s]);
+    tma_load_1d(stF + (size_t)s * TR * F, a.feat + t * TR * F, bytesF, &full[s]);
+  };
+  if (tid == 0)
+    for (int64_t k = 0; k < K && k < kStages; k++) issue(k);
 
-    if (tid < rows) {
-      // ---- a1: argmin with lowest-index ties; the row is read starting at a
-      // thread-dependent rotation so the 32 lanes hit (almost) distinct banks.
-      const float *tr = tile_t + tid * V;
-      float best = __int_as_float(0x7f800000);  // +inf
-      int bi = 0x7fffffff;
-      bool nan = false;
-      int j = tid % V;
-      for (int k = 0; k < V; k++) {
-        const float x = tr[j];
-        nan |= (x != x);
-        if (x < best || (x == best && j < bi)) {
-          best = x;
-          bi = j;
-        }
-        j = (j + 1 == V) ? 0 : j + 1;
-      }
-      if (nan) local_flags |= kFlagNanTime;
-      if (best == __int_as_float(0x7f800000)) local_flags |= kFlagAllInf;
-      uint8_t *my = srec + tid * RS;
-      my[F] = (uint8_t)bi;
-      for (int p = F + 1; p < RS; p++) my[p] = 0;
-      // ---- a2 + a3: provisional id of each feature value ----
-      const float *fr = tile_f + tid * F;
-      int f = tid % F;
-      for (int k = 0; k < F; k++) {
-        const float x = fr[f];
-        uint32_t key = __float_as_uint(x);
-        if ((key & 0x7f800000u) == 0x7f800000u) {
-          local_flags |= kFlagBadFeature;
-          key = 0;
-        }
-        if (x == 0.0f) key = 0;  // -0 -> +0 (R4)
-        uint32_t *sk = skey + f * SL;
-        uint16_t *si = sid + f * SL;
-        uint32_t h = hash_slot(key, log2sl);
-        int id = -1;
-        for (int p = 0; p < SL; p++) {
-          const uint32_t kk = sk[h];
-          if (kk == key) {
-            const uint16_t v = si[h];
-            if (v != 0xFFFF) id = v;
-            break;
-          }
-          if (kk == kEmptyKey) break;
-          h = (h + 1) & (SL - 1);
-        }
-        if (id < 0) {
-          id = (int)global_lookup(gkey, gid, gcount, flags, f, key);
-          // publish in the block cache (best effort; a full cache just misses)
-          uint32_t hh = hash_slot(key, log2sl);
-          for (int p = 0; p < SL; p++) {
-            const uint32_t old = atomicCAS(sk + hh, kEmptyKey, key);
-            if (old == kEmptyKey) {
-              si[hh] = (uint16_t)id;
-              break;
-            }
-            if (old == key) break;
-            hh = (hh + 1) & (SL - 1);
-          }
-        }
-        my[f] = (uint8_t)id;
-        f = (f + 1 == F) ? 0 : f + 1;
-      }
+  uint32_t local_flags = 0;
+  const int r = tid / P, q = tid % P;
+  const bool vec_t = (V & 3) == 0;
+  const int per = F / P;                        // features per lane when F % P == 0
+  const bool vec_f = (F % P) == 0 && (per & 3) == 0;
+  for (int64_t k = 0; k < K; k++) {
+    const int64_t t = first + k * stride;
+    const int64_t row0 = t * TR;
+    const int rows = (a.n - row0 < TR) ? (int)(a.n - row0) : TR;
+    const int s = (int)(k % kStages);
+    float *tT = stT + (size_t)s * TR * V;
+    float *tF = stF + (size_t)s * TR * F;
+    if (a.use_tma && t < nfull) {
+      mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
+    } else {  // partial last tile or unaligned inputs: plain loads, block-synchronous
+      __syncthreads();
+      for (int i = tid; i < rows * V; i += blockDim.x) tT[i] = __ldcs(a.times + row0 * V + i);
+      for (int i = tid; i < rows * F; i += blockDim.x) tF[i] = __ldcs(a.feat + row0 * F + i);
+      __syncthreads();
     }
-    __syncthreads();
-    // ---- write the tile's records: contiguous, 16-byte stores ----
-    {
-      uint8_t *dst = rec + row0 * RS;
-      const int bytes = rows * RS;
-      if (RS >= 16) {
-        const uint4 *s4 = reinterpret_cast<const uint4 *>(srec);
-        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-        for (int i = tid; i < (bytes >> 4); i += kIngestThreads) __stcs(d4 + i, s4[i]);
+    // ---- a1: label = lowest index of the minimum (P lanes per row) ----
+    float best = __int_as_float(0x7f800000);
+    int bi = 0x7fffffff;
+    bool nan = false;
+    const bool live = r < rows;
+    if (live) {
+      const float *tr = tT + (size_t)r * V;
+      if (vec_t) {
+        const float4 *t4 = reinterpret_cast<const float4 *>(tr);
+        for (int c = q; c < (V >> 2); c += P) {
+          const float4 x = t4[c];
+          nan |= (x.x != x.x) | (x.y != x.y) | (x.z != x.z) | (x.w != x.w);
+          // ascending index within this lane: strict '<' keeps the lowest
+          if (x.x < best) { best = x.x; bi = 4 * c; }
+          if (x.y < best) { best = x.y; bi = 4 * c + 1; }
+          if (x.z < best) { best = x.z; bi = 4 * c + 2; }
+          if (x.w < best) { best = x.w; bi = 4 * c + 3; }
+        }
       } else {
-        for (int i = tid; i < bytes; i += kIngestThreads) dst[i] = srec[i];
+        for (int v = q; v < V; v += P) {
+          const float x = tr[v];
+          nan |= x != x;
+          if (x < best) {
+            best = x;
+            bi = v;
+          }
+        }
       }
     }
-    __syncthreads();
+    for (int o = 1; o < P; o <<= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob < best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (live) {
+      if (nan) local_flags |= kFlagNanTime;
+      if (q == 0) {
+        if (best == __int_as_float(0x7f800000)) local_flags |= kFlagAllInf;
+        a.labels[row0 + r] = (uint8_t)(bi < V ? bi : 0);
+      }
+      // ---- a2 + a3: provisional ids of this lane's features ----
+      const float *fr = tF + (size_t)r * F;
+      uint8_t *dst = a.bins + (row0 + r) * BS;
+      if (vec_f) {
+        for (int c = 0; c < per; c += 4) {
+          const int f = q * per + c;
+          const float4 x = *reinterpret_cast<const float4 *>(fr + f);
+          const uint32_t key[4] = {canon_key(x.x, local_flags), canon_key(x.y, local_flags),
+                                   canon_key(x.z, local_flags), canon_key(x.w, local_flags)};
+          uint4 Kb[4];
+          uint2 Ib[4];
+#pragma unroll
+          for (int e = 0; e < 4; e++) {  // the 4 features' buckets, loaded together
+            const uint32_t b = hash_slot(key[e], a.log2nb);
+            Kb[e] = reinterpret_cast<const uint4 *>(ckeys + (size_t)(f + e) * NB * 4)[b];
+            Ib[e] = reinterpret_cast<const uint2 *>(cids + (size_t)(f + e) * NB * 4)[b];
+          }
+          uint32_t packed = 0;
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            int id = bucket_find(Kb[e], Ib[e], key[e]);
+            if (id < 0)
+              id = cache_miss(ckeys + (size_t)(f + e) * NB * 4, cids + (size_t)(f + e) * NB * 4,
+                              a.log2nb, key[e], a, f + e);
+            packed |= (uint32_t)(id & 0xFF) << (8 * e);
+          }
+          *reinterpret_cast<uint32_t *>(dst + f) = packed;
+        }
+      } else {
+        for (int f = q; f < F; f += P)
+          dst[f] = (uint8_t)lookup(ckeys + (size_t)f * NB * 4, cids + (size_t)f * NB * 4, a.log2nb,
+                                   canon_key(fr[f], local_flags), a, f);
+        for (int f = F + q; f < BS; f += P) dst[f] = 0;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+    if (tid == 0 && k + kStages < K) issue(k + kStages);
   }
-  if (local_flags) atomicOr(flags, local_flags);
+  if (local_flags) atomicOr(a.flags, local_flags);
 }
 
 __global__ void collect_values_kernel(const uint32_t *gkey, const uint32_t *gid,
@@ -265,19 +351,13 @@ __global__ void merge_values_kernel(const float *all_vals, const int32_t *all_cn
 }
 
 __global__ void bins_out_kernel(const uint8_t *rec, int64_t n, int F, int RS, const uint8_t *lut,
-                                uint8_t *out) {
+                                uint8_t *out) {  // rec = bins plane, RS = its row stride
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * F;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / F;
     const int f = (int)(i % F);
     out[i] = lut[f * kMaxBins + rec[r * RS + f]];
   }
-}
-
-__global__ void labels_out_kernel(const uint8_t *rec, int64_t n, int F, int RS, uint8_t *out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = rec[i * RS + F];
 }
 
 int grid_for(int64_t work, int per_block, int cap) {
@@ -288,32 +368,44 @@ int grid_for(int64_t work, int per_block, int cap) {
 
 }  // namespace
 
-void launch_ingest(const float *feat, const float *times, int64_t n, int F, int V, int RS,
+void launch_ingest(const float *feat, const float *times, int64_t n, int F, int V, int BS,
                    uint32_t *gkey, uint32_t *gid, uint32_t *gcount, uint32_t *flags,
-                   uint8_t *rec, cudaStream_t s) {
+                   uint8_t *bins, uint8_t *labels, cudaStream_t s) {
   if (n == 0) return;
-  // per-block value cache: 512 slots/feature (<= 50% load at 256 values) when it fits
-  int log2sl = 9;
-  while (log2sl > 5 && (size_t)F * (6u << log2sl) > 48 * 1024) log2sl--;
-  const size_t cache = (((size_t)F * (6u << log2sl)) + 15) / 16 * 16;
-  int TR = kIngestThreads;  // tile rows: keep the block under ~100 KB of smem
-  while (TR > 32 && cache + (size_t)TR * ((V + F) * 4 + RS) > 100 * 1024) TR >>= 1;
-  const size_t smem = cache + (size_t)TR * ((V + F) * 4 + RS);
-  const int grid = grid_for(n, TR, 148 * 8);
-  switch (RS) {
-#define CASE(R)                                                                              \
-  case R: {                                                                                  \
-    CUDA_CHECK(cudaFuncSetAttribute(ingest_kernel<R>,                                        \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    ingest_kernel<R><<<grid, kIngestThreads, smem, s>>>(feat, times, n, F, V, TR, log2sl,    \
-                                                        gkey, gid, gcount, flags, rec);      \
-    break;                                                                                   \
-  }
-    CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) CASE(128)
-#undef CASE
-    default:
-      throw Error(-1, "bad record stride");
-  }
+  IngestArgs a;
+  a.feat = feat;
+  a.times = times;
+  a.n = n;
+  a.F = F;
+  a.V = V;
+  a.BS = BS;
+  a.gkey = gkey;
+  a.gid = gid;
+  a.gcount = gcount;
+  a.flags = flags;
+  a.bins = bins;
+  a.labels = labels;
+  // per-block value cache: 128 buckets x 4 slots per feature (load <= 1/2 at
+  // 256 values), fewer when F is large
+  a.log2nb = 7;
+  while (a.log2nb > 3 && (size_t)F * (24u << a.log2nb) > 48 * 1024) a.log2nb--;
+  const size_t cache = 128 + (size_t)F * (24u << a.log2nb);
+  // P threads per row, TR = threads / P rows per tile: the largest tile whose
+  // kStages (times, features) buffers fit next to the cache
+  a.P = 4;
+  while (a.P < 32 && cache + (size_t)kStages * (kIngestThreads / a.P) * (V + F) * 4 > 220 * 1024)
+    a.P <<= 1;
+  a.TR = kIngestThreads / a.P;
+  a.use_tma = ((reinterpret_cast<uintptr_t>(feat) | reinterpret_cast<uintptr_t>(times)) & 15) == 0;
+  const size_t smem = cache + (size_t)kStages * a.TR * (V + F) * 4;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ntiles = (n + a.TR - 1) / a.TR;
+  const int grid = (int)std::min<int64_t>(ntiles, sms);
+  CUDA_CHECK(cudaFuncSetAttribute(ingest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  ingest_kernel<<<grid, kIngestThreads, smem, s>>>(a);
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -338,13 +430,6 @@ void launch_bins_out(const uint8_t *rec, int64_t n, int F, int RS, const uint8_t
                      uint8_t *out, cudaStream_t s) {
   if (n == 0) return;
   bins_out_kernel<<<grid_for(n * F, 256, 148 * 16), 256, 0, s>>>(rec, n, F, RS, lut, out);
-  CUDA_CHECK(cudaGetLastError());
-}
-
-void launch_labels_out(const uint8_t *rec, int64_t n, int F, int RS, uint8_t *out,
-                       cudaStream_t s) {
-  if (n == 0) return;
-  labels_out_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(rec, n, F, RS, out);
   CUDA_CHECK(cudaGetLastError());
 }
 

@@ -15,11 +15,17 @@ namespace {
 constexpr int kSelThreads = 256;
 
 __global__ void __launch_bounds__(kSelThreads)
-    select_kernel(const DNode *__restrict__ tree, const float *__restrict__ X, int64_t m, int F,
-                  int32_t *__restrict__ out) {
-  extern __shared__ float sx[];  // [kSelThreads][F | 1] (odd stride)
+    select_kernel(const DNode *__restrict__ gtree, int n_nodes, int tree_in_smem /* = n_top */,
+                  const float *__restrict__ X, int64_t m, int F, int32_t *__restrict__ out) {
+  extern __shared__ float sx[];  // [kSelThreads][F | 1] (odd stride) | tree copy
   const int stride = F | 1;
   const int t = threadIdx.x;
+  // the first n_top nodes (BFS order = the top levels, where every walk
+  // passes) live in shared memory; deeper nodes are read through L1/L2
+  DNode *st = reinterpret_cast<DNode *>(sx + kSelThreads * stride + (kSelThreads * stride & 1));
+  const int n_top = tree_in_smem;
+  for (int i = t; i < n_top; i += kSelThreads) st[i] = gtree[i];
+  __syncthreads();
   const bool aligned = (reinterpret_cast<uintptr_t>(X) & 15) == 0 && (F & 3) == 0;
   for (int64_t v0 = blockIdx.x * (int64_t)kSelThreads; v0 < m;
        v0 += (int64_t)gridDim.x * kSelThreads) {
@@ -46,14 +52,13 @@ __global__ void __launch_bounds__(kSelThreads)
     __syncthreads();
     if (t < rows) {
       const float *x = sx + t * stride;
-      int k = 0;
-      int32_t meta = __ldg(&tree[0].meta);
-      while (meta >= 0) {
-        const float thr = __ldg(&tree[k].thr);
-        const float v = x[meta & 63];
-        k = (meta >> 6) + (v <= thr ? 0 : 1);
-        meta = __ldg(&tree[k].meta);
+      DNode nd = n_top > 0 ? st[0] : gtree[0];
+      while (nd.meta >= 0) {
+        const float v = x[nd.meta & 63];
+        const int k = (nd.meta >> 6) + (v <= nd.thr ? 0 : 1);
+        nd = k < n_top ? st[k] : gtree[k];
       }
+      const int32_t meta = nd.meta;
       __stcs(out + v0 + t, -1 - meta);
     }
     __syncthreads();
@@ -62,15 +67,17 @@ __global__ void __launch_bounds__(kSelThreads)
 
 }  // namespace
 
-void launch_select(const DNode *tree, const float *X, int64_t m, int F, int32_t *out,
+void launch_select(const DNode *tree, int n_nodes, const float *X, int64_t m, int F, int32_t *out,
                    cudaStream_t s) {
   if (m == 0) return;
-  const size_t smem = (size_t)kSelThreads * (F | 1) * 4;
+  const size_t xs = ((size_t)kSelThreads * (F | 1) * 4 + 7) / 8 * 8;
+  const int n_top = n_nodes < 2048 ? n_nodes : 2047;  // top 11 levels: 16 KB
+  const size_t smem = xs + (size_t)n_top * sizeof(DNode);
   CUDA_CHECK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
   int64_t blocks = (m + kSelThreads - 1) / kSelThreads;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  select_kernel<<<(int)blocks, kSelThreads, smem, s>>>(tree, X, m, F, out);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  select_kernel<<<(int)blocks, kSelThreads, smem, s>>>(tree, n_nodes, n_top, X, m, F, out);
   CUDA_CHECK(cudaGetLastError());
 }
 

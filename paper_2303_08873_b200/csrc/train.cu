@@ -1,9 +1,10 @@
 // train.cu — the level-wise CART trainer's kernels.
 //
 // One tree level = one pass over the rows of the nodes being split:
-//   hist_pass_kernel  a7 partition of the previous level's splits (rows of a
-//                     parent span are scattered to the children's spans, left
-//                     from the front, right from the back) fused with a4, the
+//   hist_pass_kernel  a7 partition of the previous level's splits (the rows of
+//                     a parent span are moved — coalesced reads, warp-contiguous
+//                     writes — into the children's spans, left from the front,
+//                     right from the back) fused with a4, the
 //                     class histogram H[node][f][rank][class] of ONE child per
 //                     parent (the smaller, "direct" one), privatised in shared
 //                     memory and flushed with integer atomics;
@@ -21,69 +22,123 @@
 namespace adapt {
 namespace {
 
-constexpr int kHistThreads = 512;
+constexpr int kHistThreads = 1024;
 constexpr unsigned kFull = 0xffffffffu;
 
-template <int RS>
-struct RecWords {
-  static constexpr int N = RS >= 4 ? RS / 4 : 1;
+template <int BS>
+struct Row {  // one row's bins, BS bytes, in registers
+  static constexpr int N = BS >= 4 ? BS / 4 : 1;
   uint32_t w[N];
 };
 
-template <int RS>
-__device__ __forceinline__ void load_rec(const uint8_t *__restrict__ p, RecWords<RS> &r) {
-  if constexpr (RS >= 16) {
+template <int BS>
+__device__ __forceinline__ void load_row(const uint8_t *__restrict__ p, Row<BS> &r) {
+  if constexpr (BS >= 16) {
 #pragma unroll
-    for (int i = 0; i < RS / 16; i++) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p) + i);
+    for (int i = 0; i < BS / 16; i++) {
+      const uint4 v = *(reinterpret_cast<const uint4 *>(p) + i);
       r.w[4 * i + 0] = v.x;
       r.w[4 * i + 1] = v.y;
       r.w[4 * i + 2] = v.z;
       r.w[4 * i + 3] = v.w;
     }
-  } else if constexpr (RS == 8) {
-    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+  } else if constexpr (BS == 8) {
+    const uint2 v = *reinterpret_cast<const uint2 *>(p);
     r.w[0] = v.x;
     r.w[1] = v.y;
-  } else if constexpr (RS == 4) {
-    r.w[0] = __ldg(reinterpret_cast<const uint32_t *>(p));
+  } else if constexpr (BS == 4) {
+    r.w[0] = *reinterpret_cast<const unsigned int *>(p);
+  } else if constexpr (BS == 2) {
+    r.w[0] = *reinterpret_cast<const unsigned short *>(p);
   } else {
-    r.w[0] = __ldg(reinterpret_cast<const uint16_t *>(p));
+    r.w[0] = *p;
   }
 }
 
-template <int RS>
-__device__ __forceinline__ int rec_byte(const RecWords<RS> &r, int f) {
-  // f is warp-uniform per segment; a small unrolled select keeps r in registers
-  int out = 0;
+template <int BS>
+__device__ __forceinline__ void store_row(uint8_t *__restrict__ p, const Row<BS> &r) {
+  if constexpr (BS >= 16) {
 #pragma unroll
-  for (int i = 0; i < RecWords<RS>::N; i++)
-    if ((f >> 2) == i) out = (int)((r.w[i] >> (8 * (f & 3))) & 0xFFu);
-  return out;
+    for (int i = 0; i < BS / 16; i++)
+      __stcs(reinterpret_cast<uint4 *>(p) + i,
+             make_uint4(r.w[4 * i], r.w[4 * i + 1], r.w[4 * i + 2], r.w[4 * i + 3]));
+  } else if constexpr (BS == 8) {
+    __stcs(reinterpret_cast<uint2 *>(p), make_uint2(r.w[0], r.w[1]));
+  } else if constexpr (BS == 4) {
+    __stcs(reinterpret_cast<unsigned int *>(p), r.w[0]);
+  } else if constexpr (BS == 2) {
+    *reinterpret_cast<unsigned short *>(p) = (unsigned short)r.w[0];
+  } else {
+    *p = (uint8_t)r.w[0];
+  }
 }
 
-template <int RS>
-__global__ void __launch_bounds__(kHistThreads) hist_pass_kernel(HistPassArgs a) {
+// select w[i] for a runtime i with a tree of register selects (N = power of 2);
+// every array access has a compile-time index, so nothing spills to local memory
+template <int N>
+__device__ __forceinline__ uint32_t pick(const uint32_t *w, int i) {
+  if constexpr (N == 1) {
+    return w[0];
+  } else {
+    constexpr int H = N / 2;
+    const uint32_t lo = pick<H>(w, i & (H - 1));
+    const uint32_t hi = pick<H>(w + H, i & (H - 1));
+    return (i & H) ? hi : lo;
+  }
+}
+
+template <int BS>
+__device__ __forceinline__ int row_byte(const Row<BS> &r, int f) {
+  return (int)((pick<Row<BS>::N>(r.w, f >> 2) >> (8 * (f & 3))) & 0xFFu);
+}
+
+constexpr int kUnroll = 4;  // rows per thread per iteration (memory-level parallelism)
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// One level pass.  A cluster of `ngroups` CTAs walks the same contiguous range
+// of row positions; CTA g histograms the features of 32-bit word w0(g) of the
+// bins row (4 features) for the class slab [k0, k0+kw), so each CTA does at
+// most 4 shared-memory atomics per row.  The CTAs re-synchronise every
+// kSyncEvery iterations, which keeps them within a few hundred KB of each
+// other: each row is fetched from HBM once and served to the others from L2.
+// CTA 0 also moves the rows into the children's spans (a7).  Counters are
+// indexed by PROVISIONAL bin id (no per-feature lookup) with an odd class
+// stride (bank spread); the id -> rank map is applied once per counter when
+// the block flushes into the global histogram.
+constexpr int kSyncEvery = 8;
+
+template <int BS>
+__global__ void __launch_bounds__(kHistThreads, 1) hist_pass_kernel(HistPassArgs a) {
   extern __shared__ uint32_t sh[];  // [smem_counters] counters | lut [F*256] bytes
   uint8_t *slut = reinterpret_cast<uint8_t *>(sh + a.smem_counters);
-  __shared__ int32_t sloff[kMaxF];
+  __shared__ int32_t soff[kMaxF];   // this group's smem offset of feature f, -1 if absent
+  __shared__ int32_t sdf[kMaxF];    // distinct values of f
   const int tid = threadIdx.x, lane = tid & 31;
-  const int g = blockIdx.y;
-  // group g: features [f0, f1) x classes [k0, k1); its counters are laid out
-  // [f][rank][k - k0], i.e. the node layout restricted to the class slab
-  const int4 grp = a.groups[g];
-  const int f0 = grp.x, f1 = grp.y, k0 = grp.z, kw = grp.w - grp.z;
+  const int g = blockIdx.x % a.ngroups;
+  const int range = blockIdx.x / a.ngroups;
+  const int4 grp = a.groups[g];  // x: first class, y: classes, z: padded class stride, w: word
+  const int k0 = grp.x, kw = grp.y, kwp = grp.z, w0 = grp.w;
   const int C = a.C;
-  const int gcount = ((f1 < a.F ? a.hoff[f1] : (int)a.HS) - a.hoff[f0]) / C * kw;
+  const bool clustered = a.clustered;
   for (int i = tid; i < a.F * kMaxBins / 4; i += blockDim.x)
     reinterpret_cast<uint32_t *>(slut)[i] = reinterpret_cast<const uint32_t *>(a.lut)[i];
-  for (int f = tid; f < a.F; f += blockDim.x) sloff[f] = (a.hoff[f] - a.hoff[f0]) / C * kw;
-
-  const uint32_t R = (a.total_rows + a.blocks_per_group - 1) / a.blocks_per_group;
-  uint32_t p0 = blockIdx.x * R;
+  int gcount = 0;
+  for (int f = 0; f < a.F; f++) {
+    const int o = a.gsoff[g * a.F + f];
+    if (tid == 0) {
+      soff[f] = o;
+      sdf[f] = a.nval[f];
+    }
+    if (o >= 0) gcount = max(gcount, o + a.nval[f] * kwp);
+  }
+  const uint32_t R = (a.total_rows + a.nranges - 1) / a.nranges;
+  uint32_t p0 = range * R;
   const uint32_t p1 = min(p0 + R, a.total_rows);
-  // first segment whose span contains position p0
-  int s = 0;
+  int s = 0;  // first segment whose span contains position p0
   {
     int lo = 0, hi = a.nseg - 1;
     while (lo < hi) {
@@ -93,76 +148,86 @@ __global__ void __launch_bounds__(kHistThreads) hist_pass_kernel(HistPassArgs a)
     s = lo;
   }
   __syncthreads();
+  int my_off[4];  // smem offsets of the 4 features of word w0 (-1: not histogrammed here)
+#pragma unroll
+  for (int e = 0; e < 4; e++) my_off[e] = (4 * w0 + e < a.F) ? soff[4 * w0 + e] : -1;
+  int iter = 0;
   while (p0 < p1 && s < a.nseg) {
     const Seg sg = a.segs[s];
     const uint32_t q0 = p0 - sg.row_base;
     const uint32_t q1 = min(sg.len, p1 - sg.row_base);
     const bool hist_on = sg.direct >= 0 && sg.hslot >= 0;
-    const bool part_on = g == 0 && sg.feat >= 0 && sg.write != 0;
+    const bool part_on = g == 0 && sg.feat >= 0 && sg.write != 0 && a.bins_out != nullptr;
     if (q0 < q1 && (hist_on || part_on)) {
       if (hist_on) {
         for (int i = tid; i < gcount; i += blockDim.x) sh[i] = 0;
         __syncthreads();
       }
-      for (uint32_t qb = q0; qb < q1; qb += blockDim.x) {
-        const uint32_t q = qb + tid;
-        const bool valid = q < q1;
-        uint32_t row = 0;
-        RecWords<RS> r;
-        int label = 0;
-        bool left = true;
-        if (valid) {
-          row = a.idx_prev ? __ldg(a.idx_prev + sg.off + q) : sg.off + q;
-          const uint8_t *rp = a.rec + (size_t)row * RS;
-          load_rec<RS>(rp, r);
-          label = rec_byte<RS>(r, a.F);
-          if (sg.feat >= 0) left = slut[sg.feat * kMaxBins + rec_byte<RS>(r, sg.feat)] <= sg.thr;
-        }
-        if (part_on) {  // a7: scatter the row id into the child's span
+      for (uint32_t qb = q0; qb < q1; qb += kUnroll * blockDim.x) {
+        if (clustered && ++iter % kSyncEvery == 0) cluster_sync_all();
+        Row<BS> r[kUnroll];
+        int label[kUnroll];
+        bool valid[kUnroll];
 #pragma unroll
-          for (int side = 0; side < 2; side++) {
-            const bool mine = valid && (side == 0 ? left : !left) && ((sg.write >> side) & 1);
-            const unsigned m = __ballot_sync(kFull, mine);
-            if (m) {
-              const int leader = __ffs(m) - 1;
-              uint32_t base = 0;
-              if (lane == leader) base = atomicAdd(a.cursors + 2 * s + side, __popc(m));
-              base = __shfl_sync(kFull, base, leader);
-              if (mine) {
-                const uint32_t k = base + __popc(m & ((1u << lane) - 1));
-                a.idx_next[side == 0 ? sg.off + k : sg.off + sg.len - 1 - k] = row;
+        for (int u = 0; u < kUnroll; u++) {  // issue all loads first
+          const uint32_t q = qb + u * blockDim.x + tid;
+          valid[u] = q < q1;
+          label[u] = 0;
+          if (valid[u]) {
+            load_row<BS>(a.bins_in + (size_t)(sg.off + q) * BS, r[u]);
+            label[u] = a.lab_in[sg.off + q];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+          bool left = true;
+          if (valid[u] && sg.feat >= 0)
+            left = slut[sg.feat * kMaxBins + row_byte<BS>(r[u], sg.feat)] <= sg.thr;
+          if (part_on) {  // a7: move the row into its child's span
+#pragma unroll
+            for (int side = 0; side < 2; side++) {
+              const bool mine = valid[u] && (side == 0 ? left : !left) && ((sg.write >> side) & 1);
+              const unsigned m = __ballot_sync(kFull, mine);
+              if (m) {
+                const int leader = __ffs(m) - 1;
+                uint32_t base = 0;
+                if (lane == leader) base = atomicAdd(a.cursors + 2 * s + side, __popc(m));
+                base = __shfl_sync(kFull, base, leader);
+                if (mine) {
+                  const uint32_t k = base + __popc(m & ((1u << lane) - 1));
+                  const uint32_t pos = side == 0 ? sg.off + k : sg.off + sg.len - 1 - k;
+                  store_row<BS>(a.bins_out + (size_t)pos * BS, r[u]);
+                  __stcs(a.lab_out + pos, (uint8_t)label[u]);
+                }
               }
             }
           }
-        }
-        if (hist_on && valid && (unsigned)(label - k0) < (unsigned)kw &&
-            (sg.direct == 2 || (sg.direct == 0 && left) || (sg.direct == 1 && !left))) {
+          if (hist_on && valid[u] && (unsigned)(label[u] - k0) < (unsigned)kw &&
+              (sg.direct == 2 || (sg.direct == 0 && left) || (sg.direct == 1 && !left))) {
+            const int lk = label[u] - k0;
+            const uint32_t w = pick<Row<BS>::N>(r[u].w, w0);
 #pragma unroll
-          for (int wi = 0; wi < RecWords<RS>::N; wi++) {
-#pragma unroll
-            for (int bi = 0; bi < 4; bi++) {
-              const int f = wi * 4 + bi;
-              if (f >= f0 && f < f1) {
-                const int bin = (r.w[wi] >> (8 * bi)) & 0xFF;
-                atomicAdd(&sh[sloff[f] + (int)slut[f * kMaxBins + bin] * kw + (label - k0)], 1u);
-              }
-            }
+            for (int e = 0; e < 4; e++)
+              if (my_off[e] >= 0)
+                atomicAdd(&sh[my_off[e] + (int)((w >> (8 * e)) & 0xFF) * kwp + lk], 1u);
           }
         }
       }
       __syncthreads();
-      if (hist_on) {  // flush the block's partial histogram
-        uint32_t *dst = a.H + (size_t)sg.hslot * a.HS + a.hoff[f0];
-        if (kw == C) {
-          for (int i = tid; i < gcount; i += blockDim.x) {
-            const uint32_t v = sh[i];
-            if (v) atomicAdd(dst + i, v);
-          }
-        } else {  // class slab of one feature: row r, class k0 + j
-          for (int i = tid; i < gcount; i += blockDim.x) {
-            const uint32_t v = sh[i];
-            const int r = i / kw, j = i - r * kw;
-            if (v) atomicAdd(dst + r * C + k0 + j, v);
+      if (hist_on) {  // flush: provisional id -> rank, class slab -> classes
+        uint32_t *dst = a.H + (size_t)sg.hslot * a.HS;
+        for (int f = 0; f < a.F; f++) {
+          const int o = soff[f];
+          if (o < 0) continue;
+          const int n = sdf[f] * kwp;
+          const uint8_t *lf = slut + f * kMaxBins;
+          uint32_t *df = dst + a.hoff[f];
+          for (int i = tid; i < n; i += blockDim.x) {
+            const uint32_t v = sh[o + i];
+            if (v) {
+              const int p = i / kwp, j = i - p * kwp;
+              atomicAdd(df + (int)lf[p] * C + k0 + j, v);
+            }
           }
         }
         __syncthreads();
@@ -171,6 +236,7 @@ __global__ void __launch_bounds__(kHistThreads) hist_pass_kernel(HistPassArgs a)
     p0 = sg.row_base + q1;
     s++;
   }
+  if (clustered) cluster_sync_all();  // no CTA leaves while a partner may still sync
 }
 
 __global__ void zero_slots_kernel(uint32_t *H, int64_t HS, const int32_t *slots) {
@@ -431,18 +497,29 @@ __global__ void __launch_bounds__(256)
 void launch_hist_pass(const HistPassArgs &a, cudaStream_t s) {
   if (a.total_rows == 0 || a.nseg == 0) return;
   const size_t smem = (size_t)a.smem_counters * 4 + (size_t)a.F * kMaxBins;
-  dim3 grid(a.blocks_per_group, a.ngroups);
-  switch (a.RS) {
-#define CASE(R)                                                                               \
-  case R:                                                                                     \
-    CUDA_CHECK(cudaFuncSetAttribute(hist_pass_kernel<R>,                                      \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
-    hist_pass_kernel<R><<<grid, kHistThreads, smem, s>>>(a);                                  \
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.nranges * a.ngroups);
+  cfg.blockDim = dim3(kHistThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = a.ngroups;  // the groups of one range run together
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.clustered ? 1 : 0;
+  switch (a.BS) {
+#define CASE(B)                                                                              \
+  case B:                                                                                    \
+    CUDA_CHECK(cudaFuncSetAttribute(hist_pass_kernel<B>,                                     \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, hist_pass_kernel<B>, a));                            \
     break;
-    CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) CASE(128)
+    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
 #undef CASE
     default:
-      throw Error(-1, "bad record stride");
+      throw Error(-1, "bad bins stride");
   }
   CUDA_CHECK(cudaGetLastError());
 }
