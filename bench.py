@@ -264,7 +264,7 @@ def main():
         return
 
     peak, peak_src = peaks()
-    kern = {k: v for k, v in prof.items() if k in KERNEL_PHASES}
+    kern = {k: v for k, v in prof.items() if k.split("_L")[0] in KERNEL_PHASES}
     dom = max(kern, key=lambda k: kern[k]["ms"])
     d = kern[dom]
     achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 and d["bytes"] > 0 else None

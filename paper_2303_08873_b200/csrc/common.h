@@ -31,20 +31,26 @@ void cuda_check(cudaError_t e, const char *what);
 #define CUDA_CHECK(x) ::adapt::cuda_check((x), #x)
 
 // ---- one segment of a level pass (host-built, read by hist_pass_kernel) ----
-// A segment is the span [off, off+len) of one parent node in the level's row
-// planes.  The pass moves its rows (feat >= 0) into the children's spans of the
-// output planes — left rows from the front, right rows from the back — and
+// A segment is one piece [off, off+len) of a parent node's rows in the level's
+// input planes (a node's rows may lie in several pieces, consecutive in the
+// segment list).  Concatenating the segments gives every row a "virtual
+// position"; the output planes are indexed by it.  The pass moves the rows
+// (feat >= 0): each CTA takes a contiguous share [A, B) of a node's virtual
+// positions inside its range and writes that share's left rows at [A, ...)
+// and right rows at [..., B) — the children's pieces for the next level — and
 // accumulates the class histogram of the "direct" child (or of all rows for
 // the root pass).
 struct Seg {
-  uint32_t off;       // span start (row position in the level's planes)
-  uint32_t len;       // rows of this rank in the span
-  uint32_t row_base;  // prefix sum of len over previous segments (block work split)
-  int32_t feat;       // split feature, -1 = no partition (root pass)
-  int32_t thr;        // rank b_lo: rank <= thr goes left
-  int32_t direct;     // 0: histogram rows going left, 1: right, 2: all rows, -1: none
-  int32_t hslot;      // histogram slot of the direct child (-1: none)
-  int32_t write;      // bit0: move left rows to the output planes, bit1: right rows
+  uint32_t off;        // piece start (row position in the level's input planes)
+  uint32_t len;        // rows of this rank in the piece
+  uint32_t row_base;   // virtual position: prefix sum of len over previous segments
+  uint32_t node_base;  // virtual position of the first piece of this segment's node
+  uint32_t node_len;   // rows of the node (all its pieces)
+  int32_t feat;        // split feature, -1 = no partition (root pass)
+  int32_t thr;         // rank b_lo: rank <= thr goes left
+  int32_t direct;      // 0: histogram rows going left, 1: right, 2: all rows, -1: none
+  int32_t hslot;       // histogram slot of the direct child (-1: none)
+  int32_t write;       // bit0: move left rows to the output planes, bit1: right rows
 };
 
 // best cut of one (node, feature), exact key num/den (R13x)
@@ -86,7 +92,8 @@ struct HistPassArgs {
   const uint8_t *lab_in;     // [pos]
   uint8_t *bins_out;         // partitioned rows for the next level (null: root pass)
   uint8_t *lab_out;
-  uint32_t *cursors;         // 2 per segment (left count, right count), zeroed
+  int32_t *visits;           // [grid][max_visits][6]: seg, share [A, B), left, right moved
+  int max_visits;
   int BS, F, C;
   const uint8_t *lut;        // [F][256] prov -> rank
   const int32_t *hoff;       // [F] counter offset of feature f in a node histogram
@@ -94,7 +101,7 @@ struct HistPassArgs {
   const int4 *groups;        // [ngroups] x: first class, y: classes, z: padded stride, w: bins word
   const int32_t *gsoff;      // [ngroups][F] smem offset of feature f in group g, -1 if absent
   int ngroups;
-  int clustered;             // launched as clusters of ngroups CTAs
+  uint32_t *sync;            // [nranges] partner-sync counters, zeroed (null: no sync)
   int smem_counters;         // max counters of a group
   uint32_t *H;               // [slots][HS]
   int64_t HS;

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -213,8 +214,8 @@ constexpr int kHistSmemBudget = 200 * 1024;  // counters + LUT per level-pass CT
 struct FNode {  // a frontier node: histogrammed and split-searched at this level
   int32_t tree_idx;
   int32_t depth;
-  uint32_t off, len;  // local span in the idx arrays
-  int32_t slot;       // histogram slot at this level
+  int32_t slot;  // histogram slot at this level
+  std::vector<std::pair<uint32_t, uint32_t>> pieces;  // this rank's rows: (offset, length) in the planes
 };
 
 }  // namespace
@@ -247,7 +248,7 @@ struct adapt_region {
   std::vector<int64_t> stats;
   // scratch
   adapt::DevBuf gkey, gid, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, H0, H1, segs,
-      cursors, slots, triples, nslot, cand, res, hoff, grp, gsoff, xa, xb, oa, ob;
+      visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, psync, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall;
   // Table-1 shim state
   bool active = false;
@@ -560,12 +561,15 @@ void train_region(adapt_region *h, cudaStream_t s) {
   root.feature = -1;
   root.left = root.right = -1;
   h->tree.push_back(root);
-  std::vector<FNode> frontier{{0, 0, 0, (uint32_t)n, 0}};
-  std::vector<Seg> segs{{0, (uint32_t)n, 0, -1, 0, 2, 0, 0}};
+  std::vector<FNode> frontier(1);
+  frontier[0].tree_idx = 0;
+  frontier[0].depth = 0;
+  frontier[0].slot = 0;
+  frontier[0].pieces = {{0u, (uint32_t)n}};
+  std::vector<Seg> segs{{0, (uint32_t)n, 0, 0, (uint32_t)n, -1, 0, 2, 0, 0}};
   std::vector<int32_t> direct_slots{0};
   std::vector<int32_t> triples;
-  std::vector<int> seg_children;  // per seg: frontier index of left (or -1), right (or -1)
-  seg_children = {-1, -1};
+  std::vector<int2> seg_children{make_int2(-1, -1)};  // per seg: frontier index of left / right child
   // level planes: the root pass reads the ingest output; pass d >= 1 moves the
   // rows of the split parents from one plane pair into the other
   const uint8_t *bins_in = h->bins.as<uint8_t>(), *lab_in = h->labels.as<uint8_t>();
@@ -578,21 +582,27 @@ void train_region(adapt_region *h, cudaStream_t s) {
   CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g_ctx.device));
   DevBuf *Hcur = &h->H0, *Hprev = &h->H1;
   const int res_stride = (int)((sizeof(NodeRes) + 8 * (size_t)C + 7) / 8 * 8);
-  std::vector<uint64_t> P_of_tree;  // class totals per tree node (tree order), C each
-  P_of_tree.reserve(64 * C);
 
   for (int level = 0; !frontier.empty(); level++) {
     const int A = (int)frontier.size();
     const int nseg = (int)segs.size();
     uint32_t total = 0;
-    for (auto &sg : segs) {
-      sg.row_base = total;
-      total += sg.len;
+    for (size_t i = 0; i < segs.size(); i++) {
+      segs[i].row_base = total;
+      total += segs[i].len;
+    }
+    for (size_t i = 0; i < segs.size();) {  // node extents in virtual positions
+      size_t k = i;
+      uint32_t len = 0;
+      while (k < segs.size() && segs[k].hslot == segs[i].hslot) len += segs[k++].len;
+      for (size_t t = i; t < k; t++) {
+        segs[t].node_base = segs[i].row_base;
+        segs[t].node_len = len;
+      }
+      i = k;
     }
     Hcur->ensure((size_t)A * HS * 4);
     h2d(h->segs, segs, s);
-    h->cursors.ensure((size_t)nseg * 8 + 8);
-    CUDA_CHECK(cudaMemsetAsync(h->cursors.p, 0, (size_t)nseg * 8, s));
     h2d(h->slots, direct_slots, s);
     {
       Phase ph("zero", s, 0);
@@ -606,7 +616,6 @@ void train_region(adapt_region *h, cudaStream_t s) {
     a.lab_in = lab_in;
     a.bins_out = level == 0 ? nullptr : (out_plane ? h->binsB : h->binsA).as<uint8_t>();
     a.lab_out = level == 0 ? nullptr : (out_plane ? h->labB : h->labA).as<uint8_t>();
-    a.cursors = h->cursors.as<uint32_t>();
     a.BS = BS;
     a.F = F;
     a.C = C;
@@ -615,16 +624,39 @@ void train_region(adapt_region *h, cudaStream_t s) {
     a.nval = h->dnval.as<int32_t>();
     a.groups = h->grp.as<int4>();
     a.gsoff = h->gsoff.as<int32_t>();
-    a.clustered = ngroups > 1 && ngroups <= 8;
     a.ngroups = ngroups;
     a.smem_counters = max_group;
     a.H = Hcur->as<uint32_t>();
     a.HS = HS;
-    // one wave: every cluster of ngroups CTAs (one CTA per SM) takes an equal row range
+    // one CTA per SM; the ngroups CTAs of a range are co-resident (cooperative launch)
     a.nranges = (int)std::max<int64_t>(
-        1, std::min<int64_t>((total + 2047) / 2048, std::max(1, sms / std::min(ngroups, 8))));
+        1, std::min<int64_t>((total + 4095) / 4096, std::max(1, sms / ngroups)));
+    a.sync = nullptr;
+    if (ngroups > 1 && a.nranges * ngroups <= sms) {
+      h->psync.ensure((size_t)a.nranges * 4);
+      CUDA_CHECK(cudaMemsetAsync(h->psync.p, 0, (size_t)a.nranges * 4, s));
+      a.sync = h->psync.as<uint32_t>();
+    }
+    // segments a range can touch: the visit-report capacity per CTA
+    const uint32_t R = (total + a.nranges - 1) / std::max(1, a.nranges);
+    int max_visits = 1;
+    for (int r = 0, si = 0; r < a.nranges; r++) {
+      const uint32_t p0 = r * R, p1 = std::min<uint64_t>((uint64_t)p0 + R, total);
+      while (si + 1 < nseg && segs[si + 1].row_base <= p0) si++;
+      int k = si;
+      while (k < nseg && segs[k].row_base < p1) k++;
+      max_visits = std::max(max_visits, k - si);
+    }
+    const int grid = a.nranges * ngroups;
+    a.max_visits = max_visits;
+    h->visits.ensure((size_t)grid * max_visits * 6 * 4);
+    CUDA_CHECK(cudaMemsetAsync(h->visits.p, 0xFF, (size_t)grid * max_visits * 6 * 4, s));
+    a.visits = h->visits.as<int32_t>();
     {
-      Phase ph("hist", s, (double)total * (F + 1));
+      static const bool per_level = getenv("ADAPT_PROFILE_LEVELS") != nullptr;
+      char nm[24];
+      snprintf(nm, sizeof nm, "hist_L%02d", level);
+      Phase ph(per_level ? nm : "hist", s, (double)total * (F + 1));
       launch_hist_pass(a, s);
     }
     if (world > 1 && !direct_slots.empty())
@@ -642,7 +674,10 @@ void train_region(adapt_region *h, cudaStream_t s) {
     h->cand.ensure((size_t)A * F * sizeof(SplitCand));
     h->res.ensure((size_t)A * res_stride);
     {
-      Phase ph("split", s, 0);
+      static const bool per_level = getenv("ADAPT_PROFILE_LEVELS") != nullptr;
+      char nm[24];
+      snprintf(nm, sizeof nm, "split_L%02d", level);
+      Phase ph(per_level ? nm : "split", s, 0);
       launch_split(Hcur->as<uint32_t>(), HS, h->nslot.as<int32_t>(), A, F, C, h->hoff.as<int32_t>(),
                    h->dnval.as<int32_t>(), h->cand.as<SplitCand>(), s);
     }
@@ -652,24 +687,31 @@ void train_region(adapt_region *h, cudaStream_t s) {
                     h->hoff.as<int32_t>(), h->dnval.as<int32_t>(), h->cand.as<SplitCand>(),
                     h->res.as<uint8_t>(), res_stride, s);
     }
-    h->hres.ensure((size_t)A * res_stride + (size_t)nseg * 8);
+    const size_t vbytes = (size_t)grid * max_visits * 6 * 4;
+    h->hres.ensure((size_t)A * res_stride + vbytes);
     uint8_t *hr = h->hres.as<uint8_t>();
     CUDA_CHECK(cudaMemcpyAsync(hr, h->res.p, (size_t)A * res_stride, cudaMemcpyDeviceToHost, s));
-    uint32_t *hcur = reinterpret_cast<uint32_t *>(hr + (size_t)A * res_stride);
-    CUDA_CHECK(cudaMemcpyAsync(hcur, h->cursors.p, (size_t)nseg * 8, cudaMemcpyDeviceToHost, s));
+    int32_t *hv = reinterpret_cast<int32_t *>(hr + (size_t)A * res_stride);
+    if (level > 0) CUDA_CHECK(cudaMemcpyAsync(hv, h->visits.p, vbytes, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
 
-    // local spans of this level's frontier nodes from the partition cursors
-    int64_t rows_hist = 0;
-    for (int si = 0; si < nseg && level > 0; si++) {
-      const Seg &sg = segs[si];
-      const int jl = seg_children[2 * si], jr = seg_children[2 * si + 1];
-      if (jl >= 0) frontier[jl].off = sg.off, frontier[jl].len = hcur[2 * si];
-      if (jr >= 0) frontier[jr].off = sg.off + sg.len - hcur[2 * si + 1], frontier[jr].len = hcur[2 * si + 1];
-      if (sg.direct == 0) rows_hist += hcur[2 * si];
-      if (sg.direct == 1) rows_hist += hcur[2 * si + 1];
+    // pieces of this level's frontier nodes, from the CTAs' sub-portion reports
+    int64_t rows_hist = level == 0 ? total : 0;
+    if (level > 0) {
+      for (auto &fn : frontier) fn.pieces.clear();
+      for (int b = 0; b < grid; b++)
+        for (int v = 0; v < max_visits; v++) {
+          const int32_t *e = hv + ((size_t)b * max_visits + v) * 6;
+          if (e[0] < 0) break;
+          const Seg &sg = segs[e[0]];
+          const int2 ch = seg_children[e[0]];
+          if (ch.x >= 0 && e[3] > 0) frontier[ch.x].pieces.push_back({(uint32_t)e[1], (uint32_t)e[3]});
+          if (ch.y >= 0 && e[4] > 0)
+            frontier[ch.y].pieces.push_back({(uint32_t)(e[2] - e[4]), (uint32_t)e[4]});
+          rows_hist += sg.direct == 0 ? e[3] : (sg.direct == 1 ? e[4] : 0);
+        }
+      for (auto &fn : frontier) std::sort(fn.pieces.begin(), fn.pieces.end());
     }
-    if (level == 0) rows_hist = total;
     h->stats.push_back(A);
     h->stats.push_back(rows_hist);
     h->stats.push_back(level == 0 ? 0 : total);
@@ -678,13 +720,14 @@ void train_region(adapt_region *h, cudaStream_t s) {
     std::vector<FNode> next;
     std::vector<Seg> nsegs;
     std::vector<int32_t> ndirect, nderived_par, nderived_sib;
-    std::vector<int> nderived_j, nchildren;
+    std::vector<int> nderived_j;
+    std::vector<int2> nchildren;
     std::vector<uint64_t> P(C), PL(C), PR(C);
     for (int j = 0; j < A; j++) {
       const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + (size_t)j * res_stride);
       const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);
       const uint32_t *cLd = Pd + C;
-      FNode fn = frontier[j];
+      const FNode &fn = frontier[j];
       for (int k = 0; k < C; k++) P[k] = Pd[k];
       fill_stats(h->tree[fn.tree_idx], P.data(), C);
       h->tree[fn.tree_idx].depth = fn.depth;
@@ -712,36 +755,38 @@ void train_region(adapt_region *h, cudaStream_t s) {
       h->tree.push_back(cl);
       h->tree.push_back(cr);
       if (!inL && !inR) continue;
-      Seg sg{};
-      sg.off = fn.off;
-      sg.len = fn.len;
-      sg.feat = f;
-      sg.thr = nr->b_lo;
-      sg.write = (inL ? 1 : 0) | (inR ? 2 : 0);
       const uint64_t nL = nr->nL, nR = nr->n - nr->nL;
       int dir;
       if (inL && inR) dir = nL <= nR ? 0 : 1;  // histogram the smaller child
       else dir = inL ? 0 : 1;
-      sg.direct = dir;
-      sg.hslot = (int32_t)ndirect.size();
-      ndirect.push_back(sg.hslot);
+      const int32_t hslot = (int32_t)ndirect.size();
+      ndirect.push_back(hslot);
       int jl = -1, jr = -1;
       if (inL) {
         jl = (int)next.size();
-        next.push_back({li, fn.depth + 1, 0, 0, dir == 0 ? sg.hslot : -1});
+        next.push_back(FNode{li, fn.depth + 1, dir == 0 ? hslot : -1, {}});
       }
       if (inR) {
         jr = (int)next.size();
-        next.push_back({li + 1, fn.depth + 1, 0, 0, dir == 1 ? sg.hslot : -1});
+        next.push_back(FNode{li + 1, fn.depth + 1, dir == 1 ? hslot : -1, {}});
       }
       if (inL && inR) {  // the other child by subtraction from the parent
         nderived_j.push_back(dir == 0 ? jr : jl);
         nderived_par.push_back(fn.slot);
-        nderived_sib.push_back(sg.hslot);
+        nderived_sib.push_back(hslot);
       }
-      nsegs.push_back(sg);
-      nchildren.push_back(jl);
-      nchildren.push_back(jr);
+      for (const auto &pc : fn.pieces) {  // one segment per piece of the parent
+        Seg sg{};
+        sg.off = pc.first;
+        sg.len = pc.second;
+        sg.feat = f;
+        sg.thr = nr->b_lo;
+        sg.write = (inL ? 1 : 0) | (inR ? 2 : 0);
+        sg.direct = dir;
+        sg.hslot = hslot;
+        nsegs.push_back(sg);
+        nchildren.push_back(make_int2(jl, jr));
+      }
     }
     // derived slots follow the direct ones
     triples.clear();

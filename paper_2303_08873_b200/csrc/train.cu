@@ -18,6 +18,7 @@
 // Every quantity that decides the tree is an integer, so the result does not
 // depend on row order, on the number of ranks or on atomic ordering.
 #include "common.h"
+#include "ptx.h"
 
 namespace adapt {
 namespace {
@@ -94,21 +95,30 @@ __device__ __forceinline__ int row_byte(const Row<BS> &r, int f) {
 
 constexpr int kUnroll = 4;  // rows per thread per iteration (memory-level parallelism)
 
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n"
-               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+__device__ __forceinline__ void red_shared_inc(uint32_t addr) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
 }
 
-// One level pass.  A cluster of `ngroups` CTAs walks the same contiguous range
-// of row positions; CTA g histograms the features of 32-bit word w0(g) of the
-// bins row (4 features) for the class slab [k0, k0+kw), so each CTA does at
-// most 4 shared-memory atomics per row.  The CTAs re-synchronise every
-// kSyncEvery iterations, which keeps them within a few hundred KB of each
-// other: each row is fetched from HBM once and served to the others from L2.
-// CTA 0 also moves the rows into the children's spans (a7).  Counters are
-// indexed by PROVISIONAL bin id (no per-feature lookup) with an odd class
-// stride (bank spread); the id -> rank map is applied once per counter when
-// the block flushes into the global histogram.
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One level pass.  The G CTAs of a "range" (consecutive blockIdx.x, all
+// co-resident: one CTA per SM, launched cooperatively) walk the same
+// contiguous range of row positions.  CTA g histograms the 4 features of
+// 32-bit word w(g) of the bins row for the class slab [k0, k0+kw) — at most 4
+// shared-memory atomics per row — and moves the rows of its own contiguous
+// G-th of every segment portion into the children's pieces (a7): left rows
+// from the front of that sub-portion, right rows from its back, positions
+// from shared-memory cursors (no global atomics, no block barriers).  Each
+// CTA reports (segment, sub-portion, left/right counts), from which the host
+// builds the next level's pieces.  The G CTAs re-synchronise through a
+// global counter every kSyncEvery iterations so that a row fetched from HBM
+// by one of them is still in L2 for the others.  Counters are indexed by
+// PROVISIONAL bin id with an odd class stride; the id -> rank map is applied
+// once per counter when a node's histogram is flushed.
 constexpr int kSyncEvery = 8;
 
 template <int BS>
@@ -117,13 +127,14 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_pass_kernel(HistPassArgs
   uint8_t *slut = reinterpret_cast<uint8_t *>(sh + a.smem_counters);
   __shared__ int32_t soff[kMaxF];   // this group's smem offset of feature f, -1 if absent
   __shared__ int32_t sdf[kMaxF];    // distinct values of f
+  __shared__ uint32_t s_cur[2];     // left / right cursors of this CTA's sub-portion
   const int tid = threadIdx.x, lane = tid & 31;
-  const int g = blockIdx.x % a.ngroups;
-  const int range = blockIdx.x / a.ngroups;
+  const int G = a.ngroups;
+  const int g = blockIdx.x % G;
+  const int range = blockIdx.x / G;
   const int4 grp = a.groups[g];  // x: first class, y: classes, z: padded class stride, w: word
   const int k0 = grp.x, kw = grp.y, kwp = grp.z, w0 = grp.w;
   const int C = a.C;
-  const bool clustered = a.clustered;
   for (int i = tid; i < a.F * kMaxBins / 4; i += blockDim.x)
     reinterpret_cast<uint32_t *>(slut)[i] = reinterpret_cast<const uint32_t *>(a.lut)[i];
   int gcount = 0;
@@ -148,95 +159,126 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_pass_kernel(HistPassArgs
     s = lo;
   }
   __syncthreads();
-  int my_off[4];  // smem offsets of the 4 features of word w0 (-1: not histogrammed here)
+  // shared-memory byte address of this group's counter block of each feature of word w0
+  const uint32_t sbase = smem_u32(sh);
+  uint32_t abase[4];
 #pragma unroll
-  for (int e = 0; e < 4; e++) my_off[e] = (4 * w0 + e < a.F) ? soff[4 * w0 + e] : -1;
-  int iter = 0;
+  for (int e = 0; e < 4; e++) {
+    const int f = 4 * w0 + e;
+    abase[e] = (f < a.F && soff[f] >= 0) ? sbase + 4u * soff[f] : 0xFFFFFFFFu;
+  }
+  const uint32_t kwp4 = 4u * kwp;
+  uint32_t iter = 0, epoch = 0;
+  int visits = 0;
+  int32_t *my_visits = a.visits + (size_t)blockIdx.x * a.max_visits * 6;
   while (p0 < p1 && s < a.nseg) {
-    const Seg sg = a.segs[s];
-    const uint32_t q0 = p0 - sg.row_base;
-    const uint32_t q1 = min(sg.len, p1 - sg.row_base);
-    const bool hist_on = sg.direct >= 0 && sg.hslot >= 0;
-    const bool part_on = g == 0 && sg.feat >= 0 && sg.write != 0 && a.bins_out != nullptr;
-    if (q0 < q1 && (hist_on || part_on)) {
-      if (hist_on) {
-        for (int i = tid; i < gcount; i += blockDim.x) sh[i] = 0;
-        __syncthreads();
-      }
+    // ---- one node portion: the node's rows at virtual positions [p0, pe) ----
+    const Seg first = a.segs[s];
+    const uint32_t pe = min(p1, first.node_base + first.node_len);
+    const bool hist_on = first.direct >= 0 && first.hslot >= 0;
+    const bool moving = first.feat >= 0 && first.write != 0 && a.bins_out != nullptr;
+    // this CTA's share [A, B) of the portion: it moves these rows
+    const uint32_t L = pe - p0;
+    const uint32_t A = p0 + (uint32_t)(((uint64_t)L * g) / G);
+    const uint32_t B = p0 + (uint32_t)(((uint64_t)L * (g + 1)) / G);
+    if (hist_on)
+      for (int i = tid; i < gcount; i += blockDim.x) sh[i] = 0;
+    if (tid == 0) s_cur[0] = s_cur[1] = 0;
+    __syncthreads();
+    const int s_first = s;
+    for (; s < a.nseg && a.segs[s].row_base < pe; s++) {
+      const Seg sg = a.segs[s];
+      const uint32_t q0 = (p0 > sg.row_base ? p0 - sg.row_base : 0);
+      const uint32_t q1 = min(sg.len, pe - sg.row_base);
       for (uint32_t qb = q0; qb < q1; qb += kUnroll * blockDim.x) {
-        if (clustered && ++iter % kSyncEvery == 0) cluster_sync_all();
+        if (G > 1 && a.sync && ++iter % kSyncEvery == 0) {  // keep the G CTAs within L2 reach
+          __syncthreads();
+          if (tid == 0) {
+            epoch++;
+            atomicAdd(a.sync + range, 1u);
+            while (ld_acquire_gpu(a.sync + range) < epoch * G) __nanosleep(100);
+          }
+          __syncthreads();
+        }
         Row<BS> r[kUnroll];
         int label[kUnroll];
-        bool valid[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; u++) {  // issue all loads first
           const uint32_t q = qb + u * blockDim.x + tid;
-          valid[u] = q < q1;
-          label[u] = 0;
-          if (valid[u]) {
+          label[u] = -1;  // -1: no row
+          if (q < q1) {
             load_row<BS>(a.bins_in + (size_t)(sg.off + q) * BS, r[u]);
             label[u] = a.lab_in[sg.off + q];
+          } else {
+#pragma unroll
+            for (int i = 0; i < Row<BS>::N; i++) r[u].w[i] = 0;
           }
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; u++) {
+          const uint32_t v = sg.row_base + qb + u * blockDim.x + tid;  // virtual position
           bool left = true;
-          if (valid[u] && sg.feat >= 0)
+          if (sg.feat >= 0)
             left = slut[sg.feat * kMaxBins + row_byte<BS>(r[u], sg.feat)] <= sg.thr;
-          if (part_on) {  // a7: move the row into its child's span
-#pragma unroll
-            for (int side = 0; side < 2; side++) {
-              const bool mine = valid[u] && (side == 0 ? left : !left) && ((sg.write >> side) & 1);
-              const unsigned m = __ballot_sync(kFull, mine);
-              if (m) {
-                const int leader = __ffs(m) - 1;
-                uint32_t base = 0;
-                if (lane == leader) base = atomicAdd(a.cursors + 2 * s + side, __popc(m));
-                base = __shfl_sync(kFull, base, leader);
-                if (mine) {
-                  const uint32_t k = base + __popc(m & ((1u << lane) - 1));
-                  const uint32_t pos = side == 0 ? sg.off + k : sg.off + sg.len - 1 - k;
-                  store_row<BS>(a.bins_out + (size_t)pos * BS, r[u]);
-                  __stcs(a.lab_out + pos, (uint8_t)label[u]);
-                }
-              }
+          if (moving) {  // a7, warp-aggregated shared-memory cursors
+            const bool mine = label[u] >= 0 && v >= A && v < B;
+            const unsigned ml = __ballot_sync(kFull, mine && left && (sg.write & 1));
+            const unsigned mr = __ballot_sync(kFull, mine && !left && (sg.write & 2));
+            uint32_t base = 0;
+            if (lane == 0 && ml) base = atomicAdd(&s_cur[0], __popc(ml));
+            if (lane == 1 && mr) base = atomicAdd(&s_cur[1], __popc(mr));
+            const uint32_t bl = __shfl_sync(kFull, base, 0), br = __shfl_sync(kFull, base, 1);
+            const unsigned below = (1u << lane) - 1;
+            const bool wl = (ml >> lane) & 1, wr = (mr >> lane) & 1;
+            if (wl || wr) {
+              const uint32_t pos = wl ? A + bl + __popc(ml & below) : B - 1 - (br + __popc(mr & below));
+              store_row<BS>(a.bins_out + (size_t)pos * BS, r[u]);
+              __stcs(a.lab_out + pos, (uint8_t)label[u]);
             }
           }
-          if (hist_on && valid[u] && (unsigned)(label[u] - k0) < (unsigned)kw &&
-              (sg.direct == 2 || (sg.direct == 0 && left) || (sg.direct == 1 && !left))) {
-            const int lk = label[u] - k0;
+          if (hist_on && label[u] >= 0 && (unsigned)(label[u] - k0) < (unsigned)kw &&
+              (sg.direct == 2 || (sg.direct == 0) == left)) {
             const uint32_t w = pick<Row<BS>::N>(r[u].w, w0);
+            const uint32_t lk4 = 4u * (label[u] - k0);
 #pragma unroll
             for (int e = 0; e < 4; e++)
-              if (my_off[e] >= 0)
-                atomicAdd(&sh[my_off[e] + (int)((w >> (8 * e)) & 0xFF) * kwp + lk], 1u);
+              if (abase[e] != 0xFFFFFFFFu)
+                red_shared_inc(abase[e] + ((w >> (8 * e)) & 0xFF) * kwp4 + lk4);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (moving && tid == 0 && visits < a.max_visits) {  // report this share
+      int32_t *vv = my_visits + 6 * visits;
+      vv[0] = s_first;
+      vv[1] = (int32_t)A;
+      vv[2] = (int32_t)B;
+      vv[3] = (int32_t)s_cur[0];
+      vv[4] = (int32_t)s_cur[1];
+      vv[5] = 0;
+    }
+    if (moving) visits++;
+    if (hist_on) {  // flush: provisional id -> rank, class slab -> classes
+      uint32_t *dst = a.H + (size_t)first.hslot * a.HS;
+      for (int f = 0; f < a.F; f++) {
+        const int o = soff[f];
+        if (o < 0) continue;
+        const int n = sdf[f] * kwp;
+        const uint8_t *lf = slut + f * kMaxBins;
+        uint32_t *df = dst + a.hoff[f];
+        for (int i = tid; i < n; i += blockDim.x) {
+          const uint32_t val = sh[o + i];
+          if (val) {
+            const int pp = i / kwp, j = i - pp * kwp;
+            atomicAdd(df + (int)lf[pp] * C + k0 + j, val);
           }
         }
       }
       __syncthreads();
-      if (hist_on) {  // flush: provisional id -> rank, class slab -> classes
-        uint32_t *dst = a.H + (size_t)sg.hslot * a.HS;
-        for (int f = 0; f < a.F; f++) {
-          const int o = soff[f];
-          if (o < 0) continue;
-          const int n = sdf[f] * kwp;
-          const uint8_t *lf = slut + f * kMaxBins;
-          uint32_t *df = dst + a.hoff[f];
-          for (int i = tid; i < n; i += blockDim.x) {
-            const uint32_t v = sh[o + i];
-            if (v) {
-              const int p = i / kwp, j = i - p * kwp;
-              atomicAdd(df + (int)lf[p] * C + k0 + j, v);
-            }
-          }
-        }
-        __syncthreads();
-      }
     }
-    p0 = sg.row_base + q1;
-    s++;
+    p0 = pe;
   }
-  if (clustered) cluster_sync_all();  // no CTA leaves while a partner may still sync
 }
 
 __global__ void zero_slots_kernel(uint32_t *H, int64_t HS, const int32_t *slots) {
@@ -503,12 +545,10 @@ void launch_hist_pass(const HistPassArgs &a, cudaStream_t s) {
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = a.ngroups;  // the groups of one range run together
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency of a range's CTAs (partner sync)
+  attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = a.clustered ? 1 : 0;
+  cfg.numAttrs = a.sync ? 1 : 0;
   switch (a.BS) {
 #define CASE(B)                                                                              \
   case B:                                                                                    \
