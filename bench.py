@@ -277,7 +277,7 @@ def main():
     alg_bytes = sum(v["bytes"] for v in kern.values()) / args.steps
     cpu = None
     if world == 1 and not args.no_cpu:
-        rows = {"C4": 300_000, "C3": 300_000}.get(args.config, N)
+        rows = {"C4": 600_000, "C3": 1_000_000}.get(args.config, N)
         v, dt = cpu_baseline(cfg, min(rows, N), cfg.D)
         cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
                "sample": f"first {min(rows, N)} rows of {args.config}: labels + depth-{cfg.D} exact "
