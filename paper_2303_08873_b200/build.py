@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libadapt.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["ingest.cu", "train.cu", "select.cu", "engine.cpp"]
+SOURCES = ["ingest.cu", "level.cu", "train.cu", "select.cu", "engine.cpp"]
 
 
 def _git() -> str:
@@ -23,7 +23,8 @@ def _git() -> str:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "common.h"), os.path.join(ROOT, "include", "adapt.h")]
+    deps = srcs + [os.path.join(CSRC, "common.h"), os.path.join(CSRC, "ptx.h"),
+                   os.path.join(ROOT, "include", "adapt.h")]
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= max(map(os.path.getmtime, deps)):
         return SO
     objs = []

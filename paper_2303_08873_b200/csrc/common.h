@@ -30,7 +30,7 @@ struct Error : std::runtime_error {
 void cuda_check(cudaError_t e, const char *what);
 #define CUDA_CHECK(x) ::adapt::cuda_check((x), #x)
 
-// ---- one segment of a level pass (host-built, read by hist_pass_kernel) ----
+// ---- one segment of a row pass (host-built, read by level.cu's kernels) ----
 // A segment is one piece [off, off+len) of a parent node's rows in the level's
 // input planes (a node's rows may lie in several pieces, consecutive in the
 // segment list).  Concatenating the segments gives every row a "virtual
@@ -83,31 +83,43 @@ void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int worl
 void launch_bins_out(const uint8_t *rec, int64_t n, int F, int RS, const uint8_t *lut,
                      uint8_t *out, cudaStream_t s);
 
-// ---- kernel launchers (train.cu) ----
-struct HistPassArgs {
-  const Seg *segs;
+// ---- kernel launchers (level.cu) ----
+struct PartArgs {            // a7: move the split parents' rows into the children's pieces
+  const Seg *segs;           // pieces of the split parents (feat, thr, write set)
+  int nseg;
+  uint32_t total_rows;       // sum of the pieces' lengths (virtual positions)
+  const uint8_t *bins_in, *lab_in;  // input planes: [pos][BS], [pos]
+  uint8_t *bins_out, *lab_out;      // output planes, indexed by virtual position
+  int BS, F;
+  const uint8_t *lut;        // [F][256] id -> rank
+  int32_t *visits;           // [nranges][max_visits][6]: seg, share [A, B), left, right moved
+  int max_visits;
+  int nranges;               // CTAs, one row range each
+};
+int partition_ranges(int sms, uint32_t total_rows);
+void launch_partition(const PartArgs &a, cudaStream_t s);
+
+struct HistArgs {            // a4: class histograms of the given pieces' rows
+  const Seg *segs;           // pieces (off, len, row_base, node_base/len, hslot), grouped by node
   int nseg;
   uint32_t total_rows;
-  const uint8_t *bins_in;    // rows of this level, grouped by node span: [pos][BS]
-  const uint8_t *lab_in;     // [pos]
-  uint8_t *bins_out;         // partitioned rows for the next level (null: root pass)
-  uint8_t *lab_out;
-  int32_t *visits;           // [grid][max_visits][6]: seg, share [A, B), left, right moved
-  int max_visits;
+  const uint8_t *bins_in, *lab_in;
   int BS, F, C;
-  const uint8_t *lut;        // [F][256] prov -> rank
+  const uint8_t *lut;        // [F][256] id -> rank
   const int32_t *hoff;       // [F] counter offset of feature f in a node histogram
   const int32_t *nval;       // [F] distinct values of f
   const int4 *groups;        // [ngroups] x: first class, y: classes, z: padded stride, w: bins word
   const int32_t *gsoff;      // [ngroups][F] smem offset of feature f in group g, -1 if absent
   int ngroups;
-  uint32_t *sync;            // [nranges] partner-sync counters, zeroed (null: no sync)
   int smem_counters;         // max counters of a group
   uint32_t *H;               // [slots][HS]
   int64_t HS;
-  int nranges;               // row ranges; CTA x handles range x / ngroups, group x % ngroups
+  int nranges;               // CTA groups; CTA x handles range x / ngroups, group x % ngroups
+  uint32_t *sync;            // [nranges] partner-sync counters, zeroed (null: no sync)
 };
-void launch_hist_pass(const HistPassArgs &a, cudaStream_t s);
+void launch_hist(const HistArgs &a, cudaStream_t s);
+
+// ---- kernel launchers (train.cu) ----
 void launch_zero_slots(uint32_t *H, int64_t HS, const int32_t *slots, int n, cudaStream_t s);
 void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t HS, const int32_t *triples,
                      int n, cudaStream_t s);

@@ -215,6 +215,7 @@ struct FNode {  // a frontier node: histogrammed and split-searched at this leve
   int32_t tree_idx;
   int32_t depth;
   int32_t slot;  // histogram slot at this level
+  bool direct;   // histogrammed from its rows (else parent - sibling)
   std::vector<std::pair<uint32_t, uint32_t>> pieces;  // this rank's rows: (offset, length) in the planes
 };
 
@@ -248,7 +249,7 @@ struct adapt_region {
   std::vector<int64_t> stats;
   // scratch
   adapt::DevBuf gkey, gid, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, H0, H1, segs,
-      visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, psync, xa, xb, oa, ob;
+      hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, psync, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall;
   // Table-1 shim state
   bool active = false;
@@ -554,7 +555,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
   h2d(h->grp, groups, s);
   h2d(h->gsoff, gsoff, s);
 
-  // 2. level loop (a4-a8)
+  // 2. level loop (a4-a8).  Per level: partition the previous level's split
+  // parents (a7), histogram the smaller child of each (a4) — or the root —,
+  // sum over ranks (a5), derive the siblings, search splits (a6), decide.
   h->tree.clear();
   h->stats.clear();
   adapt_node_t root{};
@@ -565,99 +568,161 @@ void train_region(adapt_region *h, cudaStream_t s) {
   frontier[0].tree_idx = 0;
   frontier[0].depth = 0;
   frontier[0].slot = 0;
+  frontier[0].direct = true;
   frontier[0].pieces = {{0u, (uint32_t)n}};
-  std::vector<Seg> segs{{0, (uint32_t)n, 0, 0, (uint32_t)n, -1, 0, 2, 0, 0}};
+  std::vector<Seg> psegs;           // pieces of the split parents (partition input)
+  std::vector<int2> pseg_children;  // per piece: frontier index of the left / right child
   std::vector<int32_t> direct_slots{0};
   std::vector<int32_t> triples;
-  std::vector<int2> seg_children{make_int2(-1, -1)};  // per seg: frontier index of left / right child
-  // level planes: the root pass reads the ingest output; pass d >= 1 moves the
-  // rows of the split parents from one plane pair into the other
+  // planes: the root is histogrammed from the ingest output; pass d >= 1 moves
+  // the parents' rows from one plane pair into the other
   const uint8_t *bins_in = h->bins.as<uint8_t>(), *lab_in = h->labels.as<uint8_t>();
-  h->binsA.ensure((size_t)std::max<int64_t>(n, 1) * BS);
-  h->binsB.ensure((size_t)std::max<int64_t>(n, 1) * BS);
-  h->labA.ensure((size_t)std::max<int64_t>(n, 1));
-  h->labB.ensure((size_t)std::max<int64_t>(n, 1));
+  h->binsA.ensure((size_t)std::max<int64_t>(n, 1) * BS + 64);
+  h->binsB.ensure((size_t)std::max<int64_t>(n, 1) * BS + 64);
+  h->labA.ensure((size_t)std::max<int64_t>(n, 1) + 64);
+  h->labB.ensure((size_t)std::max<int64_t>(n, 1) + 64);
   int out_plane = 0;  // 0: A, 1: B
   int sms = 148;
   CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g_ctx.device));
   DevBuf *Hcur = &h->H0, *Hprev = &h->H1;
   const int res_stride = (int)((sizeof(NodeRes) + 8 * (size_t)C + 7) / 8 * 8);
-
-  for (int level = 0; !frontier.empty(); level++) {
-    const int A = (int)frontier.size();
-    const int nseg = (int)segs.size();
+  static const bool per_level = getenv("ADAPT_PROFILE_LEVELS") != nullptr;
+  char nm[32];
+  auto virtualize = [](std::vector<Seg> &v, bool by_slot) {  // row_base, node extents
     uint32_t total = 0;
-    for (size_t i = 0; i < segs.size(); i++) {
-      segs[i].row_base = total;
-      total += segs[i].len;
+    for (auto &sg : v) {
+      sg.row_base = total;
+      total += sg.len;
     }
-    for (size_t i = 0; i < segs.size();) {  // node extents in virtual positions
+    for (size_t i = 0; i < v.size();) {
       size_t k = i;
       uint32_t len = 0;
-      while (k < segs.size() && segs[k].hslot == segs[i].hslot) len += segs[k++].len;
+      const int key = by_slot ? v[i].hslot : v[i].direct;  // direct holds the parent id here
+      while (k < v.size() && (by_slot ? v[k].hslot : v[k].direct) == key) len += v[k++].len;
       for (size_t t = i; t < k; t++) {
-        segs[t].node_base = segs[i].row_base;
-        segs[t].node_len = len;
+        v[t].node_base = v[i].row_base;
+        v[t].node_len = len;
       }
       i = k;
     }
+    return total;
+  };
+
+  for (int level = 0; !frontier.empty(); level++) {
+    const int A = (int)frontier.size();
+    const uint8_t *hist_bins = bins_in, *hist_lab = lab_in;
+    int64_t rows_part = 0;
+    if (level > 0) {
+      // ---- a7: move the parents' rows into the children's pieces ----
+      uint8_t *bo = (out_plane ? h->binsB : h->binsA).as<uint8_t>();
+      uint8_t *lo = (out_plane ? h->labB : h->labA).as<uint8_t>();
+      const uint32_t total = virtualize(psegs, false);
+      rows_part = total;
+      PartArgs pa{};
+      pa.segs = nullptr;
+      pa.nseg = (int)psegs.size();
+      pa.total_rows = total;
+      pa.bins_in = bins_in;
+      pa.lab_in = lab_in;
+      pa.bins_out = bo;
+      pa.lab_out = lo;
+      pa.BS = BS;
+      pa.F = F;
+      pa.lut = h->d_lut.as<uint8_t>();
+      pa.nranges = partition_ranges(sms, total);
+      const uint32_t R = (total + pa.nranges - 1) / std::max(1, pa.nranges);
+      int max_visits = 1;  // parents a range can touch
+      for (int r = 0, si = 0; r < pa.nranges && total; r++) {
+        const uint32_t p0 = r * R, p1 = std::min<uint64_t>((uint64_t)p0 + R, total);
+        while (si + 1 < pa.nseg && psegs[si + 1].row_base <= p0) si++;
+        int k = si, nodes = 0, last = -1;
+        while (k < pa.nseg && psegs[k].row_base < p1) {
+          if (psegs[k].direct != last) nodes++, last = psegs[k].direct;
+          k++;
+        }
+        max_visits = std::max(max_visits, nodes);
+      }
+      pa.max_visits = max_visits;
+      const size_t vbytes = (size_t)pa.nranges * max_visits * 6 * 4;
+      h->visits.ensure(vbytes);
+      CUDA_CHECK(cudaMemsetAsync(h->visits.p, 0xFF, vbytes, s));
+      pa.visits = h->visits.as<int32_t>();
+      h2d(h->segs, psegs, s);
+      pa.segs = h->segs.as<Seg>();
+      {
+        snprintf(nm, sizeof nm, "partition_L%02d", level);
+        Phase ph(per_level ? nm : "partition", s, (double)total * 2 * (BS + 1));
+        launch_partition(pa, s);
+      }
+      h->hres.ensure(vbytes);
+      int32_t *hv = h->hres.as<int32_t>();
+      CUDA_CHECK(cudaMemcpyAsync(hv, h->visits.p, vbytes, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      // children's pieces, from the CTAs' share reports
+      for (auto &fn : frontier) fn.pieces.clear();
+      for (int b = 0; b < pa.nranges; b++)
+        for (int v = 0; v < max_visits; v++) {
+          const int32_t *e = hv + ((size_t)b * max_visits + v) * 6;
+          if (e[0] < 0) break;
+          const int2 ch = pseg_children[e[0]];
+          if (ch.x >= 0 && e[3] > 0) frontier[ch.x].pieces.push_back({(uint32_t)e[1], (uint32_t)e[3]});
+          if (ch.y >= 0 && e[4] > 0)
+            frontier[ch.y].pieces.push_back({(uint32_t)(e[2] - e[4]), (uint32_t)e[4]});
+        }
+      for (auto &fn : frontier) std::sort(fn.pieces.begin(), fn.pieces.end());
+      hist_bins = bo;
+      hist_lab = lo;
+    }
+    // ---- a4: histograms of the direct nodes (the root, or the smaller children) ----
+    std::vector<Seg> hsegs;
+    for (const auto &fn : frontier)
+      if (fn.direct)
+        for (const auto &pc : fn.pieces) {
+          Seg sg{};
+          sg.off = pc.first;
+          sg.len = pc.second;
+          sg.hslot = fn.slot;
+          hsegs.push_back(sg);
+        }
+    const uint32_t htotal = virtualize(hsegs, true);
     Hcur->ensure((size_t)A * HS * 4);
-    h2d(h->segs, segs, s);
     h2d(h->slots, direct_slots, s);
     {
       Phase ph("zero", s, 0);
       launch_zero_slots(Hcur->as<uint32_t>(), HS, h->slots.as<int32_t>(), (int)direct_slots.size(), s);
     }
-    HistPassArgs a{};
-    a.segs = h->segs.as<Seg>();
-    a.nseg = nseg;
-    a.total_rows = total;
-    a.bins_in = bins_in;
-    a.lab_in = lab_in;
-    a.bins_out = level == 0 ? nullptr : (out_plane ? h->binsB : h->binsA).as<uint8_t>();
-    a.lab_out = level == 0 ? nullptr : (out_plane ? h->labB : h->labA).as<uint8_t>();
-    a.BS = BS;
-    a.F = F;
-    a.C = C;
-    a.lut = h->d_lut.as<uint8_t>();
-    a.hoff = h->hoff.as<int32_t>();
-    a.nval = h->dnval.as<int32_t>();
-    a.groups = h->grp.as<int4>();
-    a.gsoff = h->gsoff.as<int32_t>();
-    a.ngroups = ngroups;
-    a.smem_counters = max_group;
-    a.H = Hcur->as<uint32_t>();
-    a.HS = HS;
-    // one CTA per SM; the ngroups CTAs of a range are co-resident (cooperative launch)
-    a.nranges = (int)std::max<int64_t>(
-        1, std::min<int64_t>((total + 4095) / 4096, std::max(1, sms / ngroups)));
-    a.sync = nullptr;
-    if (ngroups > 1 && a.nranges * ngroups <= sms) {
-      h->psync.ensure((size_t)a.nranges * 4);
-      CUDA_CHECK(cudaMemsetAsync(h->psync.p, 0, (size_t)a.nranges * 4, s));
-      a.sync = h->psync.as<uint32_t>();
-    }
-    // segments a range can touch: the visit-report capacity per CTA
-    const uint32_t R = (total + a.nranges - 1) / std::max(1, a.nranges);
-    int max_visits = 1;
-    for (int r = 0, si = 0; r < a.nranges; r++) {
-      const uint32_t p0 = r * R, p1 = std::min<uint64_t>((uint64_t)p0 + R, total);
-      while (si + 1 < nseg && segs[si + 1].row_base <= p0) si++;
-      int k = si;
-      while (k < nseg && segs[k].row_base < p1) k++;
-      max_visits = std::max(max_visits, k - si);
-    }
-    const int grid = a.nranges * ngroups;
-    a.max_visits = max_visits;
-    h->visits.ensure((size_t)grid * max_visits * 6 * 4);
-    CUDA_CHECK(cudaMemsetAsync(h->visits.p, 0xFF, (size_t)grid * max_visits * 6 * 4, s));
-    a.visits = h->visits.as<int32_t>();
-    {
-      static const bool per_level = getenv("ADAPT_PROFILE_LEVELS") != nullptr;
-      char nm[24];
+    if (htotal > 0) {
+      HistArgs ha{};
+      h2d(h->hsegs, hsegs, s);
+      ha.segs = h->hsegs.as<Seg>();
+      ha.nseg = (int)hsegs.size();
+      ha.total_rows = htotal;
+      ha.bins_in = hist_bins;
+      ha.lab_in = hist_lab;
+      ha.BS = BS;
+      ha.F = F;
+      ha.C = C;
+      ha.lut = h->d_lut.as<uint8_t>();
+      ha.hoff = h->hoff.as<int32_t>();
+      ha.nval = h->dnval.as<int32_t>();
+      ha.groups = h->grp.as<int4>();
+      ha.gsoff = h->gsoff.as<int32_t>();
+      ha.ngroups = ngroups;
+      ha.smem_counters = max_group;
+      ha.H = Hcur->as<uint32_t>();
+      ha.HS = HS;
+      // one CTA per SM; the ngroups CTAs of a range are co-resident (cooperative launch)
+      ha.nranges = (int)std::max<int64_t>(1, std::min<int64_t>((htotal + 4095) / 4096,
+                                                               std::max(1, sms / ngroups)));
+      ha.sync = nullptr;
+      if (ngroups > 1 && ha.nranges * ngroups <= sms) {
+        h->psync.ensure((size_t)ha.nranges * 4);
+        CUDA_CHECK(cudaMemsetAsync(h->psync.p, 0, (size_t)ha.nranges * 4, s));
+        ha.sync = h->psync.as<uint32_t>();
+      }
       snprintf(nm, sizeof nm, "hist_L%02d", level);
-      Phase ph(per_level ? nm : "hist", s, (double)total * (F + 1));
-      launch_hist_pass(a, s);
+      Phase ph(per_level ? nm : "hist", s, (double)htotal * (F + 1));
+      launch_hist(ha, s);
     }
     if (world > 1 && !direct_slots.empty())
       g_nccl.check(g_nccl.AllReduce(Hcur->p, Hcur->p, (size_t)direct_slots.size() * HS,
@@ -674,8 +739,6 @@ void train_region(adapt_region *h, cudaStream_t s) {
     h->cand.ensure((size_t)A * F * sizeof(SplitCand));
     h->res.ensure((size_t)A * res_stride);
     {
-      static const bool per_level = getenv("ADAPT_PROFILE_LEVELS") != nullptr;
-      char nm[24];
       snprintf(nm, sizeof nm, "split_L%02d", level);
       Phase ph(per_level ? nm : "split", s, 0);
       launch_split(Hcur->as<uint32_t>(), HS, h->nslot.as<int32_t>(), A, F, C, h->hoff.as<int32_t>(),
@@ -687,41 +750,20 @@ void train_region(adapt_region *h, cudaStream_t s) {
                     h->hoff.as<int32_t>(), h->dnval.as<int32_t>(), h->cand.as<SplitCand>(),
                     h->res.as<uint8_t>(), res_stride, s);
     }
-    const size_t vbytes = (size_t)grid * max_visits * 6 * 4;
-    h->hres.ensure((size_t)A * res_stride + vbytes);
+    h->hres.ensure((size_t)A * res_stride);
     uint8_t *hr = h->hres.as<uint8_t>();
     CUDA_CHECK(cudaMemcpyAsync(hr, h->res.p, (size_t)A * res_stride, cudaMemcpyDeviceToHost, s));
-    int32_t *hv = reinterpret_cast<int32_t *>(hr + (size_t)A * res_stride);
-    if (level > 0) CUDA_CHECK(cudaMemcpyAsync(hv, h->visits.p, vbytes, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
-
-    // pieces of this level's frontier nodes, from the CTAs' sub-portion reports
-    int64_t rows_hist = level == 0 ? total : 0;
-    if (level > 0) {
-      for (auto &fn : frontier) fn.pieces.clear();
-      for (int b = 0; b < grid; b++)
-        for (int v = 0; v < max_visits; v++) {
-          const int32_t *e = hv + ((size_t)b * max_visits + v) * 6;
-          if (e[0] < 0) break;
-          const Seg &sg = segs[e[0]];
-          const int2 ch = seg_children[e[0]];
-          if (ch.x >= 0 && e[3] > 0) frontier[ch.x].pieces.push_back({(uint32_t)e[1], (uint32_t)e[3]});
-          if (ch.y >= 0 && e[4] > 0)
-            frontier[ch.y].pieces.push_back({(uint32_t)(e[2] - e[4]), (uint32_t)e[4]});
-          rows_hist += sg.direct == 0 ? e[3] : (sg.direct == 1 ? e[4] : 0);
-        }
-      for (auto &fn : frontier) std::sort(fn.pieces.begin(), fn.pieces.end());
-    }
     h->stats.push_back(A);
-    h->stats.push_back(rows_hist);
-    h->stats.push_back(level == 0 ? 0 : total);
+    h->stats.push_back(htotal);
+    h->stats.push_back(rows_part);
 
-    // decide every frontier node; build the next level
+    // ---- decide every frontier node; build the next level ----
     std::vector<FNode> next;
     std::vector<Seg> nsegs;
+    std::vector<int2> nchildren;
     std::vector<int32_t> ndirect, nderived_par, nderived_sib;
     std::vector<int> nderived_j;
-    std::vector<int2> nchildren;
     std::vector<uint64_t> P(C), PL(C), PR(C);
     for (int j = 0; j < A; j++) {
       const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + (size_t)j * res_stride);
@@ -764,25 +806,25 @@ void train_region(adapt_region *h, cudaStream_t s) {
       int jl = -1, jr = -1;
       if (inL) {
         jl = (int)next.size();
-        next.push_back(FNode{li, fn.depth + 1, dir == 0 ? hslot : -1, {}});
+        next.push_back(FNode{li, fn.depth + 1, dir == 0 ? hslot : -1, dir == 0, {}});
       }
       if (inR) {
         jr = (int)next.size();
-        next.push_back(FNode{li + 1, fn.depth + 1, dir == 1 ? hslot : -1, {}});
+        next.push_back(FNode{li + 1, fn.depth + 1, dir == 1 ? hslot : -1, dir == 1, {}});
       }
       if (inL && inR) {  // the other child by subtraction from the parent
         nderived_j.push_back(dir == 0 ? jr : jl);
         nderived_par.push_back(fn.slot);
         nderived_sib.push_back(hslot);
       }
-      for (const auto &pc : fn.pieces) {  // one segment per piece of the parent
+      for (const auto &pc : fn.pieces) {  // one partition segment per piece of the parent
         Seg sg{};
         sg.off = pc.first;
         sg.len = pc.second;
         sg.feat = f;
         sg.thr = nr->b_lo;
         sg.write = (inL ? 1 : 0) | (inR ? 2 : 0);
-        sg.direct = dir;
+        sg.direct = j;  // parent id (groups a parent's pieces)
         sg.hslot = hslot;
         nsegs.push_back(sg);
         nchildren.push_back(make_int2(jl, jr));
@@ -798,12 +840,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
       triples.push_back(nderived_sib[i]);
     }
     frontier.swap(next);
-    segs.swap(nsegs);
-    seg_children.swap(nchildren);
+    psegs.swap(nsegs);
+    pseg_children.swap(nchildren);
     direct_slots.swap(ndirect);
     std::swap(Hcur, Hprev);
-    // the planes just written are the input of the next pass; the root pass
-    // moves nothing, so level 1 still reads the ingest output
+    // the planes just written are the input of the next partition; the root
+    // level moved nothing, so level 1 still reads the ingest output
     if (level > 0) {
       bins_in = (out_plane ? h->binsB : h->binsA).as<uint8_t>();
       lab_in = (out_plane ? h->labB : h->labA).as<uint8_t>();

@@ -1,0 +1,378 @@
+// level.cu — the row passes of one tree level.
+//
+//   partition_kernel  a7: the rows of every split parent are moved from the
+//                     input planes into the output planes.  Each CTA owns a
+//                     contiguous range of the level's "virtual positions"
+//                     (segments = pieces of the parents' rows, concatenated);
+//                     inside it, a parent's rows go to [A, ..) if they go left
+//                     and (.., B] if right, where [A, B) is the parent's share
+//                     of the range, positions from warp-aggregated shared-
+//                     memory cursors.  Each CTA reports (parent, A, B, left,
+//                     right) — the children's pieces for the next level.
+//   hist_kernel       a4: class histogram H[node][f][rank][class] of the rows
+//                     of the pieces it is given (the root, or the smaller
+//                     child of every split).  A node's histogram (Σ_f D_f × C
+//                     u32 counters, 508 KB at C4) does not fit one SM, so G
+//                     CTAs share each row range: CTA g owns the 4 features of
+//                     32-bit word w(g) of the bins row (× a class slab), i.e.
+//                     at most 4 shared-memory reductions per row.  The G CTAs
+//                     of a range are co-resident (cooperative launch, one CTA
+//                     per SM) and re-synchronise every few iterations, so a
+//                     row fetched from HBM by one is served to the others
+//                     from L2.  Counters are indexed by provisional bin id
+//                     with an odd class stride (bank spread); the id -> rank
+//                     map is applied once per counter when a node is flushed.
+// Every quantity that decides the tree is an integer, so the result does not
+// depend on row order, on the number of ranks or on atomic ordering.
+#include <algorithm>
+
+#include "common.h"
+#include "ptx.h"
+
+namespace adapt {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int BS>
+struct Row {  // one row's bins, BS bytes, in registers
+  static constexpr int N = BS >= 4 ? BS / 4 : 1;
+  uint32_t w[N];
+};
+
+template <int BS>
+__device__ __forceinline__ void load_row(const uint8_t *__restrict__ p, Row<BS> &r) {
+  if constexpr (BS >= 16) {
+#pragma unroll
+    for (int i = 0; i < BS / 16; i++) {
+      const uint4 v = *(reinterpret_cast<const uint4 *>(p) + i);
+      r.w[4 * i + 0] = v.x;
+      r.w[4 * i + 1] = v.y;
+      r.w[4 * i + 2] = v.z;
+      r.w[4 * i + 3] = v.w;
+    }
+  } else if constexpr (BS == 8) {
+    const uint2 v = *reinterpret_cast<const uint2 *>(p);
+    r.w[0] = v.x;
+    r.w[1] = v.y;
+  } else if constexpr (BS == 4) {
+    r.w[0] = *reinterpret_cast<const unsigned int *>(p);
+  } else if constexpr (BS == 2) {
+    r.w[0] = *reinterpret_cast<const unsigned short *>(p);
+  } else {
+    r.w[0] = *p;
+  }
+}
+
+template <int BS>
+__device__ __forceinline__ void store_row(uint8_t *__restrict__ p, const Row<BS> &r) {
+  if constexpr (BS >= 16) {
+#pragma unroll
+    for (int i = 0; i < BS / 16; i++)
+      __stcs(reinterpret_cast<uint4 *>(p) + i,
+             make_uint4(r.w[4 * i], r.w[4 * i + 1], r.w[4 * i + 2], r.w[4 * i + 3]));
+  } else if constexpr (BS == 8) {
+    __stcs(reinterpret_cast<uint2 *>(p), make_uint2(r.w[0], r.w[1]));
+  } else if constexpr (BS == 4) {
+    __stcs(reinterpret_cast<unsigned int *>(p), r.w[0]);
+  } else if constexpr (BS == 2) {
+    *reinterpret_cast<unsigned short *>(p) = (unsigned short)r.w[0];
+  } else {
+    *p = (uint8_t)r.w[0];
+  }
+}
+
+// w[i] for a runtime i through a tree of register selects (N = power of 2):
+// every array access has a compile-time index, so nothing goes to local memory
+template <int N>
+__device__ __forceinline__ uint32_t pick(const uint32_t *w, int i) {
+  if constexpr (N == 1) {
+    return w[0];
+  } else {
+    constexpr int H = N / 2;
+    const uint32_t lo = pick<H>(w, i & (H - 1));
+    const uint32_t hi = pick<H>(w + H, i & (H - 1));
+    return (i & H) ? hi : lo;
+  }
+}
+
+template <int BS>
+__device__ __forceinline__ int row_byte(const Row<BS> &r, int f) {
+  return (int)((pick<Row<BS>::N>(r.w, f >> 2) >> (8 * (f & 3))) & 0xFFu);
+}
+
+__device__ __forceinline__ void red_shared_inc(uint32_t addr) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ int first_seg(const Seg *segs, int nseg, uint32_t p) {
+  int lo = 0, hi = nseg - 1;  // last segment with row_base <= p
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].row_base <= p) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------ partition --
+constexpr int kPartThreads = 512;
+constexpr int kPartUnroll = 4;
+
+template <int BS>
+__global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) {
+  extern __shared__ uint8_t slut[];  // [F][256] id -> rank
+  __shared__ uint32_t s_cur[2];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < a.F * kMaxBins / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t *>(slut)[i] = reinterpret_cast<const uint32_t *>(a.lut)[i];
+  const uint32_t R = (a.total_rows + gridDim.x - 1) / gridDim.x;
+  uint32_t p0 = blockIdx.x * R;
+  const uint32_t p1 = min(p0 + R, a.total_rows);
+  int s = p0 < p1 ? first_seg(a.segs, a.nseg, p0) : a.nseg;
+  int32_t *my_visits = a.visits + (size_t)blockIdx.x * a.max_visits * 6;
+  int visits = 0;
+  __syncthreads();
+  while (p0 < p1 && s < a.nseg) {
+    // ---- one parent's rows at virtual positions [p0, pe): its share [A, B) = [p0, pe) ----
+    const Seg first = a.segs[s];
+    const uint32_t pe = min(p1, first.node_base + first.node_len);
+    const uint32_t A = p0, B = pe;
+    if (tid == 0) s_cur[0] = s_cur[1] = 0;
+    __syncthreads();
+    const int s_first = s;
+    for (; s < a.nseg && a.segs[s].row_base < pe; s++) {
+      const Seg sg = a.segs[s];
+      const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
+      const uint32_t q1 = min(sg.len, pe - sg.row_base);
+      const uint8_t *lf = slut + sg.feat * kMaxBins;
+      for (uint32_t qb = q0; qb < q1; qb += kPartUnroll * blockDim.x) {
+        Row<BS> r[kPartUnroll];
+        int label[kPartUnroll];
+#pragma unroll
+        for (int u = 0; u < kPartUnroll; u++) {  // all loads first
+          const uint32_t q = qb + u * blockDim.x + tid;
+          label[u] = -1;
+          if (q < q1) {
+            load_row<BS>(a.bins_in + (size_t)(sg.off + q) * BS, r[u]);
+            label[u] = __ldcs(a.lab_in + sg.off + q);
+          } else {
+#pragma unroll
+            for (int i = 0; i < Row<BS>::N; i++) r[u].w[i] = 0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kPartUnroll; u++) {
+          const bool valid = label[u] >= 0;
+          const bool left = lf[row_byte<BS>(r[u], sg.feat)] <= sg.thr;
+          const unsigned ml = __ballot_sync(kFull, valid && left && (sg.write & 1));
+          const unsigned mr = __ballot_sync(kFull, valid && !left && (sg.write & 2));
+          uint32_t base = 0;
+          if (lane == 0 && ml) base = atomicAdd(&s_cur[0], __popc(ml));
+          if (lane == 1 && mr) base = atomicAdd(&s_cur[1], __popc(mr));
+          const uint32_t bl = __shfl_sync(kFull, base, 0), br = __shfl_sync(kFull, base, 1);
+          const unsigned below = (1u << lane) - 1;
+          const bool wl = (ml >> lane) & 1, wr = (mr >> lane) & 1;
+          if (wl || wr) {
+            const uint32_t pos = wl ? A + bl + __popc(ml & below) : B - 1 - (br + __popc(mr & below));
+            store_row<BS>(a.bins_out + (size_t)pos * BS, r[u]);
+            __stcs(a.lab_out + pos, (uint8_t)label[u]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && visits < a.max_visits) {  // report this parent's share
+      int32_t *v = my_visits + 6 * visits;
+      v[0] = s_first;
+      v[1] = (int32_t)A;
+      v[2] = (int32_t)B;
+      v[3] = (int32_t)s_cur[0];
+      v[4] = (int32_t)s_cur[1];
+      v[5] = 0;
+    }
+    visits++;
+    p0 = pe;
+  }
+}
+
+// ------------------------------------------------------------ histogram --
+constexpr int kHistThreads = 1024;
+constexpr int kHistUnroll = 4;
+constexpr int kSyncEvery = 8;
+
+template <int BS>
+__global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
+  extern __shared__ uint32_t sh[];  // [smem_counters] counters | lut [F*256] bytes
+  uint8_t *slut = reinterpret_cast<uint8_t *>(sh + a.smem_counters);
+  __shared__ int32_t soff[kMaxF];   // this group's smem offset of feature f, -1 if absent
+  __shared__ int32_t sdf[kMaxF];    // distinct values of f
+  const int tid = threadIdx.x;
+  const int G = a.ngroups;
+  const int g = blockIdx.x % G;
+  const int range = blockIdx.x / G;
+  const int4 grp = a.groups[g];  // x: first class, y: classes, z: padded class stride, w: word
+  const int k0 = grp.x, kw = grp.y, kwp = grp.z, w0 = grp.w;
+  const int C = a.C;
+  for (int i = tid; i < a.F * kMaxBins / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t *>(slut)[i] = reinterpret_cast<const uint32_t *>(a.lut)[i];
+  int gcount = 0;
+  for (int f = 0; f < a.F; f++) {
+    const int o = a.gsoff[g * a.F + f];
+    if (tid == 0) {
+      soff[f] = o;
+      sdf[f] = a.nval[f];
+    }
+    if (o >= 0) gcount = max(gcount, o + a.nval[f] * kwp);
+  }
+  const uint32_t R = (a.total_rows + a.nranges - 1) / a.nranges;
+  uint32_t p0 = range * R;
+  const uint32_t p1 = min(p0 + R, a.total_rows);
+  int s = p0 < p1 ? first_seg(a.segs, a.nseg, p0) : a.nseg;
+  __syncthreads();
+  // shared-memory byte address of this group's counter block of each feature of word w0
+  const uint32_t sbase = smem_u32(sh);
+  uint32_t abase[4];
+#pragma unroll
+  for (int e = 0; e < 4; e++) {
+    const int f = 4 * w0 + e;
+    abase[e] = (f < a.F && soff[f] >= 0) ? sbase + 4u * soff[f] : 0xFFFFFFFFu;
+  }
+  const bool all4 = abase[0] != 0xFFFFFFFFu && abase[1] != 0xFFFFFFFFu &&
+                    abase[2] != 0xFFFFFFFFu && abase[3] != 0xFFFFFFFFu;
+  const uint32_t kwp4 = 4u * kwp;
+  uint32_t iter = 0, epoch = 0;
+  while (p0 < p1 && s < a.nseg) {
+    // ---- one node's rows at virtual positions [p0, pe) ----
+    const Seg first = a.segs[s];
+    const uint32_t pe = min(p1, first.node_base + first.node_len);
+    for (int i = tid; i < gcount; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (; s < a.nseg && a.segs[s].row_base < pe; s++) {
+      const Seg sg = a.segs[s];
+      const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
+      const uint32_t q1 = min(sg.len, pe - sg.row_base);
+      for (uint32_t qb = q0; qb < q1; qb += kHistUnroll * blockDim.x) {
+        if (a.sync && ++iter % kSyncEvery == 0) {  // keep the G CTAs within L2 reach
+          __syncthreads();
+          if (tid == 0) {
+            epoch++;
+            atomicAdd(a.sync + range, 1u);
+            while (ld_acquire_gpu(a.sync + range) < epoch * G) __nanosleep(64);
+          }
+          __syncthreads();
+        }
+        uint32_t w[kHistUnroll];
+        int label[kHistUnroll];
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; u++) {  // all loads first: only this CTA's word
+          const uint32_t q = qb + u * blockDim.x + tid;
+          label[u] = -1;
+          w[u] = 0;
+          if (q < q1) {
+            const uint8_t *p = a.bins_in + (size_t)(sg.off + q) * BS;
+            if constexpr (BS >= 4) w[u] = reinterpret_cast<const uint32_t *>(p)[w0];
+            else if constexpr (BS == 2) w[u] = *reinterpret_cast<const unsigned short *>(p);
+            else w[u] = *p;
+            label[u] = a.lab_in[sg.off + q];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; u++) {
+          if ((unsigned)(label[u] - k0) >= (unsigned)kw) continue;  // no row / other slab
+          const uint32_t lk4 = 4u * (label[u] - k0);
+          if (all4) {
+            red_shared_inc(abase[0] + ((w[u]) & 0xFF) * kwp4 + lk4);
+            red_shared_inc(abase[1] + ((w[u] >> 8) & 0xFF) * kwp4 + lk4);
+            red_shared_inc(abase[2] + ((w[u] >> 16) & 0xFF) * kwp4 + lk4);
+            red_shared_inc(abase[3] + (w[u] >> 24) * kwp4 + lk4);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; e++)
+              if (abase[e] != 0xFFFFFFFFu)
+                red_shared_inc(abase[e] + ((w[u] >> (8 * e)) & 0xFF) * kwp4 + lk4);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    {  // flush: provisional id -> rank, class slab -> classes
+      uint32_t *dst = a.H + (size_t)first.hslot * a.HS;
+      for (int f = 0; f < a.F; f++) {
+        const int o = soff[f];
+        if (o < 0) continue;
+        const int n = sdf[f] * kwp;
+        const uint8_t *lf = slut + f * kMaxBins;
+        uint32_t *df = dst + a.hoff[f];
+        for (int i = tid; i < n; i += blockDim.x) {
+          const uint32_t val = sh[o + i];
+          if (val) {
+            const int pp = i / kwp, j = i - pp * kwp;
+            atomicAdd(df + (int)lf[pp] * C + k0 + j, val);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    p0 = pe;
+  }
+}
+
+}  // namespace
+
+int partition_ranges(int sms, uint32_t total_rows) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((total_rows + 4095) / 4096, 2 * sms));
+}
+
+void launch_partition(const PartArgs &a, cudaStream_t s) {
+  if (a.total_rows == 0 || a.nseg == 0) return;
+  const size_t smem = (size_t)a.F * kMaxBins;
+  switch (a.BS) {
+#define CASE(B)                                                                               \
+  case B:                                                                                     \
+    CUDA_CHECK(cudaFuncSetAttribute(partition_kernel<B>,                                      \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
+    partition_kernel<B><<<a.nranges, kPartThreads, smem, s>>>(a);                             \
+    break;
+    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
+#undef CASE
+    default:
+      throw Error(-1, "bad bins stride");
+  }
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_hist(const HistArgs &a, cudaStream_t s) {
+  if (a.total_rows == 0 || a.nseg == 0) return;
+  const size_t smem = (size_t)a.smem_counters * 4 + (size_t)a.F * kMaxBins;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.nranges * a.ngroups);
+  cfg.blockDim = dim3(kHistThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency of a range's CTAs (partner sync)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.sync ? 1 : 0;
+  switch (a.BS) {
+#define CASE(B)                                                                              \
+  case B:                                                                                    \
+    CUDA_CHECK(cudaFuncSetAttribute(hist_kernel<B>,                                          \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, hist_kernel<B>, a));                                 \
+    break;
+    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
+#undef CASE
+    default:
+      throw Error(-1, "bad bins stride");
+  }
+  CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace adapt
