@@ -36,7 +36,7 @@ WORKLOADS = {
     "C2": "C2 region 0: 3.3e4-row table, 4 features, 7 variants (num_threads), depth 8",
     "C1": "C1: 512 profiled samples, 1 feature (trip count), host vs GPU offload, depth 4",
 }
-KERNEL_PHASES = ("ingest", "values", "merge", "zero", "partition", "hist", "subtract", "split", "winner",
+KERNEL_PHASES = ("discover", "ingest", "values", "merge", "zero", "partition", "hist", "subtract", "split", "winner",
                  "select")
 
 

@@ -72,16 +72,18 @@ struct NodeRes {
 };
 
 // ---- kernel launchers (ingest.cu) ----
-void launch_ingest(const float *feat, const float *times, int64_t n, int F, int V, int BS,
-                   uint32_t *gkey, uint32_t *gid, uint32_t *gcount, uint32_t *flags,
-                   uint8_t *bins, uint8_t *labels, cudaStream_t s);
-void launch_collect_values(const uint32_t *gkey, const uint32_t *gid, const uint32_t *gcount,
-                           int F, float *local_vals, int32_t *local_cnt, cudaStream_t s);
-void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int world, int rank,
-                         int F, float *val, int32_t *nval, uint8_t *lut, uint32_t *flags,
-                         cudaStream_t s);
-void launch_bins_out(const uint8_t *rec, int64_t n, int F, int RS, const uint8_t *lut,
-                     uint8_t *out, cudaStream_t s);
+int lookup_table_bytes(int F);  // size of the per-feature key -> rank perfect hashes
+void launch_discover(const float *feat, int64_t n, int F, uint32_t *gkey, uint32_t *gcount,
+                     uint32_t *flags, cudaStream_t s);
+void launch_collect_values(const uint32_t *gkey, const uint32_t *gcount, int F, float *local_vals,
+                           int32_t *local_cnt, cudaStream_t s);
+void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int world, int F,
+                         float *val, int32_t *nval, uint32_t *flags, cudaStream_t s);
+bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab);
+void launch_label_bin(const float *feat, const float *times, int64_t n, int F, int V, int BS,
+                      const uint8_t *tab, const uint32_t *lk_mul, uint32_t *flags, uint8_t *bins,
+                      uint8_t *labels, cudaStream_t s);
+void launch_bins_out(const uint8_t *bins, int64_t n, int F, int BS, uint8_t *out, cudaStream_t s);
 
 // ---- kernel launchers (level.cu) ----
 struct PartArgs {            // a7: move the split parents' rows into the children's pieces
@@ -91,7 +93,6 @@ struct PartArgs {            // a7: move the split parents' rows into the childr
   const uint8_t *bins_in, *lab_in;  // input planes: [pos][BS], [pos]
   uint8_t *bins_out, *lab_out;      // output planes, indexed by virtual position
   int BS, F;
-  const uint8_t *lut;        // [F][256] id -> rank
   int32_t *visits;           // [nranges][max_visits][6]: seg, share [A, B), left, right moved
   int max_visits;
   int nranges;               // CTAs, one row range each
@@ -105,7 +106,6 @@ struct HistArgs {            // a4: class histograms of the given pieces' rows
   uint32_t total_rows;
   const uint8_t *bins_in, *lab_in;
   int BS, F, C;
-  const uint8_t *lut;        // [F][256] id -> rank
   const int32_t *hoff;       // [F] counter offset of feature f in a node histogram
   const int32_t *nval;       // [F] distinct values of f
   const int4 *groups;        // [ngroups] x: first class, y: classes, z: padded stride, w: bins word

@@ -241,14 +241,13 @@ struct adapt_region {
   adapt::DevBuf binsA, binsB, labA, labB;  // level planes, rows grouped by node span
   std::vector<float> val;       // [F][256]
   std::vector<int32_t> nval;    // [F]
-  std::vector<uint8_t> lut;     // [F][256]
-  adapt::DevBuf d_lut;
   std::vector<adapt_node_t> tree;
   adapt::DevBuf d_tree;
   bool trained = false;
   std::vector<int64_t> stats;
   // scratch
-  adapt::DevBuf gkey, gid, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, H0, H1, segs,
+  adapt::DevBuf gkey, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, lk_keys, lk_mul,
+      H0, H1, segs,
       hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, psync, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall;
   // Table-1 shim state
@@ -396,7 +395,7 @@ void h2d(DevBuf &b, const std::vector<T> &v, cudaStream_t s) {
 // ------------------------------------------------------------ training --
 void train_region(adapt_region *h, cudaStream_t s) {
   const int F = h->F, V = h->V, C = V, D = h->D;
-  const int world = g_ctx.world, rank = g_ctx.rank;
+  const int world = g_ctx.world;
   // 0. source table (wide, or long records aggregated on the host)
   const float *feat = h->d_feat, *times = h->d_times;
   int64_t n = h->n;
@@ -430,61 +429,54 @@ void train_region(adapt_region *h, cudaStream_t s) {
   while (BS < F) BS <<= 1;
   h->BS = BS;
 
-  // 1. a1 + a2 + a3: one pass over the table
+  // 1. a2 discovery pass, value tables merged over ranks, then a1 + a3 in one
+  //    pass over (times, features); bins are ranks in the merged value table
   h->gkey.ensure((size_t)F * kGSlots * 4);
-  h->gid.ensure((size_t)F * kGSlots * 4);
   h->gcount.ensure((size_t)F * 4);
   h->flags.ensure(16);
-  h->bins.ensure((size_t)std::max<int64_t>(n, 1) * BS);
-  h->labels.ensure((size_t)std::max<int64_t>(n, 1));
+  h->bins.ensure((size_t)std::max<int64_t>(n, 1) * BS + 64);
+  h->labels.ensure((size_t)std::max<int64_t>(n, 1) + 64);
   CUDA_CHECK(cudaMemsetAsync(h->gkey.p, 0xFF, (size_t)F * kGSlots * 4, s));
-  CUDA_CHECK(cudaMemsetAsync(h->gid.p, 0xFF, (size_t)F * kGSlots * 4, s));
   CUDA_CHECK(cudaMemsetAsync(h->gcount.p, 0, (size_t)F * 4, s));
   CUDA_CHECK(cudaMemsetAsync(h->flags.p, 0, 16, s));
   {
-    Phase ph("ingest", s, (double)n * (4.0 * F + 4.0 * V + F + 1));  // algorithmic (SURVEY §8(d))
-    launch_ingest(feat, times, n, F, V, BS, h->gkey.as<uint32_t>(), h->gid.as<uint32_t>(),
-                  h->gcount.as<uint32_t>(), h->flags.as<uint32_t>(), h->bins.as<uint8_t>(),
-                  h->labels.as<uint8_t>(), s);
+    Phase ph("discover", s, (double)n * 4.0 * F);
+    launch_discover(feat, n, F, h->gkey.as<uint32_t>(), h->gcount.as<uint32_t>(),
+                    h->flags.as<uint32_t>(), s);
   }
-  // a2: value tables, merged over ranks
   h->lvals.ensure((size_t)F * kMaxBins * 4);
   h->lcnt.ensure((size_t)F * 4);
   h->avals.ensure((size_t)world * F * kMaxBins * 4);
   h->acnt.ensure((size_t)world * F * 4);
   h->dval.ensure((size_t)F * kMaxBins * 4);
   h->dnval.ensure((size_t)F * 4);
-  h->d_lut.ensure((size_t)F * kMaxBins);
   CUDA_CHECK(cudaMemsetAsync(h->lvals.p, 0, (size_t)F * kMaxBins * 4, s));
-  CUDA_CHECK(cudaMemsetAsync(h->d_lut.p, 0, (size_t)F * kMaxBins, s));
   CUDA_CHECK(cudaMemsetAsync(h->dval.p, 0, (size_t)F * kMaxBins * 4, s));
   {
     Phase ph("values", s, 0);
-    launch_collect_values(h->gkey.as<uint32_t>(), h->gid.as<uint32_t>(), h->gcount.as<uint32_t>(),
-                          F, h->lvals.as<float>(), h->lcnt.as<int32_t>(), s);
+    launch_collect_values(h->gkey.as<uint32_t>(), h->gcount.as<uint32_t>(), F,
+                          h->lvals.as<float>(), h->lcnt.as<int32_t>(), s);
+  }
+  if (world > 1) {
+    g_nccl.check(g_nccl.AllGather(h->lvals.p, h->avals.p, (size_t)F * kMaxBins, ncclFloat32,
+                                  g_ctx.comm, s), "allgather values");
+    g_nccl.check(g_nccl.AllGather(h->lcnt.p, h->acnt.p, (size_t)F, ncclInt32, g_ctx.comm, s),
+                 "allgather counts");
+  } else {
+    CUDA_CHECK(cudaMemcpyAsync(h->avals.p, h->lvals.p, (size_t)F * kMaxBins * 4,
+                               cudaMemcpyDeviceToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(h->acnt.p, h->lcnt.p, (size_t)F * 4, cudaMemcpyDeviceToDevice, s));
   }
   {
-    if (world > 1) {
-      g_nccl.check(g_nccl.AllGather(h->lvals.p, h->avals.p, (size_t)F * kMaxBins, ncclFloat32,
-                                    g_ctx.comm, s), "allgather values");
-      g_nccl.check(g_nccl.AllGather(h->lcnt.p, h->acnt.p, (size_t)F, ncclInt32, g_ctx.comm, s),
-                   "allgather counts");
-    } else {
-      CUDA_CHECK(cudaMemcpyAsync(h->avals.p, h->lvals.p, (size_t)F * kMaxBins * 4,
-                                 cudaMemcpyDeviceToDevice, s));
-      CUDA_CHECK(cudaMemcpyAsync(h->acnt.p, h->lcnt.p, (size_t)F * 4, cudaMemcpyDeviceToDevice, s));
-    }
     Phase ph("merge", s, 0);
-    launch_merge_values(h->avals.as<float>(), h->acnt.as<int32_t>(), world, rank, F,
-                        h->dval.as<float>(), h->dnval.as<int32_t>(), h->d_lut.as<uint8_t>(),
-                        h->flags.as<uint32_t>(), s);
+    launch_merge_values(h->avals.as<float>(), h->acnt.as<int32_t>(), world, F, h->dval.as<float>(),
+                        h->dnval.as<int32_t>(), h->flags.as<uint32_t>(), s);
   }
-  // error flags, OR-ed over ranks so that all ranks fail together
+  // error flags, summed over ranks so that all ranks fail together
   uint32_t *hs = h->hsmall.as<uint32_t>();
-  {
+  auto check_flags = [&]() {
     DevBuf fl;
     fl.ensure(16);
-    // expand bits to counters (sum == OR for 0/1 values)
     CUDA_CHECK(cudaMemcpyAsync(hs, h->flags.p, 4, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
     uint32_t bits[4] = {(hs[0] >> 0) & 1, (hs[0] >> 1) & 1, (hs[0] >> 2) & 1, (hs[0] >> 3) & 1};
@@ -498,14 +490,30 @@ void train_region(adapt_region *h, cudaStream_t s) {
     if (bits[1]) throw Error(ADAPT_E_BAD_VALUE, "NaN time");
     if (bits[2]) throw Error(ADAPT_E_BAD_VALUE, "row with every variant unmeasured (+inf)");
     if (bits[3]) throw Error(ADAPT_E_TOO_MANY_DISTINCT, "a feature has more than 256 distinct values");
-  }
+  };
+  check_flags();
+  // value tables to the host; per-feature perfect hashes value -> rank for the bin pass
   h->val.assign((size_t)F * kMaxBins, 0.f);
   h->nval.assign(F, 0);
-  h->lut.assign((size_t)F * kMaxBins, 0);
   CUDA_CHECK(cudaMemcpyAsync(h->val.data(), h->dval.p, (size_t)F * kMaxBins * 4, cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaMemcpyAsync(h->nval.data(), h->dnval.p, (size_t)F * 4, cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaMemcpyAsync(h->lut.data(), h->d_lut.p, (size_t)F * kMaxBins, cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
+  {
+    std::vector<uint8_t> tab((size_t)lookup_table_bytes(F));
+    std::vector<uint32_t> mul((size_t)2 * F);
+    for (int f = 0; f < F; f++)
+      if (!build_value_hash(&h->val[(size_t)f * kMaxBins], h->nval[f], &mul[2 * f],
+                            &tab[(size_t)f * lookup_table_bytes(1)]))
+        throw Error(ADAPT_E_CUDA, "cannot build the value hash of feature " + std::to_string(f));
+    h2d(h->lk_keys, tab, s);
+    h2d(h->lk_mul, mul, s);
+  }
+  {
+    Phase ph("ingest", s, (double)n * (4.0 * F + 4.0 * V + F + 1));  // algorithmic (SURVEY §8(d))
+    launch_label_bin(feat, times, n, F, V, BS, h->lk_keys.as<uint8_t>(), h->lk_mul.as<uint32_t>(),
+                     h->flags.as<uint32_t>(), h->bins.as<uint8_t>(), h->labels.as<uint8_t>(), s);
+  }
+  check_flags();
 
   // histogram layout: node -> [f][rank][class], features packed by D_f
   std::vector<int32_t> hoff(F);
@@ -628,7 +636,6 @@ void train_region(adapt_region *h, cudaStream_t s) {
       pa.lab_out = lo;
       pa.BS = BS;
       pa.F = F;
-      pa.lut = h->d_lut.as<uint8_t>();
       pa.nranges = partition_ranges(sms, total);
       const uint32_t R = (total + pa.nranges - 1) / std::max(1, pa.nranges);
       int max_visits = 1;  // parents a range can touch
@@ -702,7 +709,6 @@ void train_region(adapt_region *h, cudaStream_t s) {
       ha.BS = BS;
       ha.F = F;
       ha.C = C;
-      ha.lut = h->d_lut.as<uint8_t>();
       ha.hoff = h->hoff.as<int32_t>();
       ha.nval = h->dnval.as<int32_t>();
       ha.groups = h->grp.as<int4>();
@@ -1208,7 +1214,7 @@ int adapt_get_bins(adapt_region_t *h, uint8_t *out, int64_t n) {
     if (!out || n != h->trained_n) throw Error(ADAPT_E_INVALID_ARG, "n must equal the trained row count");
     DevBuf tmp;
     tmp.ensure((size_t)n * h->F + 16);
-    launch_bins_out(h->bins.as<uint8_t>(), n, h->F, h->BS, h->d_lut.as<uint8_t>(), tmp.as<uint8_t>(), 0);
+    launch_bins_out(h->bins.as<uint8_t>(), n, h->F, h->BS, tmp.as<uint8_t>(), 0);
     CUDA_CHECK(cudaMemcpy(out, tmp.p, (size_t)n * h->F, cudaMemcpyDeviceToHost));
   });
 }

@@ -1,21 +1,25 @@
-// ingest.cu — steps a1 (label), a2 (value tables) and a3 (bin) in ONE pass
-// over the profiling table.
+// ingest.cu — steps a1 (label), a2 (value tables) and a3 (bin) of SURVEY §8(a).
 //
-// a1  label[i] = lowest v attaining min_v times[i][v] under IEEE '<'; +inf is
-//     "unmeasured" and an all-+inf or NaN row is an error (R2, R3).
-// a2  the distinct float32 values of every feature are discovered on the fly
-//     in a per-feature hash table in global memory (fronted by a per-block
-//     shared-memory cache); each new value gets a provisional id in order of
-//     discovery.  After the pass a tiny kernel sorts the <= 256 values
-//     (merged over ranks) into the value table and maps provisional ids to
-//     ranks (R7, R14).
-// a3  the bin of x[i][f] is its provisional id; the rank LUT turns it into
-//     the rank in the sorted table wherever a rank is needed.  So features are
-//     read exactly once: 4F + 4V bytes in, BS + 1 bytes out per row.
-//
-// Output planes (BS = F rounded up to a power of two bytes):
-//     bins[i*BS + f] = provisional bin of feature f, labels[i] = label.
+// Two streaming passes over the profiling table:
+//   discover_kernel   reads the features once (4F bytes/row) and collects the
+//                     distinct canonical float32 values of every feature in a
+//                     per-CTA shared-memory set backed by a global lock-free
+//                     hash set (R4: -0 -> +0; NaN/Inf flagged; > 256 flagged, R14).
+//   merge_values_kernel  sorts the union of the (per-rank) sets into the value
+//                     table val[f][rank] (a2) and builds, per feature, a
+//                     perfect hash key -> rank ("hash and displace": 64
+//                     displacements + 512 one-byte slots, collision-free for the
+//                     feature's own keys — the only keys the next pass meets).
+//   label_bin_kernel  streams (times, features) tiles with 1-D TMA bulk copies
+//                     (mbarrier pipeline, one persistent CTA per SM): a1 label =
+//                     lowest index of the minimum time, +inf = unmeasured (P:173,
+//                     R2, R3); a3 bin = rank of the value through the perfect
+//                     hash (two dependent byte loads, no misses, no atomics).  Writes bins
+//                     [N][BS] (BS = F rounded up to a power of two) and labels [N].
+// So every later pass works directly in rank space (bins == ranks).
 #include <algorithm>
+#include <cstring>
+#include <vector>
 
 #include "common.h"
 #include "ptx.h"
@@ -23,139 +27,236 @@
 namespace adapt {
 namespace {
 
-constexpr int kIngestThreads = 1024;
-
-__device__ __forceinline__ uint32_t hash_slot(uint32_t key, int log2slots) {
-  return (key * 2654435761u) >> (32 - log2slots);
+__device__ __forceinline__ uint32_t hash_bits(uint32_t key, uint32_t mul, int log2n) {
+  return (key * mul) >> (32 - log2n);
 }
 
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) {
   return *(volatile const uint32_t *)p;
 }
 
-// Global, race-free insert-or-find.  The winner of the key CAS takes the next
-// id from the per-feature counter and publishes it; losers wait for it.
-__device__ uint32_t global_lookup(uint32_t *gkey, uint32_t *gid, uint32_t *gcount,
-                                  uint32_t *flags, int f, uint32_t key) {
-  uint32_t *K = gkey + (size_t)f * kGSlots;
-  uint32_t *I = gid + (size_t)f * kGSlots;
-  uint32_t h = hash_slot(key, 10);
-  static_assert(kGSlots == 1024, "hash width");
-  for (int p = 0; p < kGSlots; p++) {
-    uint32_t k = ld_volatile(K + h);
-    if (k == kEmptyKey) {
-      const uint32_t old = atomicCAS(K + h, kEmptyKey, key);
-      if (old == kEmptyKey) {
-        const uint32_t id = atomicAdd(gcount + f, 1u);
-        if (id >= (uint32_t)kMaxBins) atomicOr(flags, kFlagTooMany);
-        atomicExch(I + h, id);
-        return id < (uint32_t)kMaxBins ? id : kMaxBins - 1;
-      }
-      k = old;
-    }
-    if (k == key) {
-      uint32_t id;
-      while ((id = ld_volatile(I + h)) == kPendingId) __nanosleep(32);
-      return id < (uint32_t)kMaxBins ? id : kMaxBins - 1;
-    }
-    h = (h + 1) & (kGSlots - 1);
-  }
-  atomicOr(flags, kFlagTooMany);  // table full: far more than 256 values
-  return kMaxBins - 1;
-}
-
-// One CTA per SM, persistent over row tiles of TR rows.  Thread 0 keeps
-// kStages tiles of (times, features) in flight with 1-D TMA bulk copies that
-// complete on "full" mbarriers.  Every warp owns TR/32 rows of a tile (P = 4
-// lanes per row for TR = 256): it labels them, bins them, writes its rows'
-// bins and labels straight to global memory (coalesced) and arrives on the
-// stage's "empty" mbarrier — no block-wide barrier in the loop.
-//
-// The per-block value cache is bucketised: a feature value hashes to a bucket
-// of 4 slots whose 4 keys (16 B) and 4 provisional ids (8 B) are fetched with
-// one 128-bit and one 64-bit shared load, so a hit costs one round trip.
-constexpr int kStages = 2;
-constexpr int kWarps = kIngestThreads / 32;
-constexpr uint16_t kNoId = 0xFFFF;
-
-struct IngestArgs {
-  const float *feat, *times;
-  int64_t n;
-  int F, V, BS, TR, P, log2nb, use_tma;
-  uint32_t *gkey, *gid, *gcount, *flags;
-  uint8_t *bins, *labels;
-};
-
-__device__ __forceinline__ int bucket_find(const uint4 K, const uint2 I, uint32_t key) {
-  // id of `key` in the bucket, -1 if absent or not yet published
-  int id = -1;
-  if (K.x == key) id = I.x & 0xFFFF;
-  if (K.y == key) id = I.x >> 16;
-  if (K.z == key) id = I.y & 0xFFFF;
-  if (K.w == key) id = I.y >> 16;
-  return id == kNoId ? -1 : id;
-}
-
-__device__ __noinline__ int cache_miss(uint32_t *keys, uint16_t *ids, int log2nb, uint32_t key,
-                                       const IngestArgs &a, int f) {
-  const int NB = 1 << log2nb;
-  const uint32_t b0 = hash_slot(key, log2nb);
-  for (int p = 1; p < NB; p++) {  // later buckets of the probe sequence
-    const uint32_t b = (b0 + p) & (NB - 1);
-    const int id = bucket_find(reinterpret_cast<const uint4 *>(keys)[b],
-                               reinterpret_cast<const uint2 *>(ids)[b], key);
-    if (id >= 0) return id;
-    if (keys[4 * b + 3] == kEmptyKey) break;  // a bucket with room ends the sequence
-  }
-  const uint32_t id = global_lookup(a.gkey, a.gid, a.gcount, a.flags, f, key);
-  for (int p = 0; p < NB; p++) {  // publish (best effort: a full cache just misses)
-    const uint32_t b = (b0 + p) & (NB - 1);
-    for (int e = 0; e < 4; e++) {
-      const uint32_t old = atomicCAS(keys + 4 * b + e, kEmptyKey, key);
-      if (old == kEmptyKey) {
-        ids[4 * b + e] = (uint16_t)id;
-        return (int)id;
-      }
-      if (old == key) return (int)id;
-    }
-  }
-  return (int)id;
-}
-
-__device__ __forceinline__ uint32_t canon_key(float x, uint32_t &flags) {
+__device__ __forceinline__ uint32_t canon_key(float x, uint32_t &flags, uint32_t bad) {
   uint32_t key = __float_as_uint(x);
   if ((key & 0x7f800000u) == 0x7f800000u) {
-    flags |= kFlagBadFeature;
+    flags |= bad;
     key = 0;
   }
   return x == 0.0f ? 0u : key;  // -0 -> +0 (R4)
 }
 
-__device__ __forceinline__ int lookup(uint32_t *keys, uint16_t *ids, int log2nb, uint32_t key,
-                                      const IngestArgs &a, int f) {
-  const uint32_t b = hash_slot(key, log2nb);
-  const int id = bucket_find(reinterpret_cast<const uint4 *>(keys)[b],
-                             reinterpret_cast<const uint2 *>(ids)[b], key);
-  return id >= 0 ? id : cache_miss(keys, ids, log2nb, key, a, f);
+// perfect-hash geometry per feature: 64 displacements (u16) + 512 slot ranks (u8)
+constexpr int kPhLog2Buckets = 6, kPhLog2Slots = 9;
+constexpr int kPhBuckets = 1 << kPhLog2Buckets, kPhSlots = 1 << kPhLog2Slots;
+constexpr int kPhBytes = kPhBuckets * 2 + kPhSlots;  // 640
+
+// ------------------------------------------------------------ discovery --
+constexpr int kDiscThreads = 512;
+constexpr uint32_t kMul = 2654435761u;
+
+__device__ void global_insert(uint32_t *gkey, uint32_t *gcount, uint32_t *flags, int f, uint32_t key) {
+  uint32_t *K = gkey + (size_t)f * kGSlots;
+  uint32_t h = hash_bits(key, kMul, 10);
+  static_assert(kGSlots == 1024, "hash width");
+  for (int p = 0; p < kGSlots; p++) {
+    uint32_t k = ld_volatile(K + h);
+    if (k == kEmptyKey) {
+      k = atomicCAS(K + h, kEmptyKey, key);
+      if (k == kEmptyKey) {
+        if (atomicAdd(gcount + f, 1u) >= (uint32_t)kMaxBins) atomicOr(flags, kFlagTooMany);
+        return;
+      }
+    }
+    if (k == key) return;
+    h = (h + 1) & (kGSlots - 1);
+  }
+  atomicOr(flags, kFlagTooMany);  // table full: far more than 256 values
 }
 
-__global__ void __launch_bounds__(kIngestThreads, 1) ingest_kernel(IngestArgs a) {
+// The per-CTA value set of a feature: NB buckets of 4 keys; a key lives in
+// the first bucket of its probe sequence h, h+1, ... with a free slot, so a
+// lookup of a present key is one 16-byte shared load in the common case.
+// Slow path: walk the sequence, insert, publish globally.
+__device__ __noinline__ void see_slow(uint32_t *S, int log2nb, uint32_t key, uint32_t *gkey,
+                                      uint32_t *gcount, uint32_t *flags, int f) {
+  const int NB = 1 << log2nb;
+  uint32_t b = hash_bits(key, kMul, log2nb);
+  for (int p = 0; p < NB; p++) {
+    for (int e = 0; e < 4; e++) {
+      uint32_t k = S[4 * b + e];
+      if (k == key) return;
+      if (k == kEmptyKey) {
+        k = atomicCAS(S + 4 * b + e, kEmptyKey, key);
+        if (k == kEmptyKey) {  // first sighting in this CTA: publish globally
+          global_insert(gkey, gcount, flags, f, key);
+          return;
+        }
+        if (k == key) return;
+      }
+    }
+    b = (b + 1) & (NB - 1);
+  }
+  global_insert(gkey, gcount, flags, f, key);  // CTA set full: always ask the global one
+}
+
+constexpr int kDiscUnroll = 4;  // float4 loads in flight per thread
+
+__global__ void __launch_bounds__(kDiscThreads) discover_kernel(const float *__restrict__ feat,
+                                                               int64_t n, int F, int log2nb,
+                                                               uint32_t *gkey, uint32_t *gcount,
+                                                               uint32_t *flags) {
+  extern __shared__ uint4 sset4[];  // [F][NB] buckets of 4 keys seen by this CTA
+  uint32_t *sset = reinterpret_cast<uint32_t *>(sset4);
+  const int NB = 1 << log2nb;
+  for (int i = threadIdx.x; i < F * NB * 4; i += blockDim.x) sset[i] = kEmptyKey;
+  __syncthreads();
+  uint32_t local_flags = 0;
+  // fast path: the value is in its home bucket (almost always, once warm)
+  auto see = [&](int f, uint32_t key) {
+    const uint4 K = sset4[f * NB + hash_bits(key, kMul, log2nb)];
+    if (K.x != key && K.y != key && K.z != key && K.w != key)
+      see_slow(sset + f * NB * 4, log2nb, key, gkey, gcount, flags, f);
+  };
+  const int64_t total = n * F;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // every thread runs the same number of iterations and the warp re-converges
+  // at the end of each, so the loads stay coalesced even though the set
+  // insertions diverge
+  if ((F & 3) == 0 && (reinterpret_cast<uintptr_t>(feat) & 15) == 0) {
+    // float4 j holds features 4j % F .. +3 of one row (coalesced)
+    const float4 *f4 = reinterpret_cast<const float4 *>(feat);
+    const int64_t n4 = total / 4;
+    int f0 = (int)((4 * tid0) % F);
+    const int df = (int)((4 * stride) % F);
+    for (int64_t base = 0; base < n4; base += kDiscUnroll * stride) {
+      float4 x[kDiscUnroll];
+#pragma unroll
+      for (int u = 0; u < kDiscUnroll; u++) {
+        const int64_t j = base + u * stride + tid0;
+        x[u] = j < n4 ? __ldcs(f4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kDiscUnroll; u++) {
+        if (base + u * stride + tid0 < n4) {
+          see(f0, canon_key(x[u].x, local_flags, kFlagBadFeature));
+          see(f0 + 1, canon_key(x[u].y, local_flags, kFlagBadFeature));
+          see(f0 + 2, canon_key(x[u].z, local_flags, kFlagBadFeature));
+          see(f0 + 3, canon_key(x[u].w, local_flags, kFlagBadFeature));
+        }
+        f0 += df;
+        if (f0 >= F) f0 -= F;
+      }
+      __syncwarp();
+    }
+  } else {
+    int f0 = (int)(tid0 % F);
+    const int df = (int)(stride % F);
+    for (int64_t base = 0; base < total; base += stride) {
+      const int64_t i = base + tid0;
+      if (i < total) see(f0, canon_key(__ldcs(feat + i), local_flags, kFlagBadFeature));
+      f0 += df;
+      if (f0 >= F) f0 -= F;
+      __syncwarp();
+    }
+  }
+  if (local_flags) atomicOr(flags, local_flags);
+}
+
+__global__ void collect_values_kernel(const uint32_t *gkey, const uint32_t *gcount,
+                                      float *local_vals, int32_t *local_cnt) {
+  __shared__ uint32_t cnt;
+  const int f = blockIdx.x;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int s = threadIdx.x; s < kGSlots; s += blockDim.x) {
+    const uint32_t k = gkey[(size_t)f * kGSlots + s];
+    if (k == kEmptyKey) continue;
+    const uint32_t i = atomicAdd(&cnt, 1u);
+    if (i < (uint32_t)kMaxBins) local_vals[f * kMaxBins + i] = __uint_as_float(k);
+  }
+  if (threadIdx.x == 0) local_cnt[f] = (int32_t)min(gcount[f], (uint32_t)kMaxBins + 1);
+}
+
+// Union of every rank's distinct values of feature f, sorted into val[f][*] (a2).
+__global__ void merge_values_kernel(const float *all_vals, const int32_t *all_cnt, int world, int F,
+                                    float *val, int32_t *nval, uint32_t *flags) {
+  extern __shared__ float cand[];  // [world*256]
+  uint8_t *rep = reinterpret_cast<uint8_t *>(cand + world * kMaxBins);
+  __shared__ int s_nrep;
+  const int f = blockIdx.x;
+  int M = 0;
+  for (int p = 0; p < world; p++) {
+    const int c = all_cnt[p * F + f];
+    if (c > kMaxBins && threadIdx.x == 0) atomicOr(flags, kFlagTooMany);
+    M += min(c, kMaxBins);
+  }
+  for (int c = threadIdx.x; c < M; c += blockDim.x) {
+    int p = 0, i = c;
+    while (i >= min(all_cnt[p * F + f], kMaxBins)) {
+      i -= min(all_cnt[p * F + f], kMaxBins);
+      p++;
+    }
+    cand[c] = all_vals[((size_t)p * F + f) * kMaxBins + i];
+  }
+  if (threadIdx.x == 0) s_nrep = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < M; c += blockDim.x) {
+    const uint32_t b = __float_as_uint(cand[c]);
+    bool first = true;
+    for (int e = 0; e < c && first; e++) first = __float_as_uint(cand[e]) != b;
+    rep[c] = first;
+    if (first) atomicAdd(&s_nrep, 1);
+  }
+  __syncthreads();
+  const int D = s_nrep;
+  if (threadIdx.x == 0) {
+    nval[f] = D;
+    if (D > kMaxBins) atomicOr(flags, kFlagTooMany);
+  }
+  for (int c = threadIdx.x; c < M; c += blockDim.x) {
+    if (!rep[c]) continue;
+    const float x = cand[c];
+    int r = 0;
+    for (int e = 0; e < M; e++) r += (rep[e] && cand[e] < x);
+    if (r < kMaxBins) val[f * kMaxBins + r] = x;
+  }
+}
+
+// ------------------------------------------------------------ label + bin --
+// One CTA per SM, persistent over row tiles of TR rows.  Thread 0 keeps
+// kStages tiles of (times, features) in flight with 1-D TMA bulk copies that
+// complete on "full" mbarriers.  Every warp owns TR/32 rows of a tile (P
+// lanes per row): it labels them, bins them, writes its rows' bins and labels
+// straight to global memory and arrives on the stage's "empty" mbarrier.
+constexpr int kIngestThreads = 1024;
+constexpr int kStages = 2;
+constexpr int kWarps = kIngestThreads / 32;
+
+struct LabelBinArgs {
+  const float *feat, *times;
+  int64_t n;
+  int F, V, BS, TR, P, use_tma;
+  const uint8_t *tab;       // [F][kPhBytes] perfect hashes
+  const uint32_t *lk_mul;   // [F][2] their multipliers
+  uint32_t *flags;
+  uint8_t *bins, *labels;
+};
+
+__global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int F = a.F, V = a.V, BS = a.BS, TR = a.TR, P = a.P;
-  const int NB = 1 << a.log2nb;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
   uint64_t *empty = full + kStages;
-  uint32_t *ckeys = reinterpret_cast<uint32_t *>(smem + 128);   // [F][NB][4]
-  uint16_t *cids = reinterpret_cast<uint16_t *>(ckeys + F * NB * 4);  // [F][NB][4]
-  const size_t o1 = 128 + (size_t)F * NB * 24;
+  uint32_t *lmul = reinterpret_cast<uint32_t *>(smem + 128);  // [F][2]
+  uint8_t *tab = smem + 128 + 8 * kMaxF;                     // [F][kPhBytes]
+  const size_t o1 = (128 + 8 * kMaxF + (size_t)F * kPhBytes + 15) & ~(size_t)15;
   float *stT = reinterpret_cast<float *>(smem + o1);
   float *stF = stT + (size_t)kStages * TR * V;
 
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < F * NB * 4; i += blockDim.x) {
-    ckeys[i] = kEmptyKey;
-    cids[i] = kNoId;
-  }
+  for (int i = tid; i < F * kPhBytes / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t *>(tab)[i] = reinterpret_cast<const uint32_t *>(a.tab)[i];
+  for (int i = tid; i < 2 * F; i += blockDim.x) lmul[i] = a.lk_mul[i];
   if (tid == 0) {
     for (int s = 0; s < kStages; s++) {
       mbar_init(&full[s], 1);
@@ -185,8 +286,13 @@ __global__ void __launch_bounds__(kIngestThreads, 1) ingest_kernel(IngestArgs a)
   uint32_t local_flags = 0;
   const int r = tid / P, q = tid % P;
   const bool vec_t = (V & 3) == 0;
-  const int per = F / P;                        // features per lane when F % P == 0
+  const int per = F / P;  // features per lane when F % P == 0
   const bool vec_f = (F % P) == 0 && (per & 3) == 0;
+  auto rank_of = [&](int f, uint32_t key) -> int {  // perfect hash: 2 dependent byte loads
+    const uint8_t *t = tab + f * kPhBytes;
+    const uint32_t d = reinterpret_cast<const uint16_t *>(t)[hash_bits(key, lmul[2 * f], kPhLog2Buckets)];
+    return t[kPhBuckets * 2 + ((hash_bits(key, lmul[2 * f + 1], kPhLog2Slots) + d) & (kPhSlots - 1))];
+  };
   for (int64_t k = 0; k < K; k++) {
     const int64_t t = first + k * stride;
     const int64_t row0 = t * TR;
@@ -245,38 +351,25 @@ __global__ void __launch_bounds__(kIngestThreads, 1) ingest_kernel(IngestArgs a)
         if (best == __int_as_float(0x7f800000)) local_flags |= kFlagAllInf;
         a.labels[row0 + r] = (uint8_t)(bi < V ? bi : 0);
       }
-      // ---- a2 + a3: provisional ids of this lane's features ----
+      // ---- a3: rank of each of this lane's feature values ----
       const float *fr = tF + (size_t)r * F;
       uint8_t *dst = a.bins + (row0 + r) * BS;
       if (vec_f) {
         for (int c = 0; c < per; c += 4) {
           const int f = q * per + c;
           const float4 x = *reinterpret_cast<const float4 *>(fr + f);
-          const uint32_t key[4] = {canon_key(x.x, local_flags), canon_key(x.y, local_flags),
-                                   canon_key(x.z, local_flags), canon_key(x.w, local_flags)};
-          uint4 Kb[4];
-          uint2 Ib[4];
-#pragma unroll
-          for (int e = 0; e < 4; e++) {  // the 4 features' buckets, loaded together
-            const uint32_t b = hash_slot(key[e], a.log2nb);
-            Kb[e] = reinterpret_cast<const uint4 *>(ckeys + (size_t)(f + e) * NB * 4)[b];
-            Ib[e] = reinterpret_cast<const uint2 *>(cids + (size_t)(f + e) * NB * 4)[b];
-          }
-          uint32_t packed = 0;
-#pragma unroll
-          for (int e = 0; e < 4; e++) {
-            int id = bucket_find(Kb[e], Ib[e], key[e]);
-            if (id < 0)
-              id = cache_miss(ckeys + (size_t)(f + e) * NB * 4, cids + (size_t)(f + e) * NB * 4,
-                              a.log2nb, key[e], a, f + e);
-            packed |= (uint32_t)(id & 0xFF) << (8 * e);
-          }
-          *reinterpret_cast<uint32_t *>(dst + f) = packed;
+          const int r0 = rank_of(f, canon_key(x.x, local_flags, kFlagBadFeature));
+          const int r1 = rank_of(f + 1, canon_key(x.y, local_flags, kFlagBadFeature));
+          const int r2 = rank_of(f + 2, canon_key(x.z, local_flags, kFlagBadFeature));
+          const int r3 = rank_of(f + 3, canon_key(x.w, local_flags, kFlagBadFeature));
+          *reinterpret_cast<uint32_t *>(dst + f) =
+              (uint32_t)(r0 & 0xFF) | ((uint32_t)(r1 & 0xFF) << 8) | ((uint32_t)(r2 & 0xFF) << 16) |
+              ((uint32_t)(r3 & 0xFF) << 24);
         }
       } else {
-        for (int f = q; f < F; f += P)
-          dst[f] = (uint8_t)lookup(ckeys + (size_t)f * NB * 4, cids + (size_t)f * NB * 4, a.log2nb,
-                                   canon_key(fr[f], local_flags), a, f);
+        for (int f = q; f < F; f += P) {
+          dst[f] = (uint8_t)rank_of(f, canon_key(fr[f], local_flags, kFlagBadFeature));
+        }
         for (int f = F + q; f < BS; f += P) dst[f] = 0;
       }
     }
@@ -287,76 +380,11 @@ __global__ void __launch_bounds__(kIngestThreads, 1) ingest_kernel(IngestArgs a)
   if (local_flags) atomicOr(a.flags, local_flags);
 }
 
-__global__ void collect_values_kernel(const uint32_t *gkey, const uint32_t *gid,
-                                      const uint32_t *gcount, float *local_vals,
-                                      int32_t *local_cnt) {
-  const int f = blockIdx.x;
-  for (int s = threadIdx.x; s < kGSlots; s += blockDim.x) {
-    const uint32_t k = gkey[(size_t)f * kGSlots + s];
-    if (k == kEmptyKey) continue;
-    const uint32_t id = gid[(size_t)f * kGSlots + s];
-    if (id < (uint32_t)kMaxBins) local_vals[f * kMaxBins + id] = __uint_as_float(k);
-  }
-  if (threadIdx.x == 0) local_cnt[f] = (int32_t)min(gcount[f], (uint32_t)kMaxBins + 1);
-}
-
-// Union of every rank's distinct values of feature f, sorted; lut maps this
-// rank's provisional ids to ranks in the union (the value table, a2).
-__global__ void merge_values_kernel(const float *all_vals, const int32_t *all_cnt, int world,
-                                    int rank, int F, float *val, int32_t *nval, uint8_t *lut,
-                                    uint32_t *flags) {
-  extern __shared__ float cand[];  // [world*256]
-  uint8_t *rep = reinterpret_cast<uint8_t *>(cand + world * kMaxBins);
-  __shared__ int s_nrep;
-  const int f = blockIdx.x;
-  int M = 0;
-  for (int p = 0; p < world; p++) {
-    const int c = all_cnt[p * F + f];
-    if (c > kMaxBins && threadIdx.x == 0) atomicOr(flags, kFlagTooMany);
-    M += min(c, kMaxBins);
-  }
-  for (int c = threadIdx.x; c < M; c += blockDim.x) {
-    int p = 0, i = c;
-    while (i >= min(all_cnt[p * F + f], kMaxBins)) {
-      i -= min(all_cnt[p * F + f], kMaxBins);
-      p++;
-    }
-    cand[c] = all_vals[((size_t)p * F + f) * kMaxBins + i];
-  }
-  if (threadIdx.x == 0) s_nrep = 0;
-  __syncthreads();
-  for (int c = threadIdx.x; c < M; c += blockDim.x) {
-    const uint32_t b = __float_as_uint(cand[c]);
-    bool first = true;
-    for (int e = 0; e < c && first; e++) first = __float_as_uint(cand[e]) != b;
-    rep[c] = first;
-    if (first) atomicAdd(&s_nrep, 1);
-  }
-  __syncthreads();
-  const int D = s_nrep;
-  if (threadIdx.x == 0) {
-    nval[f] = D;
-    if (D > kMaxBins) atomicOr(flags, kFlagTooMany);
-  }
-  int base = 0;  // offset of this rank's candidates
-  for (int p = 0; p < rank; p++) base += min(all_cnt[p * F + f], kMaxBins);
-  const int mine = min(all_cnt[rank * F + f], kMaxBins);
-  for (int c = threadIdx.x; c < M; c += blockDim.x) {
-    const float x = cand[c];
-    int r = 0;
-    for (int e = 0; e < M; e++) r += (rep[e] && cand[e] < x);
-    if (rep[c] && r < kMaxBins) val[f * kMaxBins + r] = x;
-    if (c >= base && c < base + mine) lut[f * kMaxBins + (c - base)] = (uint8_t)min(r, 255);
-  }
-}
-
-__global__ void bins_out_kernel(const uint8_t *rec, int64_t n, int F, int RS, const uint8_t *lut,
-                                uint8_t *out) {  // rec = bins plane, RS = its row stride
+__global__ void bins_out_kernel(const uint8_t *bins, int64_t n, int F, int BS, uint8_t *out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * F;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / F;
-    const int f = (int)(i % F);
-    out[i] = lut[f * kMaxBins + rec[r * RS + f]];
+    out[i] = bins[r * BS + (int)(i - r * F)];
   }
 }
 
@@ -366,70 +394,139 @@ int grid_for(int64_t work, int per_block, int cap) {
   return (int)(b < cap ? b : cap);
 }
 
+int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
 }  // namespace
 
-void launch_ingest(const float *feat, const float *times, int64_t n, int F, int V, int BS,
-                   uint32_t *gkey, uint32_t *gid, uint32_t *gcount, uint32_t *flags,
-                   uint8_t *bins, uint8_t *labels, cudaStream_t s) {
+int lookup_table_bytes(int F) { return F * kPhBytes; }
+
+// Perfect hash of one feature's sorted values (host; <= 256 keys): bucket
+// h1(key) of 64 gets a displacement d so that slot (h2(key) + d) mod 512 is
+// distinct for every key; buckets are placed largest first.  Same hash_bits
+// as the device.  Returns false only if no seed works (never seen).
+bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab) {
+  auto hb = [](uint32_t key, uint32_t m, int l) { return (key * m) >> (32 - l); };
+  std::vector<uint32_t> keys(D);
+  for (int r = 0; r < D; r++) memcpy(&keys[r], &vals[r], 4);
+  for (uint32_t seed = 0; seed < 1024; seed++) {
+    const uint32_t m1 = (0x9E3779B1u + 0x85EBCA6Bu * seed) | 1u;
+    const uint32_t m2 = (0xC2B2AE35u + 0x27D4EB2Fu * seed) | 1u;
+    std::vector<std::vector<int>> buckets(kPhBuckets);
+    for (int r = 0; r < D; r++) buckets[hb(keys[r], m1, kPhLog2Buckets)].push_back(r);
+    std::vector<int> order(kPhBuckets);
+    for (int b = 0; b < kPhBuckets; b++) order[b] = b;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int x, int y) { return buckets[x].size() > buckets[y].size(); });
+    std::vector<char> used(kPhSlots, 0);
+    uint16_t disp[kPhBuckets] = {0};
+    std::vector<uint8_t> slot_rank(kPhSlots, 0);
+    bool ok = true;
+    for (int b : order) {
+      if (buckets[b].empty()) break;
+      int found = -1;
+      for (int d = 0; d < kPhSlots && found < 0; d++) {
+        bool good = true;
+        std::vector<uint32_t> taken;
+        for (int r : buckets[b]) {
+          const uint32_t sl = (hb(keys[r], m2, kPhLog2Slots) + d) & (kPhSlots - 1);
+          if (used[sl] || std::find(taken.begin(), taken.end(), sl) != taken.end()) {
+            good = false;
+            break;
+          }
+          taken.push_back(sl);
+        }
+        if (good) found = d;
+      }
+      if (found < 0) {
+        ok = false;
+        break;
+      }
+      disp[b] = (uint16_t)found;
+      for (int r : buckets[b]) {
+        const uint32_t sl = (hb(keys[r], m2, kPhLog2Slots) + found) & (kPhSlots - 1);
+        used[sl] = 1;
+        slot_rank[sl] = (uint8_t)r;
+      }
+    }
+    if (!ok) continue;
+    memcpy(tab, disp, sizeof disp);
+    memcpy(tab + kPhBuckets * 2, slot_rank.data(), kPhSlots);
+    mul[0] = m1;
+    mul[1] = m2;
+    return true;
+  }
+  return false;
+}
+
+void launch_discover(const float *feat, int64_t n, int F, uint32_t *gkey, uint32_t *gcount,
+                     uint32_t *flags, cudaStream_t s) {
   if (n == 0) return;
-  IngestArgs a;
+  int log2nb = 8;  // 256 buckets x 4 keys per feature (~1 key per bucket at 256 values)
+  while (log2nb > 4 && (size_t)F * (16u << log2nb) > 64 * 1024) log2nb--;
+  const size_t smem = (size_t)F * (16u << log2nb);
+  CUDA_CHECK(cudaFuncSetAttribute(discover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  const int grid = grid_for(n * F / 4 + 1, kDiscThreads * 4, sm_count() * 2);
+  discover_kernel<<<grid, kDiscThreads, smem, s>>>(feat, n, F, log2nb, gkey, gcount, flags);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_collect_values(const uint32_t *gkey, const uint32_t *gcount, int F, float *local_vals,
+                           int32_t *local_cnt, cudaStream_t s) {
+  collect_values_kernel<<<F, 256, 0, s>>>(gkey, gcount, local_vals, local_cnt);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int world, int F,
+                         float *val, int32_t *nval, uint32_t *flags, cudaStream_t s) {
+  const size_t smem = (size_t)world * kMaxBins * 5;
+  CUDA_CHECK(cudaFuncSetAttribute(merge_values_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  merge_values_kernel<<<F, 1024, smem, s>>>(all_vals, all_cnt, world, F, val, nval, flags);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_label_bin(const float *feat, const float *times, int64_t n, int F, int V, int BS,
+                      const uint8_t *tab, const uint32_t *lk_mul, uint32_t *flags, uint8_t *bins,
+                      uint8_t *labels, cudaStream_t s) {
+  if (n == 0) return;
+  LabelBinArgs a;
   a.feat = feat;
   a.times = times;
   a.n = n;
   a.F = F;
   a.V = V;
   a.BS = BS;
-  a.gkey = gkey;
-  a.gid = gid;
-  a.gcount = gcount;
+  a.tab = tab;
+  a.lk_mul = lk_mul;
   a.flags = flags;
   a.bins = bins;
   a.labels = labels;
-  // per-block value cache: 128 buckets x 4 slots per feature (load <= 1/2 at
-  // 256 values), fewer when F is large
-  a.log2nb = 7;
-  while (a.log2nb > 3 && (size_t)F * (24u << a.log2nb) > 48 * 1024) a.log2nb--;
-  const size_t cache = 128 + (size_t)F * (24u << a.log2nb);
+  const size_t table = (128 + 8 * kMaxF + (size_t)F * kPhBytes + 15) & ~(size_t)15;
   // P threads per row, TR = threads / P rows per tile: the largest tile whose
-  // kStages (times, features) buffers fit next to the cache
+  // kStages (times, features) buffers fit next to the table
   a.P = 4;
-  while (a.P < 32 && cache + (size_t)kStages * (kIngestThreads / a.P) * (V + F) * 4 > 220 * 1024)
+  while (a.P < 32 && table + (size_t)kStages * (kIngestThreads / a.P) * (V + F) * 4 > 220 * 1024)
     a.P <<= 1;
   a.TR = kIngestThreads / a.P;
   a.use_tma = ((reinterpret_cast<uintptr_t>(feat) | reinterpret_cast<uintptr_t>(times)) & 15) == 0;
-  const size_t smem = cache + (size_t)kStages * a.TR * (V + F) * 4;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = table + (size_t)kStages * a.TR * (V + F) * 4;
   const int64_t ntiles = (n + a.TR - 1) / a.TR;
-  const int grid = (int)std::min<int64_t>(ntiles, sms);
-  CUDA_CHECK(cudaFuncSetAttribute(ingest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const int grid = (int)std::min<int64_t>(ntiles, sm_count());
+  CUDA_CHECK(cudaFuncSetAttribute(label_bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-  ingest_kernel<<<grid, kIngestThreads, smem, s>>>(a);
+  label_bin_kernel<<<grid, kIngestThreads, smem, s>>>(a);
   CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_collect_values(const uint32_t *gkey, const uint32_t *gid, const uint32_t *gcount,
-                           int F, float *local_vals, int32_t *local_cnt, cudaStream_t s) {
-  collect_values_kernel<<<F, 256, 0, s>>>(gkey, gid, gcount, local_vals, local_cnt);
-  CUDA_CHECK(cudaGetLastError());
-}
-
-void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int world, int rank,
-                         int F, float *val, int32_t *nval, uint8_t *lut, uint32_t *flags,
-                         cudaStream_t s) {
-  const size_t smem = (size_t)world * kMaxBins * 5;
-  CUDA_CHECK(cudaFuncSetAttribute(merge_values_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  merge_values_kernel<<<F, 1024, smem, s>>>(all_vals, all_cnt, world, rank, F, val, nval, lut,
-                                            flags);
-  CUDA_CHECK(cudaGetLastError());
-}
-
-void launch_bins_out(const uint8_t *rec, int64_t n, int F, int RS, const uint8_t *lut,
-                     uint8_t *out, cudaStream_t s) {
+void launch_bins_out(const uint8_t *bins, int64_t n, int F, int BS, uint8_t *out, cudaStream_t s) {
   if (n == 0) return;
-  bins_out_kernel<<<grid_for(n * F, 256, 148 * 16), 256, 0, s>>>(rec, n, F, RS, lut, out);
+  bins_out_kernel<<<grid_for(n * F, 256, 148 * 16), 256, 0, s>>>(bins, n, F, BS, out);
   CUDA_CHECK(cudaGetLastError());
 }
 

@@ -19,9 +19,9 @@
 //                     of a range are co-resident (cooperative launch, one CTA
 //                     per SM) and re-synchronise every few iterations, so a
 //                     row fetched from HBM by one is served to the others
-//                     from L2.  Counters are indexed by provisional bin id
-//                     with an odd class stride (bank spread); the id -> rank
-//                     map is applied once per counter when a node is flushed.
+//                     from L2.  Counters use an odd class stride (bank
+//                     spread) and are flushed into the node's global
+//                     histogram with integer atomics.
 // Every quantity that decides the tree is an integer, so the result does not
 // depend on row order, on the number of ranks or on atomic ordering.
 #include <algorithm>
@@ -126,11 +126,8 @@ constexpr int kPartUnroll = 4;
 
 template <int BS>
 __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) {
-  extern __shared__ uint8_t slut[];  // [F][256] id -> rank
   __shared__ uint32_t s_cur[2];
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < a.F * kMaxBins / 4; i += blockDim.x)
-    reinterpret_cast<uint32_t *>(slut)[i] = reinterpret_cast<const uint32_t *>(a.lut)[i];
   const uint32_t R = (a.total_rows + gridDim.x - 1) / gridDim.x;
   uint32_t p0 = blockIdx.x * R;
   const uint32_t p1 = min(p0 + R, a.total_rows);
@@ -150,7 +147,6 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) 
       const Seg sg = a.segs[s];
       const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
       const uint32_t q1 = min(sg.len, pe - sg.row_base);
-      const uint8_t *lf = slut + sg.feat * kMaxBins;
       for (uint32_t qb = q0; qb < q1; qb += kPartUnroll * blockDim.x) {
         Row<BS> r[kPartUnroll];
         int label[kPartUnroll];
@@ -169,7 +165,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) 
 #pragma unroll
         for (int u = 0; u < kPartUnroll; u++) {
           const bool valid = label[u] >= 0;
-          const bool left = lf[row_byte<BS>(r[u], sg.feat)] <= sg.thr;
+          const bool left = row_byte<BS>(r[u], sg.feat) <= sg.thr;  // bins are ranks
           const unsigned ml = __ballot_sync(kFull, valid && left && (sg.write & 1));
           const unsigned mr = __ballot_sync(kFull, valid && !left && (sg.write & 2));
           uint32_t base = 0;
@@ -208,8 +204,7 @@ constexpr int kSyncEvery = 8;
 
 template <int BS>
 __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
-  extern __shared__ uint32_t sh[];  // [smem_counters] counters | lut [F*256] bytes
-  uint8_t *slut = reinterpret_cast<uint8_t *>(sh + a.smem_counters);
+  extern __shared__ uint32_t sh[];  // [smem_counters] counters
   __shared__ int32_t soff[kMaxF];   // this group's smem offset of feature f, -1 if absent
   __shared__ int32_t sdf[kMaxF];    // distinct values of f
   const int tid = threadIdx.x;
@@ -219,8 +214,6 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
   const int4 grp = a.groups[g];  // x: first class, y: classes, z: padded class stride, w: word
   const int k0 = grp.x, kw = grp.y, kwp = grp.z, w0 = grp.w;
   const int C = a.C;
-  for (int i = tid; i < a.F * kMaxBins / 4; i += blockDim.x)
-    reinterpret_cast<uint32_t *>(slut)[i] = reinterpret_cast<const uint32_t *>(a.lut)[i];
   int gcount = 0;
   for (int f = 0; f < a.F; f++) {
     const int o = a.gsoff[g * a.F + f];
@@ -301,19 +294,18 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
       }
     }
     __syncthreads();
-    {  // flush: provisional id -> rank, class slab -> classes
+    {  // flush: padded class slab -> the node's [f][rank][class] layout
       uint32_t *dst = a.H + (size_t)first.hslot * a.HS;
       for (int f = 0; f < a.F; f++) {
         const int o = soff[f];
         if (o < 0) continue;
         const int n = sdf[f] * kwp;
-        const uint8_t *lf = slut + f * kMaxBins;
         uint32_t *df = dst + a.hoff[f];
         for (int i = tid; i < n; i += blockDim.x) {
           const uint32_t val = sh[o + i];
           if (val) {
-            const int pp = i / kwp, j = i - pp * kwp;
-            atomicAdd(df + (int)lf[pp] * C + k0 + j, val);
+            const int rk = i / kwp, j = i - rk * kwp;
+            atomicAdd(df + rk * C + k0 + j, val);
           }
         }
       }
@@ -331,13 +323,10 @@ int partition_ranges(int sms, uint32_t total_rows) {
 
 void launch_partition(const PartArgs &a, cudaStream_t s) {
   if (a.total_rows == 0 || a.nseg == 0) return;
-  const size_t smem = (size_t)a.F * kMaxBins;
   switch (a.BS) {
 #define CASE(B)                                                                               \
   case B:                                                                                     \
-    CUDA_CHECK(cudaFuncSetAttribute(partition_kernel<B>,                                      \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
-    partition_kernel<B><<<a.nranges, kPartThreads, smem, s>>>(a);                             \
+    partition_kernel<B><<<a.nranges, kPartThreads, 0, s>>>(a);                                \
     break;
     CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
 #undef CASE
@@ -349,7 +338,7 @@ void launch_partition(const PartArgs &a, cudaStream_t s) {
 
 void launch_hist(const HistArgs &a, cudaStream_t s) {
   if (a.total_rows == 0 || a.nseg == 0) return;
-  const size_t smem = (size_t)a.smem_counters * 4 + (size_t)a.F * kMaxBins;
+  const size_t smem = (size_t)a.smem_counters * 4;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.nranges * a.ngroups);
   cfg.blockDim = dim3(kHistThreads);
