@@ -4,64 +4,114 @@
 //
 // The device tree is a BFS array of 8-byte nodes; the threshold is stored as
 // the largest float32 <= the double threshold, which makes the float compare
-// exact (V:A5).  Vectors are staged through shared memory with coalesced
-// 16-byte loads, each thread then walks one vector reading its features from
-// a bank-conflict-padded row.
+// exact (V:A5).  The first kTopNodes nodes (the top levels every walk visits;
+// a whole depth-12 tree) sit in shared memory, deeper ones are read through
+// L1/L2.  Vectors stream through a register-prefetched, double-buffered tile:
+// while the block walks tile k out of shared memory (odd row stride: no bank
+// conflicts between lanes), the coalesced 16-byte loads of tile k+1 are in
+// flight.
+#include <algorithm>
+
 #include "common.h"
 
 namespace adapt {
 namespace {
 
-constexpr int kSelThreads = 256;
+constexpr int kSelThreads = 512;
+constexpr int kTopNodes = 8191;  // 64 KB
 
-__global__ void __launch_bounds__(kSelThreads)
-    select_kernel(const DNode *__restrict__ gtree, int n_nodes, int tree_in_smem /* = n_top */,
-                  const float *__restrict__ X, int64_t m, int F, int32_t *__restrict__ out) {
-  extern __shared__ float sx[];  // [kSelThreads][F | 1] (odd stride) | tree copy
-  const int stride = F | 1;
+__device__ __forceinline__ DNode ldg_node(const DNode *p) {
+  const int2 v = __ldg(reinterpret_cast<const int2 *>(p));
+  DNode d;
+  d.thr = __int_as_float(v.x);
+  d.meta = v.y;
+  return d;
+}
+
+template <int F>
+__global__ void __launch_bounds__(kSelThreads, 2)
+    select_kernel(const DNode *__restrict__ gtree, int n_top, const float *__restrict__ X,
+                  int64_t m, int32_t *__restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int kStride = F | 1;                   // odd row stride of the tile
+  constexpr int kVec = F / 4;                      // float4 per vector
+  DNode *st = reinterpret_cast<DNode *>(smem);     // [n_top]
+  float *sx = reinterpret_cast<float *>(smem + (size_t)kTopNodes * sizeof(DNode));  // [T][kStride]
   const int t = threadIdx.x;
-  // the first n_top nodes (BFS order = the top levels, where every walk
-  // passes) live in shared memory; deeper nodes are read through L1/L2
-  DNode *st = reinterpret_cast<DNode *>(sx + kSelThreads * stride + (kSelThreads * stride & 1));
-  const int n_top = tree_in_smem;
   for (int i = t; i < n_top; i += kSelThreads) st[i] = gtree[i];
-  __syncthreads();
-  const bool aligned = (reinterpret_cast<uintptr_t>(X) & 15) == 0 && (F & 3) == 0;
-  for (int64_t v0 = blockIdx.x * (int64_t)kSelThreads; v0 < m;
-       v0 += (int64_t)gridDim.x * kSelThreads) {
+
+  const int64_t ntiles = (m + kSelThreads - 1) / kSelThreads;
+  float4 pre[kVec];  // this thread's share of the next tile (coalesced float4s)
+  auto fetch = [&](int64_t tile) {
+    const int64_t v0 = tile * kSelThreads;
     const int rows = (m - v0 < kSelThreads) ? (int)(m - v0) : kSelThreads;
-    const float *src = X + v0 * F;
-    const int cnt = rows * F;
-    if (aligned) {
-      const float4 *s4 = reinterpret_cast<const float4 *>(src);
-      for (int i = t; i < (cnt >> 2); i += kSelThreads) {
-        const float4 v = __ldcs(s4 + i);
-        const int e = i << 2, r = e / F, c = e - r * F;  // F % 4 == 0: one row per float4
-        float *d = sx + r * stride + c;
-        d[0] = v.x;
-        d[1] = v.y;
-        d[2] = v.z;
-        d[3] = v.w;
+    const float4 *src = reinterpret_cast<const float4 *>(X + v0 * F);
+#pragma unroll
+    for (int k = 0; k < kVec; k++) {
+      const int i = t + k * kSelThreads;  // float4 index within the tile
+      pre[k] = i < rows * kVec ? __ldcs(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int k = 0; k < kVec; k++) {
+      const int i = t + k * kSelThreads, r = i / kVec, c = (i % kVec) * 4;
+      float *d = sx + r * kStride + c;
+      d[0] = pre[k].x;
+      d[1] = pre[k].y;
+      d[2] = pre[k].z;
+      d[3] = pre[k].w;
+    }
+  };
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) fetch(tile);
+  __syncthreads();  // tree copy visible
+  for (; tile < ntiles; tile += gridDim.x) {
+    stash();
+    __syncthreads();
+    if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);  // next tile in flight during the walks
+    const int64_t v = tile * kSelThreads + t;
+    if (v < m) {
+      const float *x = sx + t * kStride;
+      DNode nd = st[0];
+      while (nd.meta >= 0) {
+        const float xv = x[nd.meta & 63];
+        const int k = (nd.meta >> 6) + (xv <= nd.thr ? 0 : 1);
+        nd = k < n_top ? st[k] : ldg_node(gtree + k);
       }
-    } else {
-      for (int i = t; i < cnt; i += kSelThreads) {
-        const int r = i / F, c = i - r * F;
-        sx[r * stride + c] = __ldcs(src + i);
-      }
+      __stcs(out + v, -1 - nd.meta);
+    }
+    __syncthreads();
+  }
+}
+
+// generic F (not a multiple of 4, or an unaligned X): scalar staging
+__global__ void __launch_bounds__(kSelThreads, 2)
+    select_kernel_any(const DNode *__restrict__ gtree, int n_top, const float *__restrict__ X,
+                      int64_t m, int F, int32_t *__restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int stride = F | 1;
+  DNode *st = reinterpret_cast<DNode *>(smem);
+  float *sx = reinterpret_cast<float *>(smem + (size_t)kTopNodes * sizeof(DNode));
+  const int t = threadIdx.x;
+  for (int i = t; i < n_top; i += kSelThreads) st[i] = gtree[i];
+  for (int64_t v0 = blockIdx.x * (int64_t)kSelThreads; v0 < m; v0 += (int64_t)gridDim.x * kSelThreads) {
+    const int rows = (m - v0 < kSelThreads) ? (int)(m - v0) : kSelThreads;
+    __syncthreads();
+    for (int i = t; i < rows * F; i += kSelThreads) {
+      const int r = i / F, c = i - r * F;
+      sx[r * stride + c] = __ldcs(X + v0 * F + i);
     }
     __syncthreads();
     if (t < rows) {
       const float *x = sx + t * stride;
-      DNode nd = n_top > 0 ? st[0] : gtree[0];
+      DNode nd = st[0];
       while (nd.meta >= 0) {
-        const float v = x[nd.meta & 63];
-        const int k = (nd.meta >> 6) + (v <= nd.thr ? 0 : 1);
-        nd = k < n_top ? st[k] : gtree[k];
+        const int k = (nd.meta >> 6) + (x[nd.meta & 63] <= nd.thr ? 0 : 1);
+        nd = k < n_top ? st[k] : ldg_node(gtree + k);
       }
-      const int32_t meta = nd.meta;
-      __stcs(out + v0 + t, -1 - meta);
+      __stcs(out + v0 + t, -1 - nd.meta);
     }
-    __syncthreads();
   }
 }
 
@@ -70,14 +120,28 @@ __global__ void __launch_bounds__(kSelThreads)
 void launch_select(const DNode *tree, int n_nodes, const float *X, int64_t m, int F, int32_t *out,
                    cudaStream_t s) {
   if (m == 0) return;
-  const size_t xs = ((size_t)kSelThreads * (F | 1) * 4 + 7) / 8 * 8;
-  const int n_top = n_nodes < 2048 ? n_nodes : 2047;  // top 11 levels: 16 KB
-  const size_t smem = xs + (size_t)n_top * sizeof(DNode);
-  CUDA_CHECK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-  int64_t blocks = (m + kSelThreads - 1) / kSelThreads;
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  select_kernel<<<(int)blocks, kSelThreads, smem, s>>>(tree, n_nodes, n_top, X, m, F, out);
+  const int n_top = std::min(n_nodes, kTopNodes);
+  const size_t smem = (size_t)kTopNodes * sizeof(DNode) + (size_t)kSelThreads * (F | 1) * 4;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (m + kSelThreads - 1) / kSelThreads;
+  const int grid = (int)std::min<int64_t>(tiles, 2 * sms);
+  const bool vec = (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  switch (vec ? F : 0) {
+#define CASE(FF)                                                                              \
+  case FF:                                                                                    \
+    CUDA_CHECK(cudaFuncSetAttribute(select_kernel<FF>,                                        \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
+    select_kernel<FF><<<grid, kSelThreads, smem, s>>>(tree, n_top, X, m, out);                \
+    break;
+    CASE(4) CASE(8) CASE(12) CASE(16) CASE(20) CASE(24) CASE(32) CASE(48) CASE(64)
+#undef CASE
+    default:
+      CUDA_CHECK(cudaFuncSetAttribute(select_kernel_any,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      select_kernel_any<<<grid, kSelThreads, smem, s>>>(tree, n_top, X, m, F, out);
+  }
   CUDA_CHECK(cudaGetLastError());
 }
 

@@ -269,3 +269,38 @@ def generate_device(cfg: Config | str, row0: int, n: int, feat_ptr: int, times_p
 def region_rows(cfg: Config, r: int) -> np.ndarray:
     """Global row ids of region r (C2: region = row mod 3)."""
     return np.arange(r, cfg.N, cfg.regions, dtype=np.int64)
+
+
+def random_tree(cfg: Config | str, depth: int, seed: int = 6):
+    """SURVEY §8(d) C5 worst case: a complete tree of the given depth, BFS order;
+    internal node k splits on feature u24(seed, k, 0) % F at the midpoint of two
+    adjacent grid values of that feature; leaf labels u24(seed, k, 1) % V.
+    Returns a dict of numpy columns (feature, left, right, label, depth, threshold)."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    n = (1 << (depth + 1)) - 1
+    k = np.arange(n, dtype=np.uint64)
+    internal = k < np.uint64((1 << depth) - 1)
+    feat = (u24(seed, k, 0) % np.uint64(cfg.F)).astype(np.int32)
+    thr = np.zeros(n, np.float64)
+    for f in range(cfg.F):
+        g = cfg.grids[f].astype(np.float64)
+        sel = np.nonzero(internal & (feat == f))[0]
+        if len(g) < 2:
+            feat[sel] = (f + 1) % cfg.F
+            continue
+        j = (u24(seed, sel.astype(np.uint64), 2) % np.uint64(len(g) - 1)).astype(np.int64)
+        thr[sel] = (g[j] + g[j + 1]) / 2
+    # features whose grid has < 2 values were remapped above; recompute their thresholds
+    for f in range(cfg.F):
+        g = cfg.grids[f].astype(np.float64)
+        sel = np.nonzero(internal & (feat == f) & (thr == 0))[0]
+        if len(sel) and len(g) >= 2:
+            j = (u24(seed, sel.astype(np.uint64), 2) % np.uint64(len(g) - 1)).astype(np.int64)
+            thr[sel] = (g[j] + g[j + 1]) / 2
+    left = np.where(internal, 2 * k.astype(np.int64) + 1, -1).astype(np.int32)
+    right = np.where(internal, 2 * k.astype(np.int64) + 2, -1).astype(np.int32)
+    label = (u24(seed, k, 1) % np.uint64(cfg.V)).astype(np.int32)
+    dep = np.floor(np.log2(k.astype(np.float64) + 1)).astype(np.int32)
+    return dict(feature=np.where(internal, feat, -1).astype(np.int32), left=left, right=right,
+                label=label, depth=dep, threshold=np.where(internal, thr, 0.0))

@@ -190,6 +190,29 @@ def test_max_distinct_and_classes():
     full_parity(X, T, 3)
 
 
+@pytest.mark.parametrize("depth", [1, 12, 16])
+def test_select_synthetic_complete_tree(depth):
+    # a complete depth-16 tree (131071 nodes: deeper than the
+    # shared-memory top) on C4-shaped vectors, vs the oracle's walk
+    cfg = synth.CONFIGS["C4"]
+    cols = synth.random_tree(cfg, depth, seed=6)
+    tree = np.zeros(len(cols["feature"]), oracle.NODE_DTYPE)
+    for k, v in cols.items():
+        tree[k] = v
+    X, _ = synth.generate(cfg, 0, 300001, seed=7)
+    X[::97, 3] = np.nan  # NaN goes right (R8)
+    h = _region(cfg.F, cfg.V, depth)
+    ad.adapt_set_tree(h, tree)
+    out = torch.empty(len(X), dtype=torch.int32, device=DEV)
+    ad.adapt_select_batch(h, torch.from_numpy(X).to(DEV), len(X), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.select(tree, X))
+    hout = np.empty(len(X), np.int32)
+    ad.adapt_select_batch_host(h, X, len(X), hout)
+    assert np.array_equal(hout, oracle.select(tree, X))
+    ad.adapt_region_destroy(h)
+
+
 def test_errors():
     s = torch.cuda.current_stream()
     h = _region(1, 2, 2)
