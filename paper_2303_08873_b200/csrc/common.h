@@ -51,6 +51,8 @@ struct Seg {
   int32_t direct;      // 0: histogram rows going left, 1: right, 2: all rows, -1: none
   int32_t hslot;       // histogram slot of the direct child (-1: none)
   int32_t write;       // bit0: move left rows to the output planes, bit1: right rows
+  int32_t cmap;        // histogram pass: this node's class map (index into HistArgs::cmaps)
+  int32_t ncls;        // histogram pass: classes present in the node
 };
 
 // best cut of one (node, feature), exact key num/den (R13x)
@@ -82,16 +84,26 @@ void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int worl
 bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab);
 void launch_label_bin(const float *feat, const float *times, int64_t n, int F, int V, int BS,
                       const uint8_t *tab, const uint32_t *lk_mul, uint32_t *flags, uint8_t *bins,
-                      uint8_t *labels, cudaStream_t s);
-void launch_bins_out(const uint8_t *bins, int64_t n, int F, int BS, uint8_t *out, cudaStream_t s);
+                      size_t pstride, uint8_t *labels, cudaStream_t s);
+void launch_bins_out(const uint8_t *bins, size_t pstride, int64_t n, int F, int BS, uint8_t *out,
+                     cudaStream_t s);
+// bytes between the bins word planes of an n-row buffer (plane p = bytes [4p, 4p+4) of each row)
+inline size_t bins_plane_stride(int64_t n, int BS) {
+  const size_t wb = BS < 4 ? BS : 4;
+  return (((size_t)(n + 16) * wb) + 255) & ~(size_t)255;
+}
+inline size_t bins_bytes(int64_t n, int BS) {
+  return bins_plane_stride(n, BS) * (BS < 4 ? 1 : BS / 4);
+}
 
 // ---- kernel launchers (level.cu) ----
 struct PartArgs {            // a7: move the split parents' rows into the children's pieces
   const Seg *segs;           // pieces of the split parents (feat, thr, write set)
   int nseg;
   uint32_t total_rows;       // sum of the pieces' lengths (virtual positions)
-  const uint8_t *bins_in, *lab_in;  // input planes: [pos][BS], [pos]
+  const uint8_t *bins_in, *lab_in;  // input: bins word planes (see level.cu), labels [pos]
   uint8_t *bins_out, *lab_out;      // output planes, indexed by virtual position
+  size_t pstride;                   // bytes between bins word planes
   int BS, F;
   int32_t *visits;           // [nranges][max_visits][6]: seg, share [A, B), left, right moved
   int max_visits;
@@ -105,11 +117,12 @@ struct HistArgs {            // a4: class histograms of the given pieces' rows
   int nseg;
   uint32_t total_rows;
   const uint8_t *bins_in, *lab_in;
+  size_t pstride;            // bytes between bins word planes
   int BS, F, C;
   const int32_t *hoff;       // [F] counter offset of feature f in a node histogram
   const int32_t *nval;       // [F] distinct values of f
   const int4 *groups;        // [ngroups] x: first class, y: classes, z: padded stride, w: bins word
-  const int32_t *gsoff;      // [ngroups][F] smem offset of feature f in group g, -1 if absent
+  const uint8_t *cmaps;      // [nodes][2C]: class -> compact index (255 absent), compact -> class
   int ngroups;
   int smem_counters;         // max counters of a group
   uint32_t *H;               // [slots][HS]

@@ -216,6 +216,7 @@ struct FNode {  // a frontier node: histogrammed and split-searched at this leve
   int32_t depth;
   int32_t slot;  // histogram slot at this level
   bool direct;   // histogrammed from its rows (else parent - sibling)
+  std::vector<uint8_t> cls;  // classes present (ascending); empty = all
   std::vector<std::pair<uint32_t, uint32_t>> pieces;  // this rank's rows: (offset, length) in the planes
 };
 
@@ -235,7 +236,8 @@ struct adapt_region {
   const float *d_feat = nullptr, *d_times = nullptr;
   adapt::DevBuf own_feat, own_times;
   // products of the last train
-  int BS = 0;                   // bins row stride (F rounded up to a power of two)
+  int BS = 0;                   // bins per row incl. padding (F rounded up to a power of two)
+  size_t pstride = 0;           // bytes between the bins word planes
   int64_t trained_n = 0;
   adapt::DevBuf bins, labels;   // ingest output in row order (kept for introspection)
   adapt::DevBuf binsA, binsB, labA, labB;  // level planes, rows grouped by node span
@@ -248,7 +250,7 @@ struct adapt_region {
   // scratch
   adapt::DevBuf gkey, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, lk_keys, lk_mul,
       H0, H1, segs,
-      hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, psync, xa, xb, oa, ob;
+      hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, cmaps, psync, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall;
   // Table-1 shim state
   bool active = false;
@@ -434,7 +436,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
   h->gkey.ensure((size_t)F * kGSlots * 4);
   h->gcount.ensure((size_t)F * 4);
   h->flags.ensure(16);
-  h->bins.ensure((size_t)std::max<int64_t>(n, 1) * BS + 64);
+  const size_t pstride = bins_plane_stride(n, BS);
+  h->pstride = pstride;
+  h->bins.ensure(bins_bytes(n, BS));
   h->labels.ensure((size_t)std::max<int64_t>(n, 1) + 64);
   CUDA_CHECK(cudaMemsetAsync(h->gkey.p, 0xFF, (size_t)F * kGSlots * 4, s));
   CUDA_CHECK(cudaMemsetAsync(h->gcount.p, 0, (size_t)F * 4, s));
@@ -511,7 +515,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
   {
     Phase ph("ingest", s, (double)n * (4.0 * F + 4.0 * V + F + 1));  // algorithmic
     launch_label_bin(feat, times, n, F, V, BS, h->lk_keys.as<uint8_t>(), h->lk_mul.as<uint32_t>(),
-                     h->flags.as<uint32_t>(), h->bins.as<uint8_t>(), h->labels.as<uint8_t>(), s);
+                     h->flags.as<uint32_t>(), h->bins.as<uint8_t>(), pstride, h->labels.as<uint8_t>(), s);
   }
   check_flags();
 
@@ -585,8 +589,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
   // planes: the root is histogrammed from the ingest output; pass d >= 1 moves
   // the parents' rows from one plane pair into the other
   const uint8_t *bins_in = h->bins.as<uint8_t>(), *lab_in = h->labels.as<uint8_t>();
-  h->binsA.ensure((size_t)std::max<int64_t>(n, 1) * BS + 64);
-  h->binsB.ensure((size_t)std::max<int64_t>(n, 1) * BS + 64);
+  h->binsA.ensure(bins_bytes(n, BS));
+  h->binsB.ensure(bins_bytes(n, BS));
   h->labA.ensure((size_t)std::max<int64_t>(n, 1) + 64);
   h->labB.ensure((size_t)std::max<int64_t>(n, 1) + 64);
   int out_plane = 0;  // 0: A, 1: B
@@ -634,6 +638,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       pa.lab_in = lab_in;
       pa.bins_out = bo;
       pa.lab_out = lo;
+      pa.pstride = pstride;
       pa.BS = BS;
       pa.F = F;
       pa.nranges = partition_ranges(sms, total);
@@ -682,15 +687,29 @@ void train_region(adapt_region *h, cudaStream_t s) {
     }
     // ---- a4: histograms of the direct nodes (the root, or the smaller children) ----
     std::vector<Seg> hsegs;
+    std::vector<uint8_t> cmaps;  // per direct node: class -> compact index, compact -> class
     for (const auto &fn : frontier)
-      if (fn.direct)
+      if (fn.direct) {
+        const int ci = (int)(cmaps.size() / (2 * C));
+        cmaps.resize(cmaps.size() + 2 * C, 255);
+        uint8_t *m = &cmaps[(size_t)ci * 2 * C];
+        int nc = 0;
+        for (int k = 0; k < C; k++)
+          if (fn.cls.empty() || std::binary_search(fn.cls.begin(), fn.cls.end(), (uint8_t)k)) {
+            m[k] = (uint8_t)nc;
+            m[C + nc] = (uint8_t)k;
+            nc++;
+          }
         for (const auto &pc : fn.pieces) {
           Seg sg{};
           sg.off = pc.first;
           sg.len = pc.second;
           sg.hslot = fn.slot;
+          sg.cmap = ci;
+          sg.ncls = nc;
           hsegs.push_back(sg);
         }
+      }
     const uint32_t htotal = virtualize(hsegs, true);
     Hcur->ensure((size_t)A * HS * 4);
     h2d(h->slots, direct_slots, s);
@@ -706,13 +725,15 @@ void train_region(adapt_region *h, cudaStream_t s) {
       ha.total_rows = htotal;
       ha.bins_in = hist_bins;
       ha.lab_in = hist_lab;
+      ha.pstride = pstride;
       ha.BS = BS;
       ha.F = F;
       ha.C = C;
       ha.hoff = h->hoff.as<int32_t>();
       ha.nval = h->dnval.as<int32_t>();
       ha.groups = h->grp.as<int4>();
-      ha.gsoff = h->gsoff.as<int32_t>();
+      h2d(h->cmaps, cmaps, s);
+      ha.cmaps = h->cmaps.as<uint8_t>();
       ha.ngroups = ngroups;
       ha.smem_counters = max_group;
       ha.H = Hcur->as<uint32_t>();
@@ -810,13 +831,19 @@ void train_region(adapt_region *h, cudaStream_t s) {
       const int32_t hslot = (int32_t)ndirect.size();
       ndirect.push_back(hslot);
       int jl = -1, jr = -1;
+      auto present = [&](const std::vector<uint64_t> &Pc) {
+        std::vector<uint8_t> v;
+        for (int k = 0; k < C; k++)
+          if (Pc[k]) v.push_back((uint8_t)k);
+        return v;
+      };
       if (inL) {
         jl = (int)next.size();
-        next.push_back(FNode{li, fn.depth + 1, dir == 0 ? hslot : -1, dir == 0, {}});
+        next.push_back(FNode{li, fn.depth + 1, dir == 0 ? hslot : -1, dir == 0, present(PL), {}});
       }
       if (inR) {
         jr = (int)next.size();
-        next.push_back(FNode{li + 1, fn.depth + 1, dir == 1 ? hslot : -1, dir == 1, {}});
+        next.push_back(FNode{li + 1, fn.depth + 1, dir == 1 ? hslot : -1, dir == 1, present(PR), {}});
       }
       if (inL && inR) {  // the other child by subtraction from the parent
         nderived_j.push_back(dir == 0 ? jr : jl);
@@ -1214,7 +1241,7 @@ int adapt_get_bins(adapt_region_t *h, uint8_t *out, int64_t n) {
     if (!out || n != h->trained_n) throw Error(ADAPT_E_INVALID_ARG, "n must equal the trained row count");
     DevBuf tmp;
     tmp.ensure((size_t)n * h->F + 16);
-    launch_bins_out(h->bins.as<uint8_t>(), n, h->F, h->BS, tmp.as<uint8_t>(), 0);
+    launch_bins_out(h->bins.as<uint8_t>(), h->pstride, n, h->F, h->BS, tmp.as<uint8_t>(), 0);
     CUDA_CHECK(cudaMemcpy(out, tmp.p, (size_t)n * h->F, cudaMemcpyDeviceToHost));
   });
 }

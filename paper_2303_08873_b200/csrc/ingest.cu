@@ -14,8 +14,9 @@
 //                     (mbarrier pipeline, one persistent CTA per SM): a1 label =
 //                     lowest index of the minimum time, +inf = unmeasured (P:173,
 //                     R2, R3); a3 bin = rank of the value through the perfect
-//                     hash (two dependent byte loads, no misses, no atomics).  Writes bins
-//                     [N][BS] (BS = F rounded up to a power of two) and labels [N].
+//                     hash (two dependent byte loads, no misses, no atomics).  Writes the
+//                     bins as word planes (plane p = bytes [4p, 4p+4) of every row's
+//                     BS = F-rounded-up-to-a-power-of-two bins) and labels [N].
 // So every later pass works directly in rank space (bins == ranks).
 #include <algorithm>
 #include <cstring>
@@ -240,6 +241,7 @@ struct LabelBinArgs {
   const uint32_t *lk_mul;   // [F][2] their multipliers
   uint32_t *flags;
   uint8_t *bins, *labels;
+  size_t pstride;           // bytes between bins word planes
 };
 
 __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinArgs a) {
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
       }
       // ---- a3: rank of each of this lane's feature values ----
       const float *fr = tF + (size_t)r * F;
-      uint8_t *dst = a.bins + (row0 + r) * BS;
+      const int64_t row = row0 + r;
       if (vec_f) {
         for (int c = 0; c < per; c += 4) {
           const int f = q * per + c;
@@ -362,15 +364,15 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
           const int r1 = rank_of(f + 1, canon_key(x.y, local_flags, kFlagBadFeature));
           const int r2 = rank_of(f + 2, canon_key(x.z, local_flags, kFlagBadFeature));
           const int r3 = rank_of(f + 3, canon_key(x.w, local_flags, kFlagBadFeature));
-          *reinterpret_cast<uint32_t *>(dst + f) =
+          *reinterpret_cast<uint32_t *>(a.bins + (f / 4) * a.pstride + row * 4) =  // word plane f/4
               (uint32_t)(r0 & 0xFF) | ((uint32_t)(r1 & 0xFF) << 8) | ((uint32_t)(r2 & 0xFF) << 16) |
               ((uint32_t)(r3 & 0xFF) << 24);
         }
       } else {
-        for (int f = q; f < F; f += P) {
-          dst[f] = (uint8_t)rank_of(f, canon_key(fr[f], local_flags, kFlagBadFeature));
-        }
-        for (int f = F + q; f < BS; f += P) dst[f] = 0;
+        const int wb = BS < 4 ? BS : 4;  // bytes per plane element
+        for (int f = q; f < BS; f += P)
+          a.bins[(BS < 4 ? 0 : f / 4) * a.pstride + row * wb + (BS < 4 ? f : f % 4)] =
+              f < F ? (uint8_t)rank_of(f, canon_key(fr[f], local_flags, kFlagBadFeature)) : 0;
       }
     }
     __syncwarp();
@@ -380,11 +382,14 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
   if (local_flags) atomicOr(a.flags, local_flags);
 }
 
-__global__ void bins_out_kernel(const uint8_t *bins, int64_t n, int F, int BS, uint8_t *out) {
+__global__ void bins_out_kernel(const uint8_t *bins, size_t pstride, int64_t n, int F, int BS,
+                                uint8_t *out) {
+  const int wb = BS < 4 ? BS : 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * F;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / F;
-    out[i] = bins[r * BS + (int)(i - r * F)];
+    const int f = (int)(i - r * F);
+    out[i] = bins[(BS < 4 ? 0 : f / 4) * pstride + r * wb + (BS < 4 ? f : f % 4)];
   }
 }
 
@@ -493,7 +498,7 @@ void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int worl
 
 void launch_label_bin(const float *feat, const float *times, int64_t n, int F, int V, int BS,
                       const uint8_t *tab, const uint32_t *lk_mul, uint32_t *flags, uint8_t *bins,
-                      uint8_t *labels, cudaStream_t s) {
+                      size_t pstride, uint8_t *labels, cudaStream_t s) {
   if (n == 0) return;
   LabelBinArgs a;
   a.feat = feat;
@@ -506,6 +511,7 @@ void launch_label_bin(const float *feat, const float *times, int64_t n, int F, i
   a.lk_mul = lk_mul;
   a.flags = flags;
   a.bins = bins;
+  a.pstride = pstride;
   a.labels = labels;
   const size_t table = (128 + 8 * kMaxF + (size_t)F * kPhBytes + 15) & ~(size_t)15;
   // P threads per row, TR = threads / P rows per tile: the largest tile whose
@@ -524,9 +530,10 @@ void launch_label_bin(const float *feat, const float *times, int64_t n, int F, i
   CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_bins_out(const uint8_t *bins, int64_t n, int F, int BS, uint8_t *out, cudaStream_t s) {
+void launch_bins_out(const uint8_t *bins, size_t pstride, int64_t n, int F, int BS, uint8_t *out,
+                     cudaStream_t s) {
   if (n == 0) return;
-  bins_out_kernel<<<grid_for(n * F, 256, 148 * 16), 256, 0, s>>>(bins, n, F, BS, out);
+  bins_out_kernel<<<grid_for(n * F, 256, 148 * 16), 256, 0, s>>>(bins, pstride, n, F, BS, out);
   CUDA_CHECK(cudaGetLastError());
 }
 

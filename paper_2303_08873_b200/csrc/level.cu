@@ -15,13 +15,16 @@
 //                     u32 counters, 508 KB at C4) does not fit one SM, so G
 //                     CTAs share each row range: CTA g owns the 4 features of
 //                     32-bit word w(g) of the bins row (× a class slab), i.e.
-//                     at most 4 shared-memory reductions per row.  The G CTAs
+//                     at most 4 shared-memory reductions per row, reading only
+//                     that word's plane (4 bytes per row).  The G CTAs
 //                     of a range are co-resident (cooperative launch, one CTA
 //                     per SM) and re-synchronise every few iterations, so a
 //                     row fetched from HBM by one is served to the others
-//                     from L2.  Counters use an odd class stride (bank
-//                     spread) and are flushed into the node's global
-//                     histogram with integer atomics.
+//                     from L2.  Per node only the classes present in it get
+//                     counters (the host knows them from the parent's split),
+//                     with an odd class stride (bank spread); the block's
+//                     counters are flushed into the node's global histogram
+//                     with integer atomics.
 // Every quantity that decides the tree is an integer, so the result does not
 // depend on row order, on the number of ranks or on atomic ordering.
 #include <algorithm>
@@ -40,45 +43,34 @@ struct Row {  // one row's bins, BS bytes, in registers
   uint32_t w[N];
 };
 
+// Bins are stored in "word planes": plane p holds bytes [4p, 4p+4) of every
+// row's bins (BS >= 4), so any 32-bit word of a row is one coalesced load and a
+// pass that needs one word reads 4 bytes per row.  BS < 4: one plane of BS-byte rows.
 template <int BS>
-__device__ __forceinline__ void load_row(const uint8_t *__restrict__ p, Row<BS> &r) {
-  if constexpr (BS >= 16) {
+__device__ __forceinline__ void load_row(const uint8_t *__restrict__ base, size_t pstride,
+                                         uint32_t row, Row<BS> &r) {
+  if constexpr (BS >= 4) {
 #pragma unroll
-    for (int i = 0; i < BS / 16; i++) {
-      const uint4 v = *(reinterpret_cast<const uint4 *>(p) + i);
-      r.w[4 * i + 0] = v.x;
-      r.w[4 * i + 1] = v.y;
-      r.w[4 * i + 2] = v.z;
-      r.w[4 * i + 3] = v.w;
-    }
-  } else if constexpr (BS == 8) {
-    const uint2 v = *reinterpret_cast<const uint2 *>(p);
-    r.w[0] = v.x;
-    r.w[1] = v.y;
-  } else if constexpr (BS == 4) {
-    r.w[0] = *reinterpret_cast<const unsigned int *>(p);
+    for (int i = 0; i < BS / 4; i++)
+      r.w[i] = *reinterpret_cast<const uint32_t *>(base + i * pstride + (size_t)row * 4);
   } else if constexpr (BS == 2) {
-    r.w[0] = *reinterpret_cast<const unsigned short *>(p);
+    r.w[0] = *reinterpret_cast<const unsigned short *>(base + (size_t)row * 2);
   } else {
-    r.w[0] = *p;
+    r.w[0] = base[row];
   }
 }
 
 template <int BS>
-__device__ __forceinline__ void store_row(uint8_t *__restrict__ p, const Row<BS> &r) {
-  if constexpr (BS >= 16) {
+__device__ __forceinline__ void store_row(uint8_t *__restrict__ base, size_t pstride, uint32_t row,
+                                          const Row<BS> &r) {
+  if constexpr (BS >= 4) {
 #pragma unroll
-    for (int i = 0; i < BS / 16; i++)
-      __stcs(reinterpret_cast<uint4 *>(p) + i,
-             make_uint4(r.w[4 * i], r.w[4 * i + 1], r.w[4 * i + 2], r.w[4 * i + 3]));
-  } else if constexpr (BS == 8) {
-    __stcs(reinterpret_cast<uint2 *>(p), make_uint2(r.w[0], r.w[1]));
-  } else if constexpr (BS == 4) {
-    __stcs(reinterpret_cast<unsigned int *>(p), r.w[0]);
+    for (int i = 0; i < BS / 4; i++)
+      __stcs(reinterpret_cast<unsigned int *>(base + i * pstride + (size_t)row * 4), r.w[i]);
   } else if constexpr (BS == 2) {
-    *reinterpret_cast<unsigned short *>(p) = (unsigned short)r.w[0];
+    *reinterpret_cast<unsigned short *>(base + (size_t)row * 2) = (unsigned short)r.w[0];
   } else {
-    *p = (uint8_t)r.w[0];
+    base[row] = (uint8_t)r.w[0];
   }
 }
 
@@ -155,7 +147,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) 
           const uint32_t q = qb + u * blockDim.x + tid;
           label[u] = -1;
           if (q < q1) {
-            load_row<BS>(a.bins_in + (size_t)(sg.off + q) * BS, r[u]);
+            load_row<BS>(a.bins_in, a.pstride, sg.off + q, r[u]);
             label[u] = __ldcs(a.lab_in + sg.off + q);
           } else {
 #pragma unroll
@@ -176,7 +168,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) 
           const bool wl = (ml >> lane) & 1, wr = (mr >> lane) & 1;
           if (wl || wr) {
             const uint32_t pos = wl ? A + bl + __popc(ml & below) : B - 1 - (br + __popc(mr & below));
-            store_row<BS>(a.bins_out + (size_t)pos * BS, r[u]);
+            store_row<BS>(a.bins_out, a.pstride, pos, r[u]);
             __stcs(a.lab_out + pos, (uint8_t)label[u]);
           }
         }
@@ -205,45 +197,48 @@ constexpr int kSyncEvery = 8;
 template <int BS>
 __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
   extern __shared__ uint32_t sh[];  // [smem_counters] counters
-  __shared__ int32_t soff[kMaxF];   // this group's smem offset of feature f, -1 if absent
-  __shared__ int32_t sdf[kMaxF];    // distinct values of f
+  __shared__ uint8_t s_cmap[kMaxC + 1];  // this node: class -> compact index (255: absent)
+  __shared__ uint8_t s_inv[kMaxC + 1];   // compact index -> class
   const int tid = threadIdx.x;
   const int G = a.ngroups;
   const int g = blockIdx.x % G;
   const int range = blockIdx.x / G;
   const int4 grp = a.groups[g];  // x: first class, y: classes, z: padded class stride, w: word
-  const int k0 = grp.x, kw = grp.y, kwp = grp.z, w0 = grp.w;
+  const int k0 = grp.x, kw = grp.y, w0 = grp.w;
+  const bool compact = a.cmaps != nullptr && kw == a.C;  // per-node class compaction
   const int C = a.C;
-  int gcount = 0;
-  for (int f = 0; f < a.F; f++) {
-    const int o = a.gsoff[g * a.F + f];
-    if (tid == 0) {
-      soff[f] = o;
-      sdf[f] = a.nval[f];
-    }
-    if (o >= 0) gcount = max(gcount, o + a.nval[f] * kwp);
-  }
+  int Dw[4];  // distinct values of the 4 features of word w0 (0: absent)
+#pragma unroll
+  for (int e = 0; e < 4; e++) Dw[e] = (4 * w0 + e < a.F) ? a.nval[4 * w0 + e] : 0;
   const uint32_t R = (a.total_rows + a.nranges - 1) / a.nranges;
   uint32_t p0 = range * R;
   const uint32_t p1 = min(p0 + R, a.total_rows);
   int s = p0 < p1 ? first_seg(a.segs, a.nseg, p0) : a.nseg;
-  __syncthreads();
-  // shared-memory byte address of this group's counter block of each feature of word w0
   const uint32_t sbase = smem_u32(sh);
-  uint32_t abase[4];
-#pragma unroll
-  for (int e = 0; e < 4; e++) {
-    const int f = 4 * w0 + e;
-    abase[e] = (f < a.F && soff[f] >= 0) ? sbase + 4u * soff[f] : 0xFFFFFFFFu;
-  }
-  const bool all4 = abase[0] != 0xFFFFFFFFu && abase[1] != 0xFFFFFFFFu &&
-                    abase[2] != 0xFFFFFFFFu && abase[3] != 0xFFFFFFFFu;
-  const uint32_t kwp4 = 4u * kwp;
   uint32_t iter = 0, epoch = 0;
   while (p0 < p1 && s < a.nseg) {
     // ---- one node's rows at virtual positions [p0, pe) ----
     const Seg first = a.segs[s];
     const uint32_t pe = min(p1, first.node_base + first.node_len);
+    // this node's class layout: compact (only the classes present) or the slab
+    const int kc = compact ? first.ncls : kw;
+    const int kwp = kc | 1;  // odd stride: bank spread
+    if (compact) {
+      const uint8_t *m = a.cmaps + (size_t)first.cmap * 2 * C;
+      for (int k = tid; k < C; k += blockDim.x) {
+        s_cmap[k] = m[k];
+        s_inv[k] = m[C + k];
+      }
+    }
+    uint32_t abase[4];
+    int gcount = 0;
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      abase[e] = Dw[e] ? sbase + 4u * gcount : 0xFFFFFFFFu;
+      gcount += Dw[e] * kwp;
+    }
+    const bool all4 = Dw[0] && Dw[1] && Dw[2] && Dw[3];
+    const uint32_t kwp4 = 4u * kwp;
     for (int i = tid; i < gcount; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     for (; s < a.nseg && a.segs[s].row_base < pe; s++) {
@@ -268,17 +263,22 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
           label[u] = -1;
           w[u] = 0;
           if (q < q1) {
-            const uint8_t *p = a.bins_in + (size_t)(sg.off + q) * BS;
-            if constexpr (BS >= 4) w[u] = reinterpret_cast<const uint32_t *>(p)[w0];
-            else if constexpr (BS == 2) w[u] = *reinterpret_cast<const unsigned short *>(p);
-            else w[u] = *p;
+            const uint32_t row = sg.off + q;  // this CTA's word: one coalesced 4-byte load
+            if constexpr (BS >= 4)
+              w[u] = *reinterpret_cast<const uint32_t *>(a.bins_in + w0 * a.pstride + (size_t)row * 4);
+            else if constexpr (BS == 2)
+              w[u] = *reinterpret_cast<const unsigned short *>(a.bins_in + (size_t)row * 2);
+            else
+              w[u] = a.bins_in[row];
             label[u] = a.lab_in[sg.off + q];
           }
         }
 #pragma unroll
         for (int u = 0; u < kHistUnroll; u++) {
-          if ((unsigned)(label[u] - k0) >= (unsigned)kw) continue;  // no row / other slab
-          const uint32_t lk4 = 4u * (label[u] - k0);
+          if (label[u] < 0) continue;
+          const int lk = compact ? (int)s_cmap[label[u]] : label[u] - k0;
+          if ((unsigned)lk >= (unsigned)kc) continue;  // other class slab
+          const uint32_t lk4 = 4u * lk;
           if (all4) {
             red_shared_inc(abase[0] + ((w[u]) & 0xFF) * kwp4 + lk4);
             red_shared_inc(abase[1] + ((w[u] >> 8) & 0xFF) * kwp4 + lk4);
@@ -294,20 +294,21 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
       }
     }
     __syncthreads();
-    {  // flush: padded class slab -> the node's [f][rank][class] layout
+    {  // flush: the node's [f][rank][class] layout (compact index -> class)
       uint32_t *dst = a.H + (size_t)first.hslot * a.HS;
-      for (int f = 0; f < a.F; f++) {
-        const int o = soff[f];
-        if (o < 0) continue;
-        const int n = sdf[f] * kwp;
-        uint32_t *df = dst + a.hoff[f];
+      int o = 0;
+      for (int e = 0; e < 4; e++) {
+        if (!Dw[e]) continue;
+        const int n = Dw[e] * kwp;
+        uint32_t *df = dst + a.hoff[4 * w0 + e];
         for (int i = tid; i < n; i += blockDim.x) {
           const uint32_t val = sh[o + i];
           if (val) {
             const int rk = i / kwp, j = i - rk * kwp;
-            atomicAdd(df + rk * C + k0 + j, val);
+            atomicAdd(df + rk * C + (compact ? (int)s_inv[j] : k0 + j), val);
           }
         }
+        o += n;
       }
     }
     __syncthreads();

@@ -98,10 +98,8 @@ __global__ void __launch_bounds__(kSplitThreads)
   uint64_t nl = 0, sl = 0, sr = 0, ntot = 0;
   for (int c0 = 0; c0 < C; c0 += kClassChunk) {
     const int kc = min(kClassChunk, C - c0);
-    for (int e = t; e < Df * kc; e += kSplitThreads) {
-      const int r = e / kc, k = e - r * kc;
-      tile[r][k] = __ldg(h + (size_t)r * C + c0 + k);
-    }
+    if (lane < kc)  // warp w loads rows w, w+8, ...: lanes read consecutive classes
+      for (int r = w; r < Df; r += kSplitThreads / 32) tile[r][lane] = __ldg(h + (size_t)r * C + c0 + lane);
     __syncthreads();
     // prefix over bins: warp w scans rows [32w, 32w+32) of column `lane`
     const int r0 = w * 32, r1 = min(r0 + 32, Df);
