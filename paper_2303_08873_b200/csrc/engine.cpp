@@ -741,8 +741,11 @@ void train_region(adapt_region *h, cudaStream_t s) {
       // one CTA per SM; the ngroups CTAs of a range are co-resident (cooperative launch)
       ha.nranges = (int)std::max<int64_t>(1, std::min<int64_t>((htotal + 4095) / 4096,
                                                                std::max(1, sms / ngroups)));
+      // each CTA reads only its own word plane, so partner CTAs share just the
+      // 1-byte labels: no lockstep needed (ADAPT_HIST_SYNC=1 re-enables it)
       ha.sync = nullptr;
-      if (ngroups > 1 && ha.nranges * ngroups <= sms) {
+      static const bool want_sync = getenv("ADAPT_HIST_SYNC") != nullptr;
+      if (want_sync && ngroups > 1 && ha.nranges * ngroups <= sms) {
         h->psync.ensure((size_t)ha.nranges * 4);
         CUDA_CHECK(cudaMemsetAsync(h->psync.p, 0, (size_t)ha.nranges * 4, s));
         ha.sync = h->psync.as<uint32_t>();

@@ -191,8 +191,8 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) 
 
 // ------------------------------------------------------------ histogram --
 constexpr int kHistThreads = 1024;
-constexpr int kHistUnroll = 4;
-constexpr int kSyncEvery = 8;
+constexpr int kHistUnroll = 16;  // rows in flight per thread (the pass is latency-bound otherwise)
+constexpr int kSyncEvery = 2;  // iterations of kHistUnroll x 1024 rows between partner syncs
 
 template <int BS>
 __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
