@@ -166,20 +166,17 @@ def main():
     import torch.distributed as dist
 
     import paper_2303_08873_b200 as ad
+    from paper_2303_08873_b200 import dist as adist
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        uid = [ad.adapt_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ad.adapt_init(local, rank, world, uid[0])
-    else:
-        ad.adapt_init(local, 0, 1)
+    adist.init_nccl(local, rank, world)
 
     cfg = synth.CONFIGS[args.config]
     N = args.rows or (cfg.N if cfg.regions == 1 else len(synth.region_rows(cfg, 0)))
-    lo, hi = rank * N // world, (rank + 1) * N // world
+    lo, hi = adist.shard_bounds(N, rank, world)
     n = hi - lo
     stream = torch.cuda.current_stream()
     flat, off = cfg.grid_table
@@ -217,11 +214,7 @@ def main():
         barrier()
     ad.adapt_profile_enable(False)
     prof = ad.adapt_profile_get()
-    ms = e0.elapsed_time(e1) / args.steps
-    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms = float(ms_t.item())
+    ms = adist.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
     tree = ad.adapt_get_tree(h)
     levels = ad.adapt_train_stats(h)
 
@@ -246,11 +239,7 @@ def main():
         for _ in range(args.e2e_steps):
             step_host()
         barrier()
-        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
-        et = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e_ms = float(et.item())
+        e2e_ms = adist.max_over_ranks((time.perf_counter() - t0) * 1e3 / args.e2e_steps, dev)
         assert np.array_equal(hout.numpy(), out.cpu().numpy()), "e2e selections differ from device path"
         e2e = {"value": N / (e2e_ms / 1e3), "unit": "samples/s",
                "h2d_bytes_per_step": int(N * (4 * cfg.F + 4 * cfg.V) + N * 4 * cfg.F),
@@ -278,7 +267,7 @@ def main():
     alg_bytes = sum(v["bytes"] for v in kern.values()) / args.steps
     cpu = None
     if world == 1 and not args.no_cpu:
-        rows = {"C4": 600_000, "C3": 1_000_000}.get(args.config, N)
+        rows = {"C4": 1_500_000, "C3": 1_000_000}.get(args.config, N)  # ~20 s of oracle work
         v, dt = cpu_baseline(cfg, min(rows, N), cfg.D)
         cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
                "sample": f"first {min(rows, N)} rows of {args.config}: labels + depth-{cfg.D} exact "

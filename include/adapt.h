@@ -27,6 +27,7 @@
 #ifndef ADAPT_H
 #define ADAPT_H
 #include <stdint.h>
+#include <stddef.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -84,6 +85,27 @@ typedef struct {
 int adapt_init(int device, int rank, int world, const void *nccl_unique_id);
 /* Writes a fresh 128-byte ncclUniqueId into out (rank 0, before adapt_init). */
 int adapt_nccl_unique_id(void *out128);
+
+/* Host-staged collectives: the same multi-rank training (value
+ * tables all-gathered, per-level histograms and error flags summed) over a
+ * transport the CALLER provides instead of NCCL, e.g. torch.distributed gloo
+ * or MPI.  Used to run several ranks on ONE device (NCCL refuses duplicate
+ * GPUs), which is how the P-invariance of the tree is tested on a 1-GPU box.
+ * The library synchronises its stream, copies the operand to pinned host
+ * memory, calls the hook, and copies the result back; no kernel changes.
+ *   all_gather(send, recv, bytes, user): recv[r*bytes .. (r+1)*bytes) = rank r's
+ *     send (bytes each, rank order); recv has world*bytes bytes.
+ *   all_reduce_u64(buf, count, user): buf[i] = sum over ranks of buf[i]
+ *     (in place; the library widens its u32 operands to u64 for the call).
+ * Hooks return 0 on success; any other value -> ADAPT_E_NCCL.  The struct is
+ * copied; `user` is passed through untouched and must outlive adapt_finalize.
+ * Same rules as adapt_init otherwise (world >= 1, rank in [0,world)). */
+typedef struct {
+  int (*all_gather)(const void *send, void *recv, size_t bytes, void *user);
+  int (*all_reduce_u64)(uint64_t *buf, size_t count, void *user);
+  void *user;
+} adapt_host_comm_t;
+int adapt_init_host_comm(int device, int rank, int world, const adapt_host_comm_t *comm);
 /* Destroys every region and the NCCL communicator; frees device memory. */
 int adapt_finalize(void);
 const char *adapt_last_error(void);

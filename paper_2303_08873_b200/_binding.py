@@ -33,7 +33,8 @@ ADAPT_E_OOM = -11
 
 # the exported symbols of include/adapt.h (checked by tests/test_boundary.py)
 SYMBOLS = [
-    "adapt_init", "adapt_nccl_unique_id", "adapt_finalize", "adapt_last_error", "adapt_version",
+    "adapt_init", "adapt_nccl_unique_id", "adapt_init_host_comm", "adapt_finalize",
+    "adapt_last_error", "adapt_version",
     "adapt_region_create", "adapt_region_destroy", "adapt_region_info", "adapt_record",
     "adapt_record_table", "adapt_distinct_pairs", "adapt_train", "adapt_train_many",
     "adapt_select", "adapt_select_batch", "adapt_select_batch_host", "adapt_get_tree",
@@ -56,6 +57,17 @@ class adapt_phase_t(ctypes.Structure):
                 ("ms", ctypes.c_double), ("bytes", ctypes.c_double)]
 
 
+_ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                 ctypes.c_void_p)
+_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t,
+                                 ctypes.c_void_p)
+
+
+class adapt_host_comm_t(ctypes.Structure):
+    _fields_ = [("all_gather", _ALLGATHER_FN), ("all_reduce_u64", _ALLREDUCE_FN),
+                ("user", ctypes.c_void_p)]
+
+
 class AdaptError(RuntimeError):
     def __init__(self, code: int, call: str, msg: str):
         super().__init__(f"{call} -> {code}: {msg}")
@@ -69,6 +81,7 @@ _P, _I, _I64, _U64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uin
 _sigs = {
     "adapt_init": [_I, _I, _I, _P],
     "adapt_nccl_unique_id": [_P],
+    "adapt_init_host_comm": [_I, _I, _I, ctypes.POINTER(adapt_host_comm_t)],
     "adapt_finalize": [],
     "adapt_region_create": [ctypes.c_char_p, _I, _I, ctypes.c_char_p, _I, _P],
     "adapt_region_destroy": [_P],
@@ -155,6 +168,45 @@ def adapt_init(device: int = 0, rank: int = 0, world: int = 1, nccl_unique_id: b
     if nccl_unique_id is not None:
         buf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
     _check(_L.adapt_init(device, rank, world, ctypes.cast(buf, _P) if buf else None), "adapt_init")
+
+
+_host_comm_keepalive = None
+
+
+def adapt_init_host_comm(device: int, rank: int, world: int, all_gather, all_reduce_u64):
+    """Host-staged collectives (adapt.h adapt_init_host_comm).
+
+    all_gather(send: np.ndarray[uint8]) -> np.ndarray[uint8] of world*len(send)
+    bytes in rank order; all_reduce_u64(buf: np.ndarray[uint64]) -> the element-wise
+    sum over ranks (np.ndarray[uint64], same length).
+    Exceptions in a hook become a non-zero return (-> ADAPT_E_NCCL)."""
+    global _host_comm_keepalive
+
+    def _ag(send, recv, nbytes, _user):
+        try:
+            snd = np.ctypeslib.as_array(ctypes.cast(send, ctypes.POINTER(ctypes.c_uint8)), (nbytes,))
+            out = np.asarray(all_gather(snd.copy()), dtype=np.uint8).reshape(-1)
+            if out.size != world * nbytes:
+                return 2
+            ctypes.memmove(recv, out.ctypes.data, out.size)
+            return 0
+        except Exception:  # noqa: BLE001  (reported through the return code)
+            return 1
+
+    def _ar(buf, count, _user):
+        try:
+            a = np.ctypeslib.as_array(buf, (count,))
+            r = np.asarray(all_reduce_u64(a.copy()), dtype=np.uint64).reshape(-1)
+            if r.size != count:
+                return 2
+            a[:] = r
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    hooks = adapt_host_comm_t(_ALLGATHER_FN(_ag), _ALLREDUCE_FN(_ar), None)
+    _host_comm_keepalive = hooks  # the library keeps the function pointers
+    _check(_L.adapt_init_host_comm(device, rank, world, ctypes.byref(hooks)), "adapt_init_host_comm")
 
 
 def adapt_nccl_unique_id() -> bytes:

@@ -189,8 +189,67 @@ struct Ctx {
   bool inited = false;
   int device = 0, rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  bool host_comm = false;  // collectives through caller hooks (adapt_init_host_comm)
+  adapt_host_comm_t hooks{};
 };
 Ctx g_ctx;
+
+// ---- the three collectives of SURVEY §8(e), over NCCL or the host hooks ----
+void host_hook(int rc, const char *what) {
+  if (rc != 0) throw Error(ADAPT_E_NCCL, std::string(what) + ": host collective hook returned " +
+                                            std::to_string(rc));
+}
+
+// sum of `count` u32 (or u64 when wide) over ranks, in place on the device
+void comm_allreduce_sum(void *dbuf, size_t count, bool wide, cudaStream_t s, const char *what) {
+  if (g_ctx.world == 1 || count == 0) return;
+  if (!g_ctx.host_comm) {
+    g_nccl.check(g_nccl.AllReduce(dbuf, dbuf, count, wide ? ncclUint64 : ncclUint32, ncclSum,
+                                  g_ctx.comm, s), what);
+    return;
+  }
+  std::vector<uint64_t> w(count);
+  if (wide) {
+    CUDA_CHECK(cudaMemcpyAsync(w.data(), dbuf, count * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  } else {
+    std::vector<uint32_t> n(count);
+    CUDA_CHECK(cudaMemcpyAsync(n.data(), dbuf, count * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < count; i++) w[i] = n[i];
+  }
+  host_hook(g_ctx.hooks.all_reduce_u64(w.data(), count, g_ctx.hooks.user), what);
+  if (wide) {
+    CUDA_CHECK(cudaMemcpyAsync(dbuf, w.data(), count * 8, cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  } else {
+    std::vector<uint32_t> n(count);
+    for (size_t i = 0; i < count; i++) {
+      if (w[i] > 0xFFFFFFFFull) throw Error(ADAPT_E_NCCL, std::string(what) + ": u32 sum overflow");
+      n[i] = (uint32_t)w[i];
+    }
+    CUDA_CHECK(cudaMemcpyAsync(dbuf, n.data(), count * 4, cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+}
+
+// drecv[r*bytes, (r+1)*bytes) = rank r's dsend, on the device
+void comm_allgather(const void *dsend, void *drecv, size_t bytes, cudaStream_t s, const char *what) {
+  if (g_ctx.world == 1) {
+    CUDA_CHECK(cudaMemcpyAsync(drecv, dsend, bytes, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  if (!g_ctx.host_comm) {
+    g_nccl.check(g_nccl.AllGather(dsend, drecv, bytes, ncclUint8, g_ctx.comm, s), what);
+    return;
+  }
+  std::vector<uint8_t> snd(bytes), rcv(bytes * g_ctx.world);
+  CUDA_CHECK(cudaMemcpyAsync(snd.data(), dsend, bytes, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  host_hook(g_ctx.hooks.all_gather(snd.data(), rcv.data(), bytes, g_ctx.hooks.user), what);
+  CUDA_CHECK(cudaMemcpyAsync(drecv, rcv.data(), rcv.size(), cudaMemcpyHostToDevice, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+}
 
 void ensure_init() {
   if (g_ctx.inited) return;
@@ -421,7 +480,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     DevBuf tmp;
     tmp.ensure(8);
     CUDA_CHECK(cudaMemcpyAsync(tmp.p, &n_total, 8, cudaMemcpyHostToDevice, s));
-    g_nccl.check(g_nccl.AllReduce(tmp.p, tmp.p, 1, ncclUint64, ncclSum, g_ctx.comm, s), "allreduce n");
+    comm_allreduce_sum(tmp.p, 1, true, s, "allreduce n");
     CUDA_CHECK(cudaMemcpyAsync(&n_total, tmp.p, 8, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
   }
@@ -461,16 +520,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
     launch_collect_values(h->gkey.as<uint32_t>(), h->gcount.as<uint32_t>(), F,
                           h->lvals.as<float>(), h->lcnt.as<int32_t>(), s);
   }
-  if (world > 1) {
-    g_nccl.check(g_nccl.AllGather(h->lvals.p, h->avals.p, (size_t)F * kMaxBins, ncclFloat32,
-                                  g_ctx.comm, s), "allgather values");
-    g_nccl.check(g_nccl.AllGather(h->lcnt.p, h->acnt.p, (size_t)F, ncclInt32, g_ctx.comm, s),
-                 "allgather counts");
-  } else {
-    CUDA_CHECK(cudaMemcpyAsync(h->avals.p, h->lvals.p, (size_t)F * kMaxBins * 4,
-                               cudaMemcpyDeviceToDevice, s));
-    CUDA_CHECK(cudaMemcpyAsync(h->acnt.p, h->lcnt.p, (size_t)F * 4, cudaMemcpyDeviceToDevice, s));
-  }
+  comm_allgather(h->lvals.p, h->avals.p, (size_t)F * kMaxBins * 4, s, "allgather values");
+  comm_allgather(h->lcnt.p, h->acnt.p, (size_t)F * 4, s, "allgather counts");
   {
     Phase ph("merge", s, 0);
     launch_merge_values(h->avals.as<float>(), h->acnt.as<int32_t>(), world, F, h->dval.as<float>(),
@@ -486,7 +537,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     uint32_t bits[4] = {(hs[0] >> 0) & 1, (hs[0] >> 1) & 1, (hs[0] >> 2) & 1, (hs[0] >> 3) & 1};
     if (world > 1) {
       CUDA_CHECK(cudaMemcpyAsync(fl.p, bits, 16, cudaMemcpyHostToDevice, s));
-      g_nccl.check(g_nccl.AllReduce(fl.p, fl.p, 4, ncclUint32, ncclSum, g_ctx.comm, s), "allreduce flags");
+      comm_allreduce_sum(fl.p, 4, false, s, "allreduce flags");
       CUDA_CHECK(cudaMemcpyAsync(bits, fl.p, 16, cudaMemcpyDeviceToHost, s));
       CUDA_CHECK(cudaStreamSynchronize(s));
     }
@@ -755,8 +806,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       launch_hist(ha, s);
     }
     if (world > 1 && !direct_slots.empty())
-      g_nccl.check(g_nccl.AllReduce(Hcur->p, Hcur->p, (size_t)direct_slots.size() * HS,
-                                    ncclUint32, ncclSum, g_ctx.comm, s), "allreduce histograms");
+      comm_allreduce_sum(Hcur->p, (size_t)direct_slots.size() * HS, false, s, "allreduce histograms");
     if (!triples.empty()) {
       h2d(h->triples, triples, s);
       Phase ph("subtract", s, 0);
@@ -988,6 +1038,32 @@ int adapt_init(int device, int rank, int world, const void *nccl_unique_id) {
     g_ctx.device = device;
     g_ctx.rank = rank;
     g_ctx.world = world;
+    g_ctx.inited = true;
+  });
+}
+
+int adapt_init_host_comm(int device, int rank, int world, const adapt_host_comm_t *comm) {
+  return guarded([&] {
+    if (world < 1 || rank < 0 || rank >= world || device < 0)
+      throw Error(ADAPT_E_INVALID_ARG, "bad device/rank/world");
+    if (!comm || !comm->all_gather || !comm->all_reduce_u64)
+      throw Error(ADAPT_E_INVALID_ARG, "null host collective hooks");
+    if (g_ctx.inited) {
+      if (g_ctx.world == 1 && g_regions.empty()) g_ctx.inited = false;
+      else throw Error(ADAPT_E_USAGE, "already initialised; call adapt_finalize first");
+    }
+    int n = 0;
+    CUDA_CHECK(cudaGetDeviceCount(&n));
+    if (device >= n) throw Error(ADAPT_E_INVALID_ARG, "no such device");
+    CUDA_CHECK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw Error(ADAPT_E_CUDA, "libadapt is built for sm_100a (B200) only");
+    g_ctx.device = device;
+    g_ctx.rank = rank;
+    g_ctx.world = world;
+    g_ctx.host_comm = true;
+    g_ctx.hooks = *comm;
     g_ctx.inited = true;
   });
 }

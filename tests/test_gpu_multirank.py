@@ -1,0 +1,138 @@
+"""Multi-rank training parity on ONE GPU (test T3 "P-invariant
+tree").  World ranks run as separate processes sharing cuda:0, each recording
+its contiguous shard; the library's collectives (value-table all-gather,
+per-level histogram and error-flag sums) go through the host-staged hooks of
+adapt_init_host_comm over gloo — NCCL refuses two ranks on one device, and the
+collective arithmetic is the same integer sum either way.  Every rank must
+return the oracle's tree for the WHOLE table, labels / bins of its own shard,
+and the oracle's selections for its shard; errors raised by one rank's data
+must fail every rank with the same code."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, job, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2303_08873_b200 as ad
+    from paper_2303_08873_b200 import dist as adist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        adist.init_host_comm(0, rank, world)
+        X, T, D = job["X"], job["T"], job["D"]
+        lo, hi = adist.shard_bounds(len(X), rank, world)
+        Xs, Ts = np.ascontiguousarray(X[lo:hi]), np.ascontiguousarray(T[lo:hi])
+        n, F = Xs.shape
+        h = ad.adapt_region_create("mr", F, T.shape[1], f"dtree,depth={D}", 0)
+        s = torch.cuda.current_stream()
+        dX = torch.from_numpy(Xs).cuda()
+        if job.get("host"):
+            ad.adapt_record_table(h, Xs, Ts, n, False, s)
+        else:
+            ad.adapt_record_table(h, dX, torch.from_numpy(Ts).cuda(), n, True, s)
+        out = {"lo": lo, "hi": hi}
+        try:
+            ad.adapt_train(h, s)
+        except ad.AdaptError as e:
+            out["error"] = e.code
+            q.put((rank, out))
+            return
+        out["tree"] = ad.adapt_get_tree(h)
+        out["labels"] = ad.adapt_get_labels(h, n)
+        out["bins"] = ad.adapt_get_bins(h, n, F)
+        sel = torch.empty(n, dtype=torch.int32, device="cuda")
+        ad.adapt_select_batch(h, dX, n, sel, s)
+        torch.cuda.synchronize()
+        out["select"] = sel.cpu().numpy()
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, job):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, job, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def _check(res, X, T, D):
+    y = oracle.labels(T)
+    ref = oracle.train(X, y, T.shape[1], D)
+    bins = oracle.bins(X)
+    for r, o in sorted(res.items()):
+        lo, hi = o["lo"], o["hi"]
+        assert "error" not in o, f"rank {r} failed: {o.get('error')}"
+        got = o["tree"]
+        assert len(got) == len(ref), f"rank {r}: {len(got)} nodes vs oracle {len(ref)}"
+        for k in ("feature", "left", "right", "label", "depth", "n"):
+            assert np.array_equal(got[k], ref[k]), f"rank {r}: {k} differs"
+        assert got["threshold"].tobytes() == ref["threshold"].tobytes()
+        np.testing.assert_allclose(got["gini"], ref["gini"], rtol=1e-12, atol=0)
+        assert np.array_equal(o["labels"], y[lo:hi]), f"rank {r}: labels"
+        assert np.array_equal(o["bins"], bins[lo:hi]), f"rank {r}: bins (global value table)"
+        assert np.array_equal(o["select"], oracle.select(ref, X[lo:hi])), f"rank {r}: select"
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_p_invariant_tree_c3(world):
+    X, T = synth.generate("C3", 0, 200_003)
+    _check(_run(world, {"X": X, "T": T, "D": 12}), X, T, 12)
+
+
+def test_p_invariant_tree_c4_slice_host_records():
+    X, T = synth.generate("C4", 0, 60_001)
+    _check(_run(2, {"X": X, "T": T, "D": 12, "host": True}), X, T, 12)
+
+
+def test_empty_shard_rank():
+    # 1 row over 2 ranks: rank 0 records an empty shard, the tree is one leaf
+    X, T = synth.generate("C1", 0, 1)
+    _check(_run(2, {"X": X, "T": T, "D": 4}), X, T, 4)
+
+
+def test_errors_fail_every_rank():
+    X, T = synth.generate("C3", 0, 4000)
+    X = X.copy()
+    X[3500, 2] = np.nan  # in rank 1's shard only
+    res = _run(2, {"X": X, "T": T, "D": 4})
+    assert [res[r].get("error") for r in range(2)] == [-6, -6]
+    # each shard has <= 256 distinct values of feature 0, the union has 300
+    X, T = synth.generate("C3", 0, 600)
+    X = X.copy()
+    X[:300, 0] = np.arange(300, dtype=np.float32) % 200          # rank 0: 0..199
+    X[300:, 0] = 100 + np.arange(300, dtype=np.float32) % 200    # rank 1: 100..299
+    res = _run(2, {"X": X, "T": T, "D": 4})
+    assert [res[r].get("error") for r in range(2)] == [-7, -7]
