@@ -49,6 +49,18 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch, from the latest
+    committed ncu --set full captures (profiles/roundNN/ncu_traffic.json)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "round*", "ncu_traffic.json")))
+    if not files:
+        return {}
+    with open(files[-1]) as fh:
+        return json.load(fh)
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -259,12 +271,26 @@ def main():
     d = kern[dom]
     achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 and d["bytes"] > 0 else None
     step_ms_phases = {k: round(v["ms"] / args.steps, 4) for k, v in kern.items()}
+    traffic = ncu_traffic().get(dom.split("_L")[0])
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                "traffic_source": (f'{traffic["source"]} ({traffic["capture"]}, one ncu --set full '
+                                   f'capture)') if traffic else None,
                 "peak_source": peak_src,
                 "bytes_per_launch": d["bytes"] / max(d["launches"], 1),
                 "ms_per_launch": d["ms"] / max(d["launches"], 1)}
     alg_bytes = sum(v["bytes"] for v in kern.values()) / args.steps
+    # the whole level loop against SURVEY §8(d)'s level figure: (F+1) bytes per
+    # row of a split node per level (the partition/histogram split of this
+    # design moves 2(F+1) + reads ~(F+4)/2 per row)
+    loop_ms = sum(step_ms_phases.get(k, 0) for k in ("partition", "hist", "zero", "subtract", "split",
+                                                   "winner"))
+    loop_rows = sum((lv["rows_part"] if i else n) for i, lv in enumerate(levels) if lv["nodes"])
+    loop_bytes = (cfg.F + 1) * loop_rows * world
+    level_loop = {"survey_bytes_per_step": loop_bytes, "ms_per_step": loop_ms,
+                  "achieved_gbs": loop_bytes / (loop_ms / 1e3) / 1e9 if loop_ms else None,
+                  "frac": loop_bytes / (loop_ms / 1e3) / 1e9 / peak if loop_ms else None}
     cpu = None
     if world == 1 and not args.no_cpu:
         rows = {"C4": 1_500_000, "C3": 1_000_000}.get(args.config, N)  # ~20 s of oracle work
@@ -289,6 +315,7 @@ def main():
         "gpu_launches": int(sum(v["launches"] for v in kern.values())),
         "gpu_launches_per_step": sum(v["launches"] for v in kern.values()) / args.steps,
         "roofline": roofline,
+        "level_loop_roofline": level_loop,
         "cpu_baseline": cpu,
         "phase_ms_per_step": step_ms_phases,
         "tree_nodes": int(len(tree)),

@@ -16,11 +16,11 @@
 //                     CTAs share each row range: CTA g owns the 4 features of
 //                     32-bit word w(g) of the bins row (× a class slab), i.e.
 //                     at most 4 shared-memory reductions per row, reading only
-//                     that word's plane (4 bytes per row).  The G CTAs
-//                     of a range are co-resident (cooperative launch, one CTA
-//                     per SM) and re-synchronise every few iterations, so a
-//                     row fetched from HBM by one is served to the others
-//                     from L2.  Per node only the classes present in it get
+//                     that word's plane (4 bytes per row), so the G CTAs
+//                     of a range share only the 1-byte labels and run
+//                     unsynchronised (ADAPT_HIST_SYNC=1 restores an optional
+//                     lockstep through a global counter; it measured slower
+//                     once bins became word planes).  Per node only the classes present in it get
 //                     counters (the host knows them from the parent's split),
 //                     with an odd class stride (bank spread); the block's
 //                     counters are flushed into the node's global histogram
