@@ -6,10 +6,10 @@
 // the largest float32 <= the double threshold, which makes the float compare
 // exact (V:A5).  The first kTopNodes nodes (the top levels every walk visits;
 // a whole depth-12 tree) sit in shared memory, deeper ones are read through
-// L1/L2.  Vectors stream through a register-prefetched, double-buffered tile:
-// while the block walks tile k out of shared memory (odd row stride: no bank
-// conflicts between lanes), the coalesced 16-byte loads of tile k+1 are in
-// flight.
+// L1/L2.  Every warp owns its tiles of 64 vectors (no block barriers): the
+// coalesced 16-byte loads of the next tile sit in registers while the lanes
+// walk the current one out of the warp's odd-stride shared-memory tile, two
+// independent walks per lane interleaved to hide the dependent smem latency.
 #include <algorithm>
 
 #include "common.h"
@@ -17,8 +17,10 @@
 namespace adapt {
 namespace {
 
-constexpr int kSelThreads = 512;
-constexpr int kTopNodes = 8191;  // 64 KB
+constexpr int kSelThreads = 1024;  // one CTA per SM: one smem copy of the tree
+constexpr int kSelChains = 2;      // vectors walked at once per lane
+constexpr int kAnyThreads = 256;   // generic-F kernel
+constexpr int kTopNodes = 8191;    // 64 KB
 
 __device__ __forceinline__ DNode ldg_node(const DNode *p) {
   const int2 v = __ldg(reinterpret_cast<const int2 *>(p));
@@ -29,64 +31,82 @@ __device__ __forceinline__ DNode ldg_node(const DNode *p) {
 }
 
 template <int F>
-__global__ void __launch_bounds__(kSelThreads, 2)
+__global__ void __launch_bounds__(kSelThreads, 1)
     select_kernel(const DNode *__restrict__ gtree, int n_top, const float *__restrict__ X,
                   int64_t m, int32_t *__restrict__ out) {
   extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int kStride = F | 1;                   // odd row stride of the tile
+  constexpr int kStride = F | 1;                   // odd row stride of a warp's tile
   constexpr int kVec = F / 4;                      // float4 per vector
+  constexpr int kRows = 32 * kSelChains;           // vectors per warp tile
+  constexpr int kLd = kRows * kVec / 32;           // float4 loads per lane per tile
   DNode *st = reinterpret_cast<DNode *>(smem);     // [n_top]
-  float *sx = reinterpret_cast<float *>(smem + (size_t)kTopNodes * sizeof(DNode));  // [T][kStride]
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  float *sx = reinterpret_cast<float *>(smem + (size_t)kTopNodes * sizeof(DNode)) +
+              (size_t)warp * kRows * kStride;      // this warp's [kRows][kStride]
   for (int i = t; i < n_top; i += kSelThreads) st[i] = gtree[i];
+  __syncthreads();  // the only block barrier: tree copy visible
 
-  const int64_t ntiles = (m + kSelThreads - 1) / kSelThreads;
-  float4 pre[kVec];  // this thread's share of the next tile (coalesced float4s)
+  // warps own tiles of kRows vectors; no block barriers in the loop
+  const int64_t ntiles = (m + kRows - 1) / kRows;
+  const int64_t nwarps = (int64_t)gridDim.x * (kSelThreads / 32);
+  float4 pre[kLd];
   auto fetch = [&](int64_t tile) {
-    const int64_t v0 = tile * kSelThreads;
-    const int rows = (m - v0 < kSelThreads) ? (int)(m - v0) : kSelThreads;
+    const int64_t v0 = tile * kRows;
+    const int rows = (m - v0 < kRows) ? (int)(m - v0) : kRows;
     const float4 *src = reinterpret_cast<const float4 *>(X + v0 * F);
 #pragma unroll
-    for (int k = 0; k < kVec; k++) {
-      const int i = t + k * kSelThreads;  // float4 index within the tile
+    for (int k = 0; k < kLd; k++) {
+      const int i = lane + 32 * k;  // float4 index within the tile: coalesced
       pre[k] = i < rows * kVec ? __ldcs(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
-  auto stash = [&]() {
+  int64_t tile = blockIdx.x * (int64_t)(kSelThreads / 32) + warp;
+  if (tile < ntiles) fetch(tile);
+  for (; tile < ntiles; tile += nwarps) {
+    __syncwarp();  // previous tile's walks done before it is overwritten
 #pragma unroll
-    for (int k = 0; k < kVec; k++) {
-      const int i = t + k * kSelThreads, r = i / kVec, c = (i % kVec) * 4;
+    for (int k = 0; k < kLd; k++) {
+      const int i = lane + 32 * k, r = i / kVec, c = (i % kVec) * 4;
       float *d = sx + r * kStride + c;
       d[0] = pre[k].x;
       d[1] = pre[k].y;
       d[2] = pre[k].z;
       d[3] = pre[k].w;
     }
-  };
-  int64_t tile = blockIdx.x;
-  if (tile < ntiles) fetch(tile);
-  __syncthreads();  // tree copy visible
-  for (; tile < ntiles; tile += gridDim.x) {
-    stash();
-    __syncthreads();
-    if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);  // next tile in flight during the walks
-    const int64_t v = tile * kSelThreads + t;
-    if (v < m) {
-      const float *x = sx + t * kStride;
-      DNode nd = st[0];
-      while (nd.meta >= 0) {
-        const float xv = x[nd.meta & 63];
-        const int k = (nd.meta >> 6) + (xv <= nd.thr ? 0 : 1);
-        nd = k < n_top ? st[k] : ldg_node(gtree + k);
-      }
-      __stcs(out + v, -1 - nd.meta);
+    __syncwarp();
+    if (tile + nwarps < ntiles) fetch(tile + nwarps);  // next tile in flight during the walks
+    const int64_t v0 = tile * kRows;
+    // kSelChains independent walks per lane, interleaved for latency hiding
+    const float *x[kSelChains];
+    DNode nd[kSelChains];
+    bool live[kSelChains];
+#pragma unroll
+    for (int c = 0; c < kSelChains; c++) {
+      x[c] = sx + (lane + 32 * c) * kStride;
+      nd[c] = st[0];
+      live[c] = v0 + lane + 32 * c < m;
     }
-    __syncthreads();
+    bool any = true;
+    while (any) {
+      any = false;
+#pragma unroll
+      for (int c = 0; c < kSelChains; c++) {
+        if (nd[c].meta >= 0) {
+          const float xv = x[c][nd[c].meta & 63];
+          const int k = (nd[c].meta >> 6) + (xv <= nd[c].thr ? 0 : 1);
+          nd[c] = k < n_top ? st[k] : ldg_node(gtree + k);
+          any |= nd[c].meta >= 0;
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kSelChains; c++)
+      if (live[c]) __stcs(out + v0 + lane + 32 * c, -1 - nd[c].meta);
   }
 }
 
 // generic F (not a multiple of 4, or an unaligned X): scalar staging
-__global__ void __launch_bounds__(kSelThreads, 2)
+__global__ void __launch_bounds__(kAnyThreads, 1)
     select_kernel_any(const DNode *__restrict__ gtree, int n_top, const float *__restrict__ X,
                       int64_t m, int F, int32_t *__restrict__ out) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -94,11 +114,11 @@ __global__ void __launch_bounds__(kSelThreads, 2)
   DNode *st = reinterpret_cast<DNode *>(smem);
   float *sx = reinterpret_cast<float *>(smem + (size_t)kTopNodes * sizeof(DNode));
   const int t = threadIdx.x;
-  for (int i = t; i < n_top; i += kSelThreads) st[i] = gtree[i];
-  for (int64_t v0 = blockIdx.x * (int64_t)kSelThreads; v0 < m; v0 += (int64_t)gridDim.x * kSelThreads) {
-    const int rows = (m - v0 < kSelThreads) ? (int)(m - v0) : kSelThreads;
+  for (int i = t; i < n_top; i += kAnyThreads) st[i] = gtree[i];
+  for (int64_t v0 = blockIdx.x * (int64_t)kAnyThreads; v0 < m; v0 += (int64_t)gridDim.x * kAnyThreads) {
+    const int rows = (m - v0 < kAnyThreads) ? (int)(m - v0) : kAnyThreads;
     __syncthreads();
-    for (int i = t; i < rows * F; i += kSelThreads) {
+    for (int i = t; i < rows * F; i += kAnyThreads) {
       const int r = i / F, c = i - r * F;
       sx[r * stride + c] = __ldcs(X + v0 * F + i);
     }
@@ -121,26 +141,33 @@ void launch_select(const DNode *tree, int n_nodes, const float *X, int64_t m, in
                    cudaStream_t s) {
   if (m == 0) return;
   const int n_top = std::min(n_nodes, kTopNodes);
-  const size_t smem = (size_t)kTopNodes * sizeof(DNode) + (size_t)kSelThreads * (F | 1) * 4;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t tiles = (m + kSelThreads - 1) / kSelThreads;
-  const int grid = (int)std::min<int64_t>(tiles, 2 * sms);
   const bool vec = (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  const size_t tree_b = (size_t)kTopNodes * sizeof(DNode);
+  // F <= 16, 16-byte aligned X: per-warp tiles, one 1024-thread CTA per SM
+  const int64_t wtiles = (m + 32 * kSelChains - 1) / (32 * kSelChains);
+  const int vgrid = (int)std::min<int64_t>((wtiles + kSelThreads / 32 - 1) / (kSelThreads / 32), sms);
   switch (vec ? F : 0) {
-#define CASE(FF)                                                                              \
-  case FF:                                                                                    \
-    CUDA_CHECK(cudaFuncSetAttribute(select_kernel<FF>,                                        \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
-    select_kernel<FF><<<grid, kSelThreads, smem, s>>>(tree, n_top, X, m, out);                \
-    break;
-    CASE(4) CASE(8) CASE(12) CASE(16) CASE(20) CASE(24) CASE(32) CASE(48) CASE(64)
+#define CASE(FF)                                                                               \
+  case FF: {                                                                                   \
+    const size_t smem = tree_b + (size_t)kSelThreads * kSelChains * (FF | 1) * 4;              \
+    CUDA_CHECK(cudaFuncSetAttribute(select_kernel<FF>,                                         \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
+    select_kernel<FF><<<vgrid, kSelThreads, smem, s>>>(tree, n_top, X, m, out);                \
+    break;                                                                                     \
+  }
+    CASE(4) CASE(8) CASE(12) CASE(16)
 #undef CASE
-    default:
+    default: {
+      const size_t smem = tree_b + (size_t)kAnyThreads * (F | 1) * 4;
+      const int64_t tiles = (m + kAnyThreads - 1) / kAnyThreads;
+      const int grid = (int)std::min<int64_t>(tiles, sms);
       CUDA_CHECK(cudaFuncSetAttribute(select_kernel_any,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      select_kernel_any<<<grid, kSelThreads, smem, s>>>(tree, n_top, X, m, F, out);
+      select_kernel_any<<<grid, kAnyThreads, smem, s>>>(tree, n_top, X, m, F, out);
+    }
   }
   CUDA_CHECK(cudaGetLastError());
 }
