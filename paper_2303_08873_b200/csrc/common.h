@@ -70,7 +70,8 @@ struct NodeRes {
   uint64_t n;               // rows in node (global)
   uint64_t nL;              // rows left of the winning cut
   int32_t valid, feat, b_lo, b_hi;
-  // followed in memory by uint32 P[C] (class totals) and uint32 cL[C]
+  // followed in memory by uint32 P[kc] (class totals) and uint32 cL[kc], compact
+  // class order (res_stride leaves room for C of each)
 };
 
 // ---- kernel launchers (ingest.cu) ----
@@ -112,35 +113,45 @@ struct PartArgs {            // a7: move the split parents' rows into the childr
 int partition_ranges(int sms, uint32_t total_rows);
 void launch_partition(const PartArgs &a, cudaStream_t s);
 
+// Node histograms are stored class-compacted: node j with kc_j present classes
+// (ascending class ids) is a [DS][kc_j] u32 matrix, DS = sum_f D_f; feature f's
+// rows are [cumD_f, cumD_f + D_f), row = rank, column = compact class index.
+// A level's nodes are concatenated: node j at element offset off_j.
 struct HistArgs {            // a4: class histograms of the given pieces' rows
-  const Seg *segs;           // pieces (off, len, row_base, node_base/len, hslot), grouped by node
+  const Seg *segs;           // pieces (off, len, row_base, node_base/len, hslot, cmap, ncls), grouped by node
   int nseg;
   uint32_t total_rows;
   const uint8_t *bins_in, *lab_in;
   size_t pstride;            // bytes between bins word planes
   int BS, F, C;
-  const int32_t *hoff;       // [F] counter offset of feature f in a node histogram
+  const int32_t *cumD;       // [F] first histogram row of feature f
   const int32_t *nval;       // [F] distinct values of f
-  const int4 *groups;        // [ngroups] x: first class, y: classes, z: padded stride, w: bins word
-  const uint8_t *cmaps;      // [nodes][2C]: class -> compact index (255 absent), compact -> class
+  const int4 *groups;        // [ngroups] x: first compact class, y: classes, z: padded stride, w: bins word
+  const uint8_t *cmaps;      // [direct nodes][C]: class -> compact index (255: absent)
   int ngroups;
   int smem_counters;         // max counters of a group
-  uint32_t *H;               // [slots][HS]
-  int64_t HS;
+  uint32_t *H;               // level histograms
+  const int64_t *soff;       // [slots] element offset of a slot's matrix in H
   int nranges;               // CTA groups; CTA x handles range x / ngroups, group x % ngroups
   uint32_t *sync;            // [nranges] partner-sync counters, zeroed (null: no sync)
 };
 void launch_hist(const HistArgs &a, cudaStream_t s);
 
+struct SubJob {              // derived node = parent - direct sibling, class-remapped
+  int64_t off_d, off_p, off_s;  // element offsets: derived (H), parent (Hprev), sibling (H)
+  int32_t kc_d, kc_p, kc_s;     // their class counts
+  int32_t map;                  // first entry in the map array: per derived class
+};                              // (parent column, sibling column or -1) as int16 pairs
+
 // ---- kernel launchers (train.cu) ----
-void launch_zero_slots(uint32_t *H, int64_t HS, const int32_t *slots, int n, cudaStream_t s);
-void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t HS, const int32_t *triples,
-                     int n, cudaStream_t s);
-void launch_split(const uint32_t *H, int64_t HS, const int32_t *node_slot, int nnodes, int F,
-                  int C, const int32_t *hoff, const int32_t *nval, SplitCand *out,
-                  cudaStream_t s);
-void launch_winner(const uint32_t *H, int64_t HS, const int32_t *node_slot, int nnodes, int F,
-                   int C, const int32_t *hoff, const int32_t *nval, const SplitCand *cand,
+void launch_zero_slots(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS, int n,
+                       int64_t max_elems, cudaStream_t s);
+void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t DS, const SubJob *jobs,
+                     const int16_t *maps, int n, int64_t max_elems, cudaStream_t s);
+void launch_split(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,
+                  int F, const int32_t *cumD, const int32_t *nval, SplitCand *out, cudaStream_t s);
+void launch_winner(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,
+                   int F, int C, const int32_t *cumD, const int32_t *nval, const SplitCand *cand,
                    uint8_t *res, int res_stride, cudaStream_t s);
 
 // ---- kernel launchers (select.cu) ----

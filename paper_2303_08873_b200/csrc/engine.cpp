@@ -13,6 +13,7 @@
 #include <time.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -76,6 +77,34 @@ struct HostBuf {  // pinned staging for small D2H copies
   ~HostBuf() {
     if (p) cudaFreeHost(p);
   }
+};
+
+// Per-level small host -> device arrays, gathered into one pinned buffer and
+// uploaded with ONE async copy (a pageable cudaMemcpyAsync per array cost
+// ~15 us of host time each, with the GPU idle).  Offsets are stable; device
+// pointers are formed after flush().  The caller synchronises the stream
+// before the next put() round (every level does).
+struct Arena {
+  std::vector<uint8_t> stage;
+  HostBuf pinned;
+  DevBuf dev;
+  template <class T>
+  size_t put(const std::vector<T> &v) {
+    const size_t off = (stage.size() + 15) & ~size_t(15);
+    stage.resize(off + v.size() * sizeof(T) + 16);
+    if (!v.empty()) memcpy(stage.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+  }
+  void flush(cudaStream_t s) {
+    if (stage.empty()) return;
+    pinned.ensure(stage.size());
+    dev.ensure(stage.size());
+    memcpy(pinned.p, stage.data(), stage.size());
+    CUDA_CHECK(cudaMemcpyAsync(dev.p, pinned.p, stage.size(), cudaMemcpyHostToDevice, s));
+  }
+  template <class T>
+  T *ptr(size_t off) const { return reinterpret_cast<T *>(static_cast<uint8_t *>(dev.p) + off); }
+  void reset() { stage.clear(); }
 };
 
 thread_local std::string g_last_error;
@@ -270,13 +299,33 @@ void ensure_init() {
 // ------------------------------------------------------------ regions --
 constexpr int kHistSmemBudget = 200 * 1024;  // counters + LUT per level-pass CTA (1 CTA/SM)
 
+struct ClassSet {  // classes present in a node (C <= 255), ascending = compact order
+  uint64_t bits[4] = {0, 0, 0, 0};
+  void add(int c) { bits[c >> 6] |= 1ull << (c & 63); }
+  bool has(int c) const { return (bits[c >> 6] >> (c & 63)) & 1; }
+  int count() const {
+    return __builtin_popcountll(bits[0]) + __builtin_popcountll(bits[1]) +
+           __builtin_popcountll(bits[2]) + __builtin_popcountll(bits[3]);
+  }
+  int rank(int c) const {  // compact column of class c (number of present classes below it)
+    int r = 0;
+    for (int w = 0; w < (c >> 6); w++) r += __builtin_popcountll(bits[w]);
+    return r + __builtin_popcountll(bits[c >> 6] & ((1ull << (c & 63)) - 1));
+  }
+  template <class Fn>
+  void each(Fn fn) const {  // fn(class, compact column), ascending
+    int k = 0;
+    for (int w = 0; w < 4; w++)
+      for (uint64_t b = bits[w]; b; b &= b - 1) fn(64 * w + __builtin_ctzll(b), k++);
+  }
+};
+
 struct FNode {  // a frontier node: histogrammed and split-searched at this level
   int32_t tree_idx;
   int32_t depth;
   int32_t slot;  // histogram slot at this level
   bool direct;   // histogrammed from its rows (else parent - sibling)
-  std::vector<uint8_t> cls;  // classes present (ascending); empty = all
-  std::vector<std::pair<uint32_t, uint32_t>> pieces;  // this rank's rows: (offset, length) in the planes
+  ClassSet cls;  // classes present; the node's histogram columns
 };
 
 }  // namespace
@@ -311,6 +360,7 @@ struct adapt_region {
       H0, H1, segs,
       hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, cmaps, psync, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall;
+  adapt::Arena stage_a, stage_b;  // per-level uploads: before the partition, before the histogram
   // Table-1 shim state
   bool active = false;
   std::vector<float> ctx_feat;
@@ -456,6 +506,17 @@ void h2d(DevBuf &b, const std::vector<T> &v, cudaStream_t s) {
 // ------------------------------------------------------------ training --
 void train_region(adapt_region *h, cudaStream_t s) {
   const int F = h->F, V = h->V, C = V, D = h->D;
+  static const bool trace = getenv("ADAPT_TRACE_HOST") != nullptr;  // host-side time per level
+  auto now_us = []() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
+  };
+  double tr[8] = {0};
+  if (trace) {
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    tr[7] = now_us();
+  }
   const int world = g_ctx.world;
   // 0. source table (wide, or long records aggregated on the host)
   const float *feat = h->d_feat, *times = h->d_times;
@@ -570,12 +631,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
   }
   check_flags();
 
-  // histogram layout: node -> [f][rank][class], features packed by D_f
-  std::vector<int32_t> hoff(F);
-  int64_t HS = 0;
+  // histogram layout: node -> [DS][kc] (rows cumD[f] + rank, compact class columns)
+  std::vector<int32_t> cumD(F);
+  int64_t DS = 0;
   for (int f = 0; f < F; f++) {
-    hoff[f] = (int32_t)HS;
-    HS += (int64_t)h->nval[f] * C;
+    cumD[f] = (int32_t)DS;
+    DS += h->nval[f];
   }
   // shared-memory groups of the level pass: group = one 32-bit word of the
   // bins row (4 features) x a class slab [k0, k0+kw); feature f takes
@@ -614,7 +675,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     gsoff.insert(gsoff.end(), t.off.begin(), t.off.end());
     max_group = std::max(max_group, t.counters);
   }
-  h2d(h->hoff, hoff, s);
+  h2d(h->hoff, cumD, s);
   h2d(h->grp, groups, s);
   h2d(h->gsoff, gsoff, s);
 
@@ -632,11 +693,20 @@ void train_region(adapt_region *h, cudaStream_t s) {
   frontier[0].depth = 0;
   frontier[0].slot = 0;
   frontier[0].direct = true;
-  frontier[0].pieces = {{0u, (uint32_t)n}};
+  for (int k = 0; k < C; k++) frontier[0].cls.add(k);
+  // this rank's rows of frontier node j: pieces [pc_start[j], pc_start[j+1]) of
+  // (offset, length) in the planes
+  std::vector<std::pair<uint32_t, uint32_t>> pcs{{0u, (uint32_t)n}};
+  std::vector<int32_t> pc_start{0, 1};
   std::vector<Seg> psegs;           // pieces of the split parents (partition input)
   std::vector<int2> pseg_children;  // per piece: frontier index of the left / right child
-  std::vector<int32_t> direct_slots{0};
-  std::vector<int32_t> triples;
+  int ndirect_slots = 1;  // direct slots are 0..ndirect_slots-1, derived ones follow
+  struct Derived {        // a derived node of the next level = parent - direct sibling
+    int j, sib_j;         // frontier indices (next level)
+    int64_t off_p;        // parent's histogram offset (this level; Hprev next level)
+    ClassSet cls_p;       // parent's classes (its columns)
+  };
+  std::vector<Derived> derived;
   // planes: the root is histogrammed from the ingest output; pass d >= 1 moves
   // the parents' rows from one plane pair into the other
   const uint8_t *bins_in = h->bins.as<uint8_t>(), *lab_in = h->labels.as<uint8_t>();
@@ -671,30 +741,72 @@ void train_region(adapt_region *h, cudaStream_t s) {
     return total;
   };
 
+  if (trace) {
+    const double t = now_us();
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    fprintf(stderr, "[adapt] ingest: host %.0f us to the level loop, then %.0f us of queued work\n",
+            t - tr[7], now_us() - t);
+  }
   for (int level = 0; !frontier.empty(); level++) {
     const int A = (int)frontier.size();
+    if (trace) tr[0] = now_us();
     const uint8_t *hist_bins = bins_in, *hist_lab = lab_in;
     int64_t rows_part = 0;
+    // ---- uploads that do not depend on this level's partition: class maps
+    // of the direct nodes, their slots, the subtraction triples, node slots ----
+    // node histograms, class-compacted: slot offsets from the nodes' class counts
+    const int nslots = A;  // every frontier node has a slot
+    std::vector<int32_t> slot_kc(nslots, 0);
+    for (const auto &fn : frontier) slot_kc[fn.slot] = fn.cls.count();
+    std::vector<int64_t> soff(nslots + 1, 0);
+    for (int k = 0; k < nslots; k++) soff[k + 1] = soff[k] + DS * slot_kc[k];
+    std::vector<uint8_t> cmaps;  // per direct node: class -> compact index (255: absent)
+    std::vector<int32_t> node_ci(A, -1), node_kc(A);
+    std::vector<int64_t> node_off(A);
+    int64_t max_direct = 0, max_derived = 0;
+    for (int j = 0; j < A; j++) {
+      const FNode &fn = frontier[j];
+      node_off[j] = soff[fn.slot];
+      node_kc[j] = fn.cls.count();
+      if (!fn.direct) {
+        max_derived = std::max<int64_t>(max_derived, DS * node_kc[j]);
+        continue;
+      }
+      max_direct = std::max<int64_t>(max_direct, DS * node_kc[j]);
+      const int ci = (int)(cmaps.size() / C);
+      cmaps.resize(cmaps.size() + C, 255);
+      uint8_t *m = &cmaps[(size_t)ci * C];
+      fn.cls.each([&](int c, int k) { m[c] = (uint8_t)k; });
+      node_ci[j] = ci;
+    }
+    std::vector<SubJob> jobs;
+    std::vector<int16_t> maps;
+    for (const auto &dv : derived) {
+      SubJob jb{};
+      jb.off_d = node_off[dv.j];
+      jb.kc_d = node_kc[dv.j];
+      jb.off_p = dv.off_p;
+      jb.kc_p = dv.cls_p.count();
+      jb.off_s = node_off[dv.sib_j];
+      jb.kc_s = node_kc[dv.sib_j];
+      jb.map = (int32_t)(maps.size() / 2);
+      const ClassSet &cs = frontier[dv.sib_j].cls;
+      frontier[dv.j].cls.each([&](int c, int) {  // derived column -> (parent, sibling or -1)
+        maps.push_back((int16_t)dv.cls_p.rank(c));
+        maps.push_back((int16_t)(cs.has(c) ? cs.rank(c) : -1));
+      });
+      jobs.push_back(jb);
+    }
+    PartArgs pa{};
+    int max_visits = 1;  // parents a partition range can touch
+    size_t vbytes = 0;
     if (level > 0) {
-      // ---- a7: move the parents' rows into the children's pieces ----
-      uint8_t *bo = (out_plane ? h->binsB : h->binsA).as<uint8_t>();
-      uint8_t *lo = (out_plane ? h->labB : h->labA).as<uint8_t>();
       const uint32_t total = virtualize(psegs, false);
       rows_part = total;
-      PartArgs pa{};
-      pa.segs = nullptr;
       pa.nseg = (int)psegs.size();
       pa.total_rows = total;
-      pa.bins_in = bins_in;
-      pa.lab_in = lab_in;
-      pa.bins_out = bo;
-      pa.lab_out = lo;
-      pa.pstride = pstride;
-      pa.BS = BS;
-      pa.F = F;
       pa.nranges = partition_ranges(sms, total);
       const uint32_t R = (total + pa.nranges - 1) / std::max(1, pa.nranges);
-      int max_visits = 1;  // parents a range can touch
       for (int r = 0, si = 0; r < pa.nranges && total; r++) {
         const uint32_t p0 = r * R, p1 = std::min<uint64_t>((uint64_t)p0 + R, total);
         while (si + 1 < pa.nseg && psegs[si + 1].row_base <= p0) si++;
@@ -705,13 +817,38 @@ void train_region(adapt_region *h, cudaStream_t s) {
         }
         max_visits = std::max(max_visits, nodes);
       }
+    }
+    Arena &sa = h->stage_a;
+    sa.reset();
+    const size_t o_cmaps = sa.put(cmaps), o_soff = sa.put(soff), o_skc = sa.put(slot_kc),
+                 o_jobs = sa.put(jobs), o_maps = sa.put(maps), o_noff = sa.put(node_off),
+                 o_nkc = sa.put(node_kc);
+    const size_t o_psegs = level > 0 ? sa.put(psegs) : 0;
+    sa.flush(s);
+    Hcur->ensure((size_t)soff[nslots] * 4 + 16);
+    {
+      Phase ph("zero", s, 0);
+      launch_zero_slots(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_soff), sa.ptr<int32_t>(o_skc), DS,
+                        ndirect_slots, max_direct, s);
+    }
+    if (level > 0) {
+      // ---- a7: move the parents' rows into the children's pieces ----
+      uint8_t *bo = (out_plane ? h->binsB : h->binsA).as<uint8_t>();
+      uint8_t *lo = (out_plane ? h->labB : h->labA).as<uint8_t>();
+      const uint32_t total = (uint32_t)rows_part;
+      pa.segs = sa.ptr<Seg>(o_psegs);
+      pa.bins_in = bins_in;
+      pa.lab_in = lab_in;
+      pa.bins_out = bo;
+      pa.lab_out = lo;
+      pa.pstride = pstride;
+      pa.BS = BS;
+      pa.F = F;
       pa.max_visits = max_visits;
-      const size_t vbytes = (size_t)pa.nranges * max_visits * 6 * 4;
+      vbytes = (size_t)pa.nranges * max_visits * 6 * 4;
       h->visits.ensure(vbytes);
       CUDA_CHECK(cudaMemsetAsync(h->visits.p, 0xFF, vbytes, s));
       pa.visits = h->visits.as<int32_t>();
-      h2d(h->segs, psegs, s);
-      pa.segs = h->segs.as<Seg>();
       {
         snprintf(nm, sizeof nm, "partition_L%02d", level);
         Phase ph(per_level ? nm : "partition", s, (double)total * 2 * (BS + 1));
@@ -720,58 +857,57 @@ void train_region(adapt_region *h, cudaStream_t s) {
       h->hres.ensure(vbytes);
       int32_t *hv = h->hres.as<int32_t>();
       CUDA_CHECK(cudaMemcpyAsync(hv, h->visits.p, vbytes, cudaMemcpyDeviceToHost, s));
+      if (trace) tr[1] = now_us();
       CUDA_CHECK(cudaStreamSynchronize(s));
-      // children's pieces, from the CTAs' share reports
-      for (auto &fn : frontier) fn.pieces.clear();
+      if (trace) tr[2] = now_us();
+      // children's pieces, from the CTAs' share reports: ranges visit a parent
+      // at most once each and in range order, so every child's pieces come out
+      // in offset order; a counting sort by child groups them (CSR)
+      std::vector<int32_t> cnt(A + 1, 0);
+      std::vector<std::array<uint32_t, 3>> flat;  // (child, offset, length)
+      flat.reserve((size_t)2 * pa.nranges * max_visits);
       for (int b = 0; b < pa.nranges; b++)
         for (int v = 0; v < max_visits; v++) {
           const int32_t *e = hv + ((size_t)b * max_visits + v) * 6;
           if (e[0] < 0) break;
           const int2 ch = pseg_children[e[0]];
-          if (ch.x >= 0 && e[3] > 0) frontier[ch.x].pieces.push_back({(uint32_t)e[1], (uint32_t)e[3]});
+          if (ch.x >= 0 && e[3] > 0) flat.push_back({(uint32_t)ch.x, (uint32_t)e[1], (uint32_t)e[3]});
           if (ch.y >= 0 && e[4] > 0)
-            frontier[ch.y].pieces.push_back({(uint32_t)(e[2] - e[4]), (uint32_t)e[4]});
+            flat.push_back({(uint32_t)ch.y, (uint32_t)(e[2] - e[4]), (uint32_t)e[4]});
         }
-      for (auto &fn : frontier) std::sort(fn.pieces.begin(), fn.pieces.end());
+      for (const auto &x : flat) cnt[x[0] + 1]++;
+      for (int j = 0; j < A; j++) cnt[j + 1] += cnt[j];
+      pc_start = cnt;
+      pcs.assign(flat.size(), {0u, 0u});
+      for (const auto &x : flat) pcs[cnt[x[0]]++] = {x[1], x[2]};
       hist_bins = bo;
       hist_lab = lo;
     }
+    if (trace) tr[3] = now_us();
     // ---- a4: histograms of the direct nodes (the root, or the smaller children) ----
     std::vector<Seg> hsegs;
-    std::vector<uint8_t> cmaps;  // per direct node: class -> compact index, compact -> class
-    for (const auto &fn : frontier)
-      if (fn.direct) {
-        const int ci = (int)(cmaps.size() / (2 * C));
-        cmaps.resize(cmaps.size() + 2 * C, 255);
-        uint8_t *m = &cmaps[(size_t)ci * 2 * C];
-        int nc = 0;
-        for (int k = 0; k < C; k++)
-          if (fn.cls.empty() || std::binary_search(fn.cls.begin(), fn.cls.end(), (uint8_t)k)) {
-            m[k] = (uint8_t)nc;
-            m[C + nc] = (uint8_t)k;
-            nc++;
-          }
-        for (const auto &pc : fn.pieces) {
-          Seg sg{};
-          sg.off = pc.first;
-          sg.len = pc.second;
-          sg.hslot = fn.slot;
-          sg.cmap = ci;
-          sg.ncls = nc;
-          hsegs.push_back(sg);
-        }
+    for (int j = 0; j < A; j++) {
+      const FNode &fn = frontier[j];
+      if (!fn.direct) continue;
+      for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {
+        const auto &pc = pcs[q];
+        Seg sg{};
+        sg.off = pc.first;
+        sg.len = pc.second;
+        sg.hslot = fn.slot;
+        sg.cmap = node_ci[j];
+        sg.ncls = node_kc[j];
+        hsegs.push_back(sg);
       }
-    const uint32_t htotal = virtualize(hsegs, true);
-    Hcur->ensure((size_t)A * HS * 4);
-    h2d(h->slots, direct_slots, s);
-    {
-      Phase ph("zero", s, 0);
-      launch_zero_slots(Hcur->as<uint32_t>(), HS, h->slots.as<int32_t>(), (int)direct_slots.size(), s);
     }
+    const uint32_t htotal = virtualize(hsegs, true);
     if (htotal > 0) {
+      Arena &sb = h->stage_b;
+      sb.reset();
+      const size_t o_hsegs = sb.put(hsegs);
+      sb.flush(s);
       HistArgs ha{};
-      h2d(h->hsegs, hsegs, s);
-      ha.segs = h->hsegs.as<Seg>();
+      ha.segs = sb.ptr<Seg>(o_hsegs);
       ha.nseg = (int)hsegs.size();
       ha.total_rows = htotal;
       ha.bins_in = hist_bins;
@@ -780,15 +916,14 @@ void train_region(adapt_region *h, cudaStream_t s) {
       ha.BS = BS;
       ha.F = F;
       ha.C = C;
-      ha.hoff = h->hoff.as<int32_t>();
+      ha.cumD = h->hoff.as<int32_t>();
       ha.nval = h->dnval.as<int32_t>();
       ha.groups = h->grp.as<int4>();
-      h2d(h->cmaps, cmaps, s);
-      ha.cmaps = h->cmaps.as<uint8_t>();
+      ha.cmaps = sa.ptr<uint8_t>(o_cmaps);
       ha.ngroups = ngroups;
       ha.smem_counters = max_group;
       ha.H = Hcur->as<uint32_t>();
-      ha.HS = HS;
+      ha.soff = sa.ptr<int64_t>(o_soff);
       // one CTA per SM; the ngroups CTAs of a range are co-resident (cooperative launch)
       ha.nranges = (int)std::max<int64_t>(1, std::min<int64_t>((htotal + 4095) / 4096,
                                                                std::max(1, sms / ngroups)));
@@ -805,35 +940,34 @@ void train_region(adapt_region *h, cudaStream_t s) {
       Phase ph(per_level ? nm : "hist", s, (double)htotal * (F + 1));
       launch_hist(ha, s);
     }
-    if (world > 1 && !direct_slots.empty())
-      comm_allreduce_sum(Hcur->p, (size_t)direct_slots.size() * HS, false, s, "allreduce histograms");
-    if (!triples.empty()) {
-      h2d(h->triples, triples, s);
+    if (world > 1 && ndirect_slots > 0)  // the direct slots are contiguous at the front
+      comm_allreduce_sum(Hcur->p, (size_t)soff[ndirect_slots], false, s, "allreduce histograms");
+    if (!jobs.empty()) {
       Phase ph("subtract", s, 0);
-      launch_subtract(Hcur->as<uint32_t>(), Hprev->as<uint32_t>(), HS, h->triples.as<int32_t>(),
-                      (int)triples.size() / 3, s);
+      launch_subtract(Hcur->as<uint32_t>(), Hprev->as<uint32_t>(), DS, sa.ptr<SubJob>(o_jobs),
+                      sa.ptr<int16_t>(o_maps), (int)jobs.size(), max_derived, s);
     }
-    std::vector<int32_t> node_slot(A);
-    for (int j = 0; j < A; j++) node_slot[j] = frontier[j].slot;
-    h2d(h->nslot, node_slot, s);
     h->cand.ensure((size_t)A * F * sizeof(SplitCand));
     h->res.ensure((size_t)A * res_stride);
     {
       snprintf(nm, sizeof nm, "split_L%02d", level);
       Phase ph(per_level ? nm : "split", s, 0);
-      launch_split(Hcur->as<uint32_t>(), HS, h->nslot.as<int32_t>(), A, F, C, h->hoff.as<int32_t>(),
+      launch_split(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_noff), sa.ptr<int32_t>(o_nkc), A, F,
+                   h->hoff.as<int32_t>(),
                    h->dnval.as<int32_t>(), h->cand.as<SplitCand>(), s);
     }
     {
       Phase ph("winner", s, 0);
-      launch_winner(Hcur->as<uint32_t>(), HS, h->nslot.as<int32_t>(), A, F, C,
+      launch_winner(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_noff), sa.ptr<int32_t>(o_nkc), A, F, C,
                     h->hoff.as<int32_t>(), h->dnval.as<int32_t>(), h->cand.as<SplitCand>(),
                     h->res.as<uint8_t>(), res_stride, s);
     }
     h->hres.ensure((size_t)A * res_stride);
     uint8_t *hr = h->hres.as<uint8_t>();
     CUDA_CHECK(cudaMemcpyAsync(hr, h->res.p, (size_t)A * res_stride, cudaMemcpyDeviceToHost, s));
+    if (trace) tr[4] = now_us();
     CUDA_CHECK(cudaStreamSynchronize(s));
+    if (trace) tr[5] = now_us();
     h->stats.push_back(A);
     h->stats.push_back(htotal);
     h->stats.push_back(rows_part);
@@ -842,18 +976,30 @@ void train_region(adapt_region *h, cudaStream_t s) {
     std::vector<FNode> next;
     std::vector<Seg> nsegs;
     std::vector<int2> nchildren;
-    std::vector<int32_t> ndirect, nderived_par, nderived_sib;
-    std::vector<int> nderived_j;
+    std::vector<Derived> nderived;
+    int ndirect = 0;
     std::vector<uint64_t> P(C), PL(C), PR(C);
+    auto present = [&](const std::vector<uint64_t> &Pc) {
+      ClassSet v;
+      for (int k = 0; k < C; k++)
+        if (Pc[k]) v.add(k);
+      return v;
+    };
     for (int j = 0; j < A; j++) {
       const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + (size_t)j * res_stride);
-      const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);
+      const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);  // compact columns
       const uint32_t *cLd = Pd + C;
       const FNode &fn = frontier[j];
-      for (int k = 0; k < C; k++) P[k] = Pd[k];
+      const int kc = node_kc[j];
+      std::fill(P.begin(), P.end(), 0);
+      std::fill(PL.begin(), PL.end(), 0);
+      fn.cls.each([&](int c, int k) {
+        P[c] = Pd[k];
+        PL[c] = cLd[k];
+      });
       fill_stats(h->tree[fn.tree_idx], P.data(), C);
       h->tree[fn.tree_idx].depth = fn.depth;
-      if (fn.depth >= D || is_pure(P.data(), C) || !nr->valid) continue;  // leaf (R10, R11)
+      if (fn.depth >= D || kc <= 1 || is_pure(P.data(), C) || !nr->valid) continue;  // leaf (R10, R11)
       const int f = nr->feat;
       adapt_node_t &nd = h->tree[fn.tree_idx];
       nd.feature = f;
@@ -862,18 +1008,16 @@ void train_region(adapt_region *h, cudaStream_t s) {
       const int32_t li = (int32_t)h->tree.size();
       nd.left = li;
       nd.right = li + 1;
-      for (int k = 0; k < C; k++) {
-        PL[k] = cLd[k];
-        PR[k] = P[k] - cLd[k];
-      }
+      for (int k = 0; k < C; k++) PR[k] = P[k] - PL[k];
       adapt_node_t cl{}, cr{};
       cl.feature = cr.feature = -1;
       cl.left = cl.right = cr.left = cr.right = -1;
       cl.depth = cr.depth = fn.depth + 1;
-      fill_stats(cl, PL.data(), C);
-      fill_stats(cr, PR.data(), C);
       const bool inL = fn.depth + 1 < D && !is_pure(PL.data(), C);
       const bool inR = fn.depth + 1 < D && !is_pure(PR.data(), C);
+      // frontier children get their stats from their own class totals next level
+      if (!inL) fill_stats(cl, PL.data(), C);
+      if (!inR) fill_stats(cr, PR.data(), C);
       h->tree.push_back(cl);
       h->tree.push_back(cr);
       if (!inL && !inR) continue;
@@ -881,29 +1025,26 @@ void train_region(adapt_region *h, cudaStream_t s) {
       int dir;
       if (inL && inR) dir = nL <= nR ? 0 : 1;  // histogram the smaller child
       else dir = inL ? 0 : 1;
-      const int32_t hslot = (int32_t)ndirect.size();
-      ndirect.push_back(hslot);
+      const int32_t hslot = ndirect++;
       int jl = -1, jr = -1;
-      auto present = [&](const std::vector<uint64_t> &Pc) {
-        std::vector<uint8_t> v;
-        for (int k = 0; k < C; k++)
-          if (Pc[k]) v.push_back((uint8_t)k);
-        return v;
-      };
       if (inL) {
         jl = (int)next.size();
-        next.push_back(FNode{li, fn.depth + 1, dir == 0 ? hslot : -1, dir == 0, present(PL), {}});
+        next.push_back(FNode{li, fn.depth + 1, dir == 0 ? hslot : -1, dir == 0, present(PL)});
       }
       if (inR) {
         jr = (int)next.size();
-        next.push_back(FNode{li + 1, fn.depth + 1, dir == 1 ? hslot : -1, dir == 1, present(PR), {}});
+        next.push_back(FNode{li + 1, fn.depth + 1, dir == 1 ? hslot : -1, dir == 1, present(PR)});
       }
-      if (inL && inR) {  // the other child by subtraction from the parent
-        nderived_j.push_back(dir == 0 ? jr : jl);
-        nderived_par.push_back(fn.slot);
-        nderived_sib.push_back(hslot);
+      if (inL && inR) {  // the other child by subtraction from this node's histogram
+        Derived dv;
+        dv.j = dir == 0 ? jr : jl;
+        dv.sib_j = dir == 0 ? jl : jr;
+        dv.off_p = node_off[j];
+        dv.cls_p = fn.cls;
+        nderived.push_back(dv);
       }
-      for (const auto &pc : fn.pieces) {  // one partition segment per piece of the parent
+      for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {  // one partition segment per piece
+        const auto &pc = pcs[q];
         Seg sg{};
         sg.off = pc.first;
         sg.len = pc.second;
@@ -917,18 +1058,17 @@ void train_region(adapt_region *h, cudaStream_t s) {
       }
     }
     // derived slots follow the direct ones
-    triples.clear();
-    for (size_t i = 0; i < nderived_j.size(); i++) {
-      const int32_t slot = (int32_t)(ndirect.size() + i);
-      next[nderived_j[i]].slot = slot;
-      triples.push_back(slot);
-      triples.push_back(nderived_par[i]);
-      triples.push_back(nderived_sib[i]);
-    }
+    for (size_t i = 0; i < nderived.size(); i++) next[nderived[i].j].slot = ndirect + (int)i;
+    if (trace)
+      fprintf(stderr, "[adapt] L%02d A=%d part-launch %.0f us, wait %.0f, pieces %.0f, "
+              "hist..winner launch %.0f, wait %.0f, decide %.0f us\n", level, A,
+              level ? tr[1] - tr[0] : 0.0, level ? tr[2] - tr[1] : 0.0, level ? tr[3] - tr[2] : 0.0,
+              tr[4] - tr[3], tr[5] - tr[4], now_us() - tr[5]);
     frontier.swap(next);
     psegs.swap(nsegs);
     pseg_children.swap(nchildren);
-    direct_slots.swap(ndirect);
+    ndirect_slots = ndirect;
+    derived.swap(nderived);
     std::swap(Hcur, Hprev);
     // the planes just written are the input of the next partition; the root
     // level moved nothing, so level 1 still reads the ingest output

@@ -198,14 +198,12 @@ template <int BS>
 __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
   extern __shared__ uint32_t sh[];  // [smem_counters] counters
   __shared__ uint8_t s_cmap[kMaxC + 1];  // this node: class -> compact index (255: absent)
-  __shared__ uint8_t s_inv[kMaxC + 1];   // compact index -> class
   const int tid = threadIdx.x;
   const int G = a.ngroups;
   const int g = blockIdx.x % G;
   const int range = blockIdx.x / G;
-  const int4 grp = a.groups[g];  // x: first class, y: classes, z: padded class stride, w: word
+  const int4 grp = a.groups[g];  // x: first compact class, y: classes, w: bins word
   const int k0 = grp.x, kw = grp.y, w0 = grp.w;
-  const bool compact = a.cmaps != nullptr && kw == a.C;  // per-node class compaction
   const int C = a.C;
   int Dw[4];  // distinct values of the 4 features of word w0 (0: absent)
 #pragma unroll
@@ -220,15 +218,18 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
     // ---- one node's rows at virtual positions [p0, pe) ----
     const Seg first = a.segs[s];
     const uint32_t pe = min(p1, first.node_base + first.node_len);
-    // this node's class layout: compact (only the classes present) or the slab
-    const int kc = compact ? first.ncls : kw;
-    const int kwp = kc | 1;  // odd stride: bank spread
-    if (compact) {
-      const uint8_t *m = a.cmaps + (size_t)first.cmap * 2 * C;
-      for (int k = tid; k < C; k += blockDim.x) {
-        s_cmap[k] = m[k];
-        s_inv[k] = m[C + k];
-      }
+    // the node's classes are its compact columns; this CTA counts [k0, k0 + kn)
+    const int kcn = first.ncls;
+    const int kn = min(kw, kcn - k0);
+    if (kn <= 0) {  // none of this node's classes fall in this CTA's slab
+      while (s < a.nseg && a.segs[s].row_base < pe) s++;
+      p0 = pe;
+      continue;
+    }
+    const int kwp = kn | 1;  // odd stride: bank spread
+    {
+      const uint8_t *m = a.cmaps + (size_t)first.cmap * C;
+      for (int k = tid; k < C; k += blockDim.x) s_cmap[k] = m[k];
     }
     uint32_t abase[4];
     int gcount = 0;
@@ -276,8 +277,8 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
 #pragma unroll
         for (int u = 0; u < kHistUnroll; u++) {
           if (label[u] < 0) continue;
-          const int lk = compact ? (int)s_cmap[label[u]] : label[u] - k0;
-          if ((unsigned)lk >= (unsigned)kc) continue;  // other class slab
+          const int lk = (int)s_cmap[label[u]] - k0;
+          if ((unsigned)lk >= (unsigned)kn) continue;  // another CTA's class slab
           const uint32_t lk4 = 4u * lk;
           if (all4) {
             red_shared_inc(abase[0] + ((w[u]) & 0xFF) * kwp4 + lk4);
@@ -294,18 +295,18 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
       }
     }
     __syncthreads();
-    {  // flush: the node's [f][rank][class] layout (compact index -> class)
-      uint32_t *dst = a.H + (size_t)first.hslot * a.HS;
+    {  // flush into the node's [DS][kcn] matrix: row cumD[f] + rank, column k0 + j
+      uint32_t *dst = a.H + a.soff[first.hslot];
       int o = 0;
       for (int e = 0; e < 4; e++) {
         if (!Dw[e]) continue;
         const int n = Dw[e] * kwp;
-        uint32_t *df = dst + a.hoff[4 * w0 + e];
+        uint32_t *df = dst + (int64_t)a.cumD[4 * w0 + e] * kcn + k0;
         for (int i = tid; i < n; i += blockDim.x) {
           const uint32_t val = sh[o + i];
           if (val) {
             const int rk = i / kwp, j = i - rk * kwp;
-            atomicAdd(df + rk * C + (compact ? (int)s_inv[j] : k0 + j), val);
+            atomicAdd(df + rk * kcn + j, val);
           }
         }
         o += n;

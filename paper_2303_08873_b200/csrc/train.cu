@@ -1,8 +1,10 @@
 // train.cu — the level-wise CART trainer's kernels.
 //
 // The histogram-side kernels of one tree level (the row passes are in level.cu):
+//   zero_slots_kernel the direct nodes' histograms before the row pass;
 //   subtract_kernel   the other ("derived") child = parent - direct sibling
-//                     (exact integer histogram subtraction);
+//                     (exact integer histogram subtraction, class-remapped:
+//                     every node is stored in its own class compaction);
 //   split_kernel      a6 per (node, feature): class-chunked block prefix scan
 //                     over bins, exact rational Gini score of every cut
 //                     between consecutive node-nonempty bins, block argmax;
@@ -19,23 +21,33 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__global__ void zero_slots_kernel(uint32_t *H, int64_t HS, const int32_t *slots) {
-  uint32_t *h = H + (size_t)slots[blockIdx.y] * HS;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < HS;
+// slots 0..n-1 (the direct nodes): zero their [DS][kc] matrices
+__global__ void zero_slots_kernel(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS) {
+  uint32_t *h = H + soff[blockIdx.y];
+  const int64_t E = DS * skc[blockIdx.y];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
        i += (int64_t)gridDim.x * blockDim.x)
     h[i] = 0;
 }
 
-// triples: (dst slot in H, parent slot in Hprev, direct sibling slot in H)
-__global__ void subtract_kernel(uint32_t *H, const uint32_t *Hprev, int64_t HS,
-                                const int32_t *triples) {
-  const int32_t *t = triples + 3 * blockIdx.y;
-  uint32_t *d = H + (size_t)t[0] * HS;
-  const uint32_t *p = Hprev + (size_t)t[1] * HS;
-  const uint32_t *q = H + (size_t)t[2] * HS;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < HS;
-       i += (int64_t)gridDim.x * blockDim.x)
-    d[i] = p[i] - q[i];
+// derived = parent - direct sibling (exact), each in its own class compaction:
+// derived column j = parent column map[j].x minus sibling column map[j].y (-1: 0)
+__global__ void subtract_kernel(uint32_t *H, const uint32_t *Hprev, int64_t DS, const SubJob *jobs,
+                                const int16_t *maps) {
+  const SubJob jb = jobs[blockIdx.y];
+  const short2 *m = reinterpret_cast<const short2 *>(maps) + jb.map;
+  uint32_t *d = H + jb.off_d;
+  const uint32_t *p = Hprev + jb.off_p;
+  const uint32_t *q = H + jb.off_s;
+  const int64_t E = DS * jb.kc_d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / jb.kc_d;
+    const int j = (int)(i - r * jb.kc_d);
+    const short2 mj = m[j];
+    const uint32_t sib = mj.y >= 0 ? q[r * jb.kc_s + mj.y] : 0u;
+    d[i] = p[r * jb.kc_p + mj.x] - sib;
+  }
 }
 
 // ---- exact comparison of scores num/den (num < 2^97, den < 2^64) ----
@@ -82,8 +94,8 @@ constexpr int kSplitThreads = 256;  // = max bins per feature
 constexpr int kClassChunk = 32;
 
 __global__ void __launch_bounds__(kSplitThreads)
-    split_kernel(const uint32_t *__restrict__ H, int64_t HS, const int32_t *node_slot, int F,
-                 int C, const int32_t *hoff, const int32_t *nval, SplitCand *out) {
+    split_kernel(const uint32_t *__restrict__ H, const int64_t *node_off, const int32_t *node_kc,
+                 int F, const int32_t *cumD, const int32_t *nval, SplitCand *out) {
   __shared__ uint32_t tile[kSplitThreads][kClassChunk + 1];
   __shared__ uint32_t segtot[kSplitThreads / 32][kClassChunk];
   __shared__ uint32_t Pk[kClassChunk];
@@ -94,7 +106,8 @@ __global__ void __launch_bounds__(kSplitThreads)
   const int node = blockIdx.x, f = blockIdx.y;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int Df = nval[f];
-  const uint32_t *h = H + (size_t)node_slot[node] * HS + hoff[f];
+  const int C = node_kc[node];  // the node's classes (compact columns)
+  const uint32_t *h = H + node_off[node] + (int64_t)cumD[f] * C;
   uint64_t nl = 0, sl = 0, sr = 0, ntot = 0;
   for (int c0 = 0; c0 < C; c0 += kClassChunk) {
     const int kc = min(kClassChunk, C - c0);
@@ -209,8 +222,8 @@ __global__ void __launch_bounds__(kSplitThreads)
 }
 
 __global__ void __launch_bounds__(256)
-    winner_kernel(const uint32_t *__restrict__ H, int64_t HS, const int32_t *node_slot, int F,
-                  int C, const int32_t *hoff, const int32_t *nval, const SplitCand *cand,
+    winner_kernel(const uint32_t *__restrict__ H, const int64_t *node_off, const int32_t *node_kc,
+                  int F, int Cmax, const int32_t *cumD, const int32_t *nval, const SplitCand *cand,
                   uint8_t *res, int res_stride) {
   __shared__ int s_f;
   __shared__ SplitCand s_c;
@@ -243,11 +256,12 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int fsel = s_f >= 0 ? s_f : 0;
   const int blo = s_f >= 0 ? s_c.b_lo : -1;
-  const uint32_t *h = H + (size_t)node_slot[node] * HS + hoff[fsel];
+  const int C = node_kc[node];
+  const uint32_t *h = H + node_off[node] + (int64_t)cumD[fsel] * C;
   const int Df = nval[fsel];
   NodeRes *nr = reinterpret_cast<NodeRes *>(res + (size_t)node * res_stride);
   uint32_t *P = reinterpret_cast<uint32_t *>(nr + 1);
-  uint32_t *cL = P + C;
+  uint32_t *cL = P + Cmax;
   for (int k = t; k < C; k += blockDim.x) {
     uint32_t tot = 0, left = 0;
     for (int r = 0; r < Df; r++) {
@@ -272,34 +286,34 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
-void launch_zero_slots(uint32_t *H, int64_t HS, const int32_t *slots, int n, cudaStream_t s) {
+void launch_zero_slots(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS, int n,
+                       int64_t max_elems, cudaStream_t s) {
   if (n == 0) return;
-  const int bx = (int)std::min<int64_t>((HS + 1023) / 1024, 64);
-  zero_slots_kernel<<<dim3(bx, n), 1024, 0, s>>>(H, HS, slots);
+  const int bx = (int)std::min<int64_t>((max_elems + 1023) / 1024, 64);
+  zero_slots_kernel<<<dim3(bx, n), 1024, 0, s>>>(H, soff, skc, DS);
   CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t HS, const int32_t *triples,
-                     int n, cudaStream_t s) {
+void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t DS, const SubJob *jobs,
+                     const int16_t *maps, int n, int64_t max_elems, cudaStream_t s) {
   if (n == 0) return;
-  const int bx = (int)std::min<int64_t>((HS + 1023) / 1024, 64);
-  subtract_kernel<<<dim3(bx, n), 1024, 0, s>>>(H, Hprev, HS, triples);
+  const int bx = (int)std::min<int64_t>((max_elems + 1023) / 1024, 64);
+  subtract_kernel<<<dim3(bx, n), 1024, 0, s>>>(H, Hprev, DS, jobs, maps);
   CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_split(const uint32_t *H, int64_t HS, const int32_t *node_slot, int nnodes, int F,
-                  int C, const int32_t *hoff, const int32_t *nval, SplitCand *out,
-                  cudaStream_t s) {
+void launch_split(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,
+                  int F, const int32_t *cumD, const int32_t *nval, SplitCand *out, cudaStream_t s) {
   if (nnodes == 0) return;
-  split_kernel<<<dim3(nnodes, F), kSplitThreads, 0, s>>>(H, HS, node_slot, F, C, hoff, nval, out);
+  split_kernel<<<dim3(nnodes, F), kSplitThreads, 0, s>>>(H, node_off, node_kc, F, cumD, nval, out);
   CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_winner(const uint32_t *H, int64_t HS, const int32_t *node_slot, int nnodes, int F,
-                   int C, const int32_t *hoff, const int32_t *nval, const SplitCand *cand,
+void launch_winner(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,
+                   int F, int C, const int32_t *cumD, const int32_t *nval, const SplitCand *cand,
                    uint8_t *res, int res_stride, cudaStream_t s) {
   if (nnodes == 0) return;
-  winner_kernel<<<nnodes, 256, 0, s>>>(H, HS, node_slot, F, C, hoff, nval, cand, res,
+  winner_kernel<<<nnodes, 256, 0, s>>>(H, node_off, node_kc, F, C, cumD, nval, cand, res,
                                        res_stride);
   CUDA_CHECK(cudaGetLastError());
 }
