@@ -144,10 +144,13 @@ struct SubJob {              // derived node = parent - direct sibling, class-re
 };                              // (parent column, sibling column or -1) as int16 pairs
 
 // ---- kernel launchers (train.cu) ----
-void launch_zero_slots(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS, int n,
-                       int64_t max_elems, cudaStream_t s);
+// zero / subtract work in chunks: cstart[j] = first chunk of job j (prefix of
+// chunk_count(elements of job j)), nblocks = total chunks
+int chunk_count(int64_t elems);
+void launch_zero_slots(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS,
+                       const int32_t *cstart, int n, int nblocks, cudaStream_t s);
 void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t DS, const SubJob *jobs,
-                     const int16_t *maps, int n, int64_t max_elems, cudaStream_t s);
+                     const int16_t *maps, const int32_t *cstart, int n, int nblocks, cudaStream_t s);
 void launch_split(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,
                   int F, const int32_t *cumD, const int32_t *nval, SplitCand *out, cudaStream_t s);
 void launch_winner(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,

@@ -476,26 +476,6 @@ void upload_tree(adapt_region *h, cudaStream_t s) {
   CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
-void fill_stats(adapt_node_t &nd, const uint64_t *P, int C) {
-  uint64_t n = 0;
-  unsigned __int128 S = 0;
-  int label = 0;
-  for (int k = 0; k < C; k++) {
-    n += P[k];
-    S += (unsigned __int128)P[k] * P[k];
-    if (P[k] > P[label]) label = k;  // ties -> lowest (R12)
-  }
-  nd.n = (int64_t)n;
-  nd.label = label;
-  nd.gini = n ? 1.0 - (double)(uint64_t)S / ((double)n * (double)n) : 0.0;
-}
-
-bool is_pure(const uint64_t *P, int C) {
-  int present = 0;
-  for (int k = 0; k < C; k++) present += P[k] > 0;
-  return present <= 1;
-}
-
 template <class T>
 void h2d(DevBuf &b, const std::vector<T> &v, cudaStream_t s) {
   b.ensure(v.size() * sizeof(T) + 16);
@@ -761,18 +741,14 @@ void train_region(adapt_region *h, cudaStream_t s) {
     std::vector<int64_t> soff(nslots + 1, 0);
     for (int k = 0; k < nslots; k++) soff[k + 1] = soff[k] + DS * slot_kc[k];
     std::vector<uint8_t> cmaps;  // per direct node: class -> compact index (255: absent)
+    cmaps.reserve((size_t)ndirect_slots * C);
     std::vector<int32_t> node_ci(A, -1), node_kc(A);
     std::vector<int64_t> node_off(A);
-    int64_t max_direct = 0, max_derived = 0;
     for (int j = 0; j < A; j++) {
       const FNode &fn = frontier[j];
       node_off[j] = soff[fn.slot];
       node_kc[j] = fn.cls.count();
-      if (!fn.direct) {
-        max_derived = std::max<int64_t>(max_derived, DS * node_kc[j]);
-        continue;
-      }
-      max_direct = std::max<int64_t>(max_direct, DS * node_kc[j]);
+      if (!fn.direct) continue;
       const int ci = (int)(cmaps.size() / C);
       cmaps.resize(cmaps.size() + C, 255);
       uint8_t *m = &cmaps[(size_t)ci * C];
@@ -781,6 +757,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
     }
     std::vector<SubJob> jobs;
     std::vector<int16_t> maps;
+    std::vector<int32_t> zstart(ndirect_slots), sstart;  // chunk prefixes (zero / subtract)
+    int zblocks = 0, sblocks = 0;
+    for (int k = 0; k < ndirect_slots; k++) {
+      zstart[k] = zblocks;
+      zblocks += chunk_count(DS * slot_kc[k]);
+    }
     for (const auto &dv : derived) {
       SubJob jb{};
       jb.off_d = node_off[dv.j];
@@ -796,7 +778,10 @@ void train_region(adapt_region *h, cudaStream_t s) {
         maps.push_back((int16_t)(cs.has(c) ? cs.rank(c) : -1));
       });
       jobs.push_back(jb);
+      sstart.push_back(sblocks);
+      sblocks += chunk_count(DS * jb.kc_d);
     }
+    if (trace) tr[6] = now_us();
     PartArgs pa{};
     int max_visits = 1;  // parents a partition range can touch
     size_t vbytes = 0;
@@ -818,18 +803,19 @@ void train_region(adapt_region *h, cudaStream_t s) {
         max_visits = std::max(max_visits, nodes);
       }
     }
+    double t_mv = trace ? now_us() : 0;
     Arena &sa = h->stage_a;
     sa.reset();
     const size_t o_cmaps = sa.put(cmaps), o_soff = sa.put(soff), o_skc = sa.put(slot_kc),
                  o_jobs = sa.put(jobs), o_maps = sa.put(maps), o_noff = sa.put(node_off),
-                 o_nkc = sa.put(node_kc);
+                 o_nkc = sa.put(node_kc), o_zst = sa.put(zstart), o_sst = sa.put(sstart);
     const size_t o_psegs = level > 0 ? sa.put(psegs) : 0;
     sa.flush(s);
     Hcur->ensure((size_t)soff[nslots] * 4 + 16);
     {
       Phase ph("zero", s, 0);
       launch_zero_slots(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_soff), sa.ptr<int32_t>(o_skc), DS,
-                        ndirect_slots, max_direct, s);
+                        sa.ptr<int32_t>(o_zst), ndirect_slots, zblocks, s);
     }
     if (level > 0) {
       // ---- a7: move the parents' rows into the children's pieces ----
@@ -945,7 +931,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     if (!jobs.empty()) {
       Phase ph("subtract", s, 0);
       launch_subtract(Hcur->as<uint32_t>(), Hprev->as<uint32_t>(), DS, sa.ptr<SubJob>(o_jobs),
-                      sa.ptr<int16_t>(o_maps), (int)jobs.size(), max_derived, s);
+                      sa.ptr<int16_t>(o_maps), sa.ptr<int32_t>(o_sst), (int)jobs.size(), sblocks, s);
     }
     h->cand.ensure((size_t)A * F * sizeof(SplitCand));
     h->res.ensure((size_t)A * res_stride);
@@ -979,27 +965,47 @@ void train_region(adapt_region *h, cudaStream_t s) {
     std::vector<Derived> nderived;
     int ndirect = 0;
     std::vector<uint64_t> P(C), PL(C), PR(C);
-    auto present = [&](const std::vector<uint64_t> &Pc) {
-      ClassSet v;
-      for (int k = 0; k < C; k++)
-        if (Pc[k]) v.add(k);
-      return v;
-    };
     for (int j = 0; j < A; j++) {
       const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + (size_t)j * res_stride);
       const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);  // compact columns
       const uint32_t *cLd = Pd + C;
       const FNode &fn = frontier[j];
+      // everything in the node's compact columns (class cl[k], ascending)
       const int kc = node_kc[j];
-      std::fill(P.begin(), P.end(), 0);
-      std::fill(PL.begin(), PL.end(), 0);
-      fn.cls.each([&](int c, int k) {
-        P[c] = Pd[k];
-        PL[c] = cLd[k];
-      });
-      fill_stats(h->tree[fn.tree_idx], P.data(), C);
+      int cl_of[kMaxC + 1];
+      fn.cls.each([&](int c, int k) { cl_of[k] = c; });
+      auto stats = [&](adapt_node_t &o, const uint64_t *cnt) {  // n, label, gini (fill_stats)
+        uint64_t nn = 0;
+        unsigned __int128 S = 0;
+        int best = 0;
+        for (int k = 0; k < kc; k++) {
+          nn += cnt[k];
+          S += (unsigned __int128)cnt[k] * cnt[k];
+          if (cnt[k] > cnt[best]) best = k;  // ties -> lowest class (R12)
+        }
+        o.n = (int64_t)nn;
+        o.label = kc ? cl_of[best] : 0;
+        o.gini = nn ? 1.0 - (double)(uint64_t)S / ((double)nn * (double)nn) : 0.0;
+      };
+      auto npresent = [&](const uint64_t *cnt) {
+        int z = 0;
+        for (int k = 0; k < kc; k++) z += cnt[k] > 0;
+        return z;
+      };
+      auto present = [&](const uint64_t *cnt) {
+        ClassSet v;
+        for (int k = 0; k < kc; k++)
+          if (cnt[k]) v.add(cl_of[k]);
+        return v;
+      };
+      for (int k = 0; k < kc; k++) {
+        P[k] = Pd[k];
+        PL[k] = cLd[k];
+        PR[k] = P[k] - PL[k];
+      }
+      stats(h->tree[fn.tree_idx], P.data());
       h->tree[fn.tree_idx].depth = fn.depth;
-      if (fn.depth >= D || kc <= 1 || is_pure(P.data(), C) || !nr->valid) continue;  // leaf (R10, R11)
+      if (fn.depth >= D || npresent(P.data()) <= 1 || !nr->valid) continue;  // leaf (R10, R11)
       const int f = nr->feat;
       adapt_node_t &nd = h->tree[fn.tree_idx];
       nd.feature = f;
@@ -1008,16 +1014,15 @@ void train_region(adapt_region *h, cudaStream_t s) {
       const int32_t li = (int32_t)h->tree.size();
       nd.left = li;
       nd.right = li + 1;
-      for (int k = 0; k < C; k++) PR[k] = P[k] - PL[k];
       adapt_node_t cl{}, cr{};
       cl.feature = cr.feature = -1;
       cl.left = cl.right = cr.left = cr.right = -1;
       cl.depth = cr.depth = fn.depth + 1;
-      const bool inL = fn.depth + 1 < D && !is_pure(PL.data(), C);
-      const bool inR = fn.depth + 1 < D && !is_pure(PR.data(), C);
+      const bool inL = fn.depth + 1 < D && npresent(PL.data()) > 1;
+      const bool inR = fn.depth + 1 < D && npresent(PR.data()) > 1;
       // frontier children get their stats from their own class totals next level
-      if (!inL) fill_stats(cl, PL.data(), C);
-      if (!inR) fill_stats(cr, PR.data(), C);
+      if (!inL) stats(cl, PL.data());
+      if (!inR) stats(cr, PR.data());
       h->tree.push_back(cl);
       h->tree.push_back(cr);
       if (!inL && !inR) continue;
@@ -1029,11 +1034,11 @@ void train_region(adapt_region *h, cudaStream_t s) {
       int jl = -1, jr = -1;
       if (inL) {
         jl = (int)next.size();
-        next.push_back(FNode{li, fn.depth + 1, dir == 0 ? hslot : -1, dir == 0, present(PL)});
+        next.push_back(FNode{li, fn.depth + 1, dir == 0 ? hslot : -1, dir == 0, present(PL.data())});
       }
       if (inR) {
         jr = (int)next.size();
-        next.push_back(FNode{li + 1, fn.depth + 1, dir == 1 ? hslot : -1, dir == 1, present(PR)});
+        next.push_back(FNode{li + 1, fn.depth + 1, dir == 1 ? hslot : -1, dir == 1, present(PR.data())});
       }
       if (inL && inR) {  // the other child by subtraction from this node's histogram
         Derived dv;
@@ -1060,9 +1065,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
     // derived slots follow the direct ones
     for (size_t i = 0; i < nderived.size(); i++) next[nderived[i].j].slot = ndirect + (int)i;
     if (trace)
-      fprintf(stderr, "[adapt] L%02d A=%d part-launch %.0f us, wait %.0f, pieces %.0f, "
+      fprintf(stderr, "[adapt] L%02d A=%d part-launch %.0f us (tables %.0f, ranges %.0f), wait %.0f, pieces %.0f, "
               "hist..winner launch %.0f, wait %.0f, decide %.0f us\n", level, A,
-              level ? tr[1] - tr[0] : 0.0, level ? tr[2] - tr[1] : 0.0, level ? tr[3] - tr[2] : 0.0,
+              level ? tr[1] - tr[0] : 0.0, tr[6] - tr[0], t_mv - tr[6], level ? tr[2] - tr[1] : 0.0, level ? tr[3] - tr[2] : 0.0,
               tr[4] - tr[3], tr[5] - tr[4], now_us() - tr[5]);
     frontier.swap(next);
     psegs.swap(nsegs);

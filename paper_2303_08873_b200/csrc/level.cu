@@ -295,21 +295,32 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
       }
     }
     __syncthreads();
-    {  // flush into the node's [DS][kcn] matrix: row cumD[f] + rank, column k0 + j
+    {  // flush into the node's [DS][kcn] matrix: row cumD[f] + rank, column k0 + j.
+       // A CTA that saw ALL of the node's rows (the common case at deep levels)
+       // owns its columns: plain stores of every counter, no atomics.
+      const bool sole = p0 <= first.node_base && pe >= first.node_base + first.node_len;
       uint32_t *dst = a.H + a.soff[first.hslot];
       int o = 0;
       for (int e = 0; e < 4; e++) {
         if (!Dw[e]) continue;
-        const int n = Dw[e] * kwp;
         uint32_t *df = dst + (int64_t)a.cumD[4 * w0 + e] * kcn + k0;
-        for (int i = tid; i < n; i += blockDim.x) {
-          const uint32_t val = sh[o + i];
-          if (val) {
-            const int rk = i / kwp, j = i - rk * kwp;
-            atomicAdd(df + rk * kcn + j, val);
+        if (sole) {
+          const int n = Dw[e] * kn;  // dense [rank][kn] block of this CTA's columns
+          for (int i = tid; i < n; i += blockDim.x) {
+            const int rk = i / kn, j = i - rk * kn;
+            df[rk * kcn + j] = sh[o + rk * kwp + j];
+          }
+        } else {
+          const int n = Dw[e] * kwp;
+          for (int i = tid; i < n; i += blockDim.x) {
+            const uint32_t val = sh[o + i];
+            if (val) {
+              const int rk = i / kwp, j = i - rk * kwp;
+              atomicAdd(df + rk * kcn + j, val);
+            }
           }
         }
-        o += n;
+        o += Dw[e] * kwp;
       }
     }
     __syncthreads();

@@ -21,27 +21,48 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Per-node matrix jobs are cut into chunks of kChunk elements; block b handles
+// chunk b of the flattened list (job found by binary search over the chunk
+// prefix), so deep levels with thousands of small nodes launch no idle blocks.
+constexpr int kChunk = 4096, kChunkThreads = 256;
+
+__device__ __forceinline__ int find_job(const int32_t *cstart, int n, int b) {
+  int lo = 0, hi = n - 1;  // last job with cstart[job] <= b
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (cstart[mid] <= b) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 // slots 0..n-1 (the direct nodes): zero their [DS][kc] matrices
-__global__ void zero_slots_kernel(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS) {
-  uint32_t *h = H + soff[blockIdx.y];
-  const int64_t E = DS * skc[blockIdx.y];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
-       i += (int64_t)gridDim.x * blockDim.x)
-    h[i] = 0;
+__global__ void __launch_bounds__(kChunkThreads)
+    zero_slots_kernel(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS,
+                      const int32_t *cstart, int n) {
+  const int y = find_job(cstart, n, blockIdx.x);
+  uint32_t *h = H + soff[y];
+  const int64_t E = DS * skc[y];
+  const int64_t i0 = (int64_t)(blockIdx.x - cstart[y]) * kChunk;
+  const int64_t i1 = min(i0 + kChunk, E);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += kChunkThreads) h[i] = 0;
 }
 
 // derived = parent - direct sibling (exact), each in its own class compaction:
 // derived column j = parent column map[j].x minus sibling column map[j].y (-1: 0)
-__global__ void subtract_kernel(uint32_t *H, const uint32_t *Hprev, int64_t DS, const SubJob *jobs,
-                                const int16_t *maps) {
-  const SubJob jb = jobs[blockIdx.y];
+__global__ void __launch_bounds__(kChunkThreads)
+    subtract_kernel(uint32_t *H, const uint32_t *Hprev, int64_t DS, const SubJob *jobs,
+                    const int16_t *maps, const int32_t *cstart, int n) {
+  const int y = find_job(cstart, n, blockIdx.x);
+  const SubJob jb = jobs[y];
   const short2 *m = reinterpret_cast<const short2 *>(maps) + jb.map;
   uint32_t *d = H + jb.off_d;
   const uint32_t *p = Hprev + jb.off_p;
   const uint32_t *q = H + jb.off_s;
   const int64_t E = DS * jb.kc_d;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t i0 = (int64_t)(blockIdx.x - cstart[y]) * kChunk;
+  const int64_t i1 = min(i0 + kChunk, E);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += kChunkThreads) {
     const int64_t r = i / jb.kc_d;
     const int j = (int)(i - r * jb.kc_d);
     const short2 mj = m[j];
@@ -111,8 +132,15 @@ __global__ void __launch_bounds__(kSplitThreads)
   uint64_t nl = 0, sl = 0, sr = 0, ntot = 0;
   for (int c0 = 0; c0 < C; c0 += kClassChunk) {
     const int kc = min(kClassChunk, C - c0);
-    if (lane < kc)  // warp w loads rows w, w+8, ...: lanes read consecutive classes
-      for (int r = w; r < Df; r += kSplitThreads / 32) tile[r][lane] = __ldg(h + (size_t)r * C + c0 + lane);
+    {  // the chunk's Df x kc counts, flat over all threads: independent loads in
+       // flight (contiguous when the node has <= kClassChunk classes)
+      const int E = Df * kc;
+#pragma unroll 4
+      for (int e = t; e < E; e += kSplitThreads) {
+        const int r = e / kc, k = e - r * kc;
+        tile[r][k] = __ldg(h + (size_t)r * C + c0 + k);
+      }
+    }
     __syncthreads();
     // prefix over bins: warp w scans rows [32w, 32w+32) of column `lane`
     const int r0 = w * 32, r1 = min(r0 + 32, Df);
@@ -262,16 +290,30 @@ __global__ void __launch_bounds__(256)
   NodeRes *nr = reinterpret_cast<NodeRes *>(res + (size_t)node * res_stride);
   uint32_t *P = reinterpret_cast<uint32_t *>(nr + 1);
   uint32_t *cL = P + Cmax;
-  for (int k = t; k < C; k += blockDim.x) {
-    uint32_t tot = 0, left = 0;
-    for (int r = 0; r < Df; r++) {
-      const uint32_t v = __ldg(h + (size_t)r * C + k);
-      tot += v;
-      if (r <= blo) left += v;
+  // class totals and left-of-cut totals: thread t sums class t % C over rows
+  // t / C, t / C + T, ... (T = threads per class), independent loads in flight
+  __shared__ uint32_t sP[kMaxC + 1], sL[kMaxC + 1];
+  for (int k = t; k < C; k += blockDim.x) sP[k] = sL[k] = 0;
+  __syncthreads();
+  if (C <= (int)blockDim.x) {
+    const int T = blockDim.x / C, k = t % C, r0 = t / C;
+    if (r0 < T) {
+      uint32_t tot = 0, left = 0;
+#pragma unroll 4
+      for (int r = r0; r < Df; r += T) {
+        const uint32_t v = __ldg(h + (size_t)r * C + k);
+        tot += v;
+        left += r <= blo ? v : 0u;
+      }
+      atomicAdd(&sP[k], tot);
+      atomicAdd(&sL[k], left);
     }
-    P[k] = tot;
-    cL[k] = left;
-    atomicAdd(&s_n, (unsigned long long)tot);
+  }
+  __syncthreads();
+  for (int k = t; k < C; k += blockDim.x) {
+    P[k] = sP[k];
+    cL[k] = sL[k];
+    atomicAdd(&s_n, (unsigned long long)sP[k]);
   }
   __syncthreads();
   if (t == 0) {
@@ -286,19 +328,19 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
-void launch_zero_slots(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS, int n,
-                       int64_t max_elems, cudaStream_t s) {
-  if (n == 0) return;
-  const int bx = (int)std::min<int64_t>((max_elems + 1023) / 1024, 64);
-  zero_slots_kernel<<<dim3(bx, n), 1024, 0, s>>>(H, soff, skc, DS);
+int chunk_count(int64_t elems) { return (int)((elems + kChunk - 1) / kChunk); }
+
+void launch_zero_slots(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS,
+                       const int32_t *cstart, int n, int nblocks, cudaStream_t s) {
+  if (n == 0 || nblocks == 0) return;
+  zero_slots_kernel<<<nblocks, kChunkThreads, 0, s>>>(H, soff, skc, DS, cstart, n);
   CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t DS, const SubJob *jobs,
-                     const int16_t *maps, int n, int64_t max_elems, cudaStream_t s) {
-  if (n == 0) return;
-  const int bx = (int)std::min<int64_t>((max_elems + 1023) / 1024, 64);
-  subtract_kernel<<<dim3(bx, n), 1024, 0, s>>>(H, Hprev, DS, jobs, maps);
+                     const int16_t *maps, const int32_t *cstart, int n, int nblocks, cudaStream_t s) {
+  if (n == 0 || nblocks == 0) return;
+  subtract_kernel<<<nblocks, kChunkThreads, 0, s>>>(H, Hprev, DS, jobs, maps, cstart, n);
   CUDA_CHECK(cudaGetLastError());
 }
 
