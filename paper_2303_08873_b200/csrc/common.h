@@ -151,7 +151,11 @@ void launch_zero_slots(uint32_t *H, const int64_t *soff, const int32_t *skc, int
                        const int32_t *cstart, int n, int nblocks, cudaStream_t s);
 void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t DS, const SubJob *jobs,
                      const int16_t *maps, const int32_t *cstart, int n, int nblocks, cudaStream_t s);
-void launch_split(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,
+// nodes with <= split_small_max_classes() classes go to the warp-per-(node, f)
+// kernel, the others to the block-per-(node, f) kernel
+int split_small_max_classes();
+void launch_split(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc,
+                  const int32_t *big_nodes, int nbig, const int32_t *small_nodes, int nsmall,
                   int F, const int32_t *cumD, const int32_t *nval, SplitCand *out, cudaStream_t s);
 void launch_winner(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,
                    int F, int C, const int32_t *cumD, const int32_t *nval, const SplitCand *cand,

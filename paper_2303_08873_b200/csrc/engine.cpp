@@ -755,6 +755,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
       fn.cls.each([&](int c, int k) { m[c] = (uint8_t)k; });
       node_ci[j] = ci;
     }
+    std::vector<int32_t> big_nodes, small_nodes;  // split search: by class count
+    for (int j = 0; j < A; j++)
+      (node_kc[j] <= split_small_max_classes() ? small_nodes : big_nodes).push_back(j);
     std::vector<SubJob> jobs;
     std::vector<int16_t> maps;
     std::vector<int32_t> zstart(ndirect_slots), sstart;  // chunk prefixes (zero / subtract)
@@ -808,7 +811,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
     sa.reset();
     const size_t o_cmaps = sa.put(cmaps), o_soff = sa.put(soff), o_skc = sa.put(slot_kc),
                  o_jobs = sa.put(jobs), o_maps = sa.put(maps), o_noff = sa.put(node_off),
-                 o_nkc = sa.put(node_kc), o_zst = sa.put(zstart), o_sst = sa.put(sstart);
+                 o_nkc = sa.put(node_kc), o_zst = sa.put(zstart), o_sst = sa.put(sstart),
+                 o_big = sa.put(big_nodes), o_small = sa.put(small_nodes);
     const size_t o_psegs = level > 0 ? sa.put(psegs) : 0;
     sa.flush(s);
     Hcur->ensure((size_t)soff[nslots] * 4 + 16);
@@ -938,8 +942,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
     {
       snprintf(nm, sizeof nm, "split_L%02d", level);
       Phase ph(per_level ? nm : "split", s, 0);
-      launch_split(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_noff), sa.ptr<int32_t>(o_nkc), A, F,
-                   h->hoff.as<int32_t>(),
+      launch_split(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_noff), sa.ptr<int32_t>(o_nkc),
+                   sa.ptr<int32_t>(o_big), (int)big_nodes.size(), sa.ptr<int32_t>(o_small),
+                   (int)small_nodes.size(), F, h->hoff.as<int32_t>(),
                    h->dnval.as<int32_t>(), h->cand.as<SplitCand>(), s);
     }
     {

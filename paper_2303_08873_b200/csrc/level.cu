@@ -300,24 +300,23 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
        // owns its columns: plain stores of every counter, no atomics.
       const bool sole = p0 <= first.node_base && pe >= first.node_base + first.node_len;
       uint32_t *dst = a.H + a.soff[first.hslot];
+      // flat over the counters; row = i / width by a float reciprocal (exact:
+      // i < 2^16, width <= 255 keeps (i + 0.5) / width >= 1/510 from an integer)
+      const int width = sole ? kn : kwp;
+      const float inv = 1.0f / (float)width;
       int o = 0;
       for (int e = 0; e < 4; e++) {
         if (!Dw[e]) continue;
         uint32_t *df = dst + (int64_t)a.cumD[4 * w0 + e] * kcn + k0;
-        if (sole) {
-          const int n = Dw[e] * kn;  // dense [rank][kn] block of this CTA's columns
-          for (int i = tid; i < n; i += blockDim.x) {
-            const int rk = i / kn, j = i - rk * kn;
-            df[rk * kcn + j] = sh[o + rk * kwp + j];
-          }
-        } else {
-          const int n = Dw[e] * kwp;
-          for (int i = tid; i < n; i += blockDim.x) {
-            const uint32_t val = sh[o + i];
-            if (val) {
-              const int rk = i / kwp, j = i - rk * kwp;
-              atomicAdd(df + rk * kcn + j, val);
-            }
+        const uint32_t *src = sh + o;
+        const int n = Dw[e] * width;
+        for (int i = tid; i < n; i += blockDim.x) {
+          const int rk = __float2int_rz(((float)i + 0.5f) * inv), j = i - rk * width;
+          if (sole) {  // dense [rank][kn] block of this CTA's columns
+            df[rk * kcn + j] = src[rk * kwp + j];
+          } else {
+            const uint32_t val = src[i];
+            if (val) atomicAdd(df + rk * kcn + j, val);
           }
         }
         o += Dw[e] * kwp;

@@ -116,7 +116,8 @@ constexpr int kClassChunk = 32;
 
 __global__ void __launch_bounds__(kSplitThreads)
     split_kernel(const uint32_t *__restrict__ H, const int64_t *node_off, const int32_t *node_kc,
-                 int F, const int32_t *cumD, const int32_t *nval, SplitCand *out) {
+                 const int32_t *nodes, int F, const int32_t *cumD, const int32_t *nval,
+                 SplitCand *out) {
   __shared__ uint32_t tile[kSplitThreads][kClassChunk + 1];
   __shared__ uint32_t segtot[kSplitThreads / 32][kClassChunk];
   __shared__ uint32_t Pk[kClassChunk];
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(kSplitThreads)
   __shared__ uint32_t nonempty[kSplitThreads / 32];
   __shared__ Key wbest[kSplitThreads / 32];
 
-  const int node = blockIdx.x, f = blockIdx.y;
+  const int node = nodes[blockIdx.x], f = blockIdx.y;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int Df = nval[f];
   const int C = node_kc[node];  // the node's classes (compact columns)
@@ -249,6 +250,150 @@ __global__ void __launch_bounds__(kSplitThreads)
   }
 }
 
+// Nodes with at most kSmallKc classes (most nodes of deep levels): one WARP per
+// (node, feature).  The Df x kc counts are staged coalesced into the warp's
+// smem tile (bin b at b*kc + b/8: one pad word per 8-bin lane segment, so the
+// lanes' segment walks hit distinct banks); lane l owns bins [8l, 8l+8):
+// per-class segment sums, warp scans for the prefix offsets and class totals,
+// then the same candidate keys, tie rules and exact comparison as split_kernel.
+constexpr int kSmallKc = 8;
+constexpr int kSmallWarps = 4;
+
+__global__ void __launch_bounds__(kSmallWarps * 32)
+    split_small_kernel(const uint32_t *__restrict__ H, const int64_t *node_off,
+                       const int32_t *node_kc, const int32_t *nodes, int njobs, int F,
+                       const int32_t *cumD, const int32_t *nval, SplitCand *out) {
+  __shared__ uint32_t wt[kSmallWarps][kSplitThreads * kSmallKc + 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int job = blockIdx.x * kSmallWarps + warp;
+  if (job >= njobs) return;  // warp-uniform; no block barriers below
+  const int node = nodes[job / F], f = job % F;
+  const int kc = node_kc[node], Df = nval[f];
+  const uint32_t *h = H + node_off[node] + (int64_t)cumD[f] * kc;
+  uint32_t *tl = wt[warp];
+  {
+    const int E = Df * kc;
+    const float inv = 1.0f / (float)kc;  // exact enough: e < 2048, kc <= 8
+#pragma unroll 4
+    for (int e = lane; e < E; e += 32) {
+      const int b = __float2int_rz(((float)e + 0.5f) * inv);
+      tl[e + (b >> 3)] = __ldg(h + e);
+    }
+  }
+  __syncwarp();
+  const int b0 = lane * 8;
+  const uint32_t *sg = tl + b0 * kc + lane;  // this lane's 8 bins (after lane pad words)
+  uint32_t acc[kSmallKc];
+  uint32_t bc[8];  // bin counts
+#pragma unroll
+  for (int k = 0; k < kSmallKc; k++) acc[k] = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < kSmallKc; k++)
+      if (k < kc && b0 + i < Df) {
+        const uint32_t v = sg[i * kc + k];
+        acc[k] += v;
+        c += v;
+      }
+    bc[i] = c;
+  }
+  uint32_t off[kSmallKc], tot[kSmallKc];
+  uint64_t ntot = 0;
+#pragma unroll
+  for (int k = 0; k < kSmallKc; k++) {
+    uint32_t x = acc[k];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    tot[k] = __shfl_sync(kFull, x, 31);
+    off[k] = x - acc[k];
+    if (k < kc) ntot += tot[k];
+  }
+  // first node-nonempty bin of this lane, and of the lanes after it
+  int first_ne = -1;
+#pragma unroll
+  for (int i = 7; i >= 0; i--)
+    if (bc[i]) first_ne = b0 + i;
+  const unsigned has = __ballot_sync(kFull, first_ne >= 0);
+  const unsigned later = lane == 31 ? 0u : has & (kFull << (lane + 1));
+  const int nf = __shfl_sync(kFull, first_ne, later ? __ffs(later) - 1 : lane);
+  int nextb[8];
+  {
+    int nx = later ? nf : -1;
+#pragma unroll
+    for (int i = 7; i >= 0; i--) {
+      nextb[i] = nx;
+      if (bc[i]) nx = b0 + i;
+    }
+  }
+  Key best;
+  best.valid = 0;
+  best.idx = b0;
+  best.hi = best.lo = 0;
+  best.den = 1;
+  int best_hi = -1;
+  uint64_t best_nl = 0;
+  uint32_t cl[kSmallKc];
+#pragma unroll
+  for (int k = 0; k < kSmallKc; k++) cl[k] = off[k];
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    uint64_t nl = 0, sl = 0, sr = 0;
+#pragma unroll
+    for (int k = 0; k < kSmallKc; k++)
+      if (k < kc && b0 + i < Df) {
+        cl[k] += sg[i * kc + k];
+        const uint64_t c = cl[k], r = (uint64_t)tot[k] - cl[k];
+        nl += c;
+        sl += c * c;
+        sr += r * r;
+      }
+    if (b0 + i < Df && bc[i] > 0 && nl < ntot) {
+      const uint64_t nR = ntot - nl;
+      Key k;
+      const uint64_t x0 = sl * nR, x1 = __umul64hi(sl, nR);
+      const uint64_t y0 = sr * nl, y1 = __umul64hi(sr, nl);
+      k.lo = x0 + y0;
+      k.hi = x1 + y1 + (k.lo < x0 ? 1 : 0);
+      k.den = nl * nR;
+      k.valid = 1;
+      k.idx = b0 + i;
+      if (better(k, best)) {  // ascending bins: ties keep the lower one
+        best = k;
+        best_hi = nextb[i];
+        best_nl = nl;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const Key other = shfl_key(best, lane ^ o);
+    const int oh = __shfl_sync(kFull, best_hi, lane ^ o);
+    const uint64_t on = __shfl_sync(kFull, best_nl, lane ^ o);
+    if (better(other, best)) {
+      best = other;
+      best_hi = oh;
+      best_nl = on;
+    }
+  }
+  if (lane == 0) {
+    SplitCand c;
+    c.num_lo = best.lo;
+    c.num_hi = best.hi;
+    c.den = best.den;
+    c.nL = best_nl;
+    c.valid = best.valid;
+    c.b_lo = best.valid ? best.idx : -1;
+    c.b_hi = best.valid ? best_hi : -1;
+    c.pad = 0;
+    out[(size_t)node * F + f] = c;
+  }
+}
+
 __global__ void __launch_bounds__(256)
     winner_kernel(const uint32_t *__restrict__ H, const int64_t *node_off, const int32_t *node_kc,
                   int F, int Cmax, const int32_t *cumD, const int32_t *nval, const SplitCand *cand,
@@ -344,12 +489,23 @@ void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t DS, const SubJo
   CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_split(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,
+void launch_split(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc,
+                  const int32_t *big_nodes, int nbig, const int32_t *small_nodes, int nsmall,
                   int F, const int32_t *cumD, const int32_t *nval, SplitCand *out, cudaStream_t s) {
-  if (nnodes == 0) return;
-  split_kernel<<<dim3(nnodes, F), kSplitThreads, 0, s>>>(H, node_off, node_kc, F, cumD, nval, out);
-  CUDA_CHECK(cudaGetLastError());
+  if (nbig > 0) {
+    split_kernel<<<dim3(nbig, F), kSplitThreads, 0, s>>>(H, node_off, node_kc, big_nodes, F, cumD,
+                                                         nval, out);
+    CUDA_CHECK(cudaGetLastError());
+  }
+  if (nsmall > 0) {
+    const int njobs = nsmall * F;
+    split_small_kernel<<<(njobs + kSmallWarps - 1) / kSmallWarps, kSmallWarps * 32, 0, s>>>(
+        H, node_off, node_kc, small_nodes, njobs, F, cumD, nval, out);
+    CUDA_CHECK(cudaGetLastError());
+  }
 }
+
+int split_small_max_classes() { return kSmallKc; }
 
 void launch_winner(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,
                    int F, int C, const int32_t *cumD, const int32_t *nval, const SplitCand *cand,
