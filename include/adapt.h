@@ -134,6 +134,26 @@ int adapt_region_info(adapt_region_t *h, int *num_features, int *num_variants, i
  * per distinct feature vector (exact float32 bits, -0 == +0), each variant's
  * time = mean of its records rounded to float32, unmeasured = +inf (R1, R4). */
 int adapt_record(adapt_region_t *h, const float *features, int variant, uint64_t elapsed_ns);
+/* Long format in bulk (the GPU record path): m records
+ * features [m][F] float32, variants [m] int32 in [0,V), elapsed_ns [m] uint64.
+ * on_device = 1: device pointers, 0: host pointers; either way the records are
+ * COPIED into the region's device store (stream-ordered on `stream`, complete
+ * when the call returns).  At adapt_train() every record — the device store
+ * first, then the adapt_record() ones in call order — is aggregated ON THE GPU
+ * into one wide row per distinct feature vector in order of first appearance
+ * (exact float32 bits, -0 == +0; time = (double)sum_ns/(double)count rounded to
+ * float32; +inf = never recorded; R1, R3, R4).  A variant outside [0,V)
+ * -> ADAPT_E_BAD_VALUE at train time; NaN/Inf features -> ADAPT_E_BAD_VALUE at
+ * train time.  Record-path aggregation is rank-local (world > 1: each rank's
+ * own records).  Total records < 2^32 (else ADAPT_E_INVALID_ARG). */
+int adapt_record_batch(adapt_region_t *h, const float *features, const int32_t *variants,
+                       const uint64_t *elapsed_ns, int64_t m, int on_device, void *stream);
+/* The wide table the last adapt_train() built from records (host copies):
+ * *n = rows; copies features [n][F] and times [n][V] when cap >= n (else only
+ * sets *n).  ADAPT_E_NOT_TRAINED before training; ADAPT_E_USAGE when the last
+ * train used adapt_record_table (or adapt_distinct_pairs re-aggregated since). */
+int adapt_get_wide_table(adapt_region_t *h, float *features, float *times, int64_t cap,
+                         int64_t *n);
 /* Wide format (the profiling table): features [n][F] float32 and times
  * [n][V] float32 nanoseconds, +inf = unmeasured (R3).  With world > 1 this is
  * the calling rank's contiguous shard; the table is the concatenation over
@@ -144,7 +164,8 @@ int adapt_record_table(adapt_region_t *h, const float *features, const float *ti
                        int on_device, void *stream);
 /* Number of distinct (feature vector, variant) pairs among the long-format
  * records ("uniqueness is defined as collecting profiling data of
- * different features and variants"). */
+ * different features and variants").  With device-batch records this runs
+ * the GPU aggregation (measured cells of the wide table). */
 int adapt_distinct_pairs(adapt_region_t *h, int64_t *count);
 
 /* ---- train (Table 1 "__apollo_region_train"; P:173 + P:253-255) --------- */

@@ -36,7 +36,7 @@ SYMBOLS = [
     "adapt_init", "adapt_nccl_unique_id", "adapt_init_host_comm", "adapt_finalize",
     "adapt_last_error", "adapt_version",
     "adapt_region_create", "adapt_region_destroy", "adapt_region_info", "adapt_record",
-    "adapt_record_table", "adapt_distinct_pairs", "adapt_train", "adapt_train_many",
+    "adapt_record_batch", "adapt_get_wide_table", "adapt_record_table", "adapt_distinct_pairs", "adapt_train", "adapt_train_many",
     "adapt_select", "adapt_select_batch", "adapt_select_batch_host", "adapt_get_tree",
     "adapt_set_tree", "adapt_get_labels", "adapt_get_value_table", "adapt_get_bins",
     "adapt_profile_enable", "adapt_profile_reset", "adapt_profile_get", "adapt_train_stats",
@@ -88,6 +88,8 @@ _sigs = {
     "adapt_region_info": [_P, _P, _P, _P, _P, _P, _P],
     "adapt_record": [_P, _P, _I, _U64],
     "adapt_record_table": [_P, _P, _P, _I64, _I, _P],
+    "adapt_record_batch": [_P, _P, _P, _P, _I64, _I, _P],
+    "adapt_get_wide_table": [_P, _P, _P, _I64, _P],
     "adapt_distinct_pairs": [_P, _P],
     "adapt_train": [_P, _P],
     "adapt_train_many": [_P, _I, _P],
@@ -255,6 +257,30 @@ def adapt_record_table(h: int, features, times, n: int | None = None, on_device:
         on_device = bool(getattr(features, "is_cuda", False))
     _check(_L.adapt_record_table(h, _ptr(features), _ptr(times), int(n), int(on_device),
                                  _stream(stream)), "adapt_record_table")
+
+
+def adapt_record_batch(h: int, features, variants, elapsed_ns, m: int | None = None,
+                       on_device: bool | None = None, stream=None):
+    """m long-format records (features [m][F] f32, variants [m] i32, elapsed_ns [m] u64)."""
+    if m is None:
+        m = int(features.shape[0])
+    if on_device is None:
+        on_device = bool(getattr(features, "is_cuda", False))
+    _check(_L.adapt_record_batch(h, _ptr(features), _ptr(variants), _ptr(elapsed_ns), int(m),
+                                 int(on_device), _stream(stream)), "adapt_record_batch")
+
+
+def adapt_get_wide_table(h: int):
+    """(features [n][F] f32, times [n][V] f32) the last train aggregated from records."""
+    n = ctypes.c_int64()
+    _check(_L.adapt_get_wide_table(h, None, None, 0, ctypes.byref(n)), "adapt_get_wide_table")
+    info = adapt_region_info(h)
+    F, V = info["num_features"], info["num_variants"]
+    feat = np.empty((n.value, F), np.float32)
+    times = np.empty((n.value, V), np.float32)
+    _check(_L.adapt_get_wide_table(h, _ptr(feat), _ptr(times), n.value, ctypes.byref(n)),
+           "adapt_get_wide_table")
+    return feat, times
 
 
 def adapt_distinct_pairs(h: int) -> int:

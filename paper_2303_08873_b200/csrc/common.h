@@ -21,6 +21,7 @@ constexpr uint32_t kFlagBadFeature = 1;   // NaN/Inf feature (R4)
 constexpr uint32_t kFlagNanTime = 2;      // NaN time (R3)
 constexpr uint32_t kFlagAllInf = 4;       // every variant unmeasured (R3)
 constexpr uint32_t kFlagTooMany = 8;      // > 256 distinct values of a feature (R14)
+constexpr uint32_t kFlagBadVariant = 16;  // recorded variant outside [0, V)
 
 struct Error : std::runtime_error {
   int code;
@@ -73,6 +74,20 @@ struct NodeRes {
   // followed in memory by uint32 P[kc] (class totals) and uint32 cL[kc], compact
   // class order (res_stride leaves room for C of each)
 };
+
+// ---- kernel launchers (records.cu): long-format records -> wide rows ----
+size_t rec_table_slots(int64_t m);  // hash-set slots for m records (power of two >= 2m)
+int rec_scan_blocks(int64_t m);     // blocks of the group-id scan
+// groups the m records; *d_groups (device) = number of distinct vectors
+void launch_rec_group(const float *feat, const int32_t *var, int64_t m, int F, int V,
+                      uint32_t *slot_rep, uint32_t *slot_first, size_t slots, uint32_t *slot_of,
+                      uint32_t *flag, uint32_t *bsum, uint32_t *d_groups, uint32_t *flags,
+                      cudaStream_t s);
+// wide rows in order of first appearance; *pairs (device, optional) = measured cells
+void launch_rec_wide(const float *feat, const int32_t *var, const uint64_t *ns, int64_t m, int F,
+                     int V, const uint32_t *slot_of, uint32_t *slot_gid, const uint32_t *flag,
+                     const uint32_t *bsum, int64_t groups, unsigned long long *sum, uint32_t *cnt,
+                     float *wide_feat, float *wide_times, uint32_t *pairs, cudaStream_t s);
 
 // ---- kernel launchers (ingest.cu) ----
 int lookup_table_bytes(int F);  // size of the per-feature key -> rank perfect hashes

@@ -334,10 +334,16 @@ struct FNode {  // a frontier node: histogrammed and split-searched at this leve
 struct adapt_region {
   std::string id;
   int F = 0, V = 0, D = 2, min_train = 0;
-  // long-format records (adapt_record)
+  // long-format records: adapt_record (host, one at a time) and
+  // adapt_record_batch (device store, rec_n records)
   std::vector<float> rfeat;
   std::vector<int32_t> rvar;
   std::vector<uint64_t> rns;
+  adapt::DevBuf rec_feat, rec_var, rec_ns;
+  int64_t rec_n = 0, rec_cap = 0;
+  adapt::DevBuf slot_rep, slot_first, slot_of, rflag, rbsum, rgroups, slot_gid, rsum, rcnt;
+  adapt::DevBuf agg_feat, agg_times;  // their wide rows (GPU aggregation output)
+  bool aggregated = false;  // the last train used the record path (adapt_get_wide_table)
   // wide table
   int64_t n = 0;
   bool have_table = false;
@@ -421,37 +427,6 @@ float canon(float x) { return x == 0.0f ? 0.0f : x; }
 
 // long -> wide: one row per distinct feature vector (exact bits,
 // -0 == +0), in order of first appearance; mean time per variant (R1).
-void aggregate_records(adapt_region *h, std::vector<float> &wf, std::vector<float> &wt) {
-  const int F = h->F, V = h->V;
-  const size_t R = h->rvar.size();
-  std::unordered_map<std::string, int64_t> row_of;
-  std::vector<uint64_t> sum;
-  std::vector<int64_t> cnt;
-  std::string key(F * 4, '\0');
-  for (size_t r = 0; r < R; r++) {
-    for (int f = 0; f < F; f++) {
-      float x = canon(h->rfeat[r * F + f]);
-      memcpy(&key[f * 4], &x, 4);
-    }
-    auto it = row_of.find(key);
-    int64_t row;
-    if (it == row_of.end()) {
-      row = (int64_t)row_of.size();
-      row_of.emplace(key, row);
-      for (int f = 0; f < F; f++) wf.push_back(canon(h->rfeat[r * F + f]));
-      sum.resize(sum.size() + V, 0);
-      cnt.resize(cnt.size() + V, 0);
-    } else {
-      row = it->second;
-    }
-    sum[row * V + h->rvar[r]] += h->rns[r];
-    cnt[row * V + h->rvar[r]] += 1;
-  }
-  wt.resize(sum.size());
-  for (size_t i = 0; i < sum.size(); i++)
-    wt[i] = cnt[i] ? (float)((double)sum[i] / (double)cnt[i]) : INFINITY;
-}
-
 float round_down_f32(double t) {  // largest float32 <= t (V:A5)
   float f = (float)t;
   if ((double)f > t) f = std::nextafter(f, -INFINITY);
@@ -483,6 +458,88 @@ void h2d(DevBuf &b, const std::vector<T> &v, cudaStream_t s) {
     CUDA_CHECK(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
 }
 
+// ------------------------------------------------------------ records --
+// grow a device buffer keeping its first `keep` bytes
+void grow_keep(DevBuf &b, size_t bytes, size_t keep, cudaStream_t s) {
+  if (bytes <= b.cap) return;
+  DevBuf nb;
+  nb.ensure(bytes);
+  if (keep) CUDA_CHECK(cudaMemcpyAsync(nb.p, b.p, keep, cudaMemcpyDeviceToDevice, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  std::swap(b.p, nb.p);
+  std::swap(b.cap, nb.cap);
+}
+
+void reserve_records(adapt_region *h, int64_t need, cudaStream_t s) {
+  if (need <= h->rec_cap) return;
+  const int64_t cap = std::max<int64_t>(need, std::max<int64_t>(2 * h->rec_cap, 1024));
+  grow_keep(h->rec_feat, (size_t)cap * h->F * 4, (size_t)h->rec_n * h->F * 4, s);
+  grow_keep(h->rec_var, (size_t)cap * 4, (size_t)h->rec_n * 4, s);
+  grow_keep(h->rec_ns, (size_t)cap * 8, (size_t)h->rec_n * 8, s);
+  h->rec_cap = cap;
+}
+
+// SURVEY §8(c) step 0 on the GPU (records.cu): every record (the device
+// store, then the host-recorded ones) -> wide rows in agg_feat / agg_times.
+// Returns the number of wide rows; *pairs (optional) = distinct (vector,
+// variant) pairs = measured cells of the wide table.
+int64_t gpu_aggregate(adapt_region *h, cudaStream_t s, int64_t *pairs) {
+  const int F = h->F, V = h->V;
+  const int64_t hn = (int64_t)h->rvar.size(), m = h->rec_n + hn;
+  if (m == 0) return 0;
+  if (m >= (int64_t)0xFFFFFFFFll) throw Error(ADAPT_E_INVALID_ARG, "more than 2^32-1 records");
+  reserve_records(h, m, s);
+  if (hn) {  // host records after the device store (re-uploaded by every call)
+    CUDA_CHECK(cudaMemcpyAsync(h->rec_feat.as<float>() + h->rec_n * F, h->rfeat.data(),
+                               (size_t)hn * F * 4, cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(h->rec_var.as<int32_t>() + h->rec_n, h->rvar.data(), (size_t)hn * 4,
+                               cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(h->rec_ns.as<uint64_t>() + h->rec_n, h->rns.data(), (size_t)hn * 8,
+                               cudaMemcpyHostToDevice, s));
+  }
+  const size_t slots = rec_table_slots(m);
+  h->slot_rep.ensure(slots * 4);
+  h->slot_first.ensure(slots * 4);
+  h->slot_gid.ensure(slots * 4);
+  h->slot_of.ensure((size_t)m * 4);
+  h->rflag.ensure((size_t)m * 4);
+  h->rbsum.ensure((size_t)rec_scan_blocks(m) * 4 + 16);
+  h->rgroups.ensure(16);
+  h->flags.ensure(16);
+  CUDA_CHECK(cudaMemsetAsync(h->flags.p, 0, 16, s));
+  uint32_t *hs = h->hsmall.as<uint32_t>();
+  {
+    Phase ph("records", s, (double)m * (4.0 * F + 12));
+    launch_rec_group(h->rec_feat.as<float>(), h->rec_var.as<int32_t>(), m, F, V,
+                     h->slot_rep.as<uint32_t>(), h->slot_first.as<uint32_t>(), slots,
+                     h->slot_of.as<uint32_t>(), h->rflag.as<uint32_t>(), h->rbsum.as<uint32_t>(),
+                     h->rgroups.as<uint32_t>(), h->flags.as<uint32_t>(), s);
+  }
+  CUDA_CHECK(cudaMemcpyAsync(hs, h->rgroups.p, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaMemcpyAsync(hs + 1, h->flags.p, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  if (hs[1] & kFlagBadVariant) throw Error(ADAPT_E_BAD_VALUE, "recorded variant out of range");
+  const int64_t G = hs[0];
+  h->agg_feat.ensure((size_t)G * F * 4 + 16);
+  h->agg_times.ensure((size_t)G * V * 4 + 16);
+  h->rsum.ensure((size_t)G * V * 8 + 16);
+  h->rcnt.ensure((size_t)G * V * 4 + 16);
+  {
+    Phase ph("records", s, 0);
+    launch_rec_wide(h->rec_feat.as<float>(), h->rec_var.as<int32_t>(), h->rec_ns.as<uint64_t>(), m,
+                    F, V, h->slot_of.as<uint32_t>(), h->slot_gid.as<uint32_t>(),
+                    h->rflag.as<uint32_t>(), h->rbsum.as<uint32_t>(), G,
+                    h->rsum.as<unsigned long long>(), h->rcnt.as<uint32_t>(), h->agg_feat.as<float>(),
+                    h->agg_times.as<float>(), pairs ? h->rgroups.as<uint32_t>() + 1 : nullptr, s);
+  }
+  if (pairs) {
+    CUDA_CHECK(cudaMemcpyAsync(hs, h->rgroups.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    *pairs = hs[0];
+  }
+  return G;
+}
+
 // ------------------------------------------------------------ training --
 void train_region(adapt_region *h, cudaStream_t s) {
   const int F = h->F, V = h->V, C = V, D = h->D;
@@ -501,19 +558,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
   // 0. source table (wide, or long records aggregated on the host)
   const float *feat = h->d_feat, *times = h->d_times;
   int64_t n = h->n;
-  if (!h->have_table) {
-    std::vector<float> wf, wt;
-    aggregate_records(h, wf, wt);
-    n = (int64_t)(wf.size() / F);
-    h->own_feat.ensure(wf.size() * 4 + 16);
-    h->own_times.ensure(wt.size() * 4 + 16);
-    if (n) {
-      CUDA_CHECK(cudaMemcpyAsync(h->own_feat.p, wf.data(), wf.size() * 4, cudaMemcpyHostToDevice, s));
-      CUDA_CHECK(cudaMemcpyAsync(h->own_times.p, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, s));
-      CUDA_CHECK(cudaStreamSynchronize(s));
-    }
-    feat = h->own_feat.as<float>();
-    times = h->own_times.as<float>();
+  h->hsmall.ensure(1 << 16);
+  h->aggregated = !h->have_table;
+  if (!h->have_table) {  // long-format records -> wide rows, on the GPU
+    n = gpu_aggregate(h, s, nullptr);
+    feat = h->agg_feat.as<float>();
+    times = h->agg_times.as<float>();
   }
   uint64_t n_total = (uint64_t)n;
   h->hsmall.ensure(1 << 16);
@@ -1272,7 +1322,7 @@ int adapt_region_info(adapt_region_t *h, int *F, int *V, int *D, int *mtd, int64
     if (V) *V = h->V;
     if (D) *D = h->D;
     if (mtd) *mtd = h->min_train;
-    if (rows) *rows = h->have_table ? h->n : (int64_t)h->rvar.size();
+    if (rows) *rows = h->have_table ? h->n : (int64_t)h->rvar.size() + h->rec_n;
     if (trained) *trained = h->trained;
   });
 }
@@ -1287,6 +1337,47 @@ int adapt_record(adapt_region_t *h, const float *features, int variant, uint64_t
     h->rfeat.insert(h->rfeat.end(), features, features + h->F);
     h->rvar.push_back(variant);
     h->rns.push_back(elapsed_ns);
+  });
+}
+
+int adapt_record_batch(adapt_region_t *h, const float *features, const int32_t *variants,
+                       const uint64_t *elapsed_ns, int64_t m, int on_device, void *stream) {
+  return guarded([&] {
+    checked(h);
+    ensure_init();
+    if (m < 0 || (m > 0 && (!features || !variants || !elapsed_ns)))
+      throw Error(ADAPT_E_INVALID_ARG, "bad record batch");
+    if (m == 0) return;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (h->rec_n + m + (int64_t)h->rvar.size() >= (int64_t)0xFFFFFFFFll)
+      throw Error(ADAPT_E_INVALID_ARG, "more than 2^32-1 records");
+    reserve_records(h, h->rec_n + m, s);
+    const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CUDA_CHECK(cudaMemcpyAsync(h->rec_feat.as<float>() + h->rec_n * h->F, features,
+                               (size_t)m * h->F * 4, k, s));
+    CUDA_CHECK(cudaMemcpyAsync(h->rec_var.as<int32_t>() + h->rec_n, variants, (size_t)m * 4, k, s));
+    CUDA_CHECK(cudaMemcpyAsync(h->rec_ns.as<uint64_t>() + h->rec_n, elapsed_ns, (size_t)m * 8, k, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));  // host sources may be reused after return
+    h->rec_n += m;
+  });
+}
+
+int adapt_get_wide_table(adapt_region_t *h, float *features, float *times, int64_t cap,
+                         int64_t *n) {
+  return guarded([&] {
+    checked(h);
+    if (!n) throw Error(ADAPT_E_INVALID_ARG, "null n");
+    if (!h->trained) throw Error(ADAPT_E_NOT_TRAINED, "not trained");
+    if (!h->aggregated) throw Error(ADAPT_E_USAGE, "the last train used a wide table, not records");
+    *n = h->trained_n;
+    if (cap < h->trained_n) return;  // size query
+    if (h->trained_n && (!features || !times)) throw Error(ADAPT_E_INVALID_ARG, "null output");
+    if (h->trained_n) {
+      CUDA_CHECK(cudaMemcpy(features, h->agg_feat.p, (size_t)h->trained_n * h->F * 4,
+                            cudaMemcpyDeviceToHost));
+      CUDA_CHECK(cudaMemcpy(times, h->agg_times.p, (size_t)h->trained_n * h->V * 4,
+                            cudaMemcpyDeviceToHost));
+    }
   });
 }
 
@@ -1321,7 +1412,14 @@ int adapt_distinct_pairs(adapt_region_t *h, int64_t *count) {
   return guarded([&] {
     checked(h);
     if (!count) throw Error(ADAPT_E_INVALID_ARG, "null count");
-    *count = distinct_pairs(h);
+    if (h->rec_n == 0) {
+      *count = distinct_pairs(h);  // host records only: the shim's per-call bookkeeping
+    } else {  // with device-batch records: measured cells of the GPU aggregation
+      ensure_init();
+      h->hsmall.ensure(1 << 16);
+      gpu_aggregate(h, nullptr, count);
+      h->aggregated = false;  // agg_feat/times now hold this count's aggregation
+    }
   });
 }
 
@@ -1578,7 +1676,8 @@ void __adapt_region_end(void *r) {
 void __adapt_region_train(void *r) {
   guarded([&] {
     adapt_region *h = checked(static_cast<adapt_region *>(r));
-    if (h->rvar.empty() && !h->have_table) throw Error(ADAPT_E_INSUFFICIENT_DATA, "no records (S:181)");
+    if (h->rvar.empty() && h->rec_n == 0 && !h->have_table)
+      throw Error(ADAPT_E_INSUFFICIENT_DATA, "no records (S:181)");
     int rc = adapt_train(h, nullptr);
     if (rc) throw Error(rc, g_last_error);
   });
