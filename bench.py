@@ -166,6 +166,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=0)
+    ap.add_argument("--records", type=int, default=20_000_000, help="record-path batch size")
+    ap.add_argument("--no-records", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -259,6 +261,32 @@ def main():
                "timer": "host wall clock around synchronous C-ABI calls, max over ranks"}
         del hX, hT, hout
 
+    # ---- the GPU record path: long-format records -> wide rows ----
+    rec = None
+    if not args.no_records and world == 1:
+        M = args.records
+        g = torch.Generator(device=dev).manual_seed(5)
+        rows = torch.randint(0, min(n, 500_000), (M,), device=dev, generator=g)
+        rv = torch.randint(0, cfg.V, (M,), device=dev, generator=g, dtype=torch.int32)
+        rX = X[rows].contiguous()
+        rns = T[rows, rv.long()].to(torch.int64).contiguous()
+        hr = ad.adapt_region_create(f"bench_rec_{args.config}", cfg.F, cfg.V, f"dtree,depth={cfg.D}", 0)
+        ad.adapt_record_batch(hr, rX, rv, rns, M, True, stream)
+        ad.adapt_train(hr, stream)  # warm-up
+        ad.adapt_profile_reset()
+        ad.adapt_profile_enable(True)
+        ad.adapt_train(hr, stream)
+        ad.adapt_profile_enable(False)
+        rp = ad.adapt_profile_get().get("records", {"ms": 0.0, "launches": 0, "bytes": 0.0})
+        wide = ad.adapt_region_info(hr)["num_rows"]
+        rec = {"records": M, "distinct_vectors": int(len(ad.adapt_get_wide_table(hr)[0])),
+               "ms": rp["ms"], "records_per_s": M / (rp["ms"] / 1e3) if rp["ms"] else None,
+               "launches": rp["launches"],
+               "note": "device-batch records from the first 5e5 C4 rows x random variants; "
+                       "GPU aggregation only (the train that follows is the main metric's path)"}
+        del rX, rns, rv, rows
+        _ = wide
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -317,6 +345,7 @@ def main():
         "roofline": roofline,
         "level_loop_roofline": level_loop,
         "cpu_baseline": cpu,
+        "record_path": rec,
         "phase_ms_per_step": step_ms_phases,
         "tree_nodes": int(len(tree)),
         "levels": levels,
