@@ -166,6 +166,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=0)
+    ap.add_argument("--depth", type=int, default=0, help="override the config's depth (testing only)")
     ap.add_argument("--records", type=int, default=20_000_000, help="record-path batch size")
     ap.add_argument("--no-records", action="store_true")
     args = ap.parse_args()
@@ -189,6 +190,9 @@ def main():
     adist.init_nccl(local, rank, world)
 
     cfg = synth.CONFIGS[args.config]
+    if args.depth:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, D=args.depth)
     N = args.rows or (cfg.N if cfg.regions == 1 else len(synth.region_rows(cfg, 0)))
     lo, hi = adist.shard_bounds(N, rank, world)
     n = hi - lo

@@ -227,6 +227,40 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
       continue;
     }
     const int kwp = kn | 1;  // odd stride: bank spread
+    int gneed = 0;           // counters the smem path would zero and flush
+#pragma unroll
+    for (int e = 0; e < 4; e++) gneed += Dw[e] * kwp;
+    if ((int64_t)(pe - p0) * 16 < gneed) {
+      // a tiny portion (deep levels): count straight into the node's global
+      // matrix (zeroed by zero_slots) — no smem zero/flush, no block barrier
+      const uint8_t *m = a.cmaps + (size_t)first.cmap * C;
+      uint32_t *dst = a.H + a.soff[first.hslot] + k0;
+      int64_t fb[4];
+#pragma unroll
+      for (int e = 0; e < 4; e++) fb[e] = Dw[e] ? (int64_t)a.cumD[4 * w0 + e] * kcn : -1;
+      for (; s < a.nseg && a.segs[s].row_base < pe; s++) {
+        const Seg sg = a.segs[s];
+        const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
+        const uint32_t q1 = min(sg.len, pe - sg.row_base);
+        for (uint32_t q = q0 + tid; q < q1; q += blockDim.x) {
+          const uint32_t row = sg.off + q;
+          uint32_t w;
+          if constexpr (BS >= 4)
+            w = *reinterpret_cast<const uint32_t *>(a.bins_in + w0 * a.pstride + (size_t)row * 4);
+          else if constexpr (BS == 2)
+            w = *reinterpret_cast<const unsigned short *>(a.bins_in + (size_t)row * 2);
+          else
+            w = a.bins_in[row];
+          const int lk = (int)__ldg(m + a.lab_in[row]) - k0;
+          if ((unsigned)lk >= (unsigned)kn) continue;
+#pragma unroll
+          for (int e = 0; e < 4; e++)
+            if (fb[e] >= 0) atomicAdd(dst + fb[e] + (int64_t)((w >> (8 * e)) & 0xFF) * kcn + lk, 1u);
+        }
+      }
+      p0 = pe;
+      continue;
+    }
     {
       const uint8_t *m = a.cmaps + (size_t)first.cmap * C;
       for (int k = tid; k < C; k += blockDim.x) s_cmap[k] = m[k];
