@@ -151,6 +151,7 @@ struct HistArgs {            // a4: class histograms of the given pieces' rows
   uint32_t *sync;            // [nranges] partner-sync counters, zeroed (null: no sync)
 };
 void launch_hist(const HistArgs &a, cudaStream_t s);
+void launch_hist_flat(const HistArgs &a, cudaStream_t s);  // small nodes: thread per row
 
 struct SubJob {              // derived node = parent - direct sibling, class-remapped
   int64_t off_d, off_p, off_s;  // element offsets: derived (H), parent (Hprev), sibling (H)

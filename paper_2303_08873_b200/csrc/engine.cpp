@@ -925,10 +925,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
     }
     if (trace) tr[3] = now_us();
     // ---- a4: histograms of the direct nodes (the root, or the smaller children) ----
-    std::vector<Seg> hsegs;
+    std::vector<Seg> hsegs, fsegs;  // big nodes: smem-privatised pass; small: flat pass
     for (int j = 0; j < A; j++) {
       const FNode &fn = frontier[j];
       if (!fn.direct) continue;
+      int64_t local = 0;
+      for (int q = pc_start[j]; q < pc_start[j + 1]; q++) local += pcs[q].second;
+      const bool small = local * 16 < DS * (node_kc[j] | 1);
       for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {
         const auto &pc = pcs[q];
         Seg sg{};
@@ -937,14 +940,15 @@ void train_region(adapt_region *h, cudaStream_t s) {
         sg.hslot = fn.slot;
         sg.cmap = node_ci[j];
         sg.ncls = node_kc[j];
-        hsegs.push_back(sg);
+        (small ? fsegs : hsegs).push_back(sg);
       }
     }
+    const uint32_t ftotal = virtualize(fsegs, true);
     const uint32_t htotal = virtualize(hsegs, true);
-    if (htotal > 0) {
+    if (htotal + ftotal > 0) {
       Arena &sb = h->stage_b;
       sb.reset();
-      const size_t o_hsegs = sb.put(hsegs);
+      const size_t o_hsegs = sb.put(hsegs), o_fsegs = sb.put(fsegs);
       sb.flush(s);
       HistArgs ha{};
       ha.segs = sb.ptr<Seg>(o_hsegs);
@@ -977,8 +981,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
         ha.sync = h->psync.as<uint32_t>();
       }
       snprintf(nm, sizeof nm, "hist_L%02d", level);
-      Phase ph(per_level ? nm : "hist", s, (double)htotal * (F + 1));
+      Phase ph(per_level ? nm : "hist", s, (double)(htotal + ftotal) * (F + 1));
       launch_hist(ha, s);
+      HistArgs fa = ha;  // the small nodes
+      fa.segs = sb.ptr<Seg>(o_fsegs);
+      fa.nseg = (int)fsegs.size();
+      fa.total_rows = ftotal;
+      launch_hist_flat(fa, s);
     }
     if (world > 1 && ndirect_slots > 0)  // the direct slots are contiguous at the front
       comm_allreduce_sum(Hcur->p, (size_t)soff[ndirect_slots], false, s, "allreduce histograms");
@@ -1010,7 +1019,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     CUDA_CHECK(cudaStreamSynchronize(s));
     if (trace) tr[5] = now_us();
     h->stats.push_back(A);
-    h->stats.push_back(htotal);
+    h->stats.push_back(htotal + ftotal);
     h->stats.push_back(rows_part);
 
     // ---- decide every frontier node; build the next level ----

@@ -361,6 +361,32 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
   }
 }
 
+// Small direct nodes (deep levels): a flat pass over their rows, one thread
+// per row and all F features, counting straight into each node's global
+// matrix (zeroed by zero_slots).  A node's smem block would cost more to zero
+// and flush than its few rows cost in global atomics.
+template <int BS>
+__global__ void __launch_bounds__(256) hist_flat_kernel(HistArgs a) {
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < a.total_rows;
+       p = (uint32_t)min((uint64_t)p + gridDim.x * blockDim.x, (uint64_t)a.total_rows)) {
+    const Seg sg = a.segs[first_seg(a.segs, a.nseg, p)];
+    const uint32_t row = sg.off + (p - sg.row_base);
+    Row<BS> r;
+    load_row<BS>(a.bins_in, a.pstride, row, r);
+    const int kcn = sg.ncls;
+    const int lk = (int)__ldg(a.cmaps + (size_t)sg.cmap * a.C + a.lab_in[row]);
+    uint32_t *dst = a.H + a.soff[sg.hslot] + lk;
+#pragma unroll
+    for (int i = 0; i < Row<BS>::N; i++)
+#pragma unroll
+      for (int e = 0; e < (BS >= 4 ? 4 : BS); e++) {
+        const int f = 4 * i + e;
+        if (f < a.F)
+          atomicAdd(dst + (int64_t)(__ldg(a.cumD + f) + (int)((r.w[i] >> (8 * e)) & 0xFF)) * kcn, 1u);
+      }
+  }
+}
+
 }  // namespace
 
 int partition_ranges(int sms, uint32_t total_rows) {
@@ -373,6 +399,25 @@ void launch_partition(const PartArgs &a, cudaStream_t s) {
 #define CASE(B)                                                                               \
   case B:                                                                                     \
     partition_kernel<B><<<a.nranges, kPartThreads, 0, s>>>(a);                                \
+    break;
+    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
+#undef CASE
+    default:
+      throw Error(-1, "bad bins stride");
+  }
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_hist_flat(const HistArgs &a, cudaStream_t s) {
+  if (a.total_rows == 0 || a.nseg == 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>((a.total_rows + 255) / 256, 8 * sms);
+  switch (a.BS) {
+#define CASE(B)                                                 \
+  case B:                                                       \
+    hist_flat_kernel<B><<<grid, 256, 0, s>>>(a);                \
     break;
     CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
 #undef CASE
