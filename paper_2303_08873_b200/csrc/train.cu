@@ -136,11 +136,15 @@ __global__ void __launch_bounds__(kSplitThreads)
     {  // the chunk's Df x kc counts, flat over all threads: independent loads in
        // flight (contiguous when the node has <= kClassChunk classes)
       const int E = Df * kc;
-#pragma unroll 4
-      for (int e = t; e < E; e += kSplitThreads) {
+      const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(&tile[0][0]);
+      for (int e = t; e < E; e += kSplitThreads) {  // async copies: all in flight at once
         const int r = e / kc, k = e - r * kc;
-        tile[r][k] = __ldg(h + (size_t)r * C + c0 + k);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                         tbase + 4u * (uint32_t)(r * (kClassChunk + 1) + k)),
+                     "l"(h + (size_t)r * C + c0 + k)
+                     : "memory");
       }
+      asm volatile("cp.async.wait_all;" ::: "memory");
     }
     __syncthreads();
     // prefix over bins: warp w scans rows [32w, 32w+32) of column `lane`
@@ -271,14 +275,17 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
   const int kc = node_kc[node], Df = nval[f];
   const uint32_t *h = H + node_off[node] + (int64_t)cumD[f] * kc;
   uint32_t *tl = wt[warp];
-  {
+  {  // asynchronous 4-byte copies (no registers held): every load in flight at once
     const int E = Df * kc;
     const float inv = 1.0f / (float)kc;  // exact enough: e < 2048, kc <= 8
-#pragma unroll 4
+    const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(tl);
     for (int e = lane; e < E; e += 32) {
       const int b = __float2int_rz(((float)e + 0.5f) * inv);
-      tl[e + (b >> 3)] = __ldg(h + e);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tbase + 4u * (e + (b >> 3))),
+                   "l"(h + e)
+                   : "memory");
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   }
   __syncwarp();
   const int b0 = lane * 8;
