@@ -76,6 +76,7 @@ def lib():
         L.oracle_value_table.argtypes = [P, i64, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P]
         L.oracle_train.argtypes = [P, P, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, i32, P]
         L.oracle_select.argtypes = [P, i32, P, i64, ctypes.c_int, P]
+        L.oracle_bootstrap.argtypes = [ctypes.c_uint64, ctypes.c_int, i64, P]
         L.oracle_gini_counts.argtypes = [P, ctypes.c_int]
         L.oracle_gini_counts.restype = ctypes.c_double
         _lib = L
@@ -195,3 +196,33 @@ def select(tree: np.ndarray, X: np.ndarray) -> np.ndarray:
 def gini_counts(counts) -> float:
     c = np.ascontiguousarray(counts, dtype=np.int64)
     return float(lib().oracle_gini_counts(_p(c), c.size))
+
+
+# ---- random forest ("rfc"; SPEC train_rfc / predict; R19-R21) ----
+def bootstrap(seed: int, tree: int, n: int) -> np.ndarray:
+    """Multiplicities of the size-n bootstrap resample of tree `tree` (R19)."""
+    w = np.zeros(max(n, 1), np.uint32)
+    rc = lib().oracle_bootstrap(ctypes.c_uint64(seed), int(tree), int(n), _p(w))
+    if rc:
+        raise OracleError(rc, "bootstrap")
+    return w[:n]
+
+
+def train_forest(X: np.ndarray, y: np.ndarray, V: int, D: int, T: int, seed: int) -> list:
+    """Tree t = the plain CART (train) on the bootstrap resample of tree t:
+    every row repeated w[i] times (SPEC train_rfc; no feature subsampling)."""
+    trees = []
+    for t in range(T):
+        w = bootstrap(seed, t, len(X)).astype(np.int64)
+        trees.append(train(np.repeat(X, w, axis=0), np.repeat(y, w), V, D))
+    return trees
+
+
+def select_forest(trees: list, X: np.ndarray) -> np.ndarray:
+    """Majority vote of the trees' selections, ties -> lowest variant (R20)."""
+    votes = np.stack([select(t, X) for t in trees])  # [T][m]
+    out = np.empty(votes.shape[1], np.int32)
+    for i in range(votes.shape[1]):
+        labels, counts = np.unique(votes[:, i], return_counts=True)  # ascending labels
+        out[i] = labels[np.argmax(counts)]  # first maximum = lowest label
+    return out

@@ -370,3 +370,23 @@ int oracle_select(const oracle_node_t *tree, int32_t n_nodes, const float *X, in
   }
   return ORACLE_OK;
 }
+
+/* ---- random forest bootstrap (R19) ---- */
+static uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+int oracle_bootstrap(uint64_t seed, int tree, int64_t n, uint32_t *w) {
+  if (n < 0 || tree < 0 || (n > 0 && !w)) return ORACLE_E_INVALID_ARG;
+  for (int64_t i = 0; i < n; i++) w[i] = 0;
+  const uint64_t key = splitmix64(seed ^ splitmix64((uint64_t)tree + 0x5851F42D4C957F2Dull));
+  for (int64_t j = 0; j < n; j++) {
+    const uint64_t h = splitmix64(key ^ splitmix64((uint64_t)j));
+    const int64_t i = (int64_t)(((unsigned __int128)h * (uint64_t)n) >> 64);
+    w[i] += 1;
+  }
+  return 0;
+}

@@ -90,6 +90,15 @@ int oracle_train(const float *X, const uint8_t *y, int64_t n, int F, int C, int 
 int oracle_select(const oracle_node_t *tree, int32_t n_nodes, const float *X,
                   int64_t m, int F, int32_t *out);
 
+/* Random forest ("rfc"; SPEC train_rfc; readings R19-R21).
+ * Bootstrap multiplicities of tree t (R19): n draws with replacement,
+ * draw j picks row floor(h_j * n / 2^64), h_j = splitmix64(key_t ^ splitmix64(j)),
+ * key_t = splitmix64(seed ^ splitmix64(t + 0x5851F42D4C957F2D)); w[i] = number of
+ * draws of row i (sum = n).  The forest itself is plain: tree t = oracle_train on
+ * the resample (rows repeated w[i] times), vote = majority, ties -> lowest
+ * (R20) — composed in oracle/__init__.py from this and oracle_train/select. */
+int oracle_bootstrap(uint64_t seed, int tree, int64_t n, uint32_t *w);
+
 /* Helper used by the pins: Gini of a class-count vector, 1 - S/(n*n). */
 double oracle_gini_counts(const int64_t *counts, int C);
 
