@@ -117,6 +117,11 @@ const char *adapt_version(void);
  * (variants are enumerated 0..V-1 in declaration order).
  * model_params: "dtree" | "dtree,depth=D" | "dtree,D" | "DecisionTree[,explore=RoundRobin]"
  * (P:142); NULL or "" -> dtree depth 2.  D in [0,24].
+ * Random forest ("rfc"): "rfc" | "rfc,T,D" | "rfc(T,D)" |
+ * "rfc,trees=T,depth=D,seed=S" | "RandomForest[...]": T trees (default 10,
+ * [1,64]) of depth D (default 2), each trained on a bootstrap resample of the
+ * table drawn from a counter RNG keyed by (seed, tree) (R19, default seed 0);
+ * selection = majority vote, ties -> lowest variant (R20).
  * min_train_data <= 0 -> V.
  * Same id and same spec -> the same handle; same id with a different
  * spec -> ADAPT_E_SPEC_MISMATCH. */
@@ -198,6 +203,12 @@ int adapt_select_batch_host(adapt_region_t *h, const float *X, int64_t m, int32_
 /* Canonical BFS node array; *n_nodes receives the node count even when cap is
  * too small (then ADAPT_E_INVALID_ARG). */
 int adapt_get_tree(adapt_region_t *h, adapt_node_t *out, int32_t cap, int32_t *n_nodes);
+/* Forests: number of trees (1 for a decision tree), and tree t in canonical
+ * BFS order (same layout and rules as adapt_get_tree; adapt_get_tree returns
+ * tree 0).  ADAPT_E_INVALID_ARG for t out of range or cap too small. */
+int adapt_forest_size(adapt_region_t *h, int32_t *trees);
+int adapt_get_forest_tree(adapt_region_t *h, int32_t t, adapt_node_t *out, int32_t cap,
+                          int32_t *n_nodes);
 /* Install a tree (model reuse across runs; synthetic trees for the
  * selection benchmark).  Validates BFS structure, features and labels. */
 int adapt_set_tree(adapt_region_t *h, const adapt_node_t *nodes, int32_t n_nodes);

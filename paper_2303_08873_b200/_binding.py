@@ -38,6 +38,7 @@ SYMBOLS = [
     "adapt_region_create", "adapt_region_destroy", "adapt_region_info", "adapt_record",
     "adapt_record_batch", "adapt_get_wide_table", "adapt_record_table", "adapt_distinct_pairs", "adapt_train", "adapt_train_many",
     "adapt_select", "adapt_select_batch", "adapt_select_batch_host", "adapt_get_tree",
+    "adapt_forest_size", "adapt_get_forest_tree",
     "adapt_set_tree", "adapt_get_labels", "adapt_get_value_table", "adapt_get_bins",
     "adapt_profile_enable", "adapt_profile_reset", "adapt_profile_get", "adapt_train_stats",
     "__adapt_region_create", "__adapt_region_begin", "__adapt_region_end",
@@ -97,6 +98,8 @@ _sigs = {
     "adapt_select_batch": [_P, _P, _I64, _P, _P],
     "adapt_select_batch_host": [_P, _P, _I64, _P, _P],
     "adapt_get_tree": [_P, _P, ctypes.c_int32, _P],
+    "adapt_forest_size": [_P, _P],
+    "adapt_get_forest_tree": [_P, ctypes.c_int32, _P, ctypes.c_int32, _P],
     "adapt_set_tree": [_P, _P, ctypes.c_int32],
     "adapt_get_labels": [_P, _P, _I64],
     "adapt_get_value_table": [_P, _I, _P, _P],
@@ -323,6 +326,22 @@ def adapt_get_tree(h: int) -> np.ndarray:
     out = np.zeros(n.value, NODE_DTYPE)
     _check(_L.adapt_get_tree(h, out.ctypes.data, n.value, ctypes.byref(n)), "adapt_get_tree")
     return out
+
+
+def adapt_forest_size(h: int) -> int:
+    t = ctypes.c_int32()
+    _check(_L.adapt_forest_size(h, ctypes.byref(t)), "adapt_forest_size")
+    return t.value
+
+
+def adapt_get_forest_tree(h: int, t: int) -> np.ndarray:
+    """Tree t of a forest (tree 0 of a decision-tree region), NODE_DTYPE records."""
+    n = ctypes.c_int32()
+    _L.adapt_get_forest_tree(h, int(t), None, 0, ctypes.byref(n))  # size query (cap 0)
+    out = np.zeros(max(n.value, 1), NODE_DTYPE)
+    _check(_L.adapt_get_forest_tree(h, int(t), out.ctypes.data, len(out), ctypes.byref(n)),
+           "adapt_get_forest_tree")
+    return out[:n.value]
 
 
 def adapt_set_tree(h: int, nodes: np.ndarray):

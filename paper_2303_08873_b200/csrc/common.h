@@ -22,6 +22,7 @@ constexpr uint32_t kFlagNanTime = 2;      // NaN time (R3)
 constexpr uint32_t kFlagAllInf = 4;       // every variant unmeasured (R3)
 constexpr uint32_t kFlagTooMany = 8;      // > 256 distinct values of a feature (R14)
 constexpr uint32_t kFlagBadVariant = 16;  // recorded variant outside [0, V)
+constexpr uint32_t kFlagBootstrap = 32;   // a bootstrap multiplicity above 255 (u8 weights)
 
 struct Error : std::runtime_error {
   int code;
@@ -119,6 +120,8 @@ struct PartArgs {            // a7: move the split parents' rows into the childr
   uint32_t total_rows;       // sum of the pieces' lengths (virtual positions)
   const uint8_t *bins_in, *lab_in;  // input: bins word planes (see level.cu), labels [pos]
   uint8_t *bins_out, *lab_out;      // output planes, indexed by virtual position
+  const uint8_t *w_in;              // forests: bootstrap weight plane (null: every row weighs 1);
+  uint8_t *w_out;                   //   rows of weight 0 are dropped, the plane moves with the rows
   size_t pstride;                   // bytes between bins word planes
   int BS, F;
   int32_t *visits;           // [nranges][max_visits][6]: seg, share [A, B), left, right moved
@@ -137,6 +140,7 @@ struct HistArgs {            // a4: class histograms of the given pieces' rows
   int nseg;
   uint32_t total_rows;
   const uint8_t *bins_in, *lab_in;
+  const uint8_t *w_in;       // forests: row weights (bootstrap multiplicities); null: 1
   size_t pstride;            // bytes between bins word planes
   int BS, F, C;
   const int32_t *cumD;       // [F] first histogram row of feature f
@@ -182,6 +186,16 @@ struct DNode {     // device inference node, 8 bytes
   float thr;       // largest float32 <= threshold (x <= thr_f64  <=>  x <= thr_f32, V:A5)
   int32_t meta;    // >= 0: (left << 6) | feature ; < 0: -1 - label
 };
+
+// ---- kernel launchers (forest.cu): random forests ----
+// u8 bootstrap weights of this rank's rows [lo, lo + n_local) for tree `tree` (R19)
+void launch_bootstrap(uint64_t seed, int tree, uint64_t n_total, uint64_t lo, int64_t n_local,
+                      uint32_t *cnt, uint8_t *w, uint32_t *flags, cudaStream_t s);
+int forest_max_trees();
+// majority vote of the T trees rooted at roots[t] in the concatenated node array
+void launch_select_forest(const DNode *nodes, int n_nodes, const int32_t *roots, int T,
+                          const float *X, int64_t m, int F, int32_t *out, cudaStream_t s);
+
 void launch_select(const DNode *tree, int n_nodes, const float *X, int64_t m, int F,
                    int32_t *out, cudaStream_t s);
 

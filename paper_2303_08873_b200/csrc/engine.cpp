@@ -355,6 +355,14 @@ struct adapt_region {
   int64_t trained_n = 0;
   adapt::DevBuf bins, labels;   // ingest output in row order (kept for introspection)
   adapt::DevBuf binsA, binsB, labA, labB;  // level planes, rows grouped by node span
+  // random forest (kind 1): T trees of depth D on bootstrap resamples (R19-R21)
+  int kind = 0;        // 0: dtree, 1: rfc
+  int T = 1;
+  uint64_t seed = 0;
+  std::vector<std::vector<adapt_node_t>> forest;  // canonical BFS trees
+  adapt::DevBuf d_forest, d_roots;                 // concatenated device nodes, root indices
+  int forest_nodes = 0;
+  adapt::DevBuf wcnt, wplane, wA, wB;              // bootstrap counts / weight planes
   std::vector<float> val;       // [F][256]
   std::vector<int32_t> nval;    // [F]
   std::vector<adapt_node_t> tree;
@@ -380,10 +388,21 @@ namespace {
 
 std::map<std::string, std::unique_ptr<adapt_region>> g_regions;
 
-int parse_params(const char *p, int *depth) {
-  *depth = 2;  // P:260 default: decision tree of depth 2
+// model_type: "dtree[,D]" / "dtree,depth=D" /
+// "DecisionTree[,explore=RoundRobin]"; "rfc[,T[,D]]" / "rfc(T,D)" /
+// "rfc,trees=T,depth=D,seed=S" / "RandomForest[...]" ("model_type(rfc,
+// 10, 4)": trees, then depth).  Defaults: dtree depth 2; rfc 10 trees
+// of depth 2, seed 0 (R21).
+int parse_params(const char *p, int *depth, int *kind, int *trees, uint64_t *seed) {
+  *depth = 2;
+  *kind = 0;
+  *trees = 1;
+  *seed = 0;
   if (!p || !*p) return 0;
   std::string s(p);
+  for (char &c : s)
+    if (c == '(') c = ',';
+  s.erase(std::remove(s.begin(), s.end(), ')'), s.end());
   std::vector<std::string> tok;
   size_t st = 0;
   while (true) {
@@ -395,23 +414,36 @@ int parse_params(const char *p, int *depth) {
     if (c == std::string::npos) break;
     st = c + 1;
   }
-  if (tok[0] != "dtree" && tok[0] != "DecisionTree")
-    throw Error(ADAPT_E_INVALID_ARG, "model kind '" + tok[0] + "' not supported (dtree)");
+  if (tok[0] == "rfc" || tok[0] == "RandomForest") {
+    *kind = 1;
+    *trees = 10;
+  } else if (tok[0] != "dtree" && tok[0] != "DecisionTree") {
+    throw Error(ADAPT_E_INVALID_ARG, "model kind '" + tok[0] + "' not supported (dtree, rfc)");
+  }
+  auto num = [&](const std::string &v, const std::string &t) {
+    char *end = nullptr;
+    const long long d = strtoll(v.c_str(), &end, 10);
+    if (v.empty() || *end) throw Error(ADAPT_E_INVALID_ARG, "bad model parameter '" + t + "'");
+    return d;
+  };
+  int positional = 0;
   for (size_t i = 1; i < tok.size(); i++) {
     const std::string &t = tok[i];
     if (t.empty()) continue;
-    std::string v = t;
-    if (t.rfind("depth=", 0) == 0) v = t.substr(6);
-    else if (t.rfind("max_depth=", 0) == 0) v = t.substr(10);
-    else if (t.rfind("explore=", 0) == 0) {
+    if (t.rfind("explore=", 0) == 0) {
       if (t != "explore=RoundRobin") throw Error(ADAPT_E_INVALID_ARG, "only explore=RoundRobin");
       continue;
     }
-    char *end = nullptr;
-    long d = strtol(v.c_str(), &end, 10);
-    if (v.empty() || *end) throw Error(ADAPT_E_INVALID_ARG, "bad model parameter '" + t + "'");
-    if (d < 0 || d > 24) throw Error(ADAPT_E_INVALID_ARG, "depth must be in [0,24]");
-    *depth = (int)d;
+    long long d;
+    if (t.rfind("depth=", 0) == 0) d = num(t.substr(6), t), *depth = (int)d;
+    else if (t.rfind("max_depth=", 0) == 0) d = num(t.substr(10), t), *depth = (int)d;
+    else if (*kind == 1 && t.rfind("trees=", 0) == 0) d = num(t.substr(6), t), *trees = (int)d;
+    else if (*kind == 1 && t.rfind("seed=", 0) == 0) *seed = (uint64_t)num(t.substr(5), t);
+    else if (*kind == 1 && positional == 0) d = num(t, t), *trees = (int)d, positional++;
+    else d = num(t, t), *depth = (int)d, positional++;
+    if (*depth < 0 || *depth > 24) throw Error(ADAPT_E_INVALID_ARG, "depth must be in [0,24]");
+    if (*trees < 1 || *trees > forest_max_trees())
+      throw Error(ADAPT_E_INVALID_ARG, "trees must be in [1,64]");
   }
   return 0;
 }
@@ -448,6 +480,34 @@ void upload_tree(adapt_region *h, cudaStream_t s) {
   h->d_tree.ensure(d.size() * sizeof(DNode));
   CUDA_CHECK(cudaMemcpyAsync(h->d_tree.p, d.data(), d.size() * sizeof(DNode),
                              cudaMemcpyHostToDevice, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+// forest: trees concatenated, child indices made absolute; roots[t] = offset
+void upload_forest(adapt_region *h, cudaStream_t s) {
+  std::vector<DNode> d;
+  std::vector<int32_t> roots;
+  for (const auto &tr : h->forest) {
+    const int32_t off = (int32_t)d.size();
+    roots.push_back(off);
+    for (const auto &nd : tr) {
+      DNode x;
+      if (nd.feature >= 0) {
+        x.thr = round_down_f32(nd.threshold);
+        x.meta = ((nd.left + off) << 6) | nd.feature;
+      } else {
+        x.thr = 0;
+        x.meta = -1 - nd.label;
+      }
+      d.push_back(x);
+    }
+  }
+  if (d.size() >= (1u << 25)) throw Error(ADAPT_E_INVALID_ARG, "forest too large (2^25 nodes)");
+  h->forest_nodes = (int)d.size();
+  h->d_forest.ensure(d.size() * sizeof(DNode) + 16);
+  h->d_roots.ensure(roots.size() * 4 + 16);
+  CUDA_CHECK(cudaMemcpyAsync(h->d_forest.p, d.data(), d.size() * sizeof(DNode), cudaMemcpyHostToDevice, s));
+  CUDA_CHECK(cudaMemcpyAsync(h->d_roots.p, roots.data(), roots.size() * 4, cudaMemcpyHostToDevice, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
@@ -712,6 +772,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
   // 2. level loop (a4-a8).  Per level: partition the previous level's split
   // parents (a7), histogram the smaller child of each (a4) — or the root —,
   // sum over ranks (a5), derive the siblings, search splits (a6), decide.
+  auto grow_tree = [&](const uint8_t *w_root) {  // one tree; w_root: bootstrap weights or null
   h->tree.clear();
   h->stats.clear();
   adapt_node_t root{};
@@ -740,6 +801,11 @@ void train_region(adapt_region *h, cudaStream_t s) {
   // planes: the root is histogrammed from the ingest output; pass d >= 1 moves
   // the parents' rows from one plane pair into the other
   const uint8_t *bins_in = h->bins.as<uint8_t>(), *lab_in = h->labels.as<uint8_t>();
+  const uint8_t *w_in = w_root;  // weight plane (forests), moved along with the rows
+  if (w_root) {
+    h->wA.ensure((size_t)std::max<int64_t>(n, 1) + 64);
+    h->wB.ensure((size_t)std::max<int64_t>(n, 1) + 64);
+  }
   h->binsA.ensure(bins_bytes(n, BS));
   h->binsB.ensure(bins_bytes(n, BS));
   h->labA.ensure((size_t)std::max<int64_t>(n, 1) + 64);
@@ -780,7 +846,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
   for (int level = 0; !frontier.empty(); level++) {
     const int A = (int)frontier.size();
     if (trace) tr[0] = now_us();
-    const uint8_t *hist_bins = bins_in, *hist_lab = lab_in;
+    const uint8_t *hist_bins = bins_in, *hist_lab = lab_in, *hist_w = w_in;
     int64_t rows_part = 0;
     // ---- uploads that do not depend on this level's partition: class maps
     // of the direct nodes, their slots, the subtraction triples, node slots ----
@@ -881,6 +947,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
       pa.lab_in = lab_in;
       pa.bins_out = bo;
       pa.lab_out = lo;
+      pa.w_in = w_in;
+      pa.w_out = w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr;
       pa.pstride = pstride;
       pa.BS = BS;
       pa.F = F;
@@ -922,6 +990,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       for (const auto &x : flat) pcs[cnt[x[0]]++] = {x[1], x[2]};
       hist_bins = bo;
       hist_lab = lo;
+      hist_w = pa.w_out;
     }
     if (trace) tr[3] = now_us();
     // ---- a4: histograms of the direct nodes (the root, or the smaller children) ----
@@ -956,6 +1025,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       ha.total_rows = htotal;
       ha.bins_in = hist_bins;
       ha.lab_in = hist_lab;
+      ha.w_in = hist_w;
       ha.pstride = pstride;
       ha.BS = BS;
       ha.F = F;
@@ -1144,22 +1214,82 @@ void train_region(adapt_region *h, cudaStream_t s) {
     if (level > 0) {
       bins_in = (out_plane ? h->binsB : h->binsA).as<uint8_t>();
       lab_in = (out_plane ? h->labB : h->labA).as<uint8_t>();
+      if (w_root) w_in = (out_plane ? h->wB : h->wA).as<uint8_t>();
       out_plane ^= 1;
     }
   }
-  // depth of every node (children got theirs when appended)
+  };  // grow_tree
+
+  if (h->kind == 0) {
+    grow_tree(nullptr);
+    h->forest.clear();
+  } else {  // random forest: T trees on bootstrap resamples of the global table (R19)
+    uint64_t lo = 0;  // this rank's first global row
+    if (world > 1) {
+      DevBuf nb, allb;
+      nb.ensure(8);
+      allb.ensure((size_t)world * 8);
+      const uint64_t mine = (uint64_t)n;
+      CUDA_CHECK(cudaMemcpyAsync(nb.p, &mine, 8, cudaMemcpyHostToDevice, s));
+      comm_allgather(nb.p, allb.p, 8, s, "allgather row counts");
+      std::vector<uint64_t> all(world);
+      CUDA_CHECK(cudaMemcpyAsync(all.data(), allb.p, (size_t)world * 8, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      for (int r = 0; r < g_ctx.rank; r++) lo += all[r];
+    }
+    h->wcnt.ensure((size_t)std::max<int64_t>(n, 1) * 4);
+    h->wplane.ensure((size_t)std::max<int64_t>(n, 1) + 64);
+    std::vector<std::vector<adapt_node_t>> forest;
+    std::vector<int64_t> stats;
+    for (int t = 0; t < h->T; t++) {
+      CUDA_CHECK(cudaMemsetAsync(h->flags.p, 0, 16, s));
+      {
+        Phase ph("bootstrap", s, 0);
+        launch_bootstrap(h->seed, t, n_total, lo, n, h->wcnt.as<uint32_t>(), h->wplane.as<uint8_t>(),
+                         h->flags.as<uint32_t>(), s);
+      }
+      CUDA_CHECK(cudaMemcpyAsync(hs, h->flags.p, 4, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      if (hs[0] & kFlagBootstrap)
+        throw Error(ADAPT_E_INVALID_ARG, "bootstrap multiplicity above 255 (u8 weights)");
+      grow_tree(h->wplane.as<uint8_t>());
+      forest.push_back(h->tree);
+      stats.insert(stats.end(), h->stats.begin(), h->stats.end());
+    }
+    h->forest.swap(forest);
+    h->stats.swap(stats);
+    h->tree = h->forest[0];
+  }
   h->trained_n = n;
   h->trained = true;
   upload_tree(h, s);
+  if (h->kind == 1) upload_forest(h, s);
 }
 
-int select_host_walk(adapt_region *h, const float *x) {
+int walk_tree(const std::vector<adapt_node_t> &tr, const float *x) {
   int k = 0;
-  while (h->tree[k].feature >= 0) {
-    const double v = (double)x[h->tree[k].feature];
-    k = v <= h->tree[k].threshold ? h->tree[k].left : h->tree[k].right;  // NaN -> right (R8)
+  while (tr[k].feature >= 0) {
+    const double v = (double)x[tr[k].feature];
+    k = v <= tr[k].threshold ? tr[k].left : tr[k].right;  // NaN -> right (R8)
   }
-  return h->tree[k].label;
+  return tr[k].label;
+}
+
+// Table-1 get_policy on the host (one vector): the tree, or the forest's
+// majority vote with ties -> lowest variant (R20)
+int select_host_walk(adapt_region *h, const float *x) {
+  if (h->forest.empty()) return walk_tree(h->tree, x);
+  std::vector<int> votes(h->V, 0);
+  for (const auto &tr : h->forest) votes[walk_tree(tr, x)]++;
+  return (int)(std::max_element(votes.begin(), votes.end()) - votes.begin());  // first max
+}
+
+void select_device(adapt_region *h, const float *X, int64_t m, int32_t *out, cudaStream_t s) {
+  if (h->forest.empty())
+    launch_select(h->d_tree.as<DNode>(), (int)h->tree.size(), X, m, h->F, out, s);
+  else
+    launch_select_forest(h->d_forest.as<DNode>(), h->forest_nodes, h->d_roots.as<int32_t>(),
+                         (int)h->forest.size(), X, m, h->F, out, s);
 }
 
 int64_t distinct_pairs(adapt_region *h) {
@@ -1295,12 +1425,15 @@ int adapt_region_create(const char *id, int num_features, int num_variants,
     if (num_variants < 1 || num_variants > kMaxC)
       throw Error(ADAPT_E_INVALID_ARG, "num_variants must be in [1,255]");
     int depth = 2;
-    parse_params(model_params, &depth);
+    int kind = 0, trees = 1;
+    uint64_t seed = 0;
+    parse_params(model_params, &depth, &kind, &trees, &seed);
     const int mtd = min_train_data > 0 ? min_train_data : num_variants;
     auto it = g_regions.find(id);
     if (it != g_regions.end()) {
       adapt_region *h = it->second.get();
-      if (h->F != num_features || h->V != num_variants || h->D != depth || h->min_train != mtd)
+      if (h->F != num_features || h->V != num_variants || h->D != depth || h->min_train != mtd ||
+          h->kind != kind || h->T != trees || h->seed != seed)
         throw Error(ADAPT_E_SPEC_MISMATCH, std::string("region '") + id + "' exists with another spec");
       *out = h;
       return;
@@ -1310,6 +1443,9 @@ int adapt_region_create(const char *id, int num_features, int num_variants,
     h->F = num_features;
     h->V = num_variants;
     h->D = depth;
+    h->kind = kind;
+    h->T = trees;
+    h->seed = seed;
     h->min_train = mtd;
     *out = h.get();
     g_regions.emplace(id, std::move(h));
@@ -1472,7 +1608,7 @@ int adapt_select_batch(adapt_region_t *h, const float *d_X, int64_t m, int32_t *
     if (!h->trained) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
     cudaStream_t s = (cudaStream_t)stream;
     Phase ph("select", s, (double)m * (4.0 * h->F + 4));
-    launch_select(h->d_tree.as<DNode>(), (int)h->tree.size(), d_X, m, h->F, d_out, s);
+    select_device(h, d_X, m, d_out, s);
   });
 }
 
@@ -1506,7 +1642,7 @@ int adapt_select_batch_host(adapt_region_t *h, const float *X, int64_t m, int32_
       CUDA_CHECK(cudaMemcpyAsync(dx, X + c * F, (size_t)k * F * 4, cudaMemcpyHostToDevice, q));
       {
         Phase ph("select", q, (double)k * (4.0 * F + 4));
-        launch_select(h->d_tree.as<DNode>(), (int)h->tree.size(), dx, k, F, dout, q);
+        select_device(h, dx, k, dout, q);
       }
       CUDA_CHECK(cudaMemcpyAsync(out + c, dout, (size_t)k * 4, cudaMemcpyDeviceToHost, q));
     }
@@ -1529,6 +1665,30 @@ int adapt_get_tree(adapt_region_t *h, adapt_node_t *out, int32_t cap, int32_t *n
   });
 }
 
+int adapt_forest_size(adapt_region_t *h, int32_t *trees) {
+  return guarded([&] {
+    checked(h);
+    if (!trees) throw Error(ADAPT_E_INVALID_ARG, "null trees");
+    if (!h->trained) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    *trees = h->forest.empty() ? 1 : (int32_t)h->forest.size();
+  });
+}
+
+int adapt_get_forest_tree(adapt_region_t *h, int32_t t, adapt_node_t *out, int32_t cap,
+                          int32_t *n_nodes) {
+  return guarded([&] {
+    checked(h);
+    if (!n_nodes) throw Error(ADAPT_E_INVALID_ARG, "null n_nodes");
+    if (!h->trained) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    const int T = h->forest.empty() ? 1 : (int)h->forest.size();
+    if (t < 0 || t >= T) throw Error(ADAPT_E_INVALID_ARG, "tree index out of range");
+    const auto &tr = h->forest.empty() ? h->tree : h->forest[t];
+    *n_nodes = (int32_t)tr.size();
+    if (!out || cap < (int32_t)tr.size()) throw Error(ADAPT_E_INVALID_ARG, "capacity too small");
+    memcpy(out, tr.data(), tr.size() * sizeof(adapt_node_t));
+  });
+}
+
 int adapt_set_tree(adapt_region_t *h, const adapt_node_t *nodes, int32_t n_nodes) {
   return guarded([&] {
     checked(h);
@@ -1545,7 +1705,9 @@ int adapt_set_tree(adapt_region_t *h, const adapt_node_t *nodes, int32_t n_nodes
         throw Error(ADAPT_E_INVALID_ARG, "bad leaf label at node " + std::to_string(k));
       }
     }
+    if (h->kind != 0) throw Error(ADAPT_E_USAGE, "adapt_set_tree on a forest region");
     h->tree.assign(nodes, nodes + n_nodes);
+    h->forest.clear();
     h->trained = true;
     upload_tree(h, 0);
   });

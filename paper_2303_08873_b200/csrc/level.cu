@@ -93,8 +93,8 @@ __device__ __forceinline__ int row_byte(const Row<BS> &r, int f) {
   return (int)((pick<Row<BS>::N>(r.w, f >> 2) >> (8 * (f & 3))) & 0xFFu);
 }
 
-__device__ __forceinline__ void red_shared_inc(uint32_t addr) {
-  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+__device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
@@ -142,6 +142,9 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) 
       for (uint32_t qb = q0; qb < q1; qb += kPartUnroll * blockDim.x) {
         Row<BS> r[kPartUnroll];
         int label[kPartUnroll];
+        uint8_t wgt[kPartUnroll];
+#pragma unroll
+        for (int u = 0; u < kPartUnroll; u++) wgt[u] = 1;
 #pragma unroll
         for (int u = 0; u < kPartUnroll; u++) {  // all loads first
           const uint32_t q = qb + u * blockDim.x + tid;
@@ -149,6 +152,8 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) 
           if (q < q1) {
             load_row<BS>(a.bins_in, a.pstride, sg.off + q, r[u]);
             label[u] = __ldcs(a.lab_in + sg.off + q);
+            // bootstrap weight (forests): rows drawn 0 times leave the tree here
+            if (a.w_in) wgt[u] = __ldcs(a.w_in + sg.off + q);
           } else {
 #pragma unroll
             for (int i = 0; i < Row<BS>::N; i++) r[u].w[i] = 0;
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) 
         }
 #pragma unroll
         for (int u = 0; u < kPartUnroll; u++) {
-          const bool valid = label[u] >= 0;
+          const bool valid = label[u] >= 0 && wgt[u] > 0;
           const bool left = row_byte<BS>(r[u], sg.feat) <= sg.thr;  // bins are ranks
           const unsigned ml = __ballot_sync(kFull, valid && left && (sg.write & 1));
           const unsigned mr = __ballot_sync(kFull, valid && !left && (sg.write & 2));
@@ -170,6 +175,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) 
             const uint32_t pos = wl ? A + bl + __popc(ml & below) : B - 1 - (br + __popc(mr & below));
             store_row<BS>(a.bins_out, a.pstride, pos, r[u]);
             __stcs(a.lab_out + pos, (uint8_t)label[u]);
+            if (a.w_out) __stcs(a.w_out + pos, wgt[u]);
           }
         }
       }
@@ -252,10 +258,11 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
           else
             w = a.bins_in[row];
           const int lk = (int)__ldg(m + a.lab_in[row]) - k0;
+          const uint32_t wv = a.w_in ? a.w_in[row] : 1u;
           if ((unsigned)lk >= (unsigned)kn) continue;
 #pragma unroll
           for (int e = 0; e < 4; e++)
-            if (fb[e] >= 0) atomicAdd(dst + fb[e] + (int64_t)((w >> (8 * e)) & 0xFF) * kcn + lk, 1u);
+            if (fb[e] >= 0) atomicAdd(dst + fb[e] + (int64_t)((w >> (8 * e)) & 0xFF) * kcn + lk, wv);
         }
       }
       p0 = pe;
@@ -292,6 +299,9 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
         }
         uint32_t w[kHistUnroll];
         int label[kHistUnroll];
+        uint32_t wv[kHistUnroll];  // row weight: 1, or the bootstrap multiplicity (forests)
+#pragma unroll
+        for (int u = 0; u < kHistUnroll; u++) wv[u] = 1;
 #pragma unroll
         for (int u = 0; u < kHistUnroll; u++) {  // all loads first: only this CTA's word
           const uint32_t q = qb + u * blockDim.x + tid;
@@ -306,6 +316,7 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
             else
               w[u] = a.bins_in[row];
             label[u] = a.lab_in[sg.off + q];
+            if (a.w_in) wv[u] = a.w_in[sg.off + q];
           }
         }
 #pragma unroll
@@ -315,15 +326,15 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
           if ((unsigned)lk >= (unsigned)kn) continue;  // another CTA's class slab
           const uint32_t lk4 = 4u * lk;
           if (all4) {
-            red_shared_inc(abase[0] + ((w[u]) & 0xFF) * kwp4 + lk4);
-            red_shared_inc(abase[1] + ((w[u] >> 8) & 0xFF) * kwp4 + lk4);
-            red_shared_inc(abase[2] + ((w[u] >> 16) & 0xFF) * kwp4 + lk4);
-            red_shared_inc(abase[3] + (w[u] >> 24) * kwp4 + lk4);
+            red_shared_add(abase[0] + ((w[u]) & 0xFF) * kwp4 + lk4, wv[u]);
+            red_shared_add(abase[1] + ((w[u] >> 8) & 0xFF) * kwp4 + lk4, wv[u]);
+            red_shared_add(abase[2] + ((w[u] >> 16) & 0xFF) * kwp4 + lk4, wv[u]);
+            red_shared_add(abase[3] + (w[u] >> 24) * kwp4 + lk4, wv[u]);
           } else {
 #pragma unroll
             for (int e = 0; e < 4; e++)
               if (abase[e] != 0xFFFFFFFFu)
-                red_shared_inc(abase[e] + ((w[u] >> (8 * e)) & 0xFF) * kwp4 + lk4);
+                red_shared_add(abase[e] + ((w[u] >> (8 * e)) & 0xFF) * kwp4 + lk4, wv[u]);
           }
         }
       }
@@ -375,6 +386,7 @@ __global__ void __launch_bounds__(256) hist_flat_kernel(HistArgs a) {
     load_row<BS>(a.bins_in, a.pstride, row, r);
     const int kcn = sg.ncls;
     const int lk = (int)__ldg(a.cmaps + (size_t)sg.cmap * a.C + a.lab_in[row]);
+    const uint32_t wv = a.w_in ? a.w_in[row] : 1u;
     uint32_t *dst = a.H + a.soff[sg.hslot] + lk;
 #pragma unroll
     for (int i = 0; i < Row<BS>::N; i++)
@@ -382,7 +394,7 @@ __global__ void __launch_bounds__(256) hist_flat_kernel(HistArgs a) {
       for (int e = 0; e < (BS >= 4 ? 4 : BS); e++) {
         const int f = 4 * i + e;
         if (f < a.F)
-          atomicAdd(dst + (int64_t)(__ldg(a.cumD + f) + (int)((r.w[i] >> (8 * e)) & 0xFF)) * kcn, 1u);
+          atomicAdd(dst + (int64_t)(__ldg(a.cumD + f) + (int)((r.w[i] >> (8 * e)) & 0xFF)) * kcn, wv);
       }
   }
 }

@@ -40,9 +40,16 @@ def test_host_side_validation():
     with pytest.raises(ad.AdaptError) as e:
         ad.adapt_region_create("b0", 2, 256)
     assert e.value.code == ad.ADAPT_E_INVALID_ARG
+    for bad in ("rfc,0,4", "rfc,65,4", "rfc,trees=3,depth=30", "gbt,3", "dtree,trees=3"):
+        with pytest.raises(ad.AdaptError) as e:
+            ad.adapt_region_create("b0", 2, 2, bad)
+        assert e.value.code == ad.ADAPT_E_INVALID_ARG, bad
+    hf = ad.adapt_region_create("bf", 2, 2, "rfc(10,4)")  # P:257 model_type(rfc, 10, 4)
+    assert ad.adapt_region_info(hf)["max_depth"] == 4
+    assert ad.adapt_region_create("bf", 2, 2, "rfc,trees=10,depth=4") == hf
     with pytest.raises(ad.AdaptError) as e:
-        ad.adapt_region_create("b0", 2, 2, "rfc,10,4")
-    assert e.value.code == ad.ADAPT_E_INVALID_ARG
+        ad.adapt_region_create("bf", 2, 2, "rfc,10,4,seed=1")  # another forest
+    assert e.value.code == ad.ADAPT_E_SPEC_MISMATCH
     with pytest.raises(ad.AdaptError) as e:
         ad.adapt_region_create("b0", 2, 2, "dtree,depth=25")
     assert e.value.code == ad.ADAPT_E_INVALID_ARG

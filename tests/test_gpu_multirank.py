@@ -48,7 +48,7 @@ def _worker(rank, world, port, job, q):
         lo, hi = adist.shard_bounds(len(X), rank, world)
         Xs, Ts = np.ascontiguousarray(X[lo:hi]), np.ascontiguousarray(T[lo:hi])
         n, F = Xs.shape
-        h = ad.adapt_region_create("mr", F, T.shape[1], f"dtree,depth={D}", 0)
+        h = ad.adapt_region_create("mr", F, T.shape[1], job.get("model", f"dtree,depth={D}"), 0)
         s = torch.cuda.current_stream()
         dX = torch.from_numpy(Xs).cuda()
         if job.get("host"):
@@ -63,6 +63,7 @@ def _worker(rank, world, port, job, q):
             q.put((rank, out))
             return
         out["tree"] = ad.adapt_get_tree(h)
+        out["forest"] = [ad.adapt_get_forest_tree(h, t) for t in range(ad.adapt_forest_size(h))]
         out["labels"] = ad.adapt_get_labels(h, n)
         out["bins"] = ad.adapt_get_bins(h, n, F)
         sel = torch.empty(n, dtype=torch.int32, device="cuda")
@@ -115,6 +116,22 @@ def test_p_invariant_tree_c3(world):
 def test_p_invariant_tree_c4_slice_host_records():
     X, T = synth.generate("C4", 0, 60_001)
     _check(_run(2, {"X": X, "T": T, "D": 12, "host": True}), X, T, 12)
+
+
+def test_p_invariant_forest():
+    # bootstrap draws run over the GLOBAL row index (R19): every rank counts
+    # the draws landing in its shard, so the forest is the single-GPU one
+    X, T = synth.generate("C3", 0, 30_001)
+    res = _run(2, {"X": X, "T": T, "D": 6, "model": "rfc,3,6,seed=4"})
+    y = oracle.labels(T)
+    ref = oracle.train_forest(X, y, T.shape[1], 6, 3, 4)
+    expect = oracle.select_forest(ref, X)
+    for r, o in sorted(res.items()):
+        assert "error" not in o
+        assert len(o["forest"]) == 3
+        for t in range(3):
+            assert o["forest"][t].tobytes() == ref[t].tobytes(), f"rank {r} tree {t}"
+        assert np.array_equal(o["select"], expect[o["lo"]:o["hi"]])
 
 
 def test_empty_shard_rank():
