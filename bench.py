@@ -36,7 +36,7 @@ WORKLOADS = {
     "C2": "C2 region 0: 3.3e4-row table, 4 features, 7 variants (num_threads), depth 8",
     "C1": "C1: 512 profiled samples, 1 feature (trip count), host vs GPU offload, depth 4",
 }
-KERNEL_PHASES = ("discover", "ingest", "values", "merge", "zero", "partition", "hist", "subtract", "split", "winner",
+KERNEL_PHASES = ("discover", "ingest", "values", "merge", "zero", "partition", "hist", "subtract", "split", "winner", "bootstrap",
                  "select")
 
 
@@ -167,6 +167,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=0)
     ap.add_argument("--depth", type=int, default=0, help="override the config's depth (testing only)")
+    ap.add_argument("--model", default="", help="model_type override, e.g. 'rfc,10,4' (P:257)")
     ap.add_argument("--records", type=int, default=20_000_000, help="record-path batch size")
     ap.add_argument("--no-records", action="store_true")
     args = ap.parse_args()
@@ -205,7 +206,8 @@ def main():
     synth.generate_device(cfg, lo, n, X.data_ptr(), T.data_ptr(), g.data_ptr(), o.data_ptr(),
                           stream.cuda_stream)
     torch.cuda.synchronize()
-    h = ad.adapt_region_create(f"bench_{args.config}", cfg.F, cfg.V, f"dtree,depth={cfg.D}", 0)
+    model = args.model or f"dtree,depth={cfg.D}"
+    h = ad.adapt_region_create(f"bench_{args.config}", cfg.F, cfg.V, model, 0)
 
     def step():
         ad.adapt_record_table(h, X, T, n, True, stream)
@@ -244,7 +246,7 @@ def main():
         hout = torch.empty(n, dtype=torch.int32, pin_memory=True)
         hX.copy_(X)
         hT.copy_(T)
-        he = ad.adapt_region_create(f"bench_e2e_{args.config}", cfg.F, cfg.V, f"dtree,depth={cfg.D}", 0)
+        he = ad.adapt_region_create(f"bench_e2e_{args.config}", cfg.F, cfg.V, model, 0)
 
         def step_host():
             ad.adapt_record_table(he, hX, hT, n, False, stream)
@@ -335,7 +337,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "rows": N, "features": cfg.F,
-                   "variants": cfg.V, "depth": cfg.D, "select_vectors": N,
+                   "variants": cfg.V, "depth": cfg.D, "model": model, "select_vectors": N,
                    "parallelism": f"dp{world}",
                    "l2": "inputs (%.1f GB) exceed the 126 MB L2; no flush needed" %
                          (N * 4 * (cfg.F + cfg.V) / 1e9)},

@@ -22,7 +22,6 @@ constexpr uint32_t kFlagNanTime = 2;      // NaN time (R3)
 constexpr uint32_t kFlagAllInf = 4;       // every variant unmeasured (R3)
 constexpr uint32_t kFlagTooMany = 8;      // > 256 distinct values of a feature (R14)
 constexpr uint32_t kFlagBadVariant = 16;  // recorded variant outside [0, V)
-constexpr uint32_t kFlagBootstrap = 32;   // a bootstrap multiplicity above 255 (u8 weights)
 
 struct Error : std::runtime_error {
   int code;
@@ -189,8 +188,10 @@ struct DNode {     // device inference node, 8 bytes
 
 // ---- kernel launchers (forest.cu): random forests ----
 // u8 bootstrap weights of this rank's rows [lo, lo + n_local) for tree `tree` (R19)
+// sums[0] = draws landing in the shard, sums[1] = sum of the weights (equal unless
+// a multiplicity overflowed u8); w needs n_local + 4 bytes
 void launch_bootstrap(uint64_t seed, int tree, uint64_t n_total, uint64_t lo, int64_t n_local,
-                      uint32_t *cnt, uint8_t *w, uint32_t *flags, cudaStream_t s);
+                      uint8_t *w, unsigned long long *sums, cudaStream_t s);
 int forest_max_trees();
 // majority vote of the T trees rooted at roots[t] in the concatenated node array
 void launch_select_forest(const DNode *nodes, int n_nodes, const int32_t *roots, int T,

@@ -1237,20 +1237,20 @@ void train_region(adapt_region *h, cudaStream_t s) {
       CUDA_CHECK(cudaStreamSynchronize(s));
       for (int r = 0; r < g_ctx.rank; r++) lo += all[r];
     }
-    h->wcnt.ensure((size_t)std::max<int64_t>(n, 1) * 4);
+    h->wcnt.ensure(16);
     h->wplane.ensure((size_t)std::max<int64_t>(n, 1) + 64);
     std::vector<std::vector<adapt_node_t>> forest;
     std::vector<int64_t> stats;
     for (int t = 0; t < h->T; t++) {
-      CUDA_CHECK(cudaMemsetAsync(h->flags.p, 0, 16, s));
       {
         Phase ph("bootstrap", s, 0);
-        launch_bootstrap(h->seed, t, n_total, lo, n, h->wcnt.as<uint32_t>(), h->wplane.as<uint8_t>(),
-                         h->flags.as<uint32_t>(), s);
+        launch_bootstrap(h->seed, t, n_total, lo, n, h->wplane.as<uint8_t>(),
+                         h->wcnt.as<unsigned long long>(), s);
       }
-      CUDA_CHECK(cudaMemcpyAsync(hs, h->flags.p, 4, cudaMemcpyDeviceToHost, s));
+      uint64_t sums[2];
+      CUDA_CHECK(cudaMemcpyAsync(sums, h->wcnt.p, 16, cudaMemcpyDeviceToHost, s));
       CUDA_CHECK(cudaStreamSynchronize(s));
-      if (hs[0] & kFlagBootstrap)
+      if (sums[0] != sums[1])
         throw Error(ADAPT_E_INVALID_ARG, "bootstrap multiplicity above 255 (u8 weights)");
       grow_tree(h->wplane.as<uint8_t>());
       forest.push_back(h->tree);
