@@ -200,8 +200,11 @@ constexpr int kHistThreads = 1024;
 constexpr int kHistUnroll = 16;  // rows in flight per thread (the pass is latency-bound otherwise)
 constexpr int kSyncEvery = 2;  // iterations of kHistUnroll x 1024 rows between partner syncs
 
-template <int BS>
+// WEIGHTED (forests): rows add their bootstrap weight; a separate instance so
+// the plain path keeps its registers (the weights cost 16 more per thread)
+template <int BS, bool WEIGHTED>
 __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
+  constexpr int UNROLL = WEIGHTED ? kHistUnroll / 2 : kHistUnroll;
   extern __shared__ uint32_t sh[];  // [smem_counters] counters
   __shared__ uint8_t s_cmap[kMaxC + 1];  // this node: class -> compact index (255: absent)
   const int tid = threadIdx.x;
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
       const Seg sg = a.segs[s];
       const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
       const uint32_t q1 = min(sg.len, pe - sg.row_base);
-      for (uint32_t qb = q0; qb < q1; qb += kHistUnroll * blockDim.x) {
+      for (uint32_t qb = q0; qb < q1; qb += UNROLL * blockDim.x) {
         if (a.sync && ++iter % kSyncEvery == 0) {  // keep the G CTAs within L2 reach
           __syncthreads();
           if (tid == 0) {
@@ -297,13 +300,13 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
           }
           __syncthreads();
         }
-        uint32_t w[kHistUnroll];
-        int label[kHistUnroll];
-        uint32_t wv[kHistUnroll];  // row weight: 1, or the bootstrap multiplicity (forests)
+        uint32_t w[UNROLL];
+        int label[UNROLL];
+        uint32_t wv[WEIGHTED ? UNROLL : 1];  // row weight: the bootstrap multiplicity
 #pragma unroll
-        for (int u = 0; u < kHistUnroll; u++) wv[u] = 1;
+        for (int u = 0; u < (WEIGHTED ? UNROLL : 1); u++) wv[u] = 1;
 #pragma unroll
-        for (int u = 0; u < kHistUnroll; u++) {  // all loads first: only this CTA's word
+        for (int u = 0; u < UNROLL; u++) {  // all loads first: only this CTA's word
           const uint32_t q = qb + u * blockDim.x + tid;
           label[u] = -1;
           w[u] = 0;
@@ -316,25 +319,25 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
             else
               w[u] = a.bins_in[row];
             label[u] = a.lab_in[sg.off + q];
-            if (a.w_in) wv[u] = a.w_in[sg.off + q];
+            if constexpr (WEIGHTED) wv[u] = a.w_in[sg.off + q];
           }
         }
 #pragma unroll
-        for (int u = 0; u < kHistUnroll; u++) {
+        for (int u = 0; u < UNROLL; u++) {
           if (label[u] < 0) continue;
           const int lk = (int)s_cmap[label[u]] - k0;
           if ((unsigned)lk >= (unsigned)kn) continue;  // another CTA's class slab
           const uint32_t lk4 = 4u * lk;
           if (all4) {
-            red_shared_add(abase[0] + ((w[u]) & 0xFF) * kwp4 + lk4, wv[u]);
-            red_shared_add(abase[1] + ((w[u] >> 8) & 0xFF) * kwp4 + lk4, wv[u]);
-            red_shared_add(abase[2] + ((w[u] >> 16) & 0xFF) * kwp4 + lk4, wv[u]);
-            red_shared_add(abase[3] + (w[u] >> 24) * kwp4 + lk4, wv[u]);
+            red_shared_add(abase[0] + ((w[u]) & 0xFF) * kwp4 + lk4, wv[WEIGHTED ? u : 0]);
+            red_shared_add(abase[1] + ((w[u] >> 8) & 0xFF) * kwp4 + lk4, wv[WEIGHTED ? u : 0]);
+            red_shared_add(abase[2] + ((w[u] >> 16) & 0xFF) * kwp4 + lk4, wv[WEIGHTED ? u : 0]);
+            red_shared_add(abase[3] + (w[u] >> 24) * kwp4 + lk4, wv[WEIGHTED ? u : 0]);
           } else {
 #pragma unroll
             for (int e = 0; e < 4; e++)
               if (abase[e] != 0xFFFFFFFFu)
-                red_shared_add(abase[e] + ((w[u] >> (8 * e)) & 0xFF) * kwp4 + lk4, wv[u]);
+                red_shared_add(abase[e] + ((w[u] >> (8 * e)) & 0xFF) * kwp4 + lk4, wv[WEIGHTED ? u : 0]);
           }
         }
       }
@@ -455,9 +458,15 @@ void launch_hist(const HistArgs &a, cudaStream_t s) {
   switch (a.BS) {
 #define CASE(B)                                                                              \
   case B:                                                                                    \
-    CUDA_CHECK(cudaFuncSetAttribute(hist_kernel<B>,                                          \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    CUDA_CHECK(cudaLaunchKernelEx(&cfg, hist_kernel<B>, a));                                 \
+    if (a.w_in) {                                                                            \
+      CUDA_CHECK(cudaFuncSetAttribute(hist_kernel<B, true>,                                  \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      CUDA_CHECK(cudaLaunchKernelEx(&cfg, hist_kernel<B, true>, a));                         \
+    } else {                                                                                 \
+      CUDA_CHECK(cudaFuncSetAttribute(hist_kernel<B, false>,                                 \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      CUDA_CHECK(cudaLaunchKernelEx(&cfg, hist_kernel<B, false>, a));                        \
+    }                                                                                        \
     break;
     CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
 #undef CASE

@@ -130,3 +130,30 @@ def test_product_path_never_touches_the_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "oracle.h" not in txt and "liboracle" not in txt, f
+
+
+def test_hot_kernels_do_not_spill():
+    """Register spills in the row passes cost 2x once (the weighted histogram
+    variant): guard every hot kernel's stack frame at zero (cuobjdump -res-usage)."""
+    import shutil
+    import subprocess
+
+    import paper_2303_08873_b200 as ad
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "-res-usage", ad.LIB_PATH], capture_output=True, text=True).stdout
+    fn = None
+    seen = 0
+    for line in out.splitlines():
+        if "Function" in line:
+            fn = line.split("Function")[-1].strip().rstrip(":")
+        elif "STACK:" in line and fn and any(k in fn for k in (
+                "hist_kernelILi16", "hist_kernelILi8", "partition_kernelILi16", "partition_kernelILi8",
+                "select_kernelILi16", "label_bin", "split_small", "split_kernel", "hist_flat")):
+            # (discover_kernel's frame is its noinline slow-path call, by design)
+            seen += 1
+            stack = int(re.search(r"STACK:(\d+)", line).group(1))
+            assert stack == 0, f"{fn} spills ({stack} bytes of stack)"
+    assert seen >= 8
