@@ -22,6 +22,7 @@ constexpr uint32_t kFlagNanTime = 2;      // NaN time (R3)
 constexpr uint32_t kFlagAllInf = 4;       // every variant unmeasured (R3)
 constexpr uint32_t kFlagTooMany = 8;      // > 256 distinct values of a feature (R14)
 constexpr uint32_t kFlagBadVariant = 16;  // recorded variant outside [0, V)
+constexpr uint32_t kFlagUnseen = 32;      // bin pass met a value the (sampled) discovery missed
 
 struct Error : std::runtime_error {
   int code;
@@ -91,16 +92,19 @@ void launch_rec_wide(const float *feat, const int32_t *var, const uint64_t *ns, 
 
 // ---- kernel launchers (ingest.cu) ----
 int lookup_table_bytes(int F);  // size of the per-feature key -> rank perfect hashes
+// n rows; chunk_rows > 0: a sampled view, row i -> i + (i / chunk_rows) * gap_rows
 void launch_discover(const float *feat, int64_t n, int F, uint32_t *gkey, uint32_t *gcount,
-                     uint32_t *flags, cudaStream_t s);
+                     uint32_t *flags, int64_t chunk_rows, int64_t gap_rows, cudaStream_t s);
 void launch_collect_values(const uint32_t *gkey, const uint32_t *gcount, int F, float *local_vals,
                            int32_t *local_cnt, cudaStream_t s);
 void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int world, int F,
                          float *val, int32_t *nval, uint32_t *flags, cudaStream_t s);
-bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab);
+bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab, uint32_t *slot_keys);
+int lookup_slots();  // hash slots per feature (slot_keys entries)
 void launch_label_bin(const float *feat, const float *times, int64_t n, int F, int V, int BS,
-                      const uint8_t *tab, const uint32_t *lk_mul, uint32_t *flags, uint8_t *bins,
-                      size_t pstride, uint8_t *labels, cudaStream_t s);
+                      const uint8_t *tab, const uint32_t *lk_mul, const uint32_t *slot_keys,
+                      uint32_t *flags, uint8_t *bins, size_t pstride, uint8_t *labels,
+                      cudaStream_t s);
 void launch_bins_out(const uint8_t *bins, size_t pstride, int64_t n, int F, int BS, uint8_t *out,
                      cudaStream_t s);
 // bytes between the bins word planes of an n-row buffer (plane p = bytes [4p, 4p+4) of each row)

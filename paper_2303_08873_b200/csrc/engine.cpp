@@ -370,7 +370,7 @@ struct adapt_region {
   bool trained = false;
   std::vector<int64_t> stats;
   // scratch
-  adapt::DevBuf gkey, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, lk_keys, lk_mul,
+  adapt::DevBuf gkey, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, lk_keys, lk_mul, lk_skeys,
       H0, H1, segs,
       hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, cmaps, psync, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall;
@@ -650,76 +650,99 @@ void train_region(adapt_region *h, cudaStream_t s) {
   h->pstride = pstride;
   h->bins.ensure(bins_bytes(n, BS));
   h->labels.ensure((size_t)std::max<int64_t>(n, 1) + 64);
-  CUDA_CHECK(cudaMemsetAsync(h->gkey.p, 0xFF, (size_t)F * kGSlots * 4, s));
-  CUDA_CHECK(cudaMemsetAsync(h->gcount.p, 0, (size_t)F * 4, s));
-  CUDA_CHECK(cudaMemsetAsync(h->flags.p, 0, 16, s));
-  {
-    Phase ph("discover", s, (double)n * 4.0 * F);
-    launch_discover(feat, n, F, h->gkey.as<uint32_t>(), h->gcount.as<uint32_t>(),
-                    h->flags.as<uint32_t>(), s);
-  }
   h->lvals.ensure((size_t)F * kMaxBins * 4);
   h->lcnt.ensure((size_t)F * 4);
   h->avals.ensure((size_t)world * F * kMaxBins * 4);
   h->acnt.ensure((size_t)world * F * 4);
   h->dval.ensure((size_t)F * kMaxBins * 4);
   h->dnval.ensure((size_t)F * 4);
-  CUDA_CHECK(cudaMemsetAsync(h->lvals.p, 0, (size_t)F * kMaxBins * 4, s));
-  CUDA_CHECK(cudaMemsetAsync(h->dval.p, 0, (size_t)F * kMaxBins * 4, s));
-  {
-    Phase ph("values", s, 0);
-    launch_collect_values(h->gkey.as<uint32_t>(), h->gcount.as<uint32_t>(), F,
-                          h->lvals.as<float>(), h->lcnt.as<int32_t>(), s);
-  }
-  comm_allgather(h->lvals.p, h->avals.p, (size_t)F * kMaxBins * 4, s, "allgather values");
-  comm_allgather(h->lcnt.p, h->acnt.p, (size_t)F * 4, s, "allgather counts");
-  {
-    Phase ph("merge", s, 0);
-    launch_merge_values(h->avals.as<float>(), h->acnt.as<int32_t>(), world, F, h->dval.as<float>(),
-                        h->dnval.as<int32_t>(), h->flags.as<uint32_t>(), s);
-  }
-  // error flags, summed over ranks so that all ranks fail together
+  // error flags, summed over ranks so that all ranks fail (or retry) together
   uint32_t *hs = h->hsmall.as<uint32_t>();
-  auto check_flags = [&]() {
+  auto check_flags = [&]() -> uint32_t {
     DevBuf fl;
-    fl.ensure(16);
+    fl.ensure(32);
     CUDA_CHECK(cudaMemcpyAsync(hs, h->flags.p, 4, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
-    uint32_t bits[4] = {(hs[0] >> 0) & 1, (hs[0] >> 1) & 1, (hs[0] >> 2) & 1, (hs[0] >> 3) & 1};
+    uint32_t bits[6];
+    for (int b = 0; b < 6; b++) bits[b] = (hs[0] >> b) & 1;
     if (world > 1) {
-      CUDA_CHECK(cudaMemcpyAsync(fl.p, bits, 16, cudaMemcpyHostToDevice, s));
-      comm_allreduce_sum(fl.p, 4, false, s, "allreduce flags");
-      CUDA_CHECK(cudaMemcpyAsync(bits, fl.p, 16, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaMemcpyAsync(fl.p, bits, 24, cudaMemcpyHostToDevice, s));
+      comm_allreduce_sum(fl.p, 6, false, s, "allreduce flags");
+      CUDA_CHECK(cudaMemcpyAsync(bits, fl.p, 24, cudaMemcpyDeviceToHost, s));
       CUDA_CHECK(cudaStreamSynchronize(s));
     }
     if (bits[0]) throw Error(ADAPT_E_BAD_VALUE, "NaN or Inf feature value");
     if (bits[1]) throw Error(ADAPT_E_BAD_VALUE, "NaN time");
     if (bits[2]) throw Error(ADAPT_E_BAD_VALUE, "row with every variant unmeasured (+inf)");
     if (bits[3]) throw Error(ADAPT_E_TOO_MANY_DISTINCT, "a feature has more than 256 distinct values");
+    uint32_t m = 0;
+    for (int b = 0; b < 6; b++) m |= (bits[b] ? 1u : 0u) << b;
+    return m;
   };
-  check_flags();
-  // value tables to the host; per-feature perfect hashes value -> rank for the bin pass
-  h->val.assign((size_t)F * kMaxBins, 0.f);
-  h->nval.assign(F, 0);
-  CUDA_CHECK(cudaMemcpyAsync(h->val.data(), h->dval.p, (size_t)F * kMaxBins * 4, cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaMemcpyAsync(h->nval.data(), h->dnval.p, (size_t)F * 4, cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  {
-    std::vector<uint8_t> tab((size_t)lookup_table_bytes(F));
-    std::vector<uint32_t> mul((size_t)2 * F);
-    for (int f = 0; f < F; f++)
-      if (!build_value_hash(&h->val[(size_t)f * kMaxBins], h->nval[f], &mul[2 * f],
-                            &tab[(size_t)f * lookup_table_bytes(1)]))
-        throw Error(ADAPT_E_CUDA, "cannot build the value hash of feature " + std::to_string(f));
-    h2d(h->lk_keys, tab, s);
-    h2d(h->lk_mul, mul, s);
+  // Discovery reads a SAMPLE of a large table first (kSampleChunks contiguous
+  // chunks spread over it): the bin pass checks every value against the
+  // resulting tables and flags any value the sample missed, and only then the
+  // whole table is discovered and binned again — the tables and bins are the
+  // exact ones either way, typically for a 1% read.
+  constexpr int64_t kSampleChunk = 1 << 15, kSampleChunks = 32;
+  const bool sampled = n > 4 * kSampleChunk * kSampleChunks;
+  for (int attempt = 0;; attempt++) {
+    CUDA_CHECK(cudaMemsetAsync(h->gkey.p, 0xFF, (size_t)F * kGSlots * 4, s));
+    CUDA_CHECK(cudaMemsetAsync(h->gcount.p, 0, (size_t)F * 4, s));
+    CUDA_CHECK(cudaMemsetAsync(h->flags.p, 0, 16, s));
+    if (sampled && attempt == 0) {
+      Phase ph("discover", s, (double)kSampleChunk * kSampleChunks * 4.0 * F);
+      const int64_t gap = (n - kSampleChunk * kSampleChunks) / (kSampleChunks - 1);
+      launch_discover(feat, kSampleChunk * kSampleChunks, F, h->gkey.as<uint32_t>(),
+                      h->gcount.as<uint32_t>(), h->flags.as<uint32_t>(), kSampleChunk, gap, s);
+    } else {
+      Phase ph("discover", s, (double)n * 4.0 * F);
+      launch_discover(feat, n, F, h->gkey.as<uint32_t>(), h->gcount.as<uint32_t>(),
+                      h->flags.as<uint32_t>(), 0, 0, s);
+    }
+    CUDA_CHECK(cudaMemsetAsync(h->lvals.p, 0, (size_t)F * kMaxBins * 4, s));
+    CUDA_CHECK(cudaMemsetAsync(h->dval.p, 0, (size_t)F * kMaxBins * 4, s));
+    {
+      Phase ph("values", s, 0);
+      launch_collect_values(h->gkey.as<uint32_t>(), h->gcount.as<uint32_t>(), F,
+                            h->lvals.as<float>(), h->lcnt.as<int32_t>(), s);
+    }
+    comm_allgather(h->lvals.p, h->avals.p, (size_t)F * kMaxBins * 4, s, "allgather values");
+    comm_allgather(h->lcnt.p, h->acnt.p, (size_t)F * 4, s, "allgather counts");
+    {
+      Phase ph("merge", s, 0);
+      launch_merge_values(h->avals.as<float>(), h->acnt.as<int32_t>(), world, F, h->dval.as<float>(),
+                          h->dnval.as<int32_t>(), h->flags.as<uint32_t>(), s);
+    }
+    check_flags();
+    // value tables to the host; per-feature perfect hashes value -> rank for the bin pass
+    h->val.assign((size_t)F * kMaxBins, 0.f);
+    h->nval.assign(F, 0);
+    CUDA_CHECK(cudaMemcpyAsync(h->val.data(), h->dval.p, (size_t)F * kMaxBins * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(h->nval.data(), h->dnval.p, (size_t)F * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    {
+      std::vector<uint8_t> tab((size_t)lookup_table_bytes(F));
+      std::vector<uint32_t> mul((size_t)2 * F), skeys((size_t)F * lookup_slots());
+      for (int f = 0; f < F; f++)
+        if (!build_value_hash(&h->val[(size_t)f * kMaxBins], h->nval[f], &mul[2 * f],
+                              &tab[(size_t)f * lookup_table_bytes(1)], &skeys[(size_t)f * lookup_slots()]))
+          throw Error(ADAPT_E_CUDA, "cannot build the value hash of feature " + std::to_string(f));
+      h2d(h->lk_keys, tab, s);
+      h2d(h->lk_mul, mul, s);
+      h2d(h->lk_skeys, skeys, s);
+    }
+    CUDA_CHECK(cudaMemsetAsync(h->flags.p, 0, 16, s));
+    {
+      Phase ph("ingest", s, (double)n * (4.0 * F + 4.0 * V + F + 1));  // algorithmic
+      launch_label_bin(feat, times, n, F, V, BS, h->lk_keys.as<uint8_t>(), h->lk_mul.as<uint32_t>(),
+                       h->lk_skeys.as<uint32_t>(), h->flags.as<uint32_t>(),
+                       h->bins.as<uint8_t>(), pstride, h->labels.as<uint8_t>(), s);
+    }
+    const uint32_t fl = check_flags();
+    if (!(fl & kFlagUnseen)) break;
+    if (attempt > 0) throw Error(ADAPT_E_CUDA, "bin pass met a value the full discovery missed");
   }
-  {
-    Phase ph("ingest", s, (double)n * (4.0 * F + 4.0 * V + F + 1));  // algorithmic
-    launch_label_bin(feat, times, n, F, V, BS, h->lk_keys.as<uint8_t>(), h->lk_mul.as<uint32_t>(),
-                     h->flags.as<uint32_t>(), h->bins.as<uint8_t>(), pstride, h->labels.as<uint8_t>(), s);
-  }
-  check_flags();
 
   // histogram layout: node -> [DS][kc] (rows cumD[f] + rank, compact class columns)
   std::vector<int32_t> cumD(F);

@@ -101,10 +101,13 @@ __device__ __noinline__ void see_slow(uint32_t *S, int log2nb, uint32_t key, uin
 
 constexpr int kDiscUnroll = 4;  // float4 loads in flight per thread
 
+// n rows of a possibly sampled view: sample row i is table row
+// i + (i / chunk_rows) * gap_rows (chunks of chunk_rows rows, gap_rows apart)
 __global__ void __launch_bounds__(kDiscThreads) discover_kernel(const float *__restrict__ feat,
                                                                int64_t n, int F, int log2nb,
                                                                uint32_t *gkey, uint32_t *gcount,
-                                                               uint32_t *flags) {
+                                                               uint32_t *flags, int64_t chunk_rows,
+                                                               int64_t gap_rows) {
   extern __shared__ uint4 sset4[];  // [F][NB] buckets of 4 keys seen by this CTA
   uint32_t *sset = reinterpret_cast<uint32_t *>(sset4);
   const int NB = 1 << log2nb;
@@ -134,7 +137,8 @@ __global__ void __launch_bounds__(kDiscThreads) discover_kernel(const float *__r
 #pragma unroll
       for (int u = 0; u < kDiscUnroll; u++) {
         const int64_t j = base + u * stride + tid0;
-        x[u] = j < n4 ? __ldcs(f4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[u] = j < n4 ? __ldcs(f4 + j + ((4 * j) / F / chunk_rows) * gap_rows * (F / 4))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < kDiscUnroll; u++) {
@@ -154,7 +158,9 @@ __global__ void __launch_bounds__(kDiscThreads) discover_kernel(const float *__r
     const int df = (int)(stride % F);
     for (int64_t base = 0; base < total; base += stride) {
       const int64_t i = base + tid0;
-      if (i < total) see(f0, canon_key(__ldcs(feat + i), local_flags, kFlagBadFeature));
+      if (i < total)
+        see(f0, canon_key(__ldcs(feat + i + (i / F / chunk_rows) * gap_rows * F), local_flags,
+                          kFlagBadFeature));
       f0 += df;
       if (f0 >= F) f0 -= F;
       __syncwarp();
@@ -239,6 +245,8 @@ struct LabelBinArgs {
   int F, V, BS, TR, P, use_tma;
   const uint8_t *tab;       // [F][kPhBytes] perfect hashes
   const uint32_t *lk_mul;   // [F][2] their multipliers
+  const uint32_t *slot_keys;  // [F][512] the key of every hash slot (0xFFFFFFFF: empty)
+  int keys_in_smem;           // copy them to smem (else read through L1: wide tables)
   uint32_t *flags;
   uint8_t *bins, *labels;
   size_t pstride;           // bytes between bins word planes
@@ -251,7 +259,9 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
   uint64_t *empty = full + kStages;
   uint32_t *lmul = reinterpret_cast<uint32_t *>(smem + 128);  // [F][2]
   uint8_t *tab = smem + 128 + 8 * kMaxF;                     // [F][kPhBytes]
-  const size_t o1 = (128 + 8 * kMaxF + (size_t)F * kPhBytes + 15) & ~(size_t)15;
+  const size_t o0 = (128 + 8 * kMaxF + (size_t)F * kPhBytes + 15) & ~(size_t)15;
+  uint32_t *skeys = reinterpret_cast<uint32_t *>(smem + o0);  // [F][kPhSlots]
+  const size_t o1 = o0 + (a.keys_in_smem ? (size_t)F * kPhSlots * 4 : 0);
   float *stT = reinterpret_cast<float *>(smem + o1);
   float *stF = stT + (size_t)kStages * TR * V;
 
@@ -259,6 +269,9 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
   for (int i = tid; i < F * kPhBytes / 4; i += blockDim.x)
     reinterpret_cast<uint32_t *>(tab)[i] = reinterpret_cast<const uint32_t *>(a.tab)[i];
   for (int i = tid; i < 2 * F; i += blockDim.x) lmul[i] = a.lk_mul[i];
+  if (a.keys_in_smem)
+    for (int i = tid; i < F * kPhSlots; i += blockDim.x) skeys[i] = a.slot_keys[i];
+  const uint32_t *kk = a.keys_in_smem ? skeys : a.slot_keys;
   if (tid == 0) {
     for (int s = 0; s < kStages; s++) {
       mbar_init(&full[s], 1);
@@ -290,10 +303,15 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
   const bool vec_t = (V & 3) == 0;
   const int per = F / P;  // features per lane when F % P == 0
   const bool vec_f = (F % P) == 0 && (per & 3) == 0;
-  auto rank_of = [&](int f, uint32_t key) -> int {  // perfect hash: 2 dependent byte loads
+  // perfect hash: the displacement, then the slot's rank and key (independent
+  // loads); a key that is not the slot's is a value the discovery (sample)
+  // missed: flagged, the caller re-discovers the whole table
+  auto rank_of = [&](int f, uint32_t key) -> int {
     const uint8_t *t = tab + f * kPhBytes;
     const uint32_t d = reinterpret_cast<const uint16_t *>(t)[hash_bits(key, lmul[2 * f], kPhLog2Buckets)];
-    return t[kPhBuckets * 2 + ((hash_bits(key, lmul[2 * f + 1], kPhLog2Slots) + d) & (kPhSlots - 1))];
+    const uint32_t sl = (hash_bits(key, lmul[2 * f + 1], kPhLog2Slots) + d) & (kPhSlots - 1);
+    if (kk[f * kPhSlots + sl] != key) local_flags |= kFlagUnseen;
+    return t[kPhBuckets * 2 + sl];
   };
   for (int64_t k = 0; k < K; k++) {
     const int64_t t = first + k * stride;
@@ -409,12 +427,13 @@ int sm_count() {
 }  // namespace
 
 int lookup_table_bytes(int F) { return F * kPhBytes; }
+int lookup_slots() { return kPhSlots; }
 
 // Perfect hash of one feature's sorted values (host; <= 256 keys): bucket
 // h1(key) of 64 gets a displacement d so that slot (h2(key) + d) mod 512 is
 // distinct for every key; buckets are placed largest first.  Same hash_bits
 // as the device.  Returns false only if no seed works (never seen).
-bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab) {
+bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab, uint32_t *slot_keys) {
   auto hb = [](uint32_t key, uint32_t m, int l) { return (key * m) >> (32 - l); };
   std::vector<uint32_t> keys(D);
   for (int r = 0; r < D; r++) memcpy(&keys[r], &vals[r], 4);
@@ -430,6 +449,7 @@ bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab) {
     std::vector<char> used(kPhSlots, 0);
     uint16_t disp[kPhBuckets] = {0};
     std::vector<uint8_t> slot_rank(kPhSlots, 0);
+    std::vector<uint32_t> skey(kPhSlots, 0xFFFFFFFFu);  // NaN bits: never a canonical key
     bool ok = true;
     for (int b : order) {
       if (buckets[b].empty()) break;
@@ -456,11 +476,13 @@ bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab) {
         const uint32_t sl = (hb(keys[r], m2, kPhLog2Slots) + found) & (kPhSlots - 1);
         used[sl] = 1;
         slot_rank[sl] = (uint8_t)r;
+        skey[sl] = keys[r];
       }
     }
     if (!ok) continue;
     memcpy(tab, disp, sizeof disp);
     memcpy(tab + kPhBuckets * 2, slot_rank.data(), kPhSlots);
+    memcpy(slot_keys, skey.data(), kPhSlots * 4);
     mul[0] = m1;
     mul[1] = m2;
     return true;
@@ -469,7 +491,7 @@ bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab) {
 }
 
 void launch_discover(const float *feat, int64_t n, int F, uint32_t *gkey, uint32_t *gcount,
-                     uint32_t *flags, cudaStream_t s) {
+                     uint32_t *flags, int64_t chunk_rows, int64_t gap_rows, cudaStream_t s) {
   if (n == 0) return;
   int log2nb = 8;  // 256 buckets x 4 keys per feature (~1 key per bucket at 256 values)
   while (log2nb > 4 && (size_t)F * (16u << log2nb) > 64 * 1024) log2nb--;
@@ -477,7 +499,8 @@ void launch_discover(const float *feat, int64_t n, int F, uint32_t *gkey, uint32
   CUDA_CHECK(cudaFuncSetAttribute(discover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
   const int grid = grid_for(n * F / 4 + 1, kDiscThreads * 4, sm_count() * 2);
-  discover_kernel<<<grid, kDiscThreads, smem, s>>>(feat, n, F, log2nb, gkey, gcount, flags);
+  discover_kernel<<<grid, kDiscThreads, smem, s>>>(feat, n, F, log2nb, gkey, gcount, flags,
+                                                   chunk_rows > 0 ? chunk_rows : n + 1, gap_rows);
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -497,8 +520,9 @@ void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int worl
 }
 
 void launch_label_bin(const float *feat, const float *times, int64_t n, int F, int V, int BS,
-                      const uint8_t *tab, const uint32_t *lk_mul, uint32_t *flags, uint8_t *bins,
-                      size_t pstride, uint8_t *labels, cudaStream_t s) {
+                      const uint8_t *tab, const uint32_t *lk_mul, const uint32_t *slot_keys,
+                      uint32_t *flags, uint8_t *bins, size_t pstride, uint8_t *labels,
+                      cudaStream_t s) {
   if (n == 0) return;
   LabelBinArgs a;
   a.feat = feat;
@@ -509,11 +533,16 @@ void launch_label_bin(const float *feat, const float *times, int64_t n, int F, i
   a.BS = BS;
   a.tab = tab;
   a.lk_mul = lk_mul;
+  a.slot_keys = slot_keys;
   a.flags = flags;
   a.bins = bins;
   a.pstride = pstride;
   a.labels = labels;
-  const size_t table = (128 + 8 * kMaxF + (size_t)F * kPhBytes + 15) & ~(size_t)15;
+  size_t table = (128 + 8 * kMaxF + (size_t)F * kPhBytes + 15) & ~(size_t)15;
+  // slot keys in smem when they leave room for 4-lane rows (always at F <= 16)
+  a.keys_in_smem = table + (size_t)F * kPhSlots * 4 +
+                           (size_t)kStages * (kIngestThreads / 4) * (V + F) * 4 <= 220 * 1024;
+  if (a.keys_in_smem) table += (size_t)F * kPhSlots * 4;
   // P threads per row, TR = threads / P rows per tile: the largest tile whose
   // kStages (times, features) buffers fit next to the table
   a.P = 4;

@@ -274,3 +274,27 @@ def test_record_path_and_shim():
     assert pol == [0, 1, 0, 1]  # round robin before training
     info = ad.adapt_region_info(r)
     assert info["trained"]  # 4 distinct (feature, variant) pairs = min_train_data
+
+
+@pytest.mark.parametrize("rare", [False, True])
+def test_sampled_discovery_is_exact(rare):
+    # tables above 4.2M rows discover their values on a 1M-row sample first;
+    # the bin pass checks every value and falls back to the full discovery
+    # when the sample missed one (a value that only occurs outside the sample)
+    rng = np.random.default_rng(21)
+    n, F, V = 4_500_000, 3, 3
+    grid = np.array([1.0, 2.5, 4.0, 8.0, 16.0, 0.0, -3.0], np.float32)
+    X = grid[rng.integers(0, len(grid), size=(n, F))]
+    T = rng.random((n, V), dtype=np.float32) + 1.0
+    T[np.arange(n), (X[:, 0] > 3).astype(int) + (X[:, 1] > 5).astype(int)] = 0.5
+    if rare:  # rows 40000 and 4.4e6 lie between the sample chunks
+        X[40_000, 1] = 123.25
+        X[4_400_000, 2] = -7.5
+    h = _train(X, T, 3)
+    for f in range(F):
+        assert np.array_equal(ad.adapt_get_value_table(h, f), oracle.value_table(X, f)), f
+    bins = ad.adapt_get_bins(h, n, F)
+    ref_bins = np.stack([np.searchsorted(oracle.value_table(X, f), X[:, f]) for f in range(F)], 1)
+    assert np.array_equal(bins, ref_bins.astype(np.uint8))
+    y = oracle.labels(T)
+    assert_tree_equal(ad.adapt_get_tree(h), oracle.train(X, y, V, 3))
