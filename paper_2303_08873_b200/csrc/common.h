@@ -76,6 +76,15 @@ struct NodeRes {
   // class order (res_stride leaves room for C of each)
 };
 
+// Raise a kernel's dynamic shared-memory limit only when a launch needs more
+// than what was set before (cudaFuncSetAttribute costs microseconds per call;
+// launchers run under the library's mutex).
+void ensure_smem_limit(const void *func, size_t bytes);
+template <class K>
+inline void smem_limit(K *kernel, size_t bytes) {
+  ensure_smem_limit(reinterpret_cast<const void *>(kernel), bytes);
+}
+
 // ---- kernel launchers (records.cu): long-format records -> wide rows ----
 size_t rec_table_slots(int64_t m);  // hash-set slots for m records (power of two >= 2m)
 int rec_scan_blocks(int64_t m);     // blocks of the group-id scan

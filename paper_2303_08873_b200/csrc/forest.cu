@@ -175,8 +175,7 @@ void launch_select_forest(const DNode *nodes, int n_nodes, const int32_t *roots,
   constexpr int W = kForestThreads / 32;
   const size_t smem = (size_t)std::min(n_nodes, kForestTop) * sizeof(DNode) +
                       (size_t)W * 32 * (F | 1) * 4 + (size_t)W * T * 32;
-  CUDA_CHECK(cudaFuncSetAttribute(select_forest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+  smem_limit(select_forest_kernel, smem);
   const int64_t tiles = (m + 31) / 32;
   const int grid = (int)std::min<int64_t>((tiles + W - 1) / W, 2 * sm_count());
   select_forest_kernel<<<grid, kForestThreads, smem, s>>>(nodes, n_nodes, roots, T, X, m, F, out);

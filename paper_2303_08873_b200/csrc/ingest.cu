@@ -496,8 +496,7 @@ void launch_discover(const float *feat, int64_t n, int F, uint32_t *gkey, uint32
   int log2nb = 8;  // 256 buckets x 4 keys per feature (~1 key per bucket at 256 values)
   while (log2nb > 4 && (size_t)F * (16u << log2nb) > 64 * 1024) log2nb--;
   const size_t smem = (size_t)F * (16u << log2nb);
-  CUDA_CHECK(cudaFuncSetAttribute(discover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+  smem_limit(discover_kernel, smem);
   const int grid = grid_for(n * F / 4 + 1, kDiscThreads * 4, sm_count() * 2);
   discover_kernel<<<grid, kDiscThreads, smem, s>>>(feat, n, F, log2nb, gkey, gcount, flags,
                                                    chunk_rows > 0 ? chunk_rows : n + 1, gap_rows);
@@ -513,8 +512,7 @@ void launch_collect_values(const uint32_t *gkey, const uint32_t *gcount, int F, 
 void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int world, int F,
                          float *val, int32_t *nval, uint32_t *flags, cudaStream_t s) {
   const size_t smem = (size_t)world * kMaxBins * 5;
-  CUDA_CHECK(cudaFuncSetAttribute(merge_values_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_limit(merge_values_kernel, smem);
   merge_values_kernel<<<F, 1024, smem, s>>>(all_vals, all_cnt, world, F, val, nval, flags);
   CUDA_CHECK(cudaGetLastError());
 }
@@ -553,8 +551,7 @@ void launch_label_bin(const float *feat, const float *times, int64_t n, int F, i
   const size_t smem = table + (size_t)kStages * a.TR * (V + F) * 4;
   const int64_t ntiles = (n + a.TR - 1) / a.TR;
   const int grid = (int)std::min<int64_t>(ntiles, sm_count());
-  CUDA_CHECK(cudaFuncSetAttribute(label_bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+  smem_limit(label_bin_kernel, smem);
   label_bin_kernel<<<grid, kIngestThreads, smem, s>>>(a);
   CUDA_CHECK(cudaGetLastError());
 }

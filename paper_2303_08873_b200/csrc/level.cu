@@ -28,6 +28,7 @@
 // Every quantity that decides the tree is an integer, so the result does not
 // depend on row order, on the number of ranks or on atomic ordering.
 #include <algorithm>
+#include <unordered_map>
 
 #include "common.h"
 #include "ptx.h"
@@ -404,6 +405,14 @@ __global__ void __launch_bounds__(256) hist_flat_kernel(HistArgs a) {
 
 }  // namespace
 
+void ensure_smem_limit(const void *func, size_t bytes) {
+  static std::unordered_map<const void *, size_t> set;
+  size_t &cur = set[func];
+  if (bytes <= cur) return;
+  CUDA_CHECK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  cur = bytes;
+}
+
 int partition_ranges(int sms, uint32_t total_rows) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((total_rows + 4095) / 4096, 2 * sms));
 }
@@ -459,12 +468,10 @@ void launch_hist(const HistArgs &a, cudaStream_t s) {
 #define CASE(B)                                                                              \
   case B:                                                                                    \
     if (a.w_in) {                                                                            \
-      CUDA_CHECK(cudaFuncSetAttribute(hist_kernel<B, true>,                                  \
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      smem_limit(hist_kernel<B, true>, smem);                                                \
       CUDA_CHECK(cudaLaunchKernelEx(&cfg, hist_kernel<B, true>, a));                         \
     } else {                                                                                 \
-      CUDA_CHECK(cudaFuncSetAttribute(hist_kernel<B, false>,                                 \
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      smem_limit(hist_kernel<B, false>, smem);                                               \
       CUDA_CHECK(cudaLaunchKernelEx(&cfg, hist_kernel<B, false>, a));                        \
     }                                                                                        \
     break;

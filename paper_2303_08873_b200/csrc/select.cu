@@ -153,8 +153,7 @@ void launch_select(const DNode *tree, int n_nodes, const float *X, int64_t m, in
 #define CASE(FF)                                                                               \
   case FF: {                                                                                   \
     const size_t smem = tree_b + (size_t)kSelThreads * kSelChains * (FF | 1) * 4;              \
-    CUDA_CHECK(cudaFuncSetAttribute(select_kernel<FF>,                                         \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
+    smem_limit(select_kernel<FF>, smem);   \
     select_kernel<FF><<<vgrid, kSelThreads, smem, s>>>(tree, n_top, X, m, out);                \
     break;                                                                                     \
   }
@@ -164,8 +163,7 @@ void launch_select(const DNode *tree, int n_nodes, const float *X, int64_t m, in
       const size_t smem = tree_b + (size_t)kAnyThreads * (F | 1) * 4;
       const int64_t tiles = (m + kAnyThreads - 1) / kAnyThreads;
       const int grid = (int)std::min<int64_t>(tiles, sms);
-      CUDA_CHECK(cudaFuncSetAttribute(select_kernel_any,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      smem_limit(select_kernel_any, smem);
       select_kernel_any<<<grid, kAnyThreads, smem, s>>>(tree, n_top, X, m, F, out);
     }
   }
