@@ -32,6 +32,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(CSRC, os.path.basename(src) + ".o")
         cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xptxas", "-v" if verbose else "-O3", f"-DADAPT_GIT=\"{_git()}\"",
+               *os.environ.get("ADAPT_NVCC_DEFS", "").split(),  # tuning sweeps only
                "-I", os.path.join(ROOT, "include"), "-x", "cu", "-c", src, "-o", obj]
         subprocess.check_call(cmd)
         objs.append(obj)

@@ -114,11 +114,21 @@ __device__ __forceinline__ int first_seg(const Seg *segs, int nseg, uint32_t p) 
 }
 
 // ------------------------------------------------------------ partition --
-constexpr int kPartThreads = 512;
-constexpr int kPartUnroll = 4;
+#ifndef ADAPT_PART_UNROLL
+#define ADAPT_PART_UNROLL 4
+#endif
+#ifndef ADAPT_HIST_UNROLL
+#define ADAPT_HIST_UNROLL 8
+#endif
+#ifndef ADAPT_PART_THREADS
+#define ADAPT_PART_THREADS 512
+#endif
+constexpr int kPartThreads = ADAPT_PART_THREADS;
+constexpr int kPartMinBlocks = 1024 / ADAPT_PART_THREADS;  // 1024 threads per SM
+constexpr int kPartUnroll = ADAPT_PART_UNROLL;  // rows in flight per thread
 
 template <int BS>
-__global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) {
+__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition_kernel(PartArgs a) {
   __shared__ uint32_t s_cur[2];
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t R = (a.total_rows + gridDim.x - 1) / gridDim.x;
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) partition_kernel(PartArgs a) 
 
 // ------------------------------------------------------------ histogram --
 constexpr int kHistThreads = 1024;
-constexpr int kHistUnroll = 16;  // rows in flight per thread (the pass is latency-bound otherwise)
+constexpr int kHistUnroll = ADAPT_HIST_UNROLL;  // rows in flight per thread (latency-bound otherwise)
 constexpr int kSyncEvery = 2;  // iterations of kHistUnroll x 1024 rows between partner syncs
 
 // WEIGHTED (forests): rows add their bootstrap weight; a separate instance so
@@ -414,7 +424,8 @@ void ensure_smem_limit(const void *func, size_t bytes) {
 }
 
 int partition_ranges(int sms, uint32_t total_rows) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>((total_rows + 4095) / 4096, 2 * sms));
+  return (int)std::max<int64_t>(1, std::min<int64_t>((total_rows + 4095) / 4096,
+                                                      (int64_t)kPartMinBlocks * sms));
 }
 
 void launch_partition(const PartArgs &a, cudaStream_t s) {

@@ -18,7 +18,10 @@ namespace adapt {
 namespace {
 
 constexpr int kSelThreads = 1024;  // one CTA per SM: one smem copy of the tree
-constexpr int kSelChains = 2;      // vectors walked at once per lane
+#ifndef ADAPT_SEL_CHAINS
+#define ADAPT_SEL_CHAINS 2
+#endif
+constexpr int kSelChains = ADAPT_SEL_CHAINS;  // vectors walked at once per lane
 constexpr int kAnyThreads = 256;   // generic-F kernel
 constexpr int kTopNodes = 8191;    // 64 KB
 
