@@ -224,6 +224,10 @@ struct Ctx {
 Ctx g_ctx;
 
 // ---- the three collectives of SURVEY §8(e), over NCCL or the host hooks ----
+// (ADAPT_NCCL_SELF=1 gives a world-1 run a 1-rank NCCL communicator so the
+// NCCL path is exercised on one GPU; collectives are then real NCCL calls)
+bool collectives_on() { return g_ctx.world > 1 || g_ctx.comm != nullptr; }
+
 void host_hook(int rc, const char *what) {
   if (rc != 0) throw Error(ADAPT_E_NCCL, std::string(what) + ": host collective hook returned " +
                                             std::to_string(rc));
@@ -231,7 +235,7 @@ void host_hook(int rc, const char *what) {
 
 // sum of `count` u32 (or u64 when wide) over ranks, in place on the device
 void comm_allreduce_sum(void *dbuf, size_t count, bool wide, cudaStream_t s, const char *what) {
-  if (g_ctx.world == 1 || count == 0) return;
+  if (!collectives_on() || count == 0) return;
   if (!g_ctx.host_comm) {
     g_nccl.check(g_nccl.AllReduce(dbuf, dbuf, count, wide ? ncclUint64 : ncclUint32, ncclSum,
                                   g_ctx.comm, s), what);
@@ -264,7 +268,7 @@ void comm_allreduce_sum(void *dbuf, size_t count, bool wide, cudaStream_t s, con
 
 // drecv[r*bytes, (r+1)*bytes) = rank r's dsend, on the device
 void comm_allgather(const void *dsend, void *drecv, size_t bytes, cudaStream_t s, const char *what) {
-  if (g_ctx.world == 1) {
+  if (!collectives_on()) {
     CUDA_CHECK(cudaMemcpyAsync(drecv, dsend, bytes, cudaMemcpyDeviceToDevice, s));
     return;
   }
@@ -627,7 +631,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
   }
   uint64_t n_total = (uint64_t)n;
   h->hsmall.ensure(1 << 16);
-  if (world > 1) {
+  if (collectives_on()) {
     DevBuf tmp;
     tmp.ensure(8);
     CUDA_CHECK(cudaMemcpyAsync(tmp.p, &n_total, 8, cudaMemcpyHostToDevice, s));
@@ -665,7 +669,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     CUDA_CHECK(cudaStreamSynchronize(s));
     uint32_t bits[6];
     for (int b = 0; b < 6; b++) bits[b] = (hs[0] >> b) & 1;
-    if (world > 1) {
+    if (collectives_on()) {
       CUDA_CHECK(cudaMemcpyAsync(fl.p, bits, 24, cudaMemcpyHostToDevice, s));
       comm_allreduce_sum(fl.p, 6, false, s, "allreduce flags");
       CUDA_CHECK(cudaMemcpyAsync(bits, fl.p, 24, cudaMemcpyDeviceToHost, s));
@@ -1082,7 +1086,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       fa.total_rows = ftotal;
       launch_hist_flat(fa, s);
     }
-    if (world > 1 && ndirect_slots > 0)  // the direct slots are contiguous at the front
+    if (collectives_on() && ndirect_slots > 0)  // the direct slots are contiguous at the front
       comm_allreduce_sum(Hcur->p, (size_t)soff[ndirect_slots], false, s, "allreduce histograms");
     if (!jobs.empty()) {
       Phase ph("subtract", s, 0);
@@ -1248,7 +1252,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     h->forest.clear();
   } else {  // random forest: T trees on bootstrap resamples of the global table (R19)
     uint64_t lo = 0;  // this rank's first global row
-    if (world > 1) {
+    if (collectives_on()) {
       DevBuf nb, allb;
       nb.ensure(8);
       allb.ensure((size_t)world * 8);
@@ -1396,6 +1400,11 @@ int adapt_init(int device, int rank, int world, const void *nccl_unique_id) {
       ncclUniqueId id;
       memcpy(&id, nccl_unique_id, sizeof(id));
       g_nccl.check(g_nccl.CommInitRank(&g_ctx.comm, world, id, rank), "ncclCommInitRank");
+    } else if (getenv("ADAPT_NCCL_SELF")) {  // testing: a 1-rank NCCL communicator
+      g_nccl.load();
+      ncclUniqueId id;
+      g_nccl.check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId");
+      g_nccl.check(g_nccl.CommInitRank(&g_ctx.comm, 1, id, 0), "ncclCommInitRank");
     }
     g_ctx.device = device;
     g_ctx.rank = rank;
