@@ -112,7 +112,7 @@ bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab, u
 int lookup_slots();  // hash slots per feature (slot_keys entries)
 void launch_label_bin(const float *feat, const float *times, int64_t n, int F, int V, int BS,
                       const uint8_t *tab, const uint32_t *lk_mul, const uint32_t *slot_keys,
-                      uint32_t *flags, uint8_t *bins, size_t pstride, uint8_t *labels,
+                      int verify, uint32_t *flags, uint8_t *bins, size_t pstride, uint8_t *labels,
                       cudaStream_t s);
 void launch_bins_out(const uint8_t *bins, size_t pstride, int64_t n, int F, int BS, uint8_t *out,
                      cudaStream_t s);

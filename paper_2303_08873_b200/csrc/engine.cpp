@@ -740,7 +740,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
     {
       Phase ph("ingest", s, (double)n * (4.0 * F + 4.0 * V + F + 1));  // algorithmic
       launch_label_bin(feat, times, n, F, V, BS, h->lk_keys.as<uint8_t>(), h->lk_mul.as<uint32_t>(),
-                       h->lk_skeys.as<uint32_t>(), h->flags.as<uint32_t>(),
+                       h->lk_skeys.as<uint32_t>(), sampled && attempt == 0 ? 1 : 0,
+                       h->flags.as<uint32_t>(),
                        h->bins.as<uint8_t>(), pstride, h->labels.as<uint8_t>(), s);
     }
     const uint32_t fl = check_flags();

@@ -247,6 +247,7 @@ struct LabelBinArgs {
   const uint32_t *lk_mul;   // [F][2] their multipliers
   const uint32_t *slot_keys;  // [F][512] the key of every hash slot (0xFFFFFFFF: empty)
   int keys_in_smem;           // copy them to smem (else read through L1: wide tables)
+  int verify;                 // check every key (the tables came from a sample)
   uint32_t *flags;
   uint8_t *bins, *labels;
   size_t pstride;           // bytes between bins word planes
@@ -306,11 +307,12 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
   // perfect hash: the displacement, then the slot's rank and key (independent
   // loads); a key that is not the slot's is a value the discovery (sample)
   // missed: flagged, the caller re-discovers the whole table
+  uint32_t miss = 0;  // OR of (slot key ^ key): nonzero iff some value was not in the tables
   auto rank_of = [&](int f, uint32_t key) -> int {
     const uint8_t *t = tab + f * kPhBytes;
     const uint32_t d = reinterpret_cast<const uint16_t *>(t)[hash_bits(key, lmul[2 * f], kPhLog2Buckets)];
     const uint32_t sl = (hash_bits(key, lmul[2 * f + 1], kPhLog2Slots) + d) & (kPhSlots - 1);
-    if (kk[f * kPhSlots + sl] != key) local_flags |= kFlagUnseen;
+    if (a.verify) miss |= kk[f * kPhSlots + sl] ^ key;
     return t[kPhBuckets * 2 + sl];
   };
   for (int64_t k = 0; k < K; k++) {
@@ -397,6 +399,7 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
     if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     if (tid == 0 && k + kStages < K) issue(k + kStages);
   }
+  if (miss) local_flags |= kFlagUnseen;
   if (local_flags) atomicOr(a.flags, local_flags);
 }
 
@@ -519,7 +522,7 @@ void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int worl
 
 void launch_label_bin(const float *feat, const float *times, int64_t n, int F, int V, int BS,
                       const uint8_t *tab, const uint32_t *lk_mul, const uint32_t *slot_keys,
-                      uint32_t *flags, uint8_t *bins, size_t pstride, uint8_t *labels,
+                      int verify, uint32_t *flags, uint8_t *bins, size_t pstride, uint8_t *labels,
                       cudaStream_t s) {
   if (n == 0) return;
   LabelBinArgs a;
@@ -532,6 +535,7 @@ void launch_label_bin(const float *feat, const float *times, int64_t n, int F, i
   a.tab = tab;
   a.lk_mul = lk_mul;
   a.slot_keys = slot_keys;
+  a.verify = verify;
   a.flags = flags;
   a.bins = bins;
   a.pstride = pstride;
