@@ -127,6 +127,70 @@ def cpu_baseline(cfg, rows: int, depth: int):
     return rows / dt, dt
 
 
+def bench_c5(args, ad, adist, torch, dev, stream, rank: int, world: int, peak: float):
+    """batched selection of M = 1e9 C4-shaped feature vectors
+    (seed 7, sharded over the ranks) by (i) a depth-16 tree trained by the
+    engine on a 1e7-row C4-shaped table (seed 5) and (ii) the synthetic complete
+    depth-16 tree (seed 6, the worst case).  Each timed launch is one
+    adapt_select_batch over the rank's whole shard (64 GB at P=1: > L2)."""
+    import dataclasses
+
+    cfg = dataclasses.replace(synth.CONFIGS["C4"], D=16)
+    flat, off = cfg.grid_table
+    g, o = torch.from_numpy(flat).to(dev), torch.from_numpy(off).to(dev)
+    Nt = args.c5_train_rows
+    tlo, thi = adist.shard_bounds(Nt, rank, world)
+    Xt = torch.empty((thi - tlo, cfg.F), dtype=torch.float32, device=dev)
+    Tt = torch.empty((thi - tlo, cfg.V), dtype=torch.float32, device=dev)
+    synth.generate_device(cfg, tlo, thi - tlo, Xt.data_ptr(), Tt.data_ptr(), g.data_ptr(), o.data_ptr(),
+                          stream.cuda_stream, seed=5)
+    trained = ad.adapt_region_create("bench_c5_trained", cfg.F, cfg.V, "dtree,depth=16", 0)
+    ad.adapt_record_table(trained, Xt, Tt, thi - tlo, True, stream)
+    ad.adapt_train(trained, stream)
+    del Xt, Tt
+    cols = synth.random_tree(cfg, 16, seed=6)
+    tree = np.zeros(len(cols["feature"]), ad.NODE_DTYPE)
+    for k, v in cols.items():
+        tree[k] = v
+    complete = ad.adapt_region_create("bench_c5_complete", cfg.F, cfg.V, "dtree,depth=16", 0)
+    ad.adapt_set_tree(complete, tree)
+    M = args.c5_vectors
+    lo, hi = adist.shard_bounds(M, rank, world)
+    m = hi - lo
+    X = torch.empty((m, cfg.F), dtype=torch.float32, device=dev)
+    out = torch.empty(m, dtype=torch.int32, device=dev)
+    synth.generate_device(cfg, lo, m, X.data_ptr(), 0, g.data_ptr(), o.data_ptr(), stream.cuda_stream,
+                          seed=7)
+    res = {"workload": "C5: depth-16 trees evaluated on 1e9 C4-shaped feature vectors (16 f32 "
+                       "features), sharded over the ranks",
+           "vectors": M, "bytes_per_vector": 4 * cfg.F + 4, "steps": args.steps, "warmup": args.warmup,
+           "l2": "X (%.0f GB per rank) exceeds the 126 MB L2; no flush needed" % (m * 4 * cfg.F / 1e9)}
+    for name, h in (("trained", trained), ("complete", complete)):
+        for _ in range(max(args.warmup, 1)):
+            ad.adapt_select_batch(h, X, m, out, stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ad.adapt_select_batch(h, X, m, out, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = adist.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
+        gbs = m * (4 * cfg.F + 4) / (ms / 1e3) / 1e9  # rank-local bytes / max-over-ranks time
+        res[name] = {"tree_nodes": int(len(ad.adapt_get_tree(h))), "ms_per_batch": ms,
+                     "selections_per_s": M / (ms / 1e3),
+                     "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                                  "frac": gbs / peak}}
+    ad.adapt_region_destroy(trained)
+    ad.adapt_region_destroy(complete)
+    del X, out
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
@@ -170,6 +234,9 @@ def main():
     ap.add_argument("--model", default="", help="model_type override, e.g. 'rfc,10,4' (P:257)")
     ap.add_argument("--records", type=int, default=20_000_000, help="record-path batch size")
     ap.add_argument("--no-records", action="store_true")
+    ap.add_argument("--c5-vectors", type=int, default=1_000_000_000, help="C5 batch size (SURVEY §8(d))")
+    ap.add_argument("--c5-train-rows", type=int, default=10_000_000)
+    ap.add_argument("--no-c5", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -293,13 +360,20 @@ def main():
         del rX, rns, rv, rows
         _ = wide
 
+    peak, peak_src = peaks()
+    c5 = None
+    if not args.no_c5 and args.config == "C4":
+        ad.adapt_region_destroy(h)
+        del X, T, out
+        torch.cuda.empty_cache()
+        c5 = bench_c5(args, ad, adist, torch, dev, stream, rank, world, peak)
+
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return
 
-    peak, peak_src = peaks()
     kern = {k: v for k, v in prof.items() if k.split("_L")[0] in KERNEL_PHASES}
     dom = max(kern, key=lambda k: kern[k]["ms"])
     d = kern[dom]
@@ -352,6 +426,7 @@ def main():
         "level_loop_roofline": level_loop,
         "cpu_baseline": cpu,
         "record_path": rec,
+        "select_c5": c5,
         "phase_ms_per_step": step_ms_phases,
         "tree_nodes": int(len(tree)),
         "levels": levels,

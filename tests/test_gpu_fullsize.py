@@ -118,3 +118,60 @@ def test_c4_full_size_sampled_parity():
     torch.cuda.synchronize()
     assert np.array_equal(out[ti].cpu().numpy(), oracle.select(tree, Xs))
     ad.adapt_region_destroy(h)
+
+
+def test_c5_full_size_sampled_selection():
+    """C5 at full size, in bench.py's launch configuration: one adapt_select_batch
+    over 1e9 C4-shaped vectors (seed 7; 64 GB) with (i) a depth-16 tree the
+    engine trains on a 1e7-row C4-shaped table (seed 5) and (ii) the synthetic
+    complete depth-16 tree (seed 6).  Sampled vectors (random + the ragged tail)
+    against the oracle's walk of the same tree (R8: x <= thr -> left)."""
+    import dataclasses
+
+    cfg = dataclasses.replace(synth.CONFIGS["C4"], D=16)
+    F, V = cfg.F, cfg.V
+    torch.cuda.set_device(DEV)
+    ad.adapt_init(0, 0, 1)
+    s = torch.cuda.current_stream()
+    flat, off = cfg.grid_table
+    g, o = torch.from_numpy(flat).to(DEV), torch.from_numpy(off).to(DEV)
+    Nt = 10_000_000
+    Xt = torch.empty((Nt, F), dtype=torch.float32, device=DEV)
+    Tt = torch.empty((Nt, V), dtype=torch.float32, device=DEV)
+    synth.generate_device(cfg, 0, Nt, Xt.data_ptr(), Tt.data_ptr(), g.data_ptr(), o.data_ptr(),
+                          s.cuda_stream, seed=5)
+    trained = ad.adapt_region_create("fullsize_c5_trained", F, V, "dtree,depth=16", 0)
+    ad.adapt_record_table(trained, Xt, Tt, Nt, True, s)
+    ad.adapt_train(trained, s)
+    del Xt, Tt
+    cols = synth.random_tree(cfg, 16, seed=6)
+    ctree = np.zeros(len(cols["feature"]), oracle.NODE_DTYPE)
+    for k, v in cols.items():
+        ctree[k] = v
+    complete = ad.adapt_region_create("fullsize_c5_complete", F, V, "dtree,depth=16", 0)
+    ad.adapt_set_tree(complete, ctree)
+    M = 1_000_000_000
+    X = torch.empty((M, F), dtype=torch.float32, device=DEV)
+    synth.generate_device(cfg, 0, M, X.data_ptr(), 0, g.data_ptr(), o.data_ptr(), s.cuda_stream, seed=7)
+    out = torch.empty(M, dtype=torch.int32, device=DEV)
+    rng = np.random.default_rng(5)
+    idx = np.unique(np.concatenate([rng.choice(M, size=100_000, replace=False),
+                                    np.arange(M - 1000, M)]))
+    ti = torch.from_numpy(idx).to(DEV)
+    Xs = X[ti].cpu().numpy()
+    # the device generator is the host one (test_synth_device_matches_host); spot-check here too
+    Xh, _ = synth.generate(cfg, int(idx[0]), 1, seed=7)
+    assert np.array_equal(Xh[0], Xs[0])
+    for h in (trained, complete):
+        tree = ad.adapt_get_tree(h)
+        assert tree["depth"].max() <= 16
+        out.fill_(-1)
+        ad.adapt_select_batch(h, X, M, out, s)
+        torch.cuda.synchronize()
+        assert np.array_equal(out[ti].cpu().numpy(), oracle.select(tree, Xs))
+        assert int((out < 0).sum()) == 0 and int((out >= V).sum()) == 0
+    assert len(ad.adapt_get_tree(trained)) > 8191  # deeper than the shared-memory top
+    ad.adapt_region_destroy(trained)
+    ad.adapt_region_destroy(complete)
+    del X, out
+    torch.cuda.empty_cache()
