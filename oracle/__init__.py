@@ -77,6 +77,9 @@ def lib():
         L.oracle_train.argtypes = [P, P, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, i32, P]
         L.oracle_select.argtypes = [P, i32, P, i64, ctypes.c_int, P]
         L.oracle_bootstrap.argtypes = [ctypes.c_uint64, ctypes.c_int, i64, P]
+        L.oracle_kfold_pos.argtypes = [ctypes.c_uint64, ctypes.c_int, i64, i64]
+        L.oracle_kfold_pos.restype = i64
+        L.oracle_kfold_groups.argtypes = [ctypes.c_uint64, ctypes.c_int, i64, ctypes.c_int, P]
         L.oracle_gini_counts.argtypes = [P, ctypes.c_int]
         L.oracle_gini_counts.restype = ctypes.c_double
         _lib = L
@@ -226,3 +229,46 @@ def select_forest(trees: list, X: np.ndarray) -> np.ndarray:
         labels, counts = np.unique(votes[:, i], return_counts=True)  # ascending labels
         out[i] = labels[np.argmax(counts)]  # first maximum = lowest label
     return out
+
+
+# ---- K-fold harness (Adaptive-25/50/75; R22) ----
+def kfold_pos(seed: int, shuffle: int, N: int, r: int) -> int:
+    """Position of row r in shuffle `shuffle` (a permutation of range(N))."""
+    return int(lib().oracle_kfold_pos(ctypes.c_uint64(seed), int(shuffle), ctypes.c_int64(N),
+                                      ctypes.c_int64(r)))
+
+
+def kfold_groups(seed: int, shuffle: int, N: int, K: int) -> np.ndarray:
+    g = np.zeros(max(N, 1), np.int32)
+    rc = lib().oracle_kfold_groups(ctypes.c_uint64(seed), int(shuffle), ctypes.c_int64(N), int(K), _p(g))
+    if rc:
+        raise OracleError(rc, "kfold_groups")
+    return g[:N]
+
+
+def kfold(X: np.ndarray, T: np.ndarray, D: int, K: int, m: int, shuffles: int, seed: int):
+    """The paper's K-fold methodology on one wide table: per shuffle
+    s and fold k, train the plain CART on the rows whose group is in
+    {(k + j) mod K : j < m} (in row order) and test it on the other rows:
+    n_correct = test rows whose selection is their label (the fastest
+    variant), t_selected / t_best = the exactly rounded sums (math.fsum) of the
+    test rows' times of the selected / the fastest variant.
+    Returns (results: list of dicts in (s, k) order, trees: list)."""
+    import math
+
+    y = labels(T)
+    N = len(X)
+    res, trees = [], []
+    for s in range(shuffles):
+        g = kfold_groups(seed, s, N, K)
+        for k in range(K):
+            train_mask = np.isin(g, [(k + j) % K for j in range(m)])
+            tree = train(X[train_mask], y[train_mask], T.shape[1], D)
+            test = np.nonzero(~train_mask)[0]
+            sel = select(tree, X[test])
+            res.append({"shuffle": s, "fold": k, "n_nodes": len(tree), "n_train": int(train_mask.sum()),
+                        "n_test": int(len(test)), "n_correct": int((sel == y[test]).sum()),
+                        "t_selected": math.fsum(float(T[i, v]) for i, v in zip(test, sel)),
+                        "t_best": math.fsum(float(T[i, y[i]]) for i in test)})
+            trees.append(tree)
+    return res, trees

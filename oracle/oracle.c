@@ -390,3 +390,36 @@ int oracle_bootstrap(uint64_t seed, int tree, int64_t n, uint32_t *w) {
   }
   return 0;
 }
+
+/* ---- K-fold harness (R22): the permutation of the inputs ----
+ * Shuffle s permutes the N global rows with a 4-round Feistel network on
+ * 2h-bit words (the smallest h >= 1 with 4^h >= N), cycle-walking until the
+ * image falls inside [0, N); group of row r = floor(pos(r) * K / N). */
+int64_t oracle_kfold_pos(uint64_t seed, int shuffle, int64_t N, int64_t r) {
+  if (N <= 0 || r < 0 || r >= N || shuffle < 0) return -1;
+  int h = 1;
+  while (h < 31 && ((uint64_t)1 << (2 * h)) < (uint64_t)N) h++;
+  const uint64_t mask = ((uint64_t)1 << h) - 1;
+  const uint64_t key = splitmix64(seed ^ splitmix64((uint64_t)shuffle + 0x2545F4914F6CDD1Dull));
+  uint64_t x = (uint64_t)r;
+  do {
+    uint64_t L = x >> h, R = x & mask;
+    for (uint64_t j = 0; j < 4; j++) {
+      const uint64_t f = splitmix64(key ^ splitmix64((R << 2) | j)) & mask;
+      const uint64_t t = L ^ f;
+      L = R;
+      R = t;
+    }
+    x = (L << h) | R;
+  } while (x >= (uint64_t)N);
+  return (int64_t)x;
+}
+
+int oracle_kfold_groups(uint64_t seed, int shuffle, int64_t N, int K, int32_t *group) {
+  if (N < 0 || K < 2 || shuffle < 0 || (N > 0 && !group)) return ORACLE_E_INVALID_ARG;
+  for (int64_t r = 0; r < N; r++) {
+    const int64_t pos = oracle_kfold_pos(seed, shuffle, N, r);
+    group[r] = (int32_t)(((unsigned __int128)pos * (unsigned)K) / (uint64_t)N);
+  }
+  return ORACLE_OK;
+}

@@ -102,4 +102,14 @@ int oracle_bootstrap(uint64_t seed, int tree, int64_t n, uint32_t *w);
 /* Helper used by the pins: Gini of a class-count vector, 1 - S/(n*n). */
 double oracle_gini_counts(const int64_t *counts, int C);
 
+/* K-fold harness ("split application inputs into K equal-sized
+ * groups ... repeated 10 times, each time shuffling the inputs"; R22).
+ * oracle_kfold_pos: the position of global row r in shuffle `shuffle` (a
+ * bijection of [0, N): 4-round Feistel on 2h bits, cycle-walking), -1 on bad
+ * arguments.  oracle_kfold_groups: group[r] = floor(pos(r) * K / N).  Model
+ * (shuffle, fold k) trains on groups {(k + j) mod K : j < m} and is tested on
+ * the others — composed in oracle/__init__.py from these and oracle_train/select. */
+int64_t oracle_kfold_pos(uint64_t seed, int shuffle, int64_t N, int64_t r);
+int oracle_kfold_groups(uint64_t seed, int shuffle, int64_t N, int K, int32_t *group);
+
 #endif
