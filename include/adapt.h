@@ -209,6 +209,38 @@ int adapt_get_tree(adapt_region_t *h, adapt_node_t *out, int32_t cap, int32_t *n
 int adapt_forest_size(adapt_region_t *h, int32_t *trees);
 int adapt_get_forest_tree(adapt_region_t *h, int32_t t, adapt_node_t *out, int32_t cap,
                           int32_t *n_nodes);
+/* ---- K-fold harness (DESIGN R22) ----
+ * The paper's evaluation methodology: "split application inputs into K
+ * equal-sized groups. A fraction f of groups is used for model training while
+ * the rest are used for testing ... K-fold creation is repeated 10 times, each
+ * time shuffling the inputs" (Adaptive-25/50/75 = K 4, m 1/2/3).  Inputs are
+ * the rows of the recorded table (all ranks: a collective call, like
+ * adapt_train).  Shuffle s permutes the global row ids (4-round Feistel on
+ * 2h-bit words, 4^h >= N, cycle-walking, keyed by (seed, s)); group of row r
+ * = floor(pos(r) K / N); model (s, k) = the region's dtree trained on the rows
+ * of groups {(k + j) mod K : j < train_groups} and tested on the others.
+ * out[s * K + k] (caller-owned, shuffles * K entries) gets the model's counts
+ * summed over ranks; t_selected / t_best are double sums of the test rows'
+ * float32 times of the selected / the fastest variant (summation order
+ * differs from the oracle's exactly rounded sum: DESIGN R22 bounds it).
+ * The region's own model is left as it was.  Borrowed device tables stay
+ * borrowed until this call returns (as for adapt_train).
+ * Errors: ADAPT_E_INVALID_ARG for K not in [2,64], train_groups not in
+ * [1,K-1], shuffles < 1 or NULL out; ADAPT_E_USAGE on a forest region;
+ * ADAPT_E_INSUFFICIENT_DATA for fewer than K rows; as adapt_train otherwise. */
+typedef struct {
+  int32_t shuffle, fold;   /* model (s, k) */
+  int32_t n_nodes, pad_;   /* size of its tree (adapt_get_kfold_tree) */
+  int64_t n_train, n_test; /* global rows */
+  int64_t n_correct;       /* test rows whose selection is their label (the fastest variant) */
+  double t_selected;       /* sum over test rows of times[i][selected] (ns) */
+  double t_best;           /* sum over test rows of times[i][label] (ns) */
+} adapt_kfold_result_t;
+int adapt_kfold(adapt_region_t *h, int K, int train_groups, int shuffles, uint64_t seed,
+                adapt_kfold_result_t *out, void *cuda_stream);
+/* Tree of model `model` (= s * K + k) of the last adapt_kfold, canonical BFS. */
+int adapt_get_kfold_tree(adapt_region_t *h, int32_t model, adapt_node_t *out, int32_t cap,
+                         int32_t *n_nodes);
 /* Install a tree (model reuse across runs; synthetic trees for the
  * selection benchmark).  Validates BFS structure, features and labels. */
 int adapt_set_tree(adapt_region_t *h, const adapt_node_t *nodes, int32_t n_nodes);

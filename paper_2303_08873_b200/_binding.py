@@ -38,7 +38,7 @@ SYMBOLS = [
     "adapt_region_create", "adapt_region_destroy", "adapt_region_info", "adapt_record",
     "adapt_record_batch", "adapt_get_wide_table", "adapt_record_table", "adapt_distinct_pairs", "adapt_train", "adapt_train_many",
     "adapt_select", "adapt_select_batch", "adapt_select_batch_host", "adapt_get_tree",
-    "adapt_forest_size", "adapt_get_forest_tree",
+    "adapt_forest_size", "adapt_get_forest_tree", "adapt_kfold", "adapt_get_kfold_tree",
     "adapt_set_tree", "adapt_get_labels", "adapt_get_value_table", "adapt_get_bins",
     "adapt_profile_enable", "adapt_profile_reset", "adapt_profile_get", "adapt_train_stats",
     "__adapt_region_create", "__adapt_region_begin", "__adapt_region_end",
@@ -51,6 +51,13 @@ NODE_DTYPE = np.dtype([
     ("gini", np.float64),
 ])
 assert NODE_DTYPE.itemsize == 48
+
+KFOLD_DTYPE = np.dtype([  # adapt_kfold_result_t
+    ("shuffle", np.int32), ("fold", np.int32), ("n_nodes", np.int32), ("pad_", np.int32),
+    ("n_train", np.int64), ("n_test", np.int64), ("n_correct", np.int64),
+    ("t_selected", np.float64), ("t_best", np.float64),
+])
+assert KFOLD_DTYPE.itemsize == 56
 
 
 class adapt_phase_t(ctypes.Structure):
@@ -100,6 +107,8 @@ _sigs = {
     "adapt_get_tree": [_P, _P, ctypes.c_int32, _P],
     "adapt_forest_size": [_P, _P],
     "adapt_get_forest_tree": [_P, ctypes.c_int32, _P, ctypes.c_int32, _P],
+    "adapt_kfold": [_P, _I, _I, _I, _U64, _P, _P],
+    "adapt_get_kfold_tree": [_P, ctypes.c_int32, _P, ctypes.c_int32, _P],
     "adapt_set_tree": [_P, _P, ctypes.c_int32],
     "adapt_get_labels": [_P, _P, _I64],
     "adapt_get_value_table": [_P, _I, _P, _P],
@@ -341,6 +350,26 @@ def adapt_get_forest_tree(h: int, t: int) -> np.ndarray:
     out = np.zeros(max(n.value, 1), NODE_DTYPE)
     _check(_L.adapt_get_forest_tree(h, int(t), out.ctypes.data, len(out), ctypes.byref(n)),
            "adapt_get_forest_tree")
+    return out[:n.value]
+
+
+def adapt_kfold(h: int, K: int, train_groups: int, shuffles: int, seed: int = 0,
+                stream=None) -> np.ndarray:
+    """The paper's K-fold harness: shuffles * K models, KFOLD_DTYPE records
+    in (shuffle, fold) order.  Collective over ranks; the table is the recorded one."""
+    out = np.zeros(shuffles * K if shuffles > 0 and K > 0 else 1, KFOLD_DTYPE)
+    _check(_L.adapt_kfold(h, int(K), int(train_groups), int(shuffles), ctypes.c_uint64(seed),
+                          out.ctypes.data, _stream(stream)), "adapt_kfold")
+    return out
+
+
+def adapt_get_kfold_tree(h: int, model: int) -> np.ndarray:
+    """Tree of K-fold model `model` (= shuffle * K + fold) of the last adapt_kfold."""
+    n = ctypes.c_int32()
+    _L.adapt_get_kfold_tree(h, int(model), None, 0, ctypes.byref(n))  # size query (cap 0)
+    out = np.zeros(max(n.value, 1), NODE_DTYPE)
+    _check(_L.adapt_get_kfold_tree(h, int(model), out.ctypes.data, len(out), ctypes.byref(n)),
+           "adapt_get_kfold_tree")
     return out[:n.value]
 
 

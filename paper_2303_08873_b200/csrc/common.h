@@ -210,7 +210,29 @@ int forest_max_trees();
 void launch_select_forest(const DNode *nodes, int n_nodes, const int32_t *roots, int T,
                           const float *X, int64_t m, int F, int32_t *out, cudaStream_t s);
 
-void launch_select(const DNode *tree, int n_nodes, const float *X, int64_t m, int F,
-                   int32_t *out, cudaStream_t s);
+// ---- kernel launchers (kfold.cu): the K-fold harness ----
+constexpr int kKfoldMaxK = 64;
+struct KfoldPartial {
+  unsigned long long n_test, n_correct;
+  double t_selected, t_best;
+};
+// d_bnd[j] = ceil(j N / K), j = 0..K (the first position of group j); w: u8 [n]
+void launch_kfold_weights(uint64_t seed, int shuffle, uint64_t N, const uint64_t *d_bnd, int K, int m,
+                          int k, uint64_t lo, int64_t n, uint8_t *w, cudaStream_t s);
+int kfold_eval_blocks();
+// part: [kfold_eval_blocks()] per-block partials over the rows with w == 0
+void launch_kfold_eval(const uint8_t *w, const uint8_t *lab, const int32_t *sel, const float *times,
+                       int64_t n, int V, KfoldPartial *part, cudaStream_t s);
+
+// a single tree: the first kSelTopNodes BFS nodes (DNode) are staged in shared
+// memory; a child index k >= n_top of a top node names bottom block k - n_top.
+// A bottom block (64 B, 16 words) holds 3 levels in heap order: words 0..6 =
+// the thresholds of its nodes p = 0..6 (children 2p+1, 2p+2; a leaf above the
+// bottom is a pass-through whose 8 descendants all carry its label), words
+// 7..14 = (ref_i << 6) | feature_p (feature of node p = i for i < 7), ref_i of
+// leaf edge i = 2(p-3) + right for p = 3..6: >= 0 the next block, < 0 -1 - label.
+constexpr int kSelTopNodes = 8191;
+void launch_select(const DNode *tree, int n_nodes, const uint4 *blocks, const float *X, int64_t m,
+                   int F, int32_t *out, cudaStream_t s);
 
 }  // namespace adapt

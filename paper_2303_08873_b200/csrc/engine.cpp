@@ -13,6 +13,7 @@
 #include <time.h>
 
 #include <algorithm>
+#include <deque>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -370,7 +371,16 @@ struct adapt_region {
   std::vector<float> val;       // [F][256]
   std::vector<int32_t> nval;    // [F]
   std::vector<adapt_node_t> tree;
-  adapt::DevBuf d_tree;
+  adapt::DevBuf d_tree, d_blocks;  // device tree: DNode top + bottom blocks (select.cu)
+  // K-fold harness (kfold.cu): set for the duration of adapt_kfold
+  struct KfoldSpec {
+    int K, m, shuffles;
+    uint64_t seed;
+    adapt_kfold_result_t *out;
+  };
+  const KfoldSpec *kfold = nullptr;
+  std::vector<std::vector<adapt_node_t>> kfold_trees;
+  adapt::DevBuf kbnd, ksel, kpart;
   bool trained = false;
   std::vector<int64_t> stats;
   // scratch
@@ -484,6 +494,59 @@ void upload_tree(adapt_region *h, cudaStream_t s) {
   h->d_tree.ensure(d.size() * sizeof(DNode));
   CUDA_CHECK(cudaMemcpyAsync(h->d_tree.p, d.data(), d.size() * sizeof(DNode),
                              cudaMemcpyHostToDevice, s));
+  // bottom blocks (common.h): the nodes below the shared-memory top, 3 levels
+  // per 64-byte block, so a walk below the top costs one L2 round trip per 3
+  // levels instead of one per level
+  const auto &tr = h->tree;
+  const int n_top = std::min<int>((int)tr.size(), kSelTopNodes);
+  std::vector<uint32_t> blk;
+  if ((int)tr.size() > n_top) {
+    int c_end = n_top;  // children of top nodes: entry blocks [0, c_end - n_top)
+    for (int k = 0; k < n_top; k++)
+      if (tr[k].feature >= 0) c_end = std::max(c_end, tr[k].right + 1);
+    blk.assign((size_t)16 * (c_end - n_top), 0u);
+    std::deque<std::pair<int64_t, int>> work;  // (block, tree node at its root)
+    for (int k = 0; k < n_top; k++)
+      if (tr[k].feature >= 0)
+        for (int c : {tr[k].left, tr[k].right})
+          if (c >= n_top) work.emplace_back(c - n_top, c);
+    while (!work.empty()) {
+      const auto [b, root] = work.front();
+      work.pop_front();
+      int pos[15];
+      pos[0] = root;
+      uint32_t w[16] = {};
+      for (int p = 0; p < 7; p++) {
+        const adapt_node_t &nd = tr[pos[p]];
+        if (nd.feature >= 0) {
+          const float t = round_down_f32(nd.threshold);
+          memcpy(&w[p], &t, 4);
+          w[7 + p] = (uint32_t)nd.feature;
+          pos[2 * p + 1] = nd.left;
+          pos[2 * p + 2] = nd.right;
+        } else {  // pass-through: both subtrees end in this leaf
+          pos[2 * p + 1] = pos[2 * p + 2] = pos[p];
+        }
+      }
+      for (int i = 0; i < 8; i++) {
+        const adapt_node_t &nd = tr[pos[7 + i]];
+        int32_t ref;
+        if (nd.feature < 0) {
+          ref = -1 - nd.label;
+        } else {
+          ref = (int32_t)(blk.size() / 16);
+          if (ref >= (1 << 25)) throw Error(ADAPT_E_INVALID_ARG, "tree too large for the select layout");
+          blk.resize(blk.size() + 16, 0u);
+          work.emplace_back(ref, pos[7 + i]);
+        }
+        w[7 + i] |= (uint32_t)ref << 6;
+      }
+      memcpy(&blk[(size_t)b * 16], w, sizeof(w));
+    }
+  }
+  h->d_blocks.ensure(std::max<size_t>(blk.size() * 4, 64));
+  if (!blk.empty())
+    CUDA_CHECK(cudaMemcpyAsync(h->d_blocks.p, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
@@ -1248,11 +1311,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
   }
   };  // grow_tree
 
-  if (h->kind == 0) {
-    grow_tree(nullptr);
-    h->forest.clear();
-  } else {  // random forest: T trees on bootstrap resamples of the global table (R19)
-    uint64_t lo = 0;  // this rank's first global row
+  auto shard_lo = [&]() {  // this rank's first global row
+    uint64_t lo = 0;
     if (collectives_on()) {
       DevBuf nb, allb;
       nb.ensure(8);
@@ -1265,6 +1325,94 @@ void train_region(adapt_region *h, cudaStream_t s) {
       CUDA_CHECK(cudaStreamSynchronize(s));
       for (int r = 0; r < g_ctx.rank; r++) lo += all[r];
     }
+    return lo;
+  };
+
+  if (h->kfold) {  // K-fold harness (R22): models on weighted subsets, tested on the rest
+    const auto &kf = *h->kfold;
+    if (n_total < (uint64_t)kf.K) throw Error(ADAPT_E_INSUFFICIENT_DATA, "fewer rows than K groups");
+    const uint64_t lo = shard_lo();
+    std::vector<uint64_t> bnd(kf.K + 1);
+    for (int j = 0; j <= kf.K; j++)  // ceil(j N / K): the first position of group j
+      bnd[j] = (uint64_t)(((unsigned __int128)j * n_total + kf.K - 1) / kf.K);
+    h2d(h->kbnd, bnd, s);
+    h->wplane.ensure((size_t)std::max<int64_t>(n, 1) + 64);
+    h->ksel.ensure((size_t)std::max<int64_t>(n, 1) * 4 + 16);
+    const int nb = kfold_eval_blocks();
+    h->kpart.ensure((size_t)nb * sizeof(KfoldPartial));
+    DevBuf kall;
+    kall.ensure((size_t)world * 32);
+    std::vector<KfoldPartial> part(nb);
+    std::vector<double> allv((size_t)world * 4);
+    h->kfold_trees.clear();
+    std::vector<int64_t> stats;
+    for (int sh = 0; sh < kf.shuffles; sh++)
+      for (int k = 0; k < kf.K; k++) {
+        {
+          Phase ph("kfold", s, (double)n);
+          launch_kfold_weights(kf.seed, sh, n_total, h->kbnd.as<uint64_t>(), kf.K, kf.m, k, lo, n,
+                               h->wplane.as<uint8_t>(), s);
+        }
+        grow_tree(h->wplane.as<uint8_t>());
+        stats.insert(stats.end(), h->stats.begin(), h->stats.end());
+        h->kfold_trees.push_back(h->tree);
+        upload_tree(h, s);
+        {
+          Phase ph("select", s, (double)n * (4.0 * F + 4));
+          launch_select(h->d_tree.as<DNode>(), (int)h->tree.size(), h->d_blocks.as<uint4>(), feat, n, F,
+                        h->ksel.as<int32_t>(), s);
+        }
+        if (n) {
+          Phase ph("kfold", s, (double)n * 6);
+          launch_kfold_eval(h->wplane.as<uint8_t>(), h->labels.as<uint8_t>(), h->ksel.as<int32_t>(), times,
+                            n, V, h->kpart.as<KfoldPartial>(), s);
+          CUDA_CHECK(cudaMemcpyAsync(part.data(), h->kpart.p, (size_t)nb * sizeof(KfoldPartial),
+                                     cudaMemcpyDeviceToHost, s));
+          CUDA_CHECK(cudaStreamSynchronize(s));
+        }
+        KfoldPartial mine{0, 0, 0.0, 0.0};
+        if (n)
+          for (const auto &p : part) {  // block order: deterministic
+            mine.n_test += p.n_test;
+            mine.n_correct += p.n_correct;
+            mine.t_selected += p.t_selected;
+            mine.t_best += p.t_best;
+          }
+        KfoldPartial tot = mine;
+        if (collectives_on()) {  // every rank's partial, summed in rank order
+          CUDA_CHECK(cudaMemcpyAsync(h->kpart.p, &mine, 32, cudaMemcpyHostToDevice, s));
+          comm_allgather(h->kpart.p, kall.p, 32, s, "allgather kfold results");
+          std::vector<KfoldPartial> all(world);
+          CUDA_CHECK(cudaMemcpyAsync(all.data(), kall.p, (size_t)world * 32, cudaMemcpyDeviceToHost, s));
+          CUDA_CHECK(cudaStreamSynchronize(s));
+          tot = all[0];
+          for (int r = 1; r < world; r++) {
+            tot.n_test += all[r].n_test;
+            tot.n_correct += all[r].n_correct;
+            tot.t_selected += all[r].t_selected;
+            tot.t_best += all[r].t_best;
+          }
+        }
+        adapt_kfold_result_t &o = kf.out[(size_t)sh * kf.K + k];
+        o.shuffle = sh;
+        o.fold = k;
+        o.n_nodes = (int32_t)h->tree.size();
+        o.pad_ = 0;
+        o.n_test = (int64_t)tot.n_test;
+        o.n_train = (int64_t)n_total - o.n_test;
+        o.n_correct = (int64_t)tot.n_correct;
+        o.t_selected = tot.t_selected;
+        o.t_best = tot.t_best;
+      }
+    h->stats.swap(stats);
+    return;  // the region's own model is restored by adapt_kfold
+  }
+
+  if (h->kind == 0) {
+    grow_tree(nullptr);
+    h->forest.clear();
+  } else {  // random forest: T trees on bootstrap resamples of the global table (R19)
+    const uint64_t lo = shard_lo();
     h->wcnt.ensure(16);
     h->wplane.ensure((size_t)std::max<int64_t>(n, 1) + 64);
     std::vector<std::vector<adapt_node_t>> forest;
@@ -1314,7 +1462,8 @@ int select_host_walk(adapt_region *h, const float *x) {
 
 void select_device(adapt_region *h, const float *X, int64_t m, int32_t *out, cudaStream_t s) {
   if (h->forest.empty())
-    launch_select(h->d_tree.as<DNode>(), (int)h->tree.size(), X, m, h->F, out, s);
+    launch_select(h->d_tree.as<DNode>(), (int)h->tree.size(), h->d_blocks.as<uint4>(), X, m, h->F,
+                  out, s);
   else
     launch_select_forest(h->d_forest.as<DNode>(), h->forest_nodes, h->d_roots.as<int32_t>(),
                          (int)h->forest.size(), X, m, h->F, out, s);
@@ -1707,6 +1856,59 @@ int adapt_forest_size(adapt_region_t *h, int32_t *trees) {
   });
 }
 
+int adapt_kfold(adapt_region_t *h, int K, int train_groups, int shuffles, uint64_t seed,
+                adapt_kfold_result_t *out, void *stream) {
+  return guarded([&] {
+    checked(h);
+    ensure_init();
+    if (K < 2 || K > kKfoldMaxK || train_groups < 1 || train_groups >= K || shuffles < 1 || !out)
+      throw Error(ADAPT_E_INVALID_ARG, "bad K-fold spec");
+    if (h->kind != 0) throw Error(ADAPT_E_USAGE, "adapt_kfold needs a dtree region");
+    cudaStream_t s = (cudaStream_t)stream;
+    // the region's own model survives the harness
+    std::vector<adapt_node_t> prev_tree = h->tree;
+    std::vector<int64_t> prev_stats = h->stats;
+    const bool prev_trained = h->trained;
+    const int64_t prev_n = h->trained_n;
+    const adapt_region::KfoldSpec spec{K, train_groups, shuffles, seed, out};
+    auto restore = [&]() {
+      h->kfold = nullptr;
+      h->tree.swap(prev_tree);
+      h->stats.swap(prev_stats);
+      h->trained = prev_trained;
+      h->trained_n = prev_n;
+      if (h->have_table && h->d_feat != h->own_feat.as<float>()) {
+        h->d_feat = nullptr;  // borrowed pointers are released when the call returns
+        h->d_times = nullptr;
+        h->have_table = false;
+      }
+    };
+    h->kfold = &spec;
+    try {
+      train_region(h, s);
+    } catch (...) {
+      restore();
+      throw;
+    }
+    restore();
+    if (h->trained && !h->tree.empty()) upload_tree(h, s);
+  });
+}
+
+int adapt_get_kfold_tree(adapt_region_t *h, int32_t model, adapt_node_t *out, int32_t cap,
+                         int32_t *n_nodes) {
+  return guarded([&] {
+    checked(h);
+    if (!n_nodes) throw Error(ADAPT_E_INVALID_ARG, "null n_nodes");
+    if (model < 0 || model >= (int32_t)h->kfold_trees.size())
+      throw Error(ADAPT_E_INVALID_ARG, "no such K-fold model");
+    const auto &tr = h->kfold_trees[model];
+    *n_nodes = (int32_t)tr.size();
+    if (!out || cap < (int32_t)tr.size()) throw Error(ADAPT_E_INVALID_ARG, "capacity too small");
+    memcpy(out, tr.data(), tr.size() * sizeof(adapt_node_t));
+  });
+}
+
 int adapt_get_forest_tree(adapt_region_t *h, int32_t t, adapt_node_t *out, int32_t cap,
                           int32_t *n_nodes) {
   return guarded([&] {
@@ -1728,8 +1930,14 @@ int adapt_set_tree(adapt_region_t *h, const adapt_node_t *nodes, int32_t n_nodes
     ensure_init();
     if (!nodes || n_nodes < 1) throw Error(ADAPT_E_INVALID_ARG, "empty tree");
     if (n_nodes >= (1 << 25)) throw Error(ADAPT_E_INVALID_ARG, "tree too large");
+    std::vector<uint8_t> has_parent(n_nodes, 0);  // a tree: one parent per node
     for (int32_t k = 0; k < n_nodes; k++) {
       const adapt_node_t &nd = nodes[k];
+      if (nd.feature >= 0 && nd.left > k && nd.right == nd.left + 1 && nd.right < n_nodes) {
+        if (has_parent[nd.left] || has_parent[nd.right])
+          throw Error(ADAPT_E_INVALID_ARG, "node with two parents at " + std::to_string(nd.left));
+        has_parent[nd.left] = has_parent[nd.right] = 1;
+      }
       if (nd.feature >= 0) {
         if (nd.feature >= h->F || nd.left <= k || nd.right != nd.left + 1 || nd.right >= n_nodes ||
             !std::isfinite(nd.threshold))

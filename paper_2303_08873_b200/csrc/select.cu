@@ -5,8 +5,10 @@
 // The device tree is a BFS array of 8-byte nodes; the threshold is stored as
 // the largest float32 <= the double threshold, which makes the float compare
 // exact (V:A5).  The first kTopNodes nodes (the top levels every walk visits;
-// a whole depth-12 tree) sit in shared memory, deeper ones are read through
-// L1/L2.  Every warp owns its tiles of 64 vectors (no block barriers): the
+// a whole depth-12 tree) sit in shared memory; below them the tree is stored
+// as 64-byte blocks of 3 levels (common.h), read with four independent
+// 16-byte loads, so a depth-16 walk pays one L2 round trip below the top
+// instead of four dependent ones.  Every warp owns its tiles of 64 vectors (no block barriers): the
 // coalesced 16-byte loads of the next tile sit in registers while the lanes
 // walk the current one out of the warp's odd-stride shared-memory tile, two
 // independent walks per lane interleaved to hide the dependent smem latency.
@@ -23,19 +25,43 @@ constexpr int kSelThreads = 1024;  // one CTA per SM: one smem copy of the tree
 #endif
 constexpr int kSelChains = ADAPT_SEL_CHAINS;  // vectors walked at once per lane
 constexpr int kAnyThreads = 256;   // generic-F kernel
-constexpr int kTopNodes = 8191;    // 64 KB
+constexpr int kTopNodes = kSelTopNodes;  // 64 KB
 
-__device__ __forceinline__ DNode ldg_node(const DNode *p) {
-  const int2 v = __ldg(reinterpret_cast<const int2 *>(p));
-  DNode d;
-  d.thr = __int_as_float(v.x);
-  d.meta = v.y;
-  return d;
+// one bottom block (common.h layout) walked in registers: 3 levels, returns
+// the next block (>= 0) or -1 - label
+__device__ __forceinline__ int walk_block(const uint4 (&w)[4], const float *x) {
+  const float t0 = __uint_as_float(w[0].x);
+  const bool g0 = !(x[w[1].w & 63] <= t0);  // NaN -> right (R8)
+  const float t1 = __uint_as_float(g0 ? w[0].z : w[0].y);
+  const bool g1 = !(x[(g0 ? w[2].y : w[2].x) & 63] <= t1);
+  const uint32_t tw = g0 ? (g1 ? w[1].z : w[1].y) : (g1 ? w[1].x : w[0].w);
+  const uint32_t fw = g0 ? (g1 ? w[3].y : w[3].x) : (g1 ? w[2].w : w[2].z);
+  const bool g2 = !(x[fw & 63] <= __uint_as_float(tw));
+  // leaf edges i = 4 g0 + 2 g1 + g2 are words 7..14
+  uint32_t r;
+  if (g0)
+    r = g1 ? (g2 ? w[3].z : w[3].y) : (g2 ? w[3].x : w[2].w);
+  else
+    r = g1 ? (g2 ? w[2].z : w[2].y) : (g2 ? w[2].x : w[1].w);
+  return (int32_t)r >> 6;
+}
+
+// two 256-bit loads (LDG.E.256 on sm_100a): each lane touches 2 sectors with 2
+// requests, half the L1 request count of four 128-bit loads
+__device__ __forceinline__ void load_block(const uint4 *__restrict__ blocks, int b, uint4 (&w)[4]) {
+  const uint4 *p = blocks + 4 * (int64_t)b;
+#pragma unroll
+  for (int i = 0; i < 4; i += 2)
+    asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[i].x), "=r"(w[i].y), "=r"(w[i].z), "=r"(w[i].w), "=r"(w[i + 1].x),
+                   "=r"(w[i + 1].y), "=r"(w[i + 1].z), "=r"(w[i + 1].w)
+                 : "l"(p + i));
 }
 
 template <int F>
 __global__ void __launch_bounds__(kSelThreads, 1)
-    select_kernel(const DNode *__restrict__ gtree, int n_top, const float *__restrict__ X,
+    select_kernel(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
+                  const float *__restrict__ X,
                   int64_t m, int32_t *__restrict__ out) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int kStride = F | 1;                   // odd row stride of a warp's tile
@@ -82,35 +108,51 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     // kSelChains independent walks per lane, interleaved for latency hiding
     const float *x[kSelChains];
     DNode nd[kSelChains];
+    int ref[kSelChains];  // -1 - label, or the bottom block the walk continues in
     bool live[kSelChains];
 #pragma unroll
     for (int c = 0; c < kSelChains; c++) {
       x[c] = sx + (lane + 32 * c) * kStride;
       nd[c] = st[0];
+      ref[c] = nd[c].meta;
       live[c] = v0 + lane + 32 * c < m;
     }
     bool any = true;
-    while (any) {
+    while (any) {  // the shared-memory top
       any = false;
 #pragma unroll
       for (int c = 0; c < kSelChains; c++) {
         if (nd[c].meta >= 0) {
           const float xv = x[c][nd[c].meta & 63];
           const int k = (nd[c].meta >> 6) + (xv <= nd[c].thr ? 0 : 1);
-          nd[c] = k < n_top ? st[k] : ldg_node(gtree + k);
-          any |= nd[c].meta >= 0;
+          if (k < n_top) {
+            nd[c] = st[k];
+            ref[c] = nd[c].meta;
+            any |= nd[c].meta >= 0;
+          } else {
+            ref[c] = k - n_top;
+            nd[c].meta = -1;
+          }
         }
       }
     }
 #pragma unroll
+    for (int c = 0; c < kSelChains; c++)  // bottom blocks (the prefetched tile holds
+      while (ref[c] >= 0) {               // registers: one chain's block at a time)
+        uint4 w[4];
+        load_block(blocks, ref[c], w);
+        ref[c] = walk_block(w, x[c]);
+      }
+#pragma unroll
     for (int c = 0; c < kSelChains; c++)
-      if (live[c]) __stcs(out + v0 + lane + 32 * c, -1 - nd[c].meta);
+      if (live[c]) __stcs(out + v0 + lane + 32 * c, -1 - ref[c]);
   }
 }
 
 // generic F (not a multiple of 4, or an unaligned X): scalar staging
 __global__ void __launch_bounds__(kAnyThreads, 1)
-    select_kernel_any(const DNode *__restrict__ gtree, int n_top, const float *__restrict__ X,
+    select_kernel_any(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
+                      const float *__restrict__ X,
                       int64_t m, int F, int32_t *__restrict__ out) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int stride = F | 1;
@@ -129,19 +171,31 @@ __global__ void __launch_bounds__(kAnyThreads, 1)
     if (t < rows) {
       const float *x = sx + t * stride;
       DNode nd = st[0];
+      int ref = nd.meta;
       while (nd.meta >= 0) {
         const int k = (nd.meta >> 6) + (x[nd.meta & 63] <= nd.thr ? 0 : 1);
-        nd = k < n_top ? st[k] : ldg_node(gtree + k);
+        if (k < n_top) {
+          nd = st[k];
+          ref = nd.meta;
+        } else {
+          ref = k - n_top;
+          break;
+        }
       }
-      __stcs(out + v0 + t, -1 - nd.meta);
+      while (ref >= 0) {
+        uint4 w[4];
+        load_block(blocks, ref, w);
+        ref = walk_block(w, x);
+      }
+      __stcs(out + v0 + t, -1 - ref);
     }
   }
 }
 
 }  // namespace
 
-void launch_select(const DNode *tree, int n_nodes, const float *X, int64_t m, int F, int32_t *out,
-                   cudaStream_t s) {
+void launch_select(const DNode *tree, int n_nodes, const uint4 *blocks, const float *X, int64_t m,
+                   int F, int32_t *out, cudaStream_t s) {
   if (m == 0) return;
   const int n_top = std::min(n_nodes, kTopNodes);
   int dev = 0, sms = 148;
@@ -157,7 +211,7 @@ void launch_select(const DNode *tree, int n_nodes, const float *X, int64_t m, in
   case FF: {                                                                                   \
     const size_t smem = tree_b + (size_t)kSelThreads * kSelChains * (FF | 1) * 4;              \
     smem_limit(select_kernel<FF>, smem);   \
-    select_kernel<FF><<<vgrid, kSelThreads, smem, s>>>(tree, n_top, X, m, out);                \
+    select_kernel<FF><<<vgrid, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, out);                \
     break;                                                                                     \
   }
     CASE(4) CASE(8) CASE(12) CASE(16)
@@ -167,7 +221,7 @@ void launch_select(const DNode *tree, int n_nodes, const float *X, int64_t m, in
       const int64_t tiles = (m + kAnyThreads - 1) / kAnyThreads;
       const int grid = (int)std::min<int64_t>(tiles, sms);
       smem_limit(select_kernel_any, smem);
-      select_kernel_any<<<grid, kAnyThreads, smem, s>>>(tree, n_top, X, m, F, out);
+      select_kernel_any<<<grid, kAnyThreads, smem, s>>>(tree, n_top, blocks, X, m, F, out);
     }
   }
   CUDA_CHECK(cudaGetLastError());

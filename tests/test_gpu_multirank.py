@@ -70,6 +70,11 @@ def _worker(rank, world, port, job, q):
         ad.adapt_select_batch(h, dX, n, sel, s)
         torch.cuda.synchronize()
         out["select"] = sel.cpu().numpy()
+        if "kfold" in job:  # the K-fold harness is collective too (R22: global row ids)
+            K, m, S, seed = job["kfold"]
+            ad.adapt_record_table(h, dX, torch.from_numpy(Ts).cuda(), n, True, s)
+            out["kfold"] = ad.adapt_kfold(h, K, m, S, seed, s)
+            out["kfold_trees"] = [ad.adapt_get_kfold_tree(h, i) for i in range(S * K)]
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -153,3 +158,20 @@ def test_errors_fail_every_rank():
     X[300:, 0] = 100 + np.arange(300, dtype=np.float32) % 200    # rank 1: 100..299
     res = _run(2, {"X": X, "T": T, "D": 4})
     assert [res[r].get("error") for r in range(2)] == [-7, -7]
+
+
+def test_p_invariant_kfold():
+    # every rank returns the single-GPU K-fold results: the models' trees are the
+    # oracle's CART on the fold's rows of the WHOLE table, counts summed over ranks
+    X, T = synth.generate("C3", 0, 30_001)
+    K, m, S, seed, D = 4, 2, 2, 9, 6
+    res = _run(2, {"X": X, "T": T, "D": D, "kfold": (K, m, S, seed)})
+    ref, trees = oracle.kfold(X, T, D, K, m, S, seed)
+    for r, o in sorted(res.items()):
+        assert "error" not in o
+        for i, (got, want) in enumerate(zip(o["kfold"], ref)):
+            for k in ("n_train", "n_test", "n_correct", "n_nodes"):
+                assert got[k] == want[k], (r, i, k)
+            np.testing.assert_allclose(got["t_selected"], want["t_selected"], rtol=len(X) * 2.0**-52)
+            np.testing.assert_allclose(got["t_best"], want["t_best"], rtol=len(X) * 2.0**-52)
+            assert o["kfold_trees"][i].tobytes() == trees[i].tobytes(), (r, i)

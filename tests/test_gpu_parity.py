@@ -213,6 +213,62 @@ def test_select_synthetic_complete_tree(depth):
     ad.adapt_region_destroy(h)
 
 
+@pytest.mark.parametrize("F", [16, 5])
+def test_select_deep_irregular_trees(F):
+    # trained trees deeper than the shared-memory top (> 8191 nodes, leaves at
+    # every depth): the walk continues in the 3-level bottom blocks, whose
+    # pass-through nodes stand in for leaves above the block bottom; F=5 runs
+    # the generic-F kernel
+    rng = np.random.default_rng(11 + F)
+    n = 60000
+    X = rng.choice(np.arange(256, dtype=np.float32) * 0.5, size=(n, F)).astype(np.float32)
+    T = rng.random((n, 9)).astype(np.float32)
+    T[X[:, 0] < 20, 0] = 0  # a pure region: leaves high up the tree
+    h = _train(X, T, 22)
+    y = oracle.labels(T)
+    ref = oracle.train(X, y, 9, 22)
+    got = ad.adapt_get_tree(h)
+    assert_tree_equal(got, ref)
+    assert len(got) > 8191 and got["depth"].max() > 16
+    Xs = np.concatenate([X, rng.choice(np.arange(260, dtype=np.float32) * 0.5 - 1, size=(20001, F))
+                         .astype(np.float32)])
+    Xs[::31, F - 1] = np.nan  # NaN goes right (R8)
+    out = torch.empty(len(Xs), dtype=torch.int32, device=DEV)
+    ad.adapt_select_batch(h, torch.from_numpy(Xs).to(DEV), len(Xs), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.select(ref, Xs))
+    ad.adapt_region_destroy(h)
+
+
+def test_select_set_tree_chain():
+    # a depth-24 caterpillar given through adapt_set_tree (BFS-valid, one child a
+    # leaf at every level) and a tree with two parents for a node (rejected)
+    F, V, D = 4, 7, 24
+    nodes = np.zeros(2 * D + 1, oracle.NODE_DTYPE)
+    for d in range(D):
+        k = 2 * d  # internal node of level d; its leaf sibling is 2d - 1
+        nodes[k] = (d % F, k + 1, k + 2, 0, d, 0, 70.0 + d, 0, 0.0)
+        nodes[k + 1] = (-1, -1, -1, d % V, d + 1, 0, 0.0, 0, 0.0)
+    nodes[2 * D] = (-1, -1, -1, 3, D, 0, 0.0, 0, 0.0)
+    h = _region(F, V, D)
+    ad.adapt_set_tree(h, nodes)
+    rng = np.random.default_rng(2)
+    X = rng.uniform(70, 105, size=(50000, F)).astype(np.float32)
+    out = torch.empty(len(X), dtype=torch.int32, device=DEV)
+    ad.adapt_select_batch(h, torch.from_numpy(X).to(DEV), len(X), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.select(nodes, X))
+    bad = np.zeros(5, oracle.NODE_DTYPE)  # nodes 1 and 2 both have children 3, 4
+    bad[0] = (0, 1, 2, 0, 0, 0, 1.0, 0, 0.0)
+    bad[1] = (0, 3, 4, 0, 1, 0, 0.5, 0, 0.0)
+    bad[2] = (0, 3, 4, 0, 1, 0, 1.5, 0, 0.0)
+    bad[3] = (-1, -1, -1, 1, 2, 0, 0.0, 0, 0.0)
+    bad[4] = (-1, -1, -1, 2, 2, 0, 0.0, 0, 0.0)
+    with pytest.raises(ad.AdaptError):
+        ad.adapt_set_tree(h, bad)
+    ad.adapt_region_destroy(h)
+
+
 def test_errors():
     s = torch.cuda.current_stream()
     h = _region(1, 2, 2)
