@@ -272,3 +272,56 @@ def kfold(X: np.ndarray, T: np.ndarray, D: int, K: int, m: int, shuffles: int, s
                         "t_best": math.fsum(float(T[i, y[i]]) for i in test)})
             trees.append(tree)
     return res, trees
+
+
+# ---- lossy quantile bins for > 256 distinct values (R23) ----
+def quantizer(X: np.ndarray, bins: int = 256):
+    """Per feature with more than `bins` distinct values (global, -0 -> +0): the
+    sorted distinct values u (np.unique as the sort primitive), bin b = distinct
+    indices [floor(b D / bins), floor((b+1) D / bins)), lower bounds lb_b =
+    u[e_b] and prev_b = u[e_b - 1] (the largest value of bin b-1, b >= 1).
+    Returns {f: (lb, prev)}; features with <= bins values are absent (exact)."""
+    Xc = canon_features(X)
+    out = {}
+    for f in range(Xc.shape[1]):
+        u = np.unique(Xc[:, f])
+        D = len(u)
+        if D <= bins:
+            continue
+        e = (np.arange(bins, dtype=np.int64) * D) // bins
+        prev = np.concatenate([[u[0]], u[e[1:] - 1]]).astype(np.float32)
+        out[f] = (u[e].astype(np.float32), prev)
+    return out
+
+
+def quantize(X: np.ndarray, q: dict) -> np.ndarray:
+    """x -> lb_{q(x)}, q(x) = #{b : lb_b <= x} - 1, on the quantised features."""
+    Xq = canon_features(X).copy()
+    for f, (lb, _) in q.items():
+        Xq[:, f] = lb[np.searchsorted(lb, Xq[:, f], side="right") - 1]
+    return Xq
+
+
+def train_quantile(X: np.ndarray, y: np.ndarray, C: int, D: int) -> np.ndarray:
+    """R23: the exact CART (train) of the quantised table; a split of a quantised
+    feature f between the node's bins a < b' then reports the raw threshold
+    ((double)prev_{a+1} + (double)lb_{a+1}) / 2, a = the largest quantised value
+    of the node's rows that goes left (rows routed through the tree by Xq)."""
+    q = quantizer(X)
+    Xq = quantize(X, q)
+    tree = train(Xq, y, C, D)
+    node_rows = {0: np.arange(len(X))}
+    for k in range(len(tree)):
+        rows = node_rows.pop(k, np.arange(0))
+        f = int(tree["feature"][k])
+        if f < 0:
+            continue
+        v = Xq[rows, f].astype(np.float64)
+        go_left = v <= tree["threshold"][k]
+        node_rows[int(tree["left"][k])] = rows[go_left]
+        node_rows[int(tree["right"][k])] = rows[~go_left]
+        if f in q:
+            lb, prev = q[f]
+            a = int(np.searchsorted(lb, v[go_left].max(), side="left"))  # lb[a] == that value
+            tree["threshold"][k] = (float(prev[a + 1]) + float(lb[a + 1])) / 2
+    return tree
