@@ -191,6 +191,50 @@ def bench_c5(args, ad, adist, torch, dev, stream, rank: int, world: int, peak: f
     return res
 
 
+def bench_kfold(args, ad, adist, torch, dev, stream, rank: int, world: int):
+    """The paper's evaluation protocol as a GPU workload: K = 4 groups,
+    10 shuffles, m = 1/2/3 training groups (Adaptive-25/50/75) = 120 depth-D
+    models on the C3 table (1e6 rows, sharded), each tested on its held-out rows."""
+    cfg = synth.CONFIGS["C3"]
+    N = cfg.N
+    lo, hi = adist.shard_bounds(N, rank, world)
+    flat, off = cfg.grid_table
+    g, o = torch.from_numpy(flat).to(dev), torch.from_numpy(off).to(dev)
+    X = torch.empty((hi - lo, cfg.F), dtype=torch.float32, device=dev)
+    T = torch.empty((hi - lo, cfg.V), dtype=torch.float32, device=dev)
+    synth.generate_device(cfg, lo, hi - lo, X.data_ptr(), T.data_ptr(), g.data_ptr(), o.data_ptr(),
+                          stream.cuda_stream)
+    h = ad.adapt_region_create("bench_kfold", cfg.F, cfg.V, f"dtree,depth={cfg.D}", 0)
+
+    def run():
+        out = []
+        for m in (1, 2, 3):
+            ad.adapt_record_table(h, X, T, hi - lo, True, stream)
+            out.append(ad.adapt_kfold(h, 4, m, 10, 1, stream))
+        return out
+
+    run()  # warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    res = run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = adist.max_over_ranks(e0.elapsed_time(e1), dev)
+    ad.adapt_region_destroy(h)
+    acc = {f"adaptive_{25 * m}": float(res[m - 1]["n_correct"].sum() / res[m - 1]["n_test"].sum())
+           for m in (1, 2, 3)}
+    slow = {f"adaptive_{25 * m}": float(res[m - 1]["t_selected"].sum() / res[m - 1]["t_best"].sum())
+            for m in (1, 2, 3)}
+    return {"workload": "C3 table (1e6 rows, 8 features, 6 variants), K=4 groups x 10 shuffles x "
+                        "m=1/2/3 training groups = 120 depth-12 models, each tested on its held-out rows",
+            "models": 120, "ms": ms, "models_per_s": 120 / (ms / 1e3),
+            "model_rows_per_s": sum(int(r["n_train"].sum()) for r in res) / (ms / 1e3),
+            "test_accuracy": acc, "time_selected_over_best": slow}
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
@@ -237,6 +281,7 @@ def main():
     ap.add_argument("--c5-vectors", type=int, default=1_000_000_000, help="C5 batch size (SURVEY §8(d))")
     ap.add_argument("--c5-train-rows", type=int, default=10_000_000)
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-kfold", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -367,6 +412,9 @@ def main():
         del X, T, out
         torch.cuda.empty_cache()
         c5 = bench_c5(args, ad, adist, torch, dev, stream, rank, world, peak)
+    kfold = None
+    if not args.no_kfold and args.config == "C4":
+        kfold = bench_kfold(args, ad, adist, torch, dev, stream, rank, world)
 
     if rank != 0:
         if world > 1:
@@ -427,6 +475,7 @@ def main():
         "cpu_baseline": cpu,
         "record_path": rec,
         "select_c5": c5,
+        "kfold": kfold,
         "phase_ms_per_step": step_ms_phases,
         "tree_nodes": int(len(tree)),
         "levels": levels,

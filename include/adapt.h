@@ -122,6 +122,11 @@ const char *adapt_version(void);
  * [1,64]) of depth D (default 2), each trained on a bootstrap resample of the
  * table drawn from a counter RNG keyed by (seed, tree) (R19, default seed 0);
  * selection = majority vote, ties -> lowest variant (R20).
+ * Lossy bins (DESIGN R23): ",bins=quantile" on a dtree or
+ * rfc spec quantises every feature with more than 256 distinct values (over
+ * all ranks) into 256 bins of equal numbers of distinct values; splits on it
+ * report raw thresholds at the bin cut points.  Default ",bins=exact": such a
+ * table fails with ADAPT_E_TOO_MANY_DISTINCT (R14).
  * min_train_data <= 0 -> V.
  * Same id and same spec -> the same handle; same id with a different
  * spec -> ADAPT_E_SPEC_MISMATCH. */

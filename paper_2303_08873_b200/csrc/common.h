@@ -210,6 +210,15 @@ int forest_max_trees();
 void launch_select_forest(const DNode *nodes, int n_nodes, const int32_t *roots, int T,
                           const float *X, int64_t m, int F, int32_t *out, cudaStream_t s);
 
+// ---- quantile.cu: lossy binning of features with > 256 distinct values (R23) ----
+size_t sort_unique_temp_bytes(int64_t n);
+void launch_column_keys(const float *X, int64_t n, int F, int f, uint32_t *keys, cudaStream_t s);
+void sort_unique_keys(const uint32_t *keys, int64_t n, uint32_t *sorted, uint32_t *out, int *d_count,
+                      void *temp, size_t temp_bytes, cudaStream_t s);
+void launch_edges(const uint32_t *ukeys, int64_t D, float *lb, float *prev, cudaStream_t s);
+void launch_quantize(const float *X, int64_t n, int F, uint64_t qmask, const float *lb, float *Xq,
+                     cudaStream_t s);
+
 // ---- kernel launchers (kfold.cu): the K-fold harness ----
 constexpr int kKfoldMaxK = 64;
 struct KfoldPartial {

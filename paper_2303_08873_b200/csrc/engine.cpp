@@ -372,6 +372,12 @@ struct adapt_region {
   std::vector<int32_t> nval;    // [F]
   std::vector<adapt_node_t> tree;
   adapt::DevBuf d_tree, d_blocks;  // device tree: DNode top + bottom blocks (select.cu)
+  // lossy quantile bins (quantile.cu, R23): features in qmask were quantised;
+  // qprev[f][b] = the largest distinct value of bin b-1 (threshold midpoints)
+  bool quantile = false;
+  uint64_t qmask = 0;
+  std::vector<float> qprev;
+  adapt::DevBuf qfeat, qlb, qprevd;
   // K-fold harness (kfold.cu): set for the duration of adapt_kfold
   struct KfoldSpec {
     int K, m, shuffles;
@@ -407,7 +413,8 @@ std::map<std::string, std::unique_ptr<adapt_region>> g_regions;
 // "rfc,trees=T,depth=D,seed=S" / "RandomForest[...]" ("model_type(rfc,
 // 10, 4)": trees, then depth).  Defaults: dtree depth 2; rfc 10 trees
 // of depth 2, seed 0 (R21).
-int parse_params(const char *p, int *depth, int *kind, int *trees, uint64_t *seed) {
+int parse_params(const char *p, int *depth, int *kind, int *trees, uint64_t *seed, bool *quantile) {
+  *quantile = false;
   *depth = 2;
   *kind = 0;
   *trees = 1;
@@ -446,6 +453,12 @@ int parse_params(const char *p, int *depth, int *kind, int *trees, uint64_t *see
     if (t.empty()) continue;
     if (t.rfind("explore=", 0) == 0) {
       if (t != "explore=RoundRobin") throw Error(ADAPT_E_INVALID_ARG, "only explore=RoundRobin");
+      continue;
+    }
+    if (t.rfind("bins=", 0) == 0) {  // R23: lossy quantile bins for > 256 distinct values
+      if (t != "bins=quantile" && t != "bins=exact")
+        throw Error(ADAPT_E_INVALID_ARG, "bins must be 'exact' or 'quantile'");
+      *quantile = t == "bins=quantile";
       continue;
     }
     long long d;
@@ -725,7 +738,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
   h->dnval.ensure((size_t)F * 4);
   // error flags, summed over ranks so that all ranks fail (or retry) together
   uint32_t *hs = h->hsmall.as<uint32_t>();
-  auto check_flags = [&]() -> uint32_t {
+  auto check_flags = [&](bool allow_too_many = false) -> uint32_t {
     DevBuf fl;
     fl.ensure(32);
     CUDA_CHECK(cudaMemcpyAsync(hs, h->flags.p, 4, cudaMemcpyDeviceToHost, s));
@@ -741,7 +754,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
     if (bits[0]) throw Error(ADAPT_E_BAD_VALUE, "NaN or Inf feature value");
     if (bits[1]) throw Error(ADAPT_E_BAD_VALUE, "NaN time");
     if (bits[2]) throw Error(ADAPT_E_BAD_VALUE, "row with every variant unmeasured (+inf)");
-    if (bits[3]) throw Error(ADAPT_E_TOO_MANY_DISTINCT, "a feature has more than 256 distinct values");
+    if (bits[3] && !allow_too_many)
+      throw Error(ADAPT_E_TOO_MANY_DISTINCT, "a feature has more than 256 distinct values");
     uint32_t m = 0;
     for (int b = 0; b < 6; b++) m |= (bits[b] ? 1u : 0u) << b;
     return m;
@@ -753,6 +767,95 @@ void train_region(adapt_region *h, cudaStream_t s) {
   // exact ones either way, typically for a 1% read.
   constexpr int64_t kSampleChunk = 1 << 15, kSampleChunks = 32;
   const bool sampled = n > 4 * kSampleChunk * kSampleChunks;
+  h->qmask = 0;
+  // R23 (bins=quantile): the features with > 256 distinct values over all ranks
+  // are replaced by their quantised copies (quantile.cu), then ingest restarts
+  auto quantize_features = [&]() {
+    std::vector<int32_t> nv(F), ac((size_t)world * F);
+    CUDA_CHECK(cudaMemcpyAsync(nv.data(), h->dnval.p, (size_t)F * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(ac.data(), h->acnt.p, (size_t)world * F * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    uint64_t qm = 0;
+    for (int f = 0; f < F; f++) {
+      bool over = nv[f] > kMaxBins;
+      for (int p = 0; p < world; p++) over |= ac[(size_t)p * F + f] > kMaxBins;
+      if (over) qm |= 1ull << f;
+    }
+    h->qlb.ensure((size_t)F * kMaxBins * 4);
+    h->qprevd.ensure((size_t)F * kMaxBins * 4);
+    CUDA_CHECK(cudaMemsetAsync(h->qlb.p, 0, (size_t)F * kMaxBins * 4, s));
+    CUDA_CHECK(cudaMemsetAsync(h->qprevd.p, 0, (size_t)F * kMaxBins * 4, s));
+    DevBuf keys, sorted, uniq, dcnt, temp, cnt8, all8, gath;
+    const int64_t nn = std::max<int64_t>(n, 1);
+    keys.ensure((size_t)nn * 4);
+    sorted.ensure((size_t)nn * 4);
+    uniq.ensure((size_t)nn * 4);
+    dcnt.ensure(16);
+    cnt8.ensure(8);
+    all8.ensure((size_t)world * 8);
+    for (int f = 0; f < F; f++) {
+      if (!((qm >> f) & 1)) continue;
+      Phase ph("quantile", s, (double)n * 4.0);
+      size_t tb = sort_unique_temp_bytes(nn);
+      temp.ensure(tb);
+      int c = 0;
+      if (n) {
+        launch_column_keys(feat, n, F, f, keys.as<uint32_t>(), s);
+        sort_unique_keys(keys.as<uint32_t>(), n, sorted.as<uint32_t>(), uniq.as<uint32_t>(), dcnt.as<int>(),
+                         temp.p, tb, s);
+        CUDA_CHECK(cudaMemcpyAsync(&c, dcnt.p, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+      }
+      const uint32_t *u = uniq.as<uint32_t>();
+      int64_t D = c;
+      if (collectives_on()) {  // union of the ranks' sorted distinct keys (padded all-gather)
+        const uint64_t mine = (uint64_t)c;
+        CUDA_CHECK(cudaMemcpyAsync(cnt8.p, &mine, 8, cudaMemcpyHostToDevice, s));
+        comm_allgather(cnt8.p, all8.p, 8, s, "allgather distinct counts");
+        std::vector<uint64_t> cs(world);
+        CUDA_CHECK(cudaMemcpyAsync(cs.data(), all8.p, (size_t)world * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        const int64_t mx = std::max<int64_t>(1, (int64_t)*std::max_element(cs.begin(), cs.end()));
+        DevBuf send, recv, rs, ru;
+        send.ensure((size_t)mx * 4);
+        recv.ensure((size_t)world * mx * 4);
+        rs.ensure((size_t)world * mx * 4);
+        ru.ensure((size_t)world * mx * 4);
+        CUDA_CHECK(cudaMemsetAsync(send.p, 0xFF, (size_t)mx * 4, s));  // pad: no finite key
+        if (c) CUDA_CHECK(cudaMemcpyAsync(send.p, uniq.p, (size_t)c * 4, cudaMemcpyDeviceToDevice, s));
+        comm_allgather(send.p, recv.p, (size_t)mx * 4, s, "allgather distinct keys");
+        tb = sort_unique_temp_bytes((int64_t)world * mx);
+        temp.ensure(tb);
+        sort_unique_keys(recv.as<uint32_t>(), (int64_t)world * mx, rs.as<uint32_t>(), ru.as<uint32_t>(),
+                         dcnt.as<int>(), temp.p, tb, s);
+        uint32_t last = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&c, dcnt.p, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        CUDA_CHECK(cudaMemcpyAsync(&last, ru.as<uint32_t>() + c - 1, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        D = c - (last == 0xFFFFFFFFu ? 1 : 0);
+        gath.ensure((size_t)std::max<int64_t>(D, 1) * 4);
+        CUDA_CHECK(cudaMemcpyAsync(gath.p, ru.p, (size_t)D * 4, cudaMemcpyDeviceToDevice, s));
+        u = gath.as<uint32_t>();
+        launch_edges(u, D, h->qlb.as<float>() + (size_t)f * kMaxBins,
+                     h->qprevd.as<float>() + (size_t)f * kMaxBins, s);
+        CUDA_CHECK(cudaStreamSynchronize(s));  // the local buffers die here
+        continue;
+      }
+      launch_edges(u, D, h->qlb.as<float>() + (size_t)f * kMaxBins,
+                   h->qprevd.as<float>() + (size_t)f * kMaxBins, s);
+    }
+    h->qprev.assign((size_t)F * kMaxBins, 0.f);
+    CUDA_CHECK(cudaMemcpyAsync(h->qprev.data(), h->qprevd.p, (size_t)F * kMaxBins * 4, cudaMemcpyDeviceToHost, s));
+    h->qfeat.ensure((size_t)std::max<int64_t>(n, 1) * F * 4);
+    {
+      Phase ph("quantile", s, (double)n * 8.0 * F);
+      launch_quantize(feat, n, F, qm, h->qlb.as<float>(), h->qfeat.as<float>(), s);
+    }
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    h->qmask = qm;
+    feat = h->qfeat.as<float>();
+  };
   for (int attempt = 0;; attempt++) {
     CUDA_CHECK(cudaMemsetAsync(h->gkey.p, 0xFF, (size_t)F * kGSlots * 4, s));
     CUDA_CHECK(cudaMemsetAsync(h->gcount.p, 0, (size_t)F * 4, s));
@@ -781,7 +884,11 @@ void train_region(adapt_region *h, cudaStream_t s) {
       launch_merge_values(h->avals.as<float>(), h->acnt.as<int32_t>(), world, F, h->dval.as<float>(),
                           h->dnval.as<int32_t>(), h->flags.as<uint32_t>(), s);
     }
-    check_flags();
+    if (check_flags(h->quantile && h->qmask == 0) & kFlagTooMany) {
+      quantize_features();
+      attempt = -1;  // ingest the quantised table from the start (sampled discovery again)
+      continue;
+    }
     // value tables to the host; per-feature perfect hashes value -> rank for the bin pass
     h->val.assign((size_t)F * kMaxBins, 0.f);
     h->nval.assign(F, 0);
@@ -1234,8 +1341,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
       const int f = nr->feat;
       adapt_node_t &nd = h->tree[fn.tree_idx];
       nd.feature = f;
-      nd.threshold = ((double)h->val[f * kMaxBins + nr->b_lo] +
-                      (double)h->val[f * kMaxBins + nr->b_hi]) / 2;  // R7
+      if ((h->qmask >> f) & 1)  // R23: between the bins b_lo and b_lo + 1 of the quantiser
+        nd.threshold = ((double)h->qprev[f * kMaxBins + nr->b_lo + 1] +
+                        (double)h->val[f * kMaxBins + nr->b_lo + 1]) / 2;
+      else
+        nd.threshold = ((double)h->val[f * kMaxBins + nr->b_lo] +
+                        (double)h->val[f * kMaxBins + nr->b_hi]) / 2;  // R7
       const int32_t li = (int32_t)h->tree.size();
       nd.left = li;
       nd.right = li + 1;
@@ -1609,13 +1720,14 @@ int adapt_region_create(const char *id, int num_features, int num_variants,
     int depth = 2;
     int kind = 0, trees = 1;
     uint64_t seed = 0;
-    parse_params(model_params, &depth, &kind, &trees, &seed);
+    bool quantile = false;
+    parse_params(model_params, &depth, &kind, &trees, &seed, &quantile);
     const int mtd = min_train_data > 0 ? min_train_data : num_variants;
     auto it = g_regions.find(id);
     if (it != g_regions.end()) {
       adapt_region *h = it->second.get();
       if (h->F != num_features || h->V != num_variants || h->D != depth || h->min_train != mtd ||
-          h->kind != kind || h->T != trees || h->seed != seed)
+          h->kind != kind || h->T != trees || h->seed != seed || h->quantile != quantile)
         throw Error(ADAPT_E_SPEC_MISMATCH, std::string("region '") + id + "' exists with another spec");
       *out = h;
       return;
@@ -1628,6 +1740,7 @@ int adapt_region_create(const char *id, int num_features, int num_variants,
     h->kind = kind;
     h->T = trees;
     h->seed = seed;
+    h->quantile = quantile;
     h->min_train = mtd;
     *out = h.get();
     g_regions.emplace(id, std::move(h));

@@ -175,3 +175,22 @@ def test_p_invariant_kfold():
             np.testing.assert_allclose(got["t_selected"], want["t_selected"], rtol=len(X) * 2.0**-52)
             np.testing.assert_allclose(got["t_best"], want["t_best"], rtol=len(X) * 2.0**-52)
             assert o["kfold_trees"][i].tobytes() == trees[i].tobytes(), (r, i)
+
+
+def test_p_invariant_quantile_bins():
+    # R23 with 2 ranks: each rank's sorted distinct keys are all-gathered and
+    # merged, so the quantiser (and the tree) is the single-table one
+    rng = np.random.default_rng(3)
+    n = 40001
+    X = np.stack([rng.normal(size=n), rng.integers(0, 7, n), rng.uniform(0, 1e4, n)], 1).astype(np.float32)
+    X[: n // 2, 2] += 1e4  # rank 0 and rank 1 see disjoint value ranges
+    T = rng.random((n, 4)).astype(np.float32)
+    T[:, 1] -= (X[:, 0] > 0.3) * 0.4
+    T[:, 2] -= (X[:, 2] < 5e3) * 0.6
+    res = _run(2, {"X": X, "T": T, "D": 7, "model": "dtree,depth=7,bins=quantile"})
+    y = oracle.labels(T)
+    ref = oracle.train_quantile(X, y, 4, 7)
+    for r, o in sorted(res.items()):
+        assert "error" not in o
+        assert o["tree"].tobytes() == ref.tobytes(), f"rank {r}"
+        assert np.array_equal(o["select"], oracle.select(ref, X[o["lo"]:o["hi"]]))
