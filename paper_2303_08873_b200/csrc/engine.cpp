@@ -394,7 +394,7 @@ struct adapt_region {
       H0, H1, segs,
       hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, cmaps, psync, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall;
-  adapt::Arena stage_a, stage_b;  // per-level uploads: before the partition, before the histogram
+  adapt::Arena stage_p, stage_a, stage_b;  // per-level uploads: partition, its tables, histogram
   // Table-1 shim state
   bool active = false;
   std::vector<float> ctx_feat;
@@ -1046,6 +1046,65 @@ void train_region(adapt_region *h, cudaStream_t s) {
     if (trace) tr[0] = now_us();
     const uint8_t *hist_bins = bins_in, *hist_lab = lab_in, *hist_w = w_in;
     int64_t rows_part = 0;
+    if (trace) tr[6] = now_us();
+    PartArgs pa{};
+    int max_visits = 1;  // parents a partition range can touch
+    size_t vbytes = 0;
+    if (level > 0) {
+      const uint32_t total = virtualize(psegs, false);
+      rows_part = total;
+      pa.nseg = (int)psegs.size();
+      pa.total_rows = total;
+      pa.nranges = partition_ranges(sms, total);
+      const uint32_t R = (total + pa.nranges - 1) / std::max(1, pa.nranges);
+      for (int r = 0, si = 0; r < pa.nranges && total; r++) {
+        const uint32_t p0 = r * R, p1 = std::min<uint64_t>((uint64_t)p0 + R, total);
+        while (si + 1 < pa.nseg && psegs[si + 1].row_base <= p0) si++;
+        int k = si, nodes = 0, last = -1;
+        while (k < pa.nseg && psegs[k].row_base < p1) {
+          if (psegs[k].direct != last) nodes++, last = psegs[k].direct;
+          k++;
+        }
+        max_visits = std::max(max_visits, nodes);
+      }
+    }
+    double t_mv = trace ? now_us() : 0;
+    // the partition goes first; the tables of the histogram / split passes are
+    // built on the host while it runs (they depend only on the frontier)
+    Arena &sp = h->stage_p;
+    sp.reset();
+    const size_t o_psegs = level > 0 ? sp.put(psegs) : 0;
+    sp.flush(s);
+    int32_t *hv = nullptr;
+    if (level > 0) {
+      // ---- a7: move the parents' rows into the children's pieces ----
+      uint8_t *bo = (out_plane ? h->binsB : h->binsA).as<uint8_t>();
+      uint8_t *lo = (out_plane ? h->labB : h->labA).as<uint8_t>();
+      const uint32_t total = (uint32_t)rows_part;
+      pa.segs = sp.ptr<Seg>(o_psegs);
+      pa.bins_in = bins_in;
+      pa.lab_in = lab_in;
+      pa.bins_out = bo;
+      pa.lab_out = lo;
+      pa.w_in = w_in;
+      pa.w_out = w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr;
+      pa.pstride = pstride;
+      pa.BS = BS;
+      pa.F = F;
+      pa.max_visits = max_visits;
+      vbytes = (size_t)pa.nranges * max_visits * 6 * 4;
+      h->visits.ensure(vbytes);
+      CUDA_CHECK(cudaMemsetAsync(h->visits.p, 0xFF, vbytes, s));
+      pa.visits = h->visits.as<int32_t>();
+      {
+        snprintf(nm, sizeof nm, "partition_L%02d", level);
+        Phase ph(per_level ? nm : "partition", s, (double)total * 2 * (BS + 1));
+        launch_partition(pa, s);
+      }
+      h->hres.ensure(vbytes);
+      hv = h->hres.as<int32_t>();
+      CUDA_CHECK(cudaMemcpyAsync(hv, h->visits.p, vbytes, cudaMemcpyDeviceToHost, s));
+    }
     // ---- uploads that do not depend on this level's partition: class maps
     // of the direct nodes, their slots, the subtraction triples, node slots ----
     // node histograms, class-compacted: slot offsets from the nodes' class counts
@@ -1099,35 +1158,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
       sblocks += chunk_count(DS * jb.kc_d);
     }
     if (trace) tr[6] = now_us();
-    PartArgs pa{};
-    int max_visits = 1;  // parents a partition range can touch
-    size_t vbytes = 0;
-    if (level > 0) {
-      const uint32_t total = virtualize(psegs, false);
-      rows_part = total;
-      pa.nseg = (int)psegs.size();
-      pa.total_rows = total;
-      pa.nranges = partition_ranges(sms, total);
-      const uint32_t R = (total + pa.nranges - 1) / std::max(1, pa.nranges);
-      for (int r = 0, si = 0; r < pa.nranges && total; r++) {
-        const uint32_t p0 = r * R, p1 = std::min<uint64_t>((uint64_t)p0 + R, total);
-        while (si + 1 < pa.nseg && psegs[si + 1].row_base <= p0) si++;
-        int k = si, nodes = 0, last = -1;
-        while (k < pa.nseg && psegs[k].row_base < p1) {
-          if (psegs[k].direct != last) nodes++, last = psegs[k].direct;
-          k++;
-        }
-        max_visits = std::max(max_visits, nodes);
-      }
-    }
-    double t_mv = trace ? now_us() : 0;
     Arena &sa = h->stage_a;
     sa.reset();
     const size_t o_cmaps = sa.put(cmaps), o_soff = sa.put(soff), o_skc = sa.put(slot_kc),
                  o_jobs = sa.put(jobs), o_maps = sa.put(maps), o_noff = sa.put(node_off),
                  o_nkc = sa.put(node_kc), o_zst = sa.put(zstart), o_sst = sa.put(sstart),
                  o_big = sa.put(big_nodes), o_small = sa.put(small_nodes);
-    const size_t o_psegs = level > 0 ? sa.put(psegs) : 0;
     sa.flush(s);
     Hcur->ensure((size_t)soff[nslots] * 4 + 16);
     {
@@ -1136,33 +1172,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
                         sa.ptr<int32_t>(o_zst), ndirect_slots, zblocks, s);
     }
     if (level > 0) {
-      // ---- a7: move the parents' rows into the children's pieces ----
       uint8_t *bo = (out_plane ? h->binsB : h->binsA).as<uint8_t>();
       uint8_t *lo = (out_plane ? h->labB : h->labA).as<uint8_t>();
-      const uint32_t total = (uint32_t)rows_part;
-      pa.segs = sa.ptr<Seg>(o_psegs);
-      pa.bins_in = bins_in;
-      pa.lab_in = lab_in;
-      pa.bins_out = bo;
-      pa.lab_out = lo;
-      pa.w_in = w_in;
-      pa.w_out = w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr;
-      pa.pstride = pstride;
-      pa.BS = BS;
-      pa.F = F;
-      pa.max_visits = max_visits;
-      vbytes = (size_t)pa.nranges * max_visits * 6 * 4;
-      h->visits.ensure(vbytes);
-      CUDA_CHECK(cudaMemsetAsync(h->visits.p, 0xFF, vbytes, s));
-      pa.visits = h->visits.as<int32_t>();
-      {
-        snprintf(nm, sizeof nm, "partition_L%02d", level);
-        Phase ph(per_level ? nm : "partition", s, (double)total * 2 * (BS + 1));
-        launch_partition(pa, s);
-      }
-      h->hres.ensure(vbytes);
-      int32_t *hv = h->hres.as<int32_t>();
-      CUDA_CHECK(cudaMemcpyAsync(hv, h->visits.p, vbytes, cudaMemcpyDeviceToHost, s));
       if (trace) tr[1] = now_us();
       CUDA_CHECK(cudaStreamSynchronize(s));
       if (trace) tr[2] = now_us();
@@ -1295,6 +1306,10 @@ void train_region(adapt_region *h, cudaStream_t s) {
     std::vector<Seg> nsegs;
     std::vector<int2> nchildren;
     std::vector<Derived> nderived;
+    next.reserve((size_t)2 * A);
+    nderived.reserve(A);
+    nchildren.reserve((size_t)2 * A);
+    h->tree.reserve(h->tree.size() + (size_t)2 * A);
     int ndirect = 0;
     std::vector<uint64_t> P(C), PL(C), PR(C);
     for (int j = 0; j < A; j++) {
