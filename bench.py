@@ -213,16 +213,18 @@ def bench_kfold(args, ad, adist, torch, dev, stream, rank: int, world: int):
             out.append(ad.adapt_kfold(h, 4, m, 10, 1, stream))
         return out
 
-    run()  # warm-up
+    for _ in range(max(args.warmup, 1)):
+        run()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    res = run()
+    for _ in range(args.steps):
+        res = run()
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = adist.max_over_ranks(e0.elapsed_time(e1), dev)
+    ms = adist.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
     ad.adapt_region_destroy(h)
     acc = {f"adaptive_{25 * m}": float(res[m - 1]["n_correct"].sum() / res[m - 1]["n_test"].sum())
            for m in (1, 2, 3)}

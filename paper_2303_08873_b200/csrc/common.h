@@ -225,13 +225,20 @@ struct KfoldPartial {
   unsigned long long n_test, n_correct;
   double t_selected, t_best;
 };
-// d_bnd[j] = ceil(j N / K), j = 0..K (the first position of group j); w: u8 [n]
-void launch_kfold_weights(uint64_t seed, int shuffle, uint64_t N, const uint64_t *d_bnd, int K, int m,
-                          int k, uint64_t lo, int64_t n, uint8_t *w, cudaStream_t s);
 int kfold_eval_blocks();
-// part: [kfold_eval_blocks()] per-block partials over the rows with w == 0
-void launch_kfold_eval(const uint8_t *w, const uint8_t *lab, const int32_t *sel, const float *times,
-                       int64_t n, int V, KfoldPartial *part, cudaStream_t s);
+// groups of the local rows in one shuffle (u8 [n]) and their local sizes (cnt [K], accumulated);
+// d_bnd[j] = ceil(j N / K), j = 0..K (the first position of group j)
+void launch_kfold_groups(uint64_t seed, int shuffle, uint64_t N, const uint64_t *d_bnd, int K, uint64_t lo,
+                         int64_t n, uint8_t *grp, unsigned long long *cnt, cudaStream_t s);
+// ingest planes -> per-(shuffle j, group g) contiguous copies at cursor[j*K+g]
+void launch_kfold_scatter(const uint8_t *bins, size_t pstride_in, const uint8_t *lab, int64_t n, int BS,
+                          const uint8_t *grp, int sb, int K, unsigned int *cursor, uint8_t *obins,
+                          size_t pstride_out, uint8_t *olab, cudaStream_t s);
+// held-out evaluation of the sb*K batch models (trees concatenated, roots[r]);
+// part: [kfold_eval_blocks()][sb*K]
+void launch_kfold_eval_many(const float *X, int64_t n, int F, int V, const float *times, const uint8_t *lab,
+                            const uint8_t *grp, int sb, int K, int m, const DNode *nodes, const int32_t *roots,
+                            KfoldPartial *part, cudaStream_t s);
 
 // a single tree: the first kSelTopNodes BFS nodes (DNode) are staged in shared
 // memory; a child index k >= n_top of a top node names bottom block k - n_top.

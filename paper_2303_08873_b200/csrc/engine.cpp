@@ -386,7 +386,8 @@ struct adapt_region {
   };
   const KfoldSpec *kfold = nullptr;
   std::vector<std::vector<adapt_node_t>> kfold_trees;
-  adapt::DevBuf kbnd, ksel, kpart;
+  adapt::DevBuf flagsum;  // error-flag sums over ranks
+  adapt::DevBuf kbnd, kpart, kgrp, kcnt, kcur, ksb, klab, knodes, kroots;
   bool trained = false;
   std::vector<int64_t> stats;
   // scratch
@@ -680,6 +681,16 @@ int64_t gpu_aggregate(adapt_region *h, cudaStream_t s, int64_t *pairs) {
   return G;
 }
 
+// K-fold models grown in one frontier (kfold.cu, R22): root r's rows are the
+// pieces pieces[r] of the planes (bins word planes with stride pstride, labels)
+struct MultiRoot {
+  int R;
+  const uint8_t *bins, *labs;
+  size_t pstride;
+  int64_t rows_out;  // rows the level passes may write (sum of the roots' rows)
+  std::vector<std::vector<std::pair<uint32_t, uint32_t>>> pieces;
+};
+
 // ------------------------------------------------------------ training --
 void train_region(adapt_region *h, cudaStream_t s) {
   const int F = h->F, V = h->V, C = V, D = h->D;
@@ -739,13 +750,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
   // error flags, summed over ranks so that all ranks fail (or retry) together
   uint32_t *hs = h->hsmall.as<uint32_t>();
   auto check_flags = [&](bool allow_too_many = false) -> uint32_t {
-    DevBuf fl;
-    fl.ensure(32);
     CUDA_CHECK(cudaMemcpyAsync(hs, h->flags.p, 4, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
     uint32_t bits[6];
     for (int b = 0; b < 6; b++) bits[b] = (hs[0] >> b) & 1;
     if (collectives_on()) {
+      DevBuf &fl = h->flagsum;
+      fl.ensure(32);
       CUDA_CHECK(cudaMemcpyAsync(fl.p, bits, 24, cudaMemcpyHostToDevice, s));
       comm_allreduce_sum(fl.p, 6, false, s, "allreduce flags");
       CUDA_CHECK(cudaMemcpyAsync(bits, fl.p, 24, cudaMemcpyDeviceToHost, s));
@@ -970,26 +981,42 @@ void train_region(adapt_region *h, cudaStream_t s) {
   // 2. level loop (a4-a8).  Per level: partition the previous level's split
   // parents (a7), histogram the smaller child of each (a4) — or the root —,
   // sum over ranks (a5), derive the siblings, search splits (a6), decide.
-  auto grow_tree = [&](const uint8_t *w_root) {  // one tree; w_root: bootstrap weights or null
+  // one tree (w_root: bootstrap weights or null), or with `mr` several trees
+  // grown in ONE frontier (K-fold models): mr->R roots whose rows are pieces of
+  // mr's planes; h->tree then holds all of them, roots first, level by level
+  auto grow_tree = [&](const uint8_t *w_root, const MultiRoot *mr = nullptr) {
   h->tree.clear();
   h->stats.clear();
+  const int R = mr ? mr->R : 1;
+  const size_t ps = mr ? mr->pstride : pstride;
+  const int64_t rows_out = mr ? mr->rows_out : n;  // plane capacity of the level passes
   adapt_node_t root{};
   root.feature = -1;
   root.left = root.right = -1;
-  h->tree.push_back(root);
-  std::vector<FNode> frontier(1);
-  frontier[0].tree_idx = 0;
-  frontier[0].depth = 0;
-  frontier[0].slot = 0;
-  frontier[0].direct = true;
-  for (int k = 0; k < C; k++) frontier[0].cls.add(k);
+  std::vector<FNode> frontier(R);
+  for (int r = 0; r < R; r++) {
+    h->tree.push_back(root);
+    frontier[r].tree_idx = r;
+    frontier[r].depth = 0;
+    frontier[r].slot = r;
+    frontier[r].direct = true;
+    for (int k = 0; k < C; k++) frontier[r].cls.add(k);
+  }
   // this rank's rows of frontier node j: pieces [pc_start[j], pc_start[j+1]) of
   // (offset, length) in the planes
   std::vector<std::pair<uint32_t, uint32_t>> pcs{{0u, (uint32_t)n}};
   std::vector<int32_t> pc_start{0, 1};
+  if (mr) {
+    pcs.clear();
+    pc_start.assign(1, 0);
+    for (int r = 0; r < R; r++) {
+      for (const auto &pc : mr->pieces[r]) pcs.push_back(pc);
+      pc_start.push_back((int32_t)pcs.size());
+    }
+  }
   std::vector<Seg> psegs;           // pieces of the split parents (partition input)
   std::vector<int2> pseg_children;  // per piece: frontier index of the left / right child
-  int ndirect_slots = 1;  // direct slots are 0..ndirect_slots-1, derived ones follow
+  int ndirect_slots = R;  // direct slots are 0..ndirect_slots-1, derived ones follow
   struct Derived {        // a derived node of the next level = parent - direct sibling
     int j, sib_j;         // frontier indices (next level)
     int64_t off_p;        // parent's histogram offset (this level; Hprev next level)
@@ -998,16 +1025,17 @@ void train_region(adapt_region *h, cudaStream_t s) {
   std::vector<Derived> derived;
   // planes: the root is histogrammed from the ingest output; pass d >= 1 moves
   // the parents' rows from one plane pair into the other
-  const uint8_t *bins_in = h->bins.as<uint8_t>(), *lab_in = h->labels.as<uint8_t>();
+  const uint8_t *bins_in = mr ? mr->bins : h->bins.as<uint8_t>();
+  const uint8_t *lab_in = mr ? mr->labs : h->labels.as<uint8_t>();
   const uint8_t *w_in = w_root;  // weight plane (forests), moved along with the rows
   if (w_root) {
     h->wA.ensure((size_t)std::max<int64_t>(n, 1) + 64);
     h->wB.ensure((size_t)std::max<int64_t>(n, 1) + 64);
   }
-  h->binsA.ensure(bins_bytes(n, BS));
-  h->binsB.ensure(bins_bytes(n, BS));
-  h->labA.ensure((size_t)std::max<int64_t>(n, 1) + 64);
-  h->labB.ensure((size_t)std::max<int64_t>(n, 1) + 64);
+  h->binsA.ensure(ps * (BS < 4 ? 1 : BS / 4));
+  h->binsB.ensure(ps * (BS < 4 ? 1 : BS / 4));
+  h->labA.ensure((size_t)std::max<int64_t>(rows_out, 1) + 64);
+  h->labB.ensure((size_t)std::max<int64_t>(rows_out, 1) + 64);
   int out_plane = 0;  // 0: A, 1: B
   int sms = 148;
   CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g_ctx.device));
@@ -1088,7 +1116,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       pa.lab_out = lo;
       pa.w_in = w_in;
       pa.w_out = w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr;
-      pa.pstride = pstride;
+      pa.pstride = ps;
       pa.BS = BS;
       pa.F = F;
       pa.max_visits = max_visits;
@@ -1235,7 +1263,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       ha.bins_in = hist_bins;
       ha.lab_in = hist_lab;
       ha.w_in = hist_w;
-      ha.pstride = pstride;
+      ha.pstride = ps;
       ha.BS = BS;
       ha.F = F;
       ha.C = C;
@@ -1454,82 +1482,156 @@ void train_region(adapt_region *h, cudaStream_t s) {
     return lo;
   };
 
-  if (h->kfold) {  // K-fold harness (R22): models on weighted subsets, tested on the rest
+  if (h->kfold) {  // K-fold harness (R22): all models of a batch of shuffles in ONE frontier
     const auto &kf = *h->kfold;
-    if (n_total < (uint64_t)kf.K) throw Error(ADAPT_E_INSUFFICIENT_DATA, "fewer rows than K groups");
+    const int K = kf.K, m = kf.m;
+    if (n_total < (uint64_t)K) throw Error(ADAPT_E_INSUFFICIENT_DATA, "fewer rows than K groups");
     const uint64_t lo = shard_lo();
-    std::vector<uint64_t> bnd(kf.K + 1);
-    for (int j = 0; j <= kf.K; j++)  // ceil(j N / K): the first position of group j
-      bnd[j] = (uint64_t)(((unsigned __int128)j * n_total + kf.K - 1) / kf.K);
+    std::vector<uint64_t> bnd(K + 1);
+    for (int j = 0; j <= K; j++)  // ceil(j N / K): the first position of group j
+      bnd[j] = (uint64_t)(((unsigned __int128)j * n_total + K - 1) / K);
     h2d(h->kbnd, bnd, s);
-    h->wplane.ensure((size_t)std::max<int64_t>(n, 1) + 64);
-    h->ksel.ensure((size_t)std::max<int64_t>(n, 1) * 4 + 16);
+    // shuffles per batch: the models' rows (m copies of the table per shuffle)
+    // must stay below 2^30 per rank (u32 positions, plane memory)
+    const int64_t per_shuffle = std::max<int64_t>(1, (int64_t)m * n);
+    const int Sb = (int)std::max<int64_t>(1, std::min<int64_t>(kf.shuffles, (1ll << 30) / per_shuffle));
     const int nb = kfold_eval_blocks();
-    h->kpart.ensure((size_t)nb * sizeof(KfoldPartial));
-    DevBuf kall;
-    kall.ensure((size_t)world * 32);
-    std::vector<KfoldPartial> part(nb);
-    std::vector<double> allv((size_t)world * 4);
     h->kfold_trees.clear();
     std::vector<int64_t> stats;
-    for (int sh = 0; sh < kf.shuffles; sh++)
-      for (int k = 0; k < kf.K; k++) {
-        {
-          Phase ph("kfold", s, (double)n);
-          launch_kfold_weights(kf.seed, sh, n_total, h->kbnd.as<uint64_t>(), kf.K, kf.m, k, lo, n,
-                               h->wplane.as<uint8_t>(), s);
-        }
-        grow_tree(h->wplane.as<uint8_t>());
-        stats.insert(stats.end(), h->stats.begin(), h->stats.end());
-        h->kfold_trees.push_back(h->tree);
-        upload_tree(h, s);
-        {
-          Phase ph("select", s, (double)n * (4.0 * F + 4));
-          launch_select(h->d_tree.as<DNode>(), (int)h->tree.size(), h->d_blocks.as<uint4>(), feat, n, F,
-                        h->ksel.as<int32_t>(), s);
-        }
-        if (n) {
-          Phase ph("kfold", s, (double)n * 6);
-          launch_kfold_eval(h->wplane.as<uint8_t>(), h->labels.as<uint8_t>(), h->ksel.as<int32_t>(), times,
-                            n, V, h->kpart.as<KfoldPartial>(), s);
-          CUDA_CHECK(cudaMemcpyAsync(part.data(), h->kpart.p, (size_t)nb * sizeof(KfoldPartial),
-                                     cudaMemcpyDeviceToHost, s));
-          CUDA_CHECK(cudaStreamSynchronize(s));
-        }
-        KfoldPartial mine{0, 0, 0.0, 0.0};
-        if (n)
-          for (const auto &p : part) {  // block order: deterministic
-            mine.n_test += p.n_test;
-            mine.n_correct += p.n_correct;
-            mine.t_selected += p.t_selected;
-            mine.t_best += p.t_best;
-          }
-        KfoldPartial tot = mine;
-        if (collectives_on()) {  // every rank's partial, summed in rank order
-          CUDA_CHECK(cudaMemcpyAsync(h->kpart.p, &mine, 32, cudaMemcpyHostToDevice, s));
-          comm_allgather(h->kpart.p, kall.p, 32, s, "allgather kfold results");
-          std::vector<KfoldPartial> all(world);
-          CUDA_CHECK(cudaMemcpyAsync(all.data(), kall.p, (size_t)world * 32, cudaMemcpyDeviceToHost, s));
-          CUDA_CHECK(cudaStreamSynchronize(s));
-          tot = all[0];
-          for (int r = 1; r < world; r++) {
-            tot.n_test += all[r].n_test;
-            tot.n_correct += all[r].n_correct;
-            tot.t_selected += all[r].t_selected;
-            tot.t_best += all[r].t_best;
-          }
-        }
-        adapt_kfold_result_t &o = kf.out[(size_t)sh * kf.K + k];
-        o.shuffle = sh;
-        o.fold = k;
-        o.n_nodes = (int32_t)h->tree.size();
-        o.pad_ = 0;
-        o.n_test = (int64_t)tot.n_test;
-        o.n_train = (int64_t)n_total - o.n_test;
-        o.n_correct = (int64_t)tot.n_correct;
-        o.t_selected = tot.t_selected;
-        o.t_best = tot.t_best;
+    for (int s0 = 0; s0 < kf.shuffles; s0 += Sb) {
+      const int sb = std::min(Sb, kf.shuffles - s0), R = sb * K;
+      const int64_t nn = std::max<int64_t>(n, 1);
+      const size_t ps = bins_plane_stride(std::max<int64_t>((int64_t)sb * m * n, (int64_t)sb * n), BS);
+      h->kgrp.ensure((size_t)sb * nn);
+      h->kcnt.ensure((size_t)R * 8);
+      CUDA_CHECK(cudaMemsetAsync(h->kcnt.p, 0, (size_t)R * 8, s));
+      {
+        Phase ph("kfold", s, (double)n * sb);
+        for (int j = 0; j < sb; j++)
+          launch_kfold_groups(kf.seed, s0 + j, n_total, h->kbnd.as<uint64_t>(), K, lo, n,
+                              h->kgrp.as<uint8_t>() + (size_t)j * nn,
+                              h->kcnt.as<unsigned long long>() + (size_t)j * K, s);
       }
+      std::vector<unsigned long long> cnt(R);
+      CUDA_CHECK(cudaMemcpyAsync(cnt.data(), h->kcnt.p, (size_t)R * 8, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      std::vector<uint32_t> cur(R);  // group (j, g) lands at [cur, cur + cnt) of the sorted planes
+      uint32_t acc = 0;
+      for (int r = 0; r < R; r++) {
+        cur[r] = acc;
+        acc += (uint32_t)cnt[r];
+      }
+      MultiRoot mr;
+      mr.R = R;
+      mr.pstride = ps;
+      mr.rows_out = (int64_t)sb * m * n;
+      mr.pieces.resize(R);
+      for (int j = 0; j < sb; j++)
+        for (int k = 0; k < K; k++)
+          for (int t = 0; t < m; t++) {
+            const int g = j * K + (k + t) % K;
+            if (cnt[g]) mr.pieces[j * K + k].push_back({cur[g], (uint32_t)cnt[g]});
+          }
+      h2d(h->kcur, cur, s);
+      h->ksb.ensure(ps * (BS < 4 ? 1 : BS / 4));
+      h->klab.ensure((size_t)sb * nn + 64);
+      {
+        Phase ph("kfold", s, (double)n * sb * 2 * (BS + 1));
+        launch_kfold_scatter(h->bins.as<uint8_t>(), pstride, h->labels.as<uint8_t>(), n, BS,
+                             h->kgrp.as<uint8_t>(), sb, K, h->kcur.as<unsigned int>(), h->ksb.as<uint8_t>(), ps,
+                             h->klab.as<uint8_t>(), s);
+      }
+      mr.bins = h->ksb.as<uint8_t>();
+      mr.labs = h->klab.as<uint8_t>();
+      grow_tree(nullptr, &mr);
+      stats.insert(stats.end(), h->stats.begin(), h->stats.end());
+      // the combined array -> one canonical BFS tree per model (BFS from its root)
+      std::vector<std::vector<adapt_node_t>> batch(R);
+      for (int r = 0; r < R; r++) {
+        auto &tr = batch[r];
+        std::vector<int32_t> q{r};
+        for (size_t qi = 0; qi < q.size(); qi++) {
+          adapt_node_t nd = h->tree[q[qi]];
+          if (nd.feature >= 0) {
+            q.push_back(nd.left);
+            q.push_back(nd.right);
+            nd.left = (int32_t)(q.size() - 2);
+            nd.right = (int32_t)(q.size() - 1);
+          }
+          tr.push_back(nd);
+        }
+      }
+      // held-out evaluation of the batch's models in one pass over the rows
+      std::vector<DNode> d;
+      std::vector<int32_t> roots;
+      for (const auto &tr : batch) {
+        const int32_t off = (int32_t)d.size();
+        roots.push_back(off);
+        for (const auto &nd : tr) {
+          DNode x;
+          x.thr = nd.feature >= 0 ? round_down_f32(nd.threshold) : 0.f;
+          x.meta = nd.feature >= 0 ? ((nd.left + off) << 6) | nd.feature : -1 - nd.label;
+          d.push_back(x);
+        }
+      }
+      if (d.size() >= (1u << 25)) throw Error(ADAPT_E_INVALID_ARG, "K-fold models too large (2^25 nodes)");
+      h2d(h->knodes, d, s);
+      h2d(h->kroots, roots, s);
+      h->kpart.ensure((size_t)nb * R * sizeof(KfoldPartial));
+      std::vector<KfoldPartial> part((size_t)nb * R);
+      if (n) {
+        Phase ph("kfold", s, (double)n * (4.0 * F + 2 + sb));
+        launch_kfold_eval_many(feat, n, F, V, times, h->labels.as<uint8_t>(), h->kgrp.as<uint8_t>(), sb, K, m,
+                               h->knodes.as<DNode>(), h->kroots.as<int32_t>(), h->kpart.as<KfoldPartial>(), s);
+        CUDA_CHECK(cudaMemcpyAsync(part.data(), h->kpart.p, part.size() * sizeof(KfoldPartial),
+                                   cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+      }
+      std::vector<KfoldPartial> mine(R, KfoldPartial{0, 0, 0.0, 0.0});
+      if (n)
+        for (int b = 0; b < nb; b++)  // block order
+          for (int r = 0; r < R; r++) {
+            const KfoldPartial &p = part[(size_t)b * R + r];
+            mine[r].n_test += p.n_test;
+            mine[r].n_correct += p.n_correct;
+            mine[r].t_selected += p.t_selected;
+            mine[r].t_best += p.t_best;
+          }
+      std::vector<KfoldPartial> tot = mine;
+      if (collectives_on()) {  // every rank's partials, summed in rank order
+        DevBuf sendb, allb;
+        sendb.ensure((size_t)R * 32);
+        allb.ensure((size_t)world * R * 32);
+        CUDA_CHECK(cudaMemcpyAsync(sendb.p, mine.data(), (size_t)R * 32, cudaMemcpyHostToDevice, s));
+        comm_allgather(sendb.p, allb.p, (size_t)R * 32, s, "allgather kfold results");
+        std::vector<KfoldPartial> all((size_t)world * R);
+        CUDA_CHECK(cudaMemcpyAsync(all.data(), allb.p, (size_t)world * R * 32, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        for (int r = 0; r < R; r++) {
+          tot[r] = all[r];
+          for (int w = 1; w < world; w++) {
+            const KfoldPartial &p = all[(size_t)w * R + r];
+            tot[r].n_test += p.n_test;
+            tot[r].n_correct += p.n_correct;
+            tot[r].t_selected += p.t_selected;
+            tot[r].t_best += p.t_best;
+          }
+        }
+      }
+      for (int r = 0; r < R; r++) {
+        adapt_kfold_result_t &o = kf.out[(size_t)s0 * K + r];
+        o.shuffle = s0 + r / K;
+        o.fold = r % K;
+        o.n_nodes = (int32_t)batch[r].size();
+        o.pad_ = 0;
+        o.n_test = (int64_t)tot[r].n_test;
+        o.n_train = (int64_t)n_total - o.n_test;
+        o.n_correct = (int64_t)tot[r].n_correct;
+        o.t_selected = tot[r].t_selected;
+        o.t_best = tot[r].t_best;
+        h->kfold_trees.push_back(std::move(batch[r]));
+      }
+    }
     h->stats.swap(stats);
     return;  // the region's own model is restored by adapt_kfold
   }

@@ -4,18 +4,24 @@
 // for testing ... K-fold creation is repeated 10 times, each time shuffling
 // the inputs"; Adaptive-25/50/75 = K = 4 with m = 1/2/3 training groups).
 //
-//   kfold_weights_kernel  R22: shuffle s permutes the GLOBAL row ids with a
+//   kfold_group_kernel    R22: shuffle s permutes the GLOBAL row ids with a
 //                         4-round Feistel network on 2h-bit words, cycle-
 //                         walking into [0, N); group = floor(pos K / N) (found
 //                         from the K+1 integer group bounds, no 64-bit
-//                         division); u8 weight 1 iff the group is one of the
-//                         fold's training groups.  The level loop trains on the
-//                         weights exactly as for forests (weight-0 rows drop
-//                         out at the first partition), so no subset is copied.
-//   kfold_eval_kernel     per test row (weight 0): the selection against the
-//                         row's label and the times of the selected / fastest
-//                         variants; one partial per block (a fixed grid), summed
-//                         on the host in block order: deterministic.
+//                         division), plus the local group sizes.
+//   kfold_scatter_kernel  counting sort of the ingest planes (bins + labels)
+//                         by (shuffle, group): group g of shuffle j becomes one
+//                         contiguous piece.  Model (j, k)'s root is then the m
+//                         pieces of its training groups, and ALL models of a
+//                         batch of shuffles grow in ONE frontier of the level
+//                         loop (engine.cpp MultiRoot): the first partition
+//                         copies each row into the m models that train on it,
+//                         so the whole protocol costs D level passes instead of
+//                         D per model.
+//   kfold_eval_many_kernel  every row walks the trees of the models that hold
+//                         it out: the selection against the row's label and the
+//                         times of the selected / fastest variants, warp sums
+//                         then per-block partials per model.
 #include <algorithm>
 
 #include "common.h"
@@ -46,60 +52,124 @@ __device__ __forceinline__ uint64_t feistel_pos(uint64_t key, uint64_t N, int h,
   return x;
 }
 
-__global__ void kfold_weights_kernel(uint64_t key, uint64_t N, int h, const uint64_t *__restrict__ bnd,
-                                     int K, int m, int k, uint64_t lo, int64_t n, uint8_t *__restrict__ w) {
+// group of every local row in shuffle s (u8) and the local group sizes
+__global__ void kfold_group_kernel(uint64_t key, uint64_t N, int h, const uint64_t *__restrict__ bnd,
+                                   int K, uint64_t lo, int64_t n, uint8_t *__restrict__ grp,
+                                   unsigned long long *__restrict__ cnt) {
   __shared__ uint64_t sb[kKfoldMaxK + 1];
+  __shared__ unsigned int sc[kKfoldMaxK];
   for (int i = threadIdx.x; i <= K; i += blockDim.x) sb[i] = bnd[i];
+  for (int i = threadIdx.x; i < K; i += blockDim.x) sc[i] = 0;
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t pos = feistel_pos(key, N, h, lo + (uint64_t)i);
-    int g = min(K - 1, (int)((double)pos * (double)K / (double)N));  // then exact, from the bounds
+    int g = min(K - 1, (int)((double)pos * (double)K / (double)N));
     while (g + 1 < K && pos >= sb[g + 1]) g++;
     while (pos < sb[g]) g--;
-    const int off = (g - k + K) % K;  // training groups k, k+1, ..., k+m-1 (mod K)
-    w[i] = off < m ? 1 : 0;
+    grp[i] = (uint8_t)g;
+    atomicAdd(&sc[g], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < K; i += blockDim.x)
+    if (sc[i]) atomicAdd(cnt + i, (unsigned long long)sc[i]);
+}
+
+// counting-sort scatter of the ingest planes by group: row i of shuffle j goes
+// to cursor[j][grp] (warp-aggregated claims); the order inside a group is
+// irrelevant (histograms are order-independent integer sums)
+__global__ void kfold_scatter_kernel(const uint8_t *__restrict__ bins, size_t pstride_in,
+                                     const uint8_t *__restrict__ lab, int64_t n, int planes, int wb,
+                                     const uint8_t *__restrict__ grp, int sb, int K,
+                                     unsigned int *__restrict__ cursor, uint8_t *__restrict__ obins,
+                                     size_t pstride_out, uint8_t *__restrict__ olab) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = n * sb;
+  for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x; t0 < total; t0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = t0 + threadIdx.x;
+    const bool live = t < total;
+    const int j = live ? (int)(t / n) : 0;
+    const int64_t i = live ? t - (int64_t)j * n : 0;
+    const int key = live ? j * K + grp[t] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(peers) - 1;
+    unsigned base = 0;
+    if (live && lane == leader) base = atomicAdd(cursor + key, (unsigned)__popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (!live) continue;
+    const uint32_t pos = base + __popc(peers & ((1u << lane) - 1));
+    olab[pos] = lab[i];
+    if (wb == 4) {
+      for (int p = 0; p < planes; p++)
+        *reinterpret_cast<uint32_t *>(obins + p * pstride_out + (size_t)pos * 4) =
+            *reinterpret_cast<const uint32_t *>(bins + p * pstride_in + (size_t)i * 4);
+    } else {
+      for (int b = 0; b < wb; b++) obins[(size_t)pos * wb + b] = bins[(size_t)i * wb + b];
+    }
   }
 }
 
-constexpr int kEvalThreads = 512;
+constexpr int kEvalManyThreads = 256;
 
-__global__ void __launch_bounds__(kEvalThreads)
-    kfold_eval_kernel(const uint8_t *__restrict__ w, const uint8_t *__restrict__ lab,
-                      const int32_t *__restrict__ sel, const float *__restrict__ times, int64_t n, int V,
-                      KfoldPartial *__restrict__ part) {
-  unsigned long long nt = 0, nc = 0;
-  double ts = 0.0, tb = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (w[i]) continue;
-    const int v = sel[i], y = lab[i];
-    nt++;
-    nc += v == y;
-    ts += (double)__ldg(times + i * V + v);
-    tb += (double)__ldg(times + i * V + y);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nt += __shfl_xor_sync(0xffffffffu, nt, o);
-    nc += __shfl_xor_sync(0xffffffffu, nc, o);
-    ts += __shfl_xor_sync(0xffffffffu, ts, o);
-    tb += __shfl_xor_sync(0xffffffffu, tb, o);
-  }
-  __shared__ KfoldPartial sp[kEvalThreads / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) sp[warp] = KfoldPartial{nt, nc, ts, tb};
+// every batch model (shuffle j, fold k) walks its tree for the rows it holds
+// out: (g - k) mod K >= m; per-model partials in shared memory, one set per block
+__global__ void __launch_bounds__(kEvalManyThreads)
+    kfold_eval_many_kernel(const float *__restrict__ X, int64_t n, int F, int V,
+                           const float *__restrict__ times, const uint8_t *__restrict__ lab,
+                           const uint8_t *__restrict__ grp, int sb, int K, int m,
+                           const DNode *__restrict__ nodes, const int32_t *__restrict__ roots,
+                           KfoldPartial *__restrict__ part) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  KfoldPartial *sp = reinterpret_cast<KfoldPartial *>(smem_raw);
+  const int R = sb * K;
+  for (int r = threadIdx.x; r < R; r += blockDim.x) sp[r] = KfoldPartial{0, 0, 0.0, 0.0};
   __syncthreads();
-  if (threadIdx.x == 0) {
-    KfoldPartial p = sp[0];
-    for (int i = 1; i < kEvalThreads / 32; i++) {  // fixed order
-      p.n_test += sp[i].n_test;
-      p.n_correct += sp[i].n_correct;
-      p.t_selected += sp[i].t_selected;
-      p.t_best += sp[i].t_best;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;  // warp-uniform trip count: lanes past n count nothing
+    const bool live = i < n;
+    const float *x = X + (live ? i : 0) * F;
+    const int y = live ? lab[i] : 0;
+    const float ty = live ? __ldg(times + i * V + y) : 0.f;
+    for (int j = 0; j < sb; j++) {
+      const int g = live ? grp[(int64_t)j * n + i] : 0;
+      for (int k = 0; k < K; k++) {
+        const bool test = live && (g - k + K) % K >= m;  // else a training row of model (j, k)
+        const int r = j * K + k;
+        unsigned correct = 0;
+        double ts = 0.0, tb = 0.0;
+        if (test) {
+          int kk = roots[r];
+          int2 nd = __ldg(reinterpret_cast<const int2 *>(nodes + kk));
+          while (nd.y >= 0) {
+            const float xv = __ldg(x + (nd.y & 63));
+            kk = (nd.y >> 6) + (xv <= __int_as_float(nd.x) ? 0 : 1);  // NaN -> right (R8)
+            nd = __ldg(reinterpret_cast<const int2 *>(nodes + kk));
+          }
+          const int v = -1 - nd.y;
+          correct = v == y;
+          ts = (double)__ldg(times + i * V + v);
+          tb = (double)ty;
+        }
+        // warp sums, then one shared-memory update per warp and model
+        const unsigned nt = __reduce_add_sync(0xffffffffu, test ? 1u : 0u);
+        const unsigned nc = __reduce_add_sync(0xffffffffu, correct);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          ts += __shfl_xor_sync(0xffffffffu, ts, o);
+          tb += __shfl_xor_sync(0xffffffffu, tb, o);
+        }
+        if (lane == 0 && nt) {
+          atomicAdd(&sp[r].n_test, (unsigned long long)nt);
+          atomicAdd(&sp[r].n_correct, (unsigned long long)nc);
+          atomicAdd(&sp[r].t_selected, ts);
+          atomicAdd(&sp[r].t_best, tb);
+        }
+      }
     }
-    part[blockIdx.x] = p;
   }
+  __syncthreads();
+  for (int r = threadIdx.x; r < R; r += blockDim.x) part[(size_t)blockIdx.x * R + r] = sp[r];
 }
 
 int sm_count() {
@@ -121,22 +191,38 @@ uint64_t kfold_key(uint64_t seed, int shuffle) {
   return mix(seed ^ mix((uint64_t)shuffle + 0x2545F4914F6CDD1Dull));
 }
 
-void launch_kfold_weights(uint64_t seed, int shuffle, uint64_t N, const uint64_t *d_bnd, int K, int m,
-                          int k, uint64_t lo, int64_t n, uint8_t *w, cudaStream_t s) {
+int kfold_eval_blocks() { return sm_count() * 2; }
+
+void launch_kfold_groups(uint64_t seed, int shuffle, uint64_t N, const uint64_t *d_bnd, int K, uint64_t lo,
+                         int64_t n, uint8_t *grp, unsigned long long *cnt, cudaStream_t s) {
   if (n == 0) return;
   int h = 1;
   while (h < 31 && (1ull << (2 * h)) < N) h++;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
-  kfold_weights_kernel<<<grid, 256, 0, s>>>(kfold_key(seed, shuffle), N, h, d_bnd, K, m, k, lo, n, w);
+  kfold_group_kernel<<<grid, 256, 0, s>>>(kfold_key(seed, shuffle), N, h, d_bnd, K, lo, n, grp, cnt);
   CUDA_CHECK(cudaGetLastError());
 }
 
-int kfold_eval_blocks() { return sm_count() * 2; }
-
-void launch_kfold_eval(const uint8_t *w, const uint8_t *lab, const int32_t *sel, const float *times,
-                       int64_t n, int V, KfoldPartial *part, cudaStream_t s) {
-  kfold_eval_kernel<<<kfold_eval_blocks(), kEvalThreads, 0, s>>>(w, lab, sel, times, n, V, part);
+void launch_kfold_scatter(const uint8_t *bins, size_t pstride_in, const uint8_t *lab, int64_t n, int BS,
+                          const uint8_t *grp, int sb, int K, unsigned int *cursor, uint8_t *obins,
+                          size_t pstride_out, uint8_t *olab, cudaStream_t s) {
+  if (n == 0) return;
+  const int planes = BS < 4 ? 1 : BS / 4, wb = BS < 4 ? BS : 4;
+  const int grid = (int)std::min<int64_t>((n * sb + 255) / 256, (int64_t)sm_count() * 8);
+  kfold_scatter_kernel<<<grid, 256, 0, s>>>(bins, pstride_in, lab, n, planes, wb, grp, sb, K, cursor, obins,
+                                            pstride_out, olab);
   CUDA_CHECK(cudaGetLastError());
 }
+
+void launch_kfold_eval_many(const float *X, int64_t n, int F, int V, const float *times, const uint8_t *lab,
+                            const uint8_t *grp, int sb, int K, int m, const DNode *nodes, const int32_t *roots,
+                            KfoldPartial *part, cudaStream_t s) {
+  const size_t smem = (size_t)sb * K * sizeof(KfoldPartial);
+  smem_limit(kfold_eval_many_kernel, smem);
+  kfold_eval_many_kernel<<<kfold_eval_blocks(), kEvalManyThreads, smem, s>>>(X, n, F, V, times, lab, grp, sb,
+                                                                              K, m, nodes, roots, part);
+  CUDA_CHECK(cudaGetLastError());
+}
+
 
 }  // namespace adapt
