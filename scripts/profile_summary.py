@@ -34,7 +34,7 @@ for r in rows:
 tot = sum(v[1] for v in per.values())
 out += ["## Launch list (one step, serialised, cold-cache)", "",
         f"Source: `{launches}` — `ncu --metrics gpu__time_duration.sum --clock-control none "
-        "python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-records`.", "",
+        "python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-records --no-c5 --no-kfold`.", "",
         "| kernel | launches | ms | share of step |", "|---|---:|---:|---:|"]
 for k, (n, ms) in sorted(per.items(), key=lambda x: -x[1][1]):
     out.append(f"| {k} | {n} | {ms:.3f} | {100 * ms / tot:.1f}% |")
@@ -61,7 +61,7 @@ for rep in reps:
     top = ", ".join(f"{k} {v:.2f}" for k, v in sorted(st.items(), key=lambda x: -x[1])[:4])
     kname = re.sub(r"\(.*", "", d.get("Kernel Name", "?"))
     base = re.sub(r"<.*", "", kname.split("::")[-1])
-    if base in PHASE:
+    if base in PHASE and "c5" not in os.path.basename(rep):  # the C4 step's kernels
         traffic[PHASE[base]] = {"dram_bytes_per_launch": (rd + wr) * 1e9, "ms": dur,
                                 "source": f"profiles/round{rnd}/ncu_summary.md",
                                 "capture": os.path.basename(rep)}
