@@ -394,7 +394,7 @@ struct adapt_region {
   adapt::DevBuf gkey, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, lk_keys, lk_mul, lk_skeys,
       H0, H1, segs,
       hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, cmaps, psync, xa, xb, oa, ob;
-  adapt::HostBuf hres, hsmall;
+  adapt::HostBuf hres, hsmall, hvis;  // winners, scalars, partition share reports
   adapt::Arena stage_p, stage_a, stage_b;  // per-level uploads: partition, its tables, histogram
   // Table-1 shim state
   bool active = false;
@@ -1069,70 +1069,84 @@ void train_region(adapt_region *h, cudaStream_t s) {
     fprintf(stderr, "[adapt] ingest: host %.0f us to the level loop, then %.0f us of queued work\n",
             t - tr[7], now_us() - t);
   }
+  // a7 launch for level lvl over the split parents' pieces `segs` (virtualised
+  // in place): input planes b_in/l_in/wi, output plane set oplane; the CTAs'
+  // share reports come back asynchronously into h->hvis
+  struct PartState {
+    bool launched = false;
+    PartArgs pa{};
+    int max_visits = 1;  // parents a partition range can touch
+    size_t vbytes = 0;
+    int64_t rows_part = 0;
+    int32_t *hv = nullptr;
+  };
+  auto start_part = [&](int lvl, std::vector<Seg> &segs, const uint8_t *b_in, const uint8_t *l_in,
+                        const uint8_t *wi, int oplane) {
+    PartState st;
+    st.launched = true;
+    PartArgs &pa = st.pa;
+    const uint32_t total = virtualize(segs, false);
+    st.rows_part = total;
+    pa.nseg = (int)segs.size();
+    pa.total_rows = total;
+    pa.nranges = partition_ranges(sms, total);
+    const uint32_t Rr = (total + pa.nranges - 1) / std::max(1, pa.nranges);
+    for (int r = 0, si = 0; r < pa.nranges && total; r++) {
+      const uint32_t p0 = r * Rr, p1 = std::min<uint64_t>((uint64_t)p0 + Rr, total);
+      while (si + 1 < pa.nseg && segs[si + 1].row_base <= p0) si++;
+      int k = si, nodes = 0, last = -1;
+      while (k < pa.nseg && segs[k].row_base < p1) {
+        if (segs[k].direct != last) nodes++, last = segs[k].direct;
+        k++;
+      }
+      st.max_visits = std::max(st.max_visits, nodes);
+    }
+    Arena &sp = h->stage_p;
+    sp.reset();
+    const size_t o_psegs = sp.put(segs);
+    sp.flush(s);
+    pa.segs = sp.ptr<Seg>(o_psegs);
+    pa.bins_in = b_in;
+    pa.lab_in = l_in;
+    pa.bins_out = (oplane ? h->binsB : h->binsA).as<uint8_t>();
+    pa.lab_out = (oplane ? h->labB : h->labA).as<uint8_t>();
+    pa.w_in = wi;
+    pa.w_out = w_root ? (oplane ? h->wB : h->wA).as<uint8_t>() : nullptr;
+    pa.pstride = ps;
+    pa.BS = BS;
+    pa.F = F;
+    pa.max_visits = st.max_visits;
+    st.vbytes = (size_t)pa.nranges * st.max_visits * 6 * 4;
+    h->visits.ensure(st.vbytes);
+    CUDA_CHECK(cudaMemsetAsync(h->visits.p, 0xFF, st.vbytes, s));
+    pa.visits = h->visits.as<int32_t>();
+    {
+      snprintf(nm, sizeof nm, "partition_L%02d", lvl);
+      Phase ph(per_level ? nm : "partition", s, (double)total * 2 * (BS + 1));
+      launch_partition(pa, s);
+    }
+    h->hvis.ensure(st.vbytes);
+    st.hv = h->hvis.as<int32_t>();
+    CUDA_CHECK(cudaMemcpyAsync(st.hv, h->visits.p, st.vbytes, cudaMemcpyDeviceToHost, s));
+    return st;
+  };
+  PartState pending;
   for (int level = 0; !frontier.empty(); level++) {
     const int A = (int)frontier.size();
     if (trace) tr[0] = now_us();
     const uint8_t *hist_bins = bins_in, *hist_lab = lab_in, *hist_w = w_in;
     int64_t rows_part = 0;
     if (trace) tr[6] = now_us();
-    PartArgs pa{};
-    int max_visits = 1;  // parents a partition range can touch
-    size_t vbytes = 0;
-    if (level > 0) {
-      const uint32_t total = virtualize(psegs, false);
-      rows_part = total;
-      pa.nseg = (int)psegs.size();
-      pa.total_rows = total;
-      pa.nranges = partition_ranges(sms, total);
-      const uint32_t R = (total + pa.nranges - 1) / std::max(1, pa.nranges);
-      for (int r = 0, si = 0; r < pa.nranges && total; r++) {
-        const uint32_t p0 = r * R, p1 = std::min<uint64_t>((uint64_t)p0 + R, total);
-        while (si + 1 < pa.nseg && psegs[si + 1].row_base <= p0) si++;
-        int k = si, nodes = 0, last = -1;
-        while (k < pa.nseg && psegs[k].row_base < p1) {
-          if (psegs[k].direct != last) nodes++, last = psegs[k].direct;
-          k++;
-        }
-        max_visits = std::max(max_visits, nodes);
-      }
-    }
+    // a7 of this level: normally launched already at the end of the previous
+    // level's split decisions (overlapping the rest of its bookkeeping)
+    PartState pst;
+    if (level > 0) pst = pending.launched ? pending : start_part(level, psegs, bins_in, lab_in, w_in, out_plane);
+    pending = PartState{};
+    PartArgs &pa = pst.pa;
+    const int max_visits = pst.max_visits;
+    rows_part = pst.rows_part;
+    int32_t *hv = pst.hv;
     double t_mv = trace ? now_us() : 0;
-    // the partition goes first; the tables of the histogram / split passes are
-    // built on the host while it runs (they depend only on the frontier)
-    Arena &sp = h->stage_p;
-    sp.reset();
-    const size_t o_psegs = level > 0 ? sp.put(psegs) : 0;
-    sp.flush(s);
-    int32_t *hv = nullptr;
-    if (level > 0) {
-      // ---- a7: move the parents' rows into the children's pieces ----
-      uint8_t *bo = (out_plane ? h->binsB : h->binsA).as<uint8_t>();
-      uint8_t *lo = (out_plane ? h->labB : h->labA).as<uint8_t>();
-      const uint32_t total = (uint32_t)rows_part;
-      pa.segs = sp.ptr<Seg>(o_psegs);
-      pa.bins_in = bins_in;
-      pa.lab_in = lab_in;
-      pa.bins_out = bo;
-      pa.lab_out = lo;
-      pa.w_in = w_in;
-      pa.w_out = w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr;
-      pa.pstride = ps;
-      pa.BS = BS;
-      pa.F = F;
-      pa.max_visits = max_visits;
-      vbytes = (size_t)pa.nranges * max_visits * 6 * 4;
-      h->visits.ensure(vbytes);
-      CUDA_CHECK(cudaMemsetAsync(h->visits.p, 0xFF, vbytes, s));
-      pa.visits = h->visits.as<int32_t>();
-      {
-        snprintf(nm, sizeof nm, "partition_L%02d", level);
-        Phase ph(per_level ? nm : "partition", s, (double)total * 2 * (BS + 1));
-        launch_partition(pa, s);
-      }
-      h->hres.ensure(vbytes);
-      hv = h->hres.as<int32_t>();
-      CUDA_CHECK(cudaMemcpyAsync(hv, h->visits.p, vbytes, cudaMemcpyDeviceToHost, s));
-    }
     // ---- uploads that do not depend on this level's partition: class maps
     // of the direct nodes, their slots, the subtraction triples, node slots ----
     // node histograms, class-compacted: slot offsets from the nodes' class counts
@@ -1200,8 +1214,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
                         sa.ptr<int32_t>(o_zst), ndirect_slots, zblocks, s);
     }
     if (level > 0) {
-      uint8_t *bo = (out_plane ? h->binsB : h->binsA).as<uint8_t>();
-      uint8_t *lo = (out_plane ? h->labB : h->labA).as<uint8_t>();
+      uint8_t *bo = pa.bins_out;
+      uint8_t *lo = pa.lab_out;
       if (trace) tr[1] = now_us();
       CUDA_CHECK(cudaStreamSynchronize(s));
       if (trace) tr[2] = now_us();
@@ -1339,6 +1353,53 @@ void train_region(adapt_region *h, cudaStream_t s) {
     nchildren.reserve((size_t)2 * A);
     h->tree.reserve(h->tree.size() + (size_t)2 * A);
     int ndirect = 0;
+    // pass 1: what the next partition needs (split feature / rank, which
+    // children stay in the frontier, the direct child's slot), then launch it;
+    // pass 2 (the tree, the next frontier's class sets and subtraction jobs)
+    // runs on the host while the GPU moves the rows
+    struct Dec {
+      bool inL, inR;
+      int32_t hslot;
+    };
+    std::vector<Dec> dec(A, Dec{false, false, -1});
+    for (int j = 0; j < A; j++) {
+      const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + (size_t)j * res_stride);
+      const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);
+      const uint32_t *cLd = Pd + C;
+      const FNode &fn = frontier[j];
+      const int kc = node_kc[j];
+      int np = 0, npl = 0, npr = 0;
+      for (int k = 0; k < kc; k++) {
+        np += Pd[k] > 0;
+        npl += cLd[k] > 0;
+        npr += Pd[k] - cLd[k] > 0;
+      }
+      if (fn.depth >= D || np <= 1 || !nr->valid) continue;  // leaf (R10, R11)
+      Dec &d = dec[j];
+      d.inL = fn.depth + 1 < D && npl > 1;
+      d.inR = fn.depth + 1 < D && npr > 1;
+      if (!d.inL && !d.inR) continue;
+      d.hslot = ndirect++;
+      for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {  // one partition segment per piece
+        const auto &pc = pcs[q];
+        Seg sg{};
+        sg.off = pc.first;
+        sg.len = pc.second;
+        sg.feat = nr->feat;
+        sg.thr = nr->b_lo;
+        sg.write = (d.inL ? 1 : 0) | (d.inR ? 2 : 0);
+        sg.direct = j;  // parent id (groups a parent's pieces)
+        sg.hslot = d.hslot;
+        nsegs.push_back(sg);
+      }
+    }
+    if (ndirect > 0) {  // the next level's a7: level 0 moved nothing, so level 1 reads its input
+      pending = level > 0 ? start_part(level + 1, nsegs, (out_plane ? h->binsB : h->binsA).as<uint8_t>(),
+                                       (out_plane ? h->labB : h->labA).as<uint8_t>(),
+                                       w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr,
+                                       out_plane ^ 1)
+                          : start_part(level + 1, nsegs, bins_in, lab_in, w_in, out_plane);
+    }
     std::vector<uint64_t> P(C), PL(C), PR(C);
     for (int j = 0; j < A; j++) {
       const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + (size_t)j * res_stride);
@@ -1397,8 +1458,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       cl.feature = cr.feature = -1;
       cl.left = cl.right = cr.left = cr.right = -1;
       cl.depth = cr.depth = fn.depth + 1;
-      const bool inL = fn.depth + 1 < D && npresent(PL.data()) > 1;
-      const bool inR = fn.depth + 1 < D && npresent(PR.data()) > 1;
+      const bool inL = dec[j].inL, inR = dec[j].inR;
       // frontier children get their stats from their own class totals next level
       if (!inL) stats(cl, PL.data());
       if (!inR) stats(cr, PR.data());
@@ -1409,7 +1469,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       int dir;
       if (inL && inR) dir = nL <= nR ? 0 : 1;  // histogram the smaller child
       else dir = inL ? 0 : 1;
-      const int32_t hslot = ndirect++;
+      const int32_t hslot = dec[j].hslot;
       int jl = -1, jr = -1;
       if (inL) {
         jl = (int)next.size();
@@ -1427,19 +1487,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
         dv.cls_p = fn.cls;
         nderived.push_back(dv);
       }
-      for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {  // one partition segment per piece
-        const auto &pc = pcs[q];
-        Seg sg{};
-        sg.off = pc.first;
-        sg.len = pc.second;
-        sg.feat = f;
-        sg.thr = nr->b_lo;
-        sg.write = (inL ? 1 : 0) | (inR ? 2 : 0);
-        sg.direct = j;  // parent id (groups a parent's pieces)
-        sg.hslot = hslot;
-        nsegs.push_back(sg);
+      for (int q = pc_start[j]; q < pc_start[j + 1]; q++)  // the children of each piece (pass 1's segments)
         nchildren.push_back(make_int2(jl, jr));
-      }
     }
     // derived slots follow the direct ones
     for (size_t i = 0; i < nderived.size(); i++) next[nderived[i].j].slot = ndirect + (int)i;

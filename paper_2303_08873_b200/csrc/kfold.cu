@@ -191,7 +191,7 @@ uint64_t kfold_key(uint64_t seed, int shuffle) {
   return mix(seed ^ mix((uint64_t)shuffle + 0x2545F4914F6CDD1Dull));
 }
 
-int kfold_eval_blocks() { return sm_count() * 2; }
+int kfold_eval_blocks() { return sm_count() * 8; }  // latency-bound tree walks: full occupancy
 
 void launch_kfold_groups(uint64_t seed, int shuffle, uint64_t N, const uint64_t *d_bnd, int K, uint64_t lo,
                          int64_t n, uint8_t *grp, unsigned long long *cnt, cudaStream_t s) {
