@@ -906,6 +906,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     CUDA_CHECK(cudaMemcpyAsync(h->val.data(), h->dval.p, (size_t)F * kMaxBins * 4, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaMemcpyAsync(h->nval.data(), h->dnval.p, (size_t)F * 4, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
+    const double t_hash = trace ? now_us() : 0;
     {
       std::vector<uint8_t> tab((size_t)lookup_table_bytes(F));
       std::vector<uint32_t> mul((size_t)2 * F), skeys((size_t)F * lookup_slots());
@@ -917,6 +918,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
       h2d(h->lk_mul, mul, s);
       h2d(h->lk_skeys, skeys, s);
     }
+    if (trace)
+      fprintf(stderr, "[adapt] ingest attempt %d: discovery..tables %.0f us, perfect hashes %.0f us (GPU idle)\n",
+              attempt, t_hash - tr[7], now_us() - t_hash);
     CUDA_CHECK(cudaMemsetAsync(h->flags.p, 0, 16, s));
     {
       Phase ph("ingest", s, (double)n * (4.0 * F + 4.0 * V + F + 1));  // algorithmic

@@ -437,55 +437,68 @@ int lookup_slots() { return kPhSlots; }
 // distinct for every key; buckets are placed largest first.  Same hash_bits
 // as the device.  Returns false only if no seed works (never seen).
 bool build_value_hash(const float *vals, int D, uint32_t mul[2], uint8_t *tab, uint32_t *slot_keys) {
+  // hash-and-displace, allocation-free (it runs on the host between the
+  // discovery and the bin pass, with the GPU idle): buckets by the first
+  // hash, largest first (ties in bucket order), each bucket gets the
+  // smallest displacement d that puts all its keys on free slots
   auto hb = [](uint32_t key, uint32_t m, int l) { return (key * m) >> (32 - l); };
-  std::vector<uint32_t> keys(D);
+  uint32_t keys[kMaxBins], h2[kMaxBins];
+  int members[kMaxBins];
   for (int r = 0; r < D; r++) memcpy(&keys[r], &vals[r], 4);
   for (uint32_t seed = 0; seed < 1024; seed++) {
     const uint32_t m1 = (0x9E3779B1u + 0x85EBCA6Bu * seed) | 1u;
     const uint32_t m2 = (0xC2B2AE35u + 0x27D4EB2Fu * seed) | 1u;
-    std::vector<std::vector<int>> buckets(kPhBuckets);
-    for (int r = 0; r < D; r++) buckets[hb(keys[r], m1, kPhLog2Buckets)].push_back(r);
-    std::vector<int> order(kPhBuckets);
-    for (int b = 0; b < kPhBuckets; b++) order[b] = b;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int x, int y) { return buckets[x].size() > buckets[y].size(); });
-    std::vector<char> used(kPhSlots, 0);
-    uint16_t disp[kPhBuckets] = {0};
-    std::vector<uint8_t> slot_rank(kPhSlots, 0);
-    std::vector<uint32_t> skey(kPhSlots, 0xFFFFFFFFu);  // NaN bits: never a canonical key
-    bool ok = true;
-    for (int b : order) {
-      if (buckets[b].empty()) break;
-      int found = -1;
-      for (int d = 0; d < kPhSlots && found < 0; d++) {
-        bool good = true;
-        std::vector<uint32_t> taken;
-        for (int r : buckets[b]) {
-          const uint32_t sl = (hb(keys[r], m2, kPhLog2Slots) + d) & (kPhSlots - 1);
-          if (used[sl] || std::find(taken.begin(), taken.end(), sl) != taken.end()) {
-            good = false;
-            break;
-          }
-          taken.push_back(sl);
-        }
-        if (good) found = d;
-      }
-      if (found < 0) {
-        ok = false;
-        break;
-      }
-      disp[b] = (uint16_t)found;
-      for (int r : buckets[b]) {
-        const uint32_t sl = (hb(keys[r], m2, kPhLog2Slots) + found) & (kPhSlots - 1);
-        used[sl] = 1;
-        slot_rank[sl] = (uint8_t)r;
-        skey[sl] = keys[r];
-      }
+    int cnt[kPhBuckets] = {0}, start[kPhBuckets + 1], fill[kPhBuckets];
+    uint8_t bk[kMaxBins];
+    int maxc = 0;
+    for (int r = 0; r < D; r++) {
+      bk[r] = (uint8_t)hb(keys[r], m1, kPhLog2Buckets);
+      h2[r] = hb(keys[r], m2, kPhLog2Slots);
+      maxc = std::max(maxc, ++cnt[bk[r]]);
     }
+    start[0] = 0;
+    for (int b = 0; b < kPhBuckets; b++) start[b + 1] = start[b] + cnt[b];
+    for (int b = 0; b < kPhBuckets; b++) fill[b] = start[b];
+    for (int r = 0; r < D; r++) members[fill[bk[r]]++] = r;  // rows in order within a bucket
+    uint8_t used[kPhSlots] = {0};
+    uint16_t disp[kPhBuckets] = {0};
+    uint8_t slot_rank[kPhSlots] = {0};
+    uint32_t skey[kPhSlots];
+    for (int i = 0; i < kPhSlots; i++) skey[i] = 0xFFFFFFFFu;  // NaN bits: never a canonical key
+    bool ok = true;
+    for (int size = maxc; size >= 1 && ok; size--)
+      for (int b = 0; b < kPhBuckets && ok; b++) {
+        if (cnt[b] != size) continue;
+        int found = -1;
+        uint32_t taken[kMaxBins];
+        for (int d = 0; d < kPhSlots && found < 0; d++) {
+          bool good = true;
+          int nt = 0;
+          for (int q = start[b]; q < start[b + 1] && good; q++) {
+            const uint32_t sl = (h2[members[q]] + d) & (kPhSlots - 1);
+            if (used[sl]) good = false;
+            for (int t = 0; t < nt && good; t++) good = taken[t] != sl;
+            taken[nt++] = sl;
+          }
+          if (good) found = d;
+        }
+        if (found < 0) {
+          ok = false;
+          break;
+        }
+        disp[b] = (uint16_t)found;
+        for (int q = start[b]; q < start[b + 1]; q++) {
+          const int r = members[q];
+          const uint32_t sl = (h2[r] + found) & (kPhSlots - 1);
+          used[sl] = 1;
+          slot_rank[sl] = (uint8_t)r;
+          skey[sl] = keys[r];
+        }
+      }
     if (!ok) continue;
     memcpy(tab, disp, sizeof disp);
-    memcpy(tab + kPhBuckets * 2, slot_rank.data(), kPhSlots);
-    memcpy(slot_keys, skey.data(), kPhSlots * 4);
+    memcpy(tab + kPhBuckets * 2, slot_rank, kPhSlots);
+    memcpy(slot_keys, skey, kPhSlots * 4);
     mul[0] = m1;
     mul[1] = m2;
     return true;
