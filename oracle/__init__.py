@@ -302,12 +302,14 @@ def quantize(X: np.ndarray, q: dict) -> np.ndarray:
     return Xq
 
 
-def train_quantile(X: np.ndarray, y: np.ndarray, C: int, D: int) -> np.ndarray:
+def train_quantile(X: np.ndarray, y: np.ndarray, C: int, D: int, q: dict | None = None) -> np.ndarray:
     """R23: the exact CART (train) of the quantised table; a split of a quantised
     feature f between the node's bins a < b' then reports the raw threshold
     ((double)prev_{a+1} + (double)lb_{a+1}) / 2, a = the largest quantised value
-    of the node's rows that goes left (rows routed through the tree by Xq)."""
-    q = quantizer(X)
+    of the node's rows that goes left (rows routed through the tree by Xq).
+    q: the quantiser (default: the one of X itself; the K-fold harness and
+    forests train on subsets / resamples with the WHOLE table's quantiser)."""
+    q = quantizer(X) if q is None else q
     Xq = quantize(X, q)
     tree = train(Xq, y, C, D)
     node_rows = {0: np.arange(len(X))}

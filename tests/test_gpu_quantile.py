@@ -89,3 +89,48 @@ def test_exact_mode_still_rejects():
         ad.adapt_train(h, None)
     assert e.value.code == ad.ADAPT_E_TOO_MANY_DISTINCT
     ad.adapt_region_destroy(h)
+
+
+def _continuous_table(n, seed):
+    rng = np.random.default_rng(seed)
+    X = np.stack([rng.normal(size=n), rng.integers(0, 5, n), rng.uniform(0, 1e3, n)], 1).astype(np.float32)
+    T = rng.random((n, 4)).astype(np.float32)
+    T[:, 1] -= (X[:, 0] > 0.2) * 0.5
+    T[:, 3] -= (X[:, 2] < 300) * 0.4
+    return X, T
+
+
+def test_kfold_with_quantile_bins():
+    # the table is quantised once (its own quantiser); every fold's model is the
+    # exact CART of its quantised rows with raw thresholds from that quantiser
+    X, T = _continuous_table(6000, 4)
+    h = ad.adapt_region_create("q_kfold", 3, 4, "dtree,depth=5,bins=quantile", 0)
+    s = torch.cuda.current_stream()
+    ad.adapt_record_table(h, torch.from_numpy(X).to(DEV), torch.from_numpy(T).to(DEV), len(X), True, s)
+    got = ad.adapt_kfold(h, 4, 2, 2, 5, s)
+    q = oracle.quantizer(X)
+    y = oracle.labels(T)
+    for i, r in enumerate(got):
+        g = oracle.kfold_groups(5, int(r["shuffle"]), len(X), 4)
+        tr = np.isin(g, [(int(r["fold"]) + j) % 4 for j in range(2)])
+        ref = oracle.train_quantile(X[tr], y[tr], 4, 5, q=q)
+        assert ad.adapt_get_kfold_tree(h, i).tobytes() == ref.tobytes(), i
+        te = ~tr
+        sel = oracle.select(ref, X[te])
+        assert r["n_test"] == te.sum() and r["n_correct"] == int((sel == y[te]).sum())
+    ad.adapt_region_destroy(h)
+
+
+def test_forest_with_quantile_bins():
+    X, T = _continuous_table(5000, 6)
+    h = ad.adapt_region_create("q_rfc", 3, 4, "rfc,3,4,seed=2,bins=quantile", 0)
+    s = torch.cuda.current_stream()
+    ad.adapt_record_table(h, torch.from_numpy(X).to(DEV), torch.from_numpy(T).to(DEV), len(X), True, s)
+    ad.adapt_train(h, s)
+    q = oracle.quantizer(X)
+    y = oracle.labels(T)
+    for t in range(3):
+        w = oracle.bootstrap(2, t, len(X)).astype(np.int64)
+        ref = oracle.train_quantile(np.repeat(X, w, axis=0), np.repeat(y, w), 4, 4, q=q)
+        assert ad.adapt_get_forest_tree(h, t).tobytes() == ref.tobytes(), t
+    ad.adapt_region_destroy(h)
