@@ -295,6 +295,7 @@ def main():
     import torch
     import torch.distributed as dist
 
+    os.environ.setdefault("ADAPT_PROFILE_LEVELS", "1")  # per-level phase names (SURVEY §8(d) reporting)
     import paper_2303_08873_b200 as ad
     from paper_2303_08873_b200 import dist as adist
 
@@ -424,7 +425,22 @@ def main():
             dist.destroy_process_group()
         return
 
-    kern = {k: v for k, v in prof.items() if k.split("_L")[0] in KERNEL_PHASES}
+    # per-level phases (partition_L03, hist_L03, split_L03) -> the levels table;
+    # everything else is aggregated per kernel phase
+    per_level = {}
+    kern = {}
+    for k, v in prof.items():
+        base, _, lv = k.partition("_L")
+        if base not in KERNEL_PHASES:
+            continue
+        if lv.isdigit():
+            per_level.setdefault(int(lv), {})[base] = round(v["ms"] / args.steps, 4)
+        a = kern.setdefault(base, {"launches": 0, "ms": 0.0, "bytes": 0.0})
+        a["launches"] += v["launches"]
+        a["ms"] += v["ms"]
+        a["bytes"] += v["bytes"]
+    for i, lv in enumerate(levels):
+        lv["ms"] = per_level.get(i, {})
     dom = max(kern, key=lambda k: kern[k]["ms"])
     d = kern[dom]
     achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 and d["bytes"] > 0 else None

@@ -264,9 +264,12 @@ int adapt_profile_reset(void);
 /* Copies up to cap phases; *n receives the number of phases. Synchronizes
  * the recorded events. */
 int adapt_profile_get(adapt_phase_t *out, int cap, int *n);
-/* Per-level statistics of the last adapt_train on this rank: for level d,
- * out[3d] = frontier nodes, out[3d+1] = rows histogrammed, out[3d+2] = rows
- * partitioned.  *levels receives the level count. */
+/* Per-level statistics of the last adapt_train on this rank (SURVEY §8(d)
+ * per-level reporting): for level d, out[5d] = frontier nodes, out[5d+1] =
+ * rows histogrammed, out[5d+2] = rows partitioned, out[5d+3] = bytes of the
+ * level's node histograms (class-compacted, direct + derived), out[5d+4] =
+ * bytes all-reduced over ranks (0 on one rank).  *levels receives the level
+ * count (forests / K-fold: the levels of every tree / batch, in order). */
 int adapt_train_stats(adapt_region_t *h, int64_t *out, int cap, int *levels);
 
 /* ---- Apollo Table-1 shim (lowering order P:558-569) ------------- */

@@ -414,11 +414,13 @@ def adapt_profile_get() -> dict:
 
 
 def adapt_train_stats(h: int) -> list:
-    buf = np.zeros(3 * 64, np.int64)
     lv = ctypes.c_int()
+    _check(_L.adapt_train_stats(h, None, 0, ctypes.byref(lv)), "adapt_train_stats")
+    buf = np.zeros(5 * max(lv.value, 1), np.int64)
     _check(_L.adapt_train_stats(h, buf.ctypes.data, buf.size, ctypes.byref(lv)), "adapt_train_stats")
-    return [dict(nodes=int(buf[3 * d]), rows_hist=int(buf[3 * d + 1]), rows_part=int(buf[3 * d + 2]))
-            for d in range(min(lv.value, 64))]
+    return [dict(nodes=int(buf[5 * d]), rows_hist=int(buf[5 * d + 1]), rows_part=int(buf[5 * d + 2]),
+                 hist_bytes=int(buf[5 * d + 3]), comm_bytes=int(buf[5 * d + 4]))
+            for d in range(lv.value)]
 
 
 # ------------------------------------------------------ Apollo Table-1 shim --

@@ -1346,6 +1346,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
     h->stats.push_back(A);
     h->stats.push_back(htotal + ftotal);
     h->stats.push_back(rows_part);
+    h->stats.push_back((int64_t)soff[nslots] * 4);  // histogram bytes (direct + derived nodes)
+    h->stats.push_back(collectives_on() ? (int64_t)soff[ndirect_slots] * 4 : 0);  // all-reduced bytes
 
     // ---- decide every frontier node; build the next level ----
     std::vector<FNode> next;
@@ -2294,11 +2296,12 @@ int adapt_profile_get(adapt_phase_t *out, int cap, int *n) {
   });
 }
 
+constexpr size_t kStatsPerLevel = 5;
 int adapt_train_stats(adapt_region_t *h, int64_t *out, int cap, int *levels) {
   return guarded([&] {
     checked(h);
     if (!levels) throw Error(ADAPT_E_INVALID_ARG, "null levels");
-    *levels = (int)(h->stats.size() / 3);
+    *levels = (int)(h->stats.size() / kStatsPerLevel);
     for (size_t i = 0; i < h->stats.size() && (int)i < cap && out; i++) out[i] = h->stats[i];
   });
 }
