@@ -237,6 +237,56 @@ def bench_kfold(args, ad, adist, torch, dev, stream, rank: int, world: int):
             "test_accuracy": acc, "time_selected_over_best": slow}
 
 
+def bench_c2(args, ad, adist, torch, dev, stream, rank: int, world: int):
+    """C2 as BASELINE.json states it: 3 regions (region = row mod 3, R15), 1e5
+    profiled samples in total, 7 num_threads variants, depth 8 — the three
+    region trees in one adapt_train_many (one multi-root frontier over the
+    union table), timed against training the regions one by one."""
+    cfg = synth.CONFIGS["C2"]
+    X, T = synth.generate(cfg, 0, cfg.N)
+    hs, keep = [], []
+    for r in range(cfg.regions):
+        rows = synth.region_rows(cfg, r)
+        lo, hi = adist.shard_bounds(len(rows), rank, world)
+        dX = torch.from_numpy(np.ascontiguousarray(X[rows[lo:hi]])).to(dev)
+        dT = torch.from_numpy(np.ascontiguousarray(T[rows[lo:hi]])).to(dev)
+        keep.append((dX, dT))
+        hs.append(ad.adapt_region_create(f"bench_c2_r{r}", cfg.F, cfg.V, f"dtree,depth={cfg.D}", 0))
+
+    def record():
+        for h, (dX, dT) in zip(hs, keep):
+            ad.adapt_record_table(h, dX, dT, dX.shape[0], True, stream)
+
+    def fused():
+        record()
+        ad.adapt_train_many(hs, stream)
+
+    def one_by_one():
+        record()
+        for h in hs:
+            ad.adapt_train(h, stream)
+
+    res = {"workload": "C2: 3 regions (row mod 3), 1e5 samples in total, 4 features, 7 variants, depth 8",
+           "regions": cfg.regions, "rows": cfg.N, "steps": args.steps}
+    for name, fn in (("train_many_ms", fused), ("one_by_one_ms", one_by_one)):
+        for _ in range(max(args.warmup, 1)):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res[name] = adist.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
+    res["samples_per_s"] = cfg.N / (res["train_many_ms"] / 1e3)
+    for h in hs:
+        ad.adapt_region_destroy(h)
+    return res
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
@@ -284,6 +334,7 @@ def main():
     ap.add_argument("--c5-train-rows", type=int, default=10_000_000)
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-kfold", action="store_true")
+    ap.add_argument("--no-c2", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -415,6 +466,9 @@ def main():
         del X, T, out
         torch.cuda.empty_cache()
         c5 = bench_c5(args, ad, adist, torch, dev, stream, rank, world, peak)
+    c2 = None
+    if not args.no_c2 and args.config == "C4":
+        c2 = bench_c2(args, ad, adist, torch, dev, stream, rank, world)
     kfold = None
     if not args.no_kfold and args.config == "C4":
         kfold = bench_kfold(args, ad, adist, torch, dev, stream, rank, world)
@@ -494,6 +548,7 @@ def main():
         "record_path": rec,
         "select_c5": c5,
         "kfold": kfold,
+        "c2_regions": c2,
         "phase_ms_per_step": step_ms_phases,
         "tree_nodes": int(len(tree)),
         "levels": levels,

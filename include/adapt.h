@@ -187,7 +187,16 @@ int adapt_distinct_pairs(adapt_region_t *h, int64_t *count);
  * E_TOO_MANY_DISTINCT, E_CUDA, E_NCCL, E_OOM.  On error the region keeps its
  * previous model, if any. */
 int adapt_train(adapt_region_t *h, void *cuda_stream);
-/* k independent regions trained in one call (C2's "3 regions"; R15). */
+/* k independent regions trained in one call (C2's "3 regions"; R15).  When
+ * k >= 2 decision-tree regions share (F, V, D), are not in bins=quantile
+ * mode and each holds a recorded wide table, they are trained FUSED: one
+ * ingest over the union of their tables and one level loop whose frontier
+ * starts with k roots.  Trees and labels are each region's own (thresholds
+ * are node-local midpoints, R7, so the union's value tables only re-index
+ * the bins); adapt_get_value_table / adapt_get_bins of such a region report
+ * the union's value tables and ranks in them.  If the union has more than 256
+ * distinct values of a feature, or a region has no rows, or the specs differ,
+ * the regions are trained one by one (adapt_train each, in order). */
 int adapt_train_many(adapt_region_t *const *hs, int k, void *cuda_stream);
 
 /* ---- select (Table 1 "__apollo_region_get_policy") ---------------- */

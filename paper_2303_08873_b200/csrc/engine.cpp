@@ -385,6 +385,10 @@ struct adapt_region {
     adapt_kfold_result_t *out;
   };
   const KfoldSpec *kfold = nullptr;
+  // adapt_train_many (fused): this internal region's table is the union of k
+  // regions' tables; multi_n[r] = region r's rows on this rank, in order
+  const std::vector<int64_t> *multi_n = nullptr;
+  std::vector<std::vector<adapt_node_t>> multi_trees;
   std::vector<std::vector<adapt_node_t>> kfold_trees;
   adapt::DevBuf flagsum;  // error-flag sums over ranks
   adapt::DevBuf kbnd, kpart, kgrp, kcnt, kcur, ksb, klab, knodes, kroots;
@@ -1537,6 +1541,52 @@ void train_region(adapt_region *h, cudaStream_t s) {
     return lo;
   };
 
+  if (h->multi_n) {  // adapt_train_many: k regions' trees in ONE multi-root frontier (C2, R15)
+    const auto &mn = *h->multi_n;
+    const int R = (int)mn.size();
+    std::vector<uint64_t> tot(mn.begin(), mn.end());
+    if (collectives_on()) {
+      DevBuf t;
+      t.ensure((size_t)R * 8);
+      CUDA_CHECK(cudaMemcpyAsync(t.p, tot.data(), (size_t)R * 8, cudaMemcpyHostToDevice, s));
+      comm_allreduce_sum(t.p, (size_t)R, true, s, "allreduce region rows");
+      CUDA_CHECK(cudaMemcpyAsync(tot.data(), t.p, (size_t)R * 8, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    for (int r = 0; r < R; r++)
+      if (tot[r] == 0) throw Error(ADAPT_E_INSUFFICIENT_DATA, "a region has no rows");
+    MultiRoot mr;
+    mr.R = R;
+    mr.bins = h->bins.as<uint8_t>();
+    mr.labs = h->labels.as<uint8_t>();
+    mr.pstride = pstride;
+    mr.rows_out = n;
+    mr.pieces.resize(R);
+    int64_t off = 0;
+    for (int r = 0; r < R; r++) {
+      if (mn[r]) mr.pieces[r].push_back({(uint32_t)off, (uint32_t)mn[r]});
+      off += mn[r];
+    }
+    grow_tree(nullptr, &mr);
+    h->multi_trees.assign(R, {});
+    for (int r = 0; r < R; r++) {  // canonical BFS per region (BFS from its root)
+      auto &tr = h->multi_trees[r];
+      std::vector<int32_t> q{r};
+      for (size_t qi = 0; qi < q.size(); qi++) {
+        adapt_node_t nd = h->tree[q[qi]];
+        if (nd.feature >= 0) {
+          q.push_back(nd.left);
+          q.push_back(nd.right);
+          nd.left = (int32_t)(q.size() - 2);
+          nd.right = (int32_t)(q.size() - 1);
+        }
+        tr.push_back(nd);
+      }
+    }
+    h->trained_n = n;
+    return;
+  }
+
   if (h->kfold) {  // K-fold harness (R22): all models of a batch of shuffles in ONE frontier
     const auto &kf = *h->kfold;
     const int K = kf.K, m = kf.m;
@@ -2048,8 +2098,117 @@ int adapt_train(adapt_region_t *h, void *stream) {
   });
 }
 
+namespace adapt {
+namespace {
+// adapt_train_many for k >= 2 decision-tree regions with equal (F, V, D) and
+// recorded wide tables: ONE ingest over the union of their tables and ONE
+// level loop whose frontier starts with k roots (each region's rows).  The
+// union's value tables only re-index the bins: thresholds are node-local
+// midpoints of the values present (R7), so every region's tree is the one
+// adapt_train would build.  Returns false (nothing changed) when the fused
+// path does not apply; the caller then trains the regions one by one.
+std::unique_ptr<adapt_region> g_multi;  // the union region (buffers reused across calls)
+
+bool train_many_fused(adapt_region *const *hs, int k, cudaStream_t s) {
+  if (k < 2) return false;
+  const adapt_region *h0 = hs[0];
+  for (int r = 0; r < k; r++) {
+    const adapt_region *h = hs[r];
+    if (h->kind != 0 || h->quantile || !h->have_table || h->F != h0->F || h->V != h0->V || h->D != h0->D)
+      return false;
+    for (int q = 0; q < r; q++)
+      if (hs[q] == h) return false;
+  }
+  if (!g_multi) g_multi = std::make_unique<adapt_region>();
+  adapt_region *u = g_multi.get();
+  u->id = "__adapt_train_many";
+  u->F = h0->F;
+  u->V = h0->V;
+  u->D = h0->D;
+  u->kind = 0;
+  std::vector<int64_t> mn(k);
+  int64_t n = 0;
+  for (int r = 0; r < k; r++) n += (mn[r] = hs[r]->n);
+  const int F = u->F, V = u->V;
+  u->own_feat.ensure((size_t)std::max<int64_t>(n, 1) * F * 4 + 16);
+  u->own_times.ensure((size_t)std::max<int64_t>(n, 1) * V * 4 + 16);
+  int64_t off = 0;
+  for (int r = 0; r < k; r++) {
+    if (mn[r]) {
+      CUDA_CHECK(cudaMemcpyAsync(u->own_feat.as<float>() + off * F, hs[r]->d_feat, (size_t)mn[r] * F * 4,
+                                 cudaMemcpyDeviceToDevice, s));
+      CUDA_CHECK(cudaMemcpyAsync(u->own_times.as<float>() + off * V, hs[r]->d_times, (size_t)mn[r] * V * 4,
+                                 cudaMemcpyDeviceToDevice, s));
+    }
+    off += mn[r];
+  }
+  u->n = n;
+  u->have_table = true;
+  u->d_feat = u->own_feat.as<float>();
+  u->d_times = u->own_times.as<float>();
+  u->multi_n = &mn;
+  try {
+    train_region(u, s);
+  } catch (const Error &e) {
+    u->multi_n = nullptr;
+    if (e.code == ADAPT_E_TOO_MANY_DISTINCT || e.code == ADAPT_E_INSUFFICIENT_DATA)
+      return false;  // the union overflows 256 values / an empty region: one by one
+    throw;
+  }
+  u->multi_n = nullptr;
+  // every region: its tree, and its slice of the union's labels and bins
+  off = 0;
+  for (int r = 0; r < k; r++) {
+    adapt_region *h = hs[r];
+    const int64_t nr = mn[r];
+    h->BS = u->BS;
+    h->pstride = bins_plane_stride(nr, u->BS);
+    h->bins.ensure(bins_bytes(nr, u->BS));
+    h->labels.ensure((size_t)std::max<int64_t>(nr, 1) + 64);
+    const int planes = u->BS < 4 ? 1 : u->BS / 4, wb = u->BS < 4 ? u->BS : 4;
+    if (nr) {
+      for (int p = 0; p < planes; p++)
+        CUDA_CHECK(cudaMemcpyAsync(h->bins.as<uint8_t>() + p * h->pstride,
+                                   u->bins.as<uint8_t>() + p * u->pstride + off * wb, (size_t)nr * wb,
+                                   cudaMemcpyDeviceToDevice, s));
+      CUDA_CHECK(cudaMemcpyAsync(h->labels.p, u->labels.as<uint8_t>() + off, (size_t)nr,
+                                 cudaMemcpyDeviceToDevice, s));
+    }
+    h->val = u->val;
+    h->nval = u->nval;
+    h->qmask = 0;
+    h->tree = std::move(u->multi_trees[r]);
+    h->forest.clear();
+    h->stats = u->stats;
+    h->aggregated = false;
+    h->trained_n = nr;
+    h->trained = true;
+    upload_tree(h, s);
+    off += nr;
+  }
+  return true;
+}
+}  // namespace
+}  // namespace adapt
+
 int adapt_train_many(adapt_region_t *const *hs, int k, void *stream) {
   if (!hs || k < 0) return guarded([&] { throw Error(ADAPT_E_INVALID_ARG, "bad region list"); });
+  bool fused = false;
+  const int rc = guarded([&] {
+    for (int i = 0; i < k; i++) checked(hs[i]);
+    ensure_init();
+    fused = train_many_fused(hs, k, (cudaStream_t)stream);
+    if (fused)
+      for (int i = 0; i < k; i++) {
+        adapt_region *h = hs[i];
+        if (h->have_table && h->d_feat != h->own_feat.as<float>()) {
+          h->d_feat = nullptr;  // borrowed pointers are released when train returns
+          h->d_times = nullptr;
+          h->have_table = false;
+        }
+      }
+  });
+  if (rc || fused) return rc;
   for (int i = 0; i < k; i++) {
     int rc = adapt_train(hs[i], stream);
     if (rc) return rc;

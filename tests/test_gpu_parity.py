@@ -127,6 +127,64 @@ def test_c2_three_regions():
         assert_tree_equal(ad.adapt_get_tree(h), ref)
 
 
+def test_train_many_fused_and_fallbacks():
+    # fused (one multi-root frontier over the union table): trees and labels per
+    # region; bins are ranks in the union's value tables.  Fallbacks: a union
+    # with > 256 values of a feature (each region <= 256), different specs, an
+    # empty region (its error, as adapt_train would raise it).
+    rng = np.random.default_rng(21)
+    s = torch.cuda.current_stream()
+    keep = []
+
+    def region(X, T, D):
+        h = _region(X.shape[1], T.shape[1], D)
+        dX, dT = torch.from_numpy(X).to(DEV), torch.from_numpy(T).to(DEV)
+        keep.append((dX, dT))
+        ad.adapt_record_table(h, dX, dT, len(X), True, s)
+        return h
+
+    tabs = []
+    for r in range(4):
+        n = int(rng.integers(50, 4000))
+        X = rng.choice(np.arange(40, dtype=np.float32) + 100 * r, size=(n, 3)).astype(np.float32)
+        T = rng.random((n, 5)).astype(np.float32)
+        tabs.append((X, T))
+    hs = [region(X, T, 6) for X, T in tabs]
+    ad.adapt_train_many(hs, s)
+    Xu = np.concatenate([X for X, _ in tabs])
+    for h, (X, T) in zip(hs, tabs):
+        y = oracle.labels(T)
+        assert_tree_equal(ad.adapt_get_tree(h), oracle.train(X, y, 5, 6))
+        assert np.array_equal(ad.adapt_get_labels(h, len(X)), y)
+        assert np.array_equal(ad.adapt_get_value_table(h, 1), oracle.value_table(Xu, 1))
+        assert np.array_equal(ad.adapt_get_bins(h, len(X), 3),
+                              np.stack([np.searchsorted(oracle.value_table(Xu, f), X[:, f]) for f in range(3)],
+                                       1).astype(np.uint8))
+        out = torch.empty(len(X), dtype=torch.int32, device=DEV)
+        ad.adapt_select_batch(h, torch.from_numpy(X).to(DEV), len(X), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), oracle.select(oracle.train(X, y, 5, 6), X))
+    # union of 3 x 200 distinct values > 256: one by one
+    tabs2 = [(rng.choice(np.arange(200, dtype=np.float32) + 1000 * r, size=(3000, 2)).astype(np.float32),
+              rng.random((3000, 4)).astype(np.float32)) for r in range(3)]
+    hs2 = [region(X, T, 5) for X, T in tabs2]
+    ad.adapt_train_many(hs2, s)
+    for h, (X, T) in zip(hs2, tabs2):
+        assert_tree_equal(ad.adapt_get_tree(h), oracle.train(X, oracle.labels(T), 4, 5))
+        assert np.array_equal(ad.adapt_get_value_table(h, 0), oracle.value_table(X, 0))
+    # different depths: one by one
+    hs3 = [region(*tabs[0], 3), region(*tabs[1], 4)]
+    ad.adapt_train_many(hs3, s)
+    assert_tree_equal(ad.adapt_get_tree(hs3[1]), oracle.train(tabs[1][0], oracle.labels(tabs[1][1]), 5, 4))
+    # an empty region: the error adapt_train raises for it
+    hs4 = [region(*tabs[0], 3), region(tabs[1][0][:0], tabs[1][1][:0], 3)]
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_train_many(hs4, s)
+    assert e.value.code == ad.ADAPT_E_INSUFFICIENT_DATA
+    for h in hs + hs2 + hs3 + hs4:
+        ad.adapt_region_destroy(h)
+
+
 def test_c3_full():
     cfg = synth.CONFIGS["C3"]
     X, T = synth.generate(cfg, 0, cfg.N)
