@@ -287,6 +287,38 @@ def bench_c2(args, ad, adist, torch, dev, stream, rank: int, world: int):
     return res
 
 
+def bench_c1(args, ad, torch, dev, stream):
+    """C1 at the paper's own scale (Table 4: 60-280 us to train a
+    depth-2 tree on ~10 tuples, 7-20 ns per inference): latency of one
+    adapt_train on C1's 512 profiled samples (depth 4, device tables; the call
+    returns with the tree on the host) and of one host-side get_policy walk
+    (adapt_select), host wall clock, median of many calls."""
+    cfg = synth.CONFIGS["C1"]
+    X, T = synth.generate(cfg, 0, cfg.N)
+    dX, dT = torch.from_numpy(X).to(dev), torch.from_numpy(T).to(dev)
+    h = ad.adapt_region_create("bench_c1", cfg.F, cfg.V, f"dtree,depth={cfg.D}", 0)
+    lat = []
+    for i in range(60):
+        ad.adapt_record_table(h, dX, dT, cfg.N, True, stream)
+        t0 = time.perf_counter()
+        ad.adapt_train(h, stream)
+        if i >= 10:
+            lat.append((time.perf_counter() - t0) * 1e6)
+    xs = [X[i] for i in range(0, cfg.N, 7)]
+    t0 = time.perf_counter()
+    reps = 200
+    for _ in range(reps):
+        for x in xs:
+            ad.adapt_select(h, x)
+    sel_ns = (time.perf_counter() - t0) * 1e9 / (reps * len(xs))
+    ad.adapt_region_destroy(h)
+    return {"workload": "C1: 512 profiled samples, 1 feature, 2 variants, depth 4",
+            "train_us_median": statistics.median(lat), "train_us_min": min(lat),
+            "select_host_ns_per_call": sel_ns,
+            "note": "adapt_select through the ctypes binding (includes Python call overhead); "
+                    "paper Table 4: 60-280 us training, 7-20 ns per inference on the host"}
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
@@ -466,6 +498,7 @@ def main():
         del X, T, out
         torch.cuda.empty_cache()
         c5 = bench_c5(args, ad, adist, torch, dev, stream, rank, world, peak)
+    c1 = bench_c1(args, ad, torch, dev, stream) if (not args.no_c2 and args.config == "C4" and world == 1) else None
     c2 = None
     if not args.no_c2 and args.config == "C4":
         c2 = bench_c2(args, ad, adist, torch, dev, stream, rank, world)
@@ -549,6 +582,7 @@ def main():
         "select_c5": c5,
         "kfold": kfold,
         "c2_regions": c2,
+        "c1_latency": c1,
         "phase_ms_per_step": step_ms_phases,
         "tree_nodes": int(len(tree)),
         "levels": levels,

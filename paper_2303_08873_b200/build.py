@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libadapt.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["ingest.cu", "level.cu", "train.cu", "select.cu", "records.cu", "forest.cu", "kfold.cu", "quantile.cu", "engine.cpp"]
+SOURCES = ["ingest.cu", "level.cu", "train.cu", "select.cu", "records.cu", "forest.cu", "kfold.cu", "quantile.cu", "small.cu", "engine.cpp"]
 
 
 def _git() -> str:

@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include "adapt.h"
+
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -218,6 +220,20 @@ void sort_unique_keys(const uint32_t *keys, int64_t n, uint32_t *sorted, uint32_
 void launch_edges(const uint32_t *ukeys, int64_t D, float *lb, float *prev, cudaStream_t s);
 void launch_quantize(const float *X, int64_t n, int F, uint64_t qmask, const float *lb, float *Xq,
                      cudaStream_t s);
+
+// ---- small.cu: the whole path for small tables in one thread block ----
+constexpr int kSmallMaxN = 512, kSmallMaxF = 8, kSmallMaxC = 16, kSmallMaxA = 64, kSmallMaxNodes = 2112;
+struct SmallOut {
+  int32_t status;   // 0: trained; 1: outside the limits or a flagged value (use the general path)
+  int32_t n_nodes;
+  int32_t nval[kSmallMaxF];
+  float val[kSmallMaxF][256];
+  adapt_node_t nodes[kSmallMaxNodes];
+};
+size_t small_smem_bytes();
+// labels -> labels[n], bins -> word planes (BS, pstride) like the ingest, tree -> out
+void launch_small_train(const float *X, const float *T, int n, int F, int V, int D, int BS, size_t pstride,
+                        uint8_t *bins, uint8_t *labels, SmallOut *out, cudaStream_t s);
 
 // ---- kernel launchers (kfold.cu): the K-fold harness ----
 constexpr int kKfoldMaxK = 64;

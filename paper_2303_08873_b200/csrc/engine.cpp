@@ -391,6 +391,7 @@ struct adapt_region {
   std::vector<std::vector<adapt_node_t>> multi_trees;
   std::vector<std::vector<adapt_node_t>> kfold_trees;
   adapt::DevBuf flagsum;  // error-flag sums over ranks
+  adapt::DevBuf dsmall;   // small.cu result (SmallOut)
   adapt::DevBuf kbnd, kpart, kgrp, kcnt, kcur, ksb, klab, knodes, kroots;
   bool trained = false;
   std::vector<int64_t> stats;
@@ -745,6 +746,39 @@ void train_region(adapt_region *h, cudaStream_t s) {
   h->pstride = pstride;
   h->bins.ensure(bins_bytes(n, BS));
   h->labels.ensure((size_t)std::max<int64_t>(n, 1) + 64);
+  // small tables (the paper's run-time scale): the whole path in one thread
+  // block, one launch, one wait (small.cu); falls through to the general path
+  // when a limit or a flagged value says so
+  static const bool no_small = getenv("ADAPT_NO_SMALL") != nullptr;
+  if (!no_small && !collectives_on() && h->kind == 0 && !h->quantile && !h->kfold && !h->multi_n &&
+      n >= 1 && n <= kSmallMaxN && F <= kSmallMaxF && V <= kSmallMaxC) {
+    h->hres.ensure(sizeof(SmallOut));
+    h->dsmall.ensure(sizeof(SmallOut));
+    {
+      Phase ph("small", s, (double)n * (4.0 * F + 4.0 * V + F + 1));
+      launch_small_train(feat, times, (int)n, F, V, D, BS, pstride, h->bins.as<uint8_t>(),
+                         h->labels.as<uint8_t>(), h->dsmall.as<SmallOut>(), s);
+    }
+    SmallOut *so = h->hres.as<SmallOut>();
+    CUDA_CHECK(cudaMemcpyAsync(so, h->dsmall.p, sizeof(SmallOut), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (so->status == 0) {
+      h->val.assign((size_t)F * kMaxBins, 0.f);
+      h->nval.assign(F, 0);
+      for (int f = 0; f < F; f++) {
+        h->nval[f] = so->nval[f];
+        memcpy(&h->val[(size_t)f * kMaxBins], so->val[f], (size_t)so->nval[f] * 4);
+      }
+      h->qmask = 0;
+      h->tree.assign(so->nodes, so->nodes + so->n_nodes);
+      h->forest.clear();
+      h->stats.clear();
+      h->trained_n = n;
+      h->trained = true;
+      upload_tree(h, s);
+      return;
+    }
+  }
   h->lvals.ensure((size_t)F * kMaxBins * 4);
   h->lcnt.ensure((size_t)F * 4);
   h->avals.ensure((size_t)world * F * kMaxBins * 4);
