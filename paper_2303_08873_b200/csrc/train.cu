@@ -409,6 +409,9 @@ __global__ void __launch_bounds__(256)
   __shared__ SplitCand s_c;
   __shared__ unsigned long long s_n;
   const int node = blockIdx.x, t = threadIdx.x;
+  __shared__ SplitCand sc[kMaxF];  // the node's F candidates, loaded in parallel
+  for (int f = t; f < F; f += blockDim.x) sc[f] = cand[(size_t)node * F + f];
+  __syncthreads();
   if (t == 0) {
     int bf = -1;
     Key bk;
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(256)
     bk.hi = bk.lo = 0;
     bk.den = 1;
     for (int f = 0; f < F; f++) {
-      const SplitCand &c = cand[(size_t)node * F + f];
+      const SplitCand &c = sc[f];
       Key k;
       k.valid = c.valid;
       k.idx = f;
@@ -430,7 +433,7 @@ __global__ void __launch_bounds__(256)
       }
     }
     s_f = bf;
-    if (bf >= 0) s_c = cand[(size_t)node * F + bf];
+    if (bf >= 0) s_c = sc[bf];
     s_n = 0;
   }
   __syncthreads();
