@@ -13,6 +13,7 @@
 // walk the current one out of the warp's odd-stride shared-memory tile, two
 // independent walks per lane interleaved to hide the dependent smem latency.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.h"
 
@@ -149,6 +150,113 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   }
 }
 
+// x[f] of a vector held in registers (N = 4, 8 or 16, a power of two): a
+// select tree on the bits of f, all indices compile-time, no local memory
+template <int N>
+__device__ __forceinline__ float pick(const float (&x)[N], int f) {
+  float t[N];
+#pragma unroll
+  for (int i = 0; i < N; i++) t[i] = x[i];
+#pragma unroll
+  for (int b = 0; (1 << b) < N; b++) {
+    const bool hi = (f >> b) & 1;
+#pragma unroll
+    for (int i = 0; i < (N >> (b + 1)); i++) t[i] = hi ? t[2 * i + 1] : t[2 * i];
+  }
+  return t[0];
+}
+
+template <int N>
+__device__ __forceinline__ int walk_block_r(const uint4 (&w)[4], const float (&x)[N]) {
+  const float t0 = __uint_as_float(w[0].x);
+  const bool g0 = !(pick<N>(x, w[1].w & 63) <= t0);  // NaN -> right (R8)
+  const float t1 = __uint_as_float(g0 ? w[0].z : w[0].y);
+  const bool g1 = !(pick<N>(x, (g0 ? w[2].y : w[2].x) & 63) <= t1);
+  const uint32_t tw = g0 ? (g1 ? w[1].z : w[1].y) : (g1 ? w[1].x : w[0].w);
+  const uint32_t fw = g0 ? (g1 ? w[3].y : w[3].x) : (g1 ? w[2].w : w[2].z);
+  const bool g2 = !(pick<N>(x, fw & 63) <= __uint_as_float(tw));
+  uint32_t r;
+  if (g0)
+    r = g1 ? (g2 ? w[3].z : w[3].y) : (g2 ? w[3].x : w[2].w);
+  else
+    r = g1 ? (g2 ? w[2].z : w[2].y) : (g2 ? w[2].x : w[1].w);
+  return (int32_t)r >> 6;
+}
+
+// One vector per lane, its features in REGISTERS: the walk reads only tree
+// nodes from shared memory (the random-feature reads of the vector tile were
+// half of the LSU wavefronts that bound the smem-x kernel above); the vector
+// reaches registers through the same coalesced tile, one uniform-feature (so
+// conflict-free) read per feature.
+template <int F>
+__global__ void __launch_bounds__(kSelThreads, 1)
+    select_kernel_r(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
+                    const float *__restrict__ X, int64_t m, int32_t *__restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int kStride = F | 1;
+  constexpr int kVec = F / 4;
+  constexpr int kRows = 32;                // one vector per lane
+  constexpr int kLd = kRows * kVec / 32;   // float4 loads per lane per tile
+  constexpr int NP = F <= 4 ? 4 : (F <= 8 ? 8 : 16);
+  DNode *st = reinterpret_cast<DNode *>(smem);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  float *sx = reinterpret_cast<float *>(smem + (size_t)kTopNodes * sizeof(DNode)) + (size_t)warp * kRows * kStride;
+  for (int i = t; i < n_top; i += kSelThreads) st[i] = gtree[i];
+  __syncthreads();
+  const int64_t ntiles = (m + kRows - 1) / kRows;
+  const int64_t nwarps = (int64_t)gridDim.x * (kSelThreads / 32);
+  float4 pre[kLd];
+  auto fetch = [&](int64_t tile) {
+    const int64_t v0 = tile * kRows;
+    const int rows = (m - v0 < kRows) ? (int)(m - v0) : kRows;
+    const float4 *src = reinterpret_cast<const float4 *>(X + v0 * F);
+#pragma unroll
+    for (int k = 0; k < kLd; k++) {
+      const int i = lane + 32 * k;
+      pre[k] = i < rows * kVec ? __ldcs(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  int64_t tile = blockIdx.x * (int64_t)(kSelThreads / 32) + warp;
+  if (tile < ntiles) fetch(tile);
+  for (; tile < ntiles; tile += nwarps) {
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kLd; k++) {
+      const int i = lane + 32 * k, r = i / kVec, c = (i % kVec) * 4;
+      float *d = sx + r * kStride + c;
+      d[0] = pre[k].x;
+      d[1] = pre[k].y;
+      d[2] = pre[k].z;
+      d[3] = pre[k].w;
+    }
+    __syncwarp();
+    float xr[NP];
+#pragma unroll
+    for (int f = 0; f < NP; f++) xr[f] = f < F ? sx[lane * kStride + f] : 0.f;
+    if (tile + nwarps < ntiles) fetch(tile + nwarps);  // next tile in flight during the walk
+    const int64_t v = tile * kRows + lane;
+    DNode nd = st[0];
+    int ref = nd.meta;
+    while (nd.meta >= 0) {  // the shared-memory top
+      const float xv = pick<NP>(xr, nd.meta & 63);
+      const int k = (nd.meta >> 6) + (xv <= nd.thr ? 0 : 1);  // NaN -> right (R8)
+      if (k < n_top) {
+        nd = st[k];
+        ref = nd.meta;
+      } else {
+        ref = k - n_top;
+        break;
+      }
+    }
+    while (ref >= 0) {  // bottom blocks
+      uint4 w[4];
+      load_block(blocks, ref, w);
+      ref = walk_block_r<NP>(w, xr);
+    }
+    if (v < m) __stcs(out + v, -1 - ref);
+  }
+}
+
 // generic F (not a multiple of 4, or an unaligned X): scalar staging
 __global__ void __launch_bounds__(kAnyThreads, 1)
     select_kernel_any(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
@@ -202,6 +310,7 @@ void launch_select(const DNode *tree, int n_nodes, const uint4 *blocks, const fl
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool vec = (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  static const bool smem_x = getenv("ADAPT_SEL_SMEMX") != nullptr;  // the smem-x kernel (A/B)
   const size_t tree_b = (size_t)kTopNodes * sizeof(DNode);
   // F <= 16, 16-byte aligned X: per-warp tiles, one 1024-thread CTA per SM
   const int64_t wtiles = (m + 32 * kSelChains - 1) / (32 * kSelChains);
@@ -209,9 +318,17 @@ void launch_select(const DNode *tree, int n_nodes, const uint4 *blocks, const fl
   switch (vec ? F : 0) {
 #define CASE(FF)                                                                               \
   case FF: {                                                                                   \
-    const size_t smem = tree_b + (size_t)kSelThreads * kSelChains * (FF | 1) * 4;              \
-    smem_limit(select_kernel<FF>, smem);   \
-    select_kernel<FF><<<vgrid, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, out);                \
+    if (smem_x) {                                                                              \
+      const size_t smem = tree_b + (size_t)kSelThreads * kSelChains * (FF | 1) * 4;            \
+      smem_limit(select_kernel<FF>, smem);                                                     \
+      select_kernel<FF><<<vgrid, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, out);      \
+    } else {                                                                                   \
+      const size_t smem = tree_b + (size_t)kSelThreads * (FF | 1) * 4;                         \
+      const int64_t tiles = (m + 31) / 32;                                                     \
+      const int g = (int)std::min<int64_t>((tiles + kSelThreads / 32 - 1) / (kSelThreads / 32), sms); \
+      smem_limit(select_kernel_r<FF>, smem);                                                   \
+      select_kernel_r<FF><<<g, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, out);        \
+    }                                                                                          \
     break;                                                                                     \
   }
     CASE(4) CASE(8) CASE(12) CASE(16)
