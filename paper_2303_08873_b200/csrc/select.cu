@@ -4,7 +4,9 @@
 //
 // The device tree is a BFS array of 8-byte nodes; the threshold is stored as
 // the largest float32 <= the double threshold, which makes the float compare
-// exact (V:A5).  The first kTopNodes nodes (the top levels every walk visits;
+// exact (V:A5).  The product kernel is select_kernel_d (each lane loads its
+// vector straight into registers; below); the tile kernels are kept for A/B
+// (ADAPT_SEL_TILE / ADAPT_SEL_SMEMX).  The first kTopNodes nodes (the top levels every walk visits;
 // a whole depth-12 tree) sit in shared memory; below them the tree is stored
 // as 64-byte blocks of 3 levels (common.h), read with four independent
 // 16-byte loads, so a depth-16 walk pays one L2 round trip below the top
@@ -257,6 +259,74 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   }
 }
 
+// As select_kernel_r, but every lane loads its own vector straight into
+// registers (256-bit loads when the rows are 32-byte aligned): no staging tile,
+// no shared-memory stores or feature reads at all; the next vector's loads are
+// in flight during the walk.
+template <int F>
+__device__ __forceinline__ void load_vec(const float *__restrict__ p, bool wide, float (&x)[F]) {
+  if constexpr (F % 8 == 0) {
+    if (wide) {
+#pragma unroll
+      for (int i = 0; i < F; i += 8)
+        asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=f"(x[i]), "=f"(x[i + 1]), "=f"(x[i + 2]), "=f"(x[i + 3]), "=f"(x[i + 4]), "=f"(x[i + 5]),
+              "=f"(x[i + 6]), "=f"(x[i + 7])
+            : "l"(p + i));
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < F; i += 4) {
+    const float4 v = __ldcs(reinterpret_cast<const float4 *>(p + i));
+    x[i] = v.x;
+    x[i + 1] = v.y;
+    x[i + 2] = v.z;
+    x[i + 3] = v.w;
+  }
+}
+
+template <int F>
+__global__ void __launch_bounds__(kSelThreads, 1)
+    select_kernel_d(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
+                    const float *__restrict__ X, int64_t m, int wide, int32_t *__restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int NP = F <= 4 ? 4 : (F <= 8 ? 8 : 16);
+  DNode *st = reinterpret_cast<DNode *>(smem);
+  const int t = threadIdx.x;
+  for (int i = t; i < n_top; i += kSelThreads) st[i] = gtree[i];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kSelThreads;
+  int64_t v = blockIdx.x * (int64_t)kSelThreads + t;
+  float nx[F];
+  if (v < m) load_vec<F>(X + v * F, wide, nx);
+  for (; v < m; v += stride) {
+    float xr[NP];
+#pragma unroll
+    for (int f = 0; f < NP; f++) xr[f] = f < F ? nx[f] : 0.f;
+    if (v + stride < m) load_vec<F>(X + (v + stride) * F, wide, nx);  // next vector in flight
+    DNode nd = st[0];
+    int ref = nd.meta;
+    while (nd.meta >= 0) {
+      const float xv = pick<NP>(xr, nd.meta & 63);
+      const int k = (nd.meta >> 6) + (xv <= nd.thr ? 0 : 1);  // NaN -> right (R8)
+      if (k < n_top) {
+        nd = st[k];
+        ref = nd.meta;
+      } else {
+        ref = k - n_top;
+        break;
+      }
+    }
+    while (ref >= 0) {
+      uint4 w[4];
+      load_block(blocks, ref, w);
+      ref = walk_block_r<NP>(w, xr);
+    }
+    __stcs(out + v, -1 - ref);
+  }
+}
+
 // generic F (not a multiple of 4, or an unaligned X): scalar staging
 __global__ void __launch_bounds__(kAnyThreads, 1)
     select_kernel_any(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
@@ -311,6 +381,8 @@ void launch_select(const DNode *tree, int n_nodes, const uint4 *blocks, const fl
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool vec = (reinterpret_cast<uintptr_t>(X) & 15) == 0;
   static const bool smem_x = getenv("ADAPT_SEL_SMEMX") != nullptr;  // the smem-x kernel (A/B)
+  // default: per-lane vector loads (select_kernel_d); A/B: the tile kernels
+  static const bool direct = getenv("ADAPT_SEL_TILE") == nullptr && !smem_x;
   const size_t tree_b = (size_t)kTopNodes * sizeof(DNode);
   // F <= 16, 16-byte aligned X: per-warp tiles, one 1024-thread CTA per SM
   const int64_t wtiles = (m + 32 * kSelChains - 1) / (32 * kSelChains);
@@ -318,7 +390,13 @@ void launch_select(const DNode *tree, int n_nodes, const uint4 *blocks, const fl
   switch (vec ? F : 0) {
 #define CASE(FF)                                                                               \
   case FF: {                                                                                   \
-    if (smem_x) {                                                                              \
+    if (direct) {                                                                              \
+      const int wide = (reinterpret_cast<uintptr_t>(X) & 31) == 0;                             \
+      const int64_t blocks_needed = (m + kSelThreads - 1) / kSelThreads;                       \
+      const int g = (int)std::min<int64_t>(blocks_needed, sms);                                \
+      smem_limit(select_kernel_d<FF>, tree_b);                                                 \
+      select_kernel_d<FF><<<g, kSelThreads, tree_b, s>>>(tree, n_top, blocks, X, m, wide, out); \
+    } else if (smem_x) {                                                                       \
       const size_t smem = tree_b + (size_t)kSelThreads * kSelChains * (FF | 1) * 4;            \
       smem_limit(select_kernel<FF>, smem);                                                     \
       select_kernel<FF><<<vgrid, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, out);      \
