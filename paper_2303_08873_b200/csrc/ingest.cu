@@ -236,7 +236,10 @@ __global__ void merge_values_kernel(const float *all_vals, const int32_t *all_cn
 // lanes per row): it labels them, bins them, writes its rows' bins and labels
 // straight to global memory and arrives on the stage's "empty" mbarrier.
 constexpr int kIngestThreads = 1024;
-constexpr int kStages = 2;
+#ifndef ADAPT_INGEST_STAGES
+#define ADAPT_INGEST_STAGES 2
+#endif
+constexpr int kStages = ADAPT_INGEST_STAGES;  // TMA tile stages (tuning knob)
 constexpr int kWarps = kIngestThreads / 32;
 
 struct LabelBinArgs {
