@@ -44,6 +44,20 @@ def _worker(rank, world, port, job, q):
     try:
         torch.cuda.set_device(0)
         adist.init_host_comm(0, rank, world)
+        if "regions" in job:  # adapt_train_many over rank shards of several regions (fused path)
+            s = torch.cuda.current_stream()
+            hs, keep = [], []
+            for r, (X, T) in enumerate(job["regions"]):
+                lo, hi = adist.shard_bounds(len(X), rank, world)
+                h = ad.adapt_region_create(f"mr_region{r}", X.shape[1], T.shape[1], f"dtree,depth={job['D']}", 0)
+                dX = torch.from_numpy(np.ascontiguousarray(X[lo:hi])).cuda()
+                dT = torch.from_numpy(np.ascontiguousarray(T[lo:hi])).cuda()
+                keep.append((dX, dT))
+                ad.adapt_record_table(h, dX, dT, hi - lo, True, s)
+                hs.append(h)
+            ad.adapt_train_many(hs, s)
+            q.put((rank, {"trees": [ad.adapt_get_tree(h) for h in hs]}))
+            return
         X, T, D = job["X"], job["T"], job["D"]
         lo, hi = adist.shard_bounds(len(X), rank, world)
         Xs, Ts = np.ascontiguousarray(X[lo:hi]), np.ascontiguousarray(T[lo:hi])
@@ -194,3 +208,19 @@ def test_p_invariant_quantile_bins():
         assert "error" not in o
         assert o["tree"].tobytes() == ref.tobytes(), f"rank {r}"
         assert np.array_equal(o["select"], oracle.select(ref, X[o["lo"]:o["hi"]]))
+
+
+def test_p_invariant_train_many_fused():
+    # three regions' trees in one multi-root frontier over the union of the
+    # ranks' shards: every rank gets every region's single-table tree
+    cfg = synth.CONFIGS["C2"]
+    X, T = synth.generate(cfg, 0, 30_000)
+    regions = []
+    for r in range(3):
+        rows = np.arange(r, len(X), 3)
+        regions.append((np.ascontiguousarray(X[rows]), np.ascontiguousarray(T[rows])))
+    res = _run(2, {"regions": regions, "D": 6})
+    for r, o in sorted(res.items()):
+        for (Xr, Tr), got in zip(regions, o["trees"]):
+            ref = oracle.train(Xr, oracle.labels(Tr), Tr.shape[1], 6)
+            assert got.tobytes() == ref.tobytes(), f"rank {r}"
