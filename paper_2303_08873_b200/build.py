@@ -23,7 +23,7 @@ def _git() -> str:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "common.h"), os.path.join(CSRC, "ptx.h"),
+    deps = srcs + [os.path.join(CSRC, "common.h"), os.path.join(CSRC, "ptx.h"), os.path.join(CSRC, "vecreg.cuh"),
                    os.path.join(ROOT, "include", "adapt.h")]
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= max(map(os.path.getmtime, deps)):
         return SO

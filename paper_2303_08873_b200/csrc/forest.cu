@@ -16,8 +16,10 @@
 //   select_forest_kernel  a9 for forests: every tree walked per vector, the
 //                      majority of their variants, ties -> lowest (R20).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.h"
+#include "vecreg.cuh"
 
 namespace adapt {
 namespace {
@@ -133,6 +135,58 @@ __global__ void __launch_bounds__(kForestThreads)
   }
 }
 
+// The product forest kernel: one vector per thread in registers (as select.cu's
+// select_kernel_d), every tree walked from the shared-memory top (deeper
+// nodes through L1/L2), the T votes in this thread's shared-memory column,
+// majority with ties -> lowest variant (R20).  1024 threads per CTA, one CTA
+// per SM; the next vector's loads are in flight during the walks.
+constexpr int kForestDThreads = 1024;
+
+template <int F>
+__global__ void __launch_bounds__(kForestDThreads, 1)
+    select_forest_d(const DNode *__restrict__ nodes, int n_nodes, const int32_t *roots, int T,
+                    const float *__restrict__ X, int64_t m, int wide, int32_t *__restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int NP = F <= 4 ? 4 : (F <= 8 ? 8 : 16);
+  const int n_top = min(n_nodes, kForestTop);
+  DNode *st = reinterpret_cast<DNode *>(smem);
+  uint8_t *votes = smem + (size_t)kForestTop * sizeof(DNode);  // [T][kForestDThreads]
+  __shared__ int32_t s_roots[64];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < n_top; i += kForestDThreads) st[i] = nodes[i];
+  for (int i = tid; i < T; i += kForestDThreads) s_roots[i] = roots[i];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kForestDThreads;
+  int64_t v = blockIdx.x * (int64_t)kForestDThreads + tid;
+  float nx[F];
+  if (v < m) load_vec<F>(X + v * F, wide, nx);
+  for (; v < m; v += stride) {
+    float xr[NP];
+#pragma unroll
+    for (int f = 0; f < NP; f++) xr[f] = f < F ? nx[f] : 0.f;
+    if (v + stride < m) load_vec<F>(X + (v + stride) * F, wide, nx);
+    for (int t = 0; t < T; t++) {
+      DNode nd = node_at(st, n_top, nodes, s_roots[t]);
+      while (nd.meta >= 0) {
+        const int k = (nd.meta >> 6) + (pick<NP>(xr, nd.meta & 63) <= nd.thr ? 0 : 1);  // NaN -> right
+        nd = node_at(st, n_top, nodes, k);
+      }
+      votes[t * kForestDThreads + tid] = (uint8_t)(-1 - nd.meta);
+    }
+    int best = 255, best_c = 0;  // majority, ties -> lowest variant (R20)
+    for (int t = 0; t < T; t++) {
+      const int l = votes[t * kForestDThreads + tid];
+      int c = 0;
+      for (int u = 0; u < T; u++) c += votes[u * kForestDThreads + tid] == l;
+      if (c > best_c || (c == best_c && l < best)) {
+        best = l;
+        best_c = c;
+      }
+    }
+    __stcs(out + v, best);
+  }
+}
+
 int sm_count() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -172,6 +226,23 @@ int forest_max_trees() { return 64; }
 void launch_select_forest(const DNode *nodes, int n_nodes, const int32_t *roots, int T,
                           const float *X, int64_t m, int F, int32_t *out, cudaStream_t s) {
   if (m == 0) return;
+  static const bool tile = getenv("ADAPT_SEL_TILE") != nullptr;  // the per-warp tile kernel (A/B)
+  if (!tile && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && (F == 4 || F == 8 || F == 12 || F == 16)) {
+    const int wide = (reinterpret_cast<uintptr_t>(X) & 31) == 0;
+    const size_t smem = (size_t)kForestTop * sizeof(DNode) + (size_t)T * kForestDThreads;
+    const int grid = (int)std::min<int64_t>((m + kForestDThreads - 1) / kForestDThreads, sm_count());
+    switch (F) {
+#define CASE(FF)                                                                                  \
+  case FF:                                                                                        \
+    smem_limit(select_forest_d<FF>, smem);                                                        \
+    select_forest_d<FF><<<grid, kForestDThreads, smem, s>>>(nodes, n_nodes, roots, T, X, m, wide, out); \
+    break;
+      CASE(4) CASE(8) CASE(12) CASE(16)
+#undef CASE
+    }
+    CUDA_CHECK(cudaGetLastError());
+    return;
+  }
   constexpr int W = kForestThreads / 32;
   const size_t smem = (size_t)std::min(n_nodes, kForestTop) * sizeof(DNode) +
                       (size_t)W * 32 * (F | 1) * 4 + (size_t)W * T * 32;

@@ -18,6 +18,7 @@
 #include <cstdlib>
 
 #include "common.h"
+#include "vecreg.cuh"
 
 namespace adapt {
 namespace {
@@ -152,22 +153,6 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   }
 }
 
-// x[f] of a vector held in registers (N = 4, 8 or 16, a power of two): a
-// select tree on the bits of f, all indices compile-time, no local memory
-template <int N>
-__device__ __forceinline__ float pick(const float (&x)[N], int f) {
-  float t[N];
-#pragma unroll
-  for (int i = 0; i < N; i++) t[i] = x[i];
-#pragma unroll
-  for (int b = 0; (1 << b) < N; b++) {
-    const bool hi = (f >> b) & 1;
-#pragma unroll
-    for (int i = 0; i < (N >> (b + 1)); i++) t[i] = hi ? t[2 * i + 1] : t[2 * i];
-  }
-  return t[0];
-}
-
 template <int N>
 __device__ __forceinline__ int walk_block_r(const uint4 (&w)[4], const float (&x)[N]) {
   const float t0 = __uint_as_float(w[0].x);
@@ -263,29 +248,6 @@ __global__ void __launch_bounds__(kSelThreads, 1)
 // registers (256-bit loads when the rows are 32-byte aligned): no staging tile,
 // no shared-memory stores or feature reads at all; the next vector's loads are
 // in flight during the walk.
-template <int F>
-__device__ __forceinline__ void load_vec(const float *__restrict__ p, bool wide, float (&x)[F]) {
-  if constexpr (F % 8 == 0) {
-    if (wide) {
-#pragma unroll
-      for (int i = 0; i < F; i += 8)
-        asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-            : "=f"(x[i]), "=f"(x[i + 1]), "=f"(x[i + 2]), "=f"(x[i + 3]), "=f"(x[i + 4]), "=f"(x[i + 5]),
-              "=f"(x[i + 6]), "=f"(x[i + 7])
-            : "l"(p + i));
-      return;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < F; i += 4) {
-    const float4 v = __ldcs(reinterpret_cast<const float4 *>(p + i));
-    x[i] = v.x;
-    x[i + 1] = v.y;
-    x[i + 2] = v.z;
-    x[i + 3] = v.w;
-  }
-}
-
 template <int F>
 __global__ void __launch_bounds__(kSelThreads, 1)
     select_kernel_d(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
