@@ -75,7 +75,7 @@ struct NodeRes {
   uint64_t nL;              // rows left of the winning cut
   int32_t valid, feat, b_lo, b_hi;
   // followed in memory by uint32 P[kc] (class totals) and uint32 cL[kc], compact
-  // class order (res_stride leaves room for C of each)
+  // class order (node j's record starts at res_off[j]: sizeof(NodeRes) + 8 kc_j, 8-aligned)
 };
 
 // Raise a kernel's dynamic shared-memory limit only when a launch needs more
@@ -193,7 +193,7 @@ void launch_split(const uint32_t *H, const int64_t *node_off, const int32_t *nod
                   int F, const int32_t *cumD, const int32_t *nval, SplitCand *out, cudaStream_t s);
 void launch_winner(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,
                    int F, int C, const int32_t *cumD, const int32_t *nval, const SplitCand *cand,
-                   uint8_t *res, int res_stride, cudaStream_t s);
+                   uint8_t *res, const int64_t *res_off, cudaStream_t s);
 
 // ---- kernel launchers (select.cu) ----
 struct DNode {     // device inference node, 8 bytes

@@ -1082,7 +1082,6 @@ void train_region(adapt_region *h, cudaStream_t s) {
   int sms = 148;
   CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g_ctx.device));
   DevBuf *Hcur = &h->H0, *Hprev = &h->H1;
-  const int res_stride = (int)((sizeof(NodeRes) + 8 * (size_t)C + 7) / 8 * 8);
   static const bool per_level = getenv("ADAPT_PROFILE_LEVELS") != nullptr;
   char nm[32];
   auto virtualize = [](std::vector<Seg> &v, bool by_slot) {  // row_base, node extents
@@ -1212,6 +1211,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
       fn.cls.each([&](int c, int k) { m[c] = (uint8_t)k; });
       node_ci[j] = ci;
     }
+    std::vector<int64_t> res_off(A + 1, 0);  // winners: compact per-node records (D2H bytes)
+    for (int j = 0; j < A; j++)
+      res_off[j + 1] = res_off[j] + (int64_t)((sizeof(NodeRes) + 8 * (size_t)node_kc[j] + 7) / 8 * 8);
     std::vector<int32_t> big_nodes, small_nodes;  // split search: by class count
     for (int j = 0; j < A; j++)
       (node_kc[j] <= split_small_max_classes() ? small_nodes : big_nodes).push_back(j);
@@ -1247,7 +1249,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     const size_t o_cmaps = sa.put(cmaps), o_soff = sa.put(soff), o_skc = sa.put(slot_kc),
                  o_jobs = sa.put(jobs), o_maps = sa.put(maps), o_noff = sa.put(node_off),
                  o_nkc = sa.put(node_kc), o_zst = sa.put(zstart), o_sst = sa.put(sstart),
-                 o_big = sa.put(big_nodes), o_small = sa.put(small_nodes);
+                 o_big = sa.put(big_nodes), o_small = sa.put(small_nodes), o_roff = sa.put(res_off);
     sa.flush(s);
     Hcur->ensure((size_t)soff[nslots] * 4 + 16);
     {
@@ -1360,7 +1362,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
                       sa.ptr<int16_t>(o_maps), sa.ptr<int32_t>(o_sst), (int)jobs.size(), sblocks, s);
     }
     h->cand.ensure((size_t)A * F * sizeof(SplitCand));
-    h->res.ensure((size_t)A * res_stride);
+    h->res.ensure((size_t)res_off[A] + 16);
     {
       snprintf(nm, sizeof nm, "split_L%02d", level);
       Phase ph(per_level ? nm : "split", s, 0);
@@ -1373,11 +1375,11 @@ void train_region(adapt_region *h, cudaStream_t s) {
       Phase ph("winner", s, 0);
       launch_winner(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_noff), sa.ptr<int32_t>(o_nkc), A, F, C,
                     h->hoff.as<int32_t>(), h->dnval.as<int32_t>(), h->cand.as<SplitCand>(),
-                    h->res.as<uint8_t>(), res_stride, s);
+                    h->res.as<uint8_t>(), sa.ptr<int64_t>(o_roff), s);
     }
-    h->hres.ensure((size_t)A * res_stride);
+    h->hres.ensure((size_t)res_off[A] + 16);
     uint8_t *hr = h->hres.as<uint8_t>();
-    CUDA_CHECK(cudaMemcpyAsync(hr, h->res.p, (size_t)A * res_stride, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(hr, h->res.p, (size_t)res_off[A], cudaMemcpyDeviceToHost, s));
     if (trace) tr[4] = now_us();
     CUDA_CHECK(cudaStreamSynchronize(s));
     if (trace) tr[5] = now_us();
@@ -1407,9 +1409,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
     };
     std::vector<Dec> dec(A, Dec{false, false, -1});
     for (int j = 0; j < A; j++) {
-      const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + (size_t)j * res_stride);
+      const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + res_off[j]);
       const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);
-      const uint32_t *cLd = Pd + C;
+      const uint32_t *cLd = Pd + node_kc[j];
       const FNode &fn = frontier[j];
       const int kc = node_kc[j];
       int np = 0, npl = 0, npr = 0;
@@ -1446,9 +1448,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
     }
     std::vector<uint64_t> P(C), PL(C), PR(C);
     for (int j = 0; j < A; j++) {
-      const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + (size_t)j * res_stride);
+      const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + res_off[j]);
       const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);  // compact columns
-      const uint32_t *cLd = Pd + C;
+      const uint32_t *cLd = Pd + node_kc[j];
       const FNode &fn = frontier[j];
       // everything in the node's compact columns (class cl[k], ascending)
       const int kc = node_kc[j];

@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
 __global__ void __launch_bounds__(256)
     winner_kernel(const uint32_t *__restrict__ H, const int64_t *node_off, const int32_t *node_kc,
                   int F, int Cmax, const int32_t *cumD, const int32_t *nval, const SplitCand *cand,
-                  uint8_t *res, int res_stride) {
+                  uint8_t *res, const int64_t *res_off) {
   __shared__ int s_f;
   __shared__ SplitCand s_c;
   __shared__ unsigned long long s_n;
@@ -442,9 +442,9 @@ __global__ void __launch_bounds__(256)
   const int C = node_kc[node];
   const uint32_t *h = H + node_off[node] + (int64_t)cumD[fsel] * C;
   const int Df = nval[fsel];
-  NodeRes *nr = reinterpret_cast<NodeRes *>(res + (size_t)node * res_stride);
+  NodeRes *nr = reinterpret_cast<NodeRes *>(res + res_off[node]);
   uint32_t *P = reinterpret_cast<uint32_t *>(nr + 1);
-  uint32_t *cL = P + Cmax;
+  uint32_t *cL = P + C;  // compact: the node's own class count
   // class totals and left-of-cut totals: thread t sums class t % C over rows
   // t / C, t / C + T, ... (T = threads per class), independent loads in flight
   __shared__ uint32_t sP[kMaxC + 1], sL[kMaxC + 1];
@@ -519,10 +519,10 @@ int split_small_max_classes() { return kSmallKc; }
 
 void launch_winner(const uint32_t *H, const int64_t *node_off, const int32_t *node_kc, int nnodes,
                    int F, int C, const int32_t *cumD, const int32_t *nval, const SplitCand *cand,
-                   uint8_t *res, int res_stride, cudaStream_t s) {
+                   uint8_t *res, const int64_t *res_off, cudaStream_t s) {
   if (nnodes == 0) return;
   winner_kernel<<<nnodes, 256, 0, s>>>(H, node_off, node_kc, F, C, cumD, nval, cand, res,
-                                       res_stride);
+                                       res_off);
   CUDA_CHECK(cudaGetLastError());
 }
 
