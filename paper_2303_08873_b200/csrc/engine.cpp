@@ -1220,6 +1220,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
     std::vector<SubJob> jobs;
     std::vector<int16_t> maps;
     std::vector<int32_t> zstart(ndirect_slots), sstart;  // chunk prefixes (zero / subtract)
+    jobs.reserve(derived.size());
+    sstart.reserve(derived.size());
+    maps.reserve(derived.size() * 2 * 16);
     int zblocks = 0, sblocks = 0;
     for (int k = 0; k < ndirect_slots; k++) {
       zstart[k] = zblocks;
