@@ -121,3 +121,25 @@ def test_model_kept_and_errors():
     assert e.value.code == ad.ADAPT_E_USAGE
     ad.adapt_region_destroy(h)
     ad.adapt_region_destroy(f)
+
+
+def test_kfold_on_recorded_samples():
+    # the Apollo flow: long-format records -> the GPU aggregation to wide
+    # rows (first appearance order, mean times) -> the K-fold harness over them
+    rng = np.random.default_rng(12)
+    R, F, V = 20000, 2, 4
+    grid = rng.choice(np.arange(60, dtype=np.float32), size=(700, F)).astype(np.float32)
+    feat = grid[rng.integers(0, len(grid), R)]
+    var = rng.integers(0, V, R).astype(np.int32)
+    ns = (1000 + 37 * feat[:, 0] * (var + 1) + rng.integers(0, 500, R)).astype(np.uint64)
+    h = _region(F, V, "dtree,depth=5")
+    ad.adapt_record_batch(h, torch.from_numpy(feat).to(DEV), torch.from_numpy(var).to(DEV),
+                          torch.from_numpy(ns.astype(np.int64)).to(DEV), R, True)
+    got = ad.adapt_kfold(h, 4, 3, 2, 8)
+    Xw, Tw = oracle.aggregate(feat, var, ns, V)
+    ref, trees = oracle.kfold(Xw, Tw, 5, 4, 3, 2, 8)
+    for i, (g, r) in enumerate(zip(got, ref)):
+        for k in ("n_train", "n_test", "n_correct", "n_nodes"):
+            assert g[k] == r[k], (i, k)
+        assert ad.adapt_get_kfold_tree(h, i).tobytes() == trees[i].tobytes()
+    ad.adapt_region_destroy(h)
