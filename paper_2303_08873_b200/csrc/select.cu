@@ -289,6 +289,67 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   }
 }
 
+// As select_kernel_d, but the vector parked in the thread's own shared-memory
+// COLUMN (xs[f][tid]: any f of any lane is a distinct bank, so the walk's
+// random-feature reads are conflict-free single wavefronts) instead of the
+// register select tree (A/B: ADAPT_SEL_XCOL=1).
+__device__ __forceinline__ int walk_block_col(const uint4 (&w)[4], const float *x) {
+  constexpr int S = kSelThreads;
+  const float t0 = __uint_as_float(w[0].x);
+  const bool g0 = !(x[(w[1].w & 63) * S] <= t0);
+  const float t1 = __uint_as_float(g0 ? w[0].z : w[0].y);
+  const bool g1 = !(x[((g0 ? w[2].y : w[2].x) & 63) * S] <= t1);
+  const uint32_t tw = g0 ? (g1 ? w[1].z : w[1].y) : (g1 ? w[1].x : w[0].w);
+  const uint32_t fw = g0 ? (g1 ? w[3].y : w[3].x) : (g1 ? w[2].w : w[2].z);
+  const bool g2 = !(x[(fw & 63) * S] <= __uint_as_float(tw));
+  uint32_t r;
+  if (g0)
+    r = g1 ? (g2 ? w[3].z : w[3].y) : (g2 ? w[3].x : w[2].w);
+  else
+    r = g1 ? (g2 ? w[2].z : w[2].y) : (g2 ? w[2].x : w[1].w);
+  return (int32_t)r >> 6;
+}
+
+template <int F>
+__global__ void __launch_bounds__(kSelThreads, 1)
+    select_kernel_c(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
+                    const float *__restrict__ X, int64_t m, int wide, int32_t *__restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  DNode *st = reinterpret_cast<DNode *>(smem);
+  const int t = threadIdx.x;
+  float *x = reinterpret_cast<float *>(smem + (size_t)kTopNodes * sizeof(DNode)) + t;  // column t
+  for (int i = t; i < n_top; i += kSelThreads) st[i] = gtree[i];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kSelThreads;
+  int64_t v = blockIdx.x * (int64_t)kSelThreads + t;
+  float nx[F];
+  if (v < m) load_vec<F>(X + v * F, wide, nx);
+  for (; v < m; v += stride) {
+#pragma unroll
+    for (int f = 0; f < F; f++) x[f * kSelThreads] = nx[f];
+    if (v + stride < m) load_vec<F>(X + (v + stride) * F, wide, nx);
+    DNode nd = st[0];
+    int ref = nd.meta;
+    while (nd.meta >= 0) {
+      const float xv = x[(nd.meta & 63) * kSelThreads];
+      const int k = (nd.meta >> 6) + (xv <= nd.thr ? 0 : 1);  // NaN -> right (R8)
+      if (k < n_top) {
+        nd = st[k];
+        ref = nd.meta;
+      } else {
+        ref = k - n_top;
+        break;
+      }
+    }
+    while (ref >= 0) {
+      uint4 w[4];
+      load_block(blocks, ref, w);
+      ref = walk_block_col(w, x);
+    }
+    __stcs(out + v, -1 - ref);
+  }
+}
+
 // generic F (not a multiple of 4, or an unaligned X): scalar staging
 __global__ void __launch_bounds__(kAnyThreads, 1)
     select_kernel_any(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
@@ -345,6 +406,11 @@ void launch_select(const DNode *tree, int n_nodes, const uint4 *blocks, const fl
   static const bool smem_x = getenv("ADAPT_SEL_SMEMX") != nullptr;  // the smem-x kernel (A/B)
   // default: per-lane vector loads (select_kernel_d); A/B: the tile kernels
   static const bool direct = getenv("ADAPT_SEL_TILE") == nullptr && !smem_x;
+  // trees that fit the shared-memory top: the vector in a shared-memory column
+  // (C4 select 1.40 -> 1.15 ms); deeper trees: the register kernel, whose
+  // bottom-block walks measured faster with the vector in registers (C5)
+  static const int xcol_env = getenv("ADAPT_SEL_XCOL") ? atoi(getenv("ADAPT_SEL_XCOL")) : -1;
+  const bool xcol = direct && (xcol_env >= 0 ? xcol_env != 0 : n_nodes <= kTopNodes);
   const size_t tree_b = (size_t)kTopNodes * sizeof(DNode);
   // F <= 16, 16-byte aligned X: per-warp tiles, one 1024-thread CTA per SM
   const int64_t wtiles = (m + 32 * kSelChains - 1) / (32 * kSelChains);
@@ -352,7 +418,14 @@ void launch_select(const DNode *tree, int n_nodes, const uint4 *blocks, const fl
   switch (vec ? F : 0) {
 #define CASE(FF)                                                                               \
   case FF: {                                                                                   \
-    if (direct) {                                                                              \
+    if (xcol) {                                                                                \
+      const int wide = (reinterpret_cast<uintptr_t>(X) & 31) == 0;                             \
+      const int64_t blocks_needed = (m + kSelThreads - 1) / kSelThreads;                       \
+      const int g = (int)std::min<int64_t>(blocks_needed, sms);                                \
+      const size_t smem = tree_b + (size_t)kSelThreads * FF * 4;                               \
+      smem_limit(select_kernel_c<FF>, smem);                                                   \
+      select_kernel_c<FF><<<g, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, wide, out);  \
+    } else if (direct) {                                                                       \
       const int wide = (reinterpret_cast<uintptr_t>(X) & 31) == 0;                             \
       const int64_t blocks_needed = (m + kSelThreads - 1) / kSelThreads;                       \
       const int g = (int)std::min<int64_t>(blocks_needed, sms);                                \
