@@ -135,9 +135,10 @@ __global__ void __launch_bounds__(kForestThreads)
   }
 }
 
-// The product forest kernel: one vector per thread in registers (as select.cu's
-// select_kernel_d), every tree walked from the shared-memory top (deeper
-// nodes through L1/L2), the T votes in this thread's shared-memory column,
+// The product forest kernel: one vector per thread, loaded straight from HBM
+// (next one in flight) and parked in the thread's own shared-memory column (as
+// select.cu's select_kernel_c), every tree walked from the shared-memory top
+// (deeper nodes through L1/L2), the T votes in the thread's vote column,
 // majority with ties -> lowest variant (R20).  1024 threads per CTA, one CTA
 // per SM; the next vector's loads are in flight during the walks.
 constexpr int kForestDThreads = 1024;
@@ -147,10 +148,11 @@ __global__ void __launch_bounds__(kForestDThreads, 1)
     select_forest_d(const DNode *__restrict__ nodes, int n_nodes, const int32_t *roots, int T,
                     const float *__restrict__ X, int64_t m, int wide, int32_t *__restrict__ out) {
   extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int NP = F <= 4 ? 4 : (F <= 8 ? 8 : 16);
   const int n_top = min(n_nodes, kForestTop);
   DNode *st = reinterpret_cast<DNode *>(smem);
   uint8_t *votes = smem + (size_t)kForestTop * sizeof(DNode);  // [T][kForestDThreads]
+  // the thread's vector in its own shared-memory column (conflict-free reads of any feature)
+  float *xc = reinterpret_cast<float *>(votes + (size_t)64 * kForestDThreads) + threadIdx.x;
   __shared__ int32_t s_roots[64];
   const int tid = threadIdx.x;
   for (int i = tid; i < n_top; i += kForestDThreads) st[i] = nodes[i];
@@ -161,14 +163,13 @@ __global__ void __launch_bounds__(kForestDThreads, 1)
   float nx[F];
   if (v < m) load_vec<F>(X + v * F, wide, nx);
   for (; v < m; v += stride) {
-    float xr[NP];
 #pragma unroll
-    for (int f = 0; f < NP; f++) xr[f] = f < F ? nx[f] : 0.f;
+    for (int f = 0; f < F; f++) xc[f * kForestDThreads] = nx[f];
     if (v + stride < m) load_vec<F>(X + (v + stride) * F, wide, nx);
     for (int t = 0; t < T; t++) {
       DNode nd = node_at(st, n_top, nodes, s_roots[t]);
       while (nd.meta >= 0) {
-        const int k = (nd.meta >> 6) + (pick<NP>(xr, nd.meta & 63) <= nd.thr ? 0 : 1);  // NaN -> right
+        const int k = (nd.meta >> 6) + (xc[(nd.meta & 63) * kForestDThreads] <= nd.thr ? 0 : 1);  // NaN -> right
         nd = node_at(st, n_top, nodes, k);
       }
       votes[t * kForestDThreads + tid] = (uint8_t)(-1 - nd.meta);
@@ -229,7 +230,8 @@ void launch_select_forest(const DNode *nodes, int n_nodes, const int32_t *roots,
   static const bool tile = getenv("ADAPT_SEL_TILE") != nullptr;  // the per-warp tile kernel (A/B)
   if (!tile && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && (F == 4 || F == 8 || F == 12 || F == 16)) {
     const int wide = (reinterpret_cast<uintptr_t>(X) & 31) == 0;
-    const size_t smem = (size_t)kForestTop * sizeof(DNode) + (size_t)T * kForestDThreads;
+    const size_t smem = (size_t)kForestTop * sizeof(DNode) + (size_t)64 * kForestDThreads +
+                        (size_t)F * kForestDThreads * 4;  // tree top, vote columns, vector columns
     const int grid = (int)std::min<int64_t>((m + kForestDThreads - 1) / kForestDThreads, sm_count());
     switch (F) {
 #define CASE(FF)                                                                                  \
