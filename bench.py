@@ -113,16 +113,31 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def cpu_baseline(cfg, rows: int, depth: int):
-    """The oracle as it stands (single-threaded C), on a bounded sample of the
-    same workload: the first `rows` rows of the table, labels + tree + select."""
+def host_cpu():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return os.cpu_count(), model
+
+
+def cpu_baseline(cfg, rows: int, depth: int, omp: bool = False):
+    """The oracle as it stands (plain C), on a bounded sample of the same
+    workload: the first `rows` rows of the table, labels + tree + select.
+    omp=True: the same source built with -fopenmp (liboracle_omp.so: features
+    of a node and vectors in parallel, identical results) on all host cores."""
     import oracle
 
     X, T = synth.generate(cfg, 0, rows)
     t0 = time.perf_counter()
     y = oracle.labels(T)
-    tree = oracle.train(X, y, cfg.V, depth)
-    oracle.select(tree, X)
+    tree = oracle.train(X, y, cfg.V, depth, omp=omp)
+    oracle.select(tree, X, omp=omp)
     dt = time.perf_counter() - t0
     return rows / dt, dt
 
@@ -340,7 +355,8 @@ def run_reference(args, rank: int, world: int):
         "config": {"workload": WORKLOADS[args.config], "sample_rows": rows},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": 1, "kind": "oracle",
                          "sample": f"first {rows} rows of {args.config} (labels + depth-{cfg.D} "
-                                   f"exact CART + select), single-threaded C oracle"},
+                                   f"exact CART + select), single-threaded C oracle",
+                         "host_cores": host_cpu()[0], "cpu_model": host_cpu()[1]},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -528,9 +544,22 @@ def main():
         a["bytes"] += v["bytes"]
     for i, lv in enumerate(levels):
         lv["ms"] = per_level.get(i, {})
+    # SURVEY §8(d) algorithmic bytes (what the method must move, not what this
+    # implementation moves): ingest 4F+4V read + F+1 written per row; training
+    # (F+1) per row of an active node per level; selection 4F read + 4 written
+    # per vector.  Per kernel phase: the phase's rows x that per-row figure.
+    F, V = cfg.F, cfg.V
+    rows_part = sum(lv["rows_part"] for lv in levels)
+    rows_hist = sum(lv["rows_hist"] for lv in levels)
+    alg = {"ingest": (4 * F + 4 * V + F + 1) * n * args.steps,
+           "partition": (F + 1) * rows_part * args.steps,
+           "hist": (F + 1) * rows_hist * args.steps,
+           "select": (4 * F + 4) * n * args.steps}
     dom = max(kern, key=lambda k: kern[k]["ms"])
     d = kern[dom]
-    achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 and d["bytes"] > 0 else None
+    alg_dom = alg.get(dom)
+    achieved = alg_dom / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 and alg_dom else None
+    impl = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 and d["bytes"] > 0 else None
     step_ms_phases = {k: round(v["ms"] / args.steps, 4) for k, v in kern.items()}
     traffic = ncu_traffic().get(dom.split("_L")[0])
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -539,26 +568,42 @@ def main():
                 "traffic_source": (f'{traffic["source"]} ({traffic["capture"]}, one ncu --set full '
                                    f'capture)') if traffic else None,
                 "peak_source": peak_src,
-                "bytes_per_launch": d["bytes"] / max(d["launches"], 1),
-                "ms_per_launch": d["ms"] / max(d["launches"], 1)}
-    alg_bytes = sum(v["bytes"] for v in kern.values()) / args.steps
+                "alg_bytes_per_launch": (alg_dom or 0) / max(d["launches"], 1),
+                "alg_bytes_rule": "SURVEY 8(d): ingest 4F+4V+F+1 per row; partition / hist (F+1) per row "
+                                  "they process; select 4F+4 per vector",
+                "ms_per_launch": d["ms"] / max(d["launches"], 1),
+                "impl_bytes_per_launch": d["bytes"] / max(d["launches"], 1),
+                "impl_frac": (impl / peak) if impl else None}
     # the whole level loop against SURVEY §8(d)'s level figure: (F+1) bytes per
-    # row of a split node per level (the partition/histogram split of this
-    # design moves 2(F+1) + reads ~(F+4)/2 per row)
+    # row of an active node per level
     loop_ms = sum(step_ms_phases.get(k, 0) for k in ("partition", "hist", "zero", "subtract", "split",
-                                                   "winner"))
+                                                   "winner", "fused"))
     loop_rows = sum((lv["rows_part"] if i else n) for i, lv in enumerate(levels) if lv["nodes"])
-    loop_bytes = (cfg.F + 1) * loop_rows * world
+    loop_bytes = (F + 1) * loop_rows * world
     level_loop = {"survey_bytes_per_step": loop_bytes, "ms_per_step": loop_ms,
                   "achieved_gbs": loop_bytes / (loop_ms / 1e3) / 1e9 if loop_ms else None,
                   "frac": loop_bytes / (loop_ms / 1e3) / 1e9 / peak if loop_ms else None}
+    ingest_bytes = (4 * F + 4 * V + F + 1) * N
+    select_bytes = (4 * F + 4) * N
+    train_ms = ms - step_ms_phases.get("select", 0)
+    step_frac = {"survey_bytes_per_step": ingest_bytes + loop_bytes + select_bytes,
+                 "frac": (ingest_bytes + loop_bytes + select_bytes) / (ms / 1e3) / 1e9 / peak,
+                 "train_frac": (ingest_bytes + loop_bytes) / (train_ms / 1e3) / 1e9 / peak,
+                 "rule": "SURVEY 8(d) bytes of the whole step (ingest + (F+1) per active row per level "
+                         "+ select) / step time / peak; train_frac without the select"}
     cpu = None
     if world == 1 and not args.no_cpu:
         rows = {"C4": 1_500_000, "C3": 1_000_000}.get(args.config, N)  # ~20 s of oracle work
+        cores, model_name = host_cpu()
         v, dt = cpu_baseline(cfg, min(rows, N), cfg.D)
+        va, dta = cpu_baseline(cfg, min(rows, N), cfg.D, omp=True)
         cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
                "sample": f"first {min(rows, N)} rows of {args.config}: labels + depth-{cfg.D} exact "
-                         f"CART + select, single-threaded C oracle ({dt:.1f} s)"}
+                         f"CART + select, single-threaded C oracle ({dt:.1f} s)",
+               "host_cores": cores, "cpu_model": model_name,
+               "all_cores": {"value": va, "unit": "samples/s", "cores": cores,
+                             "sample": f"same sample, liboracle_omp.so (oracle.c with -fopenmp: "
+                                       f"features of a node and vectors in parallel) ({dta:.1f} s)"}}
     line = {
         "metric": METRIC, "value": N / (ms / 1e3), "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -568,9 +613,9 @@ def main():
                    "parallelism": f"dp{world}",
                    "l2": "inputs (%.1f GB) exceed the 126 MB L2; no flush needed" %
                          (N * 4 * (cfg.F + cfg.V) / 1e9)},
-        "train_samples_per_s": N / ((ms - step_ms_phases.get("select", 0)) / 1e3),
+        "train_samples_per_s": N / (train_ms / 1e3),
         "select_per_s": N / (step_ms_phases["select"] / 1e3) if step_ms_phases.get("select") else None,
-        "hbm_frac_step": alg_bytes / (ms / 1e3) / 1e9 / peak,
+        "hbm_frac_step": step_frac,
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": int(sum(v["launches"] for v in kern.values())),

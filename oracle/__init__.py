@@ -21,6 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
+_SO_OMP = os.path.join(_HERE, "liboracle_omp.so")  # same source, -fopenmp (bench timing only)
 _SRC = os.path.join(_HERE, "oracle.c")
 
 OK = 0
@@ -47,25 +48,26 @@ assert NODE_DTYPE.itemsize == 48
 
 
 def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (plain -O2, no FMA contraction)."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
-        os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))
-    ):
-        subprocess.check_call(
-            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-             "-shared", "-o", _SO, _SRC, "-lm"]
-        )
+    """Compile liboracle.so with gcc (plain -O2, no FMA contraction) and the
+    all-cores build liboracle_omp.so of the same source (-fopenmp: features of
+    a node scanned in parallel, vectors walked in parallel; same results)."""
+    srcs_mtime = max(os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h")))
+    for so, extra in ((_SO, []), (_SO_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(so) or os.path.getmtime(so) < srcs_mtime:
+            subprocess.check_call(
+                ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", *extra,
+                 "-shared", "-o", so, _SRC, "-lm"]
+            )
     return _SO
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def lib(omp: bool = False):
+    if omp not in _libs:
         build()
-        L = ctypes.CDLL(_SO)
+        L = ctypes.CDLL(_SO_OMP if omp else _SO)
         P = ctypes.c_void_p
         i64, i32 = ctypes.c_int64, ctypes.c_int32
         L.oracle_canon_features.argtypes = [P, i64, ctypes.c_int, P]
@@ -82,8 +84,8 @@ def lib():
         L.oracle_kfold_groups.argtypes = [ctypes.c_uint64, ctypes.c_int, i64, ctypes.c_int, P]
         L.oracle_gini_counts.argtypes = [P, ctypes.c_int]
         L.oracle_gini_counts.restype = ctypes.c_double
-        _lib = L
-    return _lib
+        _libs[omp] = L
+    return _libs[omp]
 
 
 class OracleError(RuntimeError):
@@ -170,8 +172,10 @@ def bins(X: np.ndarray) -> np.ndarray:
     return out
 
 
-def train(X: np.ndarray, y: np.ndarray, C: int, D: int, cap: int | None = None) -> np.ndarray:
-    """Exact greedy CART, canonical BFS node array (structured NODE_DTYPE)."""
+def train(X: np.ndarray, y: np.ndarray, C: int, D: int, cap: int | None = None,
+          omp: bool = False) -> np.ndarray:
+    """Exact greedy CART, canonical BFS node array (structured NODE_DTYPE).
+    omp=True: the all-cores build (same tree; bench timing only)."""
     X = _f32(X)
     n, F = X.shape
     y = np.ascontiguousarray(y, dtype=np.uint8)
@@ -179,18 +183,18 @@ def train(X: np.ndarray, y: np.ndarray, C: int, D: int, cap: int | None = None) 
         cap = int(min(2 * n + 1, (1 << (D + 1)) - 1 if D < 30 else 2 * n + 1))
     out = np.zeros(max(cap, 1), NODE_DTYPE)
     nn = np.zeros(1, np.int32)
-    rc = lib().oracle_train(_p(X), _p(y), n, F, C, D, _p(out), max(cap, 1), _p(nn))
+    rc = lib(omp).oracle_train(_p(X), _p(y), n, F, C, D, _p(out), max(cap, 1), _p(nn))
     if rc:
         raise OracleError(rc, "train")
     return out[: int(nn[0])].copy()
 
 
-def select(tree: np.ndarray, X: np.ndarray) -> np.ndarray:
+def select(tree: np.ndarray, X: np.ndarray, omp: bool = False) -> np.ndarray:
     X = _f32(X)
     m, F = X.shape
     tree = np.ascontiguousarray(tree, dtype=NODE_DTYPE)
     out = np.empty(m, np.int32)
-    rc = lib().oracle_select(_p(tree), len(tree), _p(X), m, F, _p(out))
+    rc = lib(omp).oracle_select(_p(tree), len(tree), _p(X), m, F, _p(out))
     if rc:
         raise OracleError(rc, "select")
     return out

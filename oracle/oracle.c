@@ -14,6 +14,9 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 typedef unsigned __int128 u128;
 
@@ -259,8 +262,20 @@ int oracle_train(const float *X, const uint8_t *y, int64_t n, int F, int C, int 
   int32_t count = 1;
   int rc = ORACLE_OK;
   int64_t *cnt = malloc(sizeof(int64_t) * C);
-  int64_t *cL = malloc(sizeof(int64_t) * C);
-  pair_t *pairs = malloc(sizeof(pair_t) * n);
+  /* one sort buffer per thread: the all-cores build (-fopenmp, liboracle_omp.so,
+   * bench timing only) scans the features of a node in parallel; the plain
+   * build has one thread and the pragma below is ignored */
+  int nthr = 1;
+#ifdef _OPENMP
+  nthr = omp_get_max_threads();
+#endif
+  pair_t **tpairs = malloc(sizeof(pair_t *) * nthr);
+  int64_t **tcL = malloc(sizeof(int64_t *) * nthr);
+  for (int t = 0; t < nthr; t++) {
+    tpairs[t] = malloc(sizeof(pair_t) * n);
+    tcL[t] = malloc(sizeof(int64_t) * C);
+  }
+  cand_t *fbest = malloc(sizeof(cand_t) * F);
 
   /* nodes are processed in index order; children are appended, so this is BFS */
   for (int32_t k = 0; k < count; k++) {
@@ -285,9 +300,19 @@ int oracle_train(const float *X, const uint8_t *y, int64_t n, int F, int C, int 
       sets[k].rows = NULL;
       continue;
     }
-    cand_t best;
-    memset(&best, 0, sizeof(best));
+    /* best candidate of each feature, then the best over features in f order */
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
     for (int f = 0; f < F; f++) {
+      int t = 0;
+#ifdef _OPENMP
+      t = omp_get_thread_num();
+#endif
+      pair_t *pairs = tpairs[t];
+      int64_t *cL = tcL[t];
+      cand_t best;
+      memset(&best, 0, sizeof(best));
       for (int64_t i = 0; i < m; i++) {
         pairs[i].x = canon(X[rows[i] * F + f]);
         pairs[i].y = y[rows[i]];
@@ -317,7 +342,12 @@ int oracle_train(const float *X, const uint8_t *y, int64_t n, int F, int C, int 
           if (better(&cd, &best)) best = cd;
         }
       }
+      fbest[f] = best;
     }
+    cand_t best;
+    memset(&best, 0, sizeof(best));
+    for (int f = 0; f < F; f++)
+      if (fbest[f].valid && better(&fbest[f], &best)) best = fbest[f];
     if (!best.valid) { /* no candidate cut: all rows share every feature value (R10) */
       free(rows);
       sets[k].rows = NULL;
@@ -350,8 +380,13 @@ int oracle_train(const float *X, const uint8_t *y, int64_t n, int F, int C, int 
   for (int32_t k = 0; k < count; k++) free(sets[k].rows);
   free(sets);
   free(cnt);
-  free(cL);
-  free(pairs);
+  for (int t = 0; t < nthr; t++) {
+    free(tpairs[t]);
+    free(tcL[t]);
+  }
+  free(tpairs);
+  free(tcL);
+  free(fbest);
   *n_nodes = count;
   return rc;
 }
@@ -360,6 +395,9 @@ int oracle_train(const float *X, const uint8_t *y, int64_t n, int F, int C, int 
 int oracle_select(const oracle_node_t *tree, int32_t n_nodes, const float *X, int64_t m,
                   int F, int32_t *out) {
   if (n_nodes < 1 || m < 0 || F < 1) return ORACLE_E_INVALID_ARG;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
   for (int64_t i = 0; i < m; i++) {
     int32_t k = 0;
     while (tree[k].feature >= 0) {

@@ -160,6 +160,48 @@ def _ptr(a) -> int:
     raise TypeError(f"unsupported array type {type(a)}")
 
 
+def _check_array(a, name: str, dtype, cols: int | None, rows: int, on_device: bool | None):
+    """Validate an operand before its pointer crosses the C ABI: element type,
+    contiguity, [rows][cols] shape (at least `rows` rows) and its device."""
+    if a is None or isinstance(a, int):
+        return  # raw addresses: the caller vouches for them
+    if isinstance(a, np.ndarray):
+        if on_device:
+            raise ValueError(f"{name}: a numpy array is host memory but on_device=True")
+        dts = (dtype,) if isinstance(dtype, str) else dtype
+        if a.dtype not in [np.dtype(d) for d in dts]:
+            raise TypeError(f"{name}: dtype {a.dtype}, expected {dtype}")
+        shape = a.shape
+    elif hasattr(a, "data_ptr"):
+        import torch
+
+        dts = (dtype,) if isinstance(dtype, str) else dtype
+        if a.dtype not in [getattr(torch, d) for d in dts if hasattr(torch, d)]:
+            raise TypeError(f"{name}: dtype {a.dtype}, expected torch.{dtype}")
+        if on_device is not None and bool(a.is_cuda) != bool(on_device):
+            raise ValueError(f"{name}: tensor on {a.device} but on_device={bool(on_device)}")
+        shape = tuple(a.shape)
+    else:
+        raise TypeError(f"{name}: unsupported array type {type(a)}")
+    if cols is None:
+        ok = (len(shape) == 1 and shape[0] >= rows) or (rows == 0)
+    elif len(shape) == 2:
+        ok = shape[1] == cols and shape[0] >= rows
+    else:
+        ok = len(shape) == 1 and shape[0] >= rows * cols
+    if not ok:
+        want = f"[>= {rows}]" if cols is None else f"[>= {rows}][{cols}]"
+        raise ValueError(f"{name}: shape {shape}, expected {want}")
+    _ptr(a)  # contiguity
+
+
+# Device tables passed with on_device=1 are BORROWED until the next train
+# (adapt.h adapt_record_table): hold a reference per region so the caching
+# allocator cannot recycle them in between.  Replaced by the next record_table,
+# dropped by adapt_region_destroy.
+_borrowed: dict = {}
+
+
 def _stream(s) -> int:
     if s is None:
         return 0
@@ -244,6 +286,7 @@ def adapt_region_create(id: str, num_features: int, num_variants: int,
 
 def adapt_region_destroy(h: int):
     _check(_L.adapt_region_destroy(h), "adapt_region_destroy")
+    _borrowed.pop(h, None)
 
 
 def adapt_region_info(h: int) -> dict:
@@ -267,8 +310,15 @@ def adapt_record_table(h: int, features, times, n: int | None = None, on_device:
         n = int(features.shape[0])
     if on_device is None:
         on_device = bool(getattr(features, "is_cuda", False))
+    info = adapt_region_info(h)
+    _check_array(features, "features", "float32", info["num_features"], int(n), on_device)
+    _check_array(times, "times", "float32", info["num_variants"], int(n), on_device)
     _check(_L.adapt_record_table(h, _ptr(features), _ptr(times), int(n), int(on_device),
                                  _stream(stream)), "adapt_record_table")
+    if on_device:
+        _borrowed[h] = (features, times)
+    else:
+        _borrowed.pop(h, None)
 
 
 def adapt_record_batch(h: int, features, variants, elapsed_ns, m: int | None = None,
@@ -278,6 +328,10 @@ def adapt_record_batch(h: int, features, variants, elapsed_ns, m: int | None = N
         m = int(features.shape[0])
     if on_device is None:
         on_device = bool(getattr(features, "is_cuda", False))
+    F = adapt_region_info(h)["num_features"]
+    _check_array(features, "features", "float32", F, int(m), on_device)
+    _check_array(variants, "variants", "int32", None, int(m), on_device)
+    _check_array(elapsed_ns, "elapsed_ns", ("uint64", "int64"), None, int(m), on_device)
     _check(_L.adapt_record_batch(h, _ptr(features), _ptr(variants), _ptr(elapsed_ns), int(m),
                                  int(on_device), _stream(stream)), "adapt_record_batch")
 
@@ -318,11 +372,17 @@ def adapt_select(h: int, features) -> int:
 
 
 def adapt_select_batch(h: int, d_X, m: int, d_out, stream=None):
+    F = adapt_region_info(h)["num_features"]
+    _check_array(d_X, "X", "float32", F, int(m), True)
+    _check_array(d_out, "out", "int32", None, int(m), True)
     _check(_L.adapt_select_batch(h, _ptr(d_X), int(m), _ptr(d_out), _stream(stream)),
            "adapt_select_batch")
 
 
 def adapt_select_batch_host(h: int, X, m: int, out, stream=None):
+    F = adapt_region_info(h)["num_features"]
+    _check_array(X, "X", "float32", F, int(m), False)
+    _check_array(out, "out", "int32", None, int(m), False)
     _check(_L.adapt_select_batch_host(h, _ptr(X), int(m), _ptr(out), _stream(stream)),
            "adapt_select_batch_host")
 

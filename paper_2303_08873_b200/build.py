@@ -27,15 +27,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
                    os.path.join(ROOT, "include", "adapt.h")]
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= max(map(os.path.getmtime, deps)):
         return SO
-    objs = []
-    for src in srcs:
+    from concurrent.futures import ThreadPoolExecutor
+
+    git = _git()
+
+    def compile_one(src: str) -> str:
         obj = os.path.join(CSRC, os.path.basename(src) + ".o")
         cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-Xptxas", "-v" if verbose else "-O3", f"-DADAPT_GIT=\"{_git()}\"",
+               "-Xptxas", "-v" if verbose else "-O3", f"-DADAPT_GIT=\"{git}\"",
                *os.environ.get("ADAPT_NVCC_DEFS", "").split(),  # tuning sweeps only
                "-I", os.path.join(ROOT, "include"), "-x", "cu", "-c", src, "-o", obj]
         subprocess.check_call(cmd)
-        objs.append(obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, srcs))
     subprocess.check_call(["nvcc", *ARCH, "-shared", "-o", SO, *objs, "-ldl"])
     for o in objs:
         os.remove(o)

@@ -401,6 +401,12 @@ struct adapt_region {
       hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, cmaps, psync, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall, hvis;  // winners, scalars, partition share reports
   adapt::Arena stage_p, stage_a, stage_b;  // per-level uploads: partition, its tables, histogram
+  cudaEvent_t sel_evt = nullptr;  // recorded after every device select (upload_tree waits)
+  ~adapt_region() {
+    if (sel_evt) cudaEventDestroy(sel_evt);
+  }
+  std::unordered_set<std::string> pair_set;  // distinct (features, variant) of the host records
+  int64_t autotrain_failed_at = -1;          // pair count of the last failed auto-train
   // Table-1 shim state
   bool active = false;
   std::vector<float> ctx_feat;
@@ -413,6 +419,8 @@ namespace adapt {
 namespace {
 
 std::map<std::string, std::unique_ptr<adapt_region>> g_regions;
+// adapt_train_many's union region (buffers reused across calls; freed by adapt_finalize)
+std::unique_ptr<adapt_region> g_multi;
 
 // model_type: "dtree[,D]" / "dtree,depth=D" /
 // "DecisionTree[,explore=RoundRobin]"; "rfc[,T[,D]]" / "rfc(T,D)" /
@@ -498,7 +506,14 @@ float round_down_f32(double t) {  // largest float32 <= t (V:A5)
   return f;
 }
 
+// selects still in flight on any stream read the device tree: wait for the
+// last one (a concurrent select must never walk a half-written tree)
+void wait_selects(adapt_region *h) {
+  if (h->sel_evt) CUDA_CHECK(cudaEventSynchronize(h->sel_evt));
+}
+
 void upload_tree(adapt_region *h, cudaStream_t s) {
+  wait_selects(h);
   std::vector<DNode> d(h->tree.size());
   for (size_t k = 0; k < h->tree.size(); k++) {
     const adapt_node_t &nd = h->tree[k];
@@ -571,6 +586,7 @@ void upload_tree(adapt_region *h, cudaStream_t s) {
 
 // forest: trees concatenated, child indices made absolute; roots[t] = offset
 void upload_forest(adapt_region *h, cudaStream_t s) {
+  wait_selects(h);
   std::vector<DNode> d;
   std::vector<int32_t> roots;
   for (const auto &tr : h->forest) {
@@ -1839,22 +1855,25 @@ void select_device(adapt_region *h, const float *X, int64_t m, int32_t *out, cud
   else
     launch_select_forest(h->d_forest.as<DNode>(), h->forest_nodes, h->d_roots.as<int32_t>(),
                          (int)h->forest.size(), X, m, h->F, out, s);
+  // the device tree may be replaced (retrain, set_tree, K-fold restore) on
+  // another stream: upload_tree waits for this event before overwriting it
+  if (!h->sel_evt) CUDA_CHECK(cudaEventCreateWithFlags(&h->sel_evt, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventRecord(h->sel_evt, s));
 }
 
-int64_t distinct_pairs(adapt_region *h) {
-  std::unordered_set<std::string> seen;
-  const int F = h->F;
-  std::string key(F * 4 + 4, '\0');
-  for (size_t r = 0; r < h->rvar.size(); r++) {
-    for (int f = 0; f < F; f++) {
-      float x = canon(h->rfeat[r * F + f]);
-      memcpy(&key[f * 4], &x, 4);
-    }
-    memcpy(&key[F * 4], &h->rvar[r], 4);
-    seen.insert(key);
+// distinct (features, variant) pairs of the host records, kept
+// incrementally by adapt_record: the shim asks after every end()
+void add_pair(adapt_region *h, const float *x, int variant) {
+  std::string key((size_t)h->F * 4 + 4, '\0');
+  for (int f = 0; f < h->F; f++) {
+    const float c = canon(x[f]);
+    memcpy(&key[(size_t)f * 4], &c, 4);
   }
-  return (int64_t)seen.size();
+  memcpy(&key[(size_t)h->F * 4], &variant, 4);
+  h->pair_set.insert(std::move(key));
 }
+
+int64_t distinct_pairs(adapt_region *h) { return (int64_t)h->pair_set.size(); }
 
 template <class Fn>
 int guarded(Fn &&fn) {
@@ -1964,6 +1983,7 @@ int adapt_init_host_comm(int device, int rank, int world, const adapt_host_comm_
 int adapt_finalize(void) {
   return guarded([&] {
     g_regions.clear();
+    g_multi.reset();
     if (g_ctx.comm) g_nccl.CommDestroy(g_ctx.comm);
     g_ctx = Ctx{};
   });
@@ -2038,6 +2058,7 @@ int adapt_record(adapt_region_t *h, const float *features, int variant, uint64_t
     h->rfeat.insert(h->rfeat.end(), features, features + h->F);
     h->rvar.push_back(variant);
     h->rns.push_back(elapsed_ns);
+    add_pair(h, features, variant);
   });
 }
 
@@ -2146,7 +2167,6 @@ namespace {
 // midpoints of the values present (R7), so every region's tree is the one
 // adapt_train would build.  Returns false (nothing changed) when the fused
 // path does not apply; the caller then trains the regions one by one.
-std::unique_ptr<adapt_region> g_multi;  // the union region (buffers reused across calls)
 
 bool train_many_fused(adapt_region *const *hs, int k, cudaStream_t s) {
   if (k < 2) return false;
@@ -2562,9 +2582,15 @@ void __adapt_region_end(void *r) {
     if (ns < 0) ns = 0;
     int rc = adapt_record(h, h->ctx_feat.data(), h->ctx_policy, (uint64_t)ns);
     if (rc) throw Error(rc, g_last_error);
-    if (!h->trained && !h->have_table && distinct_pairs(h) >= h->min_train) {  // P:569 auto-train
+    const int64_t pairs = distinct_pairs(h);
+    // P:569 auto-train; after a failed attempt, retry only once new distinct
+    // pairs have arrived (the same records would fail the same way)
+    if (!h->trained && !h->have_table && pairs >= h->min_train && pairs > h->autotrain_failed_at) {
       rc = adapt_train(h, nullptr);
-      if (rc) throw Error(rc, g_last_error);
+      if (rc) {
+        h->autotrain_failed_at = pairs;
+        throw Error(rc, g_last_error);
+      }
     }
   });
 }

@@ -28,7 +28,8 @@
 // Every quantity that decides the tree is an integer, so the result does not
 // depend on row order, on the number of ranks or on atomic ordering.
 #include <algorithm>
-#include <unordered_map>
+#include <map>
+#include <utility>
 
 #include "common.h"
 #include "ptx.h"
@@ -416,8 +417,11 @@ __global__ void __launch_bounds__(256) hist_flat_kernel(HistArgs a) {
 }  // namespace
 
 void ensure_smem_limit(const void *func, size_t bytes) {
-  static std::unordered_map<const void *, size_t> set;
-  size_t &cur = set[func];
+  // cudaFuncSetAttribute applies per device: cache per (device, function)
+  static std::map<std::pair<int, const void *>, size_t> set;
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  size_t &cur = set[{dev, func}];
   if (bytes <= cur) return;
   CUDA_CHECK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   cur = bytes;

@@ -209,8 +209,9 @@ def _costs(cfg: Config, x: list, rows: np.ndarray) -> list:
 
 
 def generate(cfg: Config | str, row0: int, n: int, seed: int | None = None,
-             noise: float = 0.05):
-    """Host table rows [row0, row0+n): (features f32 [n][F], times f32 [n][V])."""
+             noise: float = 0.05, times: bool = True):
+    """Host table rows [row0, row0+n): (features f32 [n][F], times f32 [n][V]).
+    times=False skips the cost models (selection inputs): times is None."""
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
     seed = cfg.seed if seed is None else seed
@@ -219,6 +220,8 @@ def generate(cfg: Config | str, row0: int, n: int, seed: int | None = None,
     for f, g in enumerate(cfg.grids):
         idx = (u24(seed, rows, f) * np.uint64(len(g))) >> np.uint64(24)
         X[:, f] = g[idx.astype(np.int64)]
+    if not times:
+        return X, None
     x64 = [X[:, f].astype(np.float64) for f in range(cfg.F)]
     costs = _costs(cfg, x64, rows.astype(np.int64))
     T = np.empty((n, cfg.V), np.float32)

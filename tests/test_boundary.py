@@ -159,3 +159,30 @@ def test_hot_kernels_do_not_spill():
             stack = int(re.search(r"STACK:(\d+)", line).group(1))
             assert stack == 0, f"{fn} spills ({stack} bytes of stack)"
     assert seen >= 12
+
+
+def test_binding_validates_operands_and_keeps_borrowed_tables():
+    """the binding checks dtype / shape / device before a pointer
+    crosses the C ABI, and holds borrowed device tables (on_device=1) until the
+    region's next record_table or its destruction (adapt.h: borrowed until
+    adapt_train returns)."""
+    import paper_2303_08873_b200 as ad
+    from paper_2303_08873_b200 import _binding as b
+
+    h = ad.adapt_region_create("validate_cpu", 3, 2)
+    X, T = np.ones((4, 3), np.float32), np.ones((4, 2), np.float32)
+    with pytest.raises(TypeError):
+        ad.adapt_record_table(h, X.astype(np.float64), T, 4, False)
+    with pytest.raises(ValueError):
+        ad.adapt_record_table(h, np.ones((4, 2), np.float32), T, 4, False)  # F = 3
+    with pytest.raises(ValueError):
+        ad.adapt_record_table(h, X, T, 5, False)  # fewer rows than n
+    with pytest.raises(ValueError):
+        ad.adapt_record_table(h, X, T, 4, True)  # host array passed as device memory
+    with pytest.raises(ValueError):
+        ad.adapt_select_batch_host(h, np.ones((4, 2), np.float32), 4, np.empty(4, np.int32))
+    with pytest.raises(TypeError):
+        ad.adapt_select_batch_host(h, X, 4, np.empty(4, np.int64))
+    b._borrowed[h] = (X, T)  # as a successful on_device record would leave it
+    ad.adapt_region_destroy(h)
+    assert h not in b._borrowed

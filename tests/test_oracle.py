@@ -370,3 +370,18 @@ def test_negative_zero_canonical():
     assert t[0]["threshold"] == 0.5 and len(t) == 3
     vt = oracle.value_table(X, 0)
     assert vt.tolist() == [0.0, 1.0] and math.copysign(1, float(vt[0])) == 1
+
+
+def test_openmp_build_is_identical():
+    """The all-cores build (liboracle_omp.so: the same oracle.c with -fopenmp,
+    features of a node scanned in parallel and reduced in feature order) gives
+    byte-identical trees and selections — it only serves timing and the
+    full-size expected outputs (scripts/oracle_fullsize.py)."""
+    import synth
+
+    X, T = synth.generate("C4", 0, 20_000)
+    y = oracle.labels(T)
+    a = oracle.train(X, y, 48, 8)
+    b = oracle.train(X, y, 48, 8, omp=True)
+    assert len(a) > 100 and a.tobytes() == b.tobytes()
+    assert np.array_equal(oracle.select(a, X), oracle.select(a, X, omp=True))
