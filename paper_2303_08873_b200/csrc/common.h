@@ -166,7 +166,6 @@ struct HistArgs {            // a4: class histograms of the given pieces' rows
   uint32_t *H;               // level histograms
   const int64_t *soff;       // [slots] element offset of a slot's matrix in H
   int nranges;               // CTA groups; CTA x handles range x / ngroups, group x % ngroups
-  uint32_t *sync;            // [nranges] partner-sync counters, zeroed (null: no sync)
 };
 void launch_hist(const HistArgs &a, cudaStream_t s);
 void launch_hist_flat(const HistArgs &a, cudaStream_t s);  // small nodes: thread per row

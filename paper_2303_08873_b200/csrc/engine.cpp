@@ -398,7 +398,7 @@ struct adapt_region {
   // scratch
   adapt::DevBuf gkey, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, lk_keys, lk_mul, lk_skeys,
       H0, H1, segs,
-      hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, cmaps, psync, xa, xb, oa, ob;
+      hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, cmaps, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall, hvis;  // winners, scalars, partition share reports
   adapt::Arena stage_p, stage_a, stage_b;  // per-level uploads: partition, its tables, histogram
   cudaEvent_t sel_evt = nullptr;  // recorded after every device select (upload_tree waits)
@@ -1356,14 +1356,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       ha.nranges = (int)std::max<int64_t>(1, std::min<int64_t>((htotal + 4095) / 4096,
                                                                std::max(1, sms / ngroups)));
       // each CTA reads only its own word plane, so partner CTAs share just the
-      // 1-byte labels: no lockstep needed (ADAPT_HIST_SYNC=1 re-enables it)
-      ha.sync = nullptr;
-      static const bool want_sync = getenv("ADAPT_HIST_SYNC") != nullptr;
-      if (want_sync && ngroups > 1 && ha.nranges * ngroups <= sms) {
-        h->psync.ensure((size_t)ha.nranges * 4);
-        CUDA_CHECK(cudaMemsetAsync(h->psync.p, 0, (size_t)ha.nranges * 4, s));
-        ha.sync = h->psync.as<uint32_t>();
-      }
+      // 1-byte labels: they run unsynchronised
       snprintf(nm, sizeof nm, "hist_L%02d", level);
       Phase ph(per_level ? nm : "hist", s, (double)(htotal + ftotal) * (F + 1));
       launch_hist(ha, s);

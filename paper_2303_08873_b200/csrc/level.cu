@@ -18,9 +18,7 @@
 //                     at most 4 shared-memory reductions per row, reading only
 //                     that word's plane (4 bytes per row), so the G CTAs
 //                     of a range share only the 1-byte labels and run
-//                     unsynchronised (ADAPT_HIST_SYNC=1 restores an optional
-//                     lockstep through a global counter; it measured slower
-//                     once bins became word planes).  Per node only the classes present in it get
+//                     unsynchronised.  Per node only the classes present in it get
 //                     counters (the host knows them from the parent's split),
 //                     with an odd class stride (bank spread); the block's
 //                     counters are flushed into the node's global histogram
@@ -97,12 +95,6 @@ __device__ __forceinline__ int row_byte(const Row<BS> &r, int f) {
 
 __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
 }
 
 __device__ __forceinline__ int first_seg(const Seg *segs, int nseg, uint32_t p) {
@@ -210,7 +202,6 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition_kernel
 // ------------------------------------------------------------ histogram --
 constexpr int kHistThreads = 1024;
 constexpr int kHistUnroll = ADAPT_HIST_UNROLL;  // rows in flight per thread (latency-bound otherwise)
-constexpr int kSyncEvery = 2;  // iterations of kHistUnroll x 1024 rows between partner syncs
 
 // WEIGHTED (forests): rows add their bootstrap weight; a separate instance so
 // the plain path keeps its registers (the weights cost 16 more per thread)
@@ -234,7 +225,6 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
   const uint32_t p1 = min(p0 + R, a.total_rows);
   int s = p0 < p1 ? first_seg(a.segs, a.nseg, p0) : a.nseg;
   const uint32_t sbase = smem_u32(sh);
-  uint32_t iter = 0, epoch = 0;
   while (p0 < p1 && s < a.nseg) {
     // ---- one node's rows at virtual positions [p0, pe) ----
     const Seg first = a.segs[s];
@@ -303,15 +293,6 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
       const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
       const uint32_t q1 = min(sg.len, pe - sg.row_base);
       for (uint32_t qb = q0; qb < q1; qb += UNROLL * blockDim.x) {
-        if (a.sync && ++iter % kSyncEvery == 0) {  // keep the G CTAs within L2 reach
-          __syncthreads();
-          if (tid == 0) {
-            epoch++;
-            atomicAdd(a.sync + range, 1u);
-            while (ld_acquire_gpu(a.sync + range) < epoch * G) __nanosleep(64);
-          }
-          __syncthreads();
-        }
         uint32_t w[UNROLL];
         int label[UNROLL];
         uint32_t wv[WEIGHTED ? UNROLL : 1];  // row weight: the bootstrap multiplicity
@@ -474,11 +455,7 @@ void launch_hist(const HistArgs &a, cudaStream_t s) {
   cfg.blockDim = dim3(kHistThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency of a range's CTAs (partner sync)
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = a.sync ? 1 : 0;
+  cfg.numAttrs = 0;
   switch (a.BS) {
 #define CASE(B)                                                                              \
   case B:                                                                                    \

@@ -240,6 +240,46 @@ def test_degenerate_cases():
     assert len(got) == 7
 
 
+def _degenerate_tables():
+    rng = np.random.default_rng(0)
+    yield "single row", np.array([[1.5, 2.0]], np.float32), np.array([[3.0, 1.0]], np.float32), 4
+    yield "identical rows", np.ones((100, 3), np.float32), rng.random((100, 4)).astype(np.float32), 5
+    yield ("one class", np.random.default_rng(1).integers(0, 9, (500, 2)).astype(np.float32),
+           np.tile(np.array([[1, 2, 3]], np.float32), (500, 1)), 3)
+    yield ("-0/+0", np.array([[-0.0], [0.0], [1.0], [2.0]] * 10, np.float32),
+           np.array([[1, 2], [2, 1], [1, 2], [2, 1]] * 10, np.float32), 3)
+    yield ("XOR", np.array([[0, 0], [0, 1], [1, 0], [1, 1]] * 7, np.float32),
+           np.array([[1, 2], [2, 1], [2, 1], [1, 2]] * 7, np.float32), 8)
+
+
+@pytest.mark.parametrize("how", ["wide_classes", "many_rows", "many_features"])
+def test_degenerate_cases_general_path(how):
+    """The degenerate cases of test_degenerate_cases past the one-block
+    small-table limits (n <= 512, F <= 8, V <= 16), so R10 (zero-gain XOR
+    splits, no-candidate leaves), one class, -0/+0 and the single row run
+    through the general level loop (hist / split / winner kernels and the host
+    leaf logic that C4 uses):
+      wide_classes  : times padded with unmeasured (+inf) variants to V = 20;
+      many_rows     : every row repeated 13x (n > 512; multiplicity counts, R5);
+      many_features : 7 constant features appended (F > 8; never a candidate)."""
+    for name, X, T, D in _degenerate_tables():
+        if how == "wide_classes":
+            T = np.concatenate([T, np.full((len(T), 20 - T.shape[1]), np.inf, np.float32)], 1)
+        elif how == "many_rows":
+            X, T = np.repeat(X, 13, axis=0), np.repeat(T, 13, axis=0)
+        else:
+            X = np.concatenate([X, np.full((len(X), 7), 4.25, np.float32)], 1)
+        n, F = X.shape
+        h = _train(X, T, D)
+        assert len(ad.adapt_train_stats(h)) >= 1, f"{name}: did not run the level loop"
+        ad.adapt_region_destroy(h)
+        got = full_parity(X, T, D)
+        if name == "XOR":
+            assert len(got) == 7  # zero-gain splits taken (R10)
+        if name in ("single row", "identical rows", "one class"):
+            assert len(got) == 1  # no candidate cut / pure (R10)
+
+
 def test_max_distinct_and_classes():
     rng = np.random.default_rng(3)
     n = 60000

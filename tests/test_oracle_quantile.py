@@ -52,8 +52,8 @@ def _brute_root(x, y, C, cuts):
             continue
         cl = np.bincount(y[left], minlength=C)
         cr = tot - cl
-        if all(int(cl[k]) * (n - nl) == int(cr[k]) * nl for k in range(C)):
-            continue  # not improving (R10)
+        # R10: every cut with two non-empty sides competes,
+        # zero-gain ones included; they score exactly S/n, below any improving cut
         s = Fraction(int((cl.astype(object) ** 2).sum()), nl) + \
             Fraction(int((cr.astype(object) ** 2).sum()), n - nl)
         if best is None or s > best[0]:  # strict: ties keep the lowest cut
