@@ -327,11 +327,136 @@ def bench_c1(args, ad, torch, dev, stream):
             ad.adapt_select(h, x)
     sel_ns = (time.perf_counter() - t0) * 1e9 / (reps * len(xs))
     ad.adapt_region_destroy(h)
+    c_ns = None
+    exe = os.path.join(ROOT, "scripts", "select_latency")
+    if os.path.exists(exe):  # the same walk timed from C: no Python in the loop
+        import tempfile
+
+        with tempfile.TemporaryDirectory() as td:
+            xf, tf = os.path.join(td, "X.f32"), os.path.join(td, "T.f32")
+            X.tofile(xf)
+            T.tofile(tf)
+            r = subprocess.run([exe, xf, tf, str(cfg.N), str(cfg.F), str(cfg.V), f"dtree,depth={cfg.D}",
+                                "2000"], capture_output=True, text=True, timeout=120)
+            if r.returncode == 0:
+                c_ns = json.loads(r.stdout)["ns_per_call"]
     return {"workload": "C1: 512 profiled samples, 1 feature, 2 variants, depth 4",
             "train_us_median": statistics.median(lat), "train_us_min": min(lat),
             "select_host_ns_per_call": sel_ns,
-            "note": "adapt_select through the ctypes binding (includes Python call overhead); "
-                    "paper Table 4: 60-280 us training, 7-20 ns per inference on the host"}
+            "select_host_ns_per_call_c": c_ns,
+            "note": "select_host_ns_per_call: adapt_select through the ctypes binding (includes "
+                    "Python call overhead); select_host_ns_per_call_c: the same C-ABI call timed in a "
+                    "C loop (scripts/select_latency.c, 2000 passes over the 512 vectors); paper "
+                    "Table 4: 60-280 us training, 7-20 ns per inference on the host"}
+
+
+def bench_c3(args, ad, adist, torch, dev, stream, rank: int, world: int, peak: float):
+    """C3 as BASELINE.json states it: 1e6 samples, 8 features, 6 block-size
+    variants, depth 12, 256 bins — adapt_record_table + adapt_train per step."""
+    cfg = synth.CONFIGS["C3"]
+    lo, hi = adist.shard_bounds(cfg.N, rank, world)
+    flat, off = cfg.grid_table
+    g, o = torch.from_numpy(flat).to(dev), torch.from_numpy(off).to(dev)
+    X = torch.empty((hi - lo, cfg.F), dtype=torch.float32, device=dev)
+    T = torch.empty((hi - lo, cfg.V), dtype=torch.float32, device=dev)
+    synth.generate_device(cfg, lo, hi - lo, X.data_ptr(), T.data_ptr(), g.data_ptr(), o.data_ptr(),
+                          stream.cuda_stream)
+    h = ad.adapt_region_create("bench_c3", cfg.F, cfg.V, f"dtree,depth={cfg.D}", 0)
+
+    def step():
+        ad.adapt_record_table(h, X, T, hi - lo, True, stream)
+        ad.adapt_train(h, stream)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = adist.max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
+    levels = ad.adapt_train_stats(h)
+    rows = sum((lv["rows_part"] if i else hi - lo) for i, lv in enumerate(levels) if lv["nodes"])
+    byts = (4 * cfg.F + 4 * cfg.V + cfg.F + 1) * cfg.N + (cfg.F + 1) * rows * world
+    ad.adapt_region_destroy(h)
+    return {"workload": "C3: 1e6-row table, 8 features, 6 variants (GPU block size), depth 12",
+            "ms": ms, "train_samples_per_s": cfg.N / (ms / 1e3),
+            "survey_bytes": byts, "hbm_frac": byts / (ms / 1e3) / 1e9 / peak,
+            "note": "latency/launch-bound at this size (SURVEY 8(d): 26 us at 100% of HBM)"}
+
+
+def bench_scaling_proxy(args, ad, torch, dev, stream, full_levels, full_ms: float, peak: float):
+    """Multi-GPU readiness without an 8-GPU box: C4's per-rank work
+    at P = 8 — the first 1.25e7 rows of the table — on this one GPU, timed like
+    the main step, with (i) the share of the step in which no engine kernel runs
+    (host bookkeeping and launch gaps), per level and in total, and (ii) the
+    projected per-level exchange at P = 8: the default all-reduce moves
+    2 (P-1)/P x the direct nodes' histogram bytes per rank (the same histogram
+    sizes as the full table's, `full_levels`), timed at the measured 8-rank
+    NVLink all-reduce bus bandwidth of 725 GB/s (B200_PROFILING.md)."""
+    cfg = synth.CONFIGS["C4"]
+    P = 8
+    n = cfg.N // P
+    flat, off = cfg.grid_table
+    g, o = torch.from_numpy(flat).to(dev), torch.from_numpy(off).to(dev)
+    X = torch.empty((n, cfg.F), dtype=torch.float32, device=dev)
+    T = torch.empty((n, cfg.V), dtype=torch.float32, device=dev)
+    out = torch.empty(n, dtype=torch.int32, device=dev)
+    synth.generate_device(cfg, 0, n, X.data_ptr(), T.data_ptr(), g.data_ptr(), o.data_ptr(),
+                          stream.cuda_stream)
+    h = ad.adapt_region_create("bench_proxy", cfg.F, cfg.V, f"dtree,depth={cfg.D}", 0)
+
+    def step():
+        ad.adapt_record_table(h, X, T, n, True, stream)
+        ad.adapt_train(h, stream)
+        ad.adapt_select_batch(h, X, n, out, stream)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    ad.adapt_profile_reset()
+    ad.adapt_profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ad.adapt_profile_enable(False)
+    prof = ad.adapt_profile_get()
+    ms = e0.elapsed_time(e1) / args.steps
+    kern_ms = sum(v["ms"] for k, v in prof.items() if k.split("_L")[0] in KERNEL_PHASES) / args.steps
+    lv_ms = {}
+    for k, v in prof.items():
+        base, _, lv = k.partition("_L")
+        if lv.isdigit() and base in KERNEL_PHASES:
+            lv_ms[int(lv)] = lv_ms.get(int(lv), 0.0) + v["ms"] / args.steps
+    levels = ad.adapt_train_stats(h)
+    per_level = []
+    for d, lv in enumerate(levels):
+        full = full_levels[d] if d < len(full_levels) else lv
+        ar = 2 * (P - 1) / P * full.get("direct_hist_bytes", 0)
+        per_level.append({"nodes": lv["nodes"], "kernel_ms": round(lv_ms.get(d, 0.0), 4),
+                          "allreduce_bytes_per_rank": int(ar),
+                          "allreduce_ms_at_725GBps": round(ar / 725e9 * 1e3, 4)})
+    ad.adapt_region_destroy(h)
+    del X, T, out
+    torch.cuda.empty_cache()
+    comm_ms = sum(x["allreduce_ms_at_725GBps"] for x in per_level)
+    return {"workload": "C4 rows [0, 1.25e7): one rank's shard at P = 8 (strong scaling of the 1e8 table)",
+            "rows": n, "ms_per_step": ms, "kernel_ms_per_step": kern_ms,
+            "host_idle_share": max(0.0, 1 - kern_ms / ms),
+            "projected_allreduce_ms_per_step": comm_ms,
+            "projected_step_ms_p8": ms + comm_ms,
+            "projected_speedup_p8": full_ms / (ms + comm_ms),
+            "levels": per_level,
+            "note": "per-level kernel ms include partition, histogram, subtraction, split and "
+                    "winner (levels with per-level phase names); the projection adds the "
+                    "exchange serially (no overlap)"}
 
 
 def run_reference(args, rank: int, world: int):
@@ -383,6 +508,7 @@ def main():
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-kfold", action="store_true")
     ap.add_argument("--no-c2", action="store_true")
+    ap.add_argument("--no-proxy", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -521,6 +647,12 @@ def main():
     kfold = None
     if not args.no_kfold and args.config == "C4":
         kfold = bench_kfold(args, ad, adist, torch, dev, stream, rank, world)
+    c3 = None
+    if not args.no_c2 and args.config == "C4":
+        c3 = bench_c3(args, ad, adist, torch, dev, stream, rank, world, peak)
+    proxy = None
+    if not args.no_proxy and args.config == "C4" and world == 1:
+        proxy = bench_scaling_proxy(args, ad, torch, dev, stream, levels, ms, peak)
 
     if rank != 0:
         if world > 1:
@@ -628,6 +760,8 @@ def main():
         "kfold": kfold,
         "c2_regions": c2,
         "c1_latency": c1,
+        "c3_train": c3,
+        "strong_scaling_proxy": proxy,
         "phase_ms_per_step": step_ms_phases,
         "tree_nodes": int(len(tree)),
         "levels": levels,

@@ -274,11 +274,15 @@ int adapt_profile_reset(void);
  * the recorded events. */
 int adapt_profile_get(adapt_phase_t *out, int cap, int *n);
 /* Per-level statistics of the last adapt_train on this rank (SURVEY §8(d)
- * per-level reporting): for level d, out[5d] = frontier nodes, out[5d+1] =
- * rows histogrammed, out[5d+2] = rows partitioned, out[5d+3] = bytes of the
- * level's node histograms (class-compacted, direct + derived), out[5d+4] =
- * bytes all-reduced over ranks (0 on one rank).  *levels receives the level
- * count (forests / K-fold: the levels of every tree / batch, in order). */
+ * per-level reporting): for level d, out[6d] = frontier nodes, out[6d+1] =
+ * rows histogrammed, out[6d+2] = rows partitioned, out[6d+3] = bytes of the
+ * level's node histograms (class-compacted, direct + derived), out[6d+4] =
+ * bytes through the level's collectives on this rank (0 on one rank; the
+ * all-reduce input, or the reduce-scatter input plus the gathered winner
+ * records with ADAPT_HIST_COMM=rs), out[6d+5] = bytes of the DIRECT nodes'
+ * histograms (what the default all-reduce sums when world > 1; reported on
+ * one rank too, for scaling projections).  *levels receives the level count
+ * (forests / K-fold: the levels of every tree / batch, in order). */
 int adapt_train_stats(adapt_region_t *h, int64_t *out, int cap, int *levels);
 
 /* ---- Apollo Table-1 shim (lowering order P:558-569) ------------- */

@@ -476,10 +476,12 @@ def adapt_profile_get() -> dict:
 def adapt_train_stats(h: int) -> list:
     lv = ctypes.c_int()
     _check(_L.adapt_train_stats(h, None, 0, ctypes.byref(lv)), "adapt_train_stats")
-    buf = np.zeros(5 * max(lv.value, 1), np.int64)
+    K = 6  # values per level (adapt.h)
+    buf = np.zeros(K * max(lv.value, 1), np.int64)
     _check(_L.adapt_train_stats(h, buf.ctypes.data, buf.size, ctypes.byref(lv)), "adapt_train_stats")
-    return [dict(nodes=int(buf[5 * d]), rows_hist=int(buf[5 * d + 1]), rows_part=int(buf[5 * d + 2]),
-                 hist_bytes=int(buf[5 * d + 3]), comm_bytes=int(buf[5 * d + 4]))
+    return [dict(nodes=int(buf[K * d]), rows_hist=int(buf[K * d + 1]), rows_part=int(buf[K * d + 2]),
+                 hist_bytes=int(buf[K * d + 3]), comm_bytes=int(buf[K * d + 4]),
+                 direct_hist_bytes=int(buf[K * d + 5]))
             for d in range(lv.value)]
 
 

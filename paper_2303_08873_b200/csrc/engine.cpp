@@ -190,6 +190,8 @@ struct Nccl {
                             ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
+                                ncclComm_t, cudaStream_t) = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
   void load() {
     if (h) return;
@@ -205,6 +207,7 @@ struct Nccl {
     SYM(CommDestroy, "ncclCommDestroy");
     SYM(AllReduce, "ncclAllReduce");
     SYM(AllGather, "ncclAllGather");
+    SYM(ReduceScatter, "ncclReduceScatter");
     SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
   }
@@ -228,6 +231,14 @@ Ctx g_ctx;
 // (ADAPT_NCCL_SELF=1 gives a world-1 run a 1-rank NCCL communicator so the
 // NCCL path is exercised on one GPU; collectives are then real NCCL calls)
 bool collectives_on() { return g_ctx.world > 1 || g_ctx.comm != nullptr; }
+
+// per-level histogram exchange: ADAPT_HIST_COMM=rs selects the reduce-scatter
+// by node ownership (+ owner split search, winner all-gather); default: the
+// all-reduce of the direct nodes' histograms
+bool hist_comm_rs() {
+  const char *m = getenv("ADAPT_HIST_COMM");
+  return collectives_on() && m && !strcmp(m, "rs");
+}
 
 void host_hook(int rc, const char *what) {
   if (rc != 0) throw Error(ADAPT_E_NCCL, std::string(what) + ": host collective hook returned " +
@@ -265,6 +276,36 @@ void comm_allreduce_sum(void *dbuf, size_t count, bool wide, cudaStream_t s, con
     CUDA_CHECK(cudaMemcpyAsync(dbuf, n.data(), count * 4, cudaMemcpyHostToDevice, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
   }
+}
+
+// drecv[0, count) = sum over ranks of dsend[rank * count, (rank + 1) * count)
+// (u32): rank r receives the reduced chunk r (histograms summed
+// only at the owner of their nodes)
+void comm_reduce_scatter(const void *dsend, void *drecv, size_t count, cudaStream_t s,
+                         const char *what) {
+  if (!collectives_on()) {
+    CUDA_CHECK(cudaMemcpyAsync(drecv, dsend, count * 4, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  if (count == 0) return;
+  if (!g_ctx.host_comm) {
+    g_nccl.check(g_nccl.ReduceScatter(dsend, drecv, count, ncclUint32, ncclSum, g_ctx.comm, s), what);
+    return;
+  }
+  // host hooks: the element-wise sum of the whole buffer, then this rank's chunk
+  const size_t total = count * (size_t)g_ctx.world;
+  std::vector<uint32_t> n(total);
+  CUDA_CHECK(cudaMemcpyAsync(n.data(), dsend, total * 4, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  std::vector<uint64_t> w(n.begin(), n.end());
+  host_hook(g_ctx.hooks.all_reduce_u64(w.data(), total, g_ctx.hooks.user), what);
+  const size_t o = count * (size_t)g_ctx.rank;
+  for (size_t i = 0; i < count; i++) {
+    if (w[o + i] > 0xFFFFFFFFull) throw Error(ADAPT_E_NCCL, std::string(what) + ": u32 sum overflow");
+    n[i] = (uint32_t)w[o + i];
+  }
+  CUDA_CHECK(cudaMemcpyAsync(drecv, n.data(), count * 4, cudaMemcpyHostToDevice, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
 // drecv[r*bytes, (r+1)*bytes) = rank r's dsend, on the device
@@ -397,9 +438,9 @@ struct adapt_region {
   std::vector<int64_t> stats;
   // scratch
   adapt::DevBuf gkey, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, lk_keys, lk_mul, lk_skeys,
-      H0, H1, segs,
+      H0, H1, Hg, reso, resall, segs,
       hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, cmaps, xa, xb, oa, ob;
-  adapt::HostBuf hres, hsmall, hvis;  // winners, scalars, partition share reports
+  adapt::HostBuf hres, hsmall, hvis, hgat;  // winners, scalars, partition share reports, gathered winners
   adapt::Arena stage_p, stage_a, stage_b;  // per-level uploads: partition, its tables, histogram
   cudaEvent_t sel_evt = nullptr;  // recorded after every device select (upload_tree waits)
   ~adapt_region() {
@@ -1098,6 +1139,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
   int sms = 148;
   CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g_ctx.device));
   DevBuf *Hcur = &h->H0, *Hprev = &h->H1;
+  // SURVEY §8(e) "the better option": per level, every rank keeps its LOCAL
+  // histograms of all frontier nodes (derived siblings by local subtraction),
+  // a reduce-scatter sums each node's histogram only at its owner rank (slot
+  // ranges balanced by bytes), owners search the splits of their nodes, and an
+  // all-gather of the winner records gives every rank the identical decisions.
+  // Otherwise (default): all-reduce of the direct nodes, derived globally.
+  const bool rs = hist_comm_rs();
   static const bool per_level = getenv("ADAPT_PROFILE_LEVELS") != nullptr;
   char nm[32];
   auto virtualize = [](std::vector<Seg> &v, bool by_slot) {  // row_base, node extents
@@ -1212,6 +1260,26 @@ void train_region(adapt_region *h, cudaStream_t s) {
     for (const auto &fn : frontier) slot_kc[fn.slot] = fn.cls.count();
     std::vector<int64_t> soff(nslots + 1, 0);
     for (int k = 0; k < nslots; k++) soff[k + 1] = soff[k] + DS * slot_kc[k];
+    const int64_t direct_bytes = soff[ndirect_slots] * 4;  // (direct slots first)
+    // reduce-scatter mode: slot ranges [own[r], own[r+1]) owned by rank r,
+    // balanced by histogram bytes, each padded to Q counters at offset r * Q
+    const int NR = g_ctx.world, me = g_ctx.rank;
+    std::vector<int32_t> own(NR + 1, nslots);
+    int64_t Q = 0;
+    if (rs) {
+      const int64_t tot = soff[nslots];
+      for (int r = 0; r < NR; r++)
+        own[r] = (int32_t)(std::lower_bound(soff.begin(), soff.begin() + nslots, (tot * r + NR - 1) / NR) -
+                           soff.begin());
+      own[NR] = nslots;
+      for (int r = 0; r < NR; r++) Q = std::max<int64_t>(Q, soff[own[r + 1]] - soff[own[r]]);
+      Q = std::max<int64_t>(Q, 1);
+      std::vector<int64_t> ps(nslots + 1);
+      for (int r = 0; r < NR; r++)
+        for (int k = own[r]; k < own[r + 1]; k++) ps[k] = r * Q + soff[k] - soff[own[r]];
+      ps[nslots] = NR * Q;
+      soff.swap(ps);
+    }
     std::vector<uint8_t> cmaps;  // per direct node: class -> compact index (255: absent)
     cmaps.reserve((size_t)ndirect_slots * C);
     std::vector<int32_t> node_ci(A, -1), node_kc(A);
@@ -1271,6 +1339,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
                  o_big = sa.put(big_nodes), o_small = sa.put(small_nodes), o_roff = sa.put(res_off);
     sa.flush(s);
     Hcur->ensure((size_t)soff[nslots] * 4 + 16);
+    if (rs)  // padding after each owner's range: summed by the reduce-scatter, never read
+      for (int r = 0; r < NR; r++) {
+        const int64_t used = (own[r + 1] > own[r] ? soff[own[r + 1] - 1] + DS * slot_kc[own[r + 1] - 1]
+                                                  : r * Q) - r * Q;
+        if (used < Q)
+          CUDA_CHECK(cudaMemsetAsync(Hcur->as<uint32_t>() + r * Q + used, 0, (size_t)(Q - used) * 4, s));
+      }
     {
       Phase ph("zero", s, 0);
       launch_zero_slots(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_soff), sa.ptr<int32_t>(o_skc), DS,
@@ -1366,32 +1441,93 @@ void train_region(adapt_region *h, cudaStream_t s) {
       fa.total_rows = ftotal;
       launch_hist_flat(fa, s);
     }
-    if (collectives_on() && ndirect_slots > 0)  // the direct slots are contiguous at the front
+    if (!rs && collectives_on() && ndirect_slots > 0)  // the direct slots are contiguous at the front
       comm_allreduce_sum(Hcur->p, (size_t)soff[ndirect_slots], false, s, "allreduce histograms");
-    if (!jobs.empty()) {
+    if (!jobs.empty()) {  // rs: local parent - local direct sibling = the sibling's local rows
       Phase ph("subtract", s, 0);
       launch_subtract(Hcur->as<uint32_t>(), Hprev->as<uint32_t>(), DS, sa.ptr<SubJob>(o_jobs),
                       sa.ptr<int16_t>(o_maps), sa.ptr<int32_t>(o_sst), (int)jobs.size(), sblocks, s);
     }
-    h->cand.ensure((size_t)A * F * sizeof(SplitCand));
-    h->res.ensure((size_t)res_off[A] + 16);
-    {
-      snprintf(nm, sizeof nm, "split_L%02d", level);
-      Phase ph(per_level ? nm : "split", s, 0);
-      launch_split(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_noff), sa.ptr<int32_t>(o_nkc),
-                   sa.ptr<int32_t>(o_big), (int)big_nodes.size(), sa.ptr<int32_t>(o_small),
-                   (int)small_nodes.size(), F, h->hoff.as<int32_t>(),
-                   h->dnval.as<int32_t>(), h->cand.as<SplitCand>(), s);
-    }
-    {
-      Phase ph("winner", s, 0);
-      launch_winner(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_noff), sa.ptr<int32_t>(o_nkc), A, F, C,
-                    h->hoff.as<int32_t>(), h->dnval.as<int32_t>(), h->cand.as<SplitCand>(),
-                    h->res.as<uint8_t>(), sa.ptr<int64_t>(o_roff), s);
-    }
     h->hres.ensure((size_t)res_off[A] + 16);
     uint8_t *hr = h->hres.as<uint8_t>();
-    CUDA_CHECK(cudaMemcpyAsync(hr, h->res.p, (size_t)res_off[A], cudaMemcpyDeviceToHost, s));
+    int64_t comm_bytes = collectives_on() ? (int64_t)soff[ndirect_slots] * 4 : 0;
+    if (!rs) {
+      h->cand.ensure((size_t)A * F * sizeof(SplitCand));
+      h->res.ensure((size_t)res_off[A] + 16);
+      {
+        snprintf(nm, sizeof nm, "split_L%02d", level);
+        Phase ph(per_level ? nm : "split", s, 0);
+        launch_split(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_noff), sa.ptr<int32_t>(o_nkc),
+                     sa.ptr<int32_t>(o_big), (int)big_nodes.size(), sa.ptr<int32_t>(o_small),
+                     (int)small_nodes.size(), F, h->hoff.as<int32_t>(),
+                     h->dnval.as<int32_t>(), h->cand.as<SplitCand>(), s);
+      }
+      {
+        Phase ph("winner", s, 0);
+        launch_winner(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_noff), sa.ptr<int32_t>(o_nkc), A, F, C,
+                      h->hoff.as<int32_t>(), h->dnval.as<int32_t>(), h->cand.as<SplitCand>(),
+                      h->res.as<uint8_t>(), sa.ptr<int64_t>(o_roff), s);
+      }
+      CUDA_CHECK(cudaMemcpyAsync(hr, h->res.p, (size_t)res_off[A], cudaMemcpyDeviceToHost, s));
+    } else {
+      // a5 by ownership: this rank's slots summed over ranks into Hg
+      h->Hg.ensure((size_t)Q * 4 + 16);
+      comm_reduce_scatter(Hcur->p, h->Hg.p, (size_t)Q, s, "reduce-scatter histograms");
+      // a6 for the owned nodes only, in slot order: owned index i = slot own[r] + i
+      std::vector<int32_t> slot_j(nslots);
+      for (int j = 0; j < A; j++) slot_j[frontier[j].slot] = j;
+      std::vector<int64_t> ooff;
+      std::vector<int32_t> okc, obig, osmall;
+      std::vector<std::vector<int64_t>> rb(NR);  // winner record offsets of every rank's owned nodes
+      for (int r = 0; r < NR; r++) {
+        rb[r].assign(1, 0);
+        for (int k = own[r]; k < own[r + 1]; k++)
+          rb[r].push_back(rb[r].back() + (res_off[slot_j[k] + 1] - res_off[slot_j[k]]));
+      }
+      int64_t RB = 16;
+      for (int r = 0; r < NR; r++) RB = std::max(RB, rb[r].back());
+      for (int k = own[me]; k < own[me + 1]; k++) {
+        const int j = slot_j[k], i = (int)okc.size();
+        ooff.push_back(soff[k] - me * Q);
+        okc.push_back(node_kc[j]);
+        (node_kc[j] <= split_small_max_classes() ? osmall : obig).push_back(i);
+      }
+      const int m = (int)okc.size();
+      Arena &so = h->stage_b;
+      so.reset();
+      const size_t o_ooff = so.put(ooff), o_okc = so.put(okc), o_obig = so.put(obig),
+                   o_osmall = so.put(osmall), o_orb = so.put(rb[me]);
+      so.flush(s);
+      h->cand.ensure((size_t)std::max(m, 1) * F * sizeof(SplitCand));
+      h->reso.ensure((size_t)RB + 16);
+      h->resall.ensure((size_t)RB * NR + 16);
+      {
+        snprintf(nm, sizeof nm, "split_L%02d", level);
+        Phase ph(per_level ? nm : "split", s, 0);
+        launch_split(h->Hg.as<uint32_t>(), so.ptr<int64_t>(o_ooff), so.ptr<int32_t>(o_okc),
+                     so.ptr<int32_t>(o_obig), (int)obig.size(), so.ptr<int32_t>(o_osmall),
+                     (int)osmall.size(), F, h->hoff.as<int32_t>(), h->dnval.as<int32_t>(),
+                     h->cand.as<SplitCand>(), s);
+      }
+      {
+        Phase ph("winner", s, 0);
+        launch_winner(h->Hg.as<uint32_t>(), so.ptr<int64_t>(o_ooff), so.ptr<int32_t>(o_okc), m, F, C,
+                      h->hoff.as<int32_t>(), h->dnval.as<int32_t>(), h->cand.as<SplitCand>(),
+                      h->reso.as<uint8_t>(), so.ptr<int64_t>(o_orb), s);
+      }
+      // every rank gets every owner's winner records (padded to RB bytes each)
+      comm_allgather(h->reso.p, h->resall.p, (size_t)RB, s, "all-gather winners");
+      h->hgat.ensure((size_t)RB * NR + 16);
+      uint8_t *ga = h->hgat.as<uint8_t>();
+      CUDA_CHECK(cudaMemcpyAsync(ga, h->resall.p, (size_t)RB * NR, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      for (int r = 0; r < NR; r++)
+        for (int k = own[r]; k < own[r + 1]; k++) {
+          const int j = slot_j[k];
+          memcpy(hr + res_off[j], ga + (size_t)r * RB + rb[r][k - own[r]], (size_t)(res_off[j + 1] - res_off[j]));
+        }
+      comm_bytes = NR * Q * 4 + RB * NR;
+    }
     if (trace) tr[4] = now_us();
     CUDA_CHECK(cudaStreamSynchronize(s));
     if (trace) tr[5] = now_us();
@@ -1399,7 +1535,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
     h->stats.push_back(htotal + ftotal);
     h->stats.push_back(rows_part);
     h->stats.push_back((int64_t)soff[nslots] * 4);  // histogram bytes (direct + derived nodes)
-    h->stats.push_back(collectives_on() ? (int64_t)soff[ndirect_slots] * 4 : 0);  // all-reduced bytes
+    h->stats.push_back(comm_bytes);  // bytes through the per-level collectives
+    h->stats.push_back(direct_bytes);  // the direct nodes' histograms
 
     // ---- decide every frontier node; build the next level ----
     std::vector<FNode> next;
@@ -2507,7 +2644,7 @@ int adapt_profile_get(adapt_phase_t *out, int cap, int *n) {
   });
 }
 
-constexpr size_t kStatsPerLevel = 5;
+constexpr size_t kStatsPerLevel = 6;
 int adapt_train_stats(adapt_region_t *h, int64_t *out, int cap, int *levels) {
   return guarded([&] {
     checked(h);

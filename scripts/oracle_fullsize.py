@@ -86,7 +86,7 @@ def c4() -> None:
     t0 = time.time()
     sel_sha = [sha(oracle.select(tree, X[r0:r0 + CHUNK], omp=True)) for r0 in range(0, N, CHUNK)]
     t_sel = time.time() - t0
-    np.save(os.path.join(OUT, "c4_tree.npy"), tree)
+    np.savez_compressed(os.path.join(OUT, "c4_tree.npz"), tree=tree)
     meta = dict(config="C4", N=N, F=F, V=V, D=D, seed=cfg.seed, chunk=CHUNK,
                 oracle_sha=source_sha(), tree_sha=sha(tree), n_nodes=len(tree),
                 labels_sha=[sha(y[r0:r0 + CHUNK]) for r0 in range(0, N, CHUNK)],
@@ -113,7 +113,7 @@ def c5t() -> None:
     t0 = time.time()
     tree = oracle.train(X, y, cfg.V, 16, omp=True)
     t_train = time.time() - t0
-    np.save(os.path.join(OUT, "c5_trained_tree.npy"), tree)
+    np.savez_compressed(os.path.join(OUT, "c5_trained_tree.npz"), tree=tree)
     meta = dict(config="C5 training table", N=Nt, F=cfg.F, V=cfg.V, D=16, seed=5,
                 oracle_sha=source_sha(), tree_sha=sha(tree), n_nodes=len(tree),
                 labels_sha=sha(y), oracle_seconds=dict(train=round(t_train, 1), threads=os.cpu_count(), build=OMP_NOTE))
@@ -132,7 +132,7 @@ def complete_tree(cfg) -> np.ndarray:
 
 def c5s() -> None:
     cfg = c5_cfg()
-    trained = np.load(os.path.join(OUT, "c5_trained_tree.npy"))
+    trained = np.load(os.path.join(OUT, "c5_trained_tree.npz"))["tree"]
     complete = complete_tree(cfg)
     M = 1_000_000_000
     ch = 100_000_000

@@ -40,6 +40,8 @@ def _worker(rank, world, port, job, q):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    if job.get("comm"):  # per-level histogram exchange (engine.cpp hist_comm_rs)
+        os.environ["ADAPT_HIST_COMM"] = job["comm"]
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
@@ -224,3 +226,43 @@ def test_p_invariant_train_many_fused():
         for (Xr, Tr), got in zip(regions, o["trees"]):
             ref = oracle.train(Xr, oracle.labels(Tr), Tr.shape[1], 6)
             assert got.tobytes() == ref.tobytes(), f"rank {r}"
+
+
+# ---- reduce-scatter of the level's histograms by node
+# ownership, owner split search, all-gather of the winner records
+# (ADAPT_HIST_COMM=rs): every rank must still get the single-table tree ----
+@pytest.mark.parametrize("world", [2, 3])
+def test_p_invariant_tree_reduce_scatter(world):
+    X, T = synth.generate("C3", 0, 200_003)
+    _check(_run(world, {"X": X, "T": T, "D": 12, "comm": "rs"}), X, T, 12)
+
+
+def test_reduce_scatter_c4_deep_and_empty_shard():
+    X, T = synth.generate("C4", 0, 60_001)
+    _check(_run(3, {"X": X, "T": T, "D": 16, "comm": "rs"}), X, T, 16)
+    X, T = synth.generate("C1", 0, 1)
+    _check(_run(2, {"X": X, "T": T, "D": 4, "comm": "rs"}), X, T, 4)
+
+
+def test_reduce_scatter_forest_kfold_many():
+    X, T = synth.generate("C3", 0, 30_001)
+    res = _run(2, {"X": X, "T": T, "D": 6, "model": "rfc,3,6,seed=4", "comm": "rs"})
+    ref = oracle.train_forest(X, oracle.labels(T), T.shape[1], 6, 3, 4)
+    for r, o in sorted(res.items()):
+        assert "error" not in o
+        for t in range(3):
+            assert o["forest"][t].tobytes() == ref[t].tobytes(), f"rank {r} tree {t}"
+    K, m, S, seed, D = 4, 2, 2, 9, 6
+    res = _run(2, {"X": X, "T": T, "D": D, "kfold": (K, m, S, seed), "comm": "rs"})
+    _, trees = oracle.kfold(X, T, D, K, m, S, seed)
+    for r, o in sorted(res.items()):
+        assert "error" not in o
+        for i, want in enumerate(trees):
+            assert o["kfold_trees"][i].tobytes() == want.tobytes(), (r, i)
+    cfg = synth.CONFIGS["C2"]
+    X, T = synth.generate(cfg, 0, 30_000)
+    regions = [(np.ascontiguousarray(X[r::3]), np.ascontiguousarray(T[r::3])) for r in range(3)]
+    res = _run(2, {"regions": regions, "D": 6, "comm": "rs"})
+    for r, o in sorted(res.items()):
+        for (Xr, Tr), got in zip(regions, o["trees"]):
+            assert got.tobytes() == oracle.train(Xr, oracle.labels(Tr), Tr.shape[1], 6).tobytes()
