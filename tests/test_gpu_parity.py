@@ -260,13 +260,14 @@ def test_degenerate_cases_general_path(how):
     through the general level loop (hist / split / winner kernels and the host
     leaf logic that C4 uses):
       wide_classes  : times padded with unmeasured (+inf) variants to V = 20;
-      many_rows     : every row repeated 13x (n > 512; multiplicity counts, R5);
+      many_rows     : every row repeated to >= 600 rows (multiplicity counts, R5);
       many_features : 7 constant features appended (F > 8; never a candidate)."""
     for name, X, T, D in _degenerate_tables():
         if how == "wide_classes":
             T = np.concatenate([T, np.full((len(T), 20 - T.shape[1]), np.inf, np.float32)], 1)
         elif how == "many_rows":
-            X, T = np.repeat(X, 13, axis=0), np.repeat(T, 13, axis=0)
+            k = -(-600 // len(X))  # > 512 rows
+            X, T = np.repeat(X, k, axis=0), np.repeat(T, k, axis=0)
         else:
             X = np.concatenate([X, np.full((len(X), 7), 4.25, np.float32)], 1)
         n, F = X.shape
