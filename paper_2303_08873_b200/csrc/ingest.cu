@@ -402,6 +402,11 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
     if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     if (tid == 0 && k + kStages < K) issue(k + kStages);
   }
+  // drain: wait for the last phases of the empty barriers, so every arrival
+  // phase of the pipeline is consumed before the CTA exits (synccheck)
+  if (tid == 0 && a.use_tma)
+    for (int64_t k = K > kStages ? K - kStages : 0; k < K; k++)
+      if (first + k * stride < nfull) mbar_wait(&empty[k % kStages], (uint32_t)((k / kStages) & 1));
   if (miss) local_flags |= kFlagUnseen;
   if (local_flags) atomicOr(a.flags, local_flags);
 }

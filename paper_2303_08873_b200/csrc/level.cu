@@ -97,6 +97,12 @@ __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ uint32_t ld_shared_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ int first_seg(const Seg *segs, int nseg, uint32_t p) {
   int lo = 0, hi = nseg - 1;  // last segment with row_base <= p
   while (lo < hi) {
@@ -287,51 +293,98 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
     const bool all4 = Dw[0] && Dw[1] && Dw[2] && Dw[3];
     const uint32_t kwp4 = 4u * kwp;
     for (int i = tid; i < gcount; i += blockDim.x) sh[i] = 0;
+    if (tid == 0) s_cmap[255] = 255;  // label sentinel of the padded quad lanes
     __syncthreads();
+    // one row: its word w (4 features), label, weight -> up to 4 reductions
+    const uint32_t cmap_base = smem_u32(s_cmap);
+    auto count = [&](uint32_t w, int label, uint32_t wv) {
+      const int lk = (int)ld_shared_u8(cmap_base + label) - k0;
+      if ((unsigned)lk >= (unsigned)kn) return;  // another CTA's class slab (or padding)
+      const uint32_t lk4 = 4u * lk;
+      if (all4) {
+        red_shared_add(abase[0] + __byte_perm(w, 0, 0x4440) * kwp4 + lk4, wv);
+        red_shared_add(abase[1] + __byte_perm(w, 0, 0x4441) * kwp4 + lk4, wv);
+        red_shared_add(abase[2] + __byte_perm(w, 0, 0x4442) * kwp4 + lk4, wv);
+        red_shared_add(abase[3] + __byte_perm(w, 0, 0x4443) * kwp4 + lk4, wv);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+          if (abase[e] != 0xFFFFFFFFu)
+            red_shared_add(abase[e] + ((w >> (8 * e)) & 0xFF) * kwp4 + lk4, wv);
+      }
+    };
+    auto load_word = [&](uint32_t row) -> uint32_t {
+      if constexpr (BS >= 4)
+        return *reinterpret_cast<const uint32_t *>(a.bins_in + w0 * a.pstride + (size_t)row * 4);
+      else if constexpr (BS == 2)
+        return *reinterpret_cast<const unsigned short *>(a.bins_in + (size_t)row * 2);
+      else
+        return a.bins_in[row];
+    };
     for (; s < a.nseg && a.segs[s].row_base < pe; s++) {
       const Seg sg = a.segs[s];
       const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
       const uint32_t q1 = min(sg.len, pe - sg.row_base);
-      for (uint32_t qb = q0; qb < q1; qb += UNROLL * blockDim.x) {
-        uint32_t w[UNROLL];
-        int label[UNROLL];
-        uint32_t wv[WEIGHTED ? UNROLL : 1];  // row weight: the bootstrap multiplicity
+      if constexpr (BS >= 4) {
+        // rows [r0, r1): the 4-aligned body as quads (one 16-byte word load and
+        // one 4-byte label load per 4 rows), the unaligned head / tail per row
+        const uint32_t r0 = sg.off + q0, r1 = sg.off + q1;
+        const uint32_t a4 = min((r0 + 3u) & ~3u, r1), b4 = max(a4, r1 & ~3u);
+        if (tid < (int)(a4 - r0)) {
+          const uint32_t row = r0 + tid;
+          count(load_word(row), a.lab_in[row], WEIGHTED ? a.w_in[row] : 1u);
+        }
+        if (tid >= 64 && tid < 64 + (int)(r1 - b4)) {
+          const uint32_t row = b4 + tid - 64;
+          count(load_word(row), a.lab_in[row], WEIGHTED ? a.w_in[row] : 1u);
+        }
+        const uint32_t nq = (b4 - a4) >> 2;
+        const uint4 *wq = reinterpret_cast<const uint4 *>(a.bins_in + w0 * a.pstride + (size_t)a4 * 4);
+        const uint32_t *lq = reinterpret_cast<const uint32_t *>(a.lab_in + a4);
+        const uint32_t *vq = WEIGHTED ? reinterpret_cast<const uint32_t *>(a.w_in + a4) : nullptr;
+        constexpr int QU = UNROLL / 4 > 0 ? UNROLL / 4 : 1;  // quads in flight per thread
+        for (uint32_t qb = 0; qb < nq; qb += QU * blockDim.x) {
+          uint4 w[QU];
+          uint32_t l[QU], v[WEIGHTED ? QU : 1];
 #pragma unroll
-        for (int u = 0; u < (WEIGHTED ? UNROLL : 1); u++) wv[u] = 1;
+          for (int u = 0; u < QU; u++) {  // all loads first
+            const uint32_t qi = qb + u * blockDim.x + tid;
+            l[u] = 0xFFFFFFFFu;
+            w[u] = make_uint4(0, 0, 0, 0);
+            if (qi < nq) {
+              w[u] = __ldcs(wq + qi);
+              l[u] = __ldcs(lq + qi);
+              if constexpr (WEIGHTED) v[u] = __ldcs(vq + qi);
+            }
+          }
 #pragma unroll
-        for (int u = 0; u < UNROLL; u++) {  // all loads first: only this CTA's word
-          const uint32_t q = qb + u * blockDim.x + tid;
-          label[u] = -1;
-          w[u] = 0;
-          if (q < q1) {
-            const uint32_t row = sg.off + q;  // this CTA's word: one coalesced 4-byte load
-            if constexpr (BS >= 4)
-              w[u] = *reinterpret_cast<const uint32_t *>(a.bins_in + w0 * a.pstride + (size_t)row * 4);
-            else if constexpr (BS == 2)
-              w[u] = *reinterpret_cast<const unsigned short *>(a.bins_in + (size_t)row * 2);
-            else
-              w[u] = a.bins_in[row];
-            label[u] = a.lab_in[sg.off + q];
-            if constexpr (WEIGHTED) wv[u] = a.w_in[sg.off + q];
+          for (int u = 0; u < QU; u++) {
+            count(w[u].x, l[u] & 0xFF, WEIGHTED ? (v[u] & 0xFF) : 1u);
+            count(w[u].y, (l[u] >> 8) & 0xFF, WEIGHTED ? ((v[u] >> 8) & 0xFF) : 1u);
+            count(w[u].z, (l[u] >> 16) & 0xFF, WEIGHTED ? ((v[u] >> 16) & 0xFF) : 1u);
+            count(w[u].w, l[u] >> 24, WEIGHTED ? (v[u] >> 24) : 1u);
           }
         }
+      } else {
+        for (uint32_t qb = q0; qb < q1; qb += UNROLL * blockDim.x) {
+          uint32_t w[UNROLL];
+          int label[UNROLL];
+          uint32_t wv[UNROLL];
 #pragma unroll
-        for (int u = 0; u < UNROLL; u++) {
-          if (label[u] < 0) continue;
-          const int lk = (int)s_cmap[label[u]] - k0;
-          if ((unsigned)lk >= (unsigned)kn) continue;  // another CTA's class slab
-          const uint32_t lk4 = 4u * lk;
-          if (all4) {
-            red_shared_add(abase[0] + ((w[u]) & 0xFF) * kwp4 + lk4, wv[WEIGHTED ? u : 0]);
-            red_shared_add(abase[1] + ((w[u] >> 8) & 0xFF) * kwp4 + lk4, wv[WEIGHTED ? u : 0]);
-            red_shared_add(abase[2] + ((w[u] >> 16) & 0xFF) * kwp4 + lk4, wv[WEIGHTED ? u : 0]);
-            red_shared_add(abase[3] + (w[u] >> 24) * kwp4 + lk4, wv[WEIGHTED ? u : 0]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 4; e++)
-              if (abase[e] != 0xFFFFFFFFu)
-                red_shared_add(abase[e] + ((w[u] >> (8 * e)) & 0xFF) * kwp4 + lk4, wv[WEIGHTED ? u : 0]);
+          for (int u = 0; u < UNROLL; u++) {  // all loads first: only this CTA's word
+            const uint32_t q = qb + u * blockDim.x + tid;
+            label[u] = 255;
+            w[u] = 0;
+            wv[u] = 1;
+            if (q < q1) {
+              const uint32_t row = sg.off + q;
+              w[u] = load_word(row);
+              label[u] = a.lab_in[row];
+              if constexpr (WEIGHTED) wv[u] = a.w_in[row];
+            }
           }
+#pragma unroll
+          for (int u = 0; u < UNROLL; u++) count(w[u], label[u], wv[u]);
         }
       }
     }

@@ -261,7 +261,7 @@ def test_degenerate_cases_general_path(how):
     leaf logic that C4 uses):
       wide_classes  : times padded with unmeasured (+inf) variants to V = 20;
       many_rows     : every row repeated to >= 600 rows (multiplicity counts, R5);
-      many_features : 7 constant features appended (F > 8; never a candidate)."""
+      many_features : 8 constant features appended (F > 8; never a candidate)."""
     for name, X, T, D in _degenerate_tables():
         if how == "wide_classes":
             T = np.concatenate([T, np.full((len(T), 20 - T.shape[1]), np.inf, np.float32)], 1)
@@ -269,7 +269,7 @@ def test_degenerate_cases_general_path(how):
             k = -(-600 // len(X))  # > 512 rows
             X, T = np.repeat(X, k, axis=0), np.repeat(T, k, axis=0)
         else:
-            X = np.concatenate([X, np.full((len(X), 7), 4.25, np.float32)], 1)
+            X = np.concatenate([X, np.full((len(X), 8), 4.25, np.float32)], 1)
         n, F = X.shape
         h = _train(X, T, D)
         assert len(ad.adapt_train_stats(h)) >= 1, f"{name}: did not run the level loop"
