@@ -263,7 +263,25 @@ void launch_kfold_eval_many(const float *X, int64_t n, int F, int V, const float
 // 7..14 = (ref_i << 6) | feature_p (feature of node p = i for i < 7), ref_i of
 // leaf edge i = 2(p-3) + right for p = 3..6: >= 0 the next block, < 0 -1 - label.
 constexpr int kSelTopNodes = 8191;
-void launch_select(const DNode *tree, int n_nodes, const uint4 *blocks, const float *X, int64_t m,
-                   int F, int32_t *out, cudaStream_t s);
+// Trees deeper than that top (select_kernel_h): the first `td` levels as a
+// complete heap in shared memory, node h = {float bits of thr_f32, feature},
+// children 2h+1 / 2h+2 (a leaf above level td is a pass-through node whose
+// whole subtree leads to it), so the walk is td fixed steps with no bounds
+// checks; exits[h - (2^td - 1)] after the top: >= 0 a 2-level bottom block,
+// < 0 -1 - label.  A 2-level block is 32 bytes (one 256-bit load): words 0..2
+// the thresholds of its root, left and right child, word 3 their features
+// (bytes 0..2), words 4..7 the refs of its 4 exits (LL, LR, RL, RR; a leaf
+// child passes through to both of its exits).
+constexpr int kHeapMaxLevels = 14;  // 16383 nodes (128 KB) + 16384 exits (64 KB)
+struct SelTree {
+  const DNode *top;      // BFS nodes (the first kSelTopNodes are staged)
+  int n_nodes;
+  const uint4 *blocks;   // 3-level bottom blocks of the BFS layout
+  const uint2 *heap;     // [2^td - 1]
+  const int32_t *exits;  // [2^td]
+  const uint4 *blocks2;  // 2-level blocks, 2 x uint4 each
+  int td;                // heap levels (0: no heap layout)
+};
+void launch_select(const SelTree &t, const float *X, int64_t m, int F, int32_t *out, cudaStream_t s);
 
 }  // namespace adapt

@@ -413,6 +413,8 @@ struct adapt_region {
   std::vector<int32_t> nval;    // [F]
   std::vector<adapt_node_t> tree;
   adapt::DevBuf d_tree, d_blocks;  // device tree: DNode top + bottom blocks (select.cu)
+  adapt::DevBuf d_heap, d_exits, d_blocks2;  // deep trees: heap top + 2-level blocks (common.h)
+  int heap_td = 0;
   // lossy quantile bins (quantile.cu, R23): features in qmask were quantised;
   // qprev[f][b] = the largest distinct value of bin b-1 (threshold midpoints)
   bool quantile = false;
@@ -622,6 +624,82 @@ void upload_tree(adapt_region *h, cudaStream_t s) {
   h->d_blocks.ensure(std::max<size_t>(blk.size() * 4, 64));
   if (!blk.empty())
     CUDA_CHECK(cudaMemcpyAsync(h->d_blocks.p, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice, s));
+  // trees deeper than the BFS top: the heap-top layout of select_kernel_h
+  h->heap_td = 0;
+  if ((int)tr.size() > kSelTopNodes) {
+    int maxd = 0;
+    for (const auto &nd : tr) maxd = std::max(maxd, nd.depth);
+    const int td = std::min(kHeapMaxLevels, maxd);
+    const int nh = (1 << td) - 1;
+    std::vector<uint2> heap((size_t)std::max(nh, 1), make_uint2(0u, 0u));
+    std::vector<int32_t> exits((size_t)1 << td, 0);
+    std::vector<uint32_t> b2;  // 8 words per block
+    std::deque<std::pair<int64_t, int>> q2;  // (block, tree node at its root)
+    auto ref_of = [&](int t) -> int32_t {   // exit to tree node t: its label, or a new block
+      if (tr[t].feature < 0) return -1 - tr[t].label;
+      const int64_t b = (int64_t)(b2.size() / 8);
+      if (b >= (1ll << 30)) throw Error(ADAPT_E_INVALID_ARG, "tree too large for the select layout");
+      b2.resize(b2.size() + 8, 0u);
+      q2.emplace_back(b, t);
+      return (int32_t)b;
+    };
+    // heap fill: (heap position, tree node, level); leaves above td pass through
+    std::vector<std::array<int, 3>> st{{0, 0, 0}};
+    while (!st.empty()) {
+      const auto [hp, t, lv] = st.back();
+      st.pop_back();
+      if (lv == td) {
+        exits[(size_t)(hp - nh)] = ref_of(t);
+        continue;
+      }
+      const adapt_node_t &nd = tr[t];
+      if (nd.feature >= 0) {
+        const float th = round_down_f32(nd.threshold);
+        uint32_t bits;
+        memcpy(&bits, &th, 4);
+        heap[hp] = make_uint2(bits, (uint32_t)nd.feature);
+      }
+      st.push_back({2 * hp + 2, nd.feature >= 0 ? nd.right : t, lv + 1});
+      st.push_back({2 * hp + 1, nd.feature >= 0 ? nd.left : t, lv + 1});
+    }
+    while (!q2.empty()) {  // 2-level blocks, breadth first
+      const auto [b, root] = q2.front();
+      q2.pop_front();
+      uint32_t w[8] = {};
+      const adapt_node_t &r = tr[root];
+      const int kids[2] = {r.left, r.right};
+      auto thr_bits = [&](const adapt_node_t &nd) {
+        const float th = round_down_f32(nd.threshold);
+        uint32_t bits;
+        memcpy(&bits, &th, 4);
+        return bits;
+      };
+      w[0] = thr_bits(r);
+      w[3] = (uint32_t)r.feature;
+      for (int c = 0; c < 2; c++) {
+        const adapt_node_t &ch = tr[kids[c]];
+        if (ch.feature >= 0) {
+          w[1 + c] = thr_bits(ch);
+          w[3] |= (uint32_t)ch.feature << (8 * (c + 1));
+          const int32_t l = ref_of(ch.left), rr = ref_of(ch.right);
+          w[4 + 2 * c] = (uint32_t)l;
+          w[5 + 2 * c] = (uint32_t)rr;
+        } else {  // pass-through: both exits of this child are its leaf
+          const int32_t lf = -1 - ch.label;
+          w[4 + 2 * c] = w[5 + 2 * c] = (uint32_t)lf;
+        }
+      }
+      memcpy(&b2[(size_t)b * 8], w, sizeof(w));
+    }
+    h->d_heap.ensure(heap.size() * sizeof(uint2));
+    h->d_exits.ensure(exits.size() * 4);
+    h->d_blocks2.ensure(std::max<size_t>(b2.size() * 4, 64));
+    CUDA_CHECK(cudaMemcpyAsync(h->d_heap.p, heap.data(), heap.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(h->d_exits.p, exits.data(), exits.size() * 4, cudaMemcpyHostToDevice, s));
+    if (!b2.empty())
+      CUDA_CHECK(cudaMemcpyAsync(h->d_blocks2.p, b2.data(), b2.size() * 4, cudaMemcpyHostToDevice, s));
+    h->heap_td = td;
+  }
   CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
@@ -1979,12 +2057,15 @@ int select_host_walk(adapt_region *h, const float *x) {
 }
 
 void select_device(adapt_region *h, const float *X, int64_t m, int32_t *out, cudaStream_t s) {
-  if (h->forest.empty())
-    launch_select(h->d_tree.as<DNode>(), (int)h->tree.size(), h->d_blocks.as<uint4>(), X, m, h->F,
-                  out, s);
-  else
+  if (h->forest.empty()) {
+    SelTree t{h->d_tree.as<DNode>(), (int)h->tree.size(), h->d_blocks.as<uint4>(),
+              h->heap_td ? h->d_heap.as<uint2>() : nullptr, h->heap_td ? h->d_exits.as<int32_t>() : nullptr,
+              h->heap_td ? h->d_blocks2.as<uint4>() : nullptr, h->heap_td};
+    launch_select(t, X, m, h->F, out, s);
+  } else {
     launch_select_forest(h->d_forest.as<DNode>(), h->forest_nodes, h->d_roots.as<int32_t>(),
                          (int)h->forest.size(), X, m, h->F, out, s);
+  }
   // the device tree may be replaced (retrain, set_tree, K-fold restore) on
   // another stream: upload_tree waits for this event before overwriting it
   if (!h->sel_evt) CUDA_CHECK(cudaEventCreateWithFlags(&h->sel_evt, cudaEventDisableTiming));

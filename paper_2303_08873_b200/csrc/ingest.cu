@@ -290,11 +290,14 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
   const int64_t first = blockIdx.x, stride = gridDim.x;
   const int64_t K = first < ntiles ? (ntiles - 1 - first) / stride + 1 : 0;
   const uint32_t bytesT = (uint32_t)TR * V * 4, bytesF = (uint32_t)TR * F * 4;
+  // every tile's empty-barrier phase is waited exactly once by thread 0: tile
+  // k - kStages's here (before stage s is refilled), the last kStages after the
+  // loop, TMA-loaded or not (synccheck: no arrival phase left unconsumed)
   auto issue = [&](int64_t k) {  // thread 0 only
     const int64_t t = first + k * stride;
-    if (!a.use_tma || t >= nfull) return;
     const int s = (int)(k % kStages);
     if (k >= kStages) mbar_wait(&empty[s], (uint32_t)(((k / kStages) - 1) & 1));
+    if (!a.use_tma || t >= nfull) return;
     mbar_arrive_expect_tx(&full[s], bytesT + bytesF);
     tma_load_1d(stT + (size_t)s * TR * V, a.times + t * TR * V, bytesT, &full[s]);
     tma_load_1d(stF + (size_t)s * TR * F, a.feat + t * TR * F, bytesF, &full[s]);
@@ -402,11 +405,10 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
     if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     if (tid == 0 && k + kStages < K) issue(k + kStages);
   }
-  // drain: wait for the last phases of the empty barriers, so every arrival
-  // phase of the pipeline is consumed before the CTA exits (synccheck)
-  if (tid == 0 && a.use_tma)
+  // drain: the last kStages tiles' empty phases (see issue)
+  if (tid == 0)
     for (int64_t k = K > kStages ? K - kStages : 0; k < K; k++)
-      if (first + k * stride < nfull) mbar_wait(&empty[k % kStages], (uint32_t)((k / kStages) & 1));
+      mbar_wait(&empty[k % kStages], (uint32_t)((k / kStages) & 1));
   if (miss) local_flags |= kFlagUnseen;
   if (local_flags) atomicOr(a.flags, local_flags);
 }

@@ -2,18 +2,20 @@
 // feature vectors at once): walk root -> leaf with x[f] <= thr -> left
 // (S:224), NaN -> right (R8), output the leaf's variant.
 //
-// The device tree is a BFS array of 8-byte nodes; the threshold is stored as
-// the largest float32 <= the double threshold, which makes the float compare
-// exact (V:A5).  The product kernel is select_kernel_d (each lane loads its
-// vector straight into registers; below); the tile kernels are kept for A/B
-// (ADAPT_SEL_TILE / ADAPT_SEL_SMEMX).  The first kTopNodes nodes (the top levels every walk visits;
-// a whole depth-12 tree) sit in shared memory; below them the tree is stored
-// as 64-byte blocks of 3 levels (common.h), read with four independent
-// 16-byte loads, so a depth-16 walk pays one L2 round trip below the top
-// instead of four dependent ones.  Every warp owns its tiles of 64 vectors (no block barriers): the
-// coalesced 16-byte loads of the next tile sit in registers while the lanes
-// walk the current one out of the warp's odd-stride shared-memory tile, two
-// independent walks per lane interleaved to hide the dependent smem latency.
+// Thresholds are stored as the largest float32 <= the double threshold, which
+// makes the float compare exact (V:A5).  Two product kernels, both one
+// 1024-thread CTA per SM, each lane walking its own vector loaded straight
+// from HBM (the next one's loads in flight during the walk):
+//   select_kernel_c  trees within the shared-memory top (kSelTopNodes BFS
+//                    nodes, e.g. C4's depth 12): the vector parked in the
+//                    thread's own shared-memory column, so every feature read
+//                    of the walk is one conflict-free wavefront;
+//   select_kernel_h  deeper trees (C5's depth 16): the first td <= 14 levels
+//                    as a complete heap in shared memory (fixed-trip walk, no
+//                    bounds checks or child pointers), the vector in
+//                    registers, then 2-level 32-byte bottom blocks (one
+//                    256-bit load per 2 levels) — common.h SelTree.
+// select_kernel_any serves F not a multiple of 4 or unaligned X.
 #include <algorithm>
 #include <cstdlib>
 
@@ -24,10 +26,6 @@ namespace adapt {
 namespace {
 
 constexpr int kSelThreads = 1024;  // one CTA per SM: one smem copy of the tree
-#ifndef ADAPT_SEL_CHAINS
-#define ADAPT_SEL_CHAINS 2
-#endif
-constexpr int kSelChains = ADAPT_SEL_CHAINS;  // vectors walked at once per lane
 constexpr int kAnyThreads = 256;   // generic-F kernel
 constexpr int kTopNodes = kSelTopNodes;  // 64 KB
 
@@ -62,97 +60,6 @@ __device__ __forceinline__ void load_block(const uint4 *__restrict__ blocks, int
                  : "l"(p + i));
 }
 
-template <int F>
-__global__ void __launch_bounds__(kSelThreads, 1)
-    select_kernel(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
-                  const float *__restrict__ X,
-                  int64_t m, int32_t *__restrict__ out) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int kStride = F | 1;                   // odd row stride of a warp's tile
-  constexpr int kVec = F / 4;                      // float4 per vector
-  constexpr int kRows = 32 * kSelChains;           // vectors per warp tile
-  constexpr int kLd = kRows * kVec / 32;           // float4 loads per lane per tile
-  DNode *st = reinterpret_cast<DNode *>(smem);     // [n_top]
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  float *sx = reinterpret_cast<float *>(smem + (size_t)kTopNodes * sizeof(DNode)) +
-              (size_t)warp * kRows * kStride;      // this warp's [kRows][kStride]
-  for (int i = t; i < n_top; i += kSelThreads) st[i] = gtree[i];
-  __syncthreads();  // the only block barrier: tree copy visible
-
-  // warps own tiles of kRows vectors; no block barriers in the loop
-  const int64_t ntiles = (m + kRows - 1) / kRows;
-  const int64_t nwarps = (int64_t)gridDim.x * (kSelThreads / 32);
-  float4 pre[kLd];
-  auto fetch = [&](int64_t tile) {
-    const int64_t v0 = tile * kRows;
-    const int rows = (m - v0 < kRows) ? (int)(m - v0) : kRows;
-    const float4 *src = reinterpret_cast<const float4 *>(X + v0 * F);
-#pragma unroll
-    for (int k = 0; k < kLd; k++) {
-      const int i = lane + 32 * k;  // float4 index within the tile: coalesced
-      pre[k] = i < rows * kVec ? __ldcs(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  int64_t tile = blockIdx.x * (int64_t)(kSelThreads / 32) + warp;
-  if (tile < ntiles) fetch(tile);
-  for (; tile < ntiles; tile += nwarps) {
-    __syncwarp();  // previous tile's walks done before it is overwritten
-#pragma unroll
-    for (int k = 0; k < kLd; k++) {
-      const int i = lane + 32 * k, r = i / kVec, c = (i % kVec) * 4;
-      float *d = sx + r * kStride + c;
-      d[0] = pre[k].x;
-      d[1] = pre[k].y;
-      d[2] = pre[k].z;
-      d[3] = pre[k].w;
-    }
-    __syncwarp();
-    if (tile + nwarps < ntiles) fetch(tile + nwarps);  // next tile in flight during the walks
-    const int64_t v0 = tile * kRows;
-    // kSelChains independent walks per lane, interleaved for latency hiding
-    const float *x[kSelChains];
-    DNode nd[kSelChains];
-    int ref[kSelChains];  // -1 - label, or the bottom block the walk continues in
-    bool live[kSelChains];
-#pragma unroll
-    for (int c = 0; c < kSelChains; c++) {
-      x[c] = sx + (lane + 32 * c) * kStride;
-      nd[c] = st[0];
-      ref[c] = nd[c].meta;
-      live[c] = v0 + lane + 32 * c < m;
-    }
-    bool any = true;
-    while (any) {  // the shared-memory top
-      any = false;
-#pragma unroll
-      for (int c = 0; c < kSelChains; c++) {
-        if (nd[c].meta >= 0) {
-          const float xv = x[c][nd[c].meta & 63];
-          const int k = (nd[c].meta >> 6) + (xv <= nd[c].thr ? 0 : 1);
-          if (k < n_top) {
-            nd[c] = st[k];
-            ref[c] = nd[c].meta;
-            any |= nd[c].meta >= 0;
-          } else {
-            ref[c] = k - n_top;
-            nd[c].meta = -1;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < kSelChains; c++)  // bottom blocks (the prefetched tile holds
-      while (ref[c] >= 0) {               // registers: one chain's block at a time)
-        uint4 w[4];
-        load_block(blocks, ref[c], w);
-        ref[c] = walk_block(w, x[c]);
-      }
-#pragma unroll
-    for (int c = 0; c < kSelChains; c++)
-      if (live[c]) __stcs(out + v0 + lane + 32 * c, -1 - ref[c]);
-  }
-}
-
 template <int N>
 __device__ __forceinline__ int walk_block_r(const uint4 (&w)[4], const float (&x)[N]) {
   const float t0 = __uint_as_float(w[0].x);
@@ -170,84 +77,8 @@ __device__ __forceinline__ int walk_block_r(const uint4 (&w)[4], const float (&x
   return (int32_t)r >> 6;
 }
 
-// One vector per lane, its features in REGISTERS: the walk reads only tree
-// nodes from shared memory (the random-feature reads of the vector tile were
-// half of the LSU wavefronts that bound the smem-x kernel above); the vector
-// reaches registers through the same coalesced tile, one uniform-feature (so
-// conflict-free) read per feature.
-template <int F>
-__global__ void __launch_bounds__(kSelThreads, 1)
-    select_kernel_r(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
-                    const float *__restrict__ X, int64_t m, int32_t *__restrict__ out) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int kStride = F | 1;
-  constexpr int kVec = F / 4;
-  constexpr int kRows = 32;                // one vector per lane
-  constexpr int kLd = kRows * kVec / 32;   // float4 loads per lane per tile
-  constexpr int NP = F <= 4 ? 4 : (F <= 8 ? 8 : 16);
-  DNode *st = reinterpret_cast<DNode *>(smem);
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  float *sx = reinterpret_cast<float *>(smem + (size_t)kTopNodes * sizeof(DNode)) + (size_t)warp * kRows * kStride;
-  for (int i = t; i < n_top; i += kSelThreads) st[i] = gtree[i];
-  __syncthreads();
-  const int64_t ntiles = (m + kRows - 1) / kRows;
-  const int64_t nwarps = (int64_t)gridDim.x * (kSelThreads / 32);
-  float4 pre[kLd];
-  auto fetch = [&](int64_t tile) {
-    const int64_t v0 = tile * kRows;
-    const int rows = (m - v0 < kRows) ? (int)(m - v0) : kRows;
-    const float4 *src = reinterpret_cast<const float4 *>(X + v0 * F);
-#pragma unroll
-    for (int k = 0; k < kLd; k++) {
-      const int i = lane + 32 * k;
-      pre[k] = i < rows * kVec ? __ldcs(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  int64_t tile = blockIdx.x * (int64_t)(kSelThreads / 32) + warp;
-  if (tile < ntiles) fetch(tile);
-  for (; tile < ntiles; tile += nwarps) {
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < kLd; k++) {
-      const int i = lane + 32 * k, r = i / kVec, c = (i % kVec) * 4;
-      float *d = sx + r * kStride + c;
-      d[0] = pre[k].x;
-      d[1] = pre[k].y;
-      d[2] = pre[k].z;
-      d[3] = pre[k].w;
-    }
-    __syncwarp();
-    float xr[NP];
-#pragma unroll
-    for (int f = 0; f < NP; f++) xr[f] = f < F ? sx[lane * kStride + f] : 0.f;
-    if (tile + nwarps < ntiles) fetch(tile + nwarps);  // next tile in flight during the walk
-    const int64_t v = tile * kRows + lane;
-    DNode nd = st[0];
-    int ref = nd.meta;
-    while (nd.meta >= 0) {  // the shared-memory top
-      const float xv = pick<NP>(xr, nd.meta & 63);
-      const int k = (nd.meta >> 6) + (xv <= nd.thr ? 0 : 1);  // NaN -> right (R8)
-      if (k < n_top) {
-        nd = st[k];
-        ref = nd.meta;
-      } else {
-        ref = k - n_top;
-        break;
-      }
-    }
-    while (ref >= 0) {  // bottom blocks
-      uint4 w[4];
-      load_block(blocks, ref, w);
-      ref = walk_block_r<NP>(w, xr);
-    }
-    if (v < m) __stcs(out + v, -1 - ref);
-  }
-}
-
-// As select_kernel_r, but every lane loads its own vector straight into
-// registers (256-bit loads when the rows are 32-byte aligned): no staging tile,
-// no shared-memory stores or feature reads at all; the next vector's loads are
-// in flight during the walk.
+// (A/B, ADAPT_SEL_D=1: the previous deep-tree kernel — BFS top with child
+// pointers and 3-level 64-byte bottom blocks — kept for one measurement.)
 template <int F>
 __global__ void __launch_bounds__(kSelThreads, 1)
     select_kernel_d(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
@@ -350,6 +181,59 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   }
 }
 
+// one 2-level bottom block (32 B): returns the exit ref (>= 0 next block, < 0
+// -1 - label)
+template <int N>
+__device__ __forceinline__ int walk_block2(const uint4 &a, const uint4 &b, const float (&x)[N]) {
+  const bool g0 = !(pick<N>(x, a.w & 0xFF) <= __uint_as_float(a.x));  // NaN -> right (R8)
+  const float t1 = __uint_as_float(g0 ? a.z : a.y);
+  const bool g1 = !(pick<N>(x, (a.w >> (g0 ? 16 : 8)) & 0xFF) <= t1);
+  const uint32_t r = g0 ? (g1 ? b.w : b.z) : (g1 ? b.y : b.x);
+  return (int32_t)r;
+}
+
+template <int F>
+__global__ void __launch_bounds__(kSelThreads, 1)
+    select_kernel_h(const uint2 *__restrict__ gheap, const int32_t *__restrict__ gexits, int td,
+                    const uint4 *__restrict__ blocks2, const float *__restrict__ X, int64_t m, int wide,
+                    int32_t *__restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int NP = F <= 4 ? 4 : (F <= 8 ? 8 : 16);
+  const int nh = (1 << td) - 1;
+  uint2 *hs = reinterpret_cast<uint2 *>(smem);
+  int32_t *ex = reinterpret_cast<int32_t *>(smem + (size_t)nh * sizeof(uint2));
+  const int t = threadIdx.x;
+  for (int i = t; i < nh; i += kSelThreads) hs[i] = gheap[i];
+  for (int i = t; i <= nh; i += kSelThreads) ex[i] = gexits[i];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * kSelThreads;
+  int64_t v = blockIdx.x * (int64_t)kSelThreads + t;
+  float nx[F];
+  if (v < m) load_vec<F>(X + v * F, wide, nx);
+  for (; v < m; v += stride) {
+    float xr[NP];
+#pragma unroll
+    for (int f = 0; f < NP; f++) xr[f] = f < F ? nx[f] : 0.f;
+    if (v + stride < m) load_vec<F>(X + (v + stride) * F, wide, nx);  // next vector in flight
+    uint32_t k = 0;
+#pragma unroll 2
+    for (int l = 0; l < td; l++) {  // fixed trip count: leaves above td pass through
+      const uint2 nd = hs[k];
+      k = 2 * k + (pick<NP>(xr, nd.y) <= __uint_as_float(nd.x) ? 1u : 2u);
+    }
+    int ref = ex[k - nh];
+    while (ref >= 0) {
+      const uint4 *p = blocks2 + 2 * (int64_t)ref;
+      uint4 a, b;
+      asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+          : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+          : "l"(p));
+      ref = walk_block2<NP>(a, b, xr);
+    }
+    __stcs(out + v, -1 - ref);
+  }
+}
+
 // generic F (not a multiple of 4, or an unaligned X): scalar staging
 __global__ void __launch_bounds__(kAnyThreads, 1)
     select_kernel_any(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
@@ -395,54 +279,37 @@ __global__ void __launch_bounds__(kAnyThreads, 1)
 
 }  // namespace
 
-void launch_select(const DNode *tree, int n_nodes, const uint4 *blocks, const float *X, int64_t m,
-                   int F, int32_t *out, cudaStream_t s) {
+void launch_select(const SelTree &tr, const float *X, int64_t m, int F, int32_t *out, cudaStream_t s) {
   if (m == 0) return;
+  const DNode *tree = tr.top;
+  const uint4 *blocks = tr.blocks;
+  const int n_nodes = tr.n_nodes;
   const int n_top = std::min(n_nodes, kTopNodes);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool vec = (reinterpret_cast<uintptr_t>(X) & 15) == 0;
-  static const bool smem_x = getenv("ADAPT_SEL_SMEMX") != nullptr;  // the smem-x kernel (A/B)
-  // default: per-lane vector loads (select_kernel_d); A/B: the tile kernels
-  static const bool direct = getenv("ADAPT_SEL_TILE") == nullptr && !smem_x;
-  // trees that fit the shared-memory top: the vector in a shared-memory column
-  // (C4 select 1.40 -> 1.15 ms); deeper trees: the register kernel, whose
-  // bottom-block walks measured faster with the vector in registers (C5)
-  static const int xcol_env = getenv("ADAPT_SEL_XCOL") ? atoi(getenv("ADAPT_SEL_XCOL")) : -1;
-  const bool xcol = direct && (xcol_env >= 0 ? xcol_env != 0 : n_nodes <= kTopNodes);
+  static const bool old_deep = getenv("ADAPT_SEL_D") != nullptr;  // A/B: the previous deep kernel
   const size_t tree_b = (size_t)kTopNodes * sizeof(DNode);
-  // F <= 16, 16-byte aligned X: per-warp tiles, one 1024-thread CTA per SM
-  const int64_t wtiles = (m + 32 * kSelChains - 1) / (32 * kSelChains);
-  const int vgrid = (int)std::min<int64_t>((wtiles + kSelThreads / 32 - 1) / (kSelThreads / 32), sms);
+  const int wide = (reinterpret_cast<uintptr_t>(X) & 31) == 0;
+  const int g = (int)std::min<int64_t>((m + kSelThreads - 1) / kSelThreads, sms);
   switch (vec ? F : 0) {
-#define CASE(FF)                                                                               \
-  case FF: {                                                                                   \
-    if (xcol) {                                                                                \
-      const int wide = (reinterpret_cast<uintptr_t>(X) & 31) == 0;                             \
-      const int64_t blocks_needed = (m + kSelThreads - 1) / kSelThreads;                       \
-      const int g = (int)std::min<int64_t>(blocks_needed, sms);                                \
-      const size_t smem = tree_b + (size_t)kSelThreads * FF * 4;                               \
-      smem_limit(select_kernel_c<FF>, smem);                                                   \
-      select_kernel_c<FF><<<g, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, wide, out);  \
-    } else if (direct) {                                                                       \
-      const int wide = (reinterpret_cast<uintptr_t>(X) & 31) == 0;                             \
-      const int64_t blocks_needed = (m + kSelThreads - 1) / kSelThreads;                       \
-      const int g = (int)std::min<int64_t>(blocks_needed, sms);                                \
-      smem_limit(select_kernel_d<FF>, tree_b);                                                 \
+#define CASE(FF)                                                                                \
+  case FF: {                                                                                    \
+    if (n_nodes <= kTopNodes) {                                                                 \
+      const size_t smem = tree_b + (size_t)kSelThreads * FF * 4;                                \
+      smem_limit(select_kernel_c<FF>, smem);                                                    \
+      select_kernel_c<FF><<<g, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, wide, out);   \
+    } else if (tr.td > 0 && !old_deep) {                                                        \
+      const size_t smem = ((size_t)1 << tr.td) * (sizeof(uint2) + 4);                           \
+      smem_limit(select_kernel_h<FF>, smem);                                                    \
+      select_kernel_h<FF><<<g, kSelThreads, smem, s>>>(tr.heap, tr.exits, tr.td, tr.blocks2, X, m, \
+                                                       wide, out);                              \
+    } else {                                                                                    \
+      smem_limit(select_kernel_d<FF>, tree_b);                                                  \
       select_kernel_d<FF><<<g, kSelThreads, tree_b, s>>>(tree, n_top, blocks, X, m, wide, out); \
-    } else if (smem_x) {                                                                       \
-      const size_t smem = tree_b + (size_t)kSelThreads * kSelChains * (FF | 1) * 4;            \
-      smem_limit(select_kernel<FF>, smem);                                                     \
-      select_kernel<FF><<<vgrid, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, out);      \
-    } else {                                                                                   \
-      const size_t smem = tree_b + (size_t)kSelThreads * (FF | 1) * 4;                         \
-      const int64_t tiles = (m + 31) / 32;                                                     \
-      const int g = (int)std::min<int64_t>((tiles + kSelThreads / 32 - 1) / (kSelThreads / 32), sms); \
-      smem_limit(select_kernel_r<FF>, smem);                                                   \
-      select_kernel_r<FF><<<g, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, out);        \
-    }                                                                                          \
-    break;                                                                                     \
+    }                                                                                           \
+    break;                                                                                      \
   }
     CASE(4) CASE(8) CASE(12) CASE(16)
 #undef CASE
