@@ -17,7 +17,6 @@
 //                    256-bit load per 2 levels) — common.h SelTree.
 // select_kernel_any serves F not a multiple of 4 or unaligned X.
 #include <algorithm>
-#include <cstdlib>
 
 #include "common.h"
 #include "vecreg.cuh"
@@ -60,70 +59,12 @@ __device__ __forceinline__ void load_block(const uint4 *__restrict__ blocks, int
                  : "l"(p + i));
 }
 
-template <int N>
-__device__ __forceinline__ int walk_block_r(const uint4 (&w)[4], const float (&x)[N]) {
-  const float t0 = __uint_as_float(w[0].x);
-  const bool g0 = !(pick<N>(x, w[1].w & 63) <= t0);  // NaN -> right (R8)
-  const float t1 = __uint_as_float(g0 ? w[0].z : w[0].y);
-  const bool g1 = !(pick<N>(x, (g0 ? w[2].y : w[2].x) & 63) <= t1);
-  const uint32_t tw = g0 ? (g1 ? w[1].z : w[1].y) : (g1 ? w[1].x : w[0].w);
-  const uint32_t fw = g0 ? (g1 ? w[3].y : w[3].x) : (g1 ? w[2].w : w[2].z);
-  const bool g2 = !(pick<N>(x, fw & 63) <= __uint_as_float(tw));
-  uint32_t r;
-  if (g0)
-    r = g1 ? (g2 ? w[3].z : w[3].y) : (g2 ? w[3].x : w[2].w);
-  else
-    r = g1 ? (g2 ? w[2].z : w[2].y) : (g2 ? w[2].x : w[1].w);
-  return (int32_t)r >> 6;
-}
 
-// (A/B, ADAPT_SEL_D=1: the previous deep-tree kernel — BFS top with child
-// pointers and 3-level 64-byte bottom blocks — kept for one measurement.)
-template <int F>
-__global__ void __launch_bounds__(kSelThreads, 1)
-    select_kernel_d(const DNode *__restrict__ gtree, int n_top, const uint4 *__restrict__ blocks,
-                    const float *__restrict__ X, int64_t m, int wide, int32_t *__restrict__ out) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int NP = F <= 4 ? 4 : (F <= 8 ? 8 : 16);
-  DNode *st = reinterpret_cast<DNode *>(smem);
-  const int t = threadIdx.x;
-  for (int i = t; i < n_top; i += kSelThreads) st[i] = gtree[i];
-  __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * kSelThreads;
-  int64_t v = blockIdx.x * (int64_t)kSelThreads + t;
-  float nx[F];
-  if (v < m) load_vec<F>(X + v * F, wide, nx);
-  for (; v < m; v += stride) {
-    float xr[NP];
-#pragma unroll
-    for (int f = 0; f < NP; f++) xr[f] = f < F ? nx[f] : 0.f;
-    if (v + stride < m) load_vec<F>(X + (v + stride) * F, wide, nx);  // next vector in flight
-    DNode nd = st[0];
-    int ref = nd.meta;
-    while (nd.meta >= 0) {
-      const float xv = pick<NP>(xr, nd.meta & 63);
-      const int k = (nd.meta >> 6) + (xv <= nd.thr ? 0 : 1);  // NaN -> right (R8)
-      if (k < n_top) {
-        nd = st[k];
-        ref = nd.meta;
-      } else {
-        ref = k - n_top;
-        break;
-      }
-    }
-    while (ref >= 0) {
-      uint4 w[4];
-      load_block(blocks, ref, w);
-      ref = walk_block_r<NP>(w, xr);
-    }
-    __stcs(out + v, -1 - ref);
-  }
-}
-
-// As select_kernel_d, but the vector parked in the thread's own shared-memory
-// COLUMN (xs[f][tid]: any f of any lane is a distinct bank, so the walk's
-// random-feature reads are conflict-free single wavefronts) instead of the
-// register select tree (A/B: ADAPT_SEL_XCOL=1).
+// Trees within the shared-memory top: every lane loads its own vector straight
+// from HBM (256-bit loads when rows are 32-byte aligned; the next vector in
+// flight during the walk) and parks it in its own shared-memory COLUMN
+// (xs[f][tid]: any f of any lane is a distinct bank, so the walk's
+// random-feature reads are conflict-free single wavefronts).
 __device__ __forceinline__ int walk_block_col(const uint4 (&w)[4], const float *x) {
   constexpr int S = kSelThreads;
   const float t0 = __uint_as_float(w[0].x);
@@ -289,7 +230,6 @@ void launch_select(const SelTree &tr, const float *X, int64_t m, int F, int32_t 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool vec = (reinterpret_cast<uintptr_t>(X) & 15) == 0;
-  static const bool old_deep = getenv("ADAPT_SEL_D") != nullptr;  // A/B: the previous deep kernel
   const size_t tree_b = (size_t)kTopNodes * sizeof(DNode);
   const int wide = (reinterpret_cast<uintptr_t>(X) & 31) == 0;
   const int g = (int)std::min<int64_t>((m + kSelThreads - 1) / kSelThreads, sms);
@@ -300,14 +240,11 @@ void launch_select(const SelTree &tr, const float *X, int64_t m, int F, int32_t 
       const size_t smem = tree_b + (size_t)kSelThreads * FF * 4;                                \
       smem_limit(select_kernel_c<FF>, smem);                                                    \
       select_kernel_c<FF><<<g, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, wide, out);   \
-    } else if (tr.td > 0 && !old_deep) {                                                        \
+    } else {                                                                                    \
       const size_t smem = ((size_t)1 << tr.td) * (sizeof(uint2) + 4);                           \
       smem_limit(select_kernel_h<FF>, smem);                                                    \
       select_kernel_h<FF><<<g, kSelThreads, smem, s>>>(tr.heap, tr.exits, tr.td, tr.blocks2, X, m, \
                                                        wide, out);                              \
-    } else {                                                                                    \
-      smem_limit(select_kernel_d<FF>, tree_b);                                                  \
-      select_kernel_d<FF><<<g, kSelThreads, tree_b, s>>>(tree, n_top, blocks, X, m, wide, out); \
     }                                                                                           \
     break;                                                                                      \
   }

@@ -151,7 +151,7 @@ def test_hot_kernels_do_not_spill():
             fn = line.split("Function")[-1].strip().rstrip(":")
         elif "STACK:" in line and fn and any(k in fn for k in (
                 "hist_kernelILi16", "hist_kernelILi8", "partition_kernelILi16", "partition_kernelILi8",
-                "select_kernelILi16", "select_kernel_dILi16", "select_kernel_cILi16", "select_kernel_rILi16",
+                "select_kernel_hILi16", "select_kernel_cILi16",
                 "select_forest_dILi16", "label_bin",
                 "split_small", "split_kernel", "hist_flat", "small_train", "kfold_eval_many")):
             # (discover_kernel's frame is its noinline slow-path call, by design)
