@@ -33,7 +33,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src: str) -> str:
         obj = os.path.join(CSRC, os.path.basename(src) + ".o")
-        cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        # host code: x86-64-v2 (SSE4.2 + POPCNT): the level loop's class-set
+        # bookkeeping is popcount-heavy; without it every popcount is a libgcc call
+        cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-march=x86-64-v2",
                "-Xptxas", "-v" if verbose else "-O3", f"-DADAPT_GIT=\"{git}\"",
                *os.environ.get("ADAPT_NVCC_DEFS", "").split(),  # tuning sweeps only
                "-I", os.path.join(ROOT, "include"), "-x", "cu", "-c", src, "-o", obj]

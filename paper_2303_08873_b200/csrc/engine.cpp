@@ -232,12 +232,18 @@ Ctx g_ctx;
 // NCCL path is exercised on one GPU; collectives are then real NCCL calls)
 bool collectives_on() { return g_ctx.world > 1 || g_ctx.comm != nullptr; }
 
-// per-level histogram exchange: ADAPT_HIST_COMM=rs selects the reduce-scatter
-// by node ownership (+ owner split search, winner all-gather); default: the
-// all-reduce of the direct nodes' histograms
+// per-level histogram exchange: with more than one rank, the
+// reduce-scatter by node ownership + owner split search + winner all-gather
+// (the split search, node-bound at deep levels, divides by the rank count);
+// ADAPT_HIST_COMM=allreduce selects the all-reduce of the direct nodes'
+// histograms (every rank searches every split), ADAPT_HIST_COMM=rs forces the
+// reduce-scatter also on a 1-rank NCCL communicator
 bool hist_comm_rs() {
+  if (!collectives_on()) return false;
   const char *m = getenv("ADAPT_HIST_COMM");
-  return collectives_on() && m && !strcmp(m, "rs");
+  if (m && !strcmp(m, "allreduce")) return false;
+  if (m && !strcmp(m, "rs")) return true;
+  return g_ctx.world > 1;
 }
 
 void host_hook(int rc, const char *what) {
@@ -1314,9 +1320,16 @@ void train_region(adapt_region *h, cudaStream_t s) {
     return st;
   };
   PartState pending;
+  static const bool trace2 = trace && atoi(getenv("ADAPT_TRACE_HOST")) >= 2;
+  std::vector<std::pair<const char *, double>> ticks;  // (what, us) per level
+  auto tick = [&](const char *what) {
+    if (trace2) ticks.emplace_back(what, now_us());
+  };
   for (int level = 0; !frontier.empty(); level++) {
     const int A = (int)frontier.size();
     if (trace) tr[0] = now_us();
+    ticks.clear();
+    tick("start");
     const uint8_t *hist_bins = bins_in, *hist_lab = lab_in, *hist_w = w_in;
     int64_t rows_part = 0;
     if (trace) tr[6] = now_us();
@@ -1339,6 +1352,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     std::vector<int64_t> soff(nslots + 1, 0);
     for (int k = 0; k < nslots; k++) soff[k + 1] = soff[k] + DS * slot_kc[k];
     const int64_t direct_bytes = soff[ndirect_slots] * 4;  // (direct slots first)
+    tick("soff");
     // reduce-scatter mode: slot ranges [own[r], own[r+1]) owned by rank r,
     // balanced by histogram bytes, each padded to Q counters at offset r * Q
     const int NR = g_ctx.world, me = g_ctx.rank;
@@ -1373,12 +1387,14 @@ void train_region(adapt_region *h, cudaStream_t s) {
       fn.cls.each([&](int c, int k) { m[c] = (uint8_t)k; });
       node_ci[j] = ci;
     }
+    tick("cmaps");
     std::vector<int64_t> res_off(A + 1, 0);  // winners: compact per-node records (D2H bytes)
     for (int j = 0; j < A; j++)
       res_off[j + 1] = res_off[j] + (int64_t)((sizeof(NodeRes) + 8 * (size_t)node_kc[j] + 7) / 8 * 8);
     std::vector<int32_t> big_nodes, small_nodes;  // split search: by class count
     for (int j = 0; j < A; j++)
       (node_kc[j] <= split_small_max_classes() ? small_nodes : big_nodes).push_back(j);
+    tick("res_off+lists");
     std::vector<SubJob> jobs;
     std::vector<int16_t> maps;
     std::vector<int32_t> zstart(ndirect_slots), sstart;  // chunk prefixes (zero / subtract)
@@ -1409,6 +1425,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       sblocks += chunk_count(DS * jb.kc_d);
     }
     if (trace) tr[6] = now_us();
+    tick("jobs");
     Arena &sa = h->stage_a;
     sa.reset();
     const size_t o_cmaps = sa.put(cmaps), o_soff = sa.put(soff), o_skc = sa.put(slot_kc),
@@ -1433,8 +1450,10 @@ void train_region(adapt_region *h, cudaStream_t s) {
       uint8_t *bo = pa.bins_out;
       uint8_t *lo = pa.lab_out;
       if (trace) tr[1] = now_us();
+      tick("tables_upload");
       CUDA_CHECK(cudaStreamSynchronize(s));
       if (trace) tr[2] = now_us();
+      tick("wait_part");
       // children's pieces, from the CTAs' share reports: ranges visit a parent
       // at most once each and in range order, so every child's pieces come out
       // in offset order; a counting sort by child groups them (CSR)
@@ -1460,6 +1479,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       hist_w = pa.w_out;
     }
     if (trace) tr[3] = now_us();
+    tick("pieces");
     // ---- a4: histograms of the direct nodes (the root, or the smaller children) ----
     std::vector<Seg> hsegs, fsegs;  // big nodes: smem-privatised pass; small: flat pass
     for (int j = 0; j < A; j++) {
@@ -1607,8 +1627,10 @@ void train_region(adapt_region *h, cudaStream_t s) {
       comm_bytes = NR * Q * 4 + RB * NR;
     }
     if (trace) tr[4] = now_us();
+    tick("launch_hist..winner");
     CUDA_CHECK(cudaStreamSynchronize(s));
     if (trace) tr[5] = now_us();
+    tick("wait_winners");
     h->stats.push_back(A);
     h->stats.push_back(htotal + ftotal);
     h->stats.push_back(rows_part);
@@ -1666,6 +1688,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
         nsegs.push_back(sg);
       }
     }
+    tick("pass1");
     if (ndirect > 0) {  // the next level's a7: level 0 moved nothing, so level 1 reads its input
       pending = level > 0 ? start_part(level + 1, nsegs, (out_plane ? h->binsB : h->binsA).as<uint8_t>(),
                                        (out_plane ? h->labB : h->labA).as<uint8_t>(),
@@ -1673,6 +1696,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
                                        out_plane ^ 1)
                           : start_part(level + 1, nsegs, bins_in, lab_in, w_in, out_plane);
     }
+    tick("part_launch");
     std::vector<uint64_t> P(C), PL(C), PR(C);
     for (int j = 0; j < A; j++) {
       const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + res_off[j]);
@@ -1765,6 +1789,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
     }
     // derived slots follow the direct ones
     for (size_t i = 0; i < nderived.size(); i++) next[nderived[i].j].slot = ndirect + (int)i;
+    tick("pass2");
+    if (trace2) {
+      fprintf(stderr, "[adapt] L%02d host:", level);
+      for (size_t i = 1; i < ticks.size(); i++)
+        fprintf(stderr, " %s %.0f", ticks[i].first, ticks[i].second - ticks[i - 1].second);
+      fprintf(stderr, " us\n");
+    }
     if (trace)
       fprintf(stderr, "[adapt] L%02d A=%d part-launch %.0f us (tables %.0f, ranges %.0f), wait %.0f, pieces %.0f, "
               "hist..winner launch %.0f, wait %.0f, decide %.0f us\n", level, A,

@@ -1,0 +1,11 @@
+# round-2 evidence: GPU tests, smoke, driver-style bench, reference arm, launch list, ncu captures
+mkdir -p gpurun_out
+export PATH=/usr/local/cuda/bin:$PATH
+bash scripts/gpu_tests.sh
+bash scripts/gpu_bench_full.sh
+for spec in partition_kernel:4 hist_kernel:4 label_bin:0 select_kernel_c:0 split_kernel:10; do
+  NCU_KERNEL=${spec%%:*} NCU_SKIP=${spec##*:} bash scripts/gpu_ncu_one.sh
+done
+NCU_KERNEL=select_kernel_h NCU_SKIP=0 BENCH_ARGS="--no-kfold --no-c2 --no-proxy" bash scripts/gpu_ncu_one.sh
+mv gpurun_out/prof_select_kernel_h_0.ncu-rep gpurun_out/prof_select_kernel_h_c5.ncu-rep 2>/dev/null
+ls gpurun_out

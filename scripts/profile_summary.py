@@ -15,7 +15,7 @@ import os
 
 rnd, launches, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
 PHASE = {"partition_kernel": "partition", "hist_kernel": "hist", "label_bin_kernel": "ingest",
-         "discover_kernel": "discover", "select_kernel": "select", "select_kernel_d": "select", "select_kernel_c": "select",
+         "discover_kernel": "discover", "select_kernel_c": "select", "select_kernel_h": "select",
          "split_kernel": "split"}
 traffic = {}
 out = [f"# Round {rnd} ncu summary", ""]

@@ -131,7 +131,7 @@ def _check(res, X, T, D):
 @pytest.mark.parametrize("world", [2, 3])
 def test_p_invariant_tree_c3(world):
     X, T = synth.generate("C3", 0, 200_003)
-    _check(_run(world, {"X": X, "T": T, "D": 12}), X, T, 12)
+    _check(_run(world, {"X": X, "T": T, "D": 12, "comm": "allreduce"}), X, T, 12)
 
 
 def test_p_invariant_tree_c4_slice_host_records():
@@ -230,7 +230,9 @@ def test_p_invariant_train_many_fused():
 
 # ---- reduce-scatter of the level's histograms by node
 # ownership, owner split search, all-gather of the winner records
-# (ADAPT_HIST_COMM=rs): every rank must still get the single-table tree ----
+# (ADAPT_HIST_COMM=rs, the default with more than one rank; the tests above
+# without "comm" run it too, the ones below force each mode): every rank must
+# still get the single-table tree ----
 @pytest.mark.parametrize("world", [2, 3])
 def test_p_invariant_tree_reduce_scatter(world):
     X, T = synth.generate("C3", 0, 200_003)
@@ -244,16 +246,17 @@ def test_reduce_scatter_c4_deep_and_empty_shard():
     _check(_run(2, {"X": X, "T": T, "D": 4, "comm": "rs"}), X, T, 4)
 
 
-def test_reduce_scatter_forest_kfold_many():
+def test_allreduce_forest_kfold_many():
+    # the same workloads through the all-reduce mode (the default above is rs)
     X, T = synth.generate("C3", 0, 30_001)
-    res = _run(2, {"X": X, "T": T, "D": 6, "model": "rfc,3,6,seed=4", "comm": "rs"})
+    res = _run(2, {"X": X, "T": T, "D": 6, "model": "rfc,3,6,seed=4", "comm": "allreduce"})
     ref = oracle.train_forest(X, oracle.labels(T), T.shape[1], 6, 3, 4)
     for r, o in sorted(res.items()):
         assert "error" not in o
         for t in range(3):
             assert o["forest"][t].tobytes() == ref[t].tobytes(), f"rank {r} tree {t}"
     K, m, S, seed, D = 4, 2, 2, 9, 6
-    res = _run(2, {"X": X, "T": T, "D": D, "kfold": (K, m, S, seed), "comm": "rs"})
+    res = _run(2, {"X": X, "T": T, "D": D, "kfold": (K, m, S, seed), "comm": "allreduce"})
     _, trees = oracle.kfold(X, T, D, K, m, S, seed)
     for r, o in sorted(res.items()):
         assert "error" not in o
@@ -262,7 +265,7 @@ def test_reduce_scatter_forest_kfold_many():
     cfg = synth.CONFIGS["C2"]
     X, T = synth.generate(cfg, 0, 30_000)
     regions = [(np.ascontiguousarray(X[r::3]), np.ascontiguousarray(T[r::3])) for r in range(3)]
-    res = _run(2, {"regions": regions, "D": 6, "comm": "rs"})
+    res = _run(2, {"regions": regions, "D": 6, "comm": "allreduce"})
     for r, o in sorted(res.items()):
         for (Xr, Tr), got in zip(regions, o["trees"]):
             assert got.tobytes() == oracle.train(Xr, oracle.labels(Tr), Tr.shape[1], 6).tobytes()
