@@ -35,7 +35,7 @@ for r in rows:
 tot = sum(v[1] for v in per.values())
 out += ["## Launch list (one step, serialised, cold-cache)", "",
         f"Source: `{launches}` — `ncu --metrics gpu__time_duration.sum --clock-control none "
-        "python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-records --no-c5 --no-kfold --no-c2`.", "",
+        "python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-records --no-c5 --no-kfold --no-c2 --no-proxy`.", "",
         "| kernel | launches | ms | share of step |", "|---|---:|---:|---:|"]
 for k, (n, ms) in sorted(per.items(), key=lambda x: -x[1][1]):
     out.append(f"| {k} | {n} | {ms:.3f} | {100 * ms / tot:.1f}% |")
