@@ -750,6 +750,17 @@ def main():
                "all_cores": {"value": va, "unit": "samples/s", "cores": cores,
                              "sample": f"same sample, liboracle_omp.so (oracle.c with -fopenmp: "
                                        f"features of a node and vectors in parallel) ({dta:.1f} s)"}}
+        if args.config == "C4" and not args.no_c2:  # the small configs, whole tables
+            per = {}
+            for name, omp in (("C1", False), ("C2", False), ("C3", True)):
+                c = synth.CONFIGS[name]
+                rows_c = c.N if c.regions == 1 else len(synth.region_rows(c, 0))
+                vc, dtc = cpu_baseline(c, rows_c, c.D, omp=omp)
+                per[name] = {"value": vc, "unit": "samples/s", "seconds": dtc, "rows": rows_c,
+                             "cores": cores if omp else 1,
+                             "sample": f"first {rows_c} rows of {name}: labels + depth-{c.D} CART + "
+                                       f"select, {'all-cores' if omp else 'single-threaded'} oracle"}
+            cpu["per_config"] = per
     line = {
         "metric": METRIC, "value": N / (ms / 1e3), "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
