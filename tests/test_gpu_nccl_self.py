@@ -1,6 +1,7 @@
 """The NCCL transport on one GPU: with ADAPT_NCCL_SELF=1 a world-1 run gets a
 1-rank NCCL communicator, so every collective of the training path (value-table
 all-gather, histogram / flag / row-count all-reduces, the forest's row-offset
+all-gather; with ADAPT_HIST_COMM=rs the histogram reduce-scatter and the winner
 all-gather) is a real NCCL call; results must equal the plain run's and the
 oracle's.  (Multi-rank NCCL itself needs several GPUs; the multi-rank logic is
 tested through the host-staged hooks in test_gpu_multirank.py.)"""
@@ -49,3 +50,9 @@ def test_nccl_self_communicator_matches_plain_run(tmp_path):
     nccl, log = _run(tmp_path, {"ADAPT_NCCL_SELF": "1", "NCCL_DEBUG": "INFO"})
     assert "NCCL INFO" in log, "no NCCL communicator was created"
     assert plain == nccl
+    # the reduce-scatter exchange (the default with more than one rank) forced
+    # on the 1-rank communicator: ncclReduceScatter of the padded owner ranges
+    # and ncclAllGather of the winner records are real NCCL calls
+    rs, log = _run(tmp_path, {"ADAPT_NCCL_SELF": "1", "ADAPT_HIST_COMM": "rs", "NCCL_DEBUG": "INFO"})
+    assert "NCCL INFO" in log
+    assert plain == rs
