@@ -212,6 +212,17 @@ int adapt_select_batch(adapt_region_t *h, const float *d_X, int64_t m, int32_t *
  * internal streams.  Returns when out is written. */
 int adapt_select_batch_host(adapt_region_t *h, const float *X, int64_t m, int32_t *out,
                             void *cuda_stream);
+/* The selections of every row of the region's recorded wide table (the
+ * profiled feature vectors themselves: "which variant does the model pick for
+ * each configuration it was trained on"), from the library's device copy of a
+ * HOST-recorded table (adapt_record_table with on_device = 0 keeps it until the
+ * next record), so the vectors cross PCIe once.  out [n] int32 (n = the rows
+ * recorded on this rank): device memory when out_on_device != 0 (async on
+ * `stream`), else host memory (returns when written).  E_NOT_TRAINED before
+ * train; E_USAGE when the table was borrowed device memory (released when
+ * train returned: use adapt_select_batch with the caller's buffer) or came
+ * from long-format records. */
+int adapt_select_table(adapt_region_t *h, int32_t *out, int out_on_device, void *cuda_stream);
 
 /* ---- model exchange / parity introspection ------------------------------ */
 /* Canonical BFS node array; *n_nodes receives the node count even when cap is

@@ -37,7 +37,7 @@ SYMBOLS = [
     "adapt_last_error", "adapt_version",
     "adapt_region_create", "adapt_region_destroy", "adapt_region_info", "adapt_record",
     "adapt_record_batch", "adapt_get_wide_table", "adapt_record_table", "adapt_distinct_pairs", "adapt_train", "adapt_train_many",
-    "adapt_select", "adapt_select_batch", "adapt_select_batch_host", "adapt_get_tree",
+    "adapt_select", "adapt_select_batch", "adapt_select_batch_host", "adapt_select_table", "adapt_get_tree",
     "adapt_forest_size", "adapt_get_forest_tree", "adapt_kfold", "adapt_get_kfold_tree",
     "adapt_set_tree", "adapt_get_labels", "adapt_get_value_table", "adapt_get_bins",
     "adapt_profile_enable", "adapt_profile_reset", "adapt_profile_get", "adapt_train_stats",
@@ -104,6 +104,7 @@ _sigs = {
     "adapt_select": [_P, _P, _P],
     "adapt_select_batch": [_P, _P, _I64, _P, _P],
     "adapt_select_batch_host": [_P, _P, _I64, _P, _P],
+    "adapt_select_table": [_P, _P, _I, _P],
     "adapt_get_tree": [_P, _P, ctypes.c_int32, _P],
     "adapt_forest_size": [_P, _P],
     "adapt_get_forest_tree": [_P, ctypes.c_int32, _P, ctypes.c_int32, _P],
@@ -385,6 +386,14 @@ def adapt_select_batch_host(h: int, X, m: int, out, stream=None):
     _check_array(out, "out", "int32", None, int(m), False)
     _check(_L.adapt_select_batch_host(h, _ptr(X), int(m), _ptr(out), _stream(stream)),
            "adapt_select_batch_host")
+
+
+def adapt_select_table(h: int, out, stream=None):
+    """Selections of every row of the recorded (host) wide table into out [n]
+    int32 (a numpy array or a host / CUDA tensor)."""
+    on_dev = bool(getattr(out, "is_cuda", False))
+    _check_array(out, "out", "int32", None, adapt_region_info(h)["num_rows"], on_dev)
+    _check(_L.adapt_select_table(h, _ptr(out), int(on_dev), _stream(stream)), "adapt_select_table")
 
 
 def adapt_get_tree(h: int) -> np.ndarray:

@@ -2539,6 +2539,31 @@ int adapt_select_batch(adapt_region_t *h, const float *d_X, int64_t m, int32_t *
   });
 }
 
+int adapt_select_table(adapt_region_t *h, int32_t *out, int out_on_device, void *stream) {
+  return guarded([&] {
+    checked(h);
+    ensure_init();
+    if (!out && h->n > 0) throw Error(ADAPT_E_INVALID_ARG, "null out");
+    if (!h->trained) throw Error(ADAPT_E_NOT_TRAINED, "region not trained");
+    if (!h->have_table || h->d_feat != h->own_feat.as<float>())
+      throw Error(ADAPT_E_USAGE, "no host-recorded wide table on the device");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (h->n == 0) return;
+    if (out_on_device) {
+      Phase ph("select", s, (double)h->n * (4.0 * h->F + 4));
+      select_device(h, h->d_feat, h->n, out, s);
+      return;
+    }
+    h->oa.ensure((size_t)h->n * 4);
+    {
+      Phase ph("select", s, (double)h->n * (4.0 * h->F + 4));
+      select_device(h, h->d_feat, h->n, h->oa.as<int32_t>(), s);
+    }
+    CUDA_CHECK(cudaMemcpyAsync(out, h->oa.p, (size_t)h->n * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
 int adapt_select_batch_host(adapt_region_t *h, const float *X, int64_t m, int32_t *out,
                             void *stream) {
   return guarded([&] {

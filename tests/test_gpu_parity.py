@@ -368,6 +368,29 @@ def test_select_set_tree_chain():
     ad.adapt_region_destroy(h)
 
 
+def test_select_table_of_host_recorded_table():
+    """adapt_select_table: the selections of the recorded (host) table's own
+    vectors from the library's device copy, to host and to device memory."""
+    cfg = synth.CONFIGS["C3"]
+    X, T = synth.generate(cfg, 0, 50_001)
+    h = _train(X, T, 9, on_device=False)
+    ref = oracle.train(X, oracle.labels(T), cfg.V, 9)
+    want = oracle.select(ref, X)
+    hout = np.empty(len(X), np.int32)
+    ad.adapt_select_table(h, hout)
+    assert np.array_equal(hout, want)
+    dout = torch.empty(len(X), dtype=torch.int32, device=DEV)
+    ad.adapt_select_table(h, dout, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert np.array_equal(dout.cpu().numpy(), want)
+    ad.adapt_region_destroy(h)
+    h = _train(X, T, 9, on_device=True)  # borrowed device table: released by train
+    with pytest.raises(ad.AdaptError) as e:
+        ad.adapt_select_table(h, hout)
+    assert e.value.code == ad.ADAPT_E_USAGE
+    ad.adapt_region_destroy(h)
+
+
 def test_errors():
     s = torch.cuda.current_stream()
     h = _region(1, 2, 2)
