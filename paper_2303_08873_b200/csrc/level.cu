@@ -114,7 +114,7 @@ __device__ __forceinline__ int first_seg(const Seg *segs, int nseg, uint32_t p) 
 
 // ------------------------------------------------------------ partition --
 #ifndef ADAPT_PART_UNROLL
-#define ADAPT_PART_UNROLL 4
+#define ADAPT_PART_UNROLL 2
 #endif
 #ifndef ADAPT_HIST_UNROLL
 #define ADAPT_HIST_UNROLL 8
@@ -149,26 +149,34 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition_kernel
       const Seg sg = a.segs[s];
       const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
       const uint32_t q1 = min(sg.len, pe - sg.row_base);
-      for (uint32_t qb = q0; qb < q1; qb += kPartUnroll * blockDim.x) {
-        Row<BS> r[kPartUnroll];
-        int label[kPartUnroll];
-        uint8_t wgt[kPartUnroll];
+      // rows in flight: kPartUnroll per thread, loaded one batch ahead of the
+      // batch being placed (software pipeline: the next batch's loads are in
+      // flight during this batch's ballots and stores)
+      Row<BS> r[kPartUnroll], rn[kPartUnroll];
+      int label[kPartUnroll], labn[kPartUnroll];
+      uint8_t wgt[kPartUnroll], wgn[kPartUnroll];
+      auto load = [&](uint32_t qb, Row<BS>(&rr)[kPartUnroll], int(&ll)[kPartUnroll],
+                      uint8_t(&ww)[kPartUnroll]) {
 #pragma unroll
-        for (int u = 0; u < kPartUnroll; u++) wgt[u] = 1;
-#pragma unroll
-        for (int u = 0; u < kPartUnroll; u++) {  // all loads first
+        for (int u = 0; u < kPartUnroll; u++) {
           const uint32_t q = qb + u * blockDim.x + tid;
-          label[u] = -1;
+          ll[u] = -1;
+          ww[u] = 1;
           if (q < q1) {
-            load_row<BS>(a.bins_in, a.pstride, sg.off + q, r[u]);
-            label[u] = __ldcs(a.lab_in + sg.off + q);
+            load_row<BS>(a.bins_in, a.pstride, sg.off + q, rr[u]);
+            ll[u] = __ldcs(a.lab_in + sg.off + q);
             // bootstrap weight (forests): rows drawn 0 times leave the tree here
-            if (a.w_in) wgt[u] = __ldcs(a.w_in + sg.off + q);
+            if (a.w_in) ww[u] = __ldcs(a.w_in + sg.off + q);
           } else {
 #pragma unroll
-            for (int i = 0; i < Row<BS>::N; i++) r[u].w[i] = 0;
+            for (int i = 0; i < Row<BS>::N; i++) rr[u].w[i] = 0;
           }
         }
+      };
+      if (q0 < q1) load(q0, r, label, wgt);
+      for (uint32_t qb = q0; qb < q1; qb += kPartUnroll * blockDim.x) {
+        const bool more = qb + kPartUnroll * blockDim.x < q1;
+        if (more) load(qb + kPartUnroll * blockDim.x, rn, labn, wgn);
 #pragma unroll
         for (int u = 0; u < kPartUnroll; u++) {
           const bool valid = label[u] >= 0 && wgt[u] > 0;
@@ -186,6 +194,14 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition_kernel
             store_row<BS>(a.bins_out, a.pstride, pos, r[u]);
             __stcs(a.lab_out + pos, (uint8_t)label[u]);
             if (a.w_out) __stcs(a.w_out + pos, wgt[u]);
+          }
+        }
+        if (more) {
+#pragma unroll
+          for (int u = 0; u < kPartUnroll; u++) {
+            r[u] = rn[u];
+            label[u] = labn[u];
+            wgt[u] = wgn[u];
           }
         }
       }
