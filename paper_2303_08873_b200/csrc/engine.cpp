@@ -43,11 +43,17 @@ void cuda_check(cudaError_t e, const char *what) {
 namespace {
 
 // ------------------------------------------------------------ utilities --
+bool trace_allocs() {  // ADAPT_TRACE_HOST=3: report every buffer (re)allocation
+  static const bool on = getenv("ADAPT_TRACE_HOST") && atoi(getenv("ADAPT_TRACE_HOST")) >= 3;
+  return on;
+}
+
 struct DevBuf {
   void *p = nullptr;
   size_t cap = 0;
   void ensure(size_t bytes) {
     if (bytes <= cap) return;
+    if (trace_allocs()) fprintf(stderr, "[adapt] cudaMalloc %zu (had %zu)\n", bytes, cap);
     release();
     size_t want = std::max<size_t>(bytes, 256);
     CUDA_CHECK(cudaMalloc(&p, want));
@@ -57,6 +63,11 @@ struct DevBuf {
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
+  }
+  // per-level buffers whose size varies level to level and call to call:
+  // 1.5x headroom, so a later level / call rarely pays a (synchronising) cudaMalloc
+  void grow(size_t bytes) {
+    if (bytes > cap) ensure(std::max(bytes, cap + cap / 2));
   }
   template <class T>
   T *as() const { return static_cast<T *>(p); }
@@ -68,10 +79,15 @@ struct HostBuf {  // pinned staging for small D2H copies
   size_t cap = 0;
   void ensure(size_t bytes) {
     if (bytes <= cap) return;
+    if (trace_allocs()) fprintf(stderr, "[adapt] cudaMallocHost %zu (had %zu)\n", bytes, cap);
     if (p) cudaFreeHost(p);
     p = nullptr;
     CUDA_CHECK(cudaMallocHost(&p, std::max<size_t>(bytes, 4096)));
     cap = std::max<size_t>(bytes, 4096);
+  }
+  // (cudaMallocHost pins pages: milliseconds per call) 1.5x headroom
+  void grow(size_t bytes) {
+    if (bytes > cap) ensure(std::max(bytes, cap + cap / 2));
   }
   template <class T>
   T *as() const { return static_cast<T *>(p); }
@@ -86,26 +102,32 @@ struct HostBuf {  // pinned staging for small D2H copies
 // pointers are formed after flush().  The caller synchronises the stream
 // before the next put() round (every level does).
 struct Arena {
-  std::vector<uint8_t> stage;
-  HostBuf pinned;
+  HostBuf pinned;   // written directly by put() (no pageable staging copy)
   DevBuf dev;
+  size_t used = 0;
   template <class T>
   size_t put(const std::vector<T> &v) {
-    const size_t off = (stage.size() + 15) & ~size_t(15);
-    stage.resize(off + v.size() * sizeof(T) + 16);
-    if (!v.empty()) memcpy(stage.data() + off, v.data(), v.size() * sizeof(T));
+    const size_t off = (used + 15) & ~size_t(15);
+    const size_t end = off + v.size() * sizeof(T) + 16;
+    if (end > pinned.cap) {  // grow geometrically (>= 4 MB), keeping what was put so far
+      HostBuf nb;
+      nb.ensure(std::max<size_t>({end, 2 * pinned.cap, (size_t)4 << 20}));
+      if (used) memcpy(nb.p, pinned.p, used);
+      std::swap(nb.p, pinned.p);
+      std::swap(nb.cap, pinned.cap);
+    }
+    if (!v.empty()) memcpy(static_cast<uint8_t *>(pinned.p) + off, v.data(), v.size() * sizeof(T));
+    used = end;
     return off;
   }
   void flush(cudaStream_t s) {
-    if (stage.empty()) return;
-    pinned.ensure(stage.size());
-    dev.ensure(stage.size());
-    memcpy(pinned.p, stage.data(), stage.size());
-    CUDA_CHECK(cudaMemcpyAsync(dev.p, pinned.p, stage.size(), cudaMemcpyHostToDevice, s));
+    if (!used) return;
+    if (used > dev.cap) dev.ensure(std::max<size_t>({used, 2 * dev.cap, (size_t)4 << 20}));
+    CUDA_CHECK(cudaMemcpyAsync(dev.p, pinned.p, used, cudaMemcpyHostToDevice, s));
   }
   template <class T>
   T *ptr(size_t off) const { return reinterpret_cast<T *>(static_cast<uint8_t *>(dev.p) + off); }
-  void reset() { stage.clear(); }
+  void reset() { used = 0; }
 };
 
 thread_local std::string g_last_error;
@@ -1306,7 +1328,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     pa.F = F;
     pa.max_visits = st.max_visits;
     st.vbytes = (size_t)pa.nranges * st.max_visits * 6 * 4;
-    h->visits.ensure(st.vbytes);
+    h->visits.grow(st.vbytes);
     CUDA_CHECK(cudaMemsetAsync(h->visits.p, 0xFF, st.vbytes, s));
     pa.visits = h->visits.as<int32_t>();
     {
@@ -1314,7 +1336,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       Phase ph(per_level ? nm : "partition", s, (double)total * 2 * (BS + 1));
       launch_partition(pa, s);
     }
-    h->hvis.ensure(st.vbytes);
+    h->hvis.grow(st.vbytes);
     st.hv = h->hvis.as<int32_t>();
     CUDA_CHECK(cudaMemcpyAsync(st.hv, h->visits.p, st.vbytes, cudaMemcpyDeviceToHost, s));
     return st;
@@ -1433,7 +1455,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
                  o_nkc = sa.put(node_kc), o_zst = sa.put(zstart), o_sst = sa.put(sstart),
                  o_big = sa.put(big_nodes), o_small = sa.put(small_nodes), o_roff = sa.put(res_off);
     sa.flush(s);
-    Hcur->ensure((size_t)soff[nslots] * 4 + 16);
+    Hcur->grow((size_t)soff[nslots] * 4 + 16);
     if (rs)  // padding after each owner's range: summed by the reduce-scatter, never read
       for (int r = 0; r < NR; r++) {
         const int64_t used = (own[r + 1] > own[r] ? soff[own[r + 1] - 1] + DS * slot_kc[own[r + 1] - 1]
@@ -1501,6 +1523,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     }
     const uint32_t ftotal = virtualize(fsegs, true);
     const uint32_t htotal = virtualize(hsegs, true);
+    tick("hsegs");
     if (htotal + ftotal > 0) {
       Arena &sb = h->stage_b;
       sb.reset();
@@ -1532,12 +1555,15 @@ void train_region(adapt_region *h, cudaStream_t s) {
       // 1-byte labels: they run unsynchronised
       snprintf(nm, sizeof nm, "hist_L%02d", level);
       Phase ph(per_level ? nm : "hist", s, (double)(htotal + ftotal) * (F + 1));
+      tick("hist_args");
       launch_hist(ha, s);
+      tick("launch_hist");
       HistArgs fa = ha;  // the small nodes
       fa.segs = sb.ptr<Seg>(o_fsegs);
       fa.nseg = (int)fsegs.size();
       fa.total_rows = ftotal;
       launch_hist_flat(fa, s);
+      tick("launch_flat");
     }
     if (!rs && collectives_on() && ndirect_slots > 0)  // the direct slots are contiguous at the front
       comm_allreduce_sum(Hcur->p, (size_t)soff[ndirect_slots], false, s, "allreduce histograms");
@@ -1546,12 +1572,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
       launch_subtract(Hcur->as<uint32_t>(), Hprev->as<uint32_t>(), DS, sa.ptr<SubJob>(o_jobs),
                       sa.ptr<int16_t>(o_maps), sa.ptr<int32_t>(o_sst), (int)jobs.size(), sblocks, s);
     }
-    h->hres.ensure((size_t)res_off[A] + 16);
+    h->hres.grow((size_t)res_off[A] + 16);
     uint8_t *hr = h->hres.as<uint8_t>();
     int64_t comm_bytes = collectives_on() ? (int64_t)soff[ndirect_slots] * 4 : 0;
     if (!rs) {
-      h->cand.ensure((size_t)A * F * sizeof(SplitCand));
-      h->res.ensure((size_t)res_off[A] + 16);
+      h->cand.grow((size_t)A * F * sizeof(SplitCand));
+      h->res.grow((size_t)res_off[A] + 16);
       {
         snprintf(nm, sizeof nm, "split_L%02d", level);
         Phase ph(per_level ? nm : "split", s, 0);
@@ -1569,7 +1595,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       CUDA_CHECK(cudaMemcpyAsync(hr, h->res.p, (size_t)res_off[A], cudaMemcpyDeviceToHost, s));
     } else {
       // a5 by ownership: this rank's slots summed over ranks into Hg
-      h->Hg.ensure((size_t)Q * 4 + 16);
+      h->Hg.grow((size_t)Q * 4 + 16);
       comm_reduce_scatter(Hcur->p, h->Hg.p, (size_t)Q, s, "reduce-scatter histograms");
       // a6 for the owned nodes only, in slot order: owned index i = slot own[r] + i
       std::vector<int32_t> slot_j(nslots);
@@ -1596,9 +1622,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
       const size_t o_ooff = so.put(ooff), o_okc = so.put(okc), o_obig = so.put(obig),
                    o_osmall = so.put(osmall), o_orb = so.put(rb[me]);
       so.flush(s);
-      h->cand.ensure((size_t)std::max(m, 1) * F * sizeof(SplitCand));
-      h->reso.ensure((size_t)RB + 16);
-      h->resall.ensure((size_t)RB * NR + 16);
+      h->cand.grow((size_t)std::max(m, 1) * F * sizeof(SplitCand));
+      h->reso.grow((size_t)RB + 16);
+      h->resall.grow((size_t)RB * NR + 16);
       {
         snprintf(nm, sizeof nm, "split_L%02d", level);
         Phase ph(per_level ? nm : "split", s, 0);
@@ -1615,7 +1641,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       }
       // every rank gets every owner's winner records (padded to RB bytes each)
       comm_allgather(h->reso.p, h->resall.p, (size_t)RB, s, "all-gather winners");
-      h->hgat.ensure((size_t)RB * NR + 16);
+      h->hgat.grow((size_t)RB * NR + 16);
       uint8_t *ga = h->hgat.as<uint8_t>();
       CUDA_CHECK(cudaMemcpyAsync(ga, h->resall.p, (size_t)RB * NR, cudaMemcpyDeviceToHost, s));
       CUDA_CHECK(cudaStreamSynchronize(s));
@@ -1697,6 +1723,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
                           : start_part(level + 1, nsegs, bins_in, lab_in, w_in, out_plane);
     }
     tick("part_launch");
+    // one pass over a node's compact classes: n, S = sum c^2 and the majority
+    // class (ties -> lowest, R12) of the node, of its left part and of its
+    // right part, and the children's class sets
     std::vector<uint64_t> P(C), PL(C), PR(C);
     for (int j = 0; j < A; j++) {
       const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + res_off[j]);
