@@ -62,12 +62,21 @@ __global__ void __launch_bounds__(kChunkThreads)
   const int64_t E = DS * jb.kc_d;
   const int64_t i0 = (int64_t)(blockIdx.x - cstart[y]) * kChunk;
   const int64_t i1 = min(i0 + kChunk, E);
+  // element i = r * kc_d + j (i < 2^31: a node matrix is DS x kc <= 16384 x 255),
+  // advanced by kChunkThreads per step without a division
+  const int kcd = jb.kc_d;
+  const int dq = kChunkThreads / kcd, dr = kChunkThreads - dq * kcd;
+  int r = (int)((i0 + threadIdx.x) / kcd), j = (int)(i0 + threadIdx.x - (int64_t)r * kcd);
   for (int64_t i = i0 + threadIdx.x; i < i1; i += kChunkThreads) {
-    const int64_t r = i / jb.kc_d;
-    const int j = (int)(i - r * jb.kc_d);
     const short2 mj = m[j];
-    const uint32_t sib = mj.y >= 0 ? q[r * jb.kc_s + mj.y] : 0u;
-    d[i] = p[r * jb.kc_p + mj.x] - sib;
+    const uint32_t sib = mj.y >= 0 ? q[(int64_t)r * jb.kc_s + mj.y] : 0u;
+    d[i] = p[(int64_t)r * jb.kc_p + mj.x] - sib;
+    r += dq;
+    j += dr;
+    if (j >= kcd) {
+      j -= kcd;
+      r++;
+    }
   }
 }
 
@@ -137,12 +146,21 @@ __global__ void __launch_bounds__(kSplitThreads)
        // flight (contiguous when the node has <= kClassChunk classes)
       const int E = Df * kc;
       const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(&tile[0][0]);
+      // element e = r * kc + k, advanced by kSplitThreads per step without a
+      // division (r += dq, k += dr, carry)
+      const int dq = kSplitThreads / kc, dr = kSplitThreads - dq * kc;
+      int r = t / kc, k = t - r * kc;
       for (int e = t; e < E; e += kSplitThreads) {  // async copies: all in flight at once
-        const int r = e / kc, k = e - r * kc;
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
                          tbase + 4u * (uint32_t)(r * (kClassChunk + 1) + k)),
                      "l"(h + (size_t)r * C + c0 + k)
                      : "memory");
+        r += dq;
+        k += dr;
+        if (k >= kc) {
+          k -= kc;
+          r++;
+        }
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
     }
