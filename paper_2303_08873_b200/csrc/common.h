@@ -144,6 +144,10 @@ struct PartArgs {            // a7: move the split parents' rows into the childr
 };
 int partition_ranges(int sms, uint32_t total_rows);
 void launch_partition(const PartArgs &a, cudaStream_t s);
+// the partition's per-segment split / write decisions from the winner records
+// (node j's record at res + rec_off[j]); segs[i].direct = the segment's node
+void launch_decide_segs(Seg *segs, int nseg, const uint8_t *res, const int64_t *rec_off,
+                        const int32_t *node_kc, const int32_t *node_depth, int D, cudaStream_t s);
 
 // Node histograms are stored class-compacted: node j with kc_j present classes
 // (ascending class ids) is a [DS][kc_j] u32 matrix, DS = sum_f D_f; feature f's

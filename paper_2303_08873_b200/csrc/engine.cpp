@@ -124,10 +124,24 @@ struct Arena {
     if (!used) return;
     if (used > dev.cap) dev.ensure(std::max<size_t>({used, 2 * dev.cap, (size_t)4 << 20}));
     CUDA_CHECK(cudaMemcpyAsync(dev.p, pinned.p, used, cudaMemcpyHostToDevice, s));
+    if (!copied) CUDA_CHECK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventRecord(copied, s));
+    in_flight = true;
   }
   template <class T>
   T *ptr(size_t off) const { return reinterpret_cast<T *>(static_cast<uint8_t *>(dev.p) + off); }
-  void reset() { used = 0; }
+  // the pinned buffer is the SOURCE of the last flush's async copy: before it is
+  // written again that copy must have run (it can sit behind queued kernels)
+  void reset() {
+    if (in_flight) CUDA_CHECK(cudaEventSynchronize(copied));
+    in_flight = false;
+    used = 0;
+  }
+  ~Arena() {
+    if (copied) cudaEventDestroy(copied);
+  }
+  cudaEvent_t copied = nullptr;
+  bool in_flight = false;
 };
 
 thread_local std::string g_last_error;
@@ -471,10 +485,13 @@ struct adapt_region {
       H0, H1, Hg, reso, resall, segs,
       hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, cmaps, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall, hvis, hgat;  // winners, scalars, partition share reports, gathered winners
-  adapt::Arena stage_p, stage_a, stage_b;  // per-level uploads: partition, its tables, histogram
+  adapt::Arena stage_p, stage_a, stage_b, stage_r;  // per-level uploads: partition, its tables,
+                                                     // histogram segments, owner split lists
   cudaEvent_t sel_evt = nullptr;  // recorded after every device select (upload_tree waits)
+  cudaEvent_t win_evt = nullptr;  // a level's winner records are on the host
   ~adapt_region() {
     if (sel_evt) cudaEventDestroy(sel_evt);
+    if (win_evt) cudaEventDestroy(win_evt);
   }
   std::unordered_set<std::string> pair_set;  // distinct (features, variant) of the host records
   int64_t autotrain_failed_at = -1;          // pair count of the last failed auto-train
@@ -1219,7 +1236,6 @@ void train_region(adapt_region *h, cudaStream_t s) {
       pc_start.push_back((int32_t)pcs.size());
     }
   }
-  std::vector<Seg> psegs;           // pieces of the split parents (partition input)
   std::vector<int2> pseg_children;  // per piece: frontier index of the left / right child
   int ndirect_slots = R;  // direct slots are 0..ndirect_slots-1, derived ones follow
   struct Derived {        // a derived node of the next level = parent - direct sibling
@@ -1290,11 +1306,25 @@ void train_region(adapt_region *h, cudaStream_t s) {
     size_t vbytes = 0;
     int64_t rows_part = 0;
     int32_t *hv = nullptr;
+    int lvl = 0;
   };
-  auto start_part = [&](int lvl, std::vector<Seg> &segs, const uint8_t *b_in, const uint8_t *l_in,
-                        const uint8_t *wi, int oplane) {
-    PartState st;
+  // the partition launch (and its share reports' D2H), on the stream
+  auto launch_part = [&](PartState &st) {
+    {
+      snprintf(nm, sizeof nm, "partition_L%02d", st.lvl);
+      Phase ph(per_level ? nm : "partition", s, (double)st.rows_part * 2 * (BS + 1));
+      launch_partition(st.pa, s);
+    }
+    h->hvis.grow(st.vbytes);
+    st.hv = h->hvis.as<int32_t>();
+    CUDA_CHECK(cudaMemcpyAsync(st.hv, h->visits.p, st.vbytes, cudaMemcpyDeviceToHost, s));
     st.launched = true;
+  };
+  // upload a partition's segments and size its share reports; `defer`: the
+  // caller launches it (after the device has decided the segments' splits)
+  auto start_part = [&](int lvl, std::vector<Seg> &segs, const uint8_t *b_in, const uint8_t *l_in,
+                        const uint8_t *wi, int oplane, bool defer = false) {
+    PartState st;
     PartArgs &pa = st.pa;
     const uint32_t total = virtualize(segs, false);
     st.rows_part = total;
@@ -1331,14 +1361,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
     h->visits.grow(st.vbytes);
     CUDA_CHECK(cudaMemsetAsync(h->visits.p, 0xFF, st.vbytes, s));
     pa.visits = h->visits.as<int32_t>();
-    {
-      snprintf(nm, sizeof nm, "partition_L%02d", lvl);
-      Phase ph(per_level ? nm : "partition", s, (double)total * 2 * (BS + 1));
-      launch_partition(pa, s);
-    }
-    h->hvis.grow(st.vbytes);
-    st.hv = h->hvis.as<int32_t>();
-    CUDA_CHECK(cudaMemcpyAsync(st.hv, h->visits.p, st.vbytes, cudaMemcpyDeviceToHost, s));
+    st.lvl = lvl;
+    if (!defer) launch_part(st);
     return st;
   };
   PartState pending;
@@ -1358,7 +1382,10 @@ void train_region(adapt_region *h, cudaStream_t s) {
     // a7 of this level: normally launched already at the end of the previous
     // level's split decisions (overlapping the rest of its bookkeeping)
     PartState pst;
-    if (level > 0) pst = pending.launched ? pending : start_part(level, psegs, bins_in, lab_in, w_in, out_plane);
+    if (level > 0) {
+      if (!pending.launched) throw Error(ADAPT_E_CUDA, "internal: level without its partition");
+      pst = pending;
+    }
     pending = PartState{};
     PartArgs &pa = pst.pa;
     const int max_visits = pst.max_visits;
@@ -1450,10 +1477,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
     tick("jobs");
     Arena &sa = h->stage_a;
     sa.reset();
+    std::vector<int32_t> node_depth(A);
+    for (int j = 0; j < A; j++) node_depth[j] = frontier[j].depth;
     const size_t o_cmaps = sa.put(cmaps), o_soff = sa.put(soff), o_skc = sa.put(slot_kc),
                  o_jobs = sa.put(jobs), o_maps = sa.put(maps), o_noff = sa.put(node_off),
                  o_nkc = sa.put(node_kc), o_zst = sa.put(zstart), o_sst = sa.put(sstart),
-                 o_big = sa.put(big_nodes), o_small = sa.put(small_nodes), o_roff = sa.put(res_off);
+                 o_big = sa.put(big_nodes), o_small = sa.put(small_nodes), o_roff = sa.put(res_off),
+                 o_ndep = sa.put(node_depth);
     sa.flush(s);
     Hcur->grow((size_t)soff[nslots] * 4 + 16);
     if (rs)  // padding after each owner's range: summed by the reduce-scatter, never read
@@ -1500,8 +1530,42 @@ void train_region(adapt_region *h, cudaStream_t s) {
       hist_lab = lo;
       hist_w = pa.w_out;
     }
+    if (level > 0) {  // rows that reached this level's nodes (the moved rows of split parents)
+      rows_part = 0;
+      for (const auto &pc : pcs) rows_part += pc.second;
+    }
     if (trace) tr[3] = now_us();
     tick("pieces");
+    // the next level's a7, prepared now and launched right behind this level's
+    // winner kernel: its segments are every piece of every frontier node, and
+    // the device fills in each parent's split and which children stay
+    // (decide_segs_kernel) — no host round trip between the winners and the move
+    PartState early;
+    std::vector<Seg> esegs;
+    if (level + 1 < D) {
+      esegs.reserve(pcs.size());
+      for (int j = 0; j < A; j++)
+        for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {
+          Seg sg{};
+          sg.off = pcs[q].first;
+          sg.len = pcs[q].second;
+          sg.feat = -1;
+          sg.direct = j;  // parent id (groups a parent's pieces); the decision fills the rest
+          sg.hslot = -1;
+          esegs.push_back(sg);
+        }
+      early = level > 0
+                  ? start_part(level + 1, esegs, (out_plane ? h->binsB : h->binsA).as<uint8_t>(),
+                               (out_plane ? h->labB : h->labA).as<uint8_t>(),
+                               w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr, out_plane ^ 1, true)
+                  : start_part(level + 1, esegs, bins_in, lab_in, w_in, out_plane, true);
+    }
+    auto launch_early = [&](const uint8_t *res_dev) {
+      if (esegs.empty()) return;
+      launch_decide_segs(const_cast<Seg *>(early.pa.segs), (int)esegs.size(), res_dev, sa.ptr<int64_t>(o_roff),
+                         sa.ptr<int32_t>(o_nkc), sa.ptr<int32_t>(o_ndep), D, s);
+      launch_part(early);
+    };
     // ---- a4: histograms of the direct nodes (the root, or the smaller children) ----
     std::vector<Seg> hsegs, fsegs;  // big nodes: smem-privatised pass; small: flat pass
     for (int j = 0; j < A; j++) {
@@ -1593,6 +1657,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
                       h->res.as<uint8_t>(), sa.ptr<int64_t>(o_roff), s);
       }
       CUDA_CHECK(cudaMemcpyAsync(hr, h->res.p, (size_t)res_off[A], cudaMemcpyDeviceToHost, s));
+      if (!h->win_evt) CUDA_CHECK(cudaEventCreateWithFlags(&h->win_evt, cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventRecord(h->win_evt, s));
+      launch_early(h->res.as<uint8_t>());
     } else {
       // a5 by ownership: this rank's slots summed over ranks into Hg
       h->Hg.grow((size_t)Q * 4 + 16);
@@ -1617,7 +1684,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
         (node_kc[j] <= split_small_max_classes() ? osmall : obig).push_back(i);
       }
       const int m = (int)okc.size();
-      Arena &so = h->stage_b;
+      Arena &so = h->stage_r;
       so.reset();
       const size_t o_ooff = so.put(ooff), o_okc = so.put(okc), o_obig = so.put(obig),
                    o_osmall = so.put(osmall), o_orb = so.put(rb[me]);
@@ -1651,10 +1718,17 @@ void train_region(adapt_region *h, cudaStream_t s) {
           memcpy(hr + res_off[j], ga + (size_t)r * RB + rb[r][k - own[r]], (size_t)(res_off[j + 1] - res_off[j]));
         }
       comm_bytes = NR * Q * 4 + RB * NR;
+      if (!h->win_evt) CUDA_CHECK(cudaEventCreateWithFlags(&h->win_evt, cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventRecord(h->win_evt, s));
+      if (!esegs.empty()) {  // the records in node order on the device, for the early partition
+        h->res.grow((size_t)res_off[A] + 16);
+        CUDA_CHECK(cudaMemcpyAsync(h->res.p, hr, (size_t)res_off[A], cudaMemcpyHostToDevice, s));
+        launch_early(h->res.as<uint8_t>());
+      }
     }
     if (trace) tr[4] = now_us();
     tick("launch_hist..winner");
-    CUDA_CHECK(cudaStreamSynchronize(s));
+    CUDA_CHECK(cudaEventSynchronize(h->win_evt));  // the winners (the early partition may still run)
     if (trace) tr[5] = now_us();
     tick("wait_winners");
     h->stats.push_back(A);
@@ -1666,7 +1740,6 @@ void train_region(adapt_region *h, cudaStream_t s) {
 
     // ---- decide every frontier node; build the next level ----
     std::vector<FNode> next;
-    std::vector<Seg> nsegs;
     std::vector<int2> nchildren;
     std::vector<Derived> nderived;
     next.reserve((size_t)2 * A);
@@ -1701,32 +1774,17 @@ void train_region(adapt_region *h, cudaStream_t s) {
       d.inR = fn.depth + 1 < D && npr > 1;
       if (!d.inL && !d.inR) continue;
       d.hslot = ndirect++;
-      for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {  // one partition segment per piece
-        const auto &pc = pcs[q];
-        Seg sg{};
-        sg.off = pc.first;
-        sg.len = pc.second;
-        sg.feat = nr->feat;
-        sg.thr = nr->b_lo;
-        sg.write = (d.inL ? 1 : 0) | (d.inR ? 2 : 0);
-        sg.direct = j;  // parent id (groups a parent's pieces)
-        sg.hslot = d.hslot;
-        nsegs.push_back(sg);
-      }
     }
     tick("pass1");
-    if (ndirect > 0) {  // the next level's a7: level 0 moved nothing, so level 1 reads its input
-      pending = level > 0 ? start_part(level + 1, nsegs, (out_plane ? h->binsB : h->binsA).as<uint8_t>(),
-                                       (out_plane ? h->labB : h->labA).as<uint8_t>(),
-                                       w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr,
-                                       out_plane ^ 1)
-                          : start_part(level + 1, nsegs, bins_in, lab_in, w_in, out_plane);
-    }
-    tick("part_launch");
+    // the next level's a7 is already running (launched behind the winner kernel)
+    if (ndirect > 0 && !early.launched)
+      throw Error(ADAPT_E_CUDA, "internal: frontier continues without a partition");
+    pending = early;
     // one pass over a node's compact classes: n, S = sum c^2 and the majority
     // class (ties -> lowest, R12) of the node, of its left part and of its
     // right part, and the children's class sets
     std::vector<uint64_t> P(C), PL(C), PR(C);
+    std::vector<int2> kids(A, make_int2(-1, -1));  // frontier children of node j (-1: leaf / none)
     for (int j = 0; j < A; j++) {
       const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + res_off[j]);
       const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);  // compact columns
@@ -1813,9 +1871,10 @@ void train_region(adapt_region *h, cudaStream_t s) {
         dv.cls_p = fn.cls;
         nderived.push_back(dv);
       }
-      for (int q = pc_start[j]; q < pc_start[j + 1]; q++)  // the children of each piece (pass 1's segments)
-        nchildren.push_back(make_int2(jl, jr));
+      kids[j] = make_int2(jl, jr);
     }
+    for (int j = 0; j < A; j++)  // the children of each early-partition segment (all pieces)
+      for (int q = pc_start[j]; q < pc_start[j + 1]; q++) nchildren.push_back(kids[j]);
     // derived slots follow the direct ones
     for (size_t i = 0; i < nderived.size(); i++) next[nderived[i].j].slot = ndirect + (int)i;
     tick("pass2");
@@ -1831,7 +1890,6 @@ void train_region(adapt_region *h, cudaStream_t s) {
               level ? tr[1] - tr[0] : 0.0, tr[6] - tr[0], t_mv - tr[6], level ? tr[2] - tr[1] : 0.0, level ? tr[3] - tr[2] : 0.0,
               tr[4] - tr[3], tr[5] - tr[4], now_us() - tr[5]);
     frontier.swap(next);
-    psegs.swap(nsegs);
     pseg_children.swap(nchildren);
     ndirect_slots = ndirect;
     derived.swap(nderived);

@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition_kernel
     const int s_first = s;
     for (; s < a.nseg && a.segs[s].row_base < pe; s++) {
       const Seg sg = a.segs[s];
+      if (!sg.write) continue;  // a parent that does not split (or whose children are leaves)
       const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
       const uint32_t q1 = min(sg.len, pe - sg.row_base);
       // rows in flight: kPartUnroll per thread, loaded one batch ahead of the
@@ -464,7 +465,49 @@ __global__ void __launch_bounds__(256) hist_flat_kernel(HistArgs a) {
   }
 }
 
+// The next partition's decisions on the device, straight from the winner
+// records (so it launches right behind the winner kernel, without a host round
+// trip): per segment (a piece of frontier node j = seg.direct), the split
+// feature / rank and which children stay in the frontier, by the rule the host
+// applies to the same records (engine.cpp decide, R10 / R11): a node splits
+// when depth < D, it has a cut, and more than one class is present; a child
+// stays when depth + 1 < D and it holds more than one class.
+__global__ void __launch_bounds__(256) decide_segs_kernel(Seg *segs, int nseg, const uint8_t *res,
+                                                          const int64_t *rec_off, const int32_t *node_kc,
+                                                          const int32_t *node_depth, int D) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nseg) return;
+  Seg &sg = segs[i];
+  const int j = sg.direct;
+  const NodeRes *nr = reinterpret_cast<const NodeRes *>(res + rec_off[j]);
+  const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);
+  const int kc = node_kc[j];
+  const uint32_t *cLd = Pd + kc;
+  int np = 0, npl = 0, npr = 0;
+  for (int k = 0; k < kc; k++) {
+    const uint32_t p = Pd[k], l = cLd[k];
+    np += p > 0;
+    npl += l > 0;
+    npr += p - l > 0;
+  }
+  const int depth = node_depth[j];
+  int write = 0;
+  if (depth < D && np > 1 && nr->valid) {
+    write = (depth + 1 < D && npl > 1 ? 1 : 0) | (depth + 1 < D && npr > 1 ? 2 : 0);
+    sg.feat = nr->feat;
+    sg.thr = nr->b_lo;
+  }
+  sg.write = write;
+}
+
 }  // namespace
+
+void launch_decide_segs(Seg *segs, int nseg, const uint8_t *res, const int64_t *rec_off,
+                        const int32_t *node_kc, const int32_t *node_depth, int D, cudaStream_t s) {
+  if (nseg == 0) return;
+  decide_segs_kernel<<<(nseg + 255) / 256, 256, 0, s>>>(segs, nseg, res, rec_off, node_kc, node_depth, D);
+  CUDA_CHECK(cudaGetLastError());
+}
 
 void ensure_smem_limit(const void *func, size_t bytes) {
   // cudaFuncSetAttribute applies per device: cache per (device, function)
