@@ -256,6 +256,9 @@ struct LabelBinArgs {
   size_t pstride;           // bytes between bins word planes
 };
 
+// VQ / FQ: float4 chunks of times / features per lane when known at compile
+// time (the common shapes; 0 = runtime loops): fully unrolled, constant offsets
+template <int VQ, int FQ>
 __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int F = a.F, V = a.V, BS = a.BS, TR = a.TR, P = a.P;
@@ -345,7 +348,7 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
       const float *tr = tT + (size_t)r * V;
       if (vec_t) {
         const float4 *t4 = reinterpret_cast<const float4 *>(tr);
-        for (int c = q; c < (V >> 2); c += P) {
+        auto chunk = [&](int c) {
           const float4 x = t4[c];
           nan |= (x.x != x.x) | (x.y != x.y) | (x.z != x.z) | (x.w != x.w);
           // ascending index within this lane: strict '<' keeps the lowest
@@ -353,6 +356,12 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
           if (x.y < best) { best = x.y; bi = 4 * c + 1; }
           if (x.z < best) { best = x.z; bi = 4 * c + 2; }
           if (x.w < best) { best = x.w; bi = 4 * c + 3; }
+        };
+        if constexpr (VQ > 0) {
+#pragma unroll
+          for (int i = 0; i < VQ; i++) chunk(q + i * P);
+        } else {
+          for (int c = q; c < (V >> 2); c += P) chunk(c);
         }
       } else {
         for (int v = q; v < V; v += P) {
@@ -383,7 +392,8 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
       const float *fr = tF + (size_t)r * F;
       const int64_t row = row0 + r;
       if (vec_f) {
-        for (int c = 0; c < per; c += 4) {
+#pragma unroll
+        for (int c = 0; c < (FQ > 0 ? 4 * FQ : per); c += 4) {
           const int f = q * per + c;
           const float4 x = *reinterpret_cast<const float4 *>(fr + f);
           const int r0 = rank_of(f, canon_key(x.x, local_flags, kFlagBadFeature));
@@ -578,8 +588,15 @@ void launch_label_bin(const float *feat, const float *times, int64_t n, int F, i
   const size_t smem = table + (size_t)kStages * a.TR * (V + F) * 4;
   const int64_t ntiles = (n + a.TR - 1) / a.TR;
   const int grid = (int)std::min<int64_t>(ntiles, sm_count());
-  smem_limit(label_bin_kernel, smem);
-  label_bin_kernel<<<grid, kIngestThreads, smem, s>>>(a);
+  // compile-time chunk counts for C4's shape (V = 48, F = 16 at 4 lanes per row)
+  const bool c4 = a.P == 4 && V == 48 && F == 16;
+  if (c4) {
+    smem_limit(label_bin_kernel<3, 1>, smem);
+    label_bin_kernel<3, 1><<<grid, kIngestThreads, smem, s>>>(a);
+  } else {
+    smem_limit(label_bin_kernel<0, 0>, smem);
+    label_bin_kernel<0, 0><<<grid, kIngestThreads, smem, s>>>(a);
+  }
   CUDA_CHECK(cudaGetLastError());
 }
 
