@@ -120,7 +120,7 @@ __device__ __forceinline__ int first_seg(const Seg *segs, int nseg, uint32_t p) 
 #define ADAPT_HIST_UNROLL 8
 #endif
 #ifndef ADAPT_PART_THREADS
-#define ADAPT_PART_THREADS 512
+#define ADAPT_PART_THREADS 1024
 #endif
 constexpr int kPartThreads = ADAPT_PART_THREADS;
 constexpr int kPartMinBlocks = 1024 / ADAPT_PART_THREADS;  // 1024 threads per SM
