@@ -93,13 +93,17 @@ __device__ __forceinline__ int row_byte(const Row<BS> &r, int f) {
   return (int)((pick<Row<BS>::N>(r.w, f >> 2) >> (8 * (f & 3))) & 0xFFu);
 }
 
+// no "memory" clobber: the counters are read only after a __syncthreads, so
+// other loads (the class map) may move across the reductions
 __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
-  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
 }
 
+// (not volatile: the class-map lookups of a thread's rows may be hoisted ahead
+// of the reductions — the map is written before the node's rows are counted)
 __device__ __forceinline__ uint32_t ld_shared_u8(uint32_t addr) {
   uint32_t v;
-  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 
@@ -314,8 +318,9 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
     __syncthreads();
     // one row: its word w (4 features), label, weight -> up to 4 reductions
     const uint32_t cmap_base = smem_u32(s_cmap);
-    auto count = [&](uint32_t w, int label, uint32_t wv) {
-      const int lk = (int)ld_shared_u8(cmap_base + label) - k0;
+    // a row's compact class column in this CTA's slab (kn or more: skip)
+    auto column = [&](int label) { return (int)ld_shared_u8(cmap_base + label) - k0; };
+    auto count_col = [&](uint32_t w, int lk, uint32_t wv) {
       if ((unsigned)lk >= (unsigned)kn) return;  // another CTA's class slab (or padding)
       const uint32_t lk4 = 4u * lk;
       if (all4) {
@@ -330,6 +335,7 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
             red_shared_add(abase[e] + ((w >> (8 * e)) & 0xFF) * kwp4 + lk4, wv);
       }
     };
+    auto count = [&](uint32_t w, int label, uint32_t wv) { count_col(w, column(label), wv); };
     auto load_word = [&](uint32_t row) -> uint32_t {
       if constexpr (BS >= 4)
         return *reinterpret_cast<const uint32_t *>(a.bins_in + w0 * a.pstride + (size_t)row * 4);
@@ -374,12 +380,17 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
               if constexpr (WEIGHTED) v[u] = __ldcs(vq + qi);
             }
           }
+          int lk[QU][4];  // every class-map lookup first (independent), then the reductions
+#pragma unroll
+          for (int u = 0; u < QU; u++)
+#pragma unroll
+            for (int c = 0; c < 4; c++) lk[u][c] = column((l[u] >> (8 * c)) & 0xFF);
 #pragma unroll
           for (int u = 0; u < QU; u++) {
-            count(w[u].x, l[u] & 0xFF, WEIGHTED ? (v[u] & 0xFF) : 1u);
-            count(w[u].y, (l[u] >> 8) & 0xFF, WEIGHTED ? ((v[u] >> 8) & 0xFF) : 1u);
-            count(w[u].z, (l[u] >> 16) & 0xFF, WEIGHTED ? ((v[u] >> 16) & 0xFF) : 1u);
-            count(w[u].w, l[u] >> 24, WEIGHTED ? (v[u] >> 24) : 1u);
+            count_col(w[u].x, lk[u][0], WEIGHTED ? (v[u] & 0xFF) : 1u);
+            count_col(w[u].y, lk[u][1], WEIGHTED ? ((v[u] >> 8) & 0xFF) : 1u);
+            count_col(w[u].z, lk[u][2], WEIGHTED ? ((v[u] >> 16) & 0xFF) : 1u);
+            count_col(w[u].w, lk[u][3], WEIGHTED ? (v[u] >> 24) : 1u);
           }
         }
       } else {
