@@ -153,6 +153,11 @@ void launch_decide_segs(Seg *segs, int nseg, const uint8_t *res, const int64_t *
 // (ascending class ids) is a [DS][kc_j] u32 matrix, DS = sum_f D_f; feature f's
 // rows are [cumD_f, cumD_f + D_f), row = rank, column = compact class index.
 // A level's nodes are concatenated: node j at element offset off_j.
+struct HistCta {             // one histogram CTA's work: group g, virtual rows [p0, p1)
+  int32_t g;                 // from segment s0 on (the segment holding p0)
+  uint32_t p0, p1;
+  int32_t s0;
+};
 struct HistArgs {            // a4: class histograms of the given pieces' rows
   const Seg *segs;           // pieces (off, len, row_base, node_base/len, hslot, cmap, ncls), grouped by node
   int nseg;
@@ -169,7 +174,8 @@ struct HistArgs {            // a4: class histograms of the given pieces' rows
   int smem_counters;         // max counters of a group
   uint32_t *H;               // level histograms
   const int64_t *soff;       // [slots] element offset of a slot's matrix in H
-  int nranges;               // CTA groups; CTA x handles range x / ngroups, group x % ngroups
+  const HistCta *ctas;       // [nctas] per-CTA work (cost-balanced on the host)
+  int nctas;
 };
 void launch_hist(const HistArgs &a, cudaStream_t s);
 void launch_hist_flat(const HistArgs &a, cudaStream_t s);  // small nodes: thread per row

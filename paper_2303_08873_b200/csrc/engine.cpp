@@ -408,6 +408,133 @@ struct ClassSet {  // classes present in a node (C <= 255), ascending = compact 
   }
 };
 
+// a4 work split over the histogram CTAs (one per SM).  Cost model, measured on
+// B200 with per-CTA timers at C4 (DESIGN.md §6 "histogram CTA balance"): a row
+// costs row_ns of its group (its word's shared-memory reductions), a node
+// portion kNodeNs (three block barriers and the pipeline refill) plus kCtrNs per
+// counter it zeroes and flushes.  CTAs go to the groups in proportion to their
+// total cost; within a group the virtual rows are cut at equal cost, a node
+// split only where the piece carries enough rows to pay its own overhead.
+constexpr double kNodeNs = 1100.0, kCtrNs = 0.17;
+struct HistGroupCost {
+  double row_ns;  // per counted row (all classes of the node in this slab)
+  int k0, kw, dsw;  // class slab and the word's distinct values (counters = dsw * (kn | 1))
+};
+std::vector<HistCta> plan_hist_ctas(const std::vector<Seg> &segs, uint32_t total,
+                                    const std::vector<HistGroupCost> &gc, int nct) {
+  std::vector<HistCta> out;
+  const int G = (int)gc.size();
+  if (!total || segs.empty() || G == 0) return out;
+  struct N {
+    int fs, ls;  // segments [fs, ls)
+    uint32_t base, len;
+    int kc;
+  };
+  std::vector<N> nodes;
+  for (int i = 0; i < (int)segs.size();) {
+    int k = i;
+    while (k < (int)segs.size() && segs[k].hslot == segs[i].hslot) k++;
+    nodes.push_back(N{i, k, segs[i].node_base, segs[i].node_len, segs[i].ncls});
+    i = k;
+  }
+  auto kn_of = [&](const HistGroupCost &c, int kc) { return std::min(c.kw, kc - c.k0); };
+  auto row_of = [&](const HistGroupCost &c, int kc) {  // rows of other slabs are only loaded
+    return c.row_ns * (0.3 + 0.7 * (double)std::max(0, kn_of(c, kc)) / std::max(1, kc));
+  };
+  auto ovh = [&](const HistGroupCost &c, int kc) {
+    const int kn = kn_of(c, kc);
+    return kn > 0 ? kNodeNs + kCtrNs * (double)c.dsw * (kn | 1) : 0.0;
+  };
+  std::vector<double> T(G, 0.0);
+  double sum = 0;
+  for (int g = 0; g < G; g++) {
+    for (const auto &n : nodes)
+      if (kn_of(gc[g], n.kc) > 0) T[g] += ovh(gc[g], n.kc) + n.len * row_of(gc[g], n.kc);
+    sum += T[g];
+  }
+  // CTAs per group: proportional to cost, at least one for a group with work
+  nct = std::max(nct, G);
+  std::vector<int> ng(G, 0);
+  int used = 0;
+  for (int g = 0; g < G; g++)
+    if (T[g] > 0) used += ng[g] = std::max(1, (int)std::lround(nct * T[g] / sum));
+  while (used > nct) {  // rounding overshoot: trim the group with the cheapest CTAs
+    int b = -1;
+    for (int g = 0; g < G; g++)
+      if (ng[g] > 1 && (b < 0 || T[g] / ng[g] < T[b] / ng[b])) b = g;
+    if (b < 0) break;
+    ng[b]--, used--;
+  }
+  auto seg_at = [&](const N &n, uint32_t p) {
+    int k = n.fs;
+    while (k + 1 < n.ls && segs[k + 1].row_base <= p) k++;
+    return k;
+  };
+  // one group's greedy cut at `target` cost per CTA; returns the overhead the
+  // node splits added (each extra piece of a node pays its zero/flush again)
+  auto walk = [&](int g, double target, std::vector<HistCta> *emit) {
+    int made = 0;
+    double acc = 0, extra = 0;
+    uint32_t start = 0;
+    int s_start = 0;
+    bool open = false;  // the current CTA holds rows
+    auto close = [&](uint32_t end, int s_next, uint32_t next) {
+      if (end > start) {
+        if (emit) emit->push_back(HistCta{g, start, end, s_start});
+        made++;
+      }
+      start = next;
+      s_start = s_next;
+      acc = 0;
+      open = false;
+    };
+    for (const auto &n : nodes) {
+      const int kn = kn_of(gc[g], n.kc);
+      if (kn <= 0) continue;
+      const double O = ovh(gc[g], n.kc), r = row_of(gc[g], n.kc);
+      uint32_t pos = n.base, left = n.len;
+      if (!open) start = pos, s_start = n.fs;  // skip rows no CTA of g needs
+      open = true;
+      while (left > 0) {
+        if (made == ng[g] - 1) {  // the last CTA takes the rest
+          left = 0;
+          break;
+        }
+        const double all = O + left * r;
+        if (acc + all <= target) {
+          acc += all;
+          left = 0;
+          break;
+        }
+        const double room = target - acc - O;
+        const uint32_t take = room > 0 ? (uint32_t)std::min<double>(room / r, left) : 0u;
+        if (take >= 4096 && take < left) {  // split the node here
+          pos += take;
+          left -= take;
+          extra += O;
+          close(pos, emit ? seg_at(n, pos) : 0, pos);
+          open = true;
+        } else if (acc > 0) {  // the node starts the next CTA
+          close(pos, emit ? seg_at(n, pos) : 0, pos);
+          open = true;
+        } else {  // a fresh CTA that cannot split it usefully takes it whole
+          acc += all;
+          left = 0;
+        }
+      }
+    }
+    close(total, 0, total);
+    return extra;
+  };
+  for (int g = 0; g < G; g++) {
+    if (!ng[g]) continue;
+    double extra = 0;  // the target from the cost including the splits' overheads
+    for (int it = 0; it < 2; it++) extra = walk(g, (T[g] + extra) / ng[g], nullptr);
+    walk(g, (T[g] + extra) / ng[g], &out);
+  }
+  return out;
+}
+
 struct FNode {  // a frontier node: histogrammed and split-searched at this level
   int32_t tree_idx;
   int32_t depth;
@@ -1188,6 +1315,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
     }
   }
   const int ngroups = (int)gl.size();
+  std::vector<HistGroupCost> gcost;  // the CTA planner's cost model per group
+  for (auto &t : gl) {
+    double u = 0;  // ns per row: its reductions, cheaper for features with few values
+    for (int f = 4 * t.word; f < std::min(F, 4 * t.word + 4); f++)
+      u += 0.0422 + 0.0198 * std::min(h->nval[f], 64) / 64.0;
+    gcost.push_back(HistGroupCost{u, t.k0, t.kw, t.counters / t.kwp});
+  }
   int max_group = 0;
   std::vector<int4> groups;
   std::vector<int32_t> gsoff;
@@ -1591,7 +1725,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
     if (htotal + ftotal > 0) {
       Arena &sb = h->stage_b;
       sb.reset();
-      const size_t o_hsegs = sb.put(hsegs), o_fsegs = sb.put(fsegs);
+      // one CTA per SM, each reading only its own group's word plane (the CTAs
+      // of different groups share just the 1-byte labels and run unsynchronised)
+      const int nranges = (int)std::max<int64_t>(1, std::min<int64_t>((htotal + 4095) / 4096,
+                                                                      std::max(1, sms / ngroups)));
+      const std::vector<HistCta> ctas = plan_hist_ctas(hsegs, htotal, gcost, nranges * ngroups);
+      const size_t o_hsegs = sb.put(hsegs), o_fsegs = sb.put(fsegs), o_ctas = sb.put(ctas);
       sb.flush(s);
       HistArgs ha{};
       ha.segs = sb.ptr<Seg>(o_hsegs);
@@ -1612,11 +1751,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
       ha.smem_counters = max_group;
       ha.H = Hcur->as<uint32_t>();
       ha.soff = sa.ptr<int64_t>(o_soff);
-      // one CTA per SM; the ngroups CTAs of a range are co-resident (cooperative launch)
-      ha.nranges = (int)std::max<int64_t>(1, std::min<int64_t>((htotal + 4095) / 4096,
-                                                               std::max(1, sms / ngroups)));
-      // each CTA reads only its own word plane, so partner CTAs share just the
-      // 1-byte labels: they run unsynchronised
+      ha.ctas = sb.ptr<HistCta>(o_ctas);
+      ha.nctas = (int)ctas.size();
       snprintf(nm, sizeof nm, "hist_L%02d", level);
       Phase ph(per_level ? nm : "hist", s, (double)(htotal + ftotal) * (F + 1));
       tick("hist_args");

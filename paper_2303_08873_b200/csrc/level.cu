@@ -238,19 +238,17 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
   extern __shared__ uint32_t sh[];  // [smem_counters] counters
   __shared__ uint8_t s_cmap[kMaxC + 1];  // this node: class -> compact index (255: absent)
   const int tid = threadIdx.x;
-  const int G = a.ngroups;
-  const int g = blockIdx.x % G;
-  const int range = blockIdx.x / G;
+  const HistCta ct = a.ctas[blockIdx.x];
+  const int g = ct.g;
   const int4 grp = a.groups[g];  // x: first compact class, y: classes, w: bins word
   const int k0 = grp.x, kw = grp.y, w0 = grp.w;
   const int C = a.C;
   int Dw[4];  // distinct values of the 4 features of word w0 (0: absent)
 #pragma unroll
   for (int e = 0; e < 4; e++) Dw[e] = (4 * w0 + e < a.F) ? a.nval[4 * w0 + e] : 0;
-  const uint32_t R = (a.total_rows + a.nranges - 1) / a.nranges;
-  uint32_t p0 = range * R;
-  const uint32_t p1 = min(p0 + R, a.total_rows);
-  int s = p0 < p1 ? first_seg(a.segs, a.nseg, p0) : a.nseg;
+  uint32_t p0 = ct.p0;
+  const uint32_t p1 = ct.p1;
+  int s = p0 < p1 ? ct.s0 : a.nseg;
   const uint32_t sbase = smem_u32(sh);
   while (p0 < p1 && s < a.nseg) {
     // ---- one node's rows at virtual positions [p0, pe) ----
@@ -571,10 +569,10 @@ void launch_hist_flat(const HistArgs &a, cudaStream_t s) {
 }
 
 void launch_hist(const HistArgs &a, cudaStream_t s) {
-  if (a.total_rows == 0 || a.nseg == 0) return;
+  if (a.total_rows == 0 || a.nseg == 0 || a.nctas == 0) return;
   const size_t smem = (size_t)a.smem_counters * 4;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.nranges * a.ngroups);
+  cfg.gridDim = dim3(a.nctas);
   cfg.blockDim = dim3(kHistThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
