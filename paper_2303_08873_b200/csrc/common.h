@@ -10,6 +10,9 @@
 #include <string>
 
 namespace adapt {
+// every kernel this library launches bumps this (host side, under the library
+// lock): the profile's per-phase launch counts are differences of it
+extern long long g_kernel_launches;
 
 constexpr int kMaxF = 64;          // features per region (adapt.h)
 constexpr int kMaxC = 255;         // variants = classes (adapt.h)

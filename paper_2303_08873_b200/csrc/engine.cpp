@@ -154,6 +154,7 @@ struct Prof {
     int phase;
     cudaEvent_t a, b;
     double bytes;
+    long long kernels;  // kernels launched inside the phase
   };
   std::vector<std::string> names;
   std::vector<Rec> pending;
@@ -185,7 +186,7 @@ struct Prof {
       float ms = 0;
       CUDA_CHECK(cudaEventSynchronize(r.b));
       CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
-      acc[r.phase].launches += 1;
+      acc[r.phase].launches += r.kernels;
       acc[r.phase].ms += ms;
       acc[r.phase].bytes += r.bytes;
       pool.push_back(r.a);
@@ -195,6 +196,9 @@ struct Prof {
   }
 };
 Prof g_prof;
+}  // namespace
+long long g_kernel_launches = 0;
+namespace {
 
 // RAII: events around the kernel(s) launched in its scope, on `s`
 struct Phase {
@@ -202,17 +206,19 @@ struct Phase {
   cudaEvent_t a{}, b{};
   cudaStream_t s;
   double bytes;
+  long long k0 = 0;  // g_kernel_launches at the start
   Phase(const char *name, cudaStream_t st, double by) : s(st), bytes(by) {
     if (!g_prof.on) return;
     ph = g_prof.id(name);
     a = g_prof.ev();
     b = g_prof.ev();
+    k0 = g_kernel_launches;
     CUDA_CHECK(cudaEventRecord(a, s));
   }
   ~Phase() {
     if (ph < 0) return;
     cudaEventRecord(b, s);
-    g_prof.pending.push_back({ph, a, b, bytes});
+    g_prof.pending.push_back({ph, a, b, bytes, g_kernel_launches - k0});
   }
 };
 
@@ -415,7 +421,7 @@ struct ClassSet {  // classes present in a node (C <= 255), ascending = compact 
 // counter it zeroes and flushes.  CTAs go to the groups in proportion to their
 // total cost; within a group the virtual rows are cut at equal cost, a node
 // split only where the piece carries enough rows to pay its own overhead.
-constexpr double kNodeNs = 1100.0, kCtrNs = 0.17;
+constexpr double kNodeNs = 2200.0, kCtrNs = 0.13;
 struct HistGroupCost {
   double row_ns;  // per counted row (all classes of the node in this slab)
   int k0, kw, dsw;  // class slab and the word's distinct values (counters = dsw * (kn | 1))
@@ -458,6 +464,12 @@ std::vector<HistCta> plan_hist_ctas(const std::vector<Seg> &segs, uint32_t total
   int used = 0;
   for (int g = 0; g < G; g++)
     if (T[g] > 0) used += ng[g] = std::max(1, (int)std::lround(nct * T[g] / sum));
+  while (used < nct && used > 0) {  // rounding shortfall: the group with the dearest CTAs
+    int b = 0;
+    for (int g = 1; g < G; g++)
+      if (T[g] / std::max(ng[g], 1) > T[b] / std::max(ng[b], 1)) b = g;
+    ng[b]++, used++;
+  }
   while (used > nct) {  // rounding overshoot: trim the group with the cheapest CTAs
     int b = -1;
     for (int g = 0; g < G; g++)
@@ -1319,7 +1331,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
   for (auto &t : gl) {
     double u = 0;  // ns per row: its reductions, cheaper for features with few values
     for (int f = 4 * t.word; f < std::min(F, 4 * t.word + 4); f++)
-      u += 0.0422 + 0.0198 * std::min(h->nval[f], 64) / 64.0;
+      u += 0.0464 + 0.0218 * std::min(h->nval[f], 64) / 64.0;
     gcost.push_back(HistGroupCost{u, t.k0, t.kw, t.counters / t.kwp});
   }
   int max_group = 0;
@@ -1676,28 +1688,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
     // (decide_segs_kernel) — no host round trip between the winners and the move
     PartState early;
     std::vector<Seg> esegs;
-    if (level + 1 < D) {
-      esegs.reserve(pcs.size());
-      for (int j = 0; j < A; j++)
-        for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {
-          Seg sg{};
-          sg.off = pcs[q].first;
-          sg.len = pcs[q].second;
-          sg.feat = -1;
-          sg.direct = j;  // parent id (groups a parent's pieces); the decision fills the rest
-          sg.hslot = -1;
-          esegs.push_back(sg);
-        }
-      early = level > 0
-                  ? start_part(level + 1, esegs, (out_plane ? h->binsB : h->binsA).as<uint8_t>(),
-                               (out_plane ? h->labB : h->labA).as<uint8_t>(),
-                               w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr, out_plane ^ 1, true)
-                  : start_part(level + 1, esegs, bins_in, lab_in, w_in, out_plane, true);
-    }
     auto launch_early = [&](const uint8_t *res_dev) {
       if (esegs.empty()) return;
-      launch_decide_segs(const_cast<Seg *>(early.pa.segs), (int)esegs.size(), res_dev, sa.ptr<int64_t>(o_roff),
-                         sa.ptr<int32_t>(o_nkc), sa.ptr<int32_t>(o_ndep), D, s);
+      {
+        Phase ph("decide", s, 0);
+        launch_decide_segs(const_cast<Seg *>(early.pa.segs), (int)esegs.size(), res_dev, sa.ptr<int64_t>(o_roff),
+                           sa.ptr<int32_t>(o_nkc), sa.ptr<int32_t>(o_ndep), D, s);
+      }
       launch_part(early);
     };
     // ---- a4: histograms of the direct nodes (the root, or the smaller children) ----
@@ -1764,6 +1761,26 @@ void train_region(adapt_region *h, cudaStream_t s) {
       fa.total_rows = ftotal;
       launch_hist_flat(fa, s);
       tick("launch_flat");
+    }
+    // (prepared after the histogram launch: the GPU idles from the partition's
+    // end until then, and the early partition is only needed behind the winners)
+    if (level + 1 < D) {
+      esegs.reserve(pcs.size());
+      for (int j = 0; j < A; j++)
+        for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {
+          Seg sg{};
+          sg.off = pcs[q].first;
+          sg.len = pcs[q].second;
+          sg.feat = -1;
+          sg.direct = j;  // parent id (groups a parent's pieces); the decision fills the rest
+          sg.hslot = -1;
+          esegs.push_back(sg);
+        }
+      early = level > 0
+                  ? start_part(level + 1, esegs, (out_plane ? h->binsB : h->binsA).as<uint8_t>(),
+                               (out_plane ? h->labB : h->labA).as<uint8_t>(),
+                               w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr, out_plane ^ 1, true)
+                  : start_part(level + 1, esegs, bins_in, lab_in, w_in, out_plane, true);
     }
     if (!rs && collectives_on() && ndirect_slots > 0)  // the direct slots are contiguous at the front
       comm_allreduce_sum(Hcur->p, (size_t)soff[ndirect_slots], false, s, "allreduce histograms");
@@ -2260,6 +2277,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
 
   if (h->kind == 0) {
     grow_tree(nullptr);
+    if (trace) tr[7] = now_us();
     h->forest.clear();
   } else {  // random forest: T trees on bootstrap resamples of the global table (R19)
     const uint64_t lo = shard_lo();
@@ -2290,6 +2308,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
   h->trained = true;
   upload_tree(h, s);
   if (h->kind == 1) upload_forest(h, s);
+  if (trace && h->kind == 0) fprintf(stderr, "[adapt] finalize: last level's decide -> upload_tree done %.0f us\n", now_us() - tr[7]);
 }
 
 int walk_tree(const std::vector<adapt_node_t> &tr, const float *x) {

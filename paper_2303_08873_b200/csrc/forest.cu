@@ -214,10 +214,10 @@ void launch_bootstrap(uint64_t seed, int tree, uint64_t n_total, uint64_t lo, in
   if (n_total > 0 && n_local > 0) {
     const int grid = (int)std::min<uint64_t>((n_total + 255) / 256, (uint64_t)8 * sms);
     boot_count_kernel<<<grid, 256, 0, s>>>(key, n_total, lo, (uint64_t)n_local,
-                                           reinterpret_cast<uint32_t *>(w), sums);
+                                           reinterpret_cast<uint32_t *>(w), sums); ++g_kernel_launches;
     CUDA_CHECK(cudaGetLastError());
     const int g2 = (int)std::min<int64_t>((words + 255) / 256, (int64_t)8 * sms);
-    boot_sum_kernel<<<g2, 256, 0, s>>>(reinterpret_cast<const uint32_t *>(w), words, sums + 1);
+    boot_sum_kernel<<<g2, 256, 0, s>>>(reinterpret_cast<const uint32_t *>(w), words, sums + 1); ++g_kernel_launches;
     CUDA_CHECK(cudaGetLastError());
   }
 }
@@ -237,7 +237,7 @@ void launch_select_forest(const DNode *nodes, int n_nodes, const int32_t *roots,
 #define CASE(FF)                                                                                  \
   case FF:                                                                                        \
     smem_limit(select_forest_d<FF>, smem);                                                        \
-    select_forest_d<FF><<<grid, kForestDThreads, smem, s>>>(nodes, n_nodes, roots, T, X, m, wide, out); \
+    select_forest_d<FF><<<grid, kForestDThreads, smem, s>>>(nodes, n_nodes, roots, T, X, m, wide, out); ++g_kernel_launches; \
     break;
       CASE(4) CASE(8) CASE(12) CASE(16)
 #undef CASE
@@ -251,7 +251,7 @@ void launch_select_forest(const DNode *nodes, int n_nodes, const int32_t *roots,
   smem_limit(select_forest_kernel, smem);
   const int64_t tiles = (m + 31) / 32;
   const int grid = (int)std::min<int64_t>((tiles + W - 1) / W, 2 * sm_count());
-  select_forest_kernel<<<grid, kForestThreads, smem, s>>>(nodes, n_nodes, roots, T, X, m, F, out);
+  select_forest_kernel<<<grid, kForestThreads, smem, s>>>(nodes, n_nodes, roots, T, X, m, F, out); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 

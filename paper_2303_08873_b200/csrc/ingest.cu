@@ -535,13 +535,13 @@ void launch_discover(const float *feat, int64_t n, int F, uint32_t *gkey, uint32
   smem_limit(discover_kernel, smem);
   const int grid = grid_for(n * F / 4 + 1, kDiscThreads * 4, sm_count() * 2);
   discover_kernel<<<grid, kDiscThreads, smem, s>>>(feat, n, F, log2nb, gkey, gcount, flags,
-                                                   chunk_rows > 0 ? chunk_rows : n + 1, gap_rows);
+                                                   chunk_rows > 0 ? chunk_rows : n + 1, gap_rows); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_collect_values(const uint32_t *gkey, const uint32_t *gcount, int F, float *local_vals,
                            int32_t *local_cnt, cudaStream_t s) {
-  collect_values_kernel<<<F, 256, 0, s>>>(gkey, gcount, local_vals, local_cnt);
+  collect_values_kernel<<<F, 256, 0, s>>>(gkey, gcount, local_vals, local_cnt); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -549,7 +549,7 @@ void launch_merge_values(const float *all_vals, const int32_t *all_cnt, int worl
                          float *val, int32_t *nval, uint32_t *flags, cudaStream_t s) {
   const size_t smem = (size_t)world * kMaxBins * 5;
   smem_limit(merge_values_kernel, smem);
-  merge_values_kernel<<<F, 1024, smem, s>>>(all_vals, all_cnt, world, F, val, nval, flags);
+  merge_values_kernel<<<F, 1024, smem, s>>>(all_vals, all_cnt, world, F, val, nval, flags); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -592,10 +592,10 @@ void launch_label_bin(const float *feat, const float *times, int64_t n, int F, i
   const bool c4 = a.P == 4 && V == 48 && F == 16;
   if (c4) {
     smem_limit(label_bin_kernel<3, 1>, smem);
-    label_bin_kernel<3, 1><<<grid, kIngestThreads, smem, s>>>(a);
+    label_bin_kernel<3, 1><<<grid, kIngestThreads, smem, s>>>(a); ++g_kernel_launches;
   } else {
     smem_limit(label_bin_kernel<0, 0>, smem);
-    label_bin_kernel<0, 0><<<grid, kIngestThreads, smem, s>>>(a);
+    label_bin_kernel<0, 0><<<grid, kIngestThreads, smem, s>>>(a); ++g_kernel_launches;
   }
   CUDA_CHECK(cudaGetLastError());
 }
@@ -603,7 +603,7 @@ void launch_label_bin(const float *feat, const float *times, int64_t n, int F, i
 void launch_bins_out(const uint8_t *bins, size_t pstride, int64_t n, int F, int BS, uint8_t *out,
                      cudaStream_t s) {
   if (n == 0) return;
-  bins_out_kernel<<<grid_for(n * F, 256, 148 * 16), 256, 0, s>>>(bins, pstride, n, F, BS, out);
+  bins_out_kernel<<<grid_for(n * F, 256, 148 * 16), 256, 0, s>>>(bins, pstride, n, F, BS, out); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 

@@ -199,7 +199,7 @@ void launch_kfold_groups(uint64_t seed, int shuffle, uint64_t N, const uint64_t 
   int h = 1;
   while (h < 31 && (1ull << (2 * h)) < N) h++;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
-  kfold_group_kernel<<<grid, 256, 0, s>>>(kfold_key(seed, shuffle), N, h, d_bnd, K, lo, n, grp, cnt);
+  kfold_group_kernel<<<grid, 256, 0, s>>>(kfold_key(seed, shuffle), N, h, d_bnd, K, lo, n, grp, cnt); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -210,7 +210,7 @@ void launch_kfold_scatter(const uint8_t *bins, size_t pstride_in, const uint8_t 
   const int planes = BS < 4 ? 1 : BS / 4, wb = BS < 4 ? BS : 4;
   const int grid = (int)std::min<int64_t>((n * sb + 255) / 256, (int64_t)sm_count() * 8);
   kfold_scatter_kernel<<<grid, 256, 0, s>>>(bins, pstride_in, lab, n, planes, wb, grp, sb, K, cursor, obins,
-                                            pstride_out, olab);
+                                            pstride_out, olab); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -220,7 +220,7 @@ void launch_kfold_eval_many(const float *X, int64_t n, int F, int V, const float
   const size_t smem = (size_t)sb * K * sizeof(KfoldPartial);
   smem_limit(kfold_eval_many_kernel, smem);
   kfold_eval_many_kernel<<<kfold_eval_blocks(), kEvalManyThreads, smem, s>>>(X, n, F, V, times, lab, grp, sb,
-                                                                              K, m, nodes, roots, part);
+                                                                              K, m, nodes, roots, part); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 

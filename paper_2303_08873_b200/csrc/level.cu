@@ -420,26 +420,26 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
        // owns its columns: plain stores of every counter, no atomics.
       const bool sole = p0 <= first.node_base && pe >= first.node_base + first.node_len;
       uint32_t *dst = a.H + a.soff[first.hslot];
-      // flat over the counters; row = i / width by a float reciprocal (exact:
-      // i < 2^16, width <= 255 keeps (i + 0.5) / width >= 1/510 from an integer)
+      // the word's features are consecutive rows of both layouts (smem stride
+      // kwp, global stride kcn), so the flush is ONE flat pass over Rt rows;
+      // each thread steps its (row, column) by the block size without dividing
+      const int Rt = Dw[0] + Dw[1] + Dw[2] + Dw[3];
+      uint32_t *df = dst + (int64_t)a.cumD[4 * w0] * kcn + k0;
       const int width = sole ? kn : kwp;
-      const float inv = 1.0f / (float)width;
-      int o = 0;
-      for (int e = 0; e < 4; e++) {
-        if (!Dw[e]) continue;
-        uint32_t *df = dst + (int64_t)a.cumD[4 * w0 + e] * kcn + k0;
-        const uint32_t *src = sh + o;
-        const int n = Dw[e] * width;
-        for (int i = tid; i < n; i += blockDim.x) {
-          const int rk = __float2int_rz(((float)i + 0.5f) * inv), j = i - rk * width;
-          if (sole) {  // dense [rank][kn] block of this CTA's columns
-            df[rk * kcn + j] = src[rk * kwp + j];
-          } else {
-            const uint32_t val = src[i];
-            if (val) atomicAdd(df + rk * kcn + j, val);
-          }
+      const int n = Rt * width;
+      const int qs = (int)blockDim.x / width, rs = (int)blockDim.x - qs * width;
+      int rk = tid / width, j = tid - rk * width;
+#pragma unroll 4
+      for (int i = tid; i < n; i += blockDim.x) {
+        if (sole) {  // dense [rank][kn] block of this CTA's columns
+          df[rk * kcn + j] = sh[rk * kwp + j];
+        } else {
+          const uint32_t val = sh[i];
+          if (val) atomicAdd(df + rk * kcn + j, val);
         }
-        o += Dw[e] * kwp;
+        rk += qs;
+        j += rs;
+        if (j >= width) j -= width, rk++;
       }
     }
     __syncthreads();
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(256) decide_segs_kernel(Seg *segs, int nseg, c
 void launch_decide_segs(Seg *segs, int nseg, const uint8_t *res, const int64_t *rec_off,
                         const int32_t *node_kc, const int32_t *node_depth, int D, cudaStream_t s) {
   if (nseg == 0) return;
-  decide_segs_kernel<<<(nseg + 255) / 256, 256, 0, s>>>(segs, nseg, res, rec_off, node_kc, node_depth, D);
+  decide_segs_kernel<<<(nseg + 255) / 256, 256, 0, s>>>(segs, nseg, res, rec_off, node_kc, node_depth, D); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -539,7 +539,7 @@ void launch_partition(const PartArgs &a, cudaStream_t s) {
   switch (a.BS) {
 #define CASE(B)                                                                               \
   case B:                                                                                     \
-    partition_kernel<B><<<a.nranges, kPartThreads, 0, s>>>(a);                                \
+    partition_kernel<B><<<a.nranges, kPartThreads, 0, s>>>(a); ++g_kernel_launches;                                \
     break;
     CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
 #undef CASE
@@ -558,7 +558,7 @@ void launch_hist_flat(const HistArgs &a, cudaStream_t s) {
   switch (a.BS) {
 #define CASE(B)                                                 \
   case B:                                                       \
-    hist_flat_kernel<B><<<grid, 256, 0, s>>>(a);                \
+    hist_flat_kernel<B><<<grid, 256, 0, s>>>(a); ++g_kernel_launches;                \
     break;
     CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
 #undef CASE
@@ -582,10 +582,10 @@ void launch_hist(const HistArgs &a, cudaStream_t s) {
   case B:                                                                                    \
     if (a.w_in) {                                                                            \
       smem_limit(hist_kernel<B, true>, smem);                                                \
-      CUDA_CHECK(cudaLaunchKernelEx(&cfg, hist_kernel<B, true>, a));                         \
+      CUDA_CHECK(cudaLaunchKernelEx(&cfg, hist_kernel<B, true>, a)); ++g_kernel_launches;                         \
     } else {                                                                                 \
       smem_limit(hist_kernel<B, false>, smem);                                               \
-      CUDA_CHECK(cudaLaunchKernelEx(&cfg, hist_kernel<B, false>, a));                        \
+      CUDA_CHECK(cudaLaunchKernelEx(&cfg, hist_kernel<B, false>, a)); ++g_kernel_launches;                        \
     }                                                                                        \
     break;
     CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)

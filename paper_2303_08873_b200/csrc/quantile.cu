@@ -93,7 +93,7 @@ size_t sort_unique_temp_bytes(int64_t n) {
 
 void launch_column_keys(const float *X, int64_t n, int F, int f, uint32_t *keys, cudaStream_t s) {
   if (n == 0) return;
-  column_keys_kernel<<<grid_for(n), 256, 0, s>>>(X, n, F, f, keys);
+  column_keys_kernel<<<grid_for(n), 256, 0, s>>>(X, n, F, f, keys); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -108,7 +108,7 @@ void sort_unique_keys(const uint32_t *keys, int64_t n, uint32_t *sorted, uint32_
 }
 
 void launch_edges(const uint32_t *ukeys, int64_t D, float *lb, float *prev, cudaStream_t s) {
-  edges_kernel<<<1, kMaxBins, 0, s>>>(ukeys, D, lb, prev);
+  edges_kernel<<<1, kMaxBins, 0, s>>>(ukeys, D, lb, prev); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -117,7 +117,7 @@ void launch_quantize(const float *X, int64_t n, int F, uint64_t qmask, const flo
   if (n == 0) return;
   const size_t smem = (size_t)F * kMaxBins * 4;
   smem_limit(quantize_kernel, smem);
-  quantize_kernel<<<grid_for(n * F), 256, smem, s>>>(X, n, F, qmask, lb, Xq);
+  quantize_kernel<<<grid_for(n * F), 256, smem, s>>>(X, n, F, qmask, lb, Xq); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 

@@ -222,14 +222,14 @@ void launch_rec_group(const float *feat, const int32_t *var, int64_t m, int F, i
   CUDA_CHECK(cudaMemsetAsync(slot_first, 0xFF, slots * 4, s));
   rec_group_kernel<<<grid_for(m, 256), 256, 0, s>>>(feat, var, (uint32_t)m, F, V,
                                                      (uint32_t)(slots - 1), slot_rep, slot_first,
-                                                     slot_of, flags);
+                                                     slot_of, flags); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
-  rec_head_kernel<<<grid_for(m, 256), 256, 0, s>>>(slot_of, slot_first, (uint32_t)m, flag);
+  rec_head_kernel<<<grid_for(m, 256), 256, 0, s>>>(slot_of, slot_first, (uint32_t)m, flag); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
   const int nb = rec_scan_blocks(m);
-  scan_block_sums_kernel<<<nb, kScanThreads, 0, s>>>(flag, (uint32_t)m, bsum);
+  scan_block_sums_kernel<<<nb, kScanThreads, 0, s>>>(flag, (uint32_t)m, bsum); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
-  scan_sums_kernel<<<1, kScanThreads, 0, s>>>(bsum, nb, d_groups);
+  scan_sums_kernel<<<1, kScanThreads, 0, s>>>(bsum, nb, d_groups); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -239,16 +239,16 @@ void launch_rec_wide(const float *feat, const int32_t *var, const uint64_t *ns, 
                      float *wide_feat, float *wide_times, uint32_t *pairs, cudaStream_t s) {
   const int nb = rec_scan_blocks(m);
   scan_apply_kernel<<<nb, kScanThreads, 0, s>>>(flag, (uint32_t)m, bsum, slot_of, slot_gid, feat,
-                                                 F, wide_feat);
+                                                 F, wide_feat); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
   CUDA_CHECK(cudaMemsetAsync(sum, 0, (size_t)groups * V * 8, s));
   CUDA_CHECK(cudaMemsetAsync(cnt, 0, (size_t)groups * V * 4, s));
   rec_sum_kernel<<<grid_for(m, 256), 256, 0, s>>>(var, ns, slot_of, slot_gid, (uint32_t)m, V, sum,
-                                                   cnt);
+                                                   cnt); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
   if (pairs) CUDA_CHECK(cudaMemsetAsync(pairs, 0, 4, s));
   rec_mean_kernel<<<grid_for(groups * V, 256), 256, 0, s>>>(sum, cnt, (size_t)groups * V,
-                                                            wide_times, pairs);
+                                                            wide_times, pairs); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 

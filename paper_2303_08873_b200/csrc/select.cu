@@ -239,12 +239,12 @@ void launch_select(const SelTree &tr, const float *X, int64_t m, int F, int32_t 
     if (n_nodes <= kTopNodes) {                                                                 \
       const size_t smem = tree_b + (size_t)kSelThreads * FF * 4;                                \
       smem_limit(select_kernel_c<FF>, smem);                                                    \
-      select_kernel_c<FF><<<g, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, wide, out);   \
+      select_kernel_c<FF><<<g, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, wide, out); ++g_kernel_launches;   \
     } else {                                                                                    \
       const size_t smem = ((size_t)1 << tr.td) * (sizeof(uint2) + 4);                           \
       smem_limit(select_kernel_h<FF>, smem);                                                    \
       select_kernel_h<FF><<<g, kSelThreads, smem, s>>>(tr.heap, tr.exits, tr.td, tr.blocks2, X, m, \
-                                                       wide, out);                              \
+                                                       wide, out); ++g_kernel_launches;                              \
     }                                                                                           \
     break;                                                                                      \
   }
@@ -255,7 +255,7 @@ void launch_select(const SelTree &tr, const float *X, int64_t m, int F, int32_t 
       const int64_t tiles = (m + kAnyThreads - 1) / kAnyThreads;
       const int grid = (int)std::min<int64_t>(tiles, sms);
       smem_limit(select_kernel_any, smem);
-      select_kernel_any<<<grid, kAnyThreads, smem, s>>>(tree, n_top, blocks, X, m, F, out);
+      select_kernel_any<<<grid, kAnyThreads, smem, s>>>(tree, n_top, blocks, X, m, F, out); ++g_kernel_launches;
     }
   }
   CUDA_CHECK(cudaGetLastError());

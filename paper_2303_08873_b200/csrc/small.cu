@@ -427,7 +427,7 @@ void launch_small_train(const float *X, const float *T, int n, int F, int V, int
   const size_t smem = sizeof(SmallShared);
   smem_limit(small_train_kernel, smem);
   CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(SmallOut), s));
-  small_train_kernel<<<1, kT, smem, s>>>(X, T, n, F, V, D, BS, pstride, bins, labels, out);
+  small_train_kernel<<<1, kT, smem, s>>>(X, T, n, F, V, D, BS, pstride, bins, labels, out); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 

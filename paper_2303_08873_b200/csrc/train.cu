@@ -506,14 +506,14 @@ int chunk_count(int64_t elems) { return (int)((elems + kChunk - 1) / kChunk); }
 void launch_zero_slots(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS,
                        const int32_t *cstart, int n, int nblocks, cudaStream_t s) {
   if (n == 0 || nblocks == 0) return;
-  zero_slots_kernel<<<nblocks, kChunkThreads, 0, s>>>(H, soff, skc, DS, cstart, n);
+  zero_slots_kernel<<<nblocks, kChunkThreads, 0, s>>>(H, soff, skc, DS, cstart, n); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t DS, const SubJob *jobs,
                      const int16_t *maps, const int32_t *cstart, int n, int nblocks, cudaStream_t s) {
   if (n == 0 || nblocks == 0) return;
-  subtract_kernel<<<nblocks, kChunkThreads, 0, s>>>(H, Hprev, DS, jobs, maps, cstart, n);
+  subtract_kernel<<<nblocks, kChunkThreads, 0, s>>>(H, Hprev, DS, jobs, maps, cstart, n); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -522,13 +522,13 @@ void launch_split(const uint32_t *H, const int64_t *node_off, const int32_t *nod
                   int F, const int32_t *cumD, const int32_t *nval, SplitCand *out, cudaStream_t s) {
   if (nbig > 0) {
     split_kernel<<<dim3(nbig, F), kSplitThreads, 0, s>>>(H, node_off, node_kc, big_nodes, F, cumD,
-                                                         nval, out);
+                                                         nval, out); ++g_kernel_launches;
     CUDA_CHECK(cudaGetLastError());
   }
   if (nsmall > 0) {
     const int njobs = nsmall * F;
     split_small_kernel<<<(njobs + kSmallWarps - 1) / kSmallWarps, kSmallWarps * 32, 0, s>>>(
-        H, node_off, node_kc, small_nodes, njobs, F, cumD, nval, out);
+        H, node_off, node_kc, small_nodes, njobs, F, cumD, nval, out); ++g_kernel_launches;
     CUDA_CHECK(cudaGetLastError());
   }
 }
@@ -540,7 +540,7 @@ void launch_winner(const uint32_t *H, const int64_t *node_off, const int32_t *no
                    uint8_t *res, const int64_t *res_off, cudaStream_t s) {
   if (nnodes == 0) return;
   winner_kernel<<<nnodes, 256, 0, s>>>(H, node_off, node_kc, F, C, cumD, nval, cand, res,
-                                       res_off);
+                                       res_off); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
