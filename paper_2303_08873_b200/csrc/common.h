@@ -152,6 +152,23 @@ void launch_partition(const PartArgs &a, cudaStream_t s);
 void launch_decide_segs(Seg *segs, int nseg, const uint8_t *res, const int64_t *rec_off,
                         const int32_t *node_kc, const int32_t *node_depth, int D, cudaStream_t s);
 
+// The histogram segments built on the device from the partition's share
+// reports (single-rank, unweighted levels: the host planned every node's size
+// and slot range from the winners, so nothing waits for the host between the
+// partition and the histogram).  Slot slot0 + b of a direct child holds its
+// piece from partition range b; row_base = exclusive prefix of the slots' len.
+struct SegBuildArgs {
+  const int32_t *visits;     // the partition's share reports [nranges][max_visits][6]
+  int nranges, max_visits;
+  const int4 *bseg;          // per partition segment: x side of the parent's direct
+                             // child (0 left, 1 right, -1 none), y list (0 big, 1 small), z slot0 - b0
+  Seg *segs[2];              // per list: slot templates (node fields set, len 0) -> filled
+  int nslot[2];
+  uint32_t total[2];         // planned rows per list
+  int32_t *err;              // set to 1 when the pieces disagree with the planned sizes
+};
+void launch_build_hist_segs(const SegBuildArgs &a, cudaStream_t s);
+
 // Node histograms are stored class-compacted: node j with kc_j present classes
 // (ascending class ids) is a [DS][kc_j] u32 matrix, DS = sum_f D_f; feature f's
 // rows are [cumD_f, cumD_f + D_f), row = rank, column = compact class index.

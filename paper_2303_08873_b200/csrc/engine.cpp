@@ -426,23 +426,30 @@ struct HistGroupCost {
   double row_ns;  // per counted row (all classes of the node in this slab)
   int k0, kw, dsw;  // class slab and the word's distinct values (counters = dsw * (kn | 1))
 };
+struct PlanNode {
+  int fs, ls;  // its segments [fs, ls) (fs = -1: not known yet, the kernel searches)
+  uint32_t base, len;
+  int kc;
+};
+std::vector<HistCta> plan_hist_ctas(const std::vector<PlanNode> &nodes, const std::vector<Seg> &segs,
+                                    uint32_t total, const std::vector<HistGroupCost> &gc, int nct);
 std::vector<HistCta> plan_hist_ctas(const std::vector<Seg> &segs, uint32_t total,
                                     const std::vector<HistGroupCost> &gc, int nct) {
-  std::vector<HistCta> out;
-  const int G = (int)gc.size();
-  if (!total || segs.empty() || G == 0) return out;
-  struct N {
-    int fs, ls;  // segments [fs, ls)
-    uint32_t base, len;
-    int kc;
-  };
-  std::vector<N> nodes;
+  std::vector<PlanNode> nodes;
   for (int i = 0; i < (int)segs.size();) {
     int k = i;
     while (k < (int)segs.size() && segs[k].hslot == segs[i].hslot) k++;
-    nodes.push_back(N{i, k, segs[i].node_base, segs[i].node_len, segs[i].ncls});
+    nodes.push_back(PlanNode{i, k, segs[i].node_base, segs[i].node_len, segs[i].ncls});
     i = k;
   }
+  return plan_hist_ctas(nodes, segs, total, gc, nct);
+}
+std::vector<HistCta> plan_hist_ctas(const std::vector<PlanNode> &nodes, const std::vector<Seg> &segs,
+                                    uint32_t total, const std::vector<HistGroupCost> &gc, int nct) {
+  std::vector<HistCta> out;
+  const int G = (int)gc.size();
+  if (!total || nodes.empty() || G == 0) return out;
+  using N = PlanNode;
   auto kn_of = [&](const HistGroupCost &c, int kc) { return std::min(c.kw, kc - c.k0); };
   auto row_of = [&](const HistGroupCost &c, int kc) {  // rows of other slabs are only loaded
     return c.row_ns * (0.3 + 0.7 * (double)std::max(0, kn_of(c, kc)) / std::max(1, kc));
@@ -478,6 +485,7 @@ std::vector<HistCta> plan_hist_ctas(const std::vector<Seg> &segs, uint32_t total
     ng[b]--, used--;
   }
   auto seg_at = [&](const N &n, uint32_t p) {
+    if (n.fs < 0) return -1;
     int k = n.fs;
     while (k + 1 < n.ls && segs[k + 1].row_base <= p) k++;
     return k;
@@ -553,6 +561,8 @@ struct FNode {  // a frontier node: histogrammed and split-searched at this leve
   int32_t slot;  // histogram slot at this level
   bool direct;   // histogrammed from its rows (else parent - sibling)
   ClassSet cls;  // classes present; the node's histogram columns
+  int64_t rows = -1;  // its rows (the parent's winner record; single rank, unweighted)
+  int32_t par = -1, side = 0;  // parent's index in the previous frontier, left (0) / right (1) child
 };
 
 }  // namespace
@@ -628,9 +638,13 @@ struct adapt_region {
                                                      // histogram segments, owner split lists
   cudaEvent_t sel_evt = nullptr;  // recorded after every device select (upload_tree waits)
   cudaEvent_t win_evt = nullptr;  // a level's winner records are on the host
+  cudaEvent_t vis_evt = nullptr;  // a partition's share reports are on the host
+  adapt::DevBuf dseg_err;  // the device-built histogram segments disagree with the plan
+  adapt::HostBuf hseg_err;
   ~adapt_region() {
     if (sel_evt) cudaEventDestroy(sel_evt);
     if (win_evt) cudaEventDestroy(win_evt);
+    if (vis_evt) cudaEventDestroy(vis_evt);
   }
   std::unordered_set<std::string> pair_set;  // distinct (features, variant) of the host records
   int64_t autotrain_failed_at = -1;          // pair count of the last failed auto-train
@@ -1453,6 +1467,11 @@ void train_region(adapt_region *h, cudaStream_t s) {
     int64_t rows_part = 0;
     int32_t *hv = nullptr;
     int lvl = 0;
+    // for segments built on the device: each partition segment's parent, each
+    // parent's virtual span, rows per partition range
+    std::vector<int32_t> seg_parent;
+    std::vector<uint32_t> pbase, plen;
+    uint32_t Rr = 1;
   };
   // the partition launch (and its share reports' D2H), on the stream
   auto launch_part = [&](PartState &st) {
@@ -1464,6 +1483,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
     h->hvis.grow(st.vbytes);
     st.hv = h->hvis.as<int32_t>();
     CUDA_CHECK(cudaMemcpyAsync(st.hv, h->visits.p, st.vbytes, cudaMemcpyDeviceToHost, s));
+    if (!h->vis_evt) CUDA_CHECK(cudaEventCreateWithFlags(&h->vis_evt, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventRecord(h->vis_evt, s));
     st.launched = true;
   };
   // upload a partition's segments and size its share reports; `defer`: the
@@ -1478,6 +1499,15 @@ void train_region(adapt_region *h, cudaStream_t s) {
     pa.total_rows = total;
     pa.nranges = partition_ranges(sms, total);
     const uint32_t Rr = (total + pa.nranges - 1) / std::max(1, pa.nranges);
+    st.Rr = std::max<uint32_t>(Rr, 1);
+    st.seg_parent.resize(segs.size());
+    for (size_t k = 0; k < segs.size(); k++) {
+      const int p = segs[k].direct;
+      st.seg_parent[k] = p;
+      if ((int)st.pbase.size() <= p) st.pbase.resize(p + 1, 0), st.plen.resize(p + 1, 0);
+      st.pbase[p] = segs[k].node_base;
+      st.plen[p] = segs[k].node_len;
+    }
     for (int r = 0, si = 0; r < pa.nranges && total; r++) {
       const uint32_t p0 = r * Rr, p1 = std::min<uint64_t>((uint64_t)p0 + Rr, total);
       while (si + 1 < pa.nseg && segs[si + 1].row_base <= p0) si++;
@@ -1644,17 +1674,26 @@ void train_region(adapt_region *h, cudaStream_t s) {
       launch_zero_slots(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_soff), sa.ptr<int32_t>(o_skc), DS,
                         sa.ptr<int32_t>(o_zst), ndirect_slots, zblocks, s);
     }
+    // histogram segments built on the device (single rank, unweighted: every
+    // direct node's size is its parent's winner count, so the histogram pass
+    // is queued behind the partition without waiting for its share reports)
+    static const bool host_segs = getenv("ADAPT_HOST_SEGS") != nullptr;
+    const bool dev = level > 0 && !w_root && g_ctx.world == 1 && !rs && !host_segs;
     if (level > 0) {
-      uint8_t *bo = pa.bins_out;
-      uint8_t *lo = pa.lab_out;
-      if (trace) tr[1] = now_us();
-      tick("tables_upload");
-      CUDA_CHECK(cudaStreamSynchronize(s));
+      hist_bins = pa.bins_out;
+      hist_lab = pa.lab_out;
+      hist_w = pa.w_out;
+    }
+    if (trace) tr[1] = now_us();
+    tick("tables_upload");
+    // this level's pieces, from the partition's share reports: ranges visit a
+    // parent at most once each and in range order, so every child's pieces come
+    // out in offset order; a counting sort by child groups them (CSR)
+    auto wait_pieces = [&]() {
+      if (level == 0) return;
+      CUDA_CHECK(cudaEventSynchronize(h->vis_evt));
       if (trace) tr[2] = now_us();
       tick("wait_part");
-      // children's pieces, from the CTAs' share reports: ranges visit a parent
-      // at most once each and in range order, so every child's pieces come out
-      // in offset order; a counting sort by child groups them (CSR)
       std::vector<int32_t> cnt(A + 1, 0);
       std::vector<std::array<uint32_t, 3>> flat;  // (child, offset, length)
       flat.reserve((size_t)2 * pa.nranges * max_visits);
@@ -1672,14 +1711,19 @@ void train_region(adapt_region *h, cudaStream_t s) {
       pc_start = cnt;
       pcs.assign(flat.size(), {0u, 0u});
       for (const auto &x : flat) pcs[cnt[x[0]]++] = {x[1], x[2]};
-      hist_bins = bo;
-      hist_lab = lo;
-      hist_w = pa.w_out;
-    }
-    if (level > 0) {  // rows that reached this level's nodes (the moved rows of split parents)
+      // rows that reached this level's nodes (the moved rows of split parents)
       rows_part = 0;
       for (const auto &pc : pcs) rows_part += pc.second;
-    }
+      if (dev)  // the device built the histogram segments from the planned sizes
+        for (int j = 0; j < A; j++) {
+          if (!frontier[j].direct) continue;
+          int64_t local = 0;
+          for (int q = pc_start[j]; q < pc_start[j + 1]; q++) local += pcs[q].second;
+          if (local != frontier[j].rows)
+            throw Error(ADAPT_E_CUDA, "internal: a node's moved rows differ from its winner count");
+        }
+    };
+    if (!dev) wait_pieces();
     if (trace) tr[3] = now_us();
     tick("pieces");
     // the next level's a7, prepared now and launched right behind this level's
@@ -1688,6 +1732,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     // (decide_segs_kernel) — no host round trip between the winners and the move
     PartState early;
     std::vector<Seg> esegs;
+    const uint8_t *early_res = nullptr;  // winner records on the device, for decide_segs
     auto launch_early = [&](const uint8_t *res_dev) {
       if (esegs.empty()) return;
       {
@@ -1699,25 +1744,59 @@ void train_region(adapt_region *h, cudaStream_t s) {
     };
     // ---- a4: histograms of the direct nodes (the root, or the smaller children) ----
     std::vector<Seg> hsegs, fsegs;  // big nodes: smem-privatised pass; small: flat pass
-    for (int j = 0; j < A; j++) {
-      const FNode &fn = frontier[j];
-      if (!fn.direct) continue;
-      int64_t local = 0;
-      for (int q = pc_start[j]; q < pc_start[j + 1]; q++) local += pcs[q].second;
-      const bool small = local * 16 < DS * (node_kc[j] | 1);
-      for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {
-        const auto &pc = pcs[q];
+    uint32_t htotal = 0, ftotal = 0;
+    std::vector<PlanNode> pnodes;  // dev: the big nodes' planned layout
+    std::vector<int4> bseg;        // dev: per partition segment, its parent's direct child's slots
+    if (dev) {
+      // slot templates: node j's slots are the partition ranges that visit its
+      // parent (one piece each), in range order; sizes from the winner counts
+      std::vector<int4> pinfo(pst.pbase.size(), make_int4(-1, 0, 0, 0));
+      for (int j = 0; j < A; j++) {
+        const FNode &fn = frontier[j];
+        if (!fn.direct) continue;
+        const bool small = fn.rows * 16 < DS * (node_kc[j] | 1);
+        std::vector<Seg> &lst = small ? fsegs : hsegs;
+        uint32_t &tot = small ? ftotal : htotal;
+        const int p = fn.par;
+        if (p < 0 || p >= (int)pst.pbase.size() || pst.plen[p] == 0)
+          throw Error(ADAPT_E_CUDA, "internal: a direct node without a partitioned parent");
+        const int b0 = (int)(pst.pbase[p] / pst.Rr), b1 = (int)((pst.pbase[p] + pst.plen[p] - 1) / pst.Rr);
+        pinfo[p] = make_int4(fn.side, small ? 1 : 0, (int)lst.size() - b0, 0);
+        if (!small) pnodes.push_back(PlanNode{-1, -1, tot, (uint32_t)fn.rows, node_kc[j]});
         Seg sg{};
-        sg.off = pc.first;
-        sg.len = pc.second;
         sg.hslot = fn.slot;
         sg.cmap = node_ci[j];
         sg.ncls = node_kc[j];
-        (small ? fsegs : hsegs).push_back(sg);
+        sg.node_base = tot;
+        sg.node_len = (uint32_t)fn.rows;
+        sg.row_base = tot;
+        sg.feat = -1;
+        for (int b = b0; b <= b1; b++) lst.push_back(sg);
+        tot += (uint32_t)fn.rows;
       }
+      bseg.resize(pst.seg_parent.size());
+      for (size_t k = 0; k < bseg.size(); k++) bseg[k] = pinfo[pst.seg_parent[k]];
+    } else {
+      for (int j = 0; j < A; j++) {
+        const FNode &fn = frontier[j];
+        if (!fn.direct) continue;
+        int64_t local = 0;
+        for (int q = pc_start[j]; q < pc_start[j + 1]; q++) local += pcs[q].second;
+        const bool small = local * 16 < DS * (node_kc[j] | 1);
+        for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {
+          const auto &pc = pcs[q];
+          Seg sg{};
+          sg.off = pc.first;
+          sg.len = pc.second;
+          sg.hslot = fn.slot;
+          sg.cmap = node_ci[j];
+          sg.ncls = node_kc[j];
+          (small ? fsegs : hsegs).push_back(sg);
+        }
+      }
+      ftotal = virtualize(fsegs, true);
+      htotal = virtualize(hsegs, true);
     }
-    const uint32_t ftotal = virtualize(fsegs, true);
-    const uint32_t htotal = virtualize(hsegs, true);
     tick("hsegs");
     if (htotal + ftotal > 0) {
       Arena &sb = h->stage_b;
@@ -1726,11 +1805,39 @@ void train_region(adapt_region *h, cudaStream_t s) {
       // of different groups share just the 1-byte labels and run unsynchronised)
       const int nranges = (int)std::max<int64_t>(1, std::min<int64_t>((htotal + 4095) / 4096,
                                                                       std::max(1, sms / ngroups)));
-      const std::vector<HistCta> ctas = plan_hist_ctas(hsegs, htotal, gcost, nranges * ngroups);
-      const size_t o_hsegs = sb.put(hsegs), o_fsegs = sb.put(fsegs), o_ctas = sb.put(ctas);
+      tick("arena_reset");
+      const std::vector<HistCta> ctas = dev ? plan_hist_ctas(pnodes, hsegs, htotal, gcost, nranges * ngroups)
+                                            : plan_hist_ctas(hsegs, htotal, gcost, nranges * ngroups);
+      tick("plan");
+      const size_t o_hsegs = sb.put(hsegs), o_fsegs = sb.put(fsegs), o_ctas = sb.put(ctas),
+                   o_bseg = sb.put(bseg);
       sb.flush(s);
+      tick("upload_b");
+      Seg *d_hsegs = sb.ptr<Seg>(o_hsegs), *d_fsegs = sb.ptr<Seg>(o_fsegs);
+      if (dev) {  // the templates are filled in place by the builder
+        h->dseg_err.ensure(16);
+        h->hseg_err.grow(16);
+        CUDA_CHECK(cudaMemsetAsync(h->dseg_err.p, 0, 4, s));
+        SegBuildArgs ba{};
+        ba.visits = h->visits.as<int32_t>();
+        ba.nranges = pa.nranges;
+        ba.max_visits = max_visits;
+        ba.bseg = sb.ptr<int4>(o_bseg);
+        ba.segs[0] = d_hsegs;
+        ba.segs[1] = d_fsegs;
+        ba.nslot[0] = (int)hsegs.size();
+        ba.nslot[1] = (int)fsegs.size();
+        ba.total[0] = htotal;
+        ba.total[1] = ftotal;
+        ba.err = h->dseg_err.as<int32_t>();
+        {
+          Phase ph("decide", s, 0);
+          launch_build_hist_segs(ba, s);
+        }
+        CUDA_CHECK(cudaMemcpyAsync(h->hseg_err.p, h->dseg_err.p, 4, cudaMemcpyDeviceToHost, s));
+      }
       HistArgs ha{};
-      ha.segs = sb.ptr<Seg>(o_hsegs);
+      ha.segs = d_hsegs;
       ha.nseg = (int)hsegs.size();
       ha.total_rows = htotal;
       ha.bins_in = hist_bins;
@@ -1756,31 +1863,11 @@ void train_region(adapt_region *h, cudaStream_t s) {
       launch_hist(ha, s);
       tick("launch_hist");
       HistArgs fa = ha;  // the small nodes
-      fa.segs = sb.ptr<Seg>(o_fsegs);
+      fa.segs = d_fsegs;
       fa.nseg = (int)fsegs.size();
       fa.total_rows = ftotal;
       launch_hist_flat(fa, s);
       tick("launch_flat");
-    }
-    // (prepared after the histogram launch: the GPU idles from the partition's
-    // end until then, and the early partition is only needed behind the winners)
-    if (level + 1 < D) {
-      esegs.reserve(pcs.size());
-      for (int j = 0; j < A; j++)
-        for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {
-          Seg sg{};
-          sg.off = pcs[q].first;
-          sg.len = pcs[q].second;
-          sg.feat = -1;
-          sg.direct = j;  // parent id (groups a parent's pieces); the decision fills the rest
-          sg.hslot = -1;
-          esegs.push_back(sg);
-        }
-      early = level > 0
-                  ? start_part(level + 1, esegs, (out_plane ? h->binsB : h->binsA).as<uint8_t>(),
-                               (out_plane ? h->labB : h->labA).as<uint8_t>(),
-                               w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr, out_plane ^ 1, true)
-                  : start_part(level + 1, esegs, bins_in, lab_in, w_in, out_plane, true);
     }
     if (!rs && collectives_on() && ndirect_slots > 0)  // the direct slots are contiguous at the front
       comm_allreduce_sum(Hcur->p, (size_t)soff[ndirect_slots], false, s, "allreduce histograms");
@@ -1812,7 +1899,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       CUDA_CHECK(cudaMemcpyAsync(hr, h->res.p, (size_t)res_off[A], cudaMemcpyDeviceToHost, s));
       if (!h->win_evt) CUDA_CHECK(cudaEventCreateWithFlags(&h->win_evt, cudaEventDisableTiming));
       CUDA_CHECK(cudaEventRecord(h->win_evt, s));
-      launch_early(h->res.as<uint8_t>());
+      early_res = h->res.as<uint8_t>();
     } else {
       // a5 by ownership: this rank's slots summed over ranks into Hg
       h->Hg.grow((size_t)Q * 4 + 16);
@@ -1873,15 +1960,38 @@ void train_region(adapt_region *h, cudaStream_t s) {
       comm_bytes = NR * Q * 4 + RB * NR;
       if (!h->win_evt) CUDA_CHECK(cudaEventCreateWithFlags(&h->win_evt, cudaEventDisableTiming));
       CUDA_CHECK(cudaEventRecord(h->win_evt, s));
-      if (!esegs.empty()) {  // the records in node order on the device, for the early partition
+      if (level + 1 < D) {  // the records in node order on the device, for the early partition
         h->res.grow((size_t)res_off[A] + 16);
         CUDA_CHECK(cudaMemcpyAsync(h->res.p, hr, (size_t)res_off[A], cudaMemcpyHostToDevice, s));
-        launch_early(h->res.as<uint8_t>());
+        early_res = h->res.as<uint8_t>();
       }
     }
+    if (dev) wait_pieces();  // (the histogram .. winner chain is queued already)
+    // the next level's a7 (prepared after the winner launch: only needed behind it)
+    if (level + 1 < D) {
+      esegs.reserve(pcs.size());
+      for (int j = 0; j < A; j++)
+        for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {
+          Seg sg{};
+          sg.off = pcs[q].first;
+          sg.len = pcs[q].second;
+          sg.feat = -1;
+          sg.direct = j;  // parent id (groups a parent's pieces); the decision fills the rest
+          sg.hslot = -1;
+          esegs.push_back(sg);
+        }
+      early = level > 0
+                  ? start_part(level + 1, esegs, (out_plane ? h->binsB : h->binsA).as<uint8_t>(),
+                               (out_plane ? h->labB : h->labA).as<uint8_t>(),
+                               w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr, out_plane ^ 1, true)
+                  : start_part(level + 1, esegs, bins_in, lab_in, w_in, out_plane, true);
+    }
+    if (early_res) launch_early(early_res);
     if (trace) tr[4] = now_us();
     tick("launch_hist..winner");
     CUDA_CHECK(cudaEventSynchronize(h->win_evt));  // the winners (the early partition may still run)
+    if (dev && htotal + ftotal > 0 && *h->hseg_err.as<int32_t>())
+      throw Error(ADAPT_E_CUDA, "internal: device-built histogram segments disagree with the planned sizes");
     if (trace) tr[5] = now_us();
     tick("wait_winners");
     h->stats.push_back(A);
@@ -2010,11 +2120,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
       int jl = -1, jr = -1;
       if (inL) {
         jl = (int)next.size();
-        next.push_back(FNode{li, fn.depth + 1, dir == 0 ? hslot : -1, dir == 0, present(PL.data())});
+        next.push_back(FNode{li, fn.depth + 1, dir == 0 ? hslot : -1, dir == 0, present(PL.data()),
+                             (int64_t)nr->nL, j, 0});
       }
       if (inR) {
         jr = (int)next.size();
-        next.push_back(FNode{li + 1, fn.depth + 1, dir == 1 ? hslot : -1, dir == 1, present(PR.data())});
+        next.push_back(FNode{li + 1, fn.depth + 1, dir == 1 ? hslot : -1, dir == 1, present(PR.data()),
+                             (int64_t)(nr->n - nr->nL), j, 1});
       }
       if (inL && inR) {  // the other child by subtraction from this node's histogram
         Derived dv;

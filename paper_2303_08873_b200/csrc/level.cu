@@ -248,11 +248,15 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
   for (int e = 0; e < 4; e++) Dw[e] = (4 * w0 + e < a.F) ? a.nval[4 * w0 + e] : 0;
   uint32_t p0 = ct.p0;
   const uint32_t p1 = ct.p1;
-  int s = p0 < p1 ? ct.s0 : a.nseg;
+  int s = p0 < p1 ? (ct.s0 >= 0 ? ct.s0 : first_seg(a.segs, a.nseg, p0)) : a.nseg;
   const uint32_t sbase = smem_u32(sh);
   while (p0 < p1 && s < a.nseg) {
     // ---- one node's rows at virtual positions [p0, pe) ----
     const Seg first = a.segs[s];
+    if (first.len == 0) {  // an empty slot (device-built segments): the next one starts here too
+      s++;
+      continue;
+    }
     const uint32_t pe = min(p1, first.node_base + first.node_len);
     // the node's classes are its compact columns; this CTA counts [k0, k0 + kn)
     const int kcn = first.ncls;
@@ -447,6 +451,68 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
   }
 }
 
+// Histogram segments from the partition's share reports (SegBuildArgs), one
+// CTA: scatter every report's direct-child piece into its slot, then an
+// exclusive scan of the slot lengths per list gives the virtual positions; a
+// node whose first slot does not start at its planned base (or a list whose
+// total differs) flags an error for the host.
+constexpr int kBuildThreads = 1024;
+__global__ void __launch_bounds__(kBuildThreads) build_hist_segs_kernel(SegBuildArgs a) {
+  __shared__ uint32_t s_warp[kBuildThreads / 32];
+  __shared__ uint32_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nent = a.nranges * a.max_visits;
+  for (int i = tid; i < nent; i += blockDim.x) {
+    const int32_t *e = a.visits + (size_t)i * 6;
+    if (e[0] < 0) continue;
+    const int4 info = a.bseg[e[0]];
+    if (info.x < 0) continue;
+    Seg &sg = a.segs[info.y][info.z + i / a.max_visits];
+    sg.off = info.x == 0 ? (uint32_t)e[1] : (uint32_t)(e[2] - e[4]);
+    sg.len = (uint32_t)(info.x == 0 ? e[3] : e[4]);
+  }
+  __syncthreads();
+  for (int l = 0; l < 2; l++) {
+    Seg *sg = a.segs[l];
+    const int n = a.nslot[l];
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+      const int i = c0 + tid;
+      const uint32_t len = i < n ? sg[i].len : 0u;
+      uint32_t x = len;  // inclusive warp scan, then across warps
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_warp[wid] = x;
+      __syncthreads();
+      if (wid == 0) {
+        uint32_t w = s_warp[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+          if (lane >= o) w += y;
+        }
+        s_warp[lane] = w;  // inclusive over warps
+      }
+      __syncthreads();
+      const uint32_t carry = s_carry;
+      const uint32_t excl = carry + (wid ? s_warp[wid - 1] : 0u) + x - len;
+      if (i < n) {
+        sg[i].row_base = excl;
+        if ((i == 0 || sg[i - 1].hslot != sg[i].hslot) && excl != sg[i].node_base) *a.err = 1;
+      }
+      __syncthreads();
+      if (tid == 0) s_carry = carry + s_warp[31];
+      __syncthreads();
+    }
+    if (tid == 0 && s_carry != a.total[l]) *a.err = 1;
+    __syncthreads();
+  }
+}
+
 // Small direct nodes (deep levels): a flat pass over their rows, one thread
 // per row and all F features, counting straight into each node's global
 // matrix (zeroed by zero_slots).  A node's smem block would cost more to zero
@@ -510,6 +576,12 @@ __global__ void __launch_bounds__(256) decide_segs_kernel(Seg *segs, int nseg, c
 }
 
 }  // namespace
+
+void launch_build_hist_segs(const SegBuildArgs &a, cudaStream_t s) {
+  build_hist_segs_kernel<<<1, kBuildThreads, 0, s>>>(a); ++g_kernel_launches;
+  CUDA_CHECK(cudaGetLastError());
+}
+
 
 void launch_decide_segs(Seg *segs, int nseg, const uint8_t *res, const int64_t *rec_off,
                         const int32_t *node_kc, const int32_t *node_depth, int D, cudaStream_t s) {
