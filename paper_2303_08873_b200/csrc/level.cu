@@ -118,7 +118,7 @@ __device__ __forceinline__ int first_seg(const Seg *segs, int nseg, uint32_t p) 
 
 // ------------------------------------------------------------ partition --
 #ifndef ADAPT_PART_UNROLL
-#define ADAPT_PART_UNROLL 2
+#define ADAPT_PART_UNROLL 3
 #endif
 #ifndef ADAPT_HIST_UNROLL
 #define ADAPT_HIST_UNROLL 8
