@@ -1697,6 +1697,10 @@ void train_region(adapt_region *h, cudaStream_t s) {
       std::vector<int32_t> cnt(A + 1, 0);
       std::vector<std::array<uint32_t, 3>> flat;  // (child, offset, length)
       flat.reserve((size_t)2 * pa.nranges * max_visits);
+      // on the last frontier level only the direct children's rows moved
+      // (decide_segs_kernel); a derived child's rows are its share's rest
+      const bool last = level == D - 1;
+      int64_t skipped = 0;
       for (int b = 0; b < pa.nranges; b++)
         for (int v = 0; v < max_visits; v++) {
           const int32_t *e = hv + ((size_t)b * max_visits + v) * 6;
@@ -1705,14 +1709,16 @@ void train_region(adapt_region *h, cudaStream_t s) {
           if (ch.x >= 0 && e[3] > 0) flat.push_back({(uint32_t)ch.x, (uint32_t)e[1], (uint32_t)e[3]});
           if (ch.y >= 0 && e[4] > 0)
             flat.push_back({(uint32_t)ch.y, (uint32_t)(e[2] - e[4]), (uint32_t)e[4]});
+          if (last && ch.x >= 0 && ch.y >= 0 && (!frontier[ch.x].direct || !frontier[ch.y].direct))
+            skipped += (int64_t)(e[2] - e[1]) - e[3] - e[4];
         }
       for (const auto &x : flat) cnt[x[0] + 1]++;
       for (int j = 0; j < A; j++) cnt[j + 1] += cnt[j];
       pc_start = cnt;
       pcs.assign(flat.size(), {0u, 0u});
       for (const auto &x : flat) pcs[cnt[x[0]]++] = {x[1], x[2]};
-      // rows that reached this level's nodes (the moved rows of split parents)
-      rows_part = 0;
+      // rows that reached this level's nodes (moved, or left in place on the last level)
+      rows_part = skipped;
       for (const auto &pc : pcs) rows_part += pc.second;
       if (dev)  // the device built the histogram segments from the planned sizes
         for (int j = 0; j < A; j++) {

@@ -569,6 +569,11 @@ __global__ void __launch_bounds__(256) decide_segs_kernel(Seg *segs, int nseg, c
   int write = 0;
   if (depth < D && np > 1 && nr->valid) {
     write = (depth + 1 < D && npl > 1 ? 1 : 0) | (depth + 1 < D && npr > 1 ? 2 : 0);
+    // children on the LAST frontier level (depth D - 1) are histogrammed and
+    // split-searched but never partitioned again: only the direct (smaller,
+    // ties left — the host's rule) child's rows are needed; the other child's
+    // histogram is parent - direct
+    if (depth + 2 == D && write == 3) write = nr->nL <= nr->n - nr->nL ? 1 : 2;
     sg.feat = nr->feat;
     sg.thr = nr->b_lo;
   }
