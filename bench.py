@@ -36,7 +36,7 @@ WORKLOADS = {
     "C2": "C2 region 0: 3.3e4-row table, 4 features, 7 variants (num_threads), depth 8",
     "C1": "C1: 512 profiled samples, 1 feature (trip count), host vs GPU offload, depth 4",
 }
-KERNEL_PHASES = ("discover", "ingest", "values", "merge", "zero", "partition", "hist", "subtract", "split", "winner", "bootstrap",
+KERNEL_PHASES = ("discover", "ingest", "values", "merge", "zero", "partition", "tag", "hist", "subtract", "split", "winner", "bootstrap",
                  "decide", "select")
 
 
@@ -731,8 +731,8 @@ def main():
                 "impl_frac": (impl / peak) if impl else None}
     # the whole level loop against SURVEY §8(d)'s level figure: (F+1) bytes per
     # row of an active node per level
-    loop_ms = sum(step_ms_phases.get(k, 0) for k in ("partition", "hist", "zero", "subtract", "split",
-                                                   "winner", "fused"))
+    loop_ms = sum(step_ms_phases.get(k, 0) for k in ("partition", "tag", "hist", "zero", "subtract", "split",
+                                                   "winner", "decide", "fused"))
     loop_rows = sum((lv["rows_part"] if i else n) for i, lv in enumerate(levels) if lv["nodes"])
     loop_bytes = (F + 1) * loop_rows * world
     level_loop = {"survey_bytes_per_step": loop_bytes, "ms_per_step": loop_ms,

@@ -142,15 +142,39 @@ struct PartArgs {            // a7: move the split parents' rows into the childr
   size_t pstride;                   // bytes between bins word planes
   int BS, F;
   int32_t *visits;           // [nranges][max_visits][6]: seg, share [A, B), left, right moved
+                             //   (two-level move: [8]: seg, A, B, cL, LL, LR, RL, RR moved)
   int max_visits;
   int nranges;               // CTAs, one row range each
+  // Two-level schedule (DESIGN.md §6 "two-level row moves"): the rows move only
+  // every other level.  TAG pass (launch_tag): no row moves; each split
+  // parent's row gets bit 7 of its label set in lab_tag[row] (same position as
+  // the input planes) when it goes to the parent's direct child (seg.hslot =
+  // that side, 0 left / 1 right), and the share reports count every left /
+  // right row.  MOVE4 pass (launch_partition4): the same segments and ranges
+  // one level later; each row goes to one of its parent's four grandchildren
+  // (kids[2 s + c] = child c's (feat, thr, write) from its winner record), the
+  // parent's share [A, B) split at A + cL (cL from the tag pass's reports).
+  uint8_t *lab_tag;          // TAG: tagged labels out
+  const int32_t *tag_visits; // MOVE4: the TAG pass's share reports ([6] per visit)
+  const int4 *kids;          // MOVE4: per segment, per child
 };
 int partition_ranges(int sms, uint32_t total_rows);
 void launch_partition(const PartArgs &a, cudaStream_t s);
+void launch_tag(const PartArgs &a, cudaStream_t s);
+void launch_partition4(const PartArgs &a, cudaStream_t s);
+// MOVE4's per-child decisions from the tagged level's winner records:
+// kid_j[s] = the two children (frontier indices, -1: none) of segment s's
+// parent; kids[2 s + c] = (feat, thr, write, 0) by decide_segs' rule
+void launch_decide_kids(const int2 *kid_j, int nseg, const uint8_t *res, const int64_t *rec_off,
+                        const int32_t *node_kc, const int32_t *node_depth, int D, int4 *kids,
+                        cudaStream_t s);
 // the partition's per-segment split / write decisions from the winner records
 // (node j's record at res + rec_off[j]); segs[i].direct = the segment's node
+// tag != 0 (TAG pass): also seg.hslot = the side of the parent's direct child
+// (0 left, 1 right, -1 none), and the last-level single-child rule is not applied
 void launch_decide_segs(Seg *segs, int nseg, const uint8_t *res, const int64_t *rec_off,
-                        const int32_t *node_kc, const int32_t *node_depth, int D, cudaStream_t s);
+                        const int32_t *node_kc, const int32_t *node_depth, int D, cudaStream_t s,
+                        int tag = 0);
 
 // The histogram segments built on the device from the partition's share
 // reports (single-rank, unweighted levels: the host planned every node's size
@@ -196,6 +220,8 @@ struct HistArgs {            // a4: class histograms of the given pieces' rows
   const int64_t *soff;       // [slots] element offset of a slot's matrix in H
   const HistCta *ctas;       // [nctas] per-CTA work (cost-balanced on the host)
   int nctas;
+  int tagged;                // rows are the PARENT's pieces; count only labels with bit 7
+                             // (the TAG pass's mark of the direct child), class = label & 127
 };
 void launch_hist(const HistArgs &a, cudaStream_t s);
 void launch_hist_flat(const HistArgs &a, cudaStream_t s);  // small nodes: thread per row

@@ -430,16 +430,19 @@ struct PlanNode {
   int fs, ls;  // its segments [fs, ls) (fs = -1: not known yet, the kernel searches)
   uint32_t base, len;
   int kc;
+  double cf = 1.0;  // fraction of the rows read that are counted (tagged levels: child / parent rows)
 };
 std::vector<HistCta> plan_hist_ctas(const std::vector<PlanNode> &nodes, const std::vector<Seg> &segs,
                                     uint32_t total, const std::vector<HistGroupCost> &gc, int nct);
 std::vector<HistCta> plan_hist_ctas(const std::vector<Seg> &segs, uint32_t total,
-                                    const std::vector<HistGroupCost> &gc, int nct) {
+                                    const std::vector<HistGroupCost> &gc, int nct,
+                                    const std::vector<double> *cf_of_slot = nullptr) {
   std::vector<PlanNode> nodes;
   for (int i = 0; i < (int)segs.size();) {
     int k = i;
     while (k < (int)segs.size() && segs[k].hslot == segs[i].hslot) k++;
-    nodes.push_back(PlanNode{i, k, segs[i].node_base, segs[i].node_len, segs[i].ncls});
+    nodes.push_back(PlanNode{i, k, segs[i].node_base, segs[i].node_len, segs[i].ncls,
+                             cf_of_slot ? (*cf_of_slot)[segs[i].hslot] : 1.0});
     i = k;
   }
   return plan_hist_ctas(nodes, segs, total, gc, nct);
@@ -451,8 +454,9 @@ std::vector<HistCta> plan_hist_ctas(const std::vector<PlanNode> &nodes, const st
   if (!total || nodes.empty() || G == 0) return out;
   using N = PlanNode;
   auto kn_of = [&](const HistGroupCost &c, int kc) { return std::min(c.kw, kc - c.k0); };
-  auto row_of = [&](const HistGroupCost &c, int kc) {  // rows of other slabs are only loaded
-    return c.row_ns * (0.3 + 0.7 * (double)std::max(0, kn_of(c, kc)) / std::max(1, kc));
+  auto row_of = [&](const HistGroupCost &c, int kc, double cf) {  // rows of other slabs (or
+    // unmarked rows of a tagged level) are only loaded
+    return c.row_ns * (0.3 + 0.7 * cf * (double)std::max(0, kn_of(c, kc)) / std::max(1, kc));
   };
   auto ovh = [&](const HistGroupCost &c, int kc) {
     const int kn = kn_of(c, kc);
@@ -462,7 +466,7 @@ std::vector<HistCta> plan_hist_ctas(const std::vector<PlanNode> &nodes, const st
   double sum = 0;
   for (int g = 0; g < G; g++) {
     for (const auto &n : nodes)
-      if (kn_of(gc[g], n.kc) > 0) T[g] += ovh(gc[g], n.kc) + n.len * row_of(gc[g], n.kc);
+      if (kn_of(gc[g], n.kc) > 0) T[g] += ovh(gc[g], n.kc) + n.len * row_of(gc[g], n.kc, n.cf);
     sum += T[g];
   }
   // CTAs per group: proportional to cost, at least one for a group with work
@@ -511,7 +515,7 @@ std::vector<HistCta> plan_hist_ctas(const std::vector<PlanNode> &nodes, const st
     for (const auto &n : nodes) {
       const int kn = kn_of(gc[g], n.kc);
       if (kn <= 0) continue;
-      const double O = ovh(gc[g], n.kc), r = row_of(gc[g], n.kc);
+      const double O = ovh(gc[g], n.kc), r = row_of(gc[g], n.kc, n.cf);
       uint32_t pos = n.base, left = n.len;
       if (!open) start = pos, s_start = n.fs;  // skip rows no CTA of g needs
       open = true;
@@ -636,6 +640,8 @@ struct adapt_region {
   adapt::HostBuf hres, hsmall, hvis, hgat;  // winners, scalars, partition share reports, gathered winners
   adapt::Arena stage_p, stage_a, stage_b, stage_r;  // per-level uploads: partition, its tables,
                                                      // histogram segments, owner split lists
+  adapt::Arena stage_k;                  // two-level moves: MOVE4's per-segment children
+  adapt::DevBuf labT, visits2, kids;     // TAG pass labels, MOVE4 share reports, MOVE4 decisions
   cudaEvent_t sel_evt = nullptr;  // recorded after every device select (upload_tree waits)
   cudaEvent_t win_evt = nullptr;  // a level's winner records are on the host
   cudaEvent_t vis_evt = nullptr;  // a partition's share reports are on the host
@@ -1428,6 +1434,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
   // all-gather of the winner records gives every rank the identical decisions.
   // Otherwise (default): all-reduce of the direct nodes, derived globally.
   const bool rs = hist_comm_rs();
+  // two-level row moves: the rows move every other level (TAG
+  // pass, then MOVE4 one level later); one rank, unweighted rows, one tree,
+  // classes below 128 (label bit 7 carries the TAG pass's mark)
+  static const bool one_level = getenv("ADAPT_ONE_LEVEL") != nullptr;
+  const bool two_level = !one_level && !w_root && !mr && g_ctx.world == 1 && !rs && C <= 127;
+  if (two_level) h->labT.ensure((size_t)std::max<int64_t>(rows_out, 1) + 64);
+  std::vector<int4> pseg_gkids;  // per TAG segment: its parent's grandchildren (LL, LR, RL, RR)
   static const bool per_level = getenv("ADAPT_PROFILE_LEVELS") != nullptr;
   char nm[32];
   auto virtualize = [](std::vector<Seg> &v, bool by_slot) {  // row_base, node extents
@@ -1461,6 +1474,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
   // share reports come back asynchronously into h->hvis
   struct PartState {
     bool launched = false;
+    int mode = 0;  // 0: partition (2-way move), 1: TAG pass, 2: MOVE4
+    const int2 *kid_dev = nullptr;  // MOVE4: per segment, the parent's children (device)
     PartArgs pa{};
     int max_visits = 1;  // parents a partition range can touch
     size_t vbytes = 0;
@@ -1476,13 +1491,20 @@ void train_region(adapt_region *h, cudaStream_t s) {
   // the partition launch (and its share reports' D2H), on the stream
   auto launch_part = [&](PartState &st) {
     {
-      snprintf(nm, sizeof nm, "partition_L%02d", st.lvl);
-      Phase ph(per_level ? nm : "partition", s, (double)st.rows_part * 2 * (BS + 1));
-      launch_partition(st.pa, s);
+      const char *what = st.mode == 1 ? "tag" : "partition";
+      snprintf(nm, sizeof nm, "%s_L%02d", what, st.lvl);
+      // implementation bytes: a move reads and writes BS + 1 per row; TAG reads
+      // one bins word and the label, writes the label
+      Phase ph(per_level ? nm : what, s, (double)st.rows_part * (st.mode == 1 ? 6.0 : 2.0 * (BS + 1)));
+      if (st.mode == 1) launch_tag(st.pa, s);
+      else if (st.mode == 2) launch_partition4(st.pa, s);
+      else launch_partition(st.pa, s);
     }
+    st.launched = true;
+    if (st.mode == 1) return;  // the TAG pass's reports stay on the device (MOVE4 reads them)
     h->hvis.grow(st.vbytes);
     st.hv = h->hvis.as<int32_t>();
-    CUDA_CHECK(cudaMemcpyAsync(st.hv, h->visits.p, st.vbytes, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(st.hv, st.pa.visits, st.vbytes, cudaMemcpyDeviceToHost, s));
     if (!h->vis_evt) CUDA_CHECK(cudaEventCreateWithFlags(&h->vis_evt, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventRecord(h->vis_evt, s));
     st.launched = true;
@@ -1490,9 +1512,11 @@ void train_region(adapt_region *h, cudaStream_t s) {
   // upload a partition's segments and size its share reports; `defer`: the
   // caller launches it (after the device has decided the segments' splits)
   auto start_part = [&](int lvl, std::vector<Seg> &segs, const uint8_t *b_in, const uint8_t *l_in,
-                        const uint8_t *wi, int oplane, bool defer = false) {
+                        const uint8_t *wi, int oplane, bool defer = false, int mode = 0) {
     PartState st;
+    st.mode = mode;
     PartArgs &pa = st.pa;
+    pa.lab_tag = h->labT.as<uint8_t>();
     const uint32_t total = virtualize(segs, false);
     st.rows_part = total;
     pa.nseg = (int)segs.size();
@@ -1541,7 +1565,31 @@ void train_region(adapt_region *h, cudaStream_t s) {
     if (!defer) launch_part(st);
     return st;
   };
-  PartState pending;
+  // MOVE4 one level after the TAG pass `tg`: same segments (their splits decided
+  // by the TAG pass's decide), same ranges; kid_j = each segment's two children
+  auto start_move4 = [&](const PartState &tg, int lvl, const std::vector<int2> &kid_j, int oplane) {
+    PartState st = tg;
+    st.mode = 2;
+    st.launched = false;
+    st.lvl = lvl;
+    PartArgs &pa = st.pa;
+    pa.bins_out = (oplane ? h->binsB : h->binsA).as<uint8_t>();
+    pa.lab_out = (oplane ? h->labB : h->labA).as<uint8_t>();
+    pa.tag_visits = tg.pa.visits;
+    st.vbytes = (size_t)pa.nranges * st.max_visits * 8 * 4;
+    h->visits2.grow(st.vbytes);
+    CUDA_CHECK(cudaMemsetAsync(h->visits2.p, 0xFF, st.vbytes, s));
+    pa.visits = h->visits2.as<int32_t>();
+    Arena &sk = h->stage_k;
+    sk.reset();
+    const size_t o_kid = sk.put(kid_j);
+    sk.flush(s);
+    st.kid_dev = sk.ptr<int2>(o_kid);
+    h->kids.grow((size_t)std::max(pa.nseg, 1) * 2 * sizeof(int4));
+    pa.kids = h->kids.as<int4>();
+    return st;
+  };
+  PartState pending, tag_st;  // tag_st: the TAG pass behind the current tagged level
   static const bool trace2 = trace && atoi(getenv("ADAPT_TRACE_HOST")) >= 2;
   std::vector<std::pair<const char *, double>> ticks;  // (what, us) per level
   auto tick = [&](const char *what) {
@@ -1564,6 +1612,10 @@ void train_region(adapt_region *h, cudaStream_t s) {
     }
     pending = PartState{};
     PartArgs &pa = pst.pa;
+    // tagged: this level's nodes are the TAG pass's children, their rows still
+    // in the parents' pieces (pcs / pc_start), the direct ones marked in labT
+    const bool tagged = level > 0 && pst.mode == 1, after4 = level > 0 && pst.mode == 2;
+    if (tagged) tag_st = pst;
     const int max_visits = pst.max_visits;
     rows_part = pst.rows_part;
     int32_t *hv = pst.hv;
@@ -1678,8 +1730,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
     // direct node's size is its parent's winner count, so the histogram pass
     // is queued behind the partition without waiting for its share reports)
     static const bool host_segs = getenv("ADAPT_HOST_SEGS") != nullptr;
-    const bool dev = level > 0 && !w_root && g_ctx.world == 1 && !rs && !host_segs;
-    if (level > 0) {
+    const bool dev = level > 0 && pst.mode == 0 && !w_root && g_ctx.world == 1 && !rs && !host_segs;
+    if (tagged) {
+      hist_bins = pa.bins_in;
+      hist_lab = h->labT.as<uint8_t>();
+      hist_w = nullptr;
+    } else if (level > 0) {
       hist_bins = pa.bins_out;
       hist_lab = pa.lab_out;
       hist_w = pa.w_out;
@@ -1691,6 +1747,11 @@ void train_region(adapt_region *h, cudaStream_t s) {
     // out in offset order; a counting sort by child groups them (CSR)
     auto wait_pieces = [&]() {
       if (level == 0) return;
+      if (tagged || after4) {  // single rank: the nodes' rows are their winner counts
+        rows_part = 0;
+        for (const auto &fn : frontier) rows_part += fn.rows;
+      }
+      if (tagged) return;  // nothing moved: the parents' pieces serve this level
       CUDA_CHECK(cudaEventSynchronize(h->vis_evt));
       if (trace) tr[2] = now_us();
       tick("wait_part");
@@ -1701,7 +1762,18 @@ void train_region(adapt_region *h, cudaStream_t s) {
       // (decide_segs_kernel); a derived child's rows are its share's rest
       const bool last = level == D - 1;
       int64_t skipped = 0;
-      for (int b = 0; b < pa.nranges; b++)
+      for (int b = 0; b < pa.nranges && after4; b++)  // MOVE4: four grandchildren per share
+        for (int v = 0; v < max_visits; v++) {
+          const int32_t *e = hv + ((size_t)b * max_visits + v) * 8;
+          if (e[0] < 0) break;
+          const int4 gk = pseg_gkids[e[0]];
+          const uint32_t A = (uint32_t)e[1], B = (uint32_t)e[2], M = A + (uint32_t)e[3];
+          if (gk.x >= 0 && e[4] > 0) flat.push_back({(uint32_t)gk.x, A, (uint32_t)e[4]});
+          if (gk.y >= 0 && e[5] > 0) flat.push_back({(uint32_t)gk.y, M - (uint32_t)e[5], (uint32_t)e[5]});
+          if (gk.z >= 0 && e[6] > 0) flat.push_back({(uint32_t)gk.z, M, (uint32_t)e[6]});
+          if (gk.w >= 0 && e[7] > 0) flat.push_back({(uint32_t)gk.w, B - (uint32_t)e[7], (uint32_t)e[7]});
+        }
+      for (int b = 0; b < pa.nranges && !after4; b++)
         for (int v = 0; v < max_visits; v++) {
           const int32_t *e = hv + ((size_t)b * max_visits + v) * 6;
           if (e[0] < 0) break;
@@ -1718,8 +1790,10 @@ void train_region(adapt_region *h, cudaStream_t s) {
       pcs.assign(flat.size(), {0u, 0u});
       for (const auto &x : flat) pcs[cnt[x[0]]++] = {x[1], x[2]};
       // rows that reached this level's nodes (moved, or left in place on the last level)
-      rows_part = skipped;
-      for (const auto &pc : pcs) rows_part += pc.second;
+      if (!after4) {
+        rows_part = skipped;
+        for (const auto &pc : pcs) rows_part += pc.second;
+      }
       if (dev)  // the device built the histogram segments from the planned sizes
         for (int j = 0; j < A; j++) {
           if (!frontier[j].direct) continue;
@@ -1740,11 +1814,15 @@ void train_region(adapt_region *h, cudaStream_t s) {
     std::vector<Seg> esegs;
     const uint8_t *early_res = nullptr;  // winner records on the device, for decide_segs
     auto launch_early = [&](const uint8_t *res_dev) {
-      if (esegs.empty()) return;
+      if (early.pa.nseg == 0) return;
       {
         Phase ph("decide", s, 0);
-        launch_decide_segs(const_cast<Seg *>(early.pa.segs), (int)esegs.size(), res_dev, sa.ptr<int64_t>(o_roff),
-                           sa.ptr<int32_t>(o_nkc), sa.ptr<int32_t>(o_ndep), D, s);
+        if (early.mode == 2)
+          launch_decide_kids(early.kid_dev, early.pa.nseg, res_dev, sa.ptr<int64_t>(o_roff), sa.ptr<int32_t>(o_nkc),
+                             sa.ptr<int32_t>(o_ndep), D, h->kids.as<int4>(), s);
+        else
+          launch_decide_segs(const_cast<Seg *>(early.pa.segs), early.pa.nseg, res_dev, sa.ptr<int64_t>(o_roff),
+                             sa.ptr<int32_t>(o_nkc), sa.ptr<int32_t>(o_ndep), D, s, early.mode == 1);
       }
       launch_part(early);
     };
@@ -1753,6 +1831,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     uint32_t htotal = 0, ftotal = 0;
     std::vector<PlanNode> pnodes;  // dev: the big nodes' planned layout
     std::vector<int4> bseg;        // dev: per partition segment, its parent's direct child's slots
+    std::vector<double> cf_slot(tagged ? nslots : 0, 1.0);  // tagged: counted share of the rows read
     if (dev) {
       // slot templates: node j's slots are the partition ranges that visit its
       // parent (one piece each), in range order; sizes from the winner counts
@@ -1786,10 +1865,12 @@ void train_region(adapt_region *h, cudaStream_t s) {
       for (int j = 0; j < A; j++) {
         const FNode &fn = frontier[j];
         if (!fn.direct) continue;
+        const int pj = tagged ? fn.par : j;  // tagged: the parent's pieces, marked rows count
         int64_t local = 0;
-        for (int q = pc_start[j]; q < pc_start[j + 1]; q++) local += pcs[q].second;
+        for (int q = pc_start[pj]; q < pc_start[pj + 1]; q++) local += pcs[q].second;
         const bool small = local * 16 < DS * (node_kc[j] | 1);
-        for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {
+        if (tagged) cf_slot[fn.slot] = local ? (double)fn.rows / (double)local : 1.0;
+        for (int q = pc_start[pj]; q < pc_start[pj + 1]; q++) {
           const auto &pc = pcs[q];
           Seg sg{};
           sg.off = pc.first;
@@ -1813,7 +1894,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
                                                                       std::max(1, sms / ngroups)));
       tick("arena_reset");
       const std::vector<HistCta> ctas = dev ? plan_hist_ctas(pnodes, hsegs, htotal, gcost, nranges * ngroups)
-                                            : plan_hist_ctas(hsegs, htotal, gcost, nranges * ngroups);
+                                            : plan_hist_ctas(hsegs, htotal, gcost, nranges * ngroups,
+                                                             tagged ? &cf_slot : nullptr);
       tick("plan");
       const size_t o_hsegs = sb.put(hsegs), o_fsegs = sb.put(fsegs), o_ctas = sb.put(ctas),
                    o_bseg = sb.put(bseg);
@@ -1863,6 +1945,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
       ha.soff = sa.ptr<int64_t>(o_soff);
       ha.ctas = sb.ptr<HistCta>(o_ctas);
       ha.nctas = (int)ctas.size();
+      ha.tagged = tagged ? 1 : 0;
       snprintf(nm, sizeof nm, "hist_L%02d", level);
       Phase ph(per_level ? nm : "hist", s, (double)(htotal + ftotal) * (F + 1));
       tick("hist_args");
@@ -1974,7 +2057,9 @@ void train_region(adapt_region *h, cudaStream_t s) {
     }
     if (dev) wait_pieces();  // (the histogram .. winner chain is queued already)
     // the next level's a7 (prepared after the winner launch: only needed behind it)
-    if (level + 1 < D) {
+    if (level + 1 < D && tagged) {  // MOVE4 from the parents' planes (the TAG pass's segments)
+      early = start_move4(tag_st, level + 1, pseg_children, out_plane);
+    } else if (level + 1 < D) {
       esegs.reserve(pcs.size());
       for (int j = 0; j < A; j++)
         for (int q = pc_start[j]; q < pc_start[j + 1]; q++) {
@@ -1986,11 +2071,17 @@ void train_region(adapt_region *h, cudaStream_t s) {
           sg.hslot = -1;
           esegs.push_back(sg);
         }
+      // two-level: the TAG pass instead of a move — except into the last frontier
+      // level, where a partition moves only the direct children's rows (measured
+      // cheaper than TAG + a histogram over the parents' rows)
+      static const bool tag_last = getenv("ADAPT_TAG_LAST") != nullptr;
+      const int mode = two_level && (level + 2 < D || tag_last) ? 1 : 0;
       early = level > 0
                   ? start_part(level + 1, esegs, (out_plane ? h->binsB : h->binsA).as<uint8_t>(),
                                (out_plane ? h->labB : h->labA).as<uint8_t>(),
-                               w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr, out_plane ^ 1, true)
-                  : start_part(level + 1, esegs, bins_in, lab_in, w_in, out_plane, true);
+                               w_root ? (out_plane ? h->wB : h->wA).as<uint8_t>() : nullptr, out_plane ^ 1, true,
+                               mode)
+                  : start_part(level + 1, esegs, bins_in, lab_in, w_in, out_plane, true, mode);
     }
     if (early_res) launch_early(early_res);
     if (trace) tr[4] = now_us();
@@ -2144,8 +2235,17 @@ void train_region(adapt_region *h, cudaStream_t s) {
       }
       kids[j] = make_int2(jl, jr);
     }
-    for (int j = 0; j < A; j++)  // the children of each early-partition segment (all pieces)
-      for (int q = pc_start[j]; q < pc_start[j + 1]; q++) nchildren.push_back(kids[j]);
+    if (tagged) {  // MOVE4's grandchildren per TAG segment (the next level's pieces)
+      pseg_gkids.resize(pseg_children.size());
+      for (size_t q = 0; q < pseg_children.size(); q++) {
+        const int2 c = pseg_children[q];
+        const int2 l = c.x >= 0 ? kids[c.x] : make_int2(-1, -1), r = c.y >= 0 ? kids[c.y] : make_int2(-1, -1);
+        pseg_gkids[q] = make_int4(l.x, l.y, r.x, r.y);
+      }
+    } else {
+      for (int j = 0; j < A; j++)  // the children of each early-partition segment (all pieces)
+        for (int q = pc_start[j]; q < pc_start[j + 1]; q++) nchildren.push_back(kids[j]);
+    }
     // derived slots follow the direct ones
     for (size_t i = 0; i < nderived.size(); i++) next[nderived[i].j].slot = ndirect + (int)i;
     tick("pass2");
@@ -2161,13 +2261,13 @@ void train_region(adapt_region *h, cudaStream_t s) {
               level ? tr[1] - tr[0] : 0.0, tr[6] - tr[0], t_mv - tr[6], level ? tr[2] - tr[1] : 0.0, level ? tr[3] - tr[2] : 0.0,
               tr[4] - tr[3], tr[5] - tr[4], now_us() - tr[5]);
     frontier.swap(next);
-    pseg_children.swap(nchildren);
+    if (!tagged) pseg_children.swap(nchildren);
     ndirect_slots = ndirect;
     derived.swap(nderived);
     std::swap(Hcur, Hprev);
     // the planes just written are the input of the next partition; the root
     // level moved nothing, so level 1 still reads the ingest output
-    if (level > 0) {
+    if (level > 0 && !tagged) {  // (a tagged level moved nothing)
       bins_in = (out_plane ? h->binsB : h->binsA).as<uint8_t>();
       lab_in = (out_plane ? h->labB : h->labA).as<uint8_t>();
       if (w_root) w_in = (out_plane ? h->wB : h->wA).as<uint8_t>();

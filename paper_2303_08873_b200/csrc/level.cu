@@ -226,6 +226,263 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition_kernel
   }
 }
 
+// ---------------------------------------------------- two-level moves --
+// DESIGN.md §6 "two-level row moves": the rows move every other level.  The
+// TAG pass runs where a partition would, over the same segments and ranges,
+// but moves nothing: it reads the split feature's word plane and the labels,
+// writes each row's label with bit 7 = "goes to the parent's direct child"
+// into lab_tag (same position), and reports per parent share the counts of
+// ALL rows going left / right.  The next level's histogram pass counts the
+// marked rows straight from the parent's pieces; one level later MOVE4 moves
+// every row to its grandchild's piece.
+template <int BS>
+__device__ __forceinline__ uint32_t feat_word(const uint8_t *__restrict__ base, size_t pstride, uint32_t row,
+                                              int f, int &shift) {
+  if constexpr (BS >= 4) {
+    shift = 8 * (f & 3);
+    return __ldcs(reinterpret_cast<const unsigned int *>(base + (size_t)(f >> 2) * pstride + (size_t)row * 4));
+  } else if constexpr (BS == 2) {
+    shift = 8 * f;
+    return __ldcs(reinterpret_cast<const unsigned short *>(base + (size_t)row * 2));
+  } else {
+    shift = 0;
+    return __ldcs(base + row);
+  }
+}
+
+constexpr int kTagUnroll = 4;  // rows in flight per thread
+
+template <int BS>
+__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) tag_kernel(PartArgs a) {
+  __shared__ uint32_t s_cnt[2];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t R = (a.total_rows + gridDim.x - 1) / gridDim.x;
+  uint32_t p0 = blockIdx.x * R;
+  const uint32_t p1 = min(p0 + R, a.total_rows);
+  int s = p0 < p1 ? first_seg(a.segs, a.nseg, p0) : a.nseg;
+  int32_t *my_visits = a.visits + (size_t)blockIdx.x * a.max_visits * 6;
+  int visits = 0;
+  __syncthreads();
+  while (p0 < p1 && s < a.nseg) {
+    const Seg first = a.segs[s];
+    const uint32_t pe = min(p1, first.node_base + first.node_len);
+    if (tid == 0) s_cnt[0] = s_cnt[1] = 0;
+    __syncthreads();
+    const int s_first = s;
+    uint32_t nl = 0, nr = 0;
+    for (; s < a.nseg && a.segs[s].row_base < pe; s++) {
+      const Seg sg = a.segs[s];
+      if (!sg.write) continue;  // a parent that does not split (or whose children are leaves)
+      const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
+      const uint32_t q1 = min(sg.len, pe - sg.row_base);
+      const uint32_t mark_left = sg.hslot == 0 ? 0x80u : 0u, mark_right = sg.hslot == 1 ? 0x80u : 0u;
+      if constexpr (BS >= 4) {
+        // the 4-aligned body as quads: one 16-byte load of the split feature's
+        // word plane, one 4-byte label load and store per 4 rows; head / tail per row
+        const uint32_t r0 = sg.off + q0, r1 = sg.off + q1;
+        const uint32_t a4 = min((r0 + 3u) & ~3u, r1), b4 = max(a4, r1 & ~3u);
+        const int shift = 8 * (sg.feat & 3);
+        const uint8_t *plane = a.bins_in + (size_t)(sg.feat >> 2) * a.pstride;
+        auto one = [&](uint32_t row) {
+          const uint32_t w = *reinterpret_cast<const uint32_t *>(plane + (size_t)row * 4);
+          const bool left = (int)((w >> shift) & 0xFFu) <= sg.thr;
+          nl += left;
+          nr += !left;
+          a.lab_tag[row] = (uint8_t)(a.lab_in[row] | (left ? mark_left : mark_right));
+        };
+        if (tid < (int)(a4 - r0)) one(r0 + tid);
+        if (tid >= 64 && tid < 64 + (int)(r1 - b4)) one(b4 + tid - 64);
+        const uint32_t nq = (b4 - a4) >> 2;
+        const uint4 *wq = reinterpret_cast<const uint4 *>(plane + (size_t)a4 * 4);
+        const uint32_t *lq = reinterpret_cast<const uint32_t *>(a.lab_in + a4);
+        uint32_t *oq = reinterpret_cast<uint32_t *>(a.lab_tag + a4);
+        constexpr int QU = 2;  // quads in flight per thread
+        for (uint32_t qb = 0; qb < nq; qb += QU * blockDim.x) {
+          uint4 w[QU];
+          uint32_t l[QU];
+#pragma unroll
+          for (int u = 0; u < QU; u++) {
+            const uint32_t qi = qb + u * blockDim.x + tid;
+            if (qi < nq) {
+              w[u] = __ldcs(wq + qi);
+              l[u] = __ldcs(lq + qi);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < QU; u++) {
+            const uint32_t qi = qb + u * blockDim.x + tid;
+            if (qi < nq) {
+              const uint32_t x[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+              uint32_t mark = 0;
+#pragma unroll
+              for (int c = 0; c < 4; c++) {
+                const bool left = (int)((x[c] >> shift) & 0xFFu) <= sg.thr;
+                nl += left;
+                nr += !left;
+                mark |= (left ? mark_left : mark_right) << (8 * c);
+              }
+              __stcs(oq + qi, l[u] | mark);
+            }
+          }
+        }
+      } else {
+        for (uint32_t qb = q0; qb < q1; qb += kTagUnroll * blockDim.x) {
+          uint32_t w[kTagUnroll], lab[kTagUnroll];
+          int sh[kTagUnroll];
+#pragma unroll
+          for (int u = 0; u < kTagUnroll; u++) {  // all loads first
+            const uint32_t q = qb + u * blockDim.x + tid;
+            sh[u] = 0;
+            w[u] = 0;
+            lab[u] = 0;
+            if (q < q1) {
+              w[u] = feat_word<BS>(a.bins_in, a.pstride, sg.off + q, sg.feat, sh[u]);
+              lab[u] = __ldcs(a.lab_in + sg.off + q);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kTagUnroll; u++) {
+            const uint32_t q = qb + u * blockDim.x + tid;
+            if (q < q1) {
+              const bool left = (int)((w[u] >> sh[u]) & 0xFFu) <= sg.thr;  // bins are ranks
+              nl += left;
+              nr += !left;
+              __stcs(a.lab_tag + sg.off + q, (uint8_t)(lab[u] | (left ? mark_left : mark_right)));
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      nl += __shfl_xor_sync(kFull, nl, o);
+      nr += __shfl_xor_sync(kFull, nr, o);
+    }
+    if (lane == 0 && (nl | nr)) {
+      atomicAdd(&s_cnt[0], nl);
+      atomicAdd(&s_cnt[1], nr);
+    }
+    __syncthreads();
+    if (tid == 0 && visits < a.max_visits) {  // report this parent's share
+      int32_t *v = my_visits + 6 * visits;
+      v[0] = s_first;
+      v[1] = (int32_t)p0;
+      v[2] = (int32_t)pe;
+      v[3] = (int32_t)s_cnt[0];
+      v[4] = (int32_t)s_cnt[1];
+      v[5] = 0;
+    }
+    visits++;
+    p0 = pe;
+  }
+}
+
+// MOVE4: one level after the TAG pass, over its segments and ranges.  A parent's
+// share [A, B) splits at M = A + cL (cL = the TAG pass's left count of this
+// share): left-left rows from A up, left-right from M down, right-left from M
+// up, right-right from B down, positions from warp-aggregated cursors as in
+// partition_kernel; rows of a grandchild that is not in the frontier stay behind.
+template <int BS>
+__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition4_kernel(PartArgs a) {
+  __shared__ uint32_t s_cur[4];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t R = (a.total_rows + gridDim.x - 1) / gridDim.x;
+  uint32_t p0 = blockIdx.x * R;
+  const uint32_t p1 = min(p0 + R, a.total_rows);
+  int s = p0 < p1 ? first_seg(a.segs, a.nseg, p0) : a.nseg;
+  int32_t *my_visits = a.visits + (size_t)blockIdx.x * a.max_visits * 8;
+  const int32_t *tag_visits = a.tag_visits + (size_t)blockIdx.x * a.max_visits * 6;
+  int visits = 0;
+  __syncthreads();
+  while (p0 < p1 && s < a.nseg) {
+    const Seg first = a.segs[s];
+    const uint32_t pe = min(p1, first.node_base + first.node_len);
+    const uint32_t A = p0, B = pe;
+    // the TAG pass visited the same parents in the same order
+    const uint32_t M = A + (visits < a.max_visits ? (uint32_t)tag_visits[6 * visits + 3] : 0u);
+    if (tid < 4) s_cur[tid] = 0;
+    __syncthreads();
+    const int s_first = s;
+    for (; s < a.nseg && a.segs[s].row_base < pe; s++) {
+      const Seg sg = a.segs[s];
+      if (!sg.write) continue;
+      const int4 kl = a.kids[2 * s], kr = a.kids[2 * s + 1];
+      if (!(kl.z | kr.z)) continue;  // no grandchild stays in the frontier
+      const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
+      const uint32_t q1 = min(sg.len, pe - sg.row_base);
+      Row<BS> r[kPartUnroll], rn[kPartUnroll];
+      int label[kPartUnroll], labn[kPartUnroll];
+      auto load = [&](uint32_t qb, Row<BS>(&rr)[kPartUnroll], int(&ll)[kPartUnroll]) {
+#pragma unroll
+        for (int u = 0; u < kPartUnroll; u++) {
+          const uint32_t q = qb + u * blockDim.x + tid;
+          ll[u] = -1;
+          if (q < q1) {
+            load_row<BS>(a.bins_in, a.pstride, sg.off + q, rr[u]);
+            ll[u] = __ldcs(a.lab_in + sg.off + q);
+          } else {
+#pragma unroll
+            for (int i = 0; i < Row<BS>::N; i++) rr[u].w[i] = 0;
+          }
+        }
+      };
+      if (q0 < q1) load(q0, r, label);
+      for (uint32_t qb = q0; qb < q1; qb += kPartUnroll * blockDim.x) {
+        const bool more = qb + kPartUnroll * blockDim.x < q1;
+        if (more) load(qb + kPartUnroll * blockDim.x, rn, labn);
+#pragma unroll
+        for (int u = 0; u < kPartUnroll; u++) {
+          const bool left = row_byte<BS>(r[u], sg.feat) <= sg.thr;
+          const int4 k = left ? kl : kr;
+          const bool gl = k.x >= 0 && row_byte<BS>(r[u], max(k.x, 0)) <= k.y;
+          const int code = (left ? 0 : 2) | (gl ? 0 : 1);
+          const bool wr = label[u] >= 0 && (k.z & (gl ? 1 : 2));
+          // the four grandchildren's lane masks from three ballots
+          const unsigned bw = __ballot_sync(kFull, wr), b1 = __ballot_sync(kFull, wr && (code & 1)),
+                         b2 = __ballot_sync(kFull, wr && (code & 2));
+          const unsigned m[4] = {bw & ~(b1 | b2), b1 & ~b2, b2 & ~b1, b1 & b2};
+          uint32_t base = 0;
+          const unsigned ml = lane == 0 ? m[0] : lane == 1 ? m[1] : lane == 2 ? m[2] : m[3];
+          if (lane < 4 && ml) base = atomicAdd(&s_cur[lane], __popc(ml));
+          uint32_t bs[4];
+#pragma unroll
+          for (int c = 0; c < 4; c++) bs[c] = __shfl_sync(kFull, base, c);
+          if (wr) {
+            const unsigned below = (1u << lane) - 1;
+            const uint32_t bc = code == 0 ? bs[0] : code == 1 ? bs[1] : code == 2 ? bs[2] : bs[3];
+            const unsigned mc = code == 0 ? m[0] : code == 1 ? m[1] : code == 2 ? m[2] : m[3];
+            const uint32_t rk = bc + __popc(mc & below);
+            const uint32_t pos = code == 0 ? A + rk : code == 1 ? M - 1 - rk : code == 2 ? M + rk : B - 1 - rk;
+            store_row<BS>(a.bins_out, a.pstride, pos, r[u]);
+            __stcs(a.lab_out + pos, (uint8_t)label[u]);
+          }
+        }
+        if (more) {
+#pragma unroll
+          for (int u = 0; u < kPartUnroll; u++) {
+            r[u] = rn[u];
+            label[u] = labn[u];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && visits < a.max_visits) {  // this parent's share and its four pieces
+      int32_t *v = my_visits + 8 * visits;
+      v[0] = s_first;
+      v[1] = (int32_t)A;
+      v[2] = (int32_t)B;
+      v[3] = (int32_t)(M - A);
+      v[4] = (int32_t)s_cur[0];
+      v[5] = (int32_t)s_cur[1];
+      v[6] = (int32_t)s_cur[2];
+      v[7] = (int32_t)s_cur[3];
+    }
+    visits++;
+    p0 = pe;
+  }
+}
+
 // ------------------------------------------------------------ histogram --
 constexpr int kHistThreads = 1024;
 constexpr int kHistUnroll = ADAPT_HIST_UNROLL;  // rows in flight per thread (latency-bound otherwise)
@@ -291,7 +548,8 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
             w = *reinterpret_cast<const unsigned short *>(a.bins_in + (size_t)row * 2);
           else
             w = a.bins_in[row];
-          const int lk = (int)__ldg(m + a.lab_in[row]) - k0;
+          const uint32_t lb = a.lab_in[row];
+          const int lk = (!a.tagged ? (int)__ldg(m + lb) : (lb & 0x80u) ? (int)__ldg(m + (lb & 0x7Fu)) : 255) - k0;
           const uint32_t wv = a.w_in ? a.w_in[row] : 1u;
           if ((unsigned)lk >= (unsigned)kn) continue;
 #pragma unroll
@@ -304,7 +562,10 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
     }
     {
       const uint8_t *m = a.cmaps + (size_t)first.cmap * C;
-      for (int k = tid; k < C; k += blockDim.x) s_cmap[k] = m[k];
+      if (a.tagged)  // only labels marked by the TAG pass (bit 7) count
+        for (int k = tid; k < kMaxC + 1; k += blockDim.x) s_cmap[k] = k >= 128 && k - 128 < C ? m[k - 128] : 255;
+      else
+        for (int k = tid; k < C; k += blockDim.x) s_cmap[k] = m[k];
     }
     uint32_t abase[4];
     int gcount = 0;
@@ -526,7 +787,9 @@ __global__ void __launch_bounds__(256) hist_flat_kernel(HistArgs a) {
     Row<BS> r;
     load_row<BS>(a.bins_in, a.pstride, row, r);
     const int kcn = sg.ncls;
-    const int lk = (int)__ldg(a.cmaps + (size_t)sg.cmap * a.C + a.lab_in[row]);
+    const uint32_t lb = a.lab_in[row];
+    if (a.tagged && !(lb & 0x80u)) continue;  // not the direct child's row
+    const int lk = (int)__ldg(a.cmaps + (size_t)sg.cmap * a.C + (a.tagged ? lb & 0x7Fu : lb));
     const uint32_t wv = a.w_in ? a.w_in[row] : 1u;
     uint32_t *dst = a.H + a.soff[sg.hslot] + lk;
 #pragma unroll
@@ -547,13 +810,66 @@ __global__ void __launch_bounds__(256) hist_flat_kernel(HistArgs a) {
 // applies to the same records (engine.cpp decide, R10 / R11): a node splits
 // when depth < D, it has a cut, and more than one class is present; a child
 // stays when depth + 1 < D and it holds more than one class.
+// node j's split (feat, rank) and which children stay (write bits), from its record
+__device__ __forceinline__ int decide_node(const uint8_t *res, const int64_t *rec_off, const int32_t *node_kc,
+                                           const int32_t *node_depth, int D, int j, bool last_rule, int *feat,
+                                           int *thr, int *side) {
+  const NodeRes *nr = reinterpret_cast<const NodeRes *>(res + rec_off[j]);
+  const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);
+  const int kc = node_kc[j];
+  const uint32_t *cLd = Pd + kc;
+  int np = 0, npl = 0, npr = 0;
+  for (int k = 0; k < kc; k++) {
+    const uint32_t p = Pd[k], l = cLd[k];
+    np += p > 0;
+    npl += l > 0;
+    npr += p - l > 0;
+  }
+  const int depth = node_depth[j];
+  int write = 0;
+  *side = -1;
+  if (depth < D && np > 1 && nr->valid) {
+    write = (depth + 1 < D && npl > 1 ? 1 : 0) | (depth + 1 < D && npr > 1 ? 2 : 0);
+    // the direct child: the smaller when both stay (ties left — the host's rule)
+    *side = write == 3 ? (nr->nL <= nr->n - nr->nL ? 0 : 1) : write == 1 ? 0 : write == 2 ? 1 : -1;
+    // children on the LAST frontier level (depth D - 1) are never partitioned
+    // again: only the direct child's rows are needed
+    if (last_rule && depth + 2 == D && write == 3) write = *side == 0 ? 1 : 2;
+    *feat = nr->feat;
+    *thr = nr->b_lo;
+  }
+  return write;
+}
+
+__global__ void __launch_bounds__(256) decide_kids_kernel(const int2 *kid_j, int nseg, const uint8_t *res,
+                                                          const int64_t *rec_off, const int32_t *node_kc,
+                                                          const int32_t *node_depth, int D, int4 *kids) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nseg) return;
+  const int2 jj = kid_j[i];
+#pragma unroll
+  for (int c = 0; c < 2; c++) {
+    const int j = c ? jj.y : jj.x;
+    int feat = -1, thr = 0, side = -1, write = 0;
+    if (j >= 0) write = decide_node(res, rec_off, node_kc, node_depth, D, j, true, &feat, &thr, &side);
+    kids[2 * i + c] = make_int4(write ? feat : -1, thr, write, 0);
+  }
+}
+
 __global__ void __launch_bounds__(256) decide_segs_kernel(Seg *segs, int nseg, const uint8_t *res,
                                                           const int64_t *rec_off, const int32_t *node_kc,
-                                                          const int32_t *node_depth, int D) {
+                                                          const int32_t *node_depth, int D, int tag) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nseg) return;
   Seg &sg = segs[i];
   const int j = sg.direct;
+  if (tag) {  // TAG pass: both children's rows are marked / counted; hslot = the direct side
+    int feat = -1, thr = 0, side = -1;
+    sg.write = decide_node(res, rec_off, node_kc, node_depth, D, j, false, &feat, &thr, &side);
+    if (sg.write) sg.feat = feat, sg.thr = thr;
+    sg.hslot = side;
+    return;
+  }
   const NodeRes *nr = reinterpret_cast<const NodeRes *>(res + rec_off[j]);
   const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);
   const int kc = node_kc[j];
@@ -589,9 +905,46 @@ void launch_build_hist_segs(const SegBuildArgs &a, cudaStream_t s) {
 
 
 void launch_decide_segs(Seg *segs, int nseg, const uint8_t *res, const int64_t *rec_off,
-                        const int32_t *node_kc, const int32_t *node_depth, int D, cudaStream_t s) {
+                        const int32_t *node_kc, const int32_t *node_depth, int D, cudaStream_t s, int tag) {
   if (nseg == 0) return;
-  decide_segs_kernel<<<(nseg + 255) / 256, 256, 0, s>>>(segs, nseg, res, rec_off, node_kc, node_depth, D); ++g_kernel_launches;
+  decide_segs_kernel<<<(nseg + 255) / 256, 256, 0, s>>>(segs, nseg, res, rec_off, node_kc, node_depth, D, tag); ++g_kernel_launches;
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_decide_kids(const int2 *kid_j, int nseg, const uint8_t *res, const int64_t *rec_off,
+                        const int32_t *node_kc, const int32_t *node_depth, int D, int4 *kids, cudaStream_t s) {
+  if (nseg == 0) return;
+  decide_kids_kernel<<<(nseg + 255) / 256, 256, 0, s>>>(kid_j, nseg, res, rec_off, node_kc, node_depth, D, kids); ++g_kernel_launches;
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_tag(const PartArgs &a, cudaStream_t s) {
+  if (a.total_rows == 0 || a.nseg == 0) return;
+  switch (a.BS) {
+#define CASE(B)                                                                               \
+  case B:                                                                                     \
+    tag_kernel<B><<<a.nranges, kPartThreads, 0, s>>>(a); ++g_kernel_launches;                 \
+    break;
+    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
+#undef CASE
+    default:
+      throw Error(-1, "bad bins stride");
+  }
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_partition4(const PartArgs &a, cudaStream_t s) {
+  if (a.total_rows == 0 || a.nseg == 0) return;
+  switch (a.BS) {
+#define CASE(B)                                                                               \
+  case B:                                                                                     \
+    partition4_kernel<B><<<a.nranges, kPartThreads, 0, s>>>(a); ++g_kernel_launches;          \
+    break;
+    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
+#undef CASE
+    default:
+      throw Error(-1, "bad bins stride");
+  }
   CUDA_CHECK(cudaGetLastError());
 }
 

@@ -1,0 +1,17 @@
+mkdir -p gpurun_out
+export PATH=/usr/local/cuda/bin:$PATH
+for mode in two one; do
+  if [ $mode = one ]; then export ADAPT_ONE_LEVEL=1; fi
+  ADAPT_PROFILE_LEVELS=1 timeout 600 python bench.py --steps 3 --warmup 2 --no-cpu --no-e2e --no-records --no-c5 --no-kfold --no-c2 --no-proxy > gpurun_out/bench_levels_$mode.log 2>&1; echo "bench $mode rc=$?"
+  python - $mode <<'PY'
+import json,sys
+d=json.loads(open(f'gpurun_out/bench_levels_{sys.argv[1]}.log').read().strip().splitlines()[-1])
+print(sys.argv[1], d['ms_per_step'], {k: v for k, v in d['phase_ms_per_step'].items()})
+for i,l in enumerate(d['levels']): print(i, l['rows_hist'], l['rows_part'], l['ms'])
+PY
+  timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-records --no-c5 --no-kfold --no-c2 --no-proxy > gpurun_out/bench_plain_$mode.log 2>&1; echo "plain $mode rc=$?"; python -c "
+import json; d=json.loads(open('gpurun_out/bench_plain_$mode.log').read().strip().splitlines()[-1]); print('$mode', d['ms_per_step'], d['level_loop_roofline'])"
+done
+unset ADAPT_ONE_LEVEL
+NCU_KERNEL=tag_kernel NCU_SKIP=1 BENCH_ARGS="--no-c5 --no-kfold --no-c2 --no-proxy" bash scripts/gpu_ncu_one.sh
+NCU_KERNEL=partition4_kernel NCU_SKIP=1 BENCH_ARGS="--no-c5 --no-kfold --no-c2 --no-proxy" bash scripts/gpu_ncu_one.sh
