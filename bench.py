@@ -725,7 +725,8 @@ def main():
                 "peak_source": peak_src,
                 "alg_bytes_per_launch": (alg_dom or 0) / max(d["launches"], 1),
                 "alg_bytes_rule": "SURVEY 8(d): ingest 4F+4V+F+1 per row; partition / hist (F+1) per row "
-                                  "they process; select 4F+4 per vector",
+                                  "they process (a tagged level's histogram reads its parents' rows); "
+                                  "select 4F+4 per vector",
                 "ms_per_launch": d["ms"] / max(d["launches"], 1),
                 "impl_bytes_per_launch": d["bytes"] / max(d["launches"], 1),
                 "impl_frac": (impl / peak) if impl else None}
@@ -735,7 +736,10 @@ def main():
                                                    "winner", "decide", "fused"))
     loop_rows = sum((lv["rows_part"] if i else n) for i, lv in enumerate(levels) if lv["nodes"])
     loop_bytes = (F + 1) * loop_rows * world
-    level_loop = {"survey_bytes_per_step": loop_bytes, "ms_per_step": loop_ms,
+    level_loop = {"schedule": ("partition every level" if os.environ.get("ADAPT_ONE_LEVEL") or world > 1
+                               else "two-level row moves: TAG + MOVE4, partition into the last level"),
+                  "phases": "partition, tag, hist, zero, subtract, split, winner, decide",
+                  "survey_bytes_per_step": loop_bytes, "ms_per_step": loop_ms,
                   "achieved_gbs": loop_bytes / (loop_ms / 1e3) / 1e9 if loop_ms else None,
                   "frac": loop_bytes / (loop_ms / 1e3) / 1e9 / peak if loop_ms else None}
     ingest_bytes = (4 * F + 4 * V + F + 1) * N

@@ -191,11 +191,11 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition_kernel
           uint32_t base = 0;
           if (lane == 0 && ml) base = atomicAdd(&s_cur[0], __popc(ml));
           if (lane == 1 && mr) base = atomicAdd(&s_cur[1], __popc(mr));
-          const uint32_t bl = __shfl_sync(kFull, base, 0), br = __shfl_sync(kFull, base, 1);
-          const unsigned below = (1u << lane) - 1;
           const bool wl = (ml >> lane) & 1, wr = (mr >> lane) & 1;
+          const uint32_t bb = __shfl_sync(kFull, base, wl ? 0 : 1);  // lane 0: left base, 1: right
+          const unsigned below = (1u << lane) - 1;
           if (wl || wr) {
-            const uint32_t pos = wl ? A + bl + __popc(ml & below) : B - 1 - (br + __popc(mr & below));
+            const uint32_t pos = wl ? A + bb + __popc(ml & below) : B - 1 - (bb + __popc(mr & below));
             store_row<BS>(a.bins_out, a.pstride, pos, r[u]);
             __stcs(a.lab_out + pos, (uint8_t)label[u]);
             if (a.w_out) __stcs(a.w_out + pos, wgt[u]);
@@ -444,12 +444,9 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition4_kerne
           uint32_t base = 0;
           const unsigned ml = lane == 0 ? m[0] : lane == 1 ? m[1] : lane == 2 ? m[2] : m[3];
           if (lane < 4 && ml) base = atomicAdd(&s_cur[lane], __popc(ml));
-          uint32_t bs[4];
-#pragma unroll
-          for (int c = 0; c < 4; c++) bs[c] = __shfl_sync(kFull, base, c);
+          const uint32_t bc = __shfl_sync(kFull, base, code);  // lane c holds code c's base
           if (wr) {
             const unsigned below = (1u << lane) - 1;
-            const uint32_t bc = code == 0 ? bs[0] : code == 1 ? bs[1] : code == 2 ? bs[2] : bs[3];
             const unsigned mc = code == 0 ? m[0] : code == 1 ? m[1] : code == 2 ? m[2] : m[3];
             const uint32_t rk = bc + __popc(mc & below);
             const uint32_t pos = code == 0 ? A + rk : code == 1 ? M - 1 - rk : code == 2 ? M + rk : B - 1 - rk;

@@ -14,7 +14,8 @@ import json
 import os
 
 rnd, launches, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
-PHASE = {"partition_kernel": "partition", "hist_kernel": "hist", "label_bin_kernel": "ingest",
+PHASE = {"partition_kernel": "partition", "partition4_kernel": "partition", "tag_kernel": "tag",
+         "hist_kernel": "hist", "label_bin_kernel": "ingest",
          "discover_kernel": "discover", "select_kernel_c": "select", "select_kernel_h": "select",
          "split_kernel": "split"}
 traffic = {}
@@ -32,14 +33,21 @@ for r in rows:
     d = per.setdefault(name, [0, 0.0])
     d[0] += 1
     d[1] += ns / 1e6
+# bench.py runs the timed step and then a separately profiled step (per-phase
+# events): the list holds whole steps, one ingest launch each
+nst = max(1, per.get("label_bin_kernel", [1, 0])[0])
+for v in per.values():
+    v[0] /= nst
+    v[1] /= nst
 tot = sum(v[1] for v in per.values())
-out += ["## Launch list (one step, serialised, cold-cache)", "",
+out += ["## Launch list (per step, serialised, cold-cache)", "",
         f"Source: `{launches}` — `ncu --metrics gpu__time_duration.sum --clock-control none "
-        "python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-records --no-c5 --no-kfold --no-c2 --no-proxy`.", "",
+        "python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-records --no-c5 --no-kfold --no-c2 --no-proxy` "
+        f"({nst} steps in the list: the timed step and bench.py's profiled step; figures per step).", "",
         "| kernel | launches | ms | share of step |", "|---|---:|---:|---:|"]
 for k, (n, ms) in sorted(per.items(), key=lambda x: -x[1][1]):
-    out.append(f"| {k} | {n} | {ms:.3f} | {100 * ms / tot:.1f}% |")
-out += [f"| **total** | {sum(v[0] for v in per.values())} | {tot:.3f} | 100% |", ""]
+    out.append(f"| {k} | {n:g} | {ms:.3f} | {100 * ms / tot:.1f}% |")
+out += [f"| **total** | {sum(v[0] for v in per.values()):g} | {tot:.3f} | 100% |", ""]
 
 # ---- full captures ----
 out += ["## Full captures (`ncu --set full --clock-control none --import-source on`)", "",
@@ -63,9 +71,14 @@ for rep in reps:
     kname = re.sub(r"\(.*", "", d.get("Kernel Name", "?"))
     base = re.sub(r"<.*", "", kname.split("::")[-1])
     if base in PHASE and "c5" not in os.path.basename(rep):  # the C4 step's kernels
-        traffic[PHASE[base]] = {"dram_bytes_per_launch": (rd + wr) * 1e9, "ms": dur,
-                                "source": f"profiles/round{rnd}/ncu_summary.md",
-                                "capture": os.path.basename(rep)}
+        # several captures of one phase (e.g. a tagged and a plain histogram
+        # level): their mean stands for the phase's average launch
+        t = traffic.setdefault(PHASE[base], {"dram_bytes_per_launch": 0.0, "ms": 0.0, "n": 0,
+                                             "source": f"profiles/round{rnd}/ncu_summary.md", "capture": ""})
+        t["dram_bytes_per_launch"] = (t["dram_bytes_per_launch"] * t["n"] + (rd + wr) * 1e9) / (t["n"] + 1)
+        t["ms"] = (t["ms"] * t["n"] + dur) / (t["n"] + 1)
+        t["n"] += 1
+        t["capture"] = (t["capture"] + " + " if t["capture"] else "") + os.path.basename(rep)
     out.append(f"| `{rep.split('/')[-1]}` | {kname} | {dur:.3f} | {rd:.3f} | {wr:.3f} | "
                f"{(rd + wr) / dur:.2f} | "
                f"{float(d.get('dram__cycles_active.avg.pct_of_peak_sustained_elapsed', 0)):.0f} | "

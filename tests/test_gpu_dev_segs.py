@@ -1,4 +1,5 @@
-"""Histogram segments built on the device vs on the host.
+"""Histogram segments built on the device vs on the host; two-level row moves
+vs the per-level partition.
 
 On one rank without weights the level loop plans every direct node's size from
 its parent's winner record and lets `build_hist_segs_kernel` turn the
@@ -7,7 +8,15 @@ between the partition and the histogram pass).  ADAPT_HOST_SEGS=1 forces the
 host-built segments (the path multi-rank and forest runs take).  Both must give
 byte-identical trees: a single tree (C3, depth 12), a deep tree on random data
 (ragged small nodes, the flat pass), and the multi-root frontier of
-adapt_train_many (C2's three regions)."""
+adapt_train_many (C2's three regions).
+
+Two-level row moves (the default on one rank): the TAG pass marks
+the rows, the next level's histogram counts the marked rows from the parents'
+pieces and MOVE4 moves them one level later.  ADAPT_ONE_LEVEL=1 restores a
+partition at every level, ADAPT_TAG_LAST=1 tags into the last frontier level
+too; all schedules must give byte-identical trees, including shallow depths
+where the schedule degenerates (depth 2: no TAG pass; depth 3: MOVE4 straight
+into the last level)."""
 import os
 import subprocess
 import sys
@@ -44,6 +53,8 @@ rng = np.random.default_rng(5)
 Xr = rng.integers(0, 40, size=(60_000, 6)).astype(np.float32)
 Tr = rng.random((60_000, 9)).astype(np.float32)
 tree("rnd", Xr, Tr, "dtree,depth=18")
+for d in (2, 3, 4, 5):
+    tree("rnd%d" % d, Xr[: 20_000 * d], Tr[: 20_000 * d], "dtree,depth=%d" % d)
 cfg = synth.CONFIGS["C2"]
 X2, T2 = synth.generate(cfg, 0, cfg.N)
 hs = []
@@ -63,8 +74,12 @@ print("bytes", [len(o) for o in out])
 """
 
 
+_runs = [0]
+
+
 def _run(tmp_path, env_extra):
-    f = tmp_path / f"o{len(env_extra)}.npy"
+    _runs[0] += 1
+    f = tmp_path / f"o{_runs[0]}.npy"
     env = dict(os.environ, **env_extra)
     p = subprocess.run([sys.executable, "-c", CHILD, ROOT, str(f)], check=True, env=env,
                        timeout=600, capture_output=True, text=True)
@@ -76,3 +91,12 @@ def test_device_built_segments_match_host_built(tmp_path):
     host, log_h = _run(tmp_path, {"ADAPT_HOST_SEGS": "1"})
     assert len(dev) > 1000, log_d
     assert dev == host, (log_d, log_h)
+
+
+def test_two_level_moves_match_one_level(tmp_path):
+    two, log_t = _run(tmp_path, {})
+    one, log_o = _run(tmp_path, {"ADAPT_ONE_LEVEL": "1"})
+    tag_last, log_l = _run(tmp_path, {"ADAPT_TAG_LAST": "1"})
+    assert len(two) > 1000, log_t
+    assert two == one, (log_t, log_o)
+    assert two == tag_last, (log_t, log_l)

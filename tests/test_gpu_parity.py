@@ -289,6 +289,20 @@ def test_max_distinct_and_classes():
     full_parity(X, T, 3)
 
 
+@pytest.mark.parametrize("V", [127, 128])
+def test_two_level_class_limit(V):
+    """Two-level row moves mark rows with label bit 7, so they run only below 128
+    classes: V = 127 takes the TAG / MOVE4 schedule with class slabs (4 x 256
+    values x 127 classes exceed one CTA), V = 128 the per-level partition; both
+    against the oracle, several levels deep."""
+    rng = np.random.default_rng(11 + V)
+    n = 90000
+    X = rng.integers(0, 256, size=(n, 8)).astype(np.float32)
+    T = rng.random((n, V)).astype(np.float32)
+    T[:, : V // 4] *= 0.9  # fewer classes win often: deeper nodes hold few classes
+    full_parity(X, T, 6)
+
+
 @pytest.mark.parametrize("depth", [1, 12, 16])
 def test_select_synthetic_complete_tree(depth):
     # SURVEY §8(d) C5: a complete depth-16 tree (131071 nodes: deeper than the
