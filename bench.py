@@ -736,8 +736,10 @@ def main():
                                                    "winner", "decide", "fused"))
     loop_rows = sum((lv["rows_part"] if i else n) for i, lv in enumerate(levels) if lv["nodes"])
     loop_bytes = (F + 1) * loop_rows * world
-    level_loop = {"schedule": ("partition every level" if os.environ.get("ADAPT_ONE_LEVEL") or world > 1
-                               else "two-level row moves: TAG + MOVE4, partition into the last level"),
+    two_level = (not os.environ.get("ADAPT_ONE_LEVEL") and os.environ.get("ADAPT_TWO_LEVEL") != "0" and world == 1
+                 and (os.environ.get("ADAPT_TWO_LEVEL") == "1" or N >= 1 << 24))
+    level_loop = {"schedule": ("two-level row moves: TAG + MOVE4, partition into the last level" if two_level
+                               else "partition every level"),
                   "phases": "partition, tag, hist, zero, subtract, split, winner, decide",
                   "survey_bytes_per_step": loop_bytes, "ms_per_step": loop_ms,
                   "achieved_gbs": loop_bytes / (loop_ms / 1e3) / 1e9 if loop_ms else None,

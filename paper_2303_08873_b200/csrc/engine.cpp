@@ -1436,9 +1436,17 @@ void train_region(adapt_region *h, cudaStream_t s) {
   const bool rs = hist_comm_rs();
   // two-level row moves: the rows move every other level (TAG
   // pass, then MOVE4 one level later); one rank, unweighted rows, one tree,
-  // classes below 128 (label bit 7 carries the TAG pass's mark)
-  static const bool one_level = getenv("ADAPT_ONE_LEVEL") != nullptr;
-  const bool two_level = !one_level && !w_root && !mr && g_ctx.world == 1 && !rs && C <= 127;
+  // classes below 128 (label bit 7 carries the TAG pass's mark), and a table
+  // large enough for the row passes to dominate (below it the per-level
+  // schedule's device-built segments win: C3 1e6 rows 2.3 vs 3.9 ms).
+  // ADAPT_TWO_LEVEL=1 / =0 forces it on / off (read per train), as does
+  // ADAPT_ONE_LEVEL=1 (off)
+  constexpr uint64_t kTwoLevelMinRows = 1ull << 24;
+  const char *tl_env = getenv("ADAPT_TWO_LEVEL");
+  const bool tl_off = getenv("ADAPT_ONE_LEVEL") != nullptr || (tl_env && atoi(tl_env) == 0);
+  const bool tl_on = tl_env && atoi(tl_env) == 1;
+  const bool two_level = !tl_off && (tl_on || n_total >= kTwoLevelMinRows) && !w_root && !mr && g_ctx.world == 1 &&
+                         !rs && C <= 127;
   if (two_level) h->labT.ensure((size_t)std::max<int64_t>(rows_out, 1) + 64);
   std::vector<int4> pseg_gkids;  // per TAG segment: its parent's grandchildren (LL, LR, RL, RR)
   static const bool per_level = getenv("ADAPT_PROFILE_LEVELS") != nullptr;
@@ -1768,6 +1776,11 @@ void train_region(adapt_region *h, cudaStream_t s) {
           if (e[0] < 0) break;
           const int4 gk = pseg_gkids[e[0]];
           const uint32_t A = (uint32_t)e[1], B = (uint32_t)e[2], M = A + (uint32_t)e[3];
+          // the four pieces must lie inside their regions [A, M) and [M, B)
+          // (the TAG pass's count cL and MOVE4's placement agree)
+          if (e[1] > e[2] || e[3] < 0 || e[3] > e[2] - e[1] || e[4] < 0 || e[5] < 0 || e[6] < 0 || e[7] < 0 ||
+              (int64_t)e[4] + e[5] > e[3] || (int64_t)e[6] + e[7] > (int64_t)e[2] - e[1] - e[3])
+            throw Error(ADAPT_E_CUDA, "internal: MOVE4 share report outside its parent's share");
           if (gk.x >= 0 && e[4] > 0) flat.push_back({(uint32_t)gk.x, A, (uint32_t)e[4]});
           if (gk.y >= 0 && e[5] > 0) flat.push_back({(uint32_t)gk.y, M - (uint32_t)e[5], (uint32_t)e[5]});
           if (gk.z >= 0 && e[6] > 0) flat.push_back({(uint32_t)gk.z, M, (uint32_t)e[6]});

@@ -10,10 +10,11 @@ byte-identical trees: a single tree (C3, depth 12), a deep tree on random data
 (ragged small nodes, the flat pass), and the multi-root frontier of
 adapt_train_many (C2's three regions).
 
-Two-level row moves (the default on one rank): the TAG pass marks
-the rows, the next level's histogram counts the marked rows from the parents'
-pieces and MOVE4 moves them one level later.  ADAPT_ONE_LEVEL=1 restores a
-partition at every level, ADAPT_TAG_LAST=1 tags into the last frontier level
+Two-level row moves (the default on one rank for tables of 2^24
+rows and more; ADAPT_TWO_LEVEL=1 forces it at the sizes here): the TAG pass
+marks the rows, the next level's histogram counts the marked rows from the
+parents' pieces and MOVE4 moves them one level later.  ADAPT_ONE_LEVEL=1 keeps
+a partition at every level, ADAPT_TAG_LAST=1 tags into the last frontier level
 too; all schedules must give byte-identical trees, including shallow depths
 where the schedule degenerates (depth 2: no TAG pass; depth 3: MOVE4 straight
 into the last level)."""
@@ -94,9 +95,9 @@ def test_device_built_segments_match_host_built(tmp_path):
 
 
 def test_two_level_moves_match_one_level(tmp_path):
-    two, log_t = _run(tmp_path, {})
+    two, log_t = _run(tmp_path, {"ADAPT_TWO_LEVEL": "1"})
     one, log_o = _run(tmp_path, {"ADAPT_ONE_LEVEL": "1"})
-    tag_last, log_l = _run(tmp_path, {"ADAPT_TAG_LAST": "1"})
+    tag_last, log_l = _run(tmp_path, {"ADAPT_TWO_LEVEL": "1", "ADAPT_TAG_LAST": "1"})
     assert len(two) > 1000, log_t
     assert two == one, (log_t, log_o)
     assert two == tag_last, (log_t, log_l)

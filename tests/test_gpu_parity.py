@@ -290,7 +290,7 @@ def test_max_distinct_and_classes():
 
 
 @pytest.mark.parametrize("V", [127, 128])
-def test_two_level_class_limit(V):
+def test_two_level_class_limit(V, monkeypatch):
     """Two-level row moves mark rows with label bit 7, so they run only below 128
     classes: V = 127 takes the TAG / MOVE4 schedule with class slabs (4 x 256
     values x 127 classes exceed one CTA), V = 128 the per-level partition; both
@@ -300,6 +300,7 @@ def test_two_level_class_limit(V):
     X = rng.integers(0, 256, size=(n, 8)).astype(np.float32)
     T = rng.random((n, V)).astype(np.float32)
     T[:, : V // 4] *= 0.9  # fewer classes win often: deeper nodes hold few classes
+    monkeypatch.setenv("ADAPT_TWO_LEVEL", "1")  # (the engine reads it per train)
     full_parity(X, T, 6)
 
 
