@@ -634,13 +634,14 @@ struct adapt_region {
   bool trained = false;
   std::vector<int64_t> stats;
   // scratch
-  adapt::DevBuf gkey, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval, lk_keys, lk_mul, lk_skeys,
+  adapt::DevBuf gkey, gcount, flags, lvals, lcnt, avals, acnt, dval, dnval,
       H0, H1, Hg, reso, resall, segs,
       hsegs, visits, slots, triples, nslot, cand, res, hoff, grp, gsoff, cmaps, xa, xb, oa, ob;
   adapt::HostBuf hres, hsmall, hvis, hgat;  // winners, scalars, partition share reports, gathered winners
   adapt::Arena stage_p, stage_a, stage_b, stage_r;  // per-level uploads: partition, its tables,
                                                      // histogram segments, owner split lists
   adapt::Arena stage_k;                  // two-level moves: MOVE4's per-segment children
+  adapt::Arena stage_i;                  // ingest: the value hashes (one upload)
   adapt::DevBuf labT, visits2, kids;     // TAG pass labels, MOVE4 share reports, MOVE4 decisions
   cudaEvent_t sel_evt = nullptr;  // recorded after every device select (upload_tree waits)
   cudaEvent_t win_evt = nullptr;  // a level's winner records are on the host
@@ -1244,6 +1245,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
     h->qmask = qm;
     feat = h->qfeat.as<float>();
   };
+  const uint8_t *lk_tab = nullptr;  // the bin pass's value hashes (device)
+  const uint32_t *lk_mul = nullptr, *lk_sk = nullptr;
   for (int attempt = 0;; attempt++) {
     CUDA_CHECK(cudaMemsetAsync(h->gkey.p, 0xFF, (size_t)F * kGSlots * 4, s));
     CUDA_CHECK(cudaMemsetAsync(h->gcount.p, 0, (size_t)F * 4, s));
@@ -1285,15 +1288,22 @@ void train_region(adapt_region *h, cudaStream_t s) {
     CUDA_CHECK(cudaStreamSynchronize(s));
     const double t_hash = trace ? now_us() : 0;
     {
+      // the GPU waits for these (host threads per feature measured slower:
+      // spawning them costs more than the ~8 us per feature), then ONE pinned
+      // upload of all three tables
       std::vector<uint8_t> tab((size_t)lookup_table_bytes(F));
       std::vector<uint32_t> mul((size_t)2 * F), skeys((size_t)F * lookup_slots());
       for (int f = 0; f < F; f++)
         if (!build_value_hash(&h->val[(size_t)f * kMaxBins], h->nval[f], &mul[2 * f],
                               &tab[(size_t)f * lookup_table_bytes(1)], &skeys[(size_t)f * lookup_slots()]))
           throw Error(ADAPT_E_CUDA, "cannot build the value hash of feature " + std::to_string(f));
-      h2d(h->lk_keys, tab, s);
-      h2d(h->lk_mul, mul, s);
-      h2d(h->lk_skeys, skeys, s);
+      Arena &si = h->stage_i;
+      si.reset();
+      const size_t o_tab = si.put(tab), o_mul = si.put(mul), o_sk = si.put(skeys);
+      si.flush(s);
+      lk_tab = si.ptr<uint8_t>(o_tab);  // (valid until the next train's upload)
+      lk_mul = si.ptr<uint32_t>(o_mul);
+      lk_sk = si.ptr<uint32_t>(o_sk);
     }
     if (trace)
       fprintf(stderr, "[adapt] ingest attempt %d: discovery..tables %.0f us, perfect hashes %.0f us (GPU idle)\n",
@@ -1301,8 +1311,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     CUDA_CHECK(cudaMemsetAsync(h->flags.p, 0, 16, s));
     {
       Phase ph("ingest", s, (double)n * (4.0 * F + 4.0 * V + F + 1));  // algorithmic
-      launch_label_bin(feat, times, n, F, V, BS, h->lk_keys.as<uint8_t>(), h->lk_mul.as<uint32_t>(),
-                       h->lk_skeys.as<uint32_t>(), sampled && attempt == 0 ? 1 : 0,
+      launch_label_bin(feat, times, n, F, V, BS, lk_tab, lk_mul, lk_sk, sampled && attempt == 0 ? 1 : 0,
                        h->flags.as<uint32_t>(),
                        h->bins.as<uint8_t>(), pstride, h->labels.as<uint8_t>(), s);
     }
@@ -1738,7 +1747,10 @@ void train_region(adapt_region *h, cudaStream_t s) {
     // direct node's size is its parent's winner count, so the histogram pass
     // is queued behind the partition without waiting for its share reports)
     static const bool host_segs = getenv("ADAPT_HOST_SEGS") != nullptr;
-    const bool dev = level > 0 && pst.mode == 0 && !w_root && g_ctx.world == 1 && !rs && !host_segs;
+    // (small levels: the host-built segments are cheaper than the builder
+    // kernel's launch — C3's 1e6 rows: 2.17 vs 2.35 ms per train)
+    const bool dev = level > 0 && pst.mode == 0 && !w_root && g_ctx.world == 1 && !rs && !host_segs &&
+                     (pst.rows_part >= (1 << 22) || getenv("ADAPT_DEV_SEGS") != nullptr);
     if (tagged) {
       hist_bins = pa.bins_in;
       hist_lab = h->labT.as<uint8_t>();
@@ -1906,9 +1918,20 @@ void train_region(adapt_region *h, cudaStream_t s) {
       const int nranges = (int)std::max<int64_t>(1, std::min<int64_t>((htotal + 4095) / 4096,
                                                                       std::max(1, sms / ngroups)));
       tick("arena_reset");
-      const std::vector<HistCta> ctas = dev ? plan_hist_ctas(pnodes, hsegs, htotal, gcost, nranges * ngroups)
-                                            : plan_hist_ctas(hsegs, htotal, gcost, nranges * ngroups,
-                                                             tagged ? &cf_slot : nullptr);
+      // small levels (C3's 1e6-row table: every level is launch/latency-bound)
+      // take uniform row ranges per group, groups interleaved; the cost-balanced
+      // plan pays from a few million rows on (C3: 3.5 vs 2.4 ms per train)
+      constexpr uint32_t kPlanMinRows = 1u << 22;
+      std::vector<HistCta> ctas;
+      if (htotal >= kPlanMinRows) {
+        ctas = dev ? plan_hist_ctas(pnodes, hsegs, htotal, gcost, nranges * ngroups)
+                   : plan_hist_ctas(hsegs, htotal, gcost, nranges * ngroups, tagged ? &cf_slot : nullptr);
+      } else {
+        const uint32_t R = (htotal + nranges - 1) / nranges;
+        for (int r = 0; r < nranges; r++)
+          for (int g = 0; g < ngroups; g++)
+            ctas.push_back(HistCta{g, std::min<uint32_t>(r * R, htotal), std::min<uint32_t>((r + 1) * R, htotal), -1});
+      }
       tick("plan");
       const size_t o_hsegs = sb.put(hsegs), o_fsegs = sb.put(fsegs), o_ctas = sb.put(ctas),
                    o_bseg = sb.put(bseg);

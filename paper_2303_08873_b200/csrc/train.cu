@@ -430,14 +430,13 @@ __global__ void __launch_bounds__(256)
   __shared__ SplitCand sc[kMaxF];  // the node's F candidates, loaded in parallel
   for (int f = t; f < F; f += blockDim.x) sc[f] = cand[(size_t)node * F + f];
   __syncthreads();
-  if (t == 0) {
-    int bf = -1;
+  if (t < 32) {  // warp argmax over the F candidates (ties -> lowest feature)
     Key bk;
     bk.valid = 0;
     bk.idx = 0x7fffffff;
     bk.hi = bk.lo = 0;
     bk.den = 1;
-    for (int f = 0; f < F; f++) {
+    for (int f = t; f < F; f += 32) {
       const SplitCand &c = sc[f];
       Key k;
       k.valid = c.valid;
@@ -445,14 +444,19 @@ __global__ void __launch_bounds__(256)
       k.hi = c.num_hi;
       k.lo = c.num_lo;
       k.den = c.den;
-      if (k.valid && better(k, bk)) {
-        bk = k;
-        bf = f;
-      }
+      if (k.valid && better(k, bk)) bk = k;
     }
-    s_f = bf;
-    if (bf >= 0) s_c = sc[bf];
-    s_n = 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const Key other = shfl_key(bk, t ^ o);
+      if (better(other, bk)) bk = other;
+    }
+    if (t == 0) {
+      const int bf = bk.valid ? bk.idx : -1;
+      s_f = bf;
+      if (bf >= 0) s_c = sc[bf];
+      s_n = 0;
+    }
   }
   __syncthreads();
   const int fsel = s_f >= 0 ? s_f : 0;

@@ -4,7 +4,8 @@ vs the per-level partition.
 On one rank without weights the level loop plans every direct node's size from
 its parent's winner record and lets `build_hist_segs_kernel` turn the
 partition's share reports into the histogram segments (no host round trip
-between the partition and the histogram pass).  ADAPT_HOST_SEGS=1 forces the
+between the partition and the histogram pass; levels of 2^22 rows and more, or
+any level with ADAPT_DEV_SEGS=1 as here).  ADAPT_HOST_SEGS=1 forces the
 host-built segments (the path multi-rank and forest runs take).  Both must give
 byte-identical trees: a single tree (C3, depth 12), a deep tree on random data
 (ragged small nodes, the flat pass), and the multi-root frontier of
@@ -88,7 +89,7 @@ def _run(tmp_path, env_extra):
 
 
 def test_device_built_segments_match_host_built(tmp_path):
-    dev, log_d = _run(tmp_path, {})
+    dev, log_d = _run(tmp_path, {"ADAPT_DEV_SEGS": "1"})
     host, log_h = _run(tmp_path, {"ADAPT_HOST_SEGS": "1"})
     assert len(dev) > 1000, log_d
     assert dev == host, (log_d, log_h)
