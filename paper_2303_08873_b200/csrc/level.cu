@@ -382,8 +382,12 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) tag_kernel(PartA
 // share): left-left rows from A up, left-right from M down, right-left from M
 // up, right-right from B down, positions from warp-aggregated cursors as in
 // partition_kernel; rows of a grandchild that is not in the frontier stay behind.
+#ifndef ADAPT_P4_UNROLL
+#define ADAPT_P4_UNROLL 2
+#endif
 template <int BS>
 __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition4_kernel(PartArgs a) {
+  constexpr int kPartUnroll = ADAPT_P4_UNROLL;  // rows in flight per thread (this kernel)
   __shared__ uint32_t s_cur[4];
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t R = (a.total_rows + gridDim.x - 1) / gridDim.x;
@@ -442,9 +446,22 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition4_kerne
                          b2 = __ballot_sync(kFull, wr && (code & 2));
           const unsigned m[4] = {bw & ~(b1 | b2), b1 & ~b2, b2 & ~b1, b1 & b2};
           uint32_t base = 0;
-          const unsigned ml = lane == 0 ? m[0] : lane == 1 ? m[1] : lane == 2 ? m[2] : m[3];
+          const unsigned ml = (lane & 2) ? ((lane & 1) ? m[3] : m[2]) : ((lane & 1) ? m[1] : m[0]);
           if (lane < 4 && ml) base = atomicAdd(&s_cur[lane], __popc(ml));
           const uint32_t bc = __shfl_sync(kFull, base, code);  // lane c holds code c's base
+          // the lane's position without branches (selects on the code bits):
+          // codes 0 / 2 grow up from A / M, codes 1 / 3 down from M / B
+#ifndef ADAPT_P4_BRANCHY
+          const bool c1 = code & 1, c2 = code & 2;
+          const unsigned mc = c2 ? (c1 ? m[3] : m[2]) : (c1 ? m[1] : m[0]);
+          const uint32_t rk = bc + __popc(mc & ((1u << lane) - 1));
+          const uint32_t edge = c2 ? (c1 ? B : M) : (c1 ? M : A);
+          const uint32_t pos = c1 ? edge - 1 - rk : edge + rk;
+          if (wr) {
+            store_row<BS>(a.bins_out, a.pstride, pos, r[u]);
+            __stcs(a.lab_out + pos, (uint8_t)label[u]);
+          }
+#else
           if (wr) {
             const unsigned below = (1u << lane) - 1;
             const unsigned mc = code == 0 ? m[0] : code == 1 ? m[1] : code == 2 ? m[2] : m[3];
@@ -453,6 +470,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition4_kerne
             store_row<BS>(a.bins_out, a.pstride, pos, r[u]);
             __stcs(a.lab_out + pos, (uint8_t)label[u]);
           }
+#endif
         }
         if (more) {
 #pragma unroll
