@@ -57,6 +57,9 @@ Tr = rng.random((60_000, 9)).astype(np.float32)
 tree("rnd", Xr, Tr, "dtree,depth=18")
 for d in (2, 3, 4, 5):
     tree("rnd%d" % d, Xr[: 20_000 * d], Tr[: 20_000 * d], "dtree,depth=%d" % d)
+# 1-3 features: bins rows of 1, 2 and 4 bytes (the single-plane layouts)
+for F in (1, 2, 3):
+    tree("f%d" % F, np.ascontiguousarray(Xr[:, :F]), Tr, "dtree,depth=9")
 cfg = synth.CONFIGS["C2"]
 X2, T2 = synth.generate(cfg, 0, cfg.N)
 hs = []
