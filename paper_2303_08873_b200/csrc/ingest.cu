@@ -261,7 +261,13 @@ struct LabelBinArgs {
 template <int VQ, int FQ>
 __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int F = a.F, V = a.V, BS = a.BS, TR = a.TR, P = a.P;
+  // the compile-time shape (VQ, FQ > 0: C4's 48 variants and 16 features, 4
+  // lanes per row, 256-row tiles) folds the tile / stage address arithmetic
+  constexpr bool kFixed = VQ > 0 && FQ > 0;
+  const int P = kFixed ? 4 : a.P;
+  const int TR = kFixed ? kIngestThreads / 4 : a.TR;
+  const int V = kFixed ? 16 * VQ : a.V, F = kFixed ? 16 * FQ : a.F;
+  const int BS = kFixed ? 16 * FQ : a.BS;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
   uint64_t *empty = full + kStages;
   uint32_t *lmul = reinterpret_cast<uint32_t *>(smem + 128);  // [F][2]
@@ -310,9 +316,9 @@ __global__ void __launch_bounds__(kIngestThreads, 1) label_bin_kernel(LabelBinAr
 
   uint32_t local_flags = 0;
   const int r = tid / P, q = tid % P;
-  const bool vec_t = (V & 3) == 0;
+  const bool vec_t = kFixed || (V & 3) == 0;
   const int per = F / P;  // features per lane when F % P == 0
-  const bool vec_f = (F % P) == 0 && (per & 3) == 0;
+  const bool vec_f = kFixed || ((F % P) == 0 && (per & 3) == 0);
   // perfect hash: the displacement, then the slot's rank and key (independent
   // loads); a key that is not the slot's is a value the discovery (sample)
   // missed: flagged, the caller re-discovers the whole table
