@@ -74,6 +74,18 @@ __device__ __forceinline__ void store_row(uint8_t *__restrict__ base, size_t pst
   }
 }
 
+// predicated streaming stores (no divergent branch around a row's stores);
+// no "memory" clobber: nothing in these kernels reads what they write, and a
+// clobber would pin the next batch's loads behind every store
+__device__ __forceinline__ void st_cs_if(bool p, void *addr, uint32_t v) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %0, 0;\n@q st.global.cs.b32 [%1], %2;\n}" ::"r"((uint32_t)p), "l"(addr),
+               "r"(v));
+}
+__device__ __forceinline__ void st_cs_if_u8(bool p, void *addr, uint32_t v) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %0, 0;\n@q st.global.cs.u8 [%1], %2;\n}" ::"r"((uint32_t)p), "l"(addr),
+               "r"(v));
+}
+
 // w[i] for a runtime i through a tree of register selects (N = power of 2):
 // every array access has a compile-time index, so nothing goes to local memory
 template <int N>
@@ -164,18 +176,15 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition_kernel
                       uint8_t(&ww)[kPartUnroll]) {
 #pragma unroll
         for (int u = 0; u < kPartUnroll; u++) {
+          // branch-free: a lane past the segment's end re-reads its last row
+          // (q clamped; q0 < q1 here) and is marked invalid by its label
           const uint32_t q = qb + u * blockDim.x + tid;
-          ll[u] = -1;
-          ww[u] = 1;
-          if (q < q1) {
-            load_row<BS>(a.bins_in, a.pstride, sg.off + q, rr[u]);
-            ll[u] = __ldcs(a.lab_in + sg.off + q);
-            // bootstrap weight (forests): rows drawn 0 times leave the tree here
-            if (a.w_in) ww[u] = __ldcs(a.w_in + sg.off + q);
-          } else {
-#pragma unroll
-            for (int i = 0; i < Row<BS>::N; i++) rr[u].w[i] = 0;
-          }
+          const uint32_t qc = min(q, q1 - 1);
+          load_row<BS>(a.bins_in, a.pstride, sg.off + qc, rr[u]);
+          const int lb = __ldcs(a.lab_in + sg.off + qc);
+          ll[u] = q < q1 ? lb : -1;
+          // bootstrap weight (forests): rows drawn 0 times leave the tree here
+          ww[u] = a.w_in ? __ldcs(a.w_in + sg.off + qc) : (uint8_t)1;
         }
       };
       if (q0 < q1) load(q0, r, label, wgt);
@@ -194,8 +203,15 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition_kernel
           const bool wl = (ml >> lane) & 1, wr = (mr >> lane) & 1;
           const uint32_t bb = __shfl_sync(kFull, base, wl ? 0 : 1);  // lane 0: left base, 1: right
           const unsigned below = (1u << lane) - 1;
-          if (wl || wr) {
-            const uint32_t pos = wl ? A + bb + __popc(ml & below) : B - 1 - (bb + __popc(mr & below));
+          const uint32_t pos = wl ? A + bb + __popc(ml & below) : B - 1 - (bb + __popc(mr & below));
+          const bool w = wl || wr;
+          if constexpr (BS >= 4) {  // predicated stores: no branch around them
+            uint8_t *o = a.bins_out + (size_t)pos * 4;
+#pragma unroll
+            for (int i = 0; i < BS / 4; i++) st_cs_if(w, o + i * a.pstride, r[u].w[i]);
+            st_cs_if_u8(w, a.lab_out + pos, (uint32_t)label[u]);
+            if (a.w_out) st_cs_if_u8(w, a.w_out + pos, wgt[u]);
+          } else if (w) {
             store_row<BS>(a.bins_out, a.pstride, pos, r[u]);
             __stcs(a.lab_out + pos, (uint8_t)label[u]);
             if (a.w_out) __stcs(a.w_out + pos, wgt[u]);
@@ -296,7 +312,10 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) tag_kernel(PartA
         const uint4 *wq = reinterpret_cast<const uint4 *>(plane + (size_t)a4 * 4);
         const uint32_t *lq = reinterpret_cast<const uint32_t *>(a.lab_in + a4);
         uint32_t *oq = reinterpret_cast<uint32_t *>(a.lab_tag + a4);
-        constexpr int QU = 2;  // quads in flight per thread
+#ifndef ADAPT_TAG_QU
+#define ADAPT_TAG_QU 2
+#endif
+        constexpr int QU = ADAPT_TAG_QU;  // quads in flight per thread
         for (uint32_t qb = 0; qb < nq; qb += QU * blockDim.x) {
           uint4 w[QU];
           uint32_t l[QU];
