@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition_kernel
         for (int u = 0; u < kPartUnroll; u++) {
           // branch-free: a lane past the segment's end re-reads its last row
           // (q clamped; q0 < q1 here) and is marked invalid by its label
-          const uint32_t q = qb + u * blockDim.x + tid;
+          const uint32_t q = qb + u * kPartThreads + tid;
           const uint32_t qc = min(q, q1 - 1);
           load_row<BS>(a.bins_in, a.pstride, sg.off + qc, rr[u]);
           const int lb = __ldcs(a.lab_in + sg.off + qc);
@@ -188,9 +188,9 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition_kernel
         }
       };
       if (q0 < q1) load(q0, r, label, wgt);
-      for (uint32_t qb = q0; qb < q1; qb += kPartUnroll * blockDim.x) {
-        const bool more = qb + kPartUnroll * blockDim.x < q1;
-        if (more) load(qb + kPartUnroll * blockDim.x, rn, labn, wgn);
+      for (uint32_t qb = q0; qb < q1; qb += kPartUnroll * kPartThreads) {
+        const bool more = qb + kPartUnroll * kPartThreads < q1;
+        if (more) load(qb + kPartUnroll * kPartThreads, rn, labn, wgn);
 #pragma unroll
         for (int u = 0; u < kPartUnroll; u++) {
           const bool valid = label[u] >= 0 && wgt[u] > 0;
@@ -313,15 +313,15 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) tag_kernel(PartA
         const uint32_t *lq = reinterpret_cast<const uint32_t *>(a.lab_in + a4);
         uint32_t *oq = reinterpret_cast<uint32_t *>(a.lab_tag + a4);
 #ifndef ADAPT_TAG_QU
-#define ADAPT_TAG_QU 2
+#define ADAPT_TAG_QU 4
 #endif
         constexpr int QU = ADAPT_TAG_QU;  // quads in flight per thread
-        for (uint32_t qb = 0; qb < nq; qb += QU * blockDim.x) {
+        for (uint32_t qb = 0; qb < nq; qb += QU * kPartThreads) {
           uint4 w[QU];
           uint32_t l[QU];
 #pragma unroll
           for (int u = 0; u < QU; u++) {
-            const uint32_t qi = qb + u * blockDim.x + tid;
+            const uint32_t qi = qb + u * kPartThreads + tid;
             if (qi < nq) {
               w[u] = __ldcs(wq + qi);
               l[u] = __ldcs(lq + qi);
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) tag_kernel(PartA
           }
 #pragma unroll
           for (int u = 0; u < QU; u++) {
-            const uint32_t qi = qb + u * blockDim.x + tid;
+            const uint32_t qi = qb + u * kPartThreads + tid;
             if (qi < nq) {
               const uint32_t x[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
               uint32_t mark = 0;
@@ -345,12 +345,12 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) tag_kernel(PartA
           }
         }
       } else {
-        for (uint32_t qb = q0; qb < q1; qb += kTagUnroll * blockDim.x) {
+        for (uint32_t qb = q0; qb < q1; qb += kTagUnroll * kPartThreads) {
           uint32_t w[kTagUnroll], lab[kTagUnroll];
           int sh[kTagUnroll];
 #pragma unroll
           for (int u = 0; u < kTagUnroll; u++) {  // all loads first
-            const uint32_t q = qb + u * blockDim.x + tid;
+            const uint32_t q = qb + u * kPartThreads + tid;
             sh[u] = 0;
             w[u] = 0;
             lab[u] = 0;
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) tag_kernel(PartA
           }
 #pragma unroll
           for (int u = 0; u < kTagUnroll; u++) {
-            const uint32_t q = qb + u * blockDim.x + tid;
+            const uint32_t q = qb + u * kPartThreads + tid;
             if (q < q1) {
               const bool left = (int)((w[u] >> sh[u]) & 0xFFu) <= sg.thr;  // bins are ranks
               nl += left;
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition4_kerne
       auto load = [&](uint32_t qb, Row<BS>(&rr)[kPartUnroll], int(&ll)[kPartUnroll]) {
 #pragma unroll
         for (int u = 0; u < kPartUnroll; u++) {
-          const uint32_t q = qb + u * blockDim.x + tid;
+          const uint32_t q = qb + u * kPartThreads + tid;
           ll[u] = -1;
           if (q < q1) {
             load_row<BS>(a.bins_in, a.pstride, sg.off + q, rr[u]);
@@ -450,9 +450,9 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition4_kerne
         }
       };
       if (q0 < q1) load(q0, r, label);
-      for (uint32_t qb = q0; qb < q1; qb += kPartUnroll * blockDim.x) {
-        const bool more = qb + kPartUnroll * blockDim.x < q1;
-        if (more) load(qb + kPartUnroll * blockDim.x, rn, labn);
+      for (uint32_t qb = q0; qb < q1; qb += kPartUnroll * kPartThreads) {
+        const bool more = qb + kPartUnroll * kPartThreads < q1;
+        if (more) load(qb + kPartUnroll * kPartThreads, rn, labn);
 #pragma unroll
         for (int u = 0; u < kPartUnroll; u++) {
           const bool left = row_byte<BS>(r[u], sg.feat) <= sg.thr;
@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
         const Seg sg = a.segs[s];
         const uint32_t q0 = p0 > sg.row_base ? p0 - sg.row_base : 0;
         const uint32_t q1 = min(sg.len, pe - sg.row_base);
-        for (uint32_t q = q0 + tid; q < q1; q += blockDim.x) {
+        for (uint32_t q = q0 + tid; q < q1; q += kHistThreads) {
           const uint32_t row = sg.off + q;
           uint32_t w;
           if constexpr (BS >= 4)
@@ -597,9 +597,9 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
     {
       const uint8_t *m = a.cmaps + (size_t)first.cmap * C;
       if (a.tagged)  // only labels marked by the TAG pass (bit 7) count
-        for (int k = tid; k < kMaxC + 1; k += blockDim.x) s_cmap[k] = k >= 128 && k - 128 < C ? m[k - 128] : 255;
+        for (int k = tid; k < kMaxC + 1; k += kHistThreads) s_cmap[k] = k >= 128 && k - 128 < C ? m[k - 128] : 255;
       else
-        for (int k = tid; k < C; k += blockDim.x) s_cmap[k] = m[k];
+        for (int k = tid; k < C; k += kHistThreads) s_cmap[k] = m[k];
     }
     uint32_t abase[4];
     int gcount = 0;
@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
     }
     const bool all4 = Dw[0] && Dw[1] && Dw[2] && Dw[3];
     const uint32_t kwp4 = 4u * kwp;
-    for (int i = tid; i < gcount; i += blockDim.x) sh[i] = 0;
+    for (int i = tid; i < gcount; i += kHistThreads) sh[i] = 0;
     if (tid == 0) s_cmap[255] = 255;  // label sentinel of the padded quad lanes
     __syncthreads();
     // one row: its word w (4 features), label, weight -> up to 4 reductions
@@ -663,12 +663,12 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
         const uint32_t *lq = reinterpret_cast<const uint32_t *>(a.lab_in + a4);
         const uint32_t *vq = WEIGHTED ? reinterpret_cast<const uint32_t *>(a.w_in + a4) : nullptr;
         constexpr int QU = UNROLL / 4 > 0 ? UNROLL / 4 : 1;  // quads in flight per thread
-        for (uint32_t qb = 0; qb < nq; qb += QU * blockDim.x) {
+        for (uint32_t qb = 0; qb < nq; qb += QU * kHistThreads) {
           uint4 w[QU];
           uint32_t l[QU], v[WEIGHTED ? QU : 1];
 #pragma unroll
           for (int u = 0; u < QU; u++) {  // all loads first
-            const uint32_t qi = qb + u * blockDim.x + tid;
+            const uint32_t qi = qb + u * kHistThreads + tid;
             l[u] = 0xFFFFFFFFu;
             w[u] = make_uint4(0, 0, 0, 0);
             if (qi < nq) {
@@ -691,13 +691,13 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
           }
         }
       } else {
-        for (uint32_t qb = q0; qb < q1; qb += UNROLL * blockDim.x) {
+        for (uint32_t qb = q0; qb < q1; qb += UNROLL * kHistThreads) {
           uint32_t w[UNROLL];
           int label[UNROLL];
           uint32_t wv[UNROLL];
 #pragma unroll
           for (int u = 0; u < UNROLL; u++) {  // all loads first: only this CTA's word
-            const uint32_t q = qb + u * blockDim.x + tid;
+            const uint32_t q = qb + u * kHistThreads + tid;
             label[u] = 255;
             w[u] = 0;
             wv[u] = 1;
@@ -726,10 +726,10 @@ __global__ void __launch_bounds__(kHistThreads, 1) hist_kernel(HistArgs a) {
       uint32_t *df = dst + (int64_t)a.cumD[4 * w0] * kcn + k0;
       const int width = sole ? kn : kwp;
       const int n = Rt * width;
-      const int qs = (int)blockDim.x / width, rs = (int)blockDim.x - qs * width;
+      const int qs = kHistThreads / width, rs = kHistThreads - qs * width;
       int rk = tid / width, j = tid - rk * width;
 #pragma unroll 4
-      for (int i = tid; i < n; i += blockDim.x) {
+      for (int i = tid; i < n; i += kHistThreads) {
         if (sole) {  // dense [rank][kn] block of this CTA's columns
           df[rk * kcn + j] = sh[rk * kwp + j];
         } else {
