@@ -67,16 +67,36 @@ __global__ void __launch_bounds__(kChunkThreads)
   const int kcd = jb.kc_d;
   const int dq = kChunkThreads / kcd, dr = kChunkThreads - dq * kcd;
   int r = (int)((i0 + threadIdx.x) / kcd), j = (int)(i0 + threadIdx.x - (int64_t)r * kcd);
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += kChunkThreads) {
-    const short2 mj = m[j];
-    const uint32_t sib = mj.y >= 0 ? q[(int64_t)r * jb.kc_s + mj.y] : 0u;
-    d[i] = p[(int64_t)r * jb.kc_p + mj.x] - sib;
-    r += dq;
-    j += dr;
-    if (j >= kcd) {
-      j -= kcd;
-      r++;
+  // kSubUnroll elements per thread per step, every load issued before the
+  // first subtraction (the element loop is latency-bound otherwise)
+  constexpr int kSubUnroll = 4;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += kSubUnroll * kChunkThreads) {
+    int rr[kSubUnroll], jj[kSubUnroll];
+#pragma unroll
+    for (int u = 0; u < kSubUnroll; u++) {
+      rr[u] = r;
+      jj[u] = j;
+      r += dq;
+      j += dr;
+      if (j >= kcd) {
+        j -= kcd;
+        r++;
+      }
     }
+    uint32_t pv[kSubUnroll], sv[kSubUnroll];
+#pragma unroll
+    for (int u = 0; u < kSubUnroll; u++) {
+      pv[u] = 0;
+      sv[u] = 0;
+      if (i + u * kChunkThreads < i1) {
+        const short2 mj = m[jj[u]];
+        sv[u] = mj.y >= 0 ? q[(int64_t)rr[u] * jb.kc_s + mj.y] : 0u;
+        pv[u] = p[(int64_t)rr[u] * jb.kc_p + mj.x];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSubUnroll; u++)
+      if (i + u * kChunkThreads < i1) d[i + u * kChunkThreads] = pv[u] - sv[u];
   }
 }
 
