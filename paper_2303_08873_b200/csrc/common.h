@@ -182,6 +182,8 @@ void launch_decide_segs(Seg *segs, int nseg, const uint8_t *res, const int64_t *
 // partition and the histogram).  Slot slot0 + b of a direct child holds its
 // piece from partition range b; row_base = exclusive prefix of the slots' len.
 struct SegBuildArgs {
+  int mode4;                 // MOVE4 reports ([8] per visit) with two bseg entries per segment
+                             // (one per child of the parent: x = code of its direct grandchild)
   const int32_t *visits;     // the partition's share reports [nranges][max_visits][6]
   int nranges, max_visits;
   const int4 *bseg;          // per partition segment: x side of the parent's direct

@@ -1749,7 +1749,7 @@ void train_region(adapt_region *h, cudaStream_t s) {
     static const bool host_segs = getenv("ADAPT_HOST_SEGS") != nullptr;
     // (small levels: the host-built segments are cheaper than the builder
     // kernel's launch — C3's 1e6 rows: 2.17 vs 2.35 ms per train)
-    const bool dev = level > 0 && pst.mode == 0 && !w_root && g_ctx.world == 1 && !rs && !host_segs &&
+    const bool dev = level > 0 && pst.mode != 1 && !w_root && g_ctx.world == 1 && !rs && !host_segs &&
                      (pst.rows_part >= (1 << 22) || getenv("ADAPT_DEV_SEGS") != nullptr);
     if (tagged) {
       hist_bins = pa.bins_in;
@@ -1859,19 +1859,38 @@ void train_region(adapt_region *h, cudaStream_t s) {
     std::vector<double> cf_slot(tagged ? nslots : 0, 1.0);  // tagged: counted share of the rows read
     if (dev) {
       // slot templates: node j's slots are the partition ranges that visit its
-      // parent (one piece each), in range order; sizes from the winner counts
-      std::vector<int4> pinfo(pst.pbase.size(), make_int4(-1, 0, 0, 0));
+      // parent (one piece each), in range order; sizes from the winner counts.
+      // After MOVE4 the moved "parent" is j's GRANDparent (the TAG pass's
+      // segment parent) and j is one of its four grandchildren (code LL, LR,
+      // RL, RR); each of the grandparent's two children has at most one
+      // direct child, so a segment carries two slot entries.
+      const bool m4 = pst.mode == 2;
+      std::vector<int> gp_of, code_of;
+      if (m4) {
+        gp_of.assign(A, -1);
+        code_of.assign(A, -1);
+        for (size_t k = 0; k < pseg_gkids.size(); k++) {
+          const int4 gk = pseg_gkids[k];
+          const int g[4] = {gk.x, gk.y, gk.z, gk.w};
+          for (int c = 0; c < 4; c++)
+            if (g[c] >= 0) gp_of[g[c]] = pst.seg_parent[k], code_of[g[c]] = c;
+        }
+      }
+      std::vector<int4> pinfo((m4 ? 2 : 1) * pst.pbase.size(), make_int4(-1, 0, 0, 0));
       for (int j = 0; j < A; j++) {
         const FNode &fn = frontier[j];
         if (!fn.direct) continue;
         const bool small = fn.rows * 16 < DS * (node_kc[j] | 1);
         std::vector<Seg> &lst = small ? fsegs : hsegs;
         uint32_t &tot = small ? ftotal : htotal;
-        const int p = fn.par;
+        const int p = m4 ? gp_of[j] : fn.par;
         if (p < 0 || p >= (int)pst.pbase.size() || pst.plen[p] == 0)
           throw Error(ADAPT_E_CUDA, "internal: a direct node without a partitioned parent");
         const int b0 = (int)(pst.pbase[p] / pst.Rr), b1 = (int)((pst.pbase[p] + pst.plen[p] - 1) / pst.Rr);
-        pinfo[p] = make_int4(fn.side, small ? 1 : 0, (int)lst.size() - b0, 0);
+        if (m4)
+          pinfo[2 * p + (code_of[j] >> 1)] = make_int4(code_of[j], small ? 1 : 0, (int)lst.size() - b0, 0);
+        else
+          pinfo[p] = make_int4(fn.side, small ? 1 : 0, (int)lst.size() - b0, 0);
         if (!small) pnodes.push_back(PlanNode{-1, -1, tot, (uint32_t)fn.rows, node_kc[j]});
         Seg sg{};
         sg.hslot = fn.slot;
@@ -1884,8 +1903,14 @@ void train_region(adapt_region *h, cudaStream_t s) {
         for (int b = b0; b <= b1; b++) lst.push_back(sg);
         tot += (uint32_t)fn.rows;
       }
-      bseg.resize(pst.seg_parent.size());
-      for (size_t k = 0; k < bseg.size(); k++) bseg[k] = pinfo[pst.seg_parent[k]];
+      if (m4) {
+        bseg.resize(2 * pst.seg_parent.size());
+        for (size_t k = 0; k < pst.seg_parent.size(); k++)
+          for (int c = 0; c < 2; c++) bseg[2 * k + c] = pinfo[2 * pst.seg_parent[k] + c];
+      } else {
+        bseg.resize(pst.seg_parent.size());
+        for (size_t k = 0; k < bseg.size(); k++) bseg[k] = pinfo[pst.seg_parent[k]];
+      }
     } else {
       for (int j = 0; j < A; j++) {
         const FNode &fn = frontier[j];
@@ -1943,7 +1968,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
         h->hseg_err.grow(16);
         CUDA_CHECK(cudaMemsetAsync(h->dseg_err.p, 0, 4, s));
         SegBuildArgs ba{};
-        ba.visits = h->visits.as<int32_t>();
+        ba.mode4 = pst.mode == 2;
+        ba.visits = pa.visits;  // the move's share reports (MOVE4: its own buffer)
         ba.nranges = pa.nranges;
         ba.max_visits = max_visits;
         ba.bseg = sb.ptr<int4>(o_bseg);

@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(kBuildThreads) build_hist_segs_kernel(SegBuild
   __shared__ uint32_t s_carry;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nent = a.nranges * a.max_visits;
-  for (int i = tid; i < nent; i += blockDim.x) {
+  for (int i = tid; i < nent && !a.mode4; i += blockDim.x) {
     const int32_t *e = a.visits + (size_t)i * 6;
     if (e[0] < 0) continue;
     const int4 info = a.bseg[e[0]];
@@ -765,6 +765,22 @@ __global__ void __launch_bounds__(kBuildThreads) build_hist_segs_kernel(SegBuild
     Seg &sg = a.segs[info.y][info.z + i / a.max_visits];
     sg.off = info.x == 0 ? (uint32_t)e[1] : (uint32_t)(e[2] - e[4]);
     sg.len = (uint32_t)(info.x == 0 ? e[3] : e[4]);
+  }
+  // MOVE4: a share [A, B) split at M = A + cL holds LL [A, +n0), LR
+  // [M - n1, M), RL [M, +n2), RR [B - n3, B); each child's direct grandchild
+  for (int i = tid; i < nent && a.mode4; i += blockDim.x) {
+    const int32_t *e = a.visits + (size_t)i * 8;
+    if (e[0] < 0) continue;
+    const uint32_t A = (uint32_t)e[1], B = (uint32_t)e[2], M = A + (uint32_t)e[3];
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      const int4 info = a.bseg[2 * e[0] + c];
+      if (info.x < 0) continue;
+      Seg &sg = a.segs[info.y][info.z + i / a.max_visits];
+      const uint32_t n = (uint32_t)e[4 + info.x];
+      sg.off = info.x == 0 ? A : info.x == 1 ? M - n : info.x == 2 ? M : B - n;
+      sg.len = n;
+    }
   }
   __syncthreads();
   for (int l = 0; l < 2; l++) {

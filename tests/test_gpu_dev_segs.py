@@ -102,6 +102,9 @@ def test_two_level_moves_match_one_level(tmp_path):
     two, log_t = _run(tmp_path, {"ADAPT_TWO_LEVEL": "1"})
     one, log_o = _run(tmp_path, {"ADAPT_ONE_LEVEL": "1"})
     tag_last, log_l = _run(tmp_path, {"ADAPT_TWO_LEVEL": "1", "ADAPT_TAG_LAST": "1"})
+    # the histogram segments after each MOVE4 built on the device
+    two_dev, log_d = _run(tmp_path, {"ADAPT_TWO_LEVEL": "1", "ADAPT_DEV_SEGS": "1"})
     assert len(two) > 1000, log_t
     assert two == one, (log_t, log_o)
     assert two == tag_last, (log_t, log_l)
+    assert two == two_dev, (log_t, log_d)
