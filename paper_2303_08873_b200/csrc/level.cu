@@ -470,7 +470,6 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition4_kerne
           const uint32_t bc = __shfl_sync(kFull, base, code);  // lane c holds code c's base
           // the lane's position without branches (selects on the code bits):
           // codes 0 / 2 grow up from A / M, codes 1 / 3 down from M / B
-#ifndef ADAPT_P4_BRANCHY
           const bool c1 = code & 1, c2 = code & 2;
           const unsigned mc = c2 ? (c1 ? m[3] : m[2]) : (c1 ? m[1] : m[0]);
           const uint32_t rk = bc + __popc(mc & ((1u << lane) - 1));
@@ -480,16 +479,6 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) partition4_kerne
             store_row<BS>(a.bins_out, a.pstride, pos, r[u]);
             __stcs(a.lab_out + pos, (uint8_t)label[u]);
           }
-#else
-          if (wr) {
-            const unsigned below = (1u << lane) - 1;
-            const unsigned mc = code == 0 ? m[0] : code == 1 ? m[1] : code == 2 ? m[2] : m[3];
-            const uint32_t rk = bc + __popc(mc & below);
-            const uint32_t pos = code == 0 ? A + rk : code == 1 ? M - 1 - rk : code == 2 ? M + rk : B - 1 - rk;
-            store_row<BS>(a.bins_out, a.pstride, pos, r[u]);
-            __stcs(a.lab_out + pos, (uint8_t)label[u]);
-          }
-#endif
         }
         if (more) {
 #pragma unroll
