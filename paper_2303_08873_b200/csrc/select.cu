@@ -133,11 +133,14 @@ __device__ __forceinline__ int walk_block2(const uint4 &a, const uint4 &b, const
   return (int32_t)r;
 }
 
-template <int F>
+// TD > 0: the heap depth at compile time (the full 14-level heap of deep
+// trees such as C5's): the top walk unrolls completely
+template <int F, int TD = 0>
 __global__ void __launch_bounds__(kSelThreads, 1)
-    select_kernel_h(const uint2 *__restrict__ gheap, const int32_t *__restrict__ gexits, int td,
+    select_kernel_h(const uint2 *__restrict__ gheap, const int32_t *__restrict__ gexits, int td_rt,
                     const uint4 *__restrict__ blocks2, const float *__restrict__ X, int64_t m, int wide,
                     int32_t *__restrict__ out) {
+  const int td = TD > 0 ? TD : td_rt;
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int NP = F <= 4 ? 4 : (F <= 8 ? 8 : 16);
   const int nh = (1 << td) - 1;
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     for (int f = 0; f < NP; f++) xr[f] = f < F ? nx[f] : 0.f;
     if (v + stride < m) load_vec<F>(X + (v + stride) * F, wide, nx);  // next vector in flight
     uint32_t k = 0;
-#pragma unroll 2
+#pragma unroll (TD > 0 ? TD : 2)
     for (int l = 0; l < td; l++) {  // fixed trip count: leaves above td pass through
       const uint2 nd = hs[k];
       k = 2 * k + (pick<NP>(xr, nd.y) <= __uint_as_float(nd.x) ? 1u : 2u);
@@ -242,9 +245,15 @@ void launch_select(const SelTree &tr, const float *X, int64_t m, int F, int32_t 
       select_kernel_c<FF><<<g, kSelThreads, smem, s>>>(tree, n_top, blocks, X, m, wide, out); ++g_kernel_launches;   \
     } else {                                                                                    \
       const size_t smem = ((size_t)1 << tr.td) * (sizeof(uint2) + 4);                           \
-      smem_limit(select_kernel_h<FF>, smem);                                                    \
-      select_kernel_h<FF><<<g, kSelThreads, smem, s>>>(tr.heap, tr.exits, tr.td, tr.blocks2, X, m, \
-                                                       wide, out); ++g_kernel_launches;                              \
+      if (tr.td == kHeapMaxLevels) {                                                            \
+        smem_limit(select_kernel_h<FF, kHeapMaxLevels>, smem);                                  \
+        select_kernel_h<FF, kHeapMaxLevels><<<g, kSelThreads, smem, s>>>(                       \
+            tr.heap, tr.exits, tr.td, tr.blocks2, X, m, wide, out); ++g_kernel_launches;         \
+      } else {                                                                                  \
+        smem_limit(select_kernel_h<FF>, smem);                                                  \
+        select_kernel_h<FF><<<g, kSelThreads, smem, s>>>(tr.heap, tr.exits, tr.td, tr.blocks2, X, m, \
+                                                         wide, out); ++g_kernel_launches;                            \
+      }                                                                                         \
     }                                                                                           \
     break;                                                                                      \
   }
