@@ -2178,7 +2178,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
       int32_t hslot;
     };
     std::vector<Dec> dec(A, Dec{false, false, -1});
-    for (int j = 0; j < A; j++) {
+    // (the last frontier level's children are leaves: nothing to decide here)
+    for (int j = 0; j < A && level + 1 < D; j++) {
       const NodeRes *nr = reinterpret_cast<const NodeRes *>(hr + res_off[j]);
       const uint32_t *Pd = reinterpret_cast<const uint32_t *>(nr + 1);
       const uint32_t *cLd = Pd + node_kc[j];
