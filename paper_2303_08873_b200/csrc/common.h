@@ -238,8 +238,10 @@ struct SubJob {              // derived node = parent - direct sibling, class-re
 // zero / subtract work in chunks: cstart[j] = first chunk of job j (prefix of
 // chunk_count(elements of job j)), nblocks = total chunks
 int chunk_count(int64_t elems);
+// zslot (optional): job k zeroes slot zslot[k] (else slot k)
 void launch_zero_slots(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS,
-                       const int32_t *cstart, int n, int nblocks, cudaStream_t s);
+                       const int32_t *cstart, int n, int nblocks, cudaStream_t s,
+                       const int32_t *zslot = nullptr);
 void launch_subtract(uint32_t *H, const uint32_t *Hprev, int64_t DS, const SubJob *jobs,
                      const int16_t *maps, const int32_t *cstart, int n, int nblocks, cudaStream_t s);
 // nodes with <= split_small_max_classes() classes go to the warp-per-(node, f)

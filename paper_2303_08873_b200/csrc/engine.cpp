@@ -1738,11 +1738,14 @@ void train_region(adapt_region *h, cudaStream_t s) {
         if (used < Q)
           CUDA_CHECK(cudaMemsetAsync(Hcur->as<uint32_t>() + r * Q + used, 0, (size_t)(Q - used) * 4, s));
       }
-    {
+    // the direct slots are zeroed right before the histogram pass, except the
+    // ones its CTAs store whole (see "covered" below)
+    static const bool zero_all = getenv("ADAPT_ZERO_ALL") != nullptr;
+    auto zero_all_slots = [&]() {
       Phase ph("zero", s, 0);
       launch_zero_slots(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_soff), sa.ptr<int32_t>(o_skc), DS,
                         sa.ptr<int32_t>(o_zst), ndirect_slots, zblocks, s);
-    }
+    };
     // histogram segments built on the device (single rank, unweighted: every
     // direct node's size is its parent's winner count, so the histogram pass
     // is queued behind the partition without waiting for its share reports)
@@ -1958,9 +1961,53 @@ void train_region(adapt_region *h, cudaStream_t s) {
             ctas.push_back(HistCta{g, std::min<uint32_t>(r * R, htotal), std::min<uint32_t>((r + 1) * R, htotal), -1});
       }
       tick("plan");
+      // A direct slot needs no zeroing when, for every word group holding some
+      // of its classes, one CTA sees the node's whole virtual range through the
+      // shared-memory path: that CTA's flush STORES every counter of its block
+      // (hist_kernel "sole"; a tiny portion counts into global memory instead,
+      // a small node goes to the flat pass — both need the zeros)
+      std::vector<char> covered(ndirect_slots, 0);
+      if (!zero_all && !hsegs.empty()) {
+        std::vector<std::vector<std::pair<uint32_t, uint32_t>>> rg(ngroups);  // CTA ranges per group
+        for (const auto &ct : ctas) rg[ct.g].push_back({ct.p0, ct.p1});
+        for (auto &v : rg) std::sort(v.begin(), v.end());
+        for (size_t i = 0; i < hsegs.size();) {
+          size_t k = i;
+          while (k < hsegs.size() && hsegs[k].hslot == hsegs[i].hslot) k++;
+          const Seg &sg = hsegs[i];
+          const uint32_t nb = sg.node_base, ne = sg.node_base + sg.node_len;
+          bool ok = sg.hslot >= 0 && sg.hslot < ndirect_slots && sg.node_len > 0;
+          for (int g = 0; g < ngroups && ok; g++) {
+            const int kn = std::min(gl[g].kw, sg.ncls - gl[g].k0);
+            if (kn <= 0) continue;  // none of the node's classes in this group
+            if ((int64_t)sg.node_len * 16 < (int64_t)gcost[g].dsw * (kn | 1)) {
+              ok = false;  // a tiny portion: global atomics
+              break;
+            }
+            const auto &v = rg[g];
+            auto it = std::upper_bound(v.begin(), v.end(), std::make_pair(nb, UINT32_MAX));
+            ok = it != v.begin() && std::prev(it)->first <= nb && std::prev(it)->second >= ne;
+          }
+          if (ok) covered[sg.hslot] = 1;
+          i = k;
+        }
+      }
+      std::vector<int32_t> zslot, zst2;
+      int zb2 = 0;
+      for (int k = 0; k < ndirect_slots; k++) {
+        if (covered[k]) continue;
+        zslot.push_back(k);
+        zst2.push_back(zb2);
+        zb2 += chunk_count(DS * slot_kc[k]);
+      }
       const size_t o_hsegs = sb.put(hsegs), o_fsegs = sb.put(fsegs), o_ctas = sb.put(ctas),
-                   o_bseg = sb.put(bseg);
+                   o_bseg = sb.put(bseg), o_zslot = sb.put(zslot), o_zst2 = sb.put(zst2);
       sb.flush(s);
+      {
+        Phase ph("zero", s, 0);
+        launch_zero_slots(Hcur->as<uint32_t>(), sa.ptr<int64_t>(o_soff), sa.ptr<int32_t>(o_skc), DS,
+                          sb.ptr<int32_t>(o_zst2), (int)zslot.size(), zb2, s, sb.ptr<int32_t>(o_zslot));
+      }
       tick("upload_b");
       Seg *d_hsegs = sb.ptr<Seg>(o_hsegs), *d_fsegs = sb.ptr<Seg>(o_fsegs);
       if (dev) {  // the templates are filled in place by the builder
@@ -2019,6 +2066,8 @@ void train_region(adapt_region *h, cudaStream_t s) {
       fa.total_rows = ftotal;
       launch_hist_flat(fa, s);
       tick("launch_flat");
+    } else {
+      zero_all_slots();  // no rows here: the (all-reduced) slots must still be zero
     }
     if (!rs && collectives_on() && ndirect_slots > 0)  // the direct slots are contiguous at the front
       comm_allreduce_sum(Hcur->p, (size_t)soff[ndirect_slots], false, s, "allreduce histograms");

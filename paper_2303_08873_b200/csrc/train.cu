@@ -39,11 +39,12 @@ __device__ __forceinline__ int find_job(const int32_t *cstart, int n, int b) {
 // slots 0..n-1 (the direct nodes): zero their [DS][kc] matrices
 __global__ void __launch_bounds__(kChunkThreads)
     zero_slots_kernel(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS,
-                      const int32_t *cstart, int n) {
-  const int y = find_job(cstart, n, blockIdx.x);
+                      const int32_t *cstart, int n, const int32_t *zslot) {
+  const int job = find_job(cstart, n, blockIdx.x);
+  const int y = zslot ? zslot[job] : job;  // job -> slot (null: job = slot)
   uint32_t *h = H + soff[y];
   const int64_t E = DS * skc[y];
-  const int64_t i0 = (int64_t)(blockIdx.x - cstart[y]) * kChunk;
+  const int64_t i0 = (int64_t)(blockIdx.x - cstart[job]) * kChunk;
   const int64_t i1 = min(i0 + kChunk, E);
   for (int64_t i = i0 + threadIdx.x; i < i1; i += kChunkThreads) h[i] = 0;
 }
@@ -528,9 +529,9 @@ __global__ void __launch_bounds__(256)
 int chunk_count(int64_t elems) { return (int)((elems + kChunk - 1) / kChunk); }
 
 void launch_zero_slots(uint32_t *H, const int64_t *soff, const int32_t *skc, int64_t DS,
-                       const int32_t *cstart, int n, int nblocks, cudaStream_t s) {
+                       const int32_t *cstart, int n, int nblocks, cudaStream_t s, const int32_t *zslot) {
   if (n == 0 || nblocks == 0) return;
-  zero_slots_kernel<<<nblocks, kChunkThreads, 0, s>>>(H, soff, skc, DS, cstart, n); ++g_kernel_launches;
+  zero_slots_kernel<<<nblocks, kChunkThreads, 0, s>>>(H, soff, skc, DS, cstart, n, zslot); ++g_kernel_launches;
   CUDA_CHECK(cudaGetLastError());
 }
 
